@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: scheduled requests/s (score + sort + dispatch) of one scheduling
+tick over a 16M-request queue (config C4: 8 LLM pools x 32 instances, 2M
+queued requests per pool, pre-loaded ledgers), Kairos policy + time-slot
+dispatch, on 1..N B200s (one process per GPU, weak scaling: every rank owns
+its own 8 pools).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+
+One step = restore the pre-tick instance/ledger state (device copy) + kx_tick
+(order the whole queue, dispatch every pool) on the handle's stream. Inputs
+are resident in HBM and larger than L2 (16M requests x 44 B = 704 MB). `e2e`
+runs the same step through the C ABI from pinned HOST buffers (queue upload
+H2D + tick + decision-log D2H inside the timed region). `--impl reference`
+times the reference's own CPU implementation (oracle/_ref/libkxref.so, built
+from the unmodified reference sources) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "scheduled requests/sec (score+sort+dispatch) at 1M–16M queue depth; % HBM roofline"
+UNIT = "requests/s"
+N_POOLS, PER_POOL, INST_PER_POOL = 8, 2_000_000, 32
+NOW = 10.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.path = Path("/tmp") / f"kx_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def build_c4(rank: int):
+    from paper_2508_06948_b200 import workload as W
+    t0 = time.time()
+    snap = W.snapshot(n_pools=N_POOLS, per_pool=PER_POOL, seed=1 + rank,
+                      msg_base=rank * 10_000_000, uid_base=1 + rank * 10 ** 9)
+    insts = W.instances(N_POOLS, INST_PER_POOL)
+    live, running, commits = W.preload(insts, seed=7 + rank, now=NOW)
+    log(f"[rank {rank}] synthetic C4 queue: {snap.n} requests, {len(insts)} instances "
+        f"({time.time() - t0:.1f}s)")
+    return snap, insts, live, running, commits
+
+
+def make_sched(snap, insts, live, running, commits, device):
+    import paper_2508_06948_b200 as kx
+    s = kx.DeviceScheduler(insts, n_pools=N_POOLS, queue_capacity=snap.n, max_agents=len(snap.agent_pool),
+                           device=device)
+    s.set_agent_tables(snap.agent_pool, snap.priority_key, snap.topo_depth, snap.expected_T)
+    s.set_scheduler("kairos")
+    c = np.array(commits, dtype=np.float64).T if commits else np.zeros((6, 0))
+    s.commit_batch(c[0].astype(np.int32), np.array([x[1] for x in commits], np.uint64), c[2], c[3], c[4], c[5])
+    s.set_live(live, running, np.zeros(len(insts), np.int32))
+    s.checkpoint()
+    return s
+
+
+def run_mine(args):
+    import torch
+    import paper_2508_06948_b200 as kx
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    snap, insts, live, running, commits = build_c4(rank)
+    s = make_sched(snap, insts, live, running, commits, local)
+    s.upload(snap.agent, snap.prompt, snap.app_start, snap.queue_enter, snap.msg_key, snap.uid)
+    stream = torch.cuda.ExternalStream(s.stream_ptr(), device=dev)
+    lib = s.lib
+
+    def step():
+        s.restore()
+        s.tick(NOW)
+
+    for _ in range(args.warmup):
+        step()
+    s.synchronize()
+    rows, _ = s.fetch_dispatch()
+    admitted = int(sum(int(r["admitted"].sum()) for r in rows))
+    decisions = int(sum(len(r) for r in rows))
+
+    # ---- timed region: device-resident inputs ---------------------------
+    clocks = Clocks(local)
+    s.profile(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    s.synchronize()
+    launches0 = lib.kx_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    s.synchronize()
+    torch.cuda.synchronize(dev)
+    launches = lib.kx_launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    phases = s.profile_read()
+    s.profile(False)
+    if dist:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    ms_step = ms_total / args.steps
+    n_total = snap.n * ws
+    value = n_total / (ms_step / 1e3)
+
+    # ---- e2e: pinned host buffers through the C ABI ------------------------
+    pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+           for k, v in dict(agent=snap.agent.astype(np.int32), prompt=snap.prompt, app=snap.app_start,
+                            qe=snap.queue_enter, msg=snap.msg_key.view(np.int64),
+                            uid=snap.uid.view(np.int64)).items()}
+    h2d = sum(t.numel() * t.element_size() for t in pin.values())
+    view = kx._abi.kx_queue_view(*[t.data_ptr() for t in
+                                   (pin["agent"], pin["prompt"], pin["app"], pin["qe"], pin["msg"],
+                                    pin["uid"])], None, None)
+
+    def e2e_step():
+        kx._abi.check(lib.kx_queue_upload(s.h, snap.n, C.byref(view), kx._abi.KX_MEM_HOST))
+        s.restore()
+        s.tick(NOW)
+        r, c = s.fetch_dispatch()
+        return sum(x.nbytes for x in r) + sum(x.nbytes for x in c)
+
+    d2h = e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    if dist:
+        dist.barrier()
+    s.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    e1.synchronize()
+    wall_ms = 1e3 * (time.perf_counter() - w0) / e2e_steps
+    # device span between the two events on the handle's stream: covers the
+    # H2D copies, validation, tick and D2H plus any host gaps between them
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel ------------------------------------
+    hbm, peak_src = peaks()
+    dom_name, dom = max(((k, v) for k, v in phases.items() if v["alg_bytes"] > 0),
+                        key=lambda kv: kv[1]["ms"])
+    dom_launch_ms = dom["ms"] / dom["launches"]
+    dom_bytes = dom["alg_bytes"] / dom["launches"]
+    achieved = dom_bytes / (dom_launch_ms / 1e3) / 1e9
+    tot_ms = sum(v["ms"] for v in phases.values())
+    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                   "share": v["ms"] / tot_ms if tot_ms else None,
+                   "alg_GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["alg_bytes"] and v["ms"] else None}
+               for k, v in phases.items()}
+    tick_bytes = sum(v["alg_bytes"] for v in phases.values()) / args.steps
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom_name)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(snap, insts, live, running, commits, sample_pools=args.cpu_pools)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (co-located QA/RG/CG workflow shapes, workload.py; C4 snapshot)",
+            "config": {"workload": "C4: 16M queued requests, 8 LLM pools x 32 instances, Kairos "
+                                   "priority + time-slot dispatch, pre-loaded ledgers",
+                       "queue_depth_per_gpu": snap.n, "pools": N_POOLS, "instances": len(insts),
+                       "policy": "kairos+time_slot", "l2": "inputs (704 MB) larger than L2",
+                       "step": "state restore + kx_tick (order + dispatch)",
+                       "admitted_per_step": admitted, "decisions_per_step": decisions},
+            "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "alg_bytes_per_launch": dom_bytes, "peak_source": peak_src,
+                         "tick_alg_bytes": tick_bytes,
+                         "tick_frac": (tick_bytes / (ms_step / 1e3) / 1e9) / hbm},
+            "kernels": kernels,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ---- the reference's CPU path ------------------------------------------------
+def _ref_lib():
+    so = ROOT / "oracle" / "_ref" / "libkxref.so"
+    if not so.exists():
+        return None
+    L = C.CDLL(str(so))
+    P = C.c_void_p
+    L.kxref_pool_new.restype = P
+    L.kxref_pool_new.argtypes = [C.c_int, P, P, P, P, C.c_double, C.c_double, C.c_int, C.c_int, P, P,
+                                 P, P, P]
+    L.kxref_pool_free.argtypes = [P]
+    L.kxref_pool_set_live.argtypes = [P, P, P, P]
+    L.kxref_pool_commit.argtypes = [P, C.c_int32, C.c_uint64, C.c_int64, C.c_double, C.c_double]
+    L.kxref_pool_set_queue.argtypes = [P, C.c_int64, P, P, P, P, P, P, P]
+    L.kxref_pool_reset.argtypes = [P]
+    L.kxref_pool_tick.restype = C.c_int64
+    L.kxref_pool_tick.argtypes = [P, C.c_double]
+    L.kxref_pools_tick.restype = C.c_double
+    L.kxref_pools_tick.argtypes = [C.POINTER(P), C.c_int, C.c_double, C.c_int]
+    return L
+
+
+class RefPools:
+    """The reference's data structures for `pools` pools of the workload."""
+
+    def __init__(self, L, snap, insts, live, running, commits, pools):
+        self.L = L
+        names = [n.encode() for n in snap.agent_names]
+        self.cnames = (C.c_char_p * len(names))(*names)
+        self.handles = []
+        self.n = 0
+        self._keep = []
+        for p in pools:
+            ids = np.array([i.id for i in insts if i.pool == p], np.int32)
+            sel = np.isin(np.array([i.id for i in insts]), ids)
+            caps = np.array([i.capacity_tokens for i in insts])[sel]
+            ks = np.array([i.decode_rate for i in insts])[sel]
+            mb = np.array([i.max_batch for i in insts], np.int32)[sel]
+            arrs = [ids, caps, ks, mb, snap.priority_key, snap.pk_known, snap.topo_depth, snap.expected_T]
+            self._keep += arrs
+            h = L.kxref_pool_new(len(ids), ids.ctypes.data, caps.ctypes.data, ks.ctypes.data, mb.ctypes.data,
+                                 0.5, 0.85, 0, len(names), C.cast(self.cnames, C.c_void_p),
+                                 snap.priority_key.ctypes.data, snap.pk_known.ctypes.data,
+                                 snap.topo_depth.ctypes.data, snap.expected_T.ctypes.data)
+            for (iid, uid, P, k, t0, T) in commits:
+                if iid in ids:
+                    L.kxref_pool_commit(h, int(iid), int(uid), int(P), t0, T)
+            lv = np.ascontiguousarray(live[sel])
+            rn = np.ascontiguousarray(running[sel], np.int32)
+            wt = np.zeros(len(ids), np.int32)
+            self._keep += [lv, rn, wt]
+            L.kxref_pool_set_live(h, lv.ctypes.data, rn.ctypes.data, wt.ctypes.data)
+            m = snap.agent_pool[snap.agent] == p
+            cols = [np.ascontiguousarray(x[m]) for x in (snap.agent, snap.prompt, snap.app_start,
+                                                         snap.queue_enter, snap.msg_counter, snap.uid)]
+            L.kxref_pool_set_queue(h, len(cols[0]), *[c.ctypes.data for c in cols], C.cast(self.cnames, C.c_void_p))
+            self.n += len(cols[0])
+            self.handles.append(h)
+        self.arr = (C.c_void_p * len(self.handles))(*self.handles)
+
+    def tick(self, threads):
+        return self.L.kxref_pools_tick(self.arr, len(self.handles), NOW, threads)
+
+    def close(self):
+        for h in self.handles:
+            self.L.kxref_pool_free(h)
+
+
+def cpu_baseline(snap, insts, live, running, commits, sample_pools=None):
+    L = _ref_lib()
+    if L is None:
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libkxref.so not built"}
+    ncpu = os.cpu_count() or 1
+    k = sample_pools or min(N_POOLS, ncpu)
+    t0 = time.time()
+    ref = RefPools(L, snap, insts, live, running, commits, list(range(k)))
+    log(f"cpu baseline: built reference queues for {k} pools ({ref.n} requests) in {time.time() - t0:.1f}s")
+    secs = ref.tick(min(k, ncpu))
+    ref.close()
+    return {"value": ref.n / secs, "unit": UNIT, "cores": min(k, ncpu), "kind": "reference",
+            "sample": f"one tick of {k} of the 8 C4 pools ({ref.n} requests, 2M per pool), one pool per "
+                      f"thread: reference comparator std::sort + Dispatcher choose/commit over the "
+                      f"dispatched prefix + gc ({secs:.2f}s)",
+            "seconds": secs, "host_cpus": ncpu}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    L = _ref_lib()
+    if L is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libkxref.so is not built"}))
+        return
+    from paper_2508_06948_b200 import workload as W
+    snap = W.snapshot(n_pools=N_POOLS, per_pool=PER_POOL, seed=1)
+    insts = W.instances(N_POOLS, INST_PER_POOL)
+    live, running, commits = W.preload(insts, seed=7, now=NOW)
+    ncpu = os.cpu_count() or 1
+    pools = list(range(N_POOLS))
+    ref = RefPools(L, snap, insts, live, running, commits, pools)
+    threads = min(N_POOLS, ncpu)
+    first = ref.tick(threads)  # warm-up 1, also sizes the sample
+    budget = 150.0
+    per_pool = first / max(1, -(-N_POOLS // threads))
+    k = N_POOLS
+    if first * (args.steps + args.warmup) > budget:
+        k = max(1, min(N_POOLS, int(budget / (args.steps + args.warmup) / per_pool) * threads))
+    if k < N_POOLS:
+        ref.close()
+        ref = RefPools(L, snap, insts, live, running, commits, list(range(k)))
+        threads = min(k, ncpu)
+    for _ in range(max(0, args.warmup - 1)):
+        ref.tick(threads)
+    times = [ref.tick(threads) for _ in range(args.steps)]
+    ms = 1e3 * sum(times) / len(times)
+    value = ref.n / (ms / 1e3)
+    sample = (f"{k} of 8 C4 pools per step ({ref.n} requests), {threads} threads: reference comparator "
+              f"std::sort (harness.cpp:92-100) + reference Dispatcher over the dispatched prefix + gc")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (workload.py C4)",
+        "config": {"workload": "C4: 16M queued requests, 8 LLM pools x 32 instances, Kairos "
+                               "priority + time-slot dispatch, pre-loaded ledgers"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    ref.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-pools", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mine(args)
+
+
+if __name__ == "__main__":
+    main()

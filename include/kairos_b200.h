@@ -1,0 +1,261 @@
+/*
+ * kairos_b200.h — C ABI of the B200-native Kairos scheduling hot path.
+ *
+ * The reference (kairos-sim, /root/reference/proj) has no FFI: its operator
+ * API is in-process C++ (SURVEY §8b). Every entry point below replaces one
+ * reference interface, cited as file:line relative to /root/reference/proj.
+ * Conventions:
+ *   - opaque handles (kx_sched*), int status codes (KX_OK == 0), and a
+ *     thread-local message from kx_last_error(); no exceptions cross the ABI.
+ *     Status codes mirror the reference's exception types:
+ *       KX_ERR_INVALID  <- std::invalid_argument (dispatcher.cpp:21,48,129,...)
+ *       KX_ERR_LOGIC    <- std::logic_error      (dispatcher.cpp:73,255)
+ *       KX_ERR_RUNTIME  <- std::runtime_error    (engine.cpp:100)
+ *   - caller-owned structure-of-arrays buffers with explicit lengths; `mem`
+ *     says whether a pointer is host (KX_MEM_HOST) or device (KX_MEM_DEVICE).
+ *   - one CUDA stream per handle (kx_sched_stream); handles are re-entrant,
+ *     no global mutable state (engine.hpp:125-134 threading contract).
+ *   - the product path is CUDA only: with no usable sm_100 device every call
+ *     that computes fails with KX_ERR_CUDA. There is no CPU fallback.
+ */
+#ifndef KAIROS_B200_H_
+#define KAIROS_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KX_ABI_VERSION 1
+
+enum kx_status {
+  KX_OK = 0,
+  KX_ERR_INVALID = 1,   /* std::invalid_argument */
+  KX_ERR_LOGIC = 2,     /* std::logic_error */
+  KX_ERR_RUNTIME = 3,   /* std::runtime_error */
+  KX_ERR_CUDA = 4,      /* CUDA runtime failure / no device */
+  KX_ERR_CAPACITY = 5,  /* a fixed device capacity was exceeded */
+  KX_ERR_LIVELOCK = 6   /* reference would spin forever */
+};
+
+enum kx_mem { KX_MEM_HOST = 0, KX_MEM_DEVICE = 1 };
+
+/* SchedulerKind (harness.hpp:16) */
+enum kx_scheduler_kind {
+  KX_SCHED_KAIROS = 0, /* KairosScheduler   scheduler.hpp:105-133 */
+  KX_SCHED_FCFS = 1,   /* FcfsScheduler     scheduler.hpp:48-54   */
+  KX_SCHED_TOPO = 2,   /* TopoDepthScheduler scheduler.hpp:58-76  */
+  KX_SCHED_ORACLE = 3  /* OracleScheduler   scheduler.hpp:80-93   */
+};
+
+/* DispatchPolicy (dispatcher.hpp:107) */
+enum kx_dispatch_policy {
+  KX_DISPATCH_TIME_SLOT = 0,
+  KX_DISPATCH_ROUND_ROBIN = 1,
+  KX_DISPATCH_STATIC_THRESHOLD = 2
+};
+
+/* InstanceProfile (engine.hpp:25-31) plus the pool (shared LLM) it serves. */
+typedef struct kx_instance {
+  int32_t id;              /* InstanceId (dispatcher.hpp:14) */
+  int32_t pool;            /* 0..n_pools-1 */
+  double capacity_tokens;
+  double decode_rate;      /* k, tokens/s per request */
+  double prefill_rate;     /* prompt tokens/s */
+  int32_t max_batch;
+  int32_t _pad;
+} kx_instance;
+
+/* DispatcherConfig (dispatcher.hpp:112-121) + EngineConfig fields the
+ * dispatch loop reads (engine.hpp:33-41). */
+typedef struct kx_dispatcher_config {
+  int32_t policy;                 /* kx_dispatch_policy */
+  int32_t oracle_expected_time;   /* T = pure_exec of the request */
+  double slot_len;                /* 0.5 */
+  double resume_watermark;        /* 0.85 */
+  double static_threshold;        /* 0.90 */
+  double default_expected_time;   /* 1.0 */
+} kx_dispatcher_config;
+
+typedef struct kx_sched_config {
+  int32_t n_pools;                /* independent shared-LLM pools */
+  int32_t n_instances;
+  const kx_instance* instances;   /* host array, n_instances; pool-grouped order = Dispatcher ids_ order */
+  kx_dispatcher_config dispatcher;
+  int64_t queue_capacity;         /* max queued requests (all pools) */
+  int32_t max_agents;             /* capacity of the per-agent tables */
+  int32_t slot_ring;              /* ledger slots kept per instance (power of 2, >= 64) */
+  int32_t device;                 /* CUDA device ordinal */
+  int32_t log_capacity_per_pool;  /* decision-log rows per pool per round (0 = default) */
+} kx_sched_config;
+
+/* Queue contents, one element per PendingRequest (types.hpp:35-42).
+ * msg_key is any u64 whose order equals the lexicographic order of msg_id
+ * strings in the queue; agent is a dense agent index. */
+typedef struct kx_queue_view {
+  const int32_t* agent;
+  const int64_t* prompt_tokens;
+  const double* app_start;
+  const double* queue_enter;
+  const uint64_t* msg_key;
+  const uint64_t* uid;
+  const int64_t* kept_tokens;     /* nullable: CallRuntime::kept_tokens (engine.cpp:306-307) */
+  const double* pure_exec;        /* nullable: required when oracle_expected_time */
+} kx_queue_view;
+
+/* DecisionLogRow (engine.hpp:92-99) plus bookkeeping. */
+typedef struct kx_decision {
+  double time;
+  double predicted_peak;
+  uint64_t uid;
+  int64_t queue_index;            /* index into the uploaded queue */
+  int32_t agent;
+  int32_t target;                 /* InstanceId, -1 = none (dispatch stops) */
+  int32_t pool;
+  int32_t admitted;               /* 1 = popped+committed+admitted; 0 = overload retry / no target */
+} kx_decision;
+
+typedef struct kx_sched kx_sched;
+
+int kx_abi_version(void);
+const char* kx_last_error(void);
+/* 1 when an sm_100-class device is visible, 0 otherwise (no error). */
+int kx_device_available(void);
+
+/* ---- handle lifecycle ------------------------------------------------- */
+/* Replaces Dispatcher::Dispatcher (dispatcher.cpp:185-198) + Simulator's
+ * per-instance state (engine.hpp:147-153) + ReadyQueue storage. */
+int kx_sched_create(const kx_sched_config* cfg, kx_sched** out);
+int kx_sched_destroy(kx_sched* s);
+int kx_sched_stream(kx_sched* s, void** cuda_stream);
+int kx_sched_synchronize(kx_sched* s);
+
+/* ---- scheduler policy (scheduler.hpp:31-44) ----------------------------- */
+int kx_set_scheduler(kx_sched* s, int32_t kind);
+/* Per-agent tables, indexed by dense agent index:
+ *   agent_pool[a]   pool whose queue/instances serve agent a
+ *   priority_key[a] PriorityTable::priority_key(agent) incl. the cold-start
+ *                   median (priority.cpp:114-135); Kairos only
+ *   topo_depth[a]   TopoDepthScheduler::depth_of (scheduler.hpp:71-74)
+ *   expected_T[a]   ProfilerSnapshot::expected_exec_time(agent, default)
+ *                   (profiler.cpp:11-16, engine.cpp:177-185)
+ * Any of the three value tables may be NULL (kept from the previous call). */
+int kx_set_agent_tables(kx_sched* s, int32_t n_agents, const int32_t* agent_pool,
+                        const double* priority_key, const int32_t* topo_depth,
+                        const double* expected_T, uint64_t version);
+/* OracleScheduler's remaining_by_uid (scheduler.hpp:84-89): dense over
+ * [uid_base, uid_base + n); present[i] == 0 means "absent" (key 0.0). */
+int kx_set_remaining_table(kx_sched* s, uint64_t uid_base, int64_t n,
+                           const double* remaining, const uint8_t* present, int32_t mem);
+
+/* ---- ready queue (priority.hpp:70-116) ----------------------------------- */
+/* Replaces ReadyQueue contents with n requests (ReadyQueue::enqueue x n). */
+int kx_queue_upload(kx_sched* s, int64_t n, const kx_queue_view* q, int32_t mem);
+int kx_queue_size(kx_sched* s, int64_t* n);
+/* Drops every request admitted by the last dispatch round (ReadyQueue::pop
+ * of the placed prefix), keeping the others in their relative order. */
+int kx_queue_remove_admitted(kx_sched* s);
+
+/* K2: per-request OrderKey (SchedulerPolicy::order_key, scheduler.hpp:17-27),
+ * written in queue order. */
+int kx_score(kx_sched* s, double* k0, double* k1, double* k2, int32_t mem);
+
+/* K2+K3+K4: the full queue order under the active policy: the permutation
+ * std::sort with the ReadyQueue comparator would produce (priority.hpp:89-103,
+ * harness.cpp:92-100), grouped by pool. Asynchronous on the handle's stream. */
+int kx_order(kx_sched* s);
+/* perm[n] (queue indices, sorted), pool_offsets[n_pools + 1]. */
+int kx_order_fetch(kx_sched* s, uint32_t* perm, int64_t* pool_offsets, int32_t mem);
+
+/* K5: one dispatch round at time `now` over the last order: the placement
+ * part of Simulator::dispatch_loop (engine.cpp:220-268) with
+ * Dispatcher::choose/commit (dispatcher.cpp:207-262), the admission
+ * bookkeeping of admit (engine.cpp:298-319), try_admit (270-296) and
+ * Dispatcher::gc (engine.cpp:212). One CTA per pool. Asynchronous. */
+int kx_dispatch_round(kx_sched* s, double now);
+/* Copies the decision log of the last round. per_pool_count[n_pools]:
+ * rows written per pool; rows[] and candidate_peaks[] are pool-major with
+ * `row_stride` rows per pool and `peak_stride` peaks per row (>= max
+ * instances in a pool). Any output pointer may be NULL. Synchronizes. */
+int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
+                      double* candidate_peaks, int64_t* row_stride, int64_t* peak_stride);
+
+/* One scheduling tick: kx_order + kx_dispatch_round (asynchronous). */
+int kx_tick(kx_sched* s, double now);
+
+/* ---- instance / ledger state (dispatcher.cpp:44-123, 264-297) ---------- */
+/* Engine-side live view (engine.cpp:187-202): live_kv, running, waiting,
+ * indexed by position in the kx_sched_config.instances array. */
+int kx_instances_set_live(kx_sched* s, const double* live_kv, const int32_t* running,
+                          const int32_t* waiting);
+int kx_instances_get_live(kx_sched* s, double* live_kv, int32_t* running, int32_t* waiting,
+                          uint8_t* suspended);
+/* SlotLedger::try_place (dispatcher.cpp:52-68) without booking. */
+int kx_ledger_try_place(kx_sched* s, int32_t instance_id, double prefill_tokens,
+                        double decode_rate, double t_start, double expected_duration,
+                        int32_t* fits, double* predicted_peak, int64_t* violating_slot);
+/* SlotLedger::commit (dispatcher.cpp:70-79); KX_ERR_LOGIC when it exceeds. */
+int kx_ledger_commit(kx_sched* s, int32_t instance_id, uint64_t uid, double prefill_tokens,
+                     double decode_rate, double t_start, double expected_duration);
+/* Many SlotLedger::commit calls at once (e.g. preloading a pool): entry j
+ * books (uid[j], P[j], k[j], t0[j], T[j]) on instance_id[j] if try_place
+ * fits, in array order per instance; fits_out[j] = 1/0 (nullable). */
+int kx_ledger_commit_batch(kx_sched* s, int64_t n, const int32_t* instance_id, const uint64_t* uid,
+                           const double* prefill_tokens, const double* decode_rate,
+                           const double* t_start, const double* expected_duration,
+                           uint8_t* fits_out);
+/* Dispatcher::on_request_finished / on_request_preempted (dispatcher.cpp:264-276). */
+int kx_on_request_finished(kx_sched* s, int32_t instance_id, uint64_t uid, double actual_end);
+/* Dispatcher::on_overload / on_live_usage / suspended (dispatcher.cpp:278-293). */
+int kx_on_overload(kx_sched* s, int32_t instance_id);
+int kx_on_live_usage(kx_sched* s, int32_t instance_id, double live_kv);
+/* Dispatcher::gc (dispatcher.cpp:295-297). */
+int kx_gc(kx_sched* s, double now);
+/* Dense ledger view: usage[slot_ring] and exists[slot_ring] for slots
+ * base_slot .. base_slot + slot_ring - 1; active request count. */
+int kx_ledger_read(kx_sched* s, int32_t instance_id, int64_t* base_slot, double* usage,
+                   uint8_t* exists, int32_t* active_requests);
+/* Device-side snapshot of all mutable instance/ledger state, and restore. */
+int kx_state_checkpoint(kx_sched* s);
+int kx_state_restore(kx_sched* s);
+
+/* ---- measurement ---------------------------------------------------------- */
+/* Per-phase device timing with CUDA events recorded on the handle's stream
+ * around every launch of a phase (score/range, keygen, each radix pass,
+ * tie-fix, dispatch). Algorithmic bytes are the library's own per-phase
+ * accounting. */
+typedef struct kx_phase_stat {
+  char name[32];
+  double total_ms;
+  int64_t launches;
+  double alg_bytes;  /* summed over launches */
+} kx_phase_stat;
+int kx_profile_enable(kx_sched* s, int32_t enable);  /* also clears the stats */
+int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out);
+/* Kernels launched by this library (all handles) since load. */
+int64_t kx_launch_count(void);
+
+/* ---- K1: orchestrator DP ------------------------------------------------ */
+/* finalize_instance (workload.cpp:292-315) for many workflow instances at
+ * once: calls of workflow w are [wf_offsets[w], wf_offsets[w+1]), in node_id
+ * order; parent[c] is the parent's node_id within its workflow (-1 = root).
+ * Writes uid (uid_base + global call index), pure_exec and remaining_exec.
+ * One warp per workflow, reverse topological. Synchronous. */
+int kx_orchestrator_dp(int64_t n_workflows, const int64_t* wf_offsets, const int32_t* parent,
+                       const int64_t* prompt_tokens, const int64_t* target_tokens,
+                       double prefill_rate, double decode_rate, uint64_t uid_base,
+                       uint64_t* uid_out, double* pure_exec_out, double* remaining_out,
+                       int32_t mem);
+/* LatencyProfiler::record_remaining's arithmetic (profiler.cpp:31-50) for
+ * many completed workflows: finish = max exec_end (seeded with the first
+ * record), sample[r] = finish - exec_start[r]. Synchronous. */
+int kx_record_remaining(int64_t n_workflows, const int64_t* rec_offsets,
+                        const double* exec_start, const double* exec_end,
+                        double* finish_out, double* samples_out, int32_t mem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KAIROS_B200_H_ */

@@ -1,0 +1,216 @@
+// TEST / BASELINE INFRASTRUCTURE ONLY. A C-ABI bridge around the UNMODIFIED
+// reference (libkairos_ref.a built from /root/reference/proj by
+// oracle/Makefile) so bench.py can time the reference's own CPU
+// implementation of the scheduling tick:
+//   ordering  std::sort with the ReadyQueue comparator over
+//             SchedulerPolicy::order_key (harness.cpp:92-100, priority.hpp:95-98)
+//   placement the dispatch_loop sequence of engine.cpp:220-268 over the
+//             ordered queue with the reference Dispatcher
+//             (collect_live -> choose -> overload check -> commit -> admit)
+//             and Dispatcher::gc (engine.cpp:212).
+// The ordered-prefix walk replaces the reference's repeated best_index
+// scans (O(D*N) per round), which only makes the baseline faster.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kairos/dispatcher.hpp"
+#include "kairos/priority.hpp"
+#include "kairos/scheduler.hpp"
+
+using namespace kairos;
+
+namespace {
+
+struct TablePolicy : SchedulerPolicy {
+  // KairosScheduler::order_key (scheduler.hpp:111-113) over a fixed table.
+  PriorityTable table;
+  std::string name() const override { return "kairos"; }
+  OrderKey order_key(const PendingRequest& r) const override {
+    return {table.priority_key(r.agent), r.app_start, r.queue_enter};
+  }
+};
+
+struct RefPool {
+  std::unique_ptr<SchedulerPolicy> policy;
+  std::vector<InstanceId> ids;
+  std::vector<double> caps, ks;
+  std::vector<int> max_batch;
+  DispatcherConfig dcfg;
+  std::unique_ptr<Dispatcher> pristine_disp, disp;
+  std::vector<double> live0, live;
+  std::vector<int> running0, running, waiting0, waiting;
+  std::map<AgentId, double> T;
+  std::vector<PendingRequest> queue0, queue;
+  int64_t last_admitted = 0;
+  int64_t last_decisions = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+// sched_kind: 0 kairos, 1 fcfs, 2 topo_depth, 3 oracle (the latter unused).
+void* kxref_pool_new(int n_inst, const int32_t* ids, const double* caps, const double* ks,
+                     const int32_t* max_batch, double slot_len, double watermark, int sched_kind,
+                     int n_agents, const char* const* agent_names, const double* pk,
+                     const uint8_t* pk_known, const int32_t* depth, const double* T) {
+  auto* p = new RefPool();
+  for (int i = 0; i < n_inst; ++i) {
+    p->ids.push_back(ids[i]);
+    p->caps.push_back(caps[i]);
+    p->ks.push_back(ks[i]);
+    p->max_batch.push_back(max_batch[i]);
+  }
+  p->dcfg.policy = DispatchPolicy::TimeSlot;
+  p->dcfg.slot_len = slot_len;
+  p->dcfg.resume_watermark = watermark;
+  p->pristine_disp = std::make_unique<Dispatcher>(p->dcfg, p->ids, p->caps, p->ks);
+  std::map<AgentId, int> depths;
+  auto tp = std::make_unique<TablePolicy>();
+  tp->table.anchor_coord = 0.0;
+  for (int a = 0; a < n_agents; ++a) {
+    const std::string name = agent_names[a];
+    if (pk_known[a]) tp->table.coord[name] = pk[a];  // |coord - 0| = pk
+    depths[name] = depth[a];
+    p->T[name] = T[a];
+  }
+  switch (sched_kind) {
+    case 1: p->policy = std::make_unique<FcfsScheduler>(); break;
+    case 2: p->policy = std::make_unique<TopoDepthScheduler>(depths); break;
+    default: p->policy = std::move(tp); break;
+  }
+  p->live0.assign(n_inst, 0.0);
+  p->running0.assign(n_inst, 0);
+  p->waiting0.assign(n_inst, 0);
+  return p;
+}
+
+void kxref_pool_free(void* h) { delete static_cast<RefPool*>(h); }
+
+void kxref_pool_set_live(void* h, const double* live, const int32_t* running, const int32_t* waiting) {
+  auto* p = static_cast<RefPool*>(h);
+  p->live0.assign(live, live + p->ids.size());
+  p->running0.assign(running, running + p->ids.size());
+  p->waiting0.assign(waiting, waiting + p->ids.size());
+}
+
+// SlotLedger preload through Dispatcher::commit (dispatcher.cpp:252-262).
+int kxref_pool_commit(void* h, int32_t instance_id, uint64_t uid, int64_t prompt, double t0, double T) {
+  auto* p = static_cast<RefPool*>(h);
+  DispatchDecision d;
+  d.request.uid = uid;
+  d.request.prompt_tokens = prompt;
+  d.target = instance_id;
+  try {
+    p->pristine_disp->commit(d, t0, T);
+  } catch (...) {
+    return 1;
+  }
+  return 0;
+}
+
+// Queue contents; msg ids are "m-<msg_counter>" (MessageIdFactory, types.hpp:46-57).
+void kxref_pool_set_queue(void* h, int64_t n, const int32_t* agent, const int64_t* prompt,
+                          const double* app, const double* qe, const uint64_t* msg_counter,
+                          const uint64_t* uid, const char* const* agent_names) {
+  auto* p = static_cast<RefPool*>(h);
+  p->queue0.clear();
+  p->queue0.reserve(static_cast<std::size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    PendingRequest r;
+    r.msg_id = "m-" + std::to_string(msg_counter[i]);
+    r.agent = agent_names[agent[i]];
+    r.prompt_tokens = prompt[i];
+    r.app_start = app[i];
+    r.queue_enter = qe[i];
+    r.uid = uid[i];
+    p->queue0.push_back(std::move(r));
+  }
+}
+
+// Untimed: restore the pre-tick state (unsorted queue, pristine ledgers, live).
+void kxref_pool_reset(void* h) {
+  auto* p = static_cast<RefPool*>(h);
+  p->queue = p->queue0;
+  p->disp = std::make_unique<Dispatcher>(*p->pristine_disp);
+  p->live = p->live0;
+  p->running = p->running0;
+  p->waiting = p->waiting0;
+}
+
+// Timed: one scheduling tick (order + dispatch + gc). Returns admitted count.
+int64_t kxref_pool_tick(void* h, double now) {
+  auto* p = static_cast<RefPool*>(h);
+  const SchedulerPolicy& s = *p->policy;
+  std::sort(p->queue.begin(), p->queue.end(), [&](const PendingRequest& a, const PendingRequest& b) {
+    const auto ka = s.order_key(a);
+    const auto kb = s.order_key(b);
+    return std::tie(ka, a.app_start, a.queue_enter, a.msg_id, a.uid) <
+           std::tie(kb, b.app_start, b.queue_enter, b.msg_id, b.uid);
+  });
+  int64_t admitted = 0, decisions = 0;
+  const std::size_t ni = p->ids.size();
+  std::size_t pos = 0;
+  while (pos < p->queue.size()) {
+    const PendingRequest& head = p->queue[pos];
+    auto it = p->T.find(head.agent);
+    const double T = it == p->T.end() ? p->dcfg.default_expected_time : it->second;
+    std::vector<InstanceLive> live(ni);
+    for (std::size_t i = 0; i < ni; ++i) {
+      p->disp->on_live_usage(p->ids[i], p->live[i]);
+      live[i].live_kv = p->live[i];
+      live[i].running = p->running[i];
+      live[i].waiting = p->waiting[i];
+      live[i].batch_full = live[i].running + live[i].waiting >= p->max_batch[i];
+    }
+    DispatchDecision d = p->disp->choose(head, now, T, live);
+    ++decisions;
+    if (!d.target) break;
+    const std::size_t ti =
+        static_cast<std::size_t>(std::find(p->ids.begin(), p->ids.end(), *d.target) - p->ids.begin());
+    if (p->live[ti] + static_cast<double>(head.prompt_tokens) > p->caps[ti]) {
+      p->disp->on_overload(*d.target);
+      if (decisions > static_cast<int64_t>(p->queue.size() + 4 * ni + 16)) break;  // H6 guard
+      continue;
+    }
+    p->disp->commit(d, now, T);
+    p->live[ti] += static_cast<double>(head.prompt_tokens);
+    p->running[ti] += 1;
+    ++admitted;
+    ++pos;
+  }
+  p->disp->gc(now);
+  p->last_admitted = admitted;
+  p->last_decisions = decisions;
+  return admitted;
+}
+
+int64_t kxref_pool_last_decisions(void* h) { return static_cast<RefPool*>(h)->last_decisions; }
+
+// Ticks `n` pools concurrently on up to `threads` threads (the reference's
+// std::async-per-cell model, harness.cpp:189-206); returns wall seconds.
+double kxref_pools_tick(void** pools, int n, double now, int threads) {
+  for (int i = 0; i < n; ++i) kxref_pool_reset(pools[i]);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (threads <= 1) {
+    for (int i = 0; i < n; ++i) kxref_pool_tick(pools[i], now);
+  } else {
+    for (int start = 0; start < n; start += threads) {
+      std::vector<std::thread> ts;
+      for (int i = start; i < std::min(n, start + threads); ++i)
+        ts.emplace_back([=] { kxref_pool_tick(pools[i], now); });
+      for (auto& t : ts) t.join();
+    }
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+"""ctypes binding of the C ABI in include/kairos_b200.h.
+
+This is plumbing for tests and the benchmark: every computation happens in
+the CUDA kernels of libkairos_b200.so. Loading fails loudly when the library
+has not been built (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libkairos_b200.so"
+HEADER_PATH = _PKG.parent / "include" / "kairos_b200.h"
+
+KX_OK = 0
+KX_ERR_INVALID = 1
+KX_ERR_LOGIC = 2
+KX_ERR_RUNTIME = 3
+KX_ERR_CUDA = 4
+KX_ERR_CAPACITY = 5
+KX_ERR_LIVELOCK = 6
+
+KX_MEM_HOST = 0
+KX_MEM_DEVICE = 1
+
+SCHED = {"kairos": 0, "fcfs": 1, "topo_depth": 2, "oracle": 3}
+DISPATCH = {"time_slot": 0, "round_robin": 1, "static_threshold": 2}
+
+
+class KxError(RuntimeError):
+    """Raised for a non-zero kx status; `code` maps to the reference's
+    exception type (1 invalid_argument, 2 logic_error, 3 runtime_error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[kx status {code}] {msg}")
+        self.code = code
+
+
+class kx_instance(C.Structure):
+    _fields_ = [("id", C.c_int32), ("pool", C.c_int32), ("capacity_tokens", C.c_double),
+                ("decode_rate", C.c_double), ("prefill_rate", C.c_double),
+                ("max_batch", C.c_int32), ("_pad", C.c_int32)]
+
+
+class kx_dispatcher_config(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("oracle_expected_time", C.c_int32),
+                ("slot_len", C.c_double), ("resume_watermark", C.c_double),
+                ("static_threshold", C.c_double), ("default_expected_time", C.c_double)]
+
+
+class kx_sched_config(C.Structure):
+    _fields_ = [("n_pools", C.c_int32), ("n_instances", C.c_int32),
+                ("instances", C.POINTER(kx_instance)), ("dispatcher", kx_dispatcher_config),
+                ("queue_capacity", C.c_int64), ("max_agents", C.c_int32),
+                ("slot_ring", C.c_int32), ("device", C.c_int32),
+                ("log_capacity_per_pool", C.c_int32)]
+
+
+class kx_queue_view(C.Structure):
+    _fields_ = [("agent", C.c_void_p), ("prompt_tokens", C.c_void_p), ("app_start", C.c_void_p),
+                ("queue_enter", C.c_void_p), ("msg_key", C.c_void_p), ("uid", C.c_void_p),
+                ("kept_tokens", C.c_void_p), ("pure_exec", C.c_void_p)]
+
+
+class kx_decision(C.Structure):
+    _fields_ = [("time", C.c_double), ("predicted_peak", C.c_double), ("uid", C.c_uint64),
+                ("queue_index", C.c_int64), ("agent", C.c_int32), ("target", C.c_int32),
+                ("pool", C.c_int32), ("admitted", C.c_int32)]
+
+
+class kx_phase_stat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("total_ms", C.c_double), ("launches", C.c_int64),
+                ("alg_bytes", C.c_double)]
+
+
+# name -> (restype, argtypes)
+_P = C.c_void_p
+SIGNATURES = {
+    "kx_abi_version": (C.c_int, []),
+    "kx_last_error": (C.c_char_p, []),
+    "kx_device_available": (C.c_int, []),
+    "kx_sched_create": (C.c_int, [C.POINTER(kx_sched_config), C.POINTER(_P)]),
+    "kx_sched_destroy": (C.c_int, [_P]),
+    "kx_sched_stream": (C.c_int, [_P, C.POINTER(_P)]),
+    "kx_sched_synchronize": (C.c_int, [_P]),
+    "kx_set_scheduler": (C.c_int, [_P, C.c_int32]),
+    "kx_set_agent_tables": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.c_uint64]),
+    "kx_set_remaining_table": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P, C.c_int32]),
+    "kx_queue_upload": (C.c_int, [_P, C.c_int64, C.POINTER(kx_queue_view), C.c_int32]),
+    "kx_queue_size": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "kx_queue_remove_admitted": (C.c_int, [_P]),
+    "kx_score": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    "kx_order": (C.c_int, [_P]),
+    "kx_order_fetch": (C.c_int, [_P, _P, _P, C.c_int32]),
+    "kx_dispatch_round": (C.c_int, [_P, C.c_double]),
+    "kx_dispatch_fetch": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "kx_tick": (C.c_int, [_P, C.c_double]),
+    "kx_instances_set_live": (C.c_int, [_P, _P, _P, _P]),
+    "kx_instances_get_live": (C.c_int, [_P, _P, _P, _P, _P]),
+    "kx_ledger_try_place": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64)]),
+    "kx_ledger_commit": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                   C.c_double]),
+    "kx_ledger_commit_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "kx_on_request_finished": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_double]),
+    "kx_on_overload": (C.c_int, [_P, C.c_int32]),
+    "kx_on_live_usage": (C.c_int, [_P, C.c_int32, C.c_double]),
+    "kx_gc": (C.c_int, [_P, C.c_double]),
+    "kx_ledger_read": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64), _P, _P, C.POINTER(C.c_int32)]),
+    "kx_state_checkpoint": (C.c_int, [_P]),
+    "kx_state_restore": (C.c_int, [_P]),
+    "kx_profile_enable": (C.c_int, [_P, C.c_int32]),
+    "kx_profile_read": (C.c_int, [_P, C.POINTER(kx_phase_stat), C.c_int32, C.POINTER(C.c_int32)]),
+    "kx_launch_count": (C.c_int64, []),
+    "kx_orchestrator_dp": (C.c_int, [C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, C.c_uint64,
+                                     _P, _P, _P, C.c_int32]),
+    "kx_record_remaining": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, C.c_int32]),
+}
+
+_lib = None
+
+
+def load(path: str | os.PathLike | None = None) -> C.CDLL:
+    """Load libkairos_b200.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA library first (`make` or __graft_entry__.build()). "
+            "The kairos_b200 scheduling path has no CPU fallback.")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.kx_abi_version() != 1:
+        raise RuntimeError("ABI version mismatch")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != KX_OK:
+        msg = _lib.kx_last_error().decode() if _lib is not None else ""
+        raise KxError(status, msg)
+
+
+def ptr(a) -> int | None:
+    """Address of a numpy array or torch tensor (None passes through)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data

@@ -1,0 +1,1295 @@
+// extern "C" implementation of include/kairos_b200.h: handle lifecycle,
+// device allocation, uploads, and the launches of K1-K5. Host code here is
+// plumbing only; every computation runs in the CUDA kernels.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <type_traits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/kairos_b200.h"
+#include "kx_common.cuh"
+#include "kx_dispatch.cuh"
+#include "kx_order.cuh"
+#include "kx_state.cuh"
+
+namespace kx {
+std::atomic<long long> g_kx_launches{0};
+
+void launch_orchestrator_dp(int64_t n_wf, const int64_t* off, const int32_t* parent,
+                            const int64_t* prompt, const int64_t* target, double prefill,
+                            double decode, uint64_t uid_base, uint64_t* uid_out, double* pure_out,
+                            double* rem_out, int* error, int sms, cudaStream_t st);
+void launch_record_remaining(int64_t n_wf, const int64_t* off, const double* es, const double* ee,
+                             double* fin, double* samples, int sms, cudaStream_t st);
+
+// ---- small utility kernels ---------------------------------------------
+__global__ void k_fill_rem(QueueDev q, int64_t n, const double* __restrict__ table,
+                           const uint8_t* __restrict__ present, uint64_t base, int64_t tn) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double r = 0.0;  // OracleScheduler: absent uid -> 0.0 (scheduler.hpp:86-87)
+    if (table) {
+      const uint64_t u = q.uid[i];
+      if (u >= base && u - base < static_cast<uint64_t>(tn) && present[u - base]) r = table[u - base];
+    }
+    q.rem[i] = r;
+  }
+}
+
+__global__ void k_validate_queue(QueueDev q, int64_t n, int n_agents, int need_pure,
+                                 int* __restrict__ err) {
+  int e = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t a = q.agent[i];
+    if (a < 0 || a >= n_agents) e |= 1;
+    const double x = q.app_start[i], y = q.queue_enter[i];
+    if (x != x || y != y) e |= 2;
+    if (need_pure && q.pure_exec[i] != q.pure_exec[i]) e |= 2;
+  }
+  if (e) atomicOr(err, e);
+}
+
+__global__ void k_flag_count(const uint8_t* __restrict__ flags, int64_t n, int chunk,
+                             uint32_t* __restrict__ keep_counts) {
+  const int64_t b = int64_t(blockIdx.x) * chunk;
+  const int64_t e = min(b + chunk, n);
+  uint32_t c = 0;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) c += flags[i] ? 0u : 1u;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ uint32_t s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    keep_counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_scan_counts(uint32_t* __restrict__ c, int64_t m, int64_t* __restrict__ total) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int64_t i = 0; i < m; ++i) {
+      const uint32_t v = c[i];
+      c[i] = static_cast<uint32_t>(acc);
+      acc += v;
+    }
+    *total = static_cast<int64_t>(acc);
+  }
+}
+
+template <typename T>
+__global__ void k_compact(const T* __restrict__ src, T* __restrict__ dst,
+                          const uint8_t* __restrict__ flags, int64_t n, int chunk,
+                          const uint32_t* __restrict__ offs) {
+  // One warp walks its CTA's chunk in order (stable).
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int64_t b = int64_t(blockIdx.x) * chunk;
+  const int64_t e = min(b + chunk, n);
+  uint32_t out = offs[blockIdx.x];
+  for (int64_t i0 = b; i0 < e; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool keep = i < e && !flags[i];
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (keep) dst[out + __popc(m & ((1u << lane) - 1u))] = src[i];
+    out += __popc(m);
+  }
+}
+
+}  // namespace kx
+
+using namespace kx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return KX_OK;
+  } catch (const KxError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return KX_ERR_INVALID;
+  } catch (const std::logic_error& e) {
+    g_last_error = e.what();
+    return KX_ERR_LOGIC;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = "out of host memory";
+    return KX_ERR_CAPACITY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return KX_ERR_RUNTIME;
+  }
+}
+
+[[noreturn]] void fail(int code, const std::string& m) { throw KxError(code, m); }
+
+void require(bool ok, const std::string& m) {
+  if (!ok) throw std::invalid_argument(m);
+}
+
+int sm_count(int dev) {
+  int n = 0;
+  KX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+void ensure_device(int dev) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= dev)
+    fail(KX_ERR_CUDA, "no CUDA device available (the kairos_b200 path has no CPU fallback)");
+  cudaDeviceProp p{};
+  KX_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (p.major < 10)
+    fail(KX_ERR_CUDA, "kairos_b200 is built for sm_100a (B200); found sm_" +
+                          std::to_string(p.major) + std::to_string(p.minor));
+  KX_CUDA(cudaSetDevice(dev));
+}
+
+// Device bump allocation inside one cudaMalloc'ed blob.
+struct Blob {
+  char* base = nullptr;
+  size_t size = 0;
+};
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t off = 0;
+  template <typename T>
+  size_t take(size_t count) {
+    const size_t o = off;
+    off = align_up(off + count * sizeof(T));
+    return o;
+  }
+};
+
+}  // namespace
+
+struct kx_sched {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  kx_dispatcher_config dcfg{};
+  int n_pools = 0;
+  int n_inst = 0;
+  int ring = 256;
+  int max_inst_per_pool = 0;
+  int64_t cap = 0;
+  int64_t n = 0;
+  int32_t max_agents = 0;
+  int32_t n_agents = 0;
+  int32_t sched_kind = KX_SCHED_KAIROS;
+  int32_t n_pk_classes = 1;
+  int32_t n_depth_classes = 1;
+  std::vector<kx_instance> inst_host;
+  std::vector<int32_t> pool_begin_host;
+
+  QueueDev q{};
+  AgentsDev a{};
+  InstDev in{};
+  int32_t* pool_begin = nullptr;
+  Blob queue_blob, agent_blob, inst_const_blob, inst_mut_blob, inst_ckpt_blob, ws_blob, log_blob;
+  bool have_ckpt = false;
+
+  OrderWorkspace ws{};
+  OrderResultDev order{};
+  bool order_valid = false;
+  int64_t order_n = 0;
+
+  double* rem_table = nullptr;
+  uint8_t* rem_present = nullptr;
+  uint64_t rem_base = 0;
+  int64_t rem_n = 0;
+
+  int64_t log_cap = 0;
+  kx_decision* rows = nullptr;
+  double* cand = nullptr;
+  int64_t* row_count = nullptr;
+  int64_t* admitted_count = nullptr;
+  int* pool_status = nullptr;
+  bool dispatch_valid = false;
+
+  // scratch
+  int* err_flag = nullptr;
+  double* scratch_d = nullptr;
+  int64_t* scratch_i = nullptr;
+  int* scratch_s = nullptr;
+  uint32_t* compact_counts = nullptr;
+  int64_t* compact_total = nullptr;
+
+  PhaseProfiler prof;
+};
+
+namespace {
+
+void alloc_blob(Blob& b, size_t bytes) {
+  b.size = std::max<size_t>(bytes, 256);
+  KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&b.base), b.size));
+  KX_CUDA(cudaMemset(b.base, 0, b.size));
+}
+
+void free_blob(Blob& b) {
+  if (b.base) cudaFree(b.base);
+  b.base = nullptr;
+}
+
+template <typename T>
+T* at(const Blob& b, size_t off) {
+  return reinterpret_cast<T*>(b.base + off);
+}
+
+constexpr int64_t kCompactChunk = 8192;
+
+void check_err_flag(kx_sched* s, const char* what) {
+  int h = 0;
+  KX_CUDA(cudaMemcpyAsync(&h, s->err_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  KX_CUDA(cudaStreamSynchronize(s->stream));
+  if (h & 1) fail(KX_ERR_INVALID, std::string(what) + ": agent index outside the agent table");
+  if (h & 2) fail(KX_ERR_INVALID, std::string(what) + ": NaN time value");
+  if (h & 4) fail(KX_ERR_INVALID, std::string(what) + ": parent link is not parents-first");
+}
+
+void create_impl(const kx_sched_config* cfg, kx_sched** out) {
+  require(cfg && out, "null argument");
+  require(cfg->n_pools >= 1 && cfg->n_pools <= 1024, "n_pools must be in [1, 1024]");
+  require(cfg->n_instances >= 1 && cfg->instances, "dispatcher needs matching instance lists");
+  require(cfg->queue_capacity >= 1 && cfg->queue_capacity < (int64_t(1) << 30),
+          "queue_capacity must be in [1, 2^30)");
+  const int ring = cfg->slot_ring ? cfg->slot_ring : 256;
+  require(ring >= 64 && (ring & (ring - 1)) == 0, "slot_ring must be a power of two >= 64");
+  const auto& dc = cfg->dispatcher;
+  require(dc.slot_len > 0.0, "slot_len must be positive");
+  require(dc.policy >= 0 && dc.policy <= 2, "unknown dispatcher policy");
+  require(cfg->max_agents >= 1, "max_agents must be positive");
+
+  std::vector<int32_t> pool_begin(cfg->n_pools + 1, 0);
+  int prev_pool = -1;
+  std::vector<int32_t> ids;
+  for (int i = 0; i < cfg->n_instances; ++i) {
+    const kx_instance& p = cfg->instances[i];
+    require(p.pool >= 0 && p.pool < cfg->n_pools, "instance pool out of range");
+    require(p.pool >= prev_pool, "instances must be grouped by pool (non-decreasing pool)");
+    require(p.capacity_tokens > 0.0 && p.decode_rate > 0.0 && p.prefill_rate > 0.0 &&
+                p.max_batch >= 1,
+            "instance profile fields must be positive");
+    prev_pool = p.pool;
+    pool_begin[p.pool + 1] += 1;
+    ids.push_back(p.id);
+  }
+  std::sort(ids.begin(), ids.end());
+  require(std::adjacent_find(ids.begin(), ids.end()) == ids.end(), "duplicate instance id");
+  int max_pp = 0;
+  for (int p = 0; p < cfg->n_pools; ++p) {
+    require(pool_begin[p + 1] >= 1, "every pool needs at least one instance");
+    max_pp = std::max(max_pp, pool_begin[p + 1]);
+    pool_begin[p + 1] += pool_begin[p];
+  }
+  require(max_pp <= kMaxInstPerPool, "too many instances in one pool (max 512)");
+
+  ensure_device(cfg->device);
+  auto s = std::make_unique<kx_sched>();
+  s->device = cfg->device;
+  s->sms = sm_count(cfg->device);
+  KX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  s->dcfg = dc;
+  s->n_pools = cfg->n_pools;
+  s->n_inst = cfg->n_instances;
+  s->ring = ring;
+  s->max_inst_per_pool = max_pp;
+  s->cap = cfg->queue_capacity;
+  s->max_agents = cfg->max_agents;
+  s->inst_host.assign(cfg->instances, cfg->instances + cfg->n_instances);
+  s->pool_begin_host = pool_begin;
+  configure_sort_kernels();
+
+  // queue SoA
+  {
+    const size_t N = static_cast<size_t>(s->cap);
+    Layout L;
+    const size_t o_agent = L.take<int32_t>(N), o_prompt = L.take<int64_t>(N),
+                 o_app = L.take<double>(N), o_qe = L.take<double>(N), o_msg = L.take<uint64_t>(N),
+                 o_uid = L.take<uint64_t>(N), o_kept = L.take<int64_t>(N),
+                 o_pure = L.take<double>(N), o_rem = L.take<double>(N),
+                 o_adm = L.take<uint8_t>(N);
+    alloc_blob(s->queue_blob, L.off);
+    auto& b = s->queue_blob;
+    s->q = QueueDev{at<int32_t>(b, o_agent), at<int64_t>(b, o_prompt), at<double>(b, o_app),
+                    at<double>(b, o_qe),     at<uint64_t>(b, o_msg),   at<uint64_t>(b, o_uid),
+                    at<int64_t>(b, o_kept),  at<double>(b, o_pure),    at<double>(b, o_rem),
+                    at<uint8_t>(b, o_adm)};
+  }
+  // agent tables
+  {
+    const size_t A = static_cast<size_t>(s->max_agents);
+    Layout L;
+    const size_t o_pool = L.take<int32_t>(A), o_pk = L.take<double>(A),
+                 o_pkr = L.take<uint32_t>(A), o_d = L.take<int32_t>(A),
+                 o_dr = L.take<uint32_t>(A), o_T = L.take<double>(A);
+    alloc_blob(s->agent_blob, L.off);
+    auto& b = s->agent_blob;
+    s->a = AgentsDev{at<int32_t>(b, o_pool), at<double>(b, o_pk), at<uint32_t>(b, o_pkr),
+                     at<int32_t>(b, o_d),    at<uint32_t>(b, o_dr), at<double>(b, o_T)};
+  }
+  // instances: constant part
+  {
+    const size_t I = static_cast<size_t>(s->n_inst);
+    Layout L;
+    const size_t o_id = L.take<int32_t>(I), o_pool = L.take<int32_t>(I), o_cap = L.take<double>(I),
+                 o_k = L.take<double>(I), o_pf = L.take<double>(I), o_mb = L.take<int32_t>(I),
+                 o_pb = L.take<int32_t>(s->n_pools + 1);
+    alloc_blob(s->inst_const_blob, L.off);
+    auto& b = s->inst_const_blob;
+    s->in.id = at<int32_t>(b, o_id);
+    s->in.pool = at<int32_t>(b, o_pool);
+    s->in.cap = at<double>(b, o_cap);
+    s->in.decode_rate = at<double>(b, o_k);
+    s->in.prefill_rate = at<double>(b, o_pf);
+    s->in.max_batch = at<int32_t>(b, o_mb);
+    s->pool_begin = at<int32_t>(b, o_pb);
+    std::vector<int32_t> vid(I), vpool(I), vmb(I);
+    std::vector<double> vcap(I), vk(I), vpf(I);
+    for (size_t i = 0; i < I; ++i) {
+      vid[i] = s->inst_host[i].id;
+      vpool[i] = s->inst_host[i].pool;
+      vmb[i] = s->inst_host[i].max_batch;
+      vcap[i] = s->inst_host[i].capacity_tokens;
+      vk[i] = s->inst_host[i].decode_rate;
+      vpf[i] = s->inst_host[i].prefill_rate;
+    }
+    KX_CUDA(cudaMemcpy(s->in.id, vid.data(), I * 4, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->in.pool, vpool.data(), I * 4, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->in.max_batch, vmb.data(), I * 4, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->in.cap, vcap.data(), I * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->in.decode_rate, vk.data(), I * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->in.prefill_rate, vpf.data(), I * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(s->pool_begin, pool_begin.data(), (s->n_pools + 1) * 4,
+                       cudaMemcpyHostToDevice));
+  }
+  // instances: mutable part (one blob so checkpoint/restore is one copy)
+  {
+    const size_t I = static_cast<size_t>(s->n_inst);
+    const size_t R = static_cast<size_t>(ring);
+    Layout L;
+    const size_t o_live = L.take<double>(I), o_run = L.take<int32_t>(I),
+                 o_wait = L.take<int32_t>(I), o_susp = L.take<uint8_t>(I),
+                 o_base = L.take<int64_t>(I), o_hi = L.take<int64_t>(I),
+                 o_usage = L.take<double>(I * R), o_ex = L.take<uint32_t>(I * R / 32),
+                 o_na = L.take<int32_t>(I), o_au = L.take<uint64_t>(I * kActiveCap),
+                 o_ap = L.take<double>(I * kActiveCap), o_ak = L.take<double>(I * kActiveCap),
+                 o_at = L.take<double>(I * kActiveCap), o_aT = L.take<double>(I * kActiveCap),
+                 o_rr = L.take<int32_t>(s->n_pools);
+    alloc_blob(s->inst_mut_blob, L.off);
+    auto& b = s->inst_mut_blob;
+    s->in.live_kv = at<double>(b, o_live);
+    s->in.running = at<int32_t>(b, o_run);
+    s->in.waiting = at<int32_t>(b, o_wait);
+    s->in.suspended = at<uint8_t>(b, o_susp);
+    s->in.base_slot = at<int64_t>(b, o_base);
+    s->in.hi_slot = at<int64_t>(b, o_hi);
+    s->in.usage = at<double>(b, o_usage);
+    s->in.exists = at<uint32_t>(b, o_ex);
+    s->in.n_active = at<int32_t>(b, o_na);
+    s->in.act_uid = at<uint64_t>(b, o_au);
+    s->in.act_P = at<double>(b, o_ap);
+    s->in.act_k = at<double>(b, o_ak);
+    s->in.act_t0 = at<double>(b, o_at);
+    s->in.act_T = at<double>(b, o_aT);
+    s->in.rr_next = at<int32_t>(b, o_rr);
+    std::vector<int64_t> minus1(I, -1);  // hi_slot: nothing booked yet
+    KX_CUDA(cudaMemcpy(s->in.hi_slot, minus1.data(), I * 8, cudaMemcpyHostToDevice));
+  }
+  // order workspace + scratch
+  {
+    const size_t N = static_cast<size_t>(s->cap);
+    const size_t P = static_cast<size_t>(s->n_pools);
+    const size_t tie_cap = N / 2 + 1;
+    Layout L;
+    const size_t o_k0 = L.take<uint32_t>(N), o_k1 = L.take<uint32_t>(N),
+                 o_v0 = L.take<uint32_t>(N), o_v1 = L.take<uint32_t>(N);
+    const size_t lb_bytes = order_lookback_bytes(s->cap);
+    const size_t o_lb = L.take<char>(lb_bytes);
+    const size_t o_rng = L.take<PoolRange>(P), o_poff = L.take<int64_t>(P + 1);
+    // header block
+    Layout H;
+    const size_t h_hist = H.take<uint32_t>(4 * 256), h_tiles = H.take<uint32_t>(8),
+                 h_pc = H.take<uint32_t>(P), h_ns = H.take<uint32_t>(1), h_nb = H.take<uint32_t>(1),
+                 h_err = H.take<int>(1);
+    const size_t o_hdr = L.take<char>(H.off);
+    const size_t o_ss = L.take<uint32_t>(tie_cap), o_bs = L.take<uint32_t>(tie_cap),
+                 o_bl = L.take<uint32_t>(tie_cap);
+    const size_t o_errf = L.take<int>(1), o_sd = L.take<double>(4), o_si = L.take<int64_t>(4),
+                 o_ss2 = L.take<int>(4);
+    const int64_t nchunks = (s->cap + kCompactChunk - 1) / kCompactChunk;
+    const size_t o_cc = L.take<uint32_t>(nchunks + 1), o_ct = L.take<int64_t>(1);
+    alloc_blob(s->ws_blob, L.off);
+    auto& b = s->ws_blob;
+    s->ws.keys[0] = at<uint32_t>(b, o_k0);
+    s->ws.keys[1] = at<uint32_t>(b, o_k1);
+    s->ws.vals[0] = at<uint32_t>(b, o_v0);
+    s->ws.vals[1] = at<uint32_t>(b, o_v1);
+    s->ws.lookback = at<uint32_t>(b, o_lb);
+    s->ws.ranges = at<PoolRange>(b, o_rng);
+    s->ws.pool_offsets = at<int64_t>(b, o_poff);
+    s->ws.small_hdr = b.base + o_hdr;
+    s->ws.small_hdr_bytes = H.off;
+    char* hdr = b.base + o_hdr;
+    s->ws.hist = reinterpret_cast<uint32_t*>(hdr + h_hist);
+    s->ws.tile_counters = reinterpret_cast<uint32_t*>(hdr + h_tiles);
+    s->ws.pool_counts = reinterpret_cast<uint32_t*>(hdr + h_pc);
+    s->ws.n_small = reinterpret_cast<uint32_t*>(hdr + h_ns);
+    s->ws.n_big = reinterpret_cast<uint32_t*>(hdr + h_nb);
+    s->ws.error_flags = reinterpret_cast<int*>(hdr + h_err);
+    s->ws.small_starts = at<uint32_t>(b, o_ss);
+    s->ws.big_starts = at<uint32_t>(b, o_bs);
+    s->ws.big_lens = at<uint32_t>(b, o_bl);
+    s->ws.tie_cap = static_cast<uint32_t>(tie_cap);
+    s->err_flag = at<int>(b, o_errf);
+    s->scratch_d = at<double>(b, o_sd);
+    s->scratch_i = at<int64_t>(b, o_si);
+    s->scratch_s = at<int>(b, o_ss2);
+    s->compact_counts = at<uint32_t>(b, o_cc);
+    s->compact_total = at<int64_t>(b, o_ct);
+  }
+  // decision log
+  {
+    int64_t per_pool = cfg->log_capacity_per_pool;
+    if (per_pool <= 0) {
+      int64_t mb_sum_max = 0;
+      for (int p = 0; p < s->n_pools; ++p) {
+        int64_t mb = 0;
+        for (int i = pool_begin[p]; i < pool_begin[p + 1]; ++i) mb += s->inst_host[i].max_batch;
+        mb_sum_max = std::max(mb_sum_max, mb);
+      }
+      per_pool = std::max<int64_t>(4096, 2 * mb_sum_max + 16 * max_pp);
+    }
+    s->log_cap = per_pool;
+    const size_t P = static_cast<size_t>(s->n_pools);
+    Layout L;
+    const size_t o_rows = L.take<kx_decision>(P * per_pool),
+                 o_cand = L.take<double>(P * per_pool * max_pp), o_rc = L.take<int64_t>(P),
+                 o_ac = L.take<int64_t>(P), o_ps = L.take<int>(P);
+    alloc_blob(s->log_blob, L.off);
+    auto& b = s->log_blob;
+    s->rows = at<kx_decision>(b, o_rows);
+    s->cand = at<double>(b, o_cand);
+    s->row_count = at<int64_t>(b, o_rc);
+    s->admitted_count = at<int64_t>(b, o_ac);
+    s->pool_status = at<int>(b, o_ps);
+  }
+  KX_CUDA(cudaDeviceSynchronize());
+  *out = s.release();
+}
+
+void destroy_impl(kx_sched* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  free_blob(s->queue_blob);
+  free_blob(s->agent_blob);
+  free_blob(s->inst_const_blob);
+  free_blob(s->inst_mut_blob);
+  free_blob(s->inst_ckpt_blob);
+  free_blob(s->ws_blob);
+  free_blob(s->log_blob);
+  if (s->rem_table) cudaFree(s->rem_table);
+  if (s->rem_present) cudaFree(s->rem_present);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+cudaMemcpyKind kind_in(int32_t mem) {
+  return mem == KX_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+}
+cudaMemcpyKind kind_out(int32_t mem) {
+  return mem == KX_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+}
+
+void refresh_rem(kx_sched* s) {
+  if (s->n == 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>((s->n + 255) / 256, int64_t(s->sms) * 8));
+  k_fill_rem<<<grid, 256, 0, s->stream>>>(s->q, s->n, s->rem_table, s->rem_present, s->rem_base,
+                                          s->rem_n);
+  KX_CHECK_LAUNCH();
+}
+
+std::vector<uint32_t> dense_rank(const std::vector<double>& v) {
+  std::vector<double> d(v);
+  for (double x : d) require(x == x, "NaN in agent table");
+  std::sort(d.begin(), d.end());
+  d.erase(std::unique(d.begin(), d.end(), [](double a, double b) { return a == b; }), d.end());
+  std::vector<uint32_t> r(v.size());
+  for (size_t i = 0; i < v.size(); ++i)
+    r[i] = static_cast<uint32_t>(std::lower_bound(d.begin(), d.end(), v[i]) - d.begin());
+  return r;
+}
+
+OrderParams order_params(const kx_sched* s) {
+  OrderParams op{};
+  op.policy = s->sched_kind;
+  op.n_pools = s->n_pools;
+  op.n_agents = s->n_agents;
+  op.pool_bits = ceil_log2_u64(static_cast<uint64_t>(s->n_pools));
+  int classes = 1;
+  if (s->sched_kind == KX_SCHED_KAIROS) classes = s->n_pk_classes;
+  if (s->sched_kind == KX_SCHED_TOPO) classes = s->n_depth_classes;
+  op.class_bits = ceil_log2_u64(static_cast<uint64_t>(std::max(classes, 1)));
+  const int need_q = std::min(32, ceil_log2_u64(static_cast<uint64_t>(std::max<int64_t>(s->n, 2))) + 8);
+  int kb = op.pool_bits + op.class_bits + need_q;
+  kb = std::min(32, (kb + 7) / 8 * 8);
+  if (op.pool_bits + op.class_bits > 26)
+    fail(KX_ERR_CAPACITY, "pool x class key space exceeds 26 bits");
+  op.key_bits = kb;
+  op.q_bits = kb - op.pool_bits - op.class_bits;
+  return op;
+}
+
+void order_impl(kx_sched* s) {
+  require(s->n_agents > 0 || s->n == 0, "agent tables not set");
+  const OrderParams op = order_params(s);
+  s->order = launch_order(s->q, s->a, op, s->n, s->ws, s->sms, s->stream, &s->prof);
+  s->order_valid = true;
+  s->order_n = s->n;
+  s->dispatch_valid = false;
+}
+
+void dispatch_impl(kx_sched* s, double now) {
+  if (!s->order_valid || s->order_n != s->n)
+    throw std::logic_error("dispatch round needs a current queue order (call kx_order first)");
+  if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT)
+    fail(KX_ERR_INVALID, "only the time_slot dispatch policy runs on the device in this build");
+  require(s->n_agents > 0 || s->n == 0, "agent tables not set");
+  if (s->n > 0) KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
+  DispatchParams dp{};
+  dp.oracle_T = s->dcfg.oracle_expected_time;
+  dp.ring = s->ring;
+  dp.logging = 1;
+  dp.peak_stride = s->max_inst_per_pool;
+  dp.log_cap = s->log_cap;
+  dp.slot_len = s->dcfg.slot_len;
+  dp.watermark = s->dcfg.resume_watermark;
+  dp.now = now;
+  s->prof.begin("dispatch", 0.0, s->stream);
+  launch_dispatch(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp,
+                  s->n_pools, s->rows, s->cand, s->row_count, s->admitted_count, s->pool_status,
+                  s->stream);
+  s->prof.end(s->stream);
+  s->dispatch_valid = true;
+}
+
+int instance_index(const kx_sched* s, int32_t id) {
+  for (int i = 0; i < s->n_inst; ++i)
+    if (s->inst_host[i].id == id) return i;
+  throw std::invalid_argument("unknown instance id");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int kx_abi_version(void) { return KX_ABI_VERSION; }
+
+const char* kx_last_error(void) { return g_last_error.c_str(); }
+
+int kx_device_available(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceProp p{};
+  if (cudaGetDeviceProperties(&p, 0) != cudaSuccess) return 0;
+  return p.major >= 10 ? 1 : 0;
+}
+
+int kx_sched_create(const kx_sched_config* cfg, kx_sched** out) {
+  return guard([&] { create_impl(cfg, out); });
+}
+
+int kx_sched_destroy(kx_sched* s) {
+  return guard([&] { destroy_impl(s); });
+}
+
+int kx_sched_stream(kx_sched* s, void** cuda_stream) {
+  return guard([&] {
+    require(s && cuda_stream, "null argument");
+    *cuda_stream = s->stream;
+  });
+}
+
+int kx_sched_synchronize(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_set_scheduler(kx_sched* s, int32_t kind) {
+  return guard([&] {
+    require(s, "null handle");
+    require(kind >= 0 && kind <= 3, "unknown scheduler");
+    s->sched_kind = kind;
+    s->order_valid = false;
+  });
+}
+
+int kx_set_agent_tables(kx_sched* s, int32_t n_agents, const int32_t* agent_pool,
+                        const double* priority_key, const int32_t* topo_depth,
+                        const double* expected_T, uint64_t version) {
+  (void)version;
+  return guard([&] {
+    require(s, "null handle");
+    require(n_agents >= 1 && n_agents <= s->max_agents, "n_agents outside [1, max_agents]");
+    require(agent_pool != nullptr, "agent_pool is required");
+    KX_CUDA(cudaSetDevice(s->device));
+    for (int i = 0; i < n_agents; ++i)
+      require(agent_pool[i] >= 0 && agent_pool[i] < s->n_pools, "agent pool out of range");
+    const size_t A = static_cast<size_t>(n_agents);
+    KX_CUDA(cudaMemcpyAsync(s->a.pool, agent_pool, A * 4, cudaMemcpyHostToDevice, s->stream));
+    if (priority_key) {
+      const std::vector<double> pk(priority_key, priority_key + A);
+      const auto r = dense_rank(pk);
+      s->n_pk_classes = 1 + static_cast<int32_t>(*std::max_element(r.begin(), r.end()));
+      KX_CUDA(cudaMemcpyAsync(s->a.pk, priority_key, A * 8, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->a.pk_rank, r.data(), A * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));  // r is a temporary
+    } else if (s->n_agents != n_agents) {
+      s->n_pk_classes = 1;
+      KX_CUDA(cudaMemsetAsync(s->a.pk, 0, A * 8, s->stream));
+      KX_CUDA(cudaMemsetAsync(s->a.pk_rank, 0, A * 4, s->stream));
+    }
+    if (topo_depth) {
+      std::vector<double> d(A);
+      for (size_t i = 0; i < A; ++i) d[i] = static_cast<double>(topo_depth[i]);
+      const auto r = dense_rank(d);
+      s->n_depth_classes = 1 + static_cast<int32_t>(*std::max_element(r.begin(), r.end()));
+      KX_CUDA(cudaMemcpyAsync(s->a.depth, topo_depth, A * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->a.depth_rank, r.data(), A * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+    } else if (s->n_agents != n_agents) {
+      s->n_depth_classes = 1;
+      std::vector<int32_t> ones(A, 1);
+      std::vector<uint32_t> zeros(A, 0);
+      KX_CUDA(cudaMemcpyAsync(s->a.depth, ones.data(), A * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->a.depth_rank, zeros.data(), A * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    if (expected_T) {
+      KX_CUDA(cudaMemcpyAsync(s->a.T, expected_T, A * 8, cudaMemcpyHostToDevice, s->stream));
+    } else if (s->n_agents != n_agents) {
+      std::vector<double> dflt(A, s->dcfg.default_expected_time);
+      KX_CUDA(cudaMemcpyAsync(s->a.T, dflt.data(), A * 8, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    s->n_agents = n_agents;
+    s->order_valid = false;
+  });
+}
+
+int kx_set_remaining_table(kx_sched* s, uint64_t uid_base, int64_t n, const double* remaining,
+                           const uint8_t* present, int32_t mem) {
+  return guard([&] {
+    require(s, "null handle");
+    require(n >= 0, "negative table size");
+    require(n == 0 || (remaining && present), "null table");
+    KX_CUDA(cudaSetDevice(s->device));
+    if (s->rem_table) cudaFree(s->rem_table);
+    if (s->rem_present) cudaFree(s->rem_present);
+    s->rem_table = nullptr;
+    s->rem_present = nullptr;
+    s->rem_n = n;
+    s->rem_base = uid_base;
+    if (n > 0) {
+      KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->rem_table), size_t(n) * 8));
+      KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->rem_present), size_t(n)));
+      KX_CUDA(cudaMemcpyAsync(s->rem_table, remaining, size_t(n) * 8, kind_in(mem), s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->rem_present, present, size_t(n), kind_in(mem), s->stream));
+    }
+    refresh_rem(s);
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    s->order_valid = false;
+  });
+}
+
+int kx_queue_upload(kx_sched* s, int64_t n, const kx_queue_view* v, int32_t mem) {
+  return guard([&] {
+    require(s && v, "null argument");
+    require(n >= 0 && n <= s->cap, "queue size exceeds queue_capacity");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t N = static_cast<size_t>(n);
+    if (n > 0) {
+      require(v->agent && v->prompt_tokens && v->app_start && v->queue_enter && v->msg_key && v->uid,
+              "queue view is missing a required array");
+      if (s->dcfg.oracle_expected_time)
+        require(v->pure_exec != nullptr, "oracle_expected_time needs pure_exec");
+      const cudaMemcpyKind k = kind_in(mem);
+      KX_CUDA(cudaMemcpyAsync(s->q.agent, v->agent, N * 4, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.prompt, v->prompt_tokens, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.app_start, v->app_start, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.queue_enter, v->queue_enter, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.msg, v->msg_key, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.uid, v->uid, N * 8, k, s->stream));
+      if (v->kept_tokens)
+        KX_CUDA(cudaMemcpyAsync(s->q.kept, v->kept_tokens, N * 8, k, s->stream));
+      else
+        KX_CUDA(cudaMemsetAsync(s->q.kept, 0, N * 8, s->stream));
+      if (v->pure_exec) KX_CUDA(cudaMemcpyAsync(s->q.pure_exec, v->pure_exec, N * 8, k, s->stream));
+      KX_CUDA(cudaMemsetAsync(s->err_flag, 0, sizeof(int), s->stream));
+      const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(s->sms) * 8));
+      k_validate_queue<<<grid, 256, 0, s->stream>>>(s->q, n, std::max(s->n_agents, 0),
+                                                    s->dcfg.oracle_expected_time ? 1 : 0,
+                                                    s->err_flag);
+      KX_CHECK_LAUNCH();
+    }
+    s->n = n;
+    refresh_rem(s);
+    s->order_valid = false;
+    s->dispatch_valid = false;
+    if (n > 0) check_err_flag(s, "kx_queue_upload");
+  });
+}
+
+int kx_queue_size(kx_sched* s, int64_t* n) {
+  return guard([&] {
+    require(s && n, "null argument");
+    *n = s->n;
+  });
+}
+
+int kx_queue_remove_admitted(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->dispatch_valid) throw std::logic_error("no dispatch round to apply");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int64_t n = s->n;
+    if (n == 0) return;
+    const int64_t chunks = (n + kCompactChunk - 1) / kCompactChunk;
+    k_flag_count<<<static_cast<unsigned>(chunks), 256, 0, s->stream>>>(
+        s->q.admitted, n, static_cast<int>(kCompactChunk), s->compact_counts);
+    KX_CHECK_LAUNCH();
+    k_scan_counts<<<1, 32, 0, s->stream>>>(s->compact_counts, chunks, s->compact_total);
+    KX_CHECK_LAUNCH();
+    // Compact each column through the (now unused) sort buffers.
+    auto compact = [&](auto* col) {
+      using T = std::remove_pointer_t<decltype(col)>;
+      T* tmp = reinterpret_cast<T*>(s->ws.keys[0]);  // keys[0..1]+vals[0..1] = 16 B/elem
+      k_compact<T><<<static_cast<unsigned>(chunks), 32, 0, s->stream>>>(
+          col, tmp, s->q.admitted, n, static_cast<int>(kCompactChunk), s->compact_counts);
+      KX_CHECK_LAUNCH();
+      KX_CUDA(cudaMemcpyAsync(col, tmp, size_t(n) * sizeof(T), cudaMemcpyDeviceToDevice, s->stream));
+    };
+    compact(s->q.agent);
+    compact(s->q.prompt);
+    compact(s->q.app_start);
+    compact(s->q.queue_enter);
+    compact(s->q.msg);
+    compact(s->q.uid);
+    compact(s->q.kept);
+    compact(s->q.pure_exec);
+    compact(s->q.rem);
+    int64_t total = 0;
+    KX_CUDA(cudaMemcpyAsync(&total, s->compact_total, 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    s->n = total;
+    s->order_valid = false;
+    s->dispatch_valid = false;
+  });
+}
+
+int kx_score(kx_sched* s, double* k0, double* k1, double* k2, int32_t mem) {
+  return guard([&] {
+    require(s && k0 && k1 && k2, "null argument");
+    require(s->n_agents > 0 || s->n == 0, "agent tables not set");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t N = static_cast<size_t>(s->n);
+    if (N == 0) return;
+    if (mem == KX_MEM_DEVICE) {
+      launch_score(s->q, s->a, s->sched_kind, s->n, k0, k1, k2, s->sms, s->stream);
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+      return;
+    }
+    double* d = nullptr;
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), N * 24, s->stream));
+    launch_score(s->q, s->a, s->sched_kind, s->n, d, d + N, d + 2 * N, s->sms, s->stream);
+    KX_CUDA(cudaMemcpyAsync(k0, d, N * 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(k1, d + N, N * 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(k2, d + 2 * N, N * 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaFreeAsync(d, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_order(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    order_impl(s);
+  });
+}
+
+int kx_order_fetch(kx_sched* s, uint32_t* perm, int64_t* pool_offsets, int32_t mem) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->order_valid) throw std::logic_error("no current order (call kx_order)");
+    KX_CUDA(cudaSetDevice(s->device));
+    const cudaMemcpyKind k = kind_out(mem);
+    if (perm && s->n > 0)
+      KX_CUDA(cudaMemcpyAsync(perm, s->order.perm, size_t(s->n) * 4, k, s->stream));
+    if (pool_offsets)
+      KX_CUDA(cudaMemcpyAsync(pool_offsets, s->ws.pool_offsets, size_t(s->n_pools + 1) * 8, k,
+                              s->stream));
+    int flags = 0;
+    KX_CUDA(cudaMemcpyAsync(&flags, s->ws.error_flags, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (flags) fail(KX_ERR_INVALID, "queue holds an invalid agent index or NaN key");
+  });
+}
+
+int kx_dispatch_round(kx_sched* s, double now) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    dispatch_impl(s, now);
+  });
+}
+
+int kx_tick(kx_sched* s, double now) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    order_impl(s);
+    dispatch_impl(s, now);
+  });
+}
+
+int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
+                      double* candidate_peaks, int64_t* row_stride, int64_t* peak_stride) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->dispatch_valid) throw std::logic_error("no dispatch round to fetch");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t P = static_cast<size_t>(s->n_pools);
+    std::vector<int64_t> cnt(P);
+    std::vector<int> status(P);
+    KX_CUDA(cudaMemcpyAsync(cnt.data(), s->row_count, P * 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(status.data(), s->pool_status, P * 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (row_stride) *row_stride = s->log_cap;
+    if (peak_stride) *peak_stride = s->max_inst_per_pool;
+    for (size_t p = 0; p < P; ++p) {
+      if (status[p] == KX_ERR_LIVELOCK)
+        fail(KX_ERR_LIVELOCK, "pool " + std::to_string(p) +
+                                  ": overload/resume livelock (reference would spin forever)");
+      if (status[p] == KX_ERR_CAPACITY)
+        fail(KX_ERR_CAPACITY, "pool " + std::to_string(p) +
+                                  ": slot ring or active-request table capacity exceeded");
+      if (status[p] != KX_OK) fail(status[p], "pool " + std::to_string(p) + ": dispatch failed");
+      if (cnt[p] > s->log_cap && (rows || candidate_peaks))
+        fail(KX_ERR_CAPACITY, "decision log truncated (raise log_capacity_per_pool)");
+    }
+    if (per_pool_count) std::memcpy(per_pool_count, cnt.data(), P * 8);
+    if (rows)
+      KX_CUDA(cudaMemcpyAsync(rows, s->rows, P * s->log_cap * sizeof(kx_decision),
+                              cudaMemcpyDeviceToHost, s->stream));
+    if (candidate_peaks)
+      KX_CUDA(cudaMemcpyAsync(candidate_peaks, s->cand,
+                              P * s->log_cap * s->max_inst_per_pool * sizeof(double),
+                              cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_instances_set_live(kx_sched* s, const double* live_kv, const int32_t* running,
+                          const int32_t* waiting) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t I = static_cast<size_t>(s->n_inst);
+    if (live_kv) KX_CUDA(cudaMemcpyAsync(s->in.live_kv, live_kv, I * 8, cudaMemcpyHostToDevice, s->stream));
+    if (running) KX_CUDA(cudaMemcpyAsync(s->in.running, running, I * 4, cudaMemcpyHostToDevice, s->stream));
+    if (waiting) KX_CUDA(cudaMemcpyAsync(s->in.waiting, waiting, I * 4, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_instances_get_live(kx_sched* s, double* live_kv, int32_t* running, int32_t* waiting,
+                          uint8_t* suspended) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t I = static_cast<size_t>(s->n_inst);
+    if (live_kv) KX_CUDA(cudaMemcpyAsync(live_kv, s->in.live_kv, I * 8, cudaMemcpyDeviceToHost, s->stream));
+    if (running) KX_CUDA(cudaMemcpyAsync(running, s->in.running, I * 4, cudaMemcpyDeviceToHost, s->stream));
+    if (waiting) KX_CUDA(cudaMemcpyAsync(waiting, s->in.waiting, I * 4, cudaMemcpyDeviceToHost, s->stream));
+    if (suspended) KX_CUDA(cudaMemcpyAsync(suspended, s->in.suspended, I, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_ledger_try_place(kx_sched* s, int32_t instance_id, double prefill_tokens, double decode_rate,
+                        double t_start, double expected_duration, int32_t* fits,
+                        double* predicted_peak, int64_t* violating_slot) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    launch_ledger_try_place(s->in, i, s->ring, prefill_tokens, decode_rate, t_start,
+                            expected_duration, s->dcfg.slot_len, s->scratch_d, s->scratch_i,
+                            s->scratch_s, s->stream);
+    double pk = 0;
+    int64_t viol = 0;
+    int state = 0;
+    KX_CUDA(cudaMemcpyAsync(&pk, s->scratch_d, 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(&viol, s->scratch_i, 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(&state, s->scratch_s, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (state < 0) fail(KX_ERR_CAPACITY, "request span leaves the ledger's slot ring");
+    if (fits) *fits = state == 2 ? 1 : 0;
+    if (predicted_peak) *predicted_peak = state == 2 ? pk : 0.0;
+    if (violating_slot) *violating_slot = state == 2 ? 0 : viol;
+  });
+}
+
+int kx_ledger_commit(kx_sched* s, int32_t instance_id, uint64_t uid, double prefill_tokens,
+                     double decode_rate, double t_start, double expected_duration) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    launch_ledger_commit(s->in, i, s->ring, uid, prefill_tokens, decode_rate, t_start,
+                         expected_duration, s->dcfg.slot_len, s->scratch_s, s->stream);
+    int st = 0;
+    KX_CUDA(cudaMemcpyAsync(&st, s->scratch_s, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (st == KX_ERR_LOGIC) throw std::logic_error("commit after Exceeds is a contract violation");
+    if (st == KX_ERR_CAPACITY) fail(KX_ERR_CAPACITY, "ledger slot ring / active table capacity exceeded");
+  });
+}
+
+int kx_ledger_commit_batch(kx_sched* s, int64_t n, const int32_t* instance_id, const uint64_t* uid,
+                           const double* prefill_tokens, const double* decode_rate,
+                           const double* t_start, const double* expected_duration,
+                           uint8_t* fits_out) {
+  return guard([&] {
+    require(s, "null handle");
+    require(n >= 0, "negative count");
+    if (n == 0) return;
+    require(instance_id && uid && prefill_tokens && decode_rate && t_start && expected_duration,
+            "null argument");
+    KX_CUDA(cudaSetDevice(s->device));
+    std::vector<int64_t> cnt(static_cast<size_t>(s->n_inst) + 1, 0);
+    std::vector<int> idx(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) {
+      idx[static_cast<size_t>(j)] = instance_index(s, instance_id[j]);
+      cnt[static_cast<size_t>(idx[static_cast<size_t>(j)]) + 1] += 1;
+    }
+    for (int i = 0; i < s->n_inst; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int64_t> order(static_cast<size_t>(n));
+    std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
+    for (int64_t j = 0; j < n; ++j) order[static_cast<size_t>(cur[idx[static_cast<size_t>(j)]]++)] = j;
+    const size_t N = static_cast<size_t>(n);
+    char* buf = nullptr;
+    const size_t bytes = (s->n_inst + 1) * 8 + N * (8 + 8 + 8 * 4 + 1) + 64;
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s->stream));
+    auto* d_off = reinterpret_cast<int64_t*>(buf);
+    auto* d_ord = d_off + s->n_inst + 1;
+    auto* d_uid = reinterpret_cast<uint64_t*>(d_ord + N);
+    auto* d_P = reinterpret_cast<double*>(d_uid + N);
+    auto* d_k = d_P + N;
+    auto* d_t0 = d_k + N;
+    auto* d_T = d_t0 + N;
+    auto* d_fit = reinterpret_cast<uint8_t*>(d_T + N);
+    KX_CUDA(cudaMemcpyAsync(d_off, cnt.data(), (s->n_inst + 1) * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_ord, order.data(), N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_uid, uid, N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_P, prefill_tokens, N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_k, decode_rate, N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_t0, t_start, N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(d_T, expected_duration, N * 8, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemsetAsync(s->scratch_s, 0, 4, s->stream));
+    launch_ledger_commit_batch(s->in, s->n_inst, s->ring, d_off, d_ord, d_uid, d_P, d_k, d_t0, d_T,
+                               s->dcfg.slot_len, d_fit, s->scratch_s, s->stream);
+    std::vector<uint8_t> fits(N);
+    int st = 0;
+    KX_CUDA(cudaMemcpyAsync(fits.data(), d_fit, N, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(&st, s->scratch_s, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaFreeAsync(buf, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (st == KX_ERR_CAPACITY) fail(KX_ERR_CAPACITY, "ledger slot ring / active table capacity exceeded");
+    if (fits_out) std::memcpy(fits_out, fits.data(), N);
+  });
+}
+
+int kx_on_request_finished(kx_sched* s, int32_t instance_id, uint64_t uid, double actual_end) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT) return;
+    launch_ledger_finish(s->in, i, s->ring, uid, actual_end, s->dcfg.slot_len, s->stream);
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_on_overload(kx_sched* s, int32_t instance_id) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT) return;
+    launch_on_overload(s->in, i, s->stream);
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_on_live_usage(kx_sched* s, int32_t instance_id, double live_kv) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    launch_on_live_usage(s->in, i, live_kv, s->dcfg.resume_watermark, s->stream);
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_gc(kx_sched* s, double now) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    launch_gc_all(s->in, s->n_inst, s->ring, now, s->dcfg.slot_len, s->stream);
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_ledger_read(kx_sched* s, int32_t instance_id, int64_t* base_slot, double* usage,
+                   uint8_t* exists, int32_t* active_requests) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const int i = instance_index(s, instance_id);
+    const int R = s->ring;
+    int64_t base = 0;
+    std::vector<double> ring_usage(R);
+    std::vector<uint32_t> ring_ex(R / 32);
+    int32_t na = 0;
+    KX_CUDA(cudaMemcpyAsync(&base, s->in.base_slot + i, 8, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(ring_usage.data(), s->in.usage + int64_t(i) * R, R * 8,
+                            cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(ring_ex.data(), s->in.exists + int64_t(i) * (R / 32), R / 8,
+                            cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaMemcpyAsync(&na, s->in.n_active + i, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (base_slot) *base_slot = base;
+    for (int k = 0; k < R; ++k) {
+      const int64_t slot = base + k;
+      const uint32_t pos = static_cast<uint32_t>(slot) & (R - 1);
+      if (usage) usage[k] = ring_usage[pos];
+      if (exists) exists[k] = (ring_ex[pos >> 5] >> (pos & 31)) & 1u;
+    }
+    if (active_requests) *active_requests = na;
+  });
+}
+
+int kx_state_checkpoint(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    if (!s->inst_ckpt_blob.base) alloc_blob(s->inst_ckpt_blob, s->inst_mut_blob.size);
+    KX_CUDA(cudaMemcpyAsync(s->inst_ckpt_blob.base, s->inst_mut_blob.base, s->inst_mut_blob.size,
+                            cudaMemcpyDeviceToDevice, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    s->have_ckpt = true;
+  });
+}
+
+int kx_state_restore(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->have_ckpt) throw std::logic_error("no checkpoint to restore");
+    KX_CUDA(cudaSetDevice(s->device));
+    KX_CUDA(cudaMemcpyAsync(s->inst_mut_blob.base, s->inst_ckpt_blob.base, s->inst_mut_blob.size,
+                            cudaMemcpyDeviceToDevice, s->stream));
+  });
+}
+
+int kx_profile_enable(kx_sched* s, int32_t enable) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    s->prof.reset();
+    s->prof.enabled = enable != 0;
+  });
+}
+
+int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    require(s && n_out, "null argument");
+    KX_CUDA(cudaSetDevice(s->device));
+    s->prof.drain();
+    const int32_t n = static_cast<int32_t>(s->prof.phases.size());
+    *n_out = n;
+    for (int32_t i = 0; i < n && i < cap && out; ++i) {
+      const auto& p = s->prof.phases[static_cast<size_t>(i)];
+      std::memset(out[i].name, 0, sizeof(out[i].name));
+      std::strncpy(out[i].name, p.name.c_str(), sizeof(out[i].name) - 1);
+      out[i].total_ms = p.ms;
+      out[i].launches = p.launches;
+      out[i].alg_bytes = p.bytes;
+    }
+  });
+}
+
+int64_t kx_launch_count(void) { return kx::g_kx_launches.load(); }
+
+int kx_orchestrator_dp(int64_t n_workflows, const int64_t* wf_offsets, const int32_t* parent,
+                       const int64_t* prompt_tokens, const int64_t* target_tokens,
+                       double prefill_rate, double decode_rate, uint64_t uid_base,
+                       uint64_t* uid_out, double* pure_exec_out, double* remaining_out,
+                       int32_t mem) {
+  return guard([&] {
+    require(n_workflows >= 0, "negative workflow count");
+    require(prefill_rate > 0.0 && decode_rate > 0.0, "rates must be positive");
+    if (n_workflows == 0) return;
+    require(wf_offsets && parent && prompt_tokens && target_tokens && uid_out && pure_exec_out &&
+                remaining_out,
+            "null argument");
+    ensure_device(0);
+    int dev = 0;
+    KX_CUDA(cudaGetDevice(&dev));
+    const int sms = sm_count(dev);
+    cudaStream_t st = nullptr;
+    KX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    int64_t n_calls = 0;
+    const int64_t* off_d = wf_offsets;
+    const int32_t* par_d = parent;
+    const int64_t* pr_d = prompt_tokens;
+    const int64_t* tg_d = target_tokens;
+    uint64_t* uid_d = uid_out;
+    double* pure_d = pure_exec_out;
+    double* rem_d = remaining_out;
+    int* err_d = nullptr;
+    std::vector<void*> owned;
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      KX_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), st));
+      owned.push_back(p);
+      return p;
+    };
+    struct FreeGuard {
+      std::vector<void*>* v;
+      cudaStream_t s;
+      ~FreeGuard() {
+        for (void* p : *v) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+      }
+    } fg{&owned, st};
+    if (mem == KX_MEM_HOST) {
+      n_calls = wf_offsets[n_workflows];
+      require(wf_offsets[0] == 0 && n_calls >= 0, "wf_offsets must start at 0");
+      for (int64_t w = 0; w < n_workflows; ++w)
+        require(wf_offsets[w + 1] >= wf_offsets[w], "wf_offsets must be non-decreasing");
+      const size_t C = static_cast<size_t>(n_calls);
+      auto* o = static_cast<int64_t*>(dalloc((n_workflows + 1) * 8));
+      auto* pa = static_cast<int32_t*>(dalloc(C * 4));
+      auto* pr = static_cast<int64_t*>(dalloc(C * 8));
+      auto* tg = static_cast<int64_t*>(dalloc(C * 8));
+      uid_d = static_cast<uint64_t*>(dalloc(C * 8));
+      pure_d = static_cast<double*>(dalloc(C * 8));
+      rem_d = static_cast<double*>(dalloc(C * 8));
+      KX_CUDA(cudaMemcpyAsync(o, wf_offsets, (n_workflows + 1) * 8, cudaMemcpyHostToDevice, st));
+      KX_CUDA(cudaMemcpyAsync(pa, parent, C * 4, cudaMemcpyHostToDevice, st));
+      KX_CUDA(cudaMemcpyAsync(pr, prompt_tokens, C * 8, cudaMemcpyHostToDevice, st));
+      KX_CUDA(cudaMemcpyAsync(tg, target_tokens, C * 8, cudaMemcpyHostToDevice, st));
+      off_d = o;
+      par_d = pa;
+      pr_d = pr;
+      tg_d = tg;
+    } else {
+      KX_CUDA(cudaMemcpyAsync(&n_calls, wf_offsets + n_workflows, 8, cudaMemcpyDeviceToHost, st));
+      KX_CUDA(cudaStreamSynchronize(st));
+    }
+    err_d = static_cast<int*>(dalloc(4));
+    KX_CUDA(cudaMemsetAsync(err_d, 0, 4, st));
+    launch_orchestrator_dp(n_workflows, off_d, par_d, pr_d, tg_d, prefill_rate, decode_rate,
+                           uid_base, uid_d, pure_d, rem_d, err_d, sms, st);
+    int err = 0;
+    KX_CUDA(cudaMemcpyAsync(&err, err_d, 4, cudaMemcpyDeviceToHost, st));
+    if (mem == KX_MEM_HOST && n_calls > 0) {
+      const size_t C = static_cast<size_t>(n_calls);
+      KX_CUDA(cudaMemcpyAsync(uid_out, uid_d, C * 8, cudaMemcpyDeviceToHost, st));
+      KX_CUDA(cudaMemcpyAsync(pure_exec_out, pure_d, C * 8, cudaMemcpyDeviceToHost, st));
+      KX_CUDA(cudaMemcpyAsync(remaining_out, rem_d, C * 8, cudaMemcpyDeviceToHost, st));
+    }
+    KX_CUDA(cudaStreamSynchronize(st));
+    if (err) fail(KX_ERR_INVALID, "parent link is not parents-first (parent >= node id)");
+  });
+}
+
+int kx_record_remaining(int64_t n_workflows, const int64_t* rec_offsets, const double* exec_start,
+                        const double* exec_end, double* finish_out, double* samples_out,
+                        int32_t mem) {
+  return guard([&] {
+    require(n_workflows >= 0, "negative workflow count");
+    if (n_workflows == 0) return;
+    require(rec_offsets && exec_start && exec_end && finish_out && samples_out, "null argument");
+    ensure_device(0);
+    int dev = 0;
+    KX_CUDA(cudaGetDevice(&dev));
+    const int sms = sm_count(dev);
+    cudaStream_t st = nullptr;
+    KX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    if (mem == KX_MEM_DEVICE) {
+      launch_record_remaining(n_workflows, rec_offsets, exec_start, exec_end, finish_out,
+                              samples_out, sms, st);
+      KX_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    const int64_t n_rec = rec_offsets[n_workflows];
+    require(rec_offsets[0] == 0 && n_rec >= 0, "rec_offsets must start at 0");
+    const size_t R = static_cast<size_t>(n_rec), W = static_cast<size_t>(n_workflows);
+    char* buf = nullptr;
+    const size_t bytes = (W + 1) * 8 + R * 8 * 3 + W * 8 + 64;
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, st));
+    auto* o = reinterpret_cast<int64_t*>(buf);
+    auto* es = reinterpret_cast<double*>(buf + (W + 1) * 8);
+    auto* ee = es + R;
+    auto* sm = ee + R;
+    auto* fin = sm + R;
+    KX_CUDA(cudaMemcpyAsync(o, rec_offsets, (W + 1) * 8, cudaMemcpyHostToDevice, st));
+    KX_CUDA(cudaMemcpyAsync(es, exec_start, R * 8, cudaMemcpyHostToDevice, st));
+    KX_CUDA(cudaMemcpyAsync(ee, exec_end, R * 8, cudaMemcpyHostToDevice, st));
+    launch_record_remaining(n_workflows, o, es, ee, fin, sm, sms, st);
+    KX_CUDA(cudaMemcpyAsync(samples_out, sm, R * 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaMemcpyAsync(finish_out, fin, W * 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaFreeAsync(buf, st));
+    KX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Host-side interface of the dispatch kernels (kx_dispatch.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kx_state.cuh"
+
+namespace kx {
+
+constexpr int kMaxInstPerPool = 512;
+
+struct DispatchParams {
+  int32_t oracle_T;
+  int32_t ring;
+  int32_t logging;
+  int32_t peak_stride;
+  int64_t log_cap;
+  double slot_len;
+  double watermark;
+  double now;
+};
+
+void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
+                     const int32_t* pool_begin, const uint32_t* perm, const int64_t* pool_offsets,
+                     const DispatchParams& dp, int n_pools, kx_decision* rows, double* cand,
+                     int64_t* row_count, int64_t* admitted_count, int* pool_status,
+                     cudaStream_t st);
+void launch_ledger_try_place(const InstDev& in, int i, int ring, double P, double k, double t0,
+                             double T, double slot_len, double* out_peak, int64_t* out_viol,
+                             int* out_state, cudaStream_t st);
+void launch_ledger_commit(const InstDev& in, int i, int ring, uint64_t uid, double P, double k,
+                          double t0, double T, double slot_len, int* status, cudaStream_t st);
+void launch_ledger_commit_batch(const InstDev& in, int n_inst, int ring, const int64_t* off,
+                                const int64_t* order, const uint64_t* uid, const double* P,
+                                const double* k, const double* t0, const double* T, double slot_len,
+                                uint8_t* fits, int* status, cudaStream_t st);
+void launch_ledger_finish(const InstDev& in, int i, int ring, uint64_t uid, double actual_end,
+                          double slot_len, cudaStream_t st);
+void launch_on_overload(const InstDev& in, int i, cudaStream_t st);
+void launch_on_live_usage(const InstDev& in, int i, double live_kv, double watermark,
+                          cudaStream_t st);
+void launch_gc_all(const InstDev& in, int n_inst, int ring, double now, double slot_len,
+                   cudaStream_t st);
+
+}  // namespace kx

@@ -1,0 +1,502 @@
+// K2 (score), K3 (compact-key LSD radix sort) and K4 (exact tie-fix): the
+// full ReadyQueue order of every pool in one pass over HBM.
+//
+// Reference semantics: the queue is ordered by
+//   (order_key(r), app_start, queue_enter, msg_id, uid)      priority.hpp:97-98
+// with order_key per policy (scheduler.hpp:48-113). We sort by a 32-bit
+// compact key
+//   [ pool | class rank | q(primary time) ]
+// where `class` is the dense rank of the discrete primary component
+// (Kairos priority key, Topo depth; none for FCFS/Oracle) and q is a
+// monotone non-decreasing quantisation of the primary double over the
+// pool's [min, max] range. The compact key therefore never orders two
+// requests against the reference order; requests it cannot separate are
+// adjacent after the sort and are re-sorted by the exact tuple
+// (ordered-bits of the doubles, msg key, uid, queue index) in K4.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "kx_common.cuh"
+#include "kx_order.cuh"
+#include "kx_sort.cuh"
+#include "kx_state.cuh"
+
+namespace kx {
+
+__global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= passes) return;
+  uint32_t* h = hist + warp * kRadix;
+  uint32_t carry = 0;
+  for (int c = 0; c < kRadix; c += 32) {
+    const uint32_t v = h[c + lane];
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    h[c + lane] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+namespace {
+
+__device__ __forceinline__ double primary_time(const QueueDev& q, int policy, int64_t i) {
+  switch (policy) {
+    case KX_SCHED_KAIROS: return q.app_start[i];
+    case KX_SCHED_ORACLE: return q.rem[i];
+    default: return q.queue_enter[i];  // FCFS, Topo
+  }
+}
+
+__device__ __forceinline__ uint32_t class_of(const AgentsDev& a, int policy, int32_t agent) {
+  if (policy == KX_SCHED_KAIROS) return a.pk_rank[agent];
+  if (policy == KX_SCHED_TOPO) return a.depth_rank[agent];
+  return 0;
+}
+
+// Exact comparison record: ordered bits of the tuple after the class.
+struct TRec {
+  uint64_t w0, w1, w2, msg, uid;
+  uint32_t idx;
+};
+
+__device__ __forceinline__ TRec load_rec(const QueueDev& q, int policy, uint32_t idx) {
+  TRec r;
+  const double app = q.app_start[idx];
+  const double qe = q.queue_enter[idx];
+  switch (policy) {
+    case KX_SCHED_KAIROS:  // (pk, app, qe) then app, qe, msg, uid
+      r.w0 = ordered_bits(app);
+      r.w1 = ordered_bits(qe);
+      r.w2 = 0;
+      break;
+    case KX_SCHED_ORACLE:  // (rem, qe, 0) then app, qe, msg, uid
+      r.w0 = ordered_bits(q.rem[idx]);
+      r.w1 = ordered_bits(qe);
+      r.w2 = ordered_bits(app);
+      break;
+    default:  // FCFS (qe, app, 0) / Topo (depth, qe, 0): then app, qe, msg, uid
+      r.w0 = ordered_bits(qe);
+      r.w1 = ordered_bits(app);
+      r.w2 = 0;
+      break;
+  }
+  r.msg = q.msg[idx];
+  r.uid = q.uid[idx];
+  r.idx = idx;
+  return r;
+}
+
+__device__ __forceinline__ bool rec_less(const TRec& a, const TRec& b) {
+  if (a.w0 != b.w0) return a.w0 < b.w0;
+  if (a.w1 != b.w1) return a.w1 < b.w1;
+  if (a.w2 != b.w2) return a.w2 < b.w2;
+  if (a.msg != b.msg) return a.msg < b.msg;
+  if (a.uid != b.uid) return a.uid < b.uid;
+  return a.idx < b.idx;  // identical tuples: first-enqueued wins (best_index uses strict <)
+}
+
+__device__ __forceinline__ TRec shfl_rec(const TRec& r, int src) {
+  TRec o;
+  o.w0 = __shfl_sync(0xffffffffu, r.w0, src);
+  o.w1 = __shfl_sync(0xffffffffu, r.w1, src);
+  o.w2 = __shfl_sync(0xffffffffu, r.w2, src);
+  o.msg = __shfl_sync(0xffffffffu, r.msg, src);
+  o.uid = __shfl_sync(0xffffffffu, r.uid, src);
+  o.idx = __shfl_sync(0xffffffffu, r.idx, src);
+  return o;
+}
+
+}  // namespace
+
+// ---- K2: per-request OrderKey -------------------------------------------
+__global__ void k_score(QueueDev q, AgentsDev a, int policy, int64_t n, double* __restrict__ k0,
+                        double* __restrict__ k1, double* __restrict__ k2) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t ag = q.agent[i];
+    double x0, x1, x2 = 0.0;
+    switch (policy) {
+      case KX_SCHED_KAIROS: x0 = a.pk[ag]; x1 = q.app_start[i]; x2 = q.queue_enter[i]; break;
+      case KX_SCHED_FCFS: x0 = q.queue_enter[i]; x1 = q.app_start[i]; break;
+      case KX_SCHED_TOPO: x0 = static_cast<double>(a.depth[ag]); x1 = q.queue_enter[i]; break;
+      default: x0 = q.rem[i]; x1 = q.queue_enter[i]; break;
+    }
+    k0[i] = x0;
+    k1[i] = x1;
+    k2[i] = x2;
+  }
+}
+
+// ---- per-pool range of the primary time ------------------------------
+// Also validates agent indices and rejects NaN (error_flags bit 0 / bit 1).
+__global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
+                             PoolRange* __restrict__ ranges, int* __restrict__ error_flags) {
+  extern __shared__ uint64_t s_rng[];  // [2 * n_pools]: lo, hi
+  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
+    s_rng[2 * p] = ~0ull;
+    s_rng[2 * p + 1] = 0ull;
+  }
+  __syncthreads();
+  int err = 0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int32_t ag = q.agent[i];
+    if (ag < 0 || ag >= op.n_agents) {
+      err |= 1;
+      continue;
+    }
+    const double t = primary_time(q, op.policy, i);
+    if (t != t) {
+      err |= 2;
+      continue;
+    }
+    const int32_t p = a.pool[ag];
+    const uint64_t b = ordered_bits(t);
+    atomicMin(reinterpret_cast<unsigned long long*>(&s_rng[2 * p]), (unsigned long long)b);
+    atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * p + 1]), (unsigned long long)b);
+  }
+  if (err) atomicOr(error_flags, err);
+  __syncthreads();
+  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
+    if (s_rng[2 * p] != ~0ull)
+      atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p].lo_bits), (unsigned long long)s_rng[2 * p]);
+    if (s_rng[2 * p + 1] != 0ull)
+      atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p].hi_bits), (unsigned long long)s_rng[2 * p + 1]);
+  }
+}
+
+__global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pools) return;
+  PoolRange r = ranges[p];
+  if (r.lo_bits > r.hi_bits) {  // empty pool
+    r.lo = 0.0;
+    r.scale = 0.0;
+  } else {
+    const double lo = from_ordered_bits(r.lo_bits);
+    const double hi = from_ordered_bits(r.hi_bits);
+    const double span = __dsub_rn(hi, lo);
+    const double qmax = static_cast<double>((uint64_t(1) << q_bits) - 1);
+    r.lo = lo;
+    // Degenerate or non-finite range: every request shares q = 0 and the
+    // exact tie-fix orders them.
+    r.scale = (span > 0.0 && span < 1.0e300 && isfinite(lo)) ? __ddiv_rn(qmax, span) : 0.0;
+  }
+  ranges[p] = r;
+}
+
+// ---- compact key + upfront digit histograms + pool counts -------------
+__global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
+                         const PoolRange* __restrict__ ranges, uint32_t* __restrict__ keys,
+                         uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts) {
+  __shared__ uint32_t sh[4 * kRadix];
+  extern __shared__ uint32_t s_pool[];
+  const int passes = op.key_bits / kRadixBits;
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) sh[i] = 0;
+  for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) s_pool[i] = 0;
+  __syncthreads();
+  const uint32_t qmax = (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    uint32_t key = 0;
+    if (valid) {
+      const int32_t ag = q.agent[i];
+      const int32_t p = a.pool[ag];
+      const uint32_t cls = class_of(a, op.policy, ag);
+      const double t = primary_time(q, op.policy, i);
+      const PoolRange r = ranges[p];
+      // Monotone: (t - lo) and the product are correctly rounded, floor
+      // and the clamp are monotone, so t1 <= t2 implies q1 <= q2.
+      double x = __dmul_rn(__dsub_rn(t, r.lo), r.scale);
+      uint32_t qv;
+      if (!(x > 0.0)) qv = 0;
+      else if (x >= static_cast<double>(qmax)) qv = qmax;
+      else qv = static_cast<uint32_t>(x);
+      key = qv;
+      if (op.class_bits) key |= cls << op.q_bits;
+      if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+      keys[i] = key;
+      atomicAdd(&s_pool[p], 1u);
+    }
+    for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x)
+    if (s_pool[i]) atomicAdd(&pool_counts[i], s_pool[i]);
+}
+
+__global__ void k_pool_offsets(const uint32_t* __restrict__ counts, int n_pools,
+                               int64_t* __restrict__ offsets) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t acc = 0;
+    for (int p = 0; p < n_pools; ++p) {
+      offsets[p] = acc;
+      acc += counts[p];
+    }
+    offsets[n_pools] = acc;
+  }
+}
+
+// ---- K4: exact tie-fix ---------------------------------------------------
+// Lists the starts of runs of >= 2 equal compact keys, split by run length.
+__global__ void k_tie_detect(const uint32_t* __restrict__ keys, int64_t n,
+                             uint32_t* __restrict__ small_starts, uint32_t* __restrict__ n_small,
+                             uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
+                             uint32_t* __restrict__ n_big, uint32_t cap) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = keys[i];
+    const bool start = (i == 0 || keys[i - 1] != k) && (i + 1 < n && keys[i + 1] == k);
+    if (!start) continue;
+    int64_t e = i + 1;
+    while (e < n && e - i <= 32 && keys[e] == k) ++e;
+    if (e - i <= 32) {
+      const uint32_t slot = atomicAdd(n_small, 1u);
+      if (slot < cap) small_starts[slot] = static_cast<uint32_t>(i);
+    } else {
+      while (e < n && keys[e] == k) ++e;
+      const uint32_t slot = atomicAdd(n_big, 1u);
+      if (slot < cap) {
+        big_starts[slot] = static_cast<uint32_t>(i);
+        big_lens[slot] = static_cast<uint32_t>(e - i);
+      }
+    }
+  }
+}
+
+// Runs of 2..32: one warp each, bitonic sort of exact records in registers.
+__global__ void k_tie_fix_small(QueueDev q, int policy, const uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ perm, int64_t n,
+                                const uint32_t* __restrict__ starts, const uint32_t* __restrict__ n_small,
+                                uint32_t cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t total = min(*n_small, cap);
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
+    const int64_t s = starts[w];
+    const uint32_t k = keys[s];
+    const bool in = (s + lane < n) && keys[s + lane] == k;
+    const uint32_t len = __popc(__ballot_sync(0xffffffffu, in));  // run is contiguous from s
+    TRec r;
+    if (lane < static_cast<int>(len)) {
+      r = load_rec(q, policy, perm[s + lane]);
+    } else {
+      r.w0 = r.w1 = r.w2 = r.msg = r.uid = ~0ull;
+      r.idx = 0xffffffffu;
+    }
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const TRec o = shfl_rec(r, lane ^ j);
+        const bool up = (lane & kk) == 0;
+        const bool lower = (lane & j) == 0;
+        const bool o_less = rec_less(o, r);
+        // lower lane keeps min when ascending, max when descending
+        const bool take = (lower == up) ? o_less : !o_less;
+        if (take) r = o;
+      }
+    }
+    if (lane < static_cast<int>(len)) perm[s + lane] = r.idx;
+  }
+}
+
+// Runs longer than 32: one CTA each. Up to kBigSmem records are sorted in
+// shared memory (bitonic); longer runs use a global merge sort on indices
+// with the exact comparator (only for degenerate inputs).
+constexpr int kBigThreads = 512;
+constexpr int kBigSmem = 1024;
+
+__global__ void __launch_bounds__(kBigThreads)
+k_tie_fix_big(QueueDev q, int policy, uint32_t* __restrict__ perm, uint32_t* __restrict__ scratch,
+              const uint32_t* __restrict__ starts, const uint32_t* __restrict__ lens,
+              const uint32_t* __restrict__ n_big, uint32_t cap) {
+  __shared__ TRec s[kBigSmem];
+  const uint32_t total = min(*n_big, cap);
+  for (uint32_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
+    const int64_t st = starts[seg];
+    const int64_t len = lens[seg];
+    if (len <= kBigSmem) {
+      int64_t p2 = 1;
+      while (p2 < len) p2 <<= 1;
+      for (int64_t i = threadIdx.x; i < p2; i += blockDim.x) {
+        if (i < len) {
+          s[i] = load_rec(q, policy, perm[st + i]);
+        } else {
+          s[i].w0 = s[i].w1 = s[i].w2 = s[i].msg = s[i].uid = ~0ull;
+          s[i].idx = 0xffffffffu;
+        }
+      }
+      __syncthreads();
+      for (int64_t kk = 2; kk <= p2; kk <<= 1) {
+        for (int64_t j = kk >> 1; j > 0; j >>= 1) {
+          for (int64_t i = threadIdx.x; i < p2; i += blockDim.x) {
+            const int64_t l = i ^ j;
+            if (l > i) {
+              const bool up = (i & kk) == 0;
+              const bool sw = up ? rec_less(s[l], s[i]) : rec_less(s[i], s[l]);
+              if (sw) {
+                const TRec t = s[i];
+                s[i] = s[l];
+                s[l] = t;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int64_t i = threadIdx.x; i < len; i += blockDim.x) perm[st + i] = s[i].idx;
+      __syncthreads();
+    } else {
+      // Bottom-up merge sort; element i of run A lands at i + |{b in B: b < a}|.
+      uint32_t* src = perm + st;
+      uint32_t* dst = scratch + st;
+      for (int64_t w = 1; w < len; w <<= 1) {
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+          const int64_t run = i / (2 * w);
+          const int64_t a0 = run * 2 * w;
+          const int64_t b0 = a0 + w;
+          const int64_t b1 = min(a0 + 2 * w, len);
+          const bool inA = i < b0;
+          const TRec x = load_rec(q, policy, src[i]);
+          int64_t lo, hi;
+          if (inA) {
+            lo = b0 < len ? b0 : len;
+            hi = b1 > lo ? b1 : lo;
+          } else {
+            lo = a0;
+            hi = b0;
+          }
+          const int64_t base_lo = lo;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rec_less(load_rec(q, policy, src[mid]), x)) lo = mid + 1;
+            else hi = mid;
+          }
+          const int64_t within = inA ? (i - a0) : (i - b0);
+          dst[a0 + within + (lo - base_lo)] = src[i];
+        }
+        __syncthreads();
+        uint32_t* t = src;
+        src = dst;
+        dst = t;
+      }
+      if (src != perm + st)
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) perm[st + i] = src[i];
+      __syncthreads();
+    }
+  }
+}
+
+// ---- host orchestration --------------------------------------------------
+size_t order_lookback_bytes(int64_t cap) {
+  const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
+  return size_t(tiles) * kRadix * sizeof(uint32_t);
+}
+
+void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, double* k0,
+                  double* k1, double* k2, int sms, cudaStream_t st) {
+  if (n == 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
+  k_score<<<grid, 256, 0, st>>>(q, a, policy, n, k0, k1, k2);
+  KX_CHECK_LAUNCH();
+}
+
+OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
+                            int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
+                            PhaseProfiler* prof) {
+  PhaseProfiler dummy;
+  PhaseProfiler& P = prof ? *prof : dummy;
+  const double N = static_cast<double>(n);
+  OrderResultDev res{};
+  const int passes = op.key_bits / kRadixBits;
+  KX_CUDA(cudaMemsetAsync(ws.small_hdr, 0, ws.small_hdr_bytes, st));
+  // ranges: lo_bits = ~0, hi_bits = 0
+  KX_CUDA(cudaMemsetAsync(ws.ranges, 0, sizeof(PoolRange) * op.n_pools, st));
+  init_ranges(ws.ranges, op.n_pools, st);
+  if (n == 0) {
+    k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
+    KX_CHECK_LAUNCH();
+    res.perm = ws.vals[0];
+    res.keys = ws.keys[0];
+    return res;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
+  // reads agent (4 B) + primary time (8 B) per request
+  P.begin("pool_range", N * 12.0, st);
+  k_pool_range<<<grid, 256, sizeof(uint64_t) * 2 * op.n_pools, st>>>(q, a, op, n, ws.ranges,
+                                                                       ws.error_flags);
+  KX_CHECK_LAUNCH();
+  P.end(st);
+  k_range_finalize<<<(op.n_pools + 127) / 128, 128, 0, st>>>(ws.ranges, op.n_pools, op.q_bits);
+  KX_CHECK_LAUNCH();
+  // reads agent + primary time (12 B), writes the compact key (4 B)
+  P.begin("keygen_hist", N * 16.0, st);
+  k_keygen<<<grid, 256, sizeof(uint32_t) * op.n_pools, st>>>(q, a, op, n, ws.ranges, ws.keys[0],
+                                                              ws.hist, ws.pool_counts);
+  KX_CHECK_LAUNCH();
+  P.end(st);
+  k_scan_hist<<<1, 32 * passes, 0, st>>>(ws.hist, passes);
+  KX_CHECK_LAUNCH();
+  k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
+  KX_CHECK_LAUNCH();
+
+  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+  const size_t smem = sort_dyn_smem<uint32_t>();
+  int cur = 0;
+  for (int p = 0; p < passes; ++p) {
+    KX_CUDA(cudaMemsetAsync(ws.lookback, 0, size_t(tiles) * kRadix * sizeof(uint32_t), st));
+    // key (4 B) [+ index (4 B) after the first pass] in, key + index out
+    P.begin("radix_pass", N * (p == 0 ? 12.0 : 16.0), st);
+    k_onesweep_pass<uint32_t><<<static_cast<unsigned>(tiles), kSortThreads, smem, st>>>(
+        ws.keys[cur], ws.keys[cur ^ 1], p == 0 ? nullptr : ws.vals[cur], ws.vals[cur ^ 1], n,
+        p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+    KX_CHECK_LAUNCH();
+    P.end(st);
+    cur ^= 1;
+  }
+  res.keys = ws.keys[cur];
+  res.perm = ws.vals[cur];
+
+  const int tgrid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
+  // reads the sorted keys (4 B); tie runs gather their exact tuples
+  P.begin("tie_fix", N * 4.0, st);
+  k_tie_detect<<<tgrid, 256, 0, st>>>(res.keys, n, ws.small_starts, ws.n_small, ws.big_starts,
+                                       ws.big_lens, ws.n_big, ws.tie_cap);
+  KX_CHECK_LAUNCH();
+  k_tie_fix_small<<<sms * 8, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
+                                           ws.n_small, ws.tie_cap);
+  KX_CHECK_LAUNCH();
+  k_tie_fix_big<<<sms, kBigThreads, 0, st>>>(q, op.policy, res.perm, ws.vals[cur ^ 1],
+                                             ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);
+  KX_CHECK_LAUNCH();
+  P.end(st);
+  return res;
+}
+
+__global__ void k_init_ranges(PoolRange* r, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    r[p].lo_bits = ~0ull;
+    r[p].hi_bits = 0ull;
+  }
+}
+
+void init_ranges(PoolRange* r, int n, cudaStream_t st) {
+  k_init_ranges<<<(n + 127) / 128, 128, 0, st>>>(r, n);
+  KX_CHECK_LAUNCH();
+}
+
+void configure_sort_kernels() {
+  KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sort_dyn_smem<uint32_t>())));
+}
+
+}  // namespace kx

@@ -1,0 +1,48 @@
+// Host-side interface of the order pipeline (kx_order.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kx_common.cuh"
+#include "kx_state.cuh"
+
+namespace kx {
+
+struct OrderWorkspace {
+  uint32_t* keys[2];
+  uint32_t* vals[2];
+  uint32_t* lookback;
+  PoolRange* ranges;
+  int64_t* pool_offsets;  // n_pools + 1
+  // small header block, zeroed per order: hist[4*256], tile_counters[8],
+  // pool_counts[n_pools], n_small, n_big, error_flags
+  void* small_hdr;
+  size_t small_hdr_bytes;
+  uint32_t* hist;
+  uint32_t* tile_counters;
+  uint32_t* pool_counts;
+  uint32_t* n_small;
+  uint32_t* n_big;
+  int* error_flags;
+  uint32_t* small_starts;
+  uint32_t* big_starts;
+  uint32_t* big_lens;
+  uint32_t tie_cap;
+};
+
+struct OrderResultDev {
+  uint32_t* keys;  // sorted compact keys
+  uint32_t* perm;  // sorted queue indices
+};
+
+size_t order_lookback_bytes(int64_t cap);
+void init_ranges(PoolRange* r, int n, cudaStream_t st);
+void configure_sort_kernels();
+void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, double* k0,
+                  double* k1, double* k2, int sms, cudaStream_t st);
+OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
+                            int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
+                            PhaseProfiler* prof);
+
+}  // namespace kx

@@ -1,0 +1,221 @@
+// K3: LSD radix sort of (key, u32 queue index) pairs, 8-bit digits, one
+// kernel per digit pass with decoupled look-back ("onesweep" structure):
+//
+//   * an upfront histogram of every pass's digits is produced by the key
+//     generator (or by k_upfront_hist) in a single read of the keys;
+//   * each pass kernel takes a dynamic tile id, ranks its tile's digits with
+//     warp match-any + per-warp shared-memory counters (stable), publishes the
+//     tile's per-digit counts, resolves its global digit offsets by looking
+//     back over predecessor tiles (flag|count packed in one u32, so a single
+//     store publishes both), stages the tile in shared memory in digit order
+//     and writes runs of equal digits contiguously (coalesced scatter).
+//
+// The sort is stable, so LSD over the key's digits sorts by the whole key.
+// Replaces the comparator sort/arg-min scans of the reference queue
+// (priority.hpp:89-116, harness.cpp:92-100) for the compact key; ties of the
+// compact key are resolved afterwards by the exact tuple (kx_order.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kx_common.cuh"
+
+namespace kx {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 256;
+constexpr int kSortThreads = 512;
+constexpr int kSortItems = 12;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 6144 elements
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagIncl = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K key, int shift) {
+  return static_cast<uint32_t>(key >> shift) & (kRadix - 1);
+}
+
+// Per-warp-aggregated shared-memory histogram increment. When the whole warp
+// carries one digit (constant high digits are common) a single add is issued.
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t d, bool valid) {
+  const uint32_t active = __ballot_sync(0xffffffffu, valid);
+  if (!active) return;
+  const uint32_t lead = __ffs(active) - 1;
+  const uint32_t d0 = __shfl_sync(0xffffffffu, d, lead);
+  const bool uniform = __all_sync(0xffffffffu, !valid || d == d0);
+  if (uniform) {
+    if ((threadIdx.x & 31) == lead) atomicAdd(&h[d0], __popc(active));
+    return;
+  }
+  if (valid) atomicAdd(&h[d], 1u);
+}
+
+// Generic upfront histogram for a key array (used by the exact-tuple
+// fallback sorts; the order path fuses this into key generation).
+template <typename K>
+__global__ void k_upfront_hist(const K* __restrict__ keys, int64_t n, int shift0,
+                               int passes, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8 * kRadix];
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const K key = valid ? keys[i] : K(0);
+    for (int p = 0; p < passes; ++p) hist_add(&sh[p * kRadix], digit_of(key, shift0 + p * kRadixBits), valid);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// Exclusive scan of each pass's 256 bins (in place): one warp per pass.
+__global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes);
+
+template <typename K>
+struct SortSmem {
+  uint32_t warp_hist[kSortThreads / 32][kRadix];
+  uint32_t digit_start[kRadix];
+  int64_t global_base[kRadix];
+  uint32_t tile_id;
+};
+
+template <typename K>
+constexpr size_t sort_dyn_smem() {
+  return sizeof(SortSmem<K>) + size_t(kSortTile) * (sizeof(K) + sizeof(uint32_t));
+}
+
+// One stable LSD digit pass. vals_in == nullptr means "value = element index"
+// (first pass). global_excl: this pass's exclusive digit offsets.
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads)
+k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
+                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
+                int64_t n, int shift, const uint32_t* __restrict__ global_excl,
+                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
+  K* s_keys = reinterpret_cast<K*>(smem_raw + sizeof(SortSmem<K>));
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
+
+  constexpr int kWarps = kSortThreads / 32;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (tid == 0) sm.tile_id = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = sm.tile_id;
+  const int64_t base = int64_t(tile) * kSortTile;
+
+  K key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t rank[kSortItems];
+  const int64_t wbase = base + int64_t(warp) * 32 * kSortItems + lane;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t e = wbase + i * 32;
+    if (e < n) {
+      key[i] = keys_in[e];
+      val[i] = vals_in ? vals_in[e] : static_cast<uint32_t>(e);
+    } else {
+      key[i] = ~K(0);  // digit 255, ranked after every valid element
+      val[i] = 0;
+    }
+  }
+  // Stable warp-level ranking, processing items in element order.
+  uint32_t* wh = sm.warp_hist[warp];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t d = digit_of(key[i], shift);
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader) {
+      old = wh[d];
+      wh[d] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[i] = old + __popc(peers & lanemask_lt());
+  }
+  __syncthreads();
+
+  // Per digit: exclusive prefix over warps, tile total, look-back.
+  uint32_t total = 0;
+  if (tid < kRadix) {
+#pragma unroll 4
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = sm.warp_hist[w][tid];
+      sm.warp_hist[w][tid] = total;
+      total += c;
+    }
+    volatile uint32_t* lb = lookback;
+    lb[int64_t(tile) * kRadix + tid] = (tile == 0 ? kFlagIncl : kFlagAgg) | total;
+  }
+  // Exclusive scan of `total` over the 256 digits (8 warps x 32 lanes).
+  __shared__ uint32_t s_warp_sums[kRadix / 32];
+  if (tid < kRadix) {
+    uint32_t x = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp_sums[warp] = x;
+    sm.digit_start[tid] = x - total;  // warp-local exclusive
+  }
+  __syncthreads();
+  if (tid < kRadix) {
+    uint32_t add = 0;
+    for (int w = 0; w < warp; ++w) add += s_warp_sums[w];
+    sm.digit_start[tid] += add;
+    // Decoupled look-back for digit `tid`.
+    uint32_t excl = 0;
+    if (tile > 0) {
+      volatile uint32_t* lb = lookback;
+      int64_t p = int64_t(tile) - 1;
+      while (true) {
+        const uint32_t v = lb[p * kRadix + tid];
+        const uint32_t flag = v & ~kCountMask;
+        if (flag == 0) continue;  // predecessor not published yet
+        excl += v & kCountMask;
+        if (flag == kFlagIncl) break;
+        --p;
+      }
+      lb[int64_t(tile) * kRadix + tid] = kFlagIncl | (excl + total);
+    }
+    sm.global_base[tid] = int64_t(global_excl[tid]) + excl - int64_t(sm.digit_start[tid]);
+  }
+  __syncthreads();
+
+  // Stage the tile in digit order.
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t d = digit_of(key[i], shift);
+    const uint32_t pos = sm.digit_start[d] + sm.warp_hist[warp][d] + rank[i];
+    s_keys[pos] = key[i];
+    s_vals[pos] = val[i];
+  }
+  __syncthreads();
+
+  const int64_t valid = (n - base) < kSortTile ? (n - base) : kSortTile;
+#pragma unroll 4
+  for (int j = tid; j < valid; j += kSortThreads) {
+    const K k = s_keys[j];
+    const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
+    keys_out[dst] = k;
+    vals_out[dst] = s_vals[j];
+  }
+}
+
+}  // namespace kx
