@@ -317,6 +317,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
   s->inst_host.assign(cfg->instances, cfg->instances + cfg->n_instances);
   s->pool_begin_host = pool_begin;
   configure_sort_kernels();
+  configure_dispatch_kernels();
 
   // queue SoA
   {
@@ -389,7 +390,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     const size_t o_live = L.take<double>(I), o_run = L.take<int32_t>(I),
                  o_wait = L.take<int32_t>(I), o_susp = L.take<uint8_t>(I),
                  o_base = L.take<int64_t>(I), o_hi = L.take<int64_t>(I),
-                 o_usage = L.take<double>(I * R), o_ex = L.take<uint32_t>(I * R / 32),
+                 o_usage = L.take<double>(I * R), o_ex = L.take<uint8_t>(I * R),
                  o_na = L.take<int32_t>(I), o_au = L.take<uint64_t>(I * kActiveCap),
                  o_ap = L.take<double>(I * kActiveCap), o_ak = L.take<double>(I * kActiveCap),
                  o_at = L.take<double>(I * kActiveCap), o_aT = L.take<double>(I * kActiveCap),
@@ -403,7 +404,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->in.base_slot = at<int64_t>(b, o_base);
     s->in.hi_slot = at<int64_t>(b, o_hi);
     s->in.usage = at<double>(b, o_usage);
-    s->in.exists = at<uint32_t>(b, o_ex);
+    s->in.exists = at<uint8_t>(b, o_ex);
     s->in.n_active = at<int32_t>(b, o_na);
     s->in.act_uid = at<uint64_t>(b, o_au);
     s->in.act_P = at<double>(b, o_ap);
@@ -586,7 +587,7 @@ void dispatch_impl(kx_sched* s, double now) {
   dp.now = now;
   s->prof.begin("dispatch", 0.0, s->stream);
   launch_dispatch(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp,
-                  s->n_pools, s->rows, s->cand, s->row_count, s->admitted_count, s->pool_status,
+                  s->n_pools, s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count, s->pool_status,
                   s->stream);
   s->prof.end(s->stream);
   s->dispatch_valid = true;
@@ -1088,12 +1089,12 @@ int kx_ledger_read(kx_sched* s, int32_t instance_id, int64_t* base_slot, double*
     const int R = s->ring;
     int64_t base = 0;
     std::vector<double> ring_usage(R);
-    std::vector<uint32_t> ring_ex(R / 32);
+    std::vector<uint8_t> ring_ex(R);
     int32_t na = 0;
     KX_CUDA(cudaMemcpyAsync(&base, s->in.base_slot + i, 8, cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaMemcpyAsync(ring_usage.data(), s->in.usage + int64_t(i) * R, R * 8,
                             cudaMemcpyDeviceToHost, s->stream));
-    KX_CUDA(cudaMemcpyAsync(ring_ex.data(), s->in.exists + int64_t(i) * (R / 32), R / 8,
+    KX_CUDA(cudaMemcpyAsync(ring_ex.data(), s->in.exists + int64_t(i) * R, R,
                             cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaMemcpyAsync(&na, s->in.n_active + i, 4, cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaStreamSynchronize(s->stream));
@@ -1102,7 +1103,7 @@ int kx_ledger_read(kx_sched* s, int32_t instance_id, int64_t* base_slot, double*
       const int64_t slot = base + k;
       const uint32_t pos = static_cast<uint32_t>(slot) & (R - 1);
       if (usage) usage[k] = ring_usage[pos];
-      if (exists) exists[k] = (ring_ex[pos >> 5] >> (pos & 31)) & 1u;
+      if (exists) exists[k] = ring_ex[pos];
     }
     if (active_requests) *active_requests = na;
   });

@@ -9,6 +9,7 @@
 namespace kx {
 
 constexpr int kMaxInstPerPool = 512;
+constexpr int kDispSmemLimit = 200 * 1024;  // dynamic shared memory of the dispatch CTA
 
 struct DispatchParams {
   int32_t oracle_T;
@@ -21,9 +22,11 @@ struct DispatchParams {
   double now;
 };
 
+void configure_dispatch_kernels();
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      const int32_t* pool_begin, const uint32_t* perm, const int64_t* pool_offsets,
-                     const DispatchParams& dp, int n_pools, kx_decision* rows, double* cand,
+                     const DispatchParams& dp, int n_pools, int max_inst_per_pool, kx_decision* rows,
+                     double* cand,
                      int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st);
 void launch_ledger_try_place(const InstDev& in, int i, int ring, double P, double k, double t0,

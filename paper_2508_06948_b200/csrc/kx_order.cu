@@ -143,6 +143,17 @@ __global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
   }
   __syncthreads();
   int err = 0;
+  // Per-thread running (pool, min, max), flushed to shared memory only when
+  // the pool changes: pools are mostly contiguous in a queue, so the shared
+  // atomics stay rare instead of hitting one address per request.
+  int32_t cur = -1;
+  uint64_t lo = ~0ull, hi = 0ull;
+  auto flush = [&]() {
+    if (cur >= 0) {
+      atomicMin(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur]), (unsigned long long)lo);
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur + 1]), (unsigned long long)hi);
+    }
+  };
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t ag = q.agent[i];
@@ -157,9 +168,16 @@ __global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
     }
     const int32_t p = a.pool[ag];
     const uint64_t b = ordered_bits(t);
-    atomicMin(reinterpret_cast<unsigned long long*>(&s_rng[2 * p]), (unsigned long long)b);
-    atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * p + 1]), (unsigned long long)b);
+    if (p != cur) {
+      flush();
+      cur = p;
+      lo = ~0ull;
+      hi = 0ull;
+    }
+    lo = b < lo ? b : lo;
+    hi = b > hi ? b : hi;
   }
+  flush();
   if (err) atomicOr(error_flags, err);
   __syncthreads();
   for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
@@ -201,6 +219,8 @@ __global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
   for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) s_pool[i] = 0;
   __syncthreads();
   const uint32_t qmax = (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
+  int32_t cur_pool = -1;
+  uint32_t cur_cnt = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -223,10 +243,16 @@ __global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
       if (op.class_bits) key |= cls << op.q_bits;
       if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
       keys[i] = key;
-      atomicAdd(&s_pool[p], 1u);
+      if (p != cur_pool) {
+        if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
+        cur_pool = p;
+        cur_cnt = 0;
+      }
+      ++cur_cnt;
     }
     for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
   }
+  if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
@@ -247,19 +273,73 @@ __global__ void k_pool_offsets(const uint32_t* __restrict__ counts, int n_pools,
 }
 
 // ---- K4: exact tie-fix ---------------------------------------------------
-// Lists the starts of runs of >= 2 equal compact keys, split by run length.
-__global__ void k_tie_detect(const uint32_t* __restrict__ keys, int64_t n,
-                             uint32_t* __restrict__ small_starts, uint32_t* __restrict__ n_small,
-                             uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
-                             uint32_t* __restrict__ n_big, uint32_t cap) {
+// Runs of equal compact keys are re-sorted by the exact tuple. Runs of up to
+// kThreadRun requests (the common case: a workflow's repeated agent shares
+// app_start) are sorted by the thread that finds the run start, with no
+// list and no atomics; msg/uid are fetched only when the time fields tie.
+// Longer runs are listed for the warp / CTA kernels below.
+constexpr int kThreadRun = 16;
+
+namespace {
+
+struct TKey {
+  uint64_t w0, w1, w2;
+  uint32_t idx;
+};
+
+__device__ __forceinline__ TKey load_tkey(const QueueDev& q, int policy, uint32_t idx) {
+  TKey r;
+  const double app = q.app_start[idx];
+  const double qe = q.queue_enter[idx];
+  switch (policy) {
+    case KX_SCHED_KAIROS: r.w0 = ordered_bits(app); r.w1 = ordered_bits(qe); r.w2 = 0; break;
+    case KX_SCHED_ORACLE: r.w0 = ordered_bits(q.rem[idx]); r.w1 = ordered_bits(qe); r.w2 = ordered_bits(app); break;
+    default: r.w0 = ordered_bits(qe); r.w1 = ordered_bits(app); r.w2 = 0; break;
+  }
+  r.idx = idx;
+  return r;
+}
+
+__device__ __forceinline__ bool tkey_less(const QueueDev& q, const TKey& a, const TKey& b) {
+  if (a.w0 != b.w0) return a.w0 < b.w0;
+  if (a.w1 != b.w1) return a.w1 < b.w1;
+  if (a.w2 != b.w2) return a.w2 < b.w2;
+  const uint64_t ma = q.msg[a.idx], mb = q.msg[b.idx];
+  if (ma != mb) return ma < mb;
+  const uint64_t ua = q.uid[a.idx], ub = q.uid[b.idx];
+  if (ua != ub) return ua < ub;
+  return a.idx < b.idx;
+}
+
+}  // namespace
+
+__global__ void k_tie_runs(QueueDev q, int policy, const uint32_t* __restrict__ keys,
+                           uint32_t* __restrict__ perm, int64_t n,
+                           uint32_t* __restrict__ small_starts, uint32_t* __restrict__ n_small,
+                           uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
+                           uint32_t* __restrict__ n_big, uint32_t cap) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = keys[i];
     const bool start = (i == 0 || keys[i - 1] != k) && (i + 1 < n && keys[i + 1] == k);
     if (!start) continue;
-    int64_t e = i + 1;
+    int64_t e = i + 2;
     while (e < n && e - i <= 32 && keys[e] == k) ++e;
-    if (e - i <= 32) {
+    const int len = static_cast<int>(e - i);
+    if (len <= kThreadRun) {
+      TKey r[kThreadRun];
+      for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
+      for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
+        const TKey x = r[j];
+        int m = j - 1;
+        while (m >= 0 && tkey_less(q, x, r[m])) {
+          r[m + 1] = r[m];
+          --m;
+        }
+        r[m + 1] = x;
+      }
+      for (int j = 0; j < len; ++j) perm[i + j] = r[j].idx;
+    } else if (len <= 32) {
       const uint32_t slot = atomicAdd(n_small, 1u);
       if (slot < cap) small_starts[slot] = static_cast<uint32_t>(i);
     } else {
@@ -468,8 +548,8 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   const int tgrid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
   // reads the sorted keys (4 B); tie runs gather their exact tuples
   P.begin("tie_fix", N * 4.0, st);
-  k_tie_detect<<<tgrid, 256, 0, st>>>(res.keys, n, ws.small_starts, ws.n_small, ws.big_starts,
-                                       ws.big_lens, ws.n_big, ws.tie_cap);
+  k_tie_runs<<<tgrid, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts, ws.n_small,
+                                     ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);
   KX_CHECK_LAUNCH();
   k_tie_fix_small<<<sms * 8, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
                                            ws.n_small, ws.tie_cap);

@@ -53,7 +53,7 @@ struct InstDev {
   int64_t* base_slot;   // lowest retained slot (gc boundary)
   int64_t* hi_slot;     // highest slot ever booked (>= base_slot - 1)
   double* usage;        // [n_inst * ring]
-  uint32_t* exists;     // [n_inst * ring / 32] bitmask: slot present in usage_ map
+  uint8_t* exists;      // [n_inst * ring]: slot present in the usage_ map (plain byte stores)
   int32_t* n_active;
   uint64_t* act_uid;    // [n_inst * kActiveCap]
   double* act_P;

@@ -94,3 +94,27 @@ def test_random_ledger_sequences_match_oracle(gpu_lib):
         b = L.slots()
         assert a.keys() == b.keys()
         assert all(bits(a[x]) == bits(b[x]) for x in a)
+
+
+def test_commit_batch_equals_sequential_commits(gpu_lib):
+    rng = np.random.default_rng(31)
+    inst = [kx.InstanceProfile(id=5 + 2 * i, capacity_tokens=4000.0, decode_rate=30.0 + i, max_batch=8)
+            for i in range(6)]
+    a = kx.DeviceScheduler(inst, queue_capacity=16, max_agents=4)
+    b = kx.DeviceScheduler(inst, queue_capacity=16, max_agents=4)
+    n = 300
+    ids = rng.choice([p.id for p in inst], n).astype(np.int32)
+    P = rng.integers(10, 800, n).astype(float)
+    k = np.array([30.0 + (i - 5) // 2 for i in ids])
+    t0 = rng.uniform(0, 2, n)
+    T = rng.uniform(0.2, 8, n)
+    fits = a.commit_batch(ids, np.arange(n, dtype=np.uint64) + 1, P, k, t0, T)
+    for j in range(n):
+        f, _, _ = b.try_place(int(ids[j]), P[j], k[j], t0[j], T[j])
+        assert f == bool(fits[j])
+        if f:
+            b.commit(int(ids[j]), j + 1, P[j], k[j], t0[j], T[j])
+    for p in inst:
+        x, y = a.ledger(p.id), b.ledger(p.id)
+        assert x[1] == y[1] and x[0].keys() == y[0].keys()
+        assert all(bits(x[0][s]) == bits(y[0][s]) for s in x[0])
