@@ -114,6 +114,7 @@ def make_sched(snap, insts, live, running, commits, device):
     c = np.array(commits, dtype=np.float64).T if commits else np.zeros((6, 0))
     s.commit_batch(c[0].astype(np.int32), np.array([x[1] for x in commits], np.uint64), c[2], c[3], c[4], c[5])
     s.set_live(live, running, np.zeros(len(insts), np.int32))
+    s.gc(NOW)  # the pre-loaded state is the end of the previous round (engine.cpp:212)
     s.checkpoint()
     return s
 
@@ -283,6 +284,7 @@ def _ref_lib():
     L.kxref_pool_free.argtypes = [P]
     L.kxref_pool_set_live.argtypes = [P, P, P, P]
     L.kxref_pool_commit.argtypes = [P, C.c_int32, C.c_uint64, C.c_int64, C.c_double, C.c_double]
+    L.kxref_pool_gc.argtypes = [P, C.c_double]
     L.kxref_pool_set_queue.argtypes = [P, C.c_int64, P, P, P, P, P, P, P]
     L.kxref_pool_reset.argtypes = [P]
     L.kxref_pool_tick.restype = C.c_int64
@@ -317,6 +319,7 @@ class RefPools:
             for (iid, uid, P, k, t0, T) in commits:
                 if iid in ids:
                     L.kxref_pool_commit(h, int(iid), int(uid), int(P), t0, T)
+            L.kxref_pool_gc(h, NOW)
             lv = np.ascontiguousarray(live[sel])
             rn = np.ascontiguousarray(running[sel], np.int32)
             wt = np.zeros(len(ids), np.int32)

@@ -116,6 +116,9 @@ int kxref_pool_commit(void* h, int32_t instance_id, uint64_t uid, int64_t prompt
   return 0;
 }
 
+// Dispatcher::gc on the pre-tick state (the previous round ended at `now`).
+void kxref_pool_gc(void* h, double now) { static_cast<RefPool*>(h)->pristine_disp->gc(now); }
+
 // Queue contents; msg ids are "m-<msg_counter>" (MessageIdFactory, types.hpp:46-57).
 void kxref_pool_set_queue(void* h, int64_t n, const int32_t* agent, const int64_t* prompt,
                           const double* app, const double* qe, const uint64_t* msg_counter,

@@ -27,7 +27,7 @@ namespace kx {
 
 namespace {
 
-constexpr int kDispThreads = 1024;
+constexpr int kDispThreads = 512;
 constexpr int kDispWarps = kDispThreads / 32;
 constexpr int kHeadBatch = 64;
 
@@ -51,53 +51,93 @@ struct Ring {
   int64_t hi;
 };
 
-// SlotLedger::try_place (dispatcher.cpp:52-68), one warp: lanes stride the
-// retained slots; first violating span slot = warp min, peak = warp max.
-__device__ Eval warp_try_place(const Ring& r, int ring, double cap, double P, double k, double t0,
-                               double T, double slot_len, bool* overflow) {
-  const int lane = threadIdx.x & 31;
+// The candidate's memory model for one head (t0 = now): span and the
+// constants peak_in_slot compares against (dispatcher.cpp:19-42).
+struct Span {
   int64_t first, last;
-  span_bounds_dev(t0, T, slot_len, &first, &last);
-  const double t_end = __dadd_rn(t0, T);
-  if (last >= first && (first < r.base || last >= r.base + ring)) *overflow = true;
-  const int64_t smax = r.hi > last ? r.hi : last;
-  double peak = 0.0;
-  int64_t viol = INT64_MAX;
+  double t0, t_end, t0e, tee;  // t0 + eps, t_end - eps
+};
+
+__device__ __forceinline__ Span make_span(double t0, double T, double slot_len) {
+  Span sp;
+  span_bounds_dev(t0, T, slot_len, &sp.first, &sp.last);
+  sp.t0 = t0;
+  sp.t_end = __dadd_rn(t0, T);
+  sp.t0e = __dadd_rn(t0, kTimeEpsilon);
+  sp.tee = __dsub_rn(sp.t_end, kTimeEpsilon);
+  return sp;
+}
+
+// peak_in_slot (dispatcher.cpp:33-42) with the per-head constants hoisted.
+__device__ __forceinline__ double pis(const Span& sp, double P, double k, int64_t slot,
+                                      double slot_len) {
+  const double slot_start = __dmul_rn(static_cast<double>(slot), slot_len);
+  const double slot_end = __dadd_rn(slot_start, slot_len);
+  if (slot_end <= sp.t0e || slot_start >= sp.tee) return 0.0;
+  const double eval_t = (sp.t_end < slot_end) ? sp.t_end : slot_end;
+  return __dadd_rn(P, __dmul_rn(k, __dsub_rn(eval_t, sp.t0)));
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+  const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(v >> 32));
+  const uint32_t lo = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(v >> 32) == hi
+                                                         ? static_cast<uint32_t>(v) : 0u);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+  const uint32_t hi = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(v >> 32));
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(v >> 32) == hi
+                                                         ? static_cast<uint32_t>(v) : 0xffffffffu);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// SlotLedger::try_place (dispatcher.cpp:52-68), one warp: lanes stride the
+// retained slots; first violating span slot = warp min, peak = warp max
+// (REDUX on the order-preserving bits: max/min are exact).
+__device__ Eval warp_try_place(const Ring& r, int ring, double cap, double P, double k,
+                               const Span& sp, double slot_len, bool* overflow) {
+  const int lane = threadIdx.x & 31;
+  if (sp.last >= sp.first && (sp.first < r.base || sp.last >= r.base + ring)) *overflow = true;
+  const int64_t smax = r.hi > sp.last ? r.hi : sp.last;
+  uint64_t peak = ordered_bits(0.0);
+  uint32_t viol = 0xffffffffu;  // offset from base
   for (int64_t s = r.base + lane; s <= smax; s += 32) {
     const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
-    const bool in_span = (s >= first && s <= last);
+    const bool in_span = (s >= sp.first && s <= sp.last);
     const bool exists = r.ex[pos] != 0;
     if (!(in_span || exists)) continue;
     const double used = exists ? r.usage[pos] : 0.0;
-    const double total = __dadd_rn(used, peak_in_slot_dev(P, k, t0, t_end, s, slot_len));
-    if (in_span && total > cap && s < viol) viol = s;
-    peak = fmax(peak, total);
+    const double total = __dadd_rn(used, pis(sp, P, k, s, slot_len));
+    const uint32_t off = static_cast<uint32_t>(s - r.base);
+    if (in_span && total > cap && off < viol) viol = off;
+    const uint64_t tb = ordered_bits(total);
+    peak = tb > peak ? tb : peak;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t v2 = __shfl_xor_sync(0xffffffffu, viol, o);
-    viol = v2 < viol ? v2 : viol;
-    peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-  }
+  viol = __reduce_min_sync(0xffffffffu, viol);
   Eval e;
-  e.state = viol != INT64_MAX ? kExceeds : kFits;
-  e.peak = peak;
-  e.viol = viol;
+  if (viol != 0xffffffffu) {
+    e.state = kExceeds;
+    e.viol = r.base + viol;
+    e.peak = 0.0;
+  } else {
+    e.state = kFits;
+    e.viol = 0;
+    e.peak = from_ordered_bits(warp_max_u64(peak));
+  }
   return e;
 }
 
 // SlotLedger::commit's booking (dispatcher.cpp:75-78), one warp.
-__device__ void warp_commit(Ring& r, int ring, double P, double k, double t0, double T,
+__device__ void warp_commit(Ring& r, int ring, double P, double k, const Span& sp,
                             double slot_len) {
   const int lane = threadIdx.x & 31;
-  int64_t first, last;
-  span_bounds_dev(t0, T, slot_len, &first, &last);
-  const double t_end = __dadd_rn(t0, T);
-  for (int64_t s = first + lane; s <= last; s += 32) {
+  for (int64_t s = sp.first + lane; s <= sp.last; s += 32) {
     const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
-    r.usage[pos] = __dadd_rn(r.usage[pos], peak_in_slot_dev(P, k, t0, t_end, s, slot_len));
+    r.usage[pos] = __dadd_rn(r.usage[pos], pis(sp, P, k, s, slot_len));
     r.ex[pos] = 1;
   }
-  if (last >= first && last > r.hi) r.hi = last;
+  if (sp.last >= sp.first && sp.last > r.hi) r.hi = sp.last;
   __syncwarp();
 }
 
@@ -164,64 +204,62 @@ __device__ __forceinline__ Ring global_ring(const InstDev& in, int i, int ring) 
   return r;
 }
 
-// Shared-memory layout of the dispatch kernel for a pool of `ni` instances.
-struct DispSmem {
-  double *live, *cap, *k, *snap, *peak, *h_T;
-  int64_t *base, *hi, *viol, *h_prompt, *h_kept;
-  uint64_t* h_uid;
-  int32_t *run, *wait, *mb, *id, *h_agent;
-  uint32_t* h_idx;
-  uint8_t *susp, *state;
-  double* usage;  // ni * ring (smem-staged rings only)
-  uint8_t* ex;
+}  // namespace
+
+// Byte offsets of the dispatch kernel's shared-memory arrays (host-computed,
+// passed by value so the kernel never re-derives them).
+struct DispLayout {
+  uint32_t live, cap, k, snap, peak, base, hi, viol, run, wait, mb, id, susp, state;
+  uint32_t h_T, h_prompt, h_kept, h_uid, h_agent, h_idx, h_first, h_last, h_tend;
+  uint32_t usage, ex, total;
 };
 
-__host__ __device__ inline size_t disp_align(size_t x) { return (x + 15) & ~size_t(15); }
-
-__host__ __device__ inline size_t disp_smem_bytes(int ni, int ring, bool smem_ring, DispSmem* out,
-                                                  unsigned char* base) {
-  size_t o = 0;
+DispLayout disp_layout(int ni, int ring, bool smem_ring) {
+  DispLayout L{};
+  uint32_t o = 0;
   auto take = [&](size_t bytes) {
-    const size_t at = o;
-    o = disp_align(o + bytes);
-    return base ? base + at : nullptr;
+    const uint32_t at = o;
+    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
+    return at;
   };
-  DispSmem d;
-  d.live = reinterpret_cast<double*>(take(8 * ni));
-  d.cap = reinterpret_cast<double*>(take(8 * ni));
-  d.k = reinterpret_cast<double*>(take(8 * ni));
-  d.snap = reinterpret_cast<double*>(take(8 * 2 * ni));
-  d.peak = reinterpret_cast<double*>(take(8 * 2 * ni));
-  d.base = reinterpret_cast<int64_t*>(take(8 * ni));
-  d.hi = reinterpret_cast<int64_t*>(take(8 * ni));
-  d.viol = reinterpret_cast<int64_t*>(take(8 * 2 * ni));
-  d.run = reinterpret_cast<int32_t*>(take(4 * ni));
-  d.wait = reinterpret_cast<int32_t*>(take(4 * ni));
-  d.mb = reinterpret_cast<int32_t*>(take(4 * ni));
-  d.id = reinterpret_cast<int32_t*>(take(4 * ni));
-  d.susp = take(ni);
-  d.state = take(2 * ni);
-  d.h_T = reinterpret_cast<double*>(take(8 * kHeadBatch));
-  d.h_prompt = reinterpret_cast<int64_t*>(take(8 * kHeadBatch));
-  d.h_kept = reinterpret_cast<int64_t*>(take(8 * kHeadBatch));
-  d.h_uid = reinterpret_cast<uint64_t*>(take(8 * kHeadBatch));
-  d.h_agent = reinterpret_cast<int32_t*>(take(4 * kHeadBatch));
-  d.h_idx = reinterpret_cast<uint32_t*>(take(4 * kHeadBatch));
-  d.usage = smem_ring ? reinterpret_cast<double*>(take(size_t(8) * ni * ring)) : nullptr;
-  d.ex = smem_ring ? take(size_t(ni) * ring) : nullptr;
-  if (out) *out = d;
-  return o;
+  L.live = take(8 * ni);
+  L.cap = take(8 * ni);
+  L.k = take(8 * ni);
+  L.snap = take(8 * 2 * ni);
+  L.peak = take(8 * 2 * ni);
+  L.base = take(8 * ni);
+  L.hi = take(8 * ni);
+  L.viol = take(8 * 2 * ni);
+  L.run = take(4 * ni);
+  L.wait = take(4 * ni);
+  L.mb = take(4 * ni);
+  L.id = take(4 * ni);
+  L.susp = take(ni);
+  L.state = take(2 * ni);
+  L.h_T = take(8 * kHeadBatch);
+  L.h_prompt = take(8 * kHeadBatch);
+  L.h_kept = take(8 * kHeadBatch);
+  L.h_uid = take(8 * kHeadBatch);
+  L.h_agent = take(4 * kHeadBatch);
+  L.h_idx = take(4 * kHeadBatch);
+  L.h_first = take(8 * kHeadBatch);
+  L.h_last = take(8 * kHeadBatch);
+  L.h_tend = take(8 * kHeadBatch);
+  L.usage = smem_ring ? take(size_t(8) * ni * ring) : 0;
+  L.ex = smem_ring ? take(size_t(ni) * ring) : 0;
+  L.total = o;
+  return L;
 }
 
-}  // namespace
+#define SM(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
 
 template <bool kSmemRing>
 __global__ void __launch_bounds__(kDispThreads)
 k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
                     const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
-                    DispatchParams dp, kx_decision* __restrict__ rows, double* __restrict__ cand,
-                    int64_t* __restrict__ row_count, int64_t* __restrict__ admitted_count,
-                    int* __restrict__ pool_status) {
+                    DispatchParams dp, DispLayout lay, kx_decision* __restrict__ rows,
+                    double* __restrict__ cand, int64_t* __restrict__ row_count,
+                    int64_t* __restrict__ admitted_count, int* __restrict__ pool_status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_status;
   const int pool = blockIdx.x;
@@ -231,30 +269,28 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
   const int ni = pool_begin[pool + 1] - ib;
   const int ring = dp.ring;
   const double now = dp.now;
-  DispSmem S;
-  disp_smem_bytes(ni, ring, kSmemRing, &S, smem_raw);
 
   // Stage the pool's instance state (and rings) in shared memory.
   for (int li = threadIdx.x; li < ni; li += kDispThreads) {
     const int i = ib + li;
-    S.live[li] = in.live_kv[i];
-    S.cap[li] = in.cap[i];
-    S.k[li] = in.decode_rate[i];
-    S.base[li] = in.base_slot[i];
-    S.hi[li] = in.hi_slot[i];
-    S.run[li] = in.running[i];
-    S.wait[li] = in.waiting[i];
-    S.mb[li] = in.max_batch[i];
-    S.id[li] = in.id[i];
-    S.susp[li] = in.suspended[i];
+    SM(double, live)[li] = in.live_kv[i];
+    SM(double, cap)[li] = in.cap[i];
+    SM(double, k)[li] = in.decode_rate[i];
+    SM(int64_t, base)[li] = in.base_slot[i];
+    SM(int64_t, hi)[li] = in.hi_slot[i];
+    SM(int32_t, run)[li] = in.running[i];
+    SM(int32_t, wait)[li] = in.waiting[i];
+    SM(int32_t, mb)[li] = in.max_batch[i];
+    SM(int32_t, id)[li] = in.id[i];
+    SM(uint8_t, susp)[li] = in.suspended[i];
   }
   if (kSmemRing) {
     const int64_t tot = int64_t(ni) * ring;
     const double* gu = in.usage + int64_t(ib) * ring;
     const uint8_t* ge = in.exists + int64_t(ib) * ring;
     for (int64_t j = threadIdx.x; j < tot; j += kDispThreads) {
-      S.usage[j] = gu[j];
-      S.ex[j] = ge[j];
+      SM(double, usage)[j] = gu[j];
+      SM(uint8_t, ex)[j] = ge[j];
     }
   }
   if (threadIdx.x == 0) s_status = KX_OK;
@@ -263,14 +299,14 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
   auto ring_of = [&](int li) {
     Ring r;
     if (kSmemRing) {
-      r.usage = S.usage + int64_t(li) * ring;
-      r.ex = S.ex + int64_t(li) * ring;
+      r.usage = SM(double, usage) + int64_t(li) * ring;
+      r.ex = SM(uint8_t, ex) + int64_t(li) * ring;
     } else {
       r.usage = in.usage + int64_t(ib + li) * ring;
       r.ex = in.exists + int64_t(ib + li) * ring;
     }
-    r.base = S.base[li];
-    r.hi = S.hi[li];
+    r.base = SM(int64_t, base)[li];
+    r.hi = SM(int64_t, hi)[li];
     return r;
   };
 
@@ -280,6 +316,7 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
   int64_t nrows = 0, nadm = 0;
   int retries = 0;
   int par = 0;
+  const double t0e = __dadd_rn(now, kTimeEpsilon);
 
   while (pos < q_end) {
     if (pos >= hb_start + hb_n) {  // refill the head batch (prefix of the pool's order)
@@ -287,46 +324,61 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
       hb_start = pos;
       hb_n = q_end - pos < kHeadBatch ? q_end - pos : kHeadBatch;
       if (threadIdx.x < hb_n) {
-        const uint32_t idx = perm[pos + threadIdx.x];
+        const int t = threadIdx.x;
+        const uint32_t idx = perm[pos + t];
         const int32_t a = q.agent[idx];
-        S.h_idx[threadIdx.x] = idx;
-        S.h_agent[threadIdx.x] = a;
-        S.h_prompt[threadIdx.x] = q.prompt[idx];
-        S.h_kept[threadIdx.x] = q.kept[idx];
-        S.h_uid[threadIdx.x] = q.uid[idx];
-        S.h_T[threadIdx.x] = dp.oracle_T ? q.pure_exec[idx] : ag.T[a];
+        const double T = dp.oracle_T ? q.pure_exec[idx] : ag.T[a];
+        SM(uint32_t, h_idx)[t] = idx;
+        SM(int32_t, h_agent)[t] = a;
+        SM(int64_t, h_prompt)[t] = q.prompt[idx];
+        SM(int64_t, h_kept)[t] = q.kept[idx];
+        SM(uint64_t, h_uid)[t] = q.uid[idx];
+        SM(double, h_T)[t] = T;
+        int64_t f, l;
+        span_bounds_dev(now, T, dp.slot_len, &f, &l);
+        SM(int64_t, h_first)[t] = f;
+        SM(int64_t, h_last)[t] = l;
+        SM(double, h_tend)[t] = __dadd_rn(now, T);
       }
       __syncthreads();
     }
     const int h = static_cast<int>(pos - hb_start);
-    const int64_t prompt = S.h_prompt[h];
+    const int64_t prompt = SM(int64_t, h_prompt)[h];
     const double P = static_cast<double>(prompt);
-    const double T = S.h_T[h];
+    const double T = SM(double, h_T)[h];
+    Span sp;
+    sp.first = SM(int64_t, h_first)[h];
+    sp.last = SM(int64_t, h_last)[h];
+    sp.t0 = now;
+    sp.t_end = SM(double, h_tend)[h];
+    sp.t0e = t0e;
+    sp.tee = __dsub_rn(sp.t_end, kTimeEpsilon);
     bool overflow = false;
 
     for (int li = warp; li < ni; li += kDispWarps) {
       // collect_live: watermark resume on the freshest usage, then batch_full.
-      const double live = S.live[li];
-      uint8_t susp = S.susp[li];
-      if (susp && live < __dmul_rn(dp.watermark, S.cap[li])) {
+      const double live = SM(double, live)[li];
+      uint8_t susp = SM(uint8_t, susp)[li];
+      if (susp && live < __dmul_rn(dp.watermark, SM(double, cap)[li])) {
         susp = 0;
         __syncwarp();
-        if (lane == 0) S.susp[li] = 0;
+        if (lane == 0) SM(uint8_t, susp)[li] = 0;
       }
-      const bool full = S.run[li] + S.wait[li] >= S.mb[li];
+      const bool full = SM(int32_t, run)[li] + SM(int32_t, wait)[li] >= SM(int32_t, mb)[li];
       Eval e;
       if (susp || full) {
         e.state = kExcluded;
         e.peak = 0.0;
         e.viol = 0;
       } else {
-        e = warp_try_place(ring_of(li), ring, S.cap[li], P, S.k[li], now, T, dp.slot_len, &overflow);
+        e = warp_try_place(ring_of(li), ring, SM(double, cap)[li], P, SM(double, k)[li], sp,
+                           dp.slot_len, &overflow);
       }
       if (lane == 0) {
-        S.peak[par * ni + li] = e.peak;
-        S.viol[par * ni + li] = e.viol;
-        S.state[par * ni + li] = e.state;
-        S.snap[par * ni + li] = live;
+        SM(double, peak)[par * ni + li] = e.peak;
+        SM(int64_t, viol)[par * ni + li] = e.viol;
+        SM(uint8_t, state)[par * ni + li] = e.state;
+        SM(double, snap)[par * ni + li] = live;
       }
     }
     if (overflow && lane == 0) atomicExch(&s_status, KX_ERR_CAPACITY);
@@ -334,51 +386,47 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
     if (s_status != KX_OK) break;
 
     // select_instance: min (peak, InstanceId) over fitting candidates (H9).
-    double bpeak = 0.0;
-    int bid = INT32_MAX, bli = -1;
+    uint64_t bkey = ~0ull;
+    uint32_t bid = 0xffffffffu;
+    int bli = -1;
     for (int li = lane; li < ni; li += 32) {
-      if (S.state[par * ni + li] != kFits) continue;
-      const double pk = S.peak[par * ni + li];
-      const int id = S.id[li];
-      if (bli < 0 || pk < bpeak || (pk == bpeak && id < bid)) {
-        bpeak = pk;
+      if (SM(uint8_t, state)[par * ni + li] != kFits) continue;
+      const uint64_t kb = ordered_bits(SM(double, peak)[par * ni + li]);
+      const uint32_t id = static_cast<uint32_t>(SM(int32_t, id)[li]) ^ 0x80000000u;
+      if (bli < 0 || kb < bkey || (kb == bkey && id < bid)) {
+        bkey = kb;
         bid = id;
         bli = li;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double p2 = __shfl_xor_sync(0xffffffffu, bpeak, o);
-      const int id2 = __shfl_xor_sync(0xffffffffu, bid, o);
-      const int l2 = __shfl_xor_sync(0xffffffffu, bli, o);
-      if (l2 >= 0 && (bli < 0 || p2 < bpeak || (p2 == bpeak && (id2 < bid || (id2 == bid && l2 < bli))))) {
-        bpeak = p2;
-        bid = id2;
-        bli = l2;
-      }
-    }
+    const uint64_t wkey = warp_min_u64(bkey);
+    const uint32_t wid = __reduce_min_sync(0xffffffffu, (bli >= 0 && bkey == wkey) ? bid : 0xffffffffu);
+    const uint32_t winners = __ballot_sync(0xffffffffu, bli >= 0 && bkey == wkey && bid == wid);
+    bli = winners ? __shfl_sync(0xffffffffu, bli, __ffs(winners) - 1) : -1;
+    const double bpeak = bli >= 0 ? SM(double, peak)[par * ni + bli] : 0.0;
     // Overload check (engine.cpp:254-258) on the owner's live snapshot.
-    const bool overload = bli >= 0 && __dadd_rn(S.snap[par * ni + bli], P) > S.cap[bli];
+    const bool overload = bli >= 0 && __dadd_rn(SM(double, snap)[par * ni + bli], P) > SM(double, cap)[bli];
 
-    if (warp == 0) {  // decision log (engine.cpp:242-246)
+    if (warp == kDispWarps - 1) {  // decision log (engine.cpp:242-246)
       if (nrows < dp.log_cap) {
         const int64_t r = int64_t(pool) * dp.log_cap + nrows;
         if (lane == 0) {
           kx_decision d;
           d.time = now;
           d.predicted_peak = bli >= 0 ? bpeak : 0.0;
-          d.uid = S.h_uid[h];
-          d.queue_index = S.h_idx[h];
-          d.agent = S.h_agent[h];
-          d.target = bli >= 0 ? bid : -1;
+          d.uid = SM(uint64_t, h_uid)[h];
+          d.queue_index = SM(uint32_t, h_idx)[h];
+          d.agent = SM(int32_t, h_agent)[h];
+          d.target = bli >= 0 ? SM(int32_t, id)[bli] : -1;
           d.pool = pool;
           d.admitted = (bli >= 0 && !overload) ? 1 : 0;
           rows[r] = d;
         }
         for (int li = lane; li < ni; li += 32) {
-          const uint8_t st = S.state[par * ni + li];
+          const uint8_t st = SM(uint8_t, state)[par * ni + li];
           double v = -1.0;
-          if (st == kFits) v = S.peak[par * ni + li];
-          else if (st == kExceeds) v = __dsub_rn(-static_cast<double>(S.viol[par * ni + li]), 1.0);
+          if (st == kFits) v = SM(double, peak)[par * ni + li];
+          else if (st == kExceeds) v = __dsub_rn(-static_cast<double>(SM(int64_t, viol)[par * ni + li]), 1.0);
           cand[r * dp.peak_stride + li] = v;
         }
       }
@@ -387,7 +435,7 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
     if (bli < 0) break;  // head keeps its place until the next round (engine.cpp:247)
     const bool owner = (bli % kDispWarps) == warp;
     if (overload) {
-      if (owner && lane == 0) S.susp[bli] = 1;  // Dispatcher::on_overload
+      if (owner && lane == 0) SM(uint8_t, susp)[bli] = 1;  // Dispatcher::on_overload
       if (++retries > ni) {
         if (threadIdx.x == 0) s_status = KX_ERR_LIVELOCK;
         break;
@@ -398,13 +446,16 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
     retries = 0;
     if (owner) {
       Ring r = ring_of(bli);
-      warp_commit(r, ring, P, S.k[bli], now, T, dp.slot_len);
+      const double k = SM(double, k)[bli];
+      warp_commit(r, ring, P, k, sp, dp.slot_len);
       if (lane == 0) {
-        S.hi[bli] = r.hi;
-        S.live[bli] = __dadd_rn(S.live[bli], static_cast<double>(prompt + S.h_kept[h]));
-        S.run[bli] += 1;
-        q.admitted[S.h_idx[h]] = 1;
-        active_append(in, ib + bli, S.h_uid[h], P, S.k[bli], now, T, &s_status);
+        SM(int64_t, hi)[bli] = r.hi;
+        SM(double, live)[bli] = __dadd_rn(SM(double, live)[bli],
+                                          static_cast<double>(prompt + SM(int64_t, h_kept)[h]));
+        SM(int32_t, run)[bli] += 1;
+        const uint32_t idx = SM(uint32_t, h_idx)[h];
+        q.admitted[idx] = 1;
+        active_append(in, ib + bli, SM(uint64_t, h_uid)[h], P, k, now, T, &s_status);
       }
       __syncwarp();
     }
@@ -418,26 +469,26 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
     Ring r = ring_of(li);
     warp_gc_slots(r, ring, now, dp.slot_len);
     if (lane == 0) {
-      S.base[li] = r.base;
+      SM(int64_t, base)[li] = r.base;
       active_gc(in, ib + li, now);
     }
   }
   __syncthreads();
   for (int li = threadIdx.x; li < ni; li += kDispThreads) {
     const int i = ib + li;
-    in.live_kv[i] = S.live[li];
-    in.base_slot[i] = S.base[li];
-    in.hi_slot[i] = S.hi[li];
-    in.running[i] = S.run[li];
-    in.suspended[i] = S.susp[li];
+    in.live_kv[i] = SM(double, live)[li];
+    in.base_slot[i] = SM(int64_t, base)[li];
+    in.hi_slot[i] = SM(int64_t, hi)[li];
+    in.running[i] = SM(int32_t, run)[li];
+    in.suspended[i] = SM(uint8_t, susp)[li];
   }
   if (kSmemRing) {
     const int64_t tot = int64_t(ni) * ring;
     double* gu = in.usage + int64_t(ib) * ring;
     uint8_t* ge = in.exists + int64_t(ib) * ring;
     for (int64_t j = threadIdx.x; j < tot; j += kDispThreads) {
-      gu[j] = S.usage[j];
-      ge[j] = S.ex[j];
+      gu[j] = SM(double, usage)[j];
+      ge[j] = SM(uint8_t, ex)[j];
     }
   }
   if (threadIdx.x == 0) {
@@ -447,13 +498,15 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
   }
 }
 
+#undef SM
+
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
 __global__ void k_ledger_try_place(InstDev in, int i, int ring, double P, double k, double t0,
                                    double T, double slot_len, double* out_peak, int64_t* out_viol,
                                    int* out_state) {
   bool overflow = false;
-  const Eval e = warp_try_place(global_ring(in, i, ring), ring, in.cap[i], P, k, t0, T, slot_len,
-                                &overflow);
+  const Eval e = warp_try_place(global_ring(in, i, ring), ring, in.cap[i], P, k,
+                                make_span(t0, T, slot_len), slot_len, &overflow);
   if (threadIdx.x == 0) {
     *out_peak = e.peak;
     *out_viol = e.viol;
@@ -466,13 +519,14 @@ __device__ bool warp_commit_checked(InstDev& in, int i, int ring, uint64_t uid, 
                                     double t0, double T, double slot_len, int* status) {
   bool overflow = false;
   Ring r = global_ring(in, i, ring);
-  const Eval e = warp_try_place(r, ring, in.cap[i], P, k, t0, T, slot_len, &overflow);
+  const Span sp = make_span(t0, T, slot_len);
+  const Eval e = warp_try_place(r, ring, in.cap[i], P, k, sp, slot_len, &overflow);
   if (overflow) {
     if ((threadIdx.x & 31) == 0) *status = KX_ERR_CAPACITY;
     return false;
   }
   if (e.state != kFits) return false;
-  warp_commit(r, ring, P, k, t0, T, slot_len);
+  warp_commit(r, ring, P, k, sp, slot_len);
   if ((threadIdx.x & 31) == 0) {
     in.hi_slot[i] = r.hi;
     active_append(in, i, uid, P, k, t0, T, status);
@@ -572,16 +626,16 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      const DispatchParams& dp, int n_pools, int max_inst_per_pool, kx_decision* rows,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st) {
-  const size_t with_ring = disp_smem_bytes(max_inst_per_pool, dp.ring, true, nullptr, nullptr);
-  if (with_ring <= static_cast<size_t>(kDispSmemLimit)) {
-    k_dispatch_timeslot<true><<<n_pools, kDispThreads, with_ring, st>>>(
-        q, a, in, pool_begin, perm, pool_offsets, dp, rows, cand, row_count, admitted_count,
-        pool_status);
+  const DispLayout with_ring = disp_layout(max_inst_per_pool, dp.ring, true);
+  if (with_ring.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+    k_dispatch_timeslot<true><<<n_pools, kDispThreads, with_ring.total, st>>>(
+        q, a, in, pool_begin, perm, pool_offsets, dp, with_ring, rows, cand, row_count,
+        admitted_count, pool_status);
   } else {
-    const size_t no_ring = disp_smem_bytes(max_inst_per_pool, dp.ring, false, nullptr, nullptr);
-    k_dispatch_timeslot<false><<<n_pools, kDispThreads, no_ring, st>>>(
-        q, a, in, pool_begin, perm, pool_offsets, dp, rows, cand, row_count, admitted_count,
-        pool_status);
+    const DispLayout no_ring = disp_layout(max_inst_per_pool, dp.ring, false);
+    k_dispatch_timeslot<false><<<n_pools, kDispThreads, no_ring.total, st>>>(
+        q, a, in, pool_begin, perm, pool_offsets, dp, no_ring, rows, cand, row_count,
+        admitted_count, pool_status);
   }
   KX_CHECK_LAUNCH();
 }
