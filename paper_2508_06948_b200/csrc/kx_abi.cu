@@ -52,7 +52,8 @@ __global__ void k_validate_queue(QueueDev q, int64_t n, int n_agents, int need_p
     if (a < 0 || a >= n_agents) e |= 1;
     const double x = q.app_start[i], y = q.queue_enter[i];
     if (x != x || y != y) e |= 2;
-    if (need_pure && q.pure_exec[i] != q.pure_exec[i]) e |= 2;
+    if (need_pure && !(q.pure_exec[i] >= 0.0)) e |= 8;
+    if (q.prompt[i] < 0 || q.kept[i] < 0) e |= 8;
   }
   if (e) atomicOr(err, e);
 }
@@ -263,6 +264,7 @@ void check_err_flag(kx_sched* s, const char* what) {
   if (h & 1) fail(KX_ERR_INVALID, std::string(what) + ": agent index outside the agent table");
   if (h & 2) fail(KX_ERR_INVALID, std::string(what) + ": NaN time value");
   if (h & 4) fail(KX_ERR_INVALID, std::string(what) + ": parent link is not parents-first");
+  if (h & 8) fail(KX_ERR_INVALID, std::string(what) + ": negative token count or pure_exec");
 }
 
 void create_impl(const kx_sched_config* cfg, kx_sched** out) {
@@ -693,6 +695,8 @@ int kx_set_agent_tables(kx_sched* s, int32_t n_agents, const int32_t* agent_pool
       KX_CUDA(cudaStreamSynchronize(s->stream));
     }
     if (expected_T) {
+      for (size_t i = 0; i < A; ++i)
+        require(expected_T[i] >= 0.0, "expected execution time must be non-negative");
       KX_CUDA(cudaMemcpyAsync(s->a.T, expected_T, A * 8, cudaMemcpyHostToDevice, s->stream));
     } else if (s->n_agents != n_agents) {
       std::vector<double> dflt(A, s->dcfg.default_expected_time);

@@ -500,6 +500,296 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 
 #undef SM
 
+// ---- K5 fast path: pools of <= 32 instances ----------------------------------
+// Lanes = instances, warps = interleaved slot subsets (warp w owns absolute
+// slots s with s % kLaneWarps == w). Every warp keeps an identical register
+// copy of each lane-instance's live state (it is updated deterministically),
+// evaluates its slot subset for all instances at once, publishes per-instance
+// partial (first violating slot, peak) to shared memory, and after the single
+// barrier of the decision every warp combines the partials, computes the same
+// arg-min (REDUX), and books the target's slots of its own subset. Ledger
+// rings are staged transposed (usage[slot][instance]) so a warp's 32 lanes
+// read 32 consecutive words.
+constexpr int kLaneWarps = 4;
+constexpr int kLaneThreads = 32 * kLaneWarps;
+
+struct LaneLayout {
+  uint32_t part_viol, part_peak, h_T, h_prompt, h_kept, h_uid, h_agent, h_idx, h_first, h_last,
+      h_tend, usage, ex, total;
+};
+
+LaneLayout lane_layout(int ring) {
+  LaneLayout L{};
+  uint32_t o = 0;
+  auto take = [&](size_t bytes) {
+    const uint32_t at = o;
+    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
+    return at;
+  };
+  L.part_viol = take(4 * 2 * kLaneWarps * 32);
+  L.part_peak = take(8 * 2 * kLaneWarps * 32);
+  L.h_T = take(8 * kHeadBatch);
+  L.h_prompt = take(8 * kHeadBatch);
+  L.h_kept = take(8 * kHeadBatch);
+  L.h_uid = take(8 * kHeadBatch);
+  L.h_agent = take(4 * kHeadBatch);
+  L.h_idx = take(4 * kHeadBatch);
+  L.h_first = take(8 * kHeadBatch);
+  L.h_last = take(8 * kHeadBatch);
+  L.h_tend = take(8 * kHeadBatch);
+  L.usage = take(size_t(8) * 32 * ring);
+  L.ex = take(size_t(32) * ring);
+  L.total = o;
+  return L;
+}
+
+#define SL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
+
+__global__ void __launch_bounds__(kLaneThreads)
+k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
+                 const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
+                 DispatchParams dp, LaneLayout lay, kx_decision* __restrict__ rows,
+                 double* __restrict__ cand, int64_t* __restrict__ row_count,
+                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_status;
+  const int pool = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ib = pool_begin[pool];
+  const int ni = pool_begin[pool + 1] - ib;
+  const int ring = dp.ring;
+  const double now = dp.now;
+  const bool act = lane < ni;
+  const int i = ib + (act ? lane : 0);
+
+  // Per-lane instance state (identical copies in every warp).
+  const double cap = act ? in.cap[i] : 0.0;
+  const double kr = act ? in.decode_rate[i] : 0.0;
+  const int32_t mb = act ? in.max_batch[i] : 0;
+  const int32_t id = act ? in.id[i] : 0x7fffffff;
+  const int32_t waiting = act ? in.waiting[i] : 0;
+  double live = act ? in.live_kv[i] : 0.0;
+  int32_t running = act ? in.running[i] : 0;
+  bool susp = act ? in.suspended[i] != 0 : false;
+  int64_t base = act ? in.base_slot[i] : 0;
+  int64_t hi = act ? in.hi_slot[i] : -1;
+  // Common slot origin of the pool (bases are equal after any gc; the
+  // per-lane base still bounds what each instance retains).
+  const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
+
+  // Stage the rings transposed: usage[pos][lane].
+  double* su = SL(double, usage);
+  uint8_t* se = SL(uint8_t, ex);
+  for (int j = threadIdx.x; j < 32 * ring; j += kLaneThreads) {
+    const int li = j % 32, pos = j / 32;
+    const bool a = li < ni;
+    su[j] = a ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
+    se[j] = a ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+  }
+  if (threadIdx.x == 0) s_status = KX_OK;
+  __syncthreads();
+
+  const int64_t q_end = pool_offsets[pool + 1];
+  int64_t pos = pool_offsets[pool];
+  int64_t hb_start = pos, hb_n = 0;
+  int64_t nrows = 0, nadm = 0;
+  int retries = 0;
+  int par = 0;
+  const double t0e = __dadd_rn(now, kTimeEpsilon);
+  uint32_t* pv = SL(uint32_t, part_viol);
+  uint64_t* pp = SL(uint64_t, part_peak);
+
+  while (pos < q_end) {
+    if (pos >= hb_start + hb_n) {  // refill the head batch (prefix of the pool's order)
+      __syncthreads();
+      hb_start = pos;
+      hb_n = q_end - pos < kHeadBatch ? q_end - pos : kHeadBatch;
+      if (threadIdx.x < hb_n) {
+        const int t = threadIdx.x;
+        const uint32_t idx = perm[pos + t];
+        const int32_t a = q.agent[idx];
+        const double T = dp.oracle_T ? q.pure_exec[idx] : ag.T[a];
+        SL(uint32_t, h_idx)[t] = idx;
+        SL(int32_t, h_agent)[t] = a;
+        SL(int64_t, h_prompt)[t] = q.prompt[idx];
+        SL(int64_t, h_kept)[t] = q.kept[idx];
+        SL(uint64_t, h_uid)[t] = q.uid[idx];
+        SL(double, h_T)[t] = T;
+        int64_t f, l;
+        span_bounds_dev(now, T, dp.slot_len, &f, &l);
+        SL(int64_t, h_first)[t] = f;
+        SL(int64_t, h_last)[t] = l;
+        SL(double, h_tend)[t] = __dadd_rn(now, T);
+      }
+      __syncthreads();
+    }
+    const int h = static_cast<int>(pos - hb_start);
+    const int64_t prompt = SL(int64_t, h_prompt)[h];
+    const double P = static_cast<double>(prompt);
+    Span sp;
+    sp.first = SL(int64_t, h_first)[h];
+    sp.last = SL(int64_t, h_last)[h];
+    sp.t0 = now;
+    sp.t_end = SL(double, h_tend)[h];
+    sp.t0e = t0e;
+    sp.tee = __dsub_rn(sp.t_end, kTimeEpsilon);
+    const bool nonempty = sp.last >= sp.first;
+
+    // collect_live (engine.cpp:187-202): watermark resume, batch_full.
+    if (susp && live < __dmul_rn(dp.watermark, cap)) susp = false;
+    const bool full = running + waiting >= mb;
+    const bool eligible = act && !susp && !full;
+    const bool overflow = eligible && nonempty && (sp.first < base || sp.last >= base + ring);
+
+    // Partial try_place over this warp's slots: s = B + warp + kLaneWarps*m.
+    uint32_t viol = 0xffffffffu;
+    uint64_t peak = 0;  // raw bits: totals are non-negative (prompt >= 0, k > 0)
+    if (eligible) {
+      const int64_t smax = hi > sp.last ? hi : sp.last;
+      for (int64_t s = B + warp; s <= smax; s += kLaneWarps) {
+        if (s < base) continue;
+        const int p2 = static_cast<int>(s & (ring - 1));
+        const bool in_span = s >= sp.first && s <= sp.last;
+        const bool exists = se[p2 * 32 + lane] != 0;
+        if (!(in_span || exists)) continue;
+        const double used = exists ? su[p2 * 32 + lane] : 0.0;
+        const double total = __dadd_rn(used, pis(sp, P, kr, s, dp.slot_len));
+        if (in_span && total > cap) {
+          const uint32_t off = static_cast<uint32_t>(s - B);
+          viol = off < viol ? off : viol;
+        }
+        const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total));
+        peak = tb > peak ? tb : peak;
+      }
+    }
+    pv[(par * kLaneWarps + warp) * 32 + lane] = viol;
+    pp[(par * kLaneWarps + warp) * 32 + lane] = peak;
+    if (overflow) atomicExch(&s_status, KX_ERR_CAPACITY);
+    __syncthreads();
+    if (s_status != KX_OK) break;
+
+    // Combine the partials of all warps for this lane's instance.
+#pragma unroll
+    for (int w = 0; w < kLaneWarps; ++w) {
+      if (w == warp) continue;
+      const uint32_t v2 = pv[(par * kLaneWarps + w) * 32 + lane];
+      const uint64_t p2 = pp[(par * kLaneWarps + w) * 32 + lane];
+      viol = v2 < viol ? v2 : viol;
+      peak = p2 > peak ? p2 : peak;
+    }
+    const bool fits = eligible && viol == 0xffffffffu;
+    // select_instance: min (peak, InstanceId) (H9), all warps identically.
+    const uint64_t key = fits ? peak : ~0ull;
+    const uint64_t wkey = warp_min_u64(key);
+    const uint32_t uid_ = static_cast<uint32_t>(id) ^ 0x80000000u;
+    const uint32_t wid = __reduce_min_sync(0xffffffffu, (fits && key == wkey) ? uid_ : 0xffffffffu);
+    const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey && uid_ == wid);
+    const int bl = winners ? __ffs(winners) - 1 : -1;
+    const double bpeak = bl >= 0 ? __longlong_as_double(static_cast<long long>(wkey)) : 0.0;
+    const double blive = __shfl_sync(0xffffffffu, live, bl >= 0 ? bl : 0);
+    const double bcap = __shfl_sync(0xffffffffu, cap, bl >= 0 ? bl : 0);
+    const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
+    const int32_t bid = __shfl_sync(0xffffffffu, id, bl >= 0 ? bl : 0);
+
+    if (warp == 0) {  // decision log (engine.cpp:242-246)
+      if (nrows < dp.log_cap) {
+        const int64_t r = int64_t(pool) * dp.log_cap + nrows;
+        if (lane == 0) {
+          kx_decision d;
+          d.time = now;
+          d.predicted_peak = bpeak;
+          d.uid = SL(uint64_t, h_uid)[h];
+          d.queue_index = SL(uint32_t, h_idx)[h];
+          d.agent = SL(int32_t, h_agent)[h];
+          d.target = bl >= 0 ? bid : -1;
+          d.pool = pool;
+          d.admitted = (bl >= 0 && !overload) ? 1 : 0;
+          rows[r] = d;
+        }
+        if (act) {
+          double v = -1.0;
+          if (eligible) {
+            v = fits ? __longlong_as_double(static_cast<long long>(peak))
+                     : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
+          }
+          cand[r * dp.peak_stride + lane] = v;
+        }
+      }
+    }
+    ++nrows;
+    if (bl < 0) break;  // head keeps its place (engine.cpp:247)
+    if (overload) {
+      if (lane == bl) susp = true;  // Dispatcher::on_overload
+      if (++retries > ni) {
+        if (threadIdx.x == 0) s_status = KX_ERR_LIVELOCK;
+        break;
+      }
+      par ^= 1;
+      continue;
+    }
+    retries = 0;
+    // Dispatcher::commit: each warp books the target's span slots it owns.
+    {
+      const double kt = __shfl_sync(0xffffffffu, kr, bl);
+      const int64_t f0 = sp.first + ((((B + warp) - sp.first) % kLaneWarps) + kLaneWarps) % kLaneWarps;
+      for (int64_t s = f0 + int64_t(lane) * kLaneWarps; s <= sp.last; s += 32 * kLaneWarps) {
+        const int p2 = static_cast<int>(s & (ring - 1));
+        su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pis(sp, P, kt, s, dp.slot_len));
+        se[p2 * 32 + bl] = 1;
+      }
+      if (lane == bl) {
+        if (nonempty && sp.last > hi) hi = sp.last;
+        live = __dadd_rn(live, static_cast<double>(prompt + SL(int64_t, h_kept)[h]));  // admit
+        running += 1;
+      }
+      if (warp == 0 && lane == bl) {
+        q.admitted[SL(uint32_t, h_idx)[h]] = 1;
+        active_append(in, i, SL(uint64_t, h_uid)[h], P, kt, now, SL(double, h_T)[h], &s_status);
+      }
+    }
+    ++nadm;
+    ++pos;
+    par ^= 1;
+  }
+  __syncthreads();
+  // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
+  const int64_t current =
+      static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(now, kTimeEpsilon), dp.slot_len)));
+  if (act && current > base) {
+    const int64_t stop = current < base + ring ? current : base + ring;
+    for (int64_t s = base + warp; s < stop; s += kLaneWarps) {
+      const int p2 = static_cast<int>(s & (ring - 1));
+      su[p2 * 32 + lane] = 0.0;
+      se[p2 * 32 + lane] = 0;
+    }
+    base = current;
+  }
+  if (warp == 0 && act) active_gc(in, i, now);
+  __syncthreads();
+  if (warp == 0 && act) {
+    in.live_kv[i] = live;
+    in.base_slot[i] = base;
+    in.hi_slot[i] = hi;
+    in.running[i] = running;
+    in.suspended[i] = susp ? 1 : 0;
+  }
+  for (int j = threadIdx.x; j < 32 * ring; j += kLaneThreads) {
+    const int li = j % 32, p2 = j / 32;
+    if (li < ni) {
+      in.usage[int64_t(ib + li) * ring + p2] = su[j];
+      in.exists[int64_t(ib + li) * ring + p2] = se[j];
+    }
+  }
+  if (threadIdx.x == 0) {
+    row_count[pool] = nrows;
+    admitted_count[pool] = nadm;
+    pool_status[pool] = s_status;
+  }
+}
+
+#undef SL
+
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
 __global__ void k_ledger_try_place(InstDev in, int i, int ring, double P, double k, double t0,
                                    double T, double slot_len, double* out_peak, int64_t* out_viol,
@@ -615,6 +905,8 @@ __global__ void k_gc_all(InstDev in, int n_inst, int ring, double now, double sl
 
 // ---- host wrappers -------------------------------------------------------
 void configure_dispatch_kernels() {
+  KX_CUDA(cudaFuncSetAttribute(k_dispatch_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -626,6 +918,17 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      const DispatchParams& dp, int n_pools, int max_inst_per_pool, kx_decision* rows,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st) {
+  if (max_inst_per_pool <= 32) {
+    const LaneLayout ll = lane_layout(dp.ring);
+    if (ll.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+      k_dispatch_lanes<<<n_pools, kLaneThreads, ll.total, st>>>(q, a, in, pool_begin, perm,
+                                                               pool_offsets, dp, ll, rows, cand,
+                                                               row_count, admitted_count,
+                                                               pool_status);
+      KX_CHECK_LAUNCH();
+      return;
+    }
+  }
   const DispLayout with_ring = disp_layout(max_inst_per_pool, dp.ring, true);
   if (with_ring.total <= static_cast<uint32_t>(kDispSmemLimit)) {
     k_dispatch_timeslot<true><<<n_pools, kDispThreads, with_ring.total, st>>>(

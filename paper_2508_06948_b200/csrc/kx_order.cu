@@ -154,28 +154,44 @@ __global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
       atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur + 1]), (unsigned long long)hi);
     }
   };
+  // Four independent elements per thread per iteration keep enough loads in
+  // flight to stream at HBM rate.
+  constexpr int U = 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int32_t ag = q.agent[i];
-    if (ag < 0 || ag >= op.n_agents) {
-      err |= 1;
-      continue;
+  for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    int32_t ags[U];
+    double ts[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      ags[u] = i < n ? q.agent[i] : -1;
+      ts[u] = i < n ? primary_time(q, op.policy, i) : 0.0;
     }
-    const double t = primary_time(q, op.policy, i);
-    if (t != t) {
-      err |= 2;
-      continue;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) continue;
+      const int32_t ag = ags[u];
+      if (ag < 0 || ag >= op.n_agents) {
+        err |= 1;
+        continue;
+      }
+      const double t = ts[u];
+      if (t != t) {
+        err |= 2;
+        continue;
+      }
+      const int32_t p = a.pool[ag];
+      const uint64_t bb = ordered_bits(t);
+      if (p != cur) {
+        flush();
+        cur = p;
+        lo = ~0ull;
+        hi = 0ull;
+      }
+      lo = bb < lo ? bb : lo;
+      hi = bb > hi ? bb : hi;
     }
-    const int32_t p = a.pool[ag];
-    const uint64_t b = ordered_bits(t);
-    if (p != cur) {
-      flush();
-      cur = p;
-      lo = ~0ull;
-      hi = 0ull;
-    }
-    lo = b < lo ? b : lo;
-    hi = b > hi ? b : hi;
   }
   flush();
   if (err) atomicOr(error_flags, err);
@@ -221,36 +237,48 @@ __global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
   const uint32_t qmax = (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
   int32_t cur_pool = -1;
   uint32_t cur_cnt = 0;
+  constexpr int U = 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    const bool valid = i < n;
-    uint32_t key = 0;
-    if (valid) {
-      const int32_t ag = q.agent[i];
-      const int32_t p = a.pool[ag];
-      const uint32_t cls = class_of(a, op.policy, ag);
-      const double t = primary_time(q, op.policy, i);
-      const PoolRange r = ranges[p];
-      // Monotone: (t - lo) and the product are correctly rounded, floor
-      // and the clamp are monotone, so t1 <= t2 implies q1 <= q2.
-      double x = __dmul_rn(__dsub_rn(t, r.lo), r.scale);
-      uint32_t qv;
-      if (!(x > 0.0)) qv = 0;
-      else if (x >= static_cast<double>(qmax)) qv = qmax;
-      else qv = static_cast<uint32_t>(x);
-      key = qv;
-      if (op.class_bits) key |= cls << op.q_bits;
-      if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
-      keys[i] = key;
-      if (p != cur_pool) {
-        if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
-        cur_pool = p;
-        cur_cnt = 0;
-      }
-      ++cur_cnt;
+  for (int64_t b0 = int64_t(blockIdx.x) * blockDim.x; b0 < n; b0 += U * stride) {
+    int32_t ags[U];
+    double ts[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + u * stride + threadIdx.x;
+      ags[u] = i < n ? q.agent[i] : 0;
+      ts[u] = i < n ? primary_time(q, op.policy, i) : 0.0;
     }
-    for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = b0 + u * stride + threadIdx.x;
+      const bool valid = i < n;
+      uint32_t key = 0;
+      if (valid) {
+        const int32_t ag = ags[u];
+        const int32_t p = a.pool[ag];
+        const uint32_t cls = class_of(a, op.policy, ag);
+        const PoolRange r = ranges[p];
+        // Monotone: (t - lo) and the product are correctly rounded, floor
+        // and the clamp are monotone, so t1 <= t2 implies q1 <= q2.
+        const double x = __dmul_rn(__dsub_rn(ts[u], r.lo), r.scale);
+        uint32_t qv;
+        if (!(x > 0.0)) qv = 0;
+        else if (x >= static_cast<double>(qmax)) qv = qmax;
+        else qv = static_cast<uint32_t>(x);
+        key = qv;
+        if (op.class_bits) key |= cls << op.q_bits;
+        if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+        keys[i] = key;
+        if (p != cur_pool) {
+          if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
+          cur_pool = p;
+          cur_cnt = 0;
+        }
+        ++cur_cnt;
+      }
+      // every lane reaches hist_add (warp-collective)
+      for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
+    }
   }
   if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
   __syncthreads();
@@ -508,7 +536,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     res.keys = ws.keys[0];
     return res;
   }
-  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 4));
+  const int grid = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, int64_t(sms) * 8));
   // reads agent (4 B) + primary time (8 B) per request
   P.begin("pool_range", N * 12.0, st);
   k_pool_range<<<grid, 256, sizeof(uint64_t) * 2 * op.n_pools, st>>>(q, a, op, n, ws.ranges,
