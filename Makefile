@@ -13,7 +13,9 @@ PKG      := paper_2508_06948_b200
 SRC      := $(PKG)/csrc
 OUT      := $(PKG)/_lib
 CU       := kx_abi kx_order kx_dispatch kx_orchestrator
-OBJS     := $(patsubst %,$(OUT)/obj/%.o,$(CU))
+CPP      := kx_workload
+OBJS     := $(patsubst %,$(OUT)/obj/%.o,$(CU)) $(patsubst %,$(OUT)/obj/%.cpp.o,$(CPP))
+CXXFLAGS := -std=c++20 -O2 -ffp-contract=off -fPIC -Wall -Wextra
 HDRS     := $(wildcard $(SRC)/*.cuh) include/kairos_b200.h
 
 .PHONY: all oracle sass clean
@@ -22,6 +24,10 @@ all: $(OUT)/libkairos_b200.so
 $(OUT)/obj/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OUT)/obj
 	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OUT)/obj/%.cpp.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OUT)/obj
+	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(OUT)/libkairos_b200.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart

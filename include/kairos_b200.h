@@ -236,6 +236,23 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 /* Kernels launched by this library (all handles) since load. */
 int64_t kx_launch_count(void);
 
+/* ---- workload synthesis (host) ------------------------------------------ */
+/* realize() (workload.cpp:319-372) for the built-in templates
+ * (workload.cpp:462-560); app_mask selects QA/RG/CG in that order
+ * (colocated_workload = all three). Agents are indexed in the order of
+ * kx_builtin_agent_name(0..9). Same seed -> the reference's realization. */
+enum kx_app_mask { KX_APPS_QA = 1, KX_APPS_RG = 2, KX_APPS_CG = 4 };
+typedef struct kx_realization kx_realization;
+const char* kx_builtin_agent_name(int32_t agent);
+int kx_realize_builtin(uint32_t app_mask, double rate, double duration, uint64_t seed,
+                       double prefill_rate, double decode_rate, kx_realization** out);
+int kx_realization_sizes(const kx_realization* r, int64_t* n_workflows, int64_t* n_calls);
+/* Any output may be NULL; wf_offsets has n_workflows + 1 entries. */
+int kx_realization_copy(const kx_realization* r, double* arrival, int32_t* app, int64_t* wf_offsets,
+                        int32_t* agent, int32_t* parent, int64_t* prompt, int64_t* target,
+                        double* pure_exec, double* remaining, uint64_t* uid);
+void kx_realization_free(kx_realization* r);
+
 /* ---- K1: orchestrator DP ------------------------------------------------ */
 /* finalize_instance (workload.cpp:292-315) for many workflow instances at
  * once: calls of workflow w are [wf_offsets[w], wf_offsets[w+1]), in node_id

@@ -608,9 +608,17 @@ void gen_dp(const std::string& dir, const std::string& name, const WorkloadConfi
   std::vector<int64_t> off{0}, prompt, target;
   std::vector<int32_t> parent;
   std::vector<uint64_t> uid;
-  std::vector<double> pure, rem, rem_map;
+  std::vector<double> pure, rem, rem_map, arrival;
+  std::vector<int32_t> builtin_agent;
+  const char* builtin[10] = {"Router", "Math", "Humanities", "Researcher", "Writer",
+                             "ProductManager", "Architect", "ProjectManager", "Engineer", "QAEngineer"};
   for (const auto& inst : real.instances) {
+    arrival.push_back(inst.arrival);
     for (const auto& c : inst.calls) {
+      int32_t bi = -1;
+      for (int a = 0; a < 10; ++a)
+        if (c.agent == builtin[a]) bi = a;
+      builtin_agent.push_back(bi);
       parent.push_back(c.parents.empty() ? -1 : c.parents[0]);
       prompt.push_back(c.prompt_tokens);
       target.push_back(c.target_tokens);
@@ -629,6 +637,8 @@ void gen_dp(const std::string& dir, const std::string& name, const WorkloadConfi
   k.f64("pure_exec", pure);
   k.f64("remaining_exec", rem);
   k.f64("remaining_by_uid", rem_map);
+  k.f64("arrival", arrival);
+  k.i32("builtin_agent", builtin_agent);
   k.scalar_f("prefill_rate", rates.prefill_rate);
   k.scalar_f("decode_rate", rates.decode_rate);
   k.write(dir + "/" + name);
@@ -748,6 +758,7 @@ int main(int argc, char** argv) {
   gen_dispatch(dir, "dispatch_preload.kxf", 12, 16, 6, 3000.0, 8, 120, 400.0, true);
   gen_dispatch(dir, "dispatch_overload.kxf", 13, 5, 64, 1000.0, 5, 80, 150.0, false);
   gen_dp(dir, "dp_colocated.kxf", colocated_workload(3.0, 400.0, 3), ReferenceRates{8000.0, 50.0}, 3);
+  gen_dp(dir, "dp_cg.kxf", cg_workload(2.0, 300.0, 11), ReferenceRates{6000.0, 40.0}, 11);
   {
     WorkloadConfig cfg;
     cfg.apps = {fan_app(6), qa_app()};

@@ -115,6 +115,12 @@ SIGNATURES = {
     "kx_profile_enable": (C.c_int, [_P, C.c_int32]),
     "kx_profile_read": (C.c_int, [_P, C.POINTER(kx_phase_stat), C.c_int32, C.POINTER(C.c_int32)]),
     "kx_launch_count": (C.c_int64, []),
+    "kx_builtin_agent_name": (C.c_char_p, [C.c_int32]),
+    "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
+                                     C.c_double, C.POINTER(_P)]),
+    "kx_realization_sizes": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "kx_realization_copy": (C.c_int, [_P] + [_P] * 10),
+    "kx_realization_free": (None, [_P]),
     "kx_orchestrator_dp": (C.c_int, [C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, C.c_uint64,
                                      _P, _P, _P, C.c_int32]),
     "kx_record_remaining": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, C.c_int32]),

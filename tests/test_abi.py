@@ -17,7 +17,7 @@ HEADER = ROOT / "include" / "kairos_b200.h"
 
 def declared_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(kx_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|void|const char\*)\s+(kx_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_abi():
