@@ -25,7 +25,7 @@ namespace kx {
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
-constexpr int kSortThreads = 512;
+constexpr int kSortThreads = 256;
 constexpr int kSortItems = 12;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 6144 elements
 constexpr uint32_t kFlagAgg = 1u << 30;
