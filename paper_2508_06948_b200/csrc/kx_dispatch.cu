@@ -574,6 +574,7 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   bool susp = act ? in.suspended[i] != 0 : false;
   int64_t base = act ? in.base_slot[i] : 0;
   int64_t hi = act ? in.hi_slot[i] : -1;
+  int32_t nact = act ? in.n_active[i] : 0;  // active_ size, kept in a register
   // Common slot origin of the pool (bases are equal after any gc; the
   // per-lane base still bounds what each instance retains).
   const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
@@ -763,9 +764,21 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         live = __dadd_rn(live, static_cast<double>(prompt + SL(int64_t, h_kept)[h]));  // admit
         running += 1;
       }
-      if (warp == 0 && lane == bl) {
-        q.admitted[SL(uint32_t, h_idx)[h]] = 1;
-        active_append(in, i, SL(uint64_t, h_uid)[h], P, kt, now, SL(double, h_T)[h], &s_status);
+      if (lane == bl) {
+        if (nact < kActiveCap) {
+          if (warp == 0) {  // active_[uid] = m (dispatcher.cpp:78): stores only
+            q.admitted[SL(uint32_t, h_idx)[h]] = 1;
+            const int64_t o = int64_t(i) * kActiveCap + nact;
+            in.act_uid[o] = SL(uint64_t, h_uid)[h];
+            in.act_P[o] = P;
+            in.act_k[o] = kt;
+            in.act_t0[o] = now;
+            in.act_T[o] = SL(double, h_T)[h];
+          }
+          ++nact;
+        } else if (warp == 0) {
+          s_status = KX_ERR_CAPACITY;
+        }
       }
     }
     ++nadm;
@@ -785,7 +798,10 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     }
     base = current;
   }
-  if (warp == 0 && act) active_gc(in, i, now);
+  if (warp == 0 && act) {
+    in.n_active[i] = nact;
+    active_gc(in, i, now);
+  }
   __syncthreads();
   if (warp == 0 && act) {
     in.live_kv[i] = live;
