@@ -12,6 +12,7 @@
 // scans (O(D*N) per round), which only makes the baseline faster.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 #include <map>
@@ -217,3 +218,140 @@ double kxref_pools_tick(void** pools, int n, double now, int threads) {
 }
 
 }  // extern "C"
+
+// ---- full replica simulation (tests of the device replica engine) -------
+// Runs the reference Simulator (engine.cpp:85-123) on a flattened
+// realization whose agents are the built-in template agents, exactly as
+// run_cell wires it (harness.cpp:104-150), and returns completion-order
+// records, counters and compute_metrics (metrics.cpp:13-88).
+#include "kairos/engine.hpp"
+#include "kairos/metrics.hpp"
+#include "kairos/workflow.hpp"
+
+namespace {
+const char* kBuiltin[10] = {"Router", "Math", "Humanities", "Researcher", "Writer",
+                            "ProductManager", "Architect", "ProjectManager", "Engineer", "QAEngineer"};
+}
+
+extern "C" int kxref_sim_run(
+    int64_t n_wf, const double* arrival, const int64_t* wf_off, const int32_t* agent,
+    const int32_t* parent, const int64_t* prompt, const int64_t* target, const double* pure,
+    const double* rem, const uint64_t* uid, int n_inst, const int32_t* ids, const double* caps,
+    const double* ks, const double* prefill, const int32_t* max_batch, int sched_kind,
+    int dispatch_policy, int oracle_T, double slot_len, double watermark, double static_threshold,
+    double default_T, double dispatch_period, double recompute_fraction, const int32_t* topo_depth,
+    uint64_t* c_uid, double* c_exec_start, double* c_exec_end, int32_t* c_instance,
+    double* c_first_enqueue, double* c_queue_seconds, int32_t* c_episodes, int32_t* c_preemptions,
+    int64_t* w_index, double* w_finish, int64_t* w_output_tokens, int64_t* w_calls,
+    double* scalars, int64_t* n_calls_done, int64_t* n_wf_done) {
+  try {
+    WorkloadRealization real;
+    for (int64_t w = 0; w < n_wf; ++w) {
+      PlannedInstance inst;
+      inst.msg_id = "m-" + std::to_string(w);
+      inst.arrival = arrival[w];
+      for (int64_t c = wf_off[w]; c < wf_off[w + 1]; ++c) {
+        PlannedCall pc;
+        pc.node_id = static_cast<int>(c - wf_off[w]);
+        pc.agent = kBuiltin[agent[c]];
+        if (parent[c] >= 0) pc.parents.push_back(parent[c]);
+        pc.prompt_tokens = prompt[c];
+        pc.target_tokens = target[c];
+        pc.pure_exec = pure[c];
+        pc.remaining_exec = rem[c];
+        pc.uid = uid[c];
+        real.remaining_by_uid[pc.uid] = rem[c];
+        inst.calls.push_back(pc);
+      }
+      inst.entry = inst.calls.empty() ? "" : inst.calls[0].agent;
+      real.total_calls += inst.calls.size();
+      real.instances.push_back(std::move(inst));
+    }
+    EngineConfig ecfg;
+    std::vector<InstanceId> vid;
+    std::vector<double> vcap, vk;
+    for (int i = 0; i < n_inst; ++i) {
+      InstanceProfile p;
+      p.id = ids[i];
+      p.capacity_tokens = caps[i];
+      p.decode_rate = ks[i];
+      p.prefill_rate = prefill[i];
+      p.max_batch = max_batch[i];
+      ecfg.instances.push_back(p);
+      vid.push_back(ids[i]);
+      vcap.push_back(caps[i]);
+      vk.push_back(ks[i]);
+    }
+    ecfg.dispatch_period = dispatch_period;
+    ecfg.recompute_fraction = recompute_fraction;
+    ecfg.default_expected_time = default_T;
+    DispatcherConfig dcfg;
+    dcfg.policy = static_cast<DispatchPolicy>(dispatch_policy);
+    dcfg.slot_len = slot_len;
+    dcfg.resume_watermark = watermark;
+    dcfg.static_threshold = static_threshold;
+    dcfg.default_expected_time = default_T;
+    dcfg.oracle_expected_time = oracle_T != 0;
+    std::map<AgentId, int> depths;
+    for (int a = 0; a < 10; ++a) depths[kBuiltin[a]] = topo_depth[a];
+    std::unique_ptr<SchedulerPolicy> sched;
+    switch (sched_kind) {
+      case 1: sched = std::make_unique<FcfsScheduler>(); break;
+      case 2: sched = std::make_unique<TopoDepthScheduler>(depths); break;
+      case 3: sched = std::make_unique<OracleScheduler>(&real.remaining_by_uid); break;
+      default: {
+        KairosSchedulerConfig kc;
+        sched = std::make_unique<KairosScheduler>(kc);
+      }
+    }
+    Dispatcher disp(dcfg, vid, vcap, vk);
+    LatencyProfiler profiler;
+    WorkflowAnalyzer analyzer;
+    Simulator sim(ecfg, real, *sched, disp, profiler, analyzer);
+    RunResult run = sim.run();
+    for (std::size_t j = 0; j < run.calls.size(); ++j) {
+      const auto& c = run.calls[j];
+      c_uid[j] = c.uid;
+      c_exec_start[j] = c.record.exec_start;
+      c_exec_end[j] = c.record.exec_end;
+      c_instance[j] = c.instance;
+      c_first_enqueue[j] = c.first_enqueue;
+      c_queue_seconds[j] = c.queue_seconds;
+      c_episodes[j] = c.episodes;
+      c_preemptions[j] = c.preemptions;
+    }
+    for (std::size_t j = 0; j < run.instances.size(); ++j) {
+      const auto& w = run.instances[j];
+      w_index[j] = std::stoll(w.msg_id.substr(2));
+      w_finish[j] = w.finish;
+      w_output_tokens[j] = w.output_tokens;
+      w_calls[j] = static_cast<int64_t>(w.calls);
+    }
+    *n_calls_done = static_cast<int64_t>(run.calls.size());
+    *n_wf_done = static_cast<int64_t>(run.instances.size());
+    const MetricsReport m = compute_metrics("x", 0, run);
+    const double s[] = {static_cast<double>(run.preemption_events),
+                        static_cast<double>(run.preempted_requests),
+                        run.wasted_kv_tokens,
+                        run.completed_kv_tokens,
+                        run.prefill_seconds,
+                        run.decode_seconds,
+                        static_cast<double>(run.total_events),
+                        run.end_time,
+                        m.mean_token_latency,
+                        m.p90_token_latency,
+                        m.p95_token_latency,
+                        m.p99_token_latency,
+                        m.mean_request_token_latency,
+                        m.mean_queueing_ratio,
+                        m.preemption_rate,
+                        m.wasted_memory_fraction,
+                        m.decode_time_fraction,
+                        m.total_queue_seconds};
+    for (std::size_t j = 0; j < sizeof(s) / sizeof(s[0]); ++j) scalars[j] = s[j];
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "kxref_sim_run: %s\n", e.what());
+    return 1;
+  }
+}

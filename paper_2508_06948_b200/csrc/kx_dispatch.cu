@@ -510,7 +510,7 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 // arg-min (REDUX), and books the target's slots of its own subset. Ledger
 // rings are staged transposed (usage[slot][instance]) so a warp's 32 lanes
 // read 32 consecutive words.
-constexpr int kLaneWarps = 8;
+constexpr int kLaneWarps = 4;
 constexpr int kLaneThreads = 32 * kLaneWarps;
 
 struct LaneLayout {
@@ -650,35 +650,35 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     uint32_t viol = 0xffffffffu;
     uint64_t peak = 0;  // raw bits: totals are non-negative (prompt >= 0, k > 0)
     {
-      const int64_t my_smax = eligible ? (hi > sp.last ? hi : sp.last) : B - 1;
-      const int64_t smax = static_cast<int64_t>(__reduce_max_sync(0xffffffffu,
-          static_cast<uint32_t>(my_smax - B + 1))) + B - 1;  // warp-uniform
-      const int64_t nslots = smax >= B + warp ? (smax - B - warp) / kLaneWarps + 1 : 0;
-      for (int64_t m0 = 0; m0 < nslots; m0 += 32) {
-        // lane j describes slot s_{m0+j}
-        const int64_t sj = B + warp + (m0 + lane) * kLaneWarps;
-        const double slot_start = __dmul_rn(static_cast<double>(sj), dp.slot_len);
+      // 32-bit slot offsets from the pool origin B (the ring spans < 2^31).
+      const int32_t lo_off = static_cast<int32_t>(base - B);
+      const int32_t first_off = static_cast<int32_t>(sp.first - B);
+      const int32_t last_off = static_cast<int32_t>(sp.last - B);
+      const int32_t my_top = eligible ? static_cast<int32_t>((hi > sp.last ? hi : sp.last) - B) : -1;
+      const int32_t top = static_cast<int32_t>(__reduce_max_sync(0xffffffffu, static_cast<uint32_t>(my_top + 1))) - 1;
+      const int32_t nslots = top >= warp ? (top - warp) / kLaneWarps + 1 : 0;
+      for (int32_t m0 = 0; m0 < nslots; m0 += 32) {
+        // lane j describes slot offset o_j = warp + kLaneWarps * (m0 + j)
+        const int32_t oj = warp + kLaneWarps * (m0 + lane);
+        const double slot_start = __dmul_rn(static_cast<double>(B + oj), dp.slot_len);
         const double slot_end = __dadd_rn(slot_start, dp.slot_len);
         const bool zero = slot_end <= sp.t0e || slot_start >= sp.tee;
         const double eval_t = (sp.t_end < slot_end) ? sp.t_end : slot_end;
         const double dtj = zero ? -1.0 : __dsub_rn(eval_t, sp.t0);  // dt >= 0 when not zero
-        const int cnt = static_cast<int>(nslots - m0 < 32 ? nslots - m0 : 32);
+        const int cnt = nslots - m0 < 32 ? nslots - m0 : 32;
 #pragma unroll 4
         for (int j = 0; j < cnt; ++j) {
-          const double dt = __shfl_sync(0xffffffffu, dtj, j);
-          const int64_t s = B + warp + (m0 + j) * kLaneWarps;
-          if (!eligible || s < base) continue;
-          const int p2 = static_cast<int>(s & (ring - 1));
-          const bool in_span = s >= sp.first && s <= sp.last;
+          const double dt = __shfl_sync(0xffffffffu, dtj, j);  // all lanes take part
+          const int32_t o = warp + kLaneWarps * (m0 + j);
+          if (!eligible || o < lo_off) continue;
+          const int p2 = static_cast<int>((B + o) & (ring - 1));
+          const bool in_span = o >= first_off && o <= last_off;
           const bool exists = se[p2 * 32 + lane] != 0;
           if (!(in_span || exists)) continue;
           const double used = exists ? su[p2 * 32 + lane] : 0.0;
           const double pk = dt < 0.0 ? 0.0 : __dadd_rn(P, __dmul_rn(kr, dt));
           const double total = __dadd_rn(used, pk);
-          if (in_span && total > cap) {
-            const uint32_t off = static_cast<uint32_t>(s - B);
-            viol = off < viol ? off : viol;
-          }
+          if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
           const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total));
           peak = tb > peak ? tb : peak;
         }
