@@ -236,6 +236,70 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 /* Kernels launched by this library (all handles) since load. */
 int64_t kx_launch_count(void);
 
+/* ---- K6: replica engine --------------------------------------------------- */
+/* Simulator::run (engine.cpp:85-486) for many independent replicas at once,
+ * one warp per replica: the (time, kind, seq) event order, continuous
+ * batching, per-token KV growth, preempt-with-recompute and the dispatch
+ * rounds of engine.cpp:204-296. Supported: FCFS / TopoDepth / Oracle
+ * scheduling with TimeSlot (oracle_expected_time), RoundRobin or
+ * StaticThreshold dispatch. */
+typedef struct kx_engine_config {
+  int32_t n_instances;
+  int32_t scheduler;              /* KX_SCHED_FCFS / TOPO / ORACLE */
+  const kx_instance* instances;   /* pool ignored */
+  kx_dispatcher_config dispatcher;
+  int32_t n_agents;
+  int32_t slot_ring;              /* 0 = 256 */
+  const int32_t* topo_depth;      /* per agent index (TopoDepthScheduler) */
+  double dispatch_period;         /* engine.hpp:35 (0.1) */
+  double recompute_fraction;      /* engine.hpp:36 (1.0) */
+  int32_t heap_capacity;          /* 0 = 1024 pending events per replica */
+  int32_t device;
+  uint64_t max_events;            /* 0 = 2e8 (engine.cpp:25) */
+} kx_engine_config;
+
+/* Replicas concatenated (host arrays). Replica r owns workflows
+ * [wf_base[r], wf_base[r+1]) in arrival order (msg ids "m-<local index>")
+ * and their calls [wf_offsets[w], wf_offsets[w+1]) in node order. */
+typedef struct kx_replica_batch {
+  int32_t n_replicas;
+  int32_t _pad;
+  const int64_t* wf_base;         /* [R+1] */
+  const double* arrival;          /* [W] */
+  const int64_t* wf_offsets;      /* [W+1] */
+  const int32_t* agent;           /* [C] agent index */
+  const int32_t* parent;          /* [C] parent node id, -1 = entry */
+  const int64_t* prompt_tokens;   /* [C] */
+  const int64_t* target_tokens;   /* [C] */
+  const double* pure_exec;        /* [C] */
+  const double* remaining;        /* [C] remaining_by_uid (Oracle key) */
+  const uint64_t* uid;            /* [C] */
+} kx_replica_batch;
+
+/* RunResult (engine.hpp:101-118), host arrays allocated by the caller; any
+ * pointer may be NULL. Completion-ordered arrays use each replica's own
+ * segment (calls: [wf_offsets[wf_base[r]], ...), workflows: [wf_base[r], ...)). */
+typedef struct kx_replica_results {
+  int64_t* call_order;            /* [C] completed call (global index), completion order */
+  double* exec_start;             /* [C] completion order */
+  double* exec_end;               /* [C] completion order */
+  int32_t* instance;              /* [C] completion order (instance index) */
+  double* first_enqueue;          /* [C] by call */
+  double* queue_seconds;          /* [C] by call */
+  int32_t* episodes;              /* [C] by call */
+  int32_t* preemptions;           /* [C] by call */
+  int64_t* wf_order;              /* [W] completed workflow (global index), completion order */
+  double* wf_finish;              /* [W] by workflow */
+  int64_t* wf_output_tokens;      /* [W] by workflow */
+  int32_t* wf_calls;              /* [W] by workflow */
+  double* scalars;                /* [R*8]: preemption_events, preempted_requests, wasted_kv,
+                                     completed_kv, prefill_seconds, decode_seconds, events, end_time */
+  int64_t* counts;                /* [R*4]: calls done, workflows done, status, events */
+} kx_replica_results;
+
+int kx_replicas_run(const kx_engine_config* cfg, const kx_replica_batch* batch,
+                    kx_replica_results* out, double* device_ms);
+
 /* ---- workload synthesis (host) ------------------------------------------ */
 /* realize() (workload.cpp:319-372) for the built-in templates
  * (workload.cpp:462-560); app_mask selects QA/RG/CG in that order

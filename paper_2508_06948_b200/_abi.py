@@ -70,6 +70,27 @@ class kx_decision(C.Structure):
                 ("pool", C.c_int32), ("admitted", C.c_int32)]
 
 
+class kx_engine_config(C.Structure):
+    _fields_ = [("n_instances", C.c_int32), ("scheduler", C.c_int32),
+                ("instances", C.POINTER(kx_instance)), ("dispatcher", kx_dispatcher_config),
+                ("n_agents", C.c_int32), ("slot_ring", C.c_int32), ("topo_depth", C.c_void_p),
+                ("dispatch_period", C.c_double), ("recompute_fraction", C.c_double),
+                ("heap_capacity", C.c_int32), ("device", C.c_int32), ("max_events", C.c_uint64)]
+
+
+class kx_replica_batch(C.Structure):
+    _fields_ = [("n_replicas", C.c_int32), ("_pad", C.c_int32)] + [
+        (n, C.c_void_p) for n in ["wf_base", "arrival", "wf_offsets", "agent", "parent",
+                                  "prompt_tokens", "target_tokens", "pure_exec", "remaining", "uid"]]
+
+
+class kx_replica_results(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in [
+        "call_order", "exec_start", "exec_end", "instance", "first_enqueue", "queue_seconds",
+        "episodes", "preemptions", "wf_order", "wf_finish", "wf_output_tokens", "wf_calls",
+        "scalars", "counts"]]
+
+
 class kx_phase_stat(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("total_ms", C.c_double), ("launches", C.c_int64),
                 ("alg_bytes", C.c_double)]
@@ -115,6 +136,8 @@ SIGNATURES = {
     "kx_profile_enable": (C.c_int, [_P, C.c_int32]),
     "kx_profile_read": (C.c_int, [_P, C.POINTER(kx_phase_stat), C.c_int32, C.POINTER(C.c_int32)]),
     "kx_launch_count": (C.c_int64, []),
+    "kx_replicas_run": (C.c_int, [C.POINTER(kx_engine_config), C.POINTER(kx_replica_batch),
+                                  C.POINTER(kx_replica_results), C.POINTER(C.c_double)]),
     "kx_builtin_agent_name": (C.c_char_p, [C.c_int32]),
     "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                      C.c_double, C.POINTER(_P)]),

@@ -16,6 +16,7 @@
 #include "../../include/kairos_b200.h"
 #include "kx_common.cuh"
 #include "kx_dispatch.cuh"
+#include "kx_engine.cuh"
 #include "kx_order.cuh"
 #include "kx_state.cuh"
 
@@ -603,6 +604,252 @@ int instance_index(const kx_sched* s, int32_t id) {
 
 }  // namespace
 
+namespace {
+
+// Order-preserving key of "m-<n>" (see MsgKeyer in kairos_b200.hpp).
+uint64_t msg_key_of(uint64_t n) {
+  char d[24];
+  int nd = 0;
+  do {
+    d[nd++] = static_cast<char>(n % 10);
+    n /= 10;
+  } while (n);
+  uint64_t k = 0;
+  for (int j = 0; j < 18; ++j) k = k * 11 + (j < nd ? static_cast<uint64_t>(d[nd - 1 - j]) + 1 : 0);
+  return k;
+}
+
+struct DevArena {
+  std::vector<void*> ptrs;
+  template <typename T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    KX_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* upload(const T* h, size_t n) {
+    T* d = alloc<T>(n);
+    if (n) KX_CUDA(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  ~DevArena() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, kx_replica_results* out,
+                       double* device_ms) {
+  require(cfg && b && out, "null argument");
+  require(cfg->n_instances >= 1 && cfg->n_instances <= 32 && cfg->instances,
+          "engine supports 1..32 instances per replica");
+  require(cfg->scheduler == KX_SCHED_FCFS || cfg->scheduler == KX_SCHED_TOPO ||
+              cfg->scheduler == KX_SCHED_ORACLE,
+          "replica engine supports the fcfs, topo_depth and oracle schedulers");
+  const auto& dc = cfg->dispatcher;
+  require(dc.policy >= 0 && dc.policy <= 2, "unknown dispatcher policy");
+  require(dc.policy != KX_DISPATCH_TIME_SLOT || dc.oracle_expected_time,
+          "time_slot dispatch in the replica engine needs oracle_expected_time");
+  require(dc.slot_len > 0.0, "slot_len must be positive");
+  require(b->n_replicas >= 1, "no replicas");
+  require(cfg->n_agents >= 1, "n_agents must be positive");
+  const int R = b->n_replicas;
+  const int64_t W = b->wf_base[R];
+  require(b->wf_base[0] == 0 && W >= 0, "wf_base must start at 0");
+  const int64_t C = b->wf_offsets[W];
+  require(b->wf_offsets[0] == 0 && C >= 0 && C < (int64_t(1) << 31), "bad wf_offsets");
+  int max_run = 1;
+  for (int i = 0; i < cfg->n_instances; ++i) {
+    const kx_instance& p = cfg->instances[i];
+    require(p.capacity_tokens > 0 && p.decode_rate > 0 && p.prefill_rate > 0 && p.max_batch >= 1,
+            "instance profile fields must be positive");
+    max_run = std::max(max_run, p.max_batch);
+  }
+  require(max_run <= 1024, "max_batch above 1024");
+  // Host-side derived arrays: call -> workflow, children CSR, msg keys.
+  std::vector<int64_t> call_base(R + 1);
+  std::vector<int32_t> call_wf(C), has_parent(C), child(C);
+  std::vector<int64_t> child_off(C + 1, 0);
+  std::vector<uint64_t> wf_msg(W);
+  for (int r = 0; r < R; ++r) {
+    require(b->wf_base[r + 1] >= b->wf_base[r], "wf_base must be non-decreasing");
+    call_base[r] = b->wf_offsets[b->wf_base[r]];
+    for (int64_t w = b->wf_base[r]; w < b->wf_base[r + 1]; ++w) {
+      wf_msg[w] = msg_key_of(static_cast<uint64_t>(w - b->wf_base[r]));
+      if (w > b->wf_base[r]) require(b->arrival[w] >= b->arrival[w - 1], "arrivals must be sorted");
+    }
+  }
+  call_base[R] = C;
+  double maxpeak = 0.0, maxcap = 0.0;
+  for (int i = 0; i < cfg->n_instances; ++i) maxcap = std::max(maxcap, cfg->instances[i].capacity_tokens);
+  for (int64_t w = 0; w < W; ++w) {
+    require(b->wf_offsets[w + 1] >= b->wf_offsets[w], "wf_offsets must be non-decreasing");
+    for (int64_t c = b->wf_offsets[w]; c < b->wf_offsets[w + 1]; ++c) {
+      const int32_t p = b->parent[c];
+      require(p >= -1 && p < c - b->wf_offsets[w], "parent link is not parents-first");
+      require(b->agent[c] >= 0 && b->agent[c] < cfg->n_agents, "agent index outside the agent table");
+      require(b->prompt_tokens[c] >= 0 && b->target_tokens[c] >= 1, "token counts out of range");
+      call_wf[c] = static_cast<int32_t>(w);
+      has_parent[c] = p >= 0;
+      if (p >= 0) child_off[b->wf_offsets[w] + p + 1] += 1;
+      maxpeak = std::max(maxpeak, static_cast<double>(b->prompt_tokens[c] + b->target_tokens[c]));
+    }
+  }
+  // Simulator's constructor check (engine.cpp:55-71).
+  require(maxpeak <= maxcap, "instance capacity below largest single-request peak");
+  for (int64_t c = 0; c < C; ++c) child_off[c + 1] += child_off[c];
+  {
+    std::vector<int64_t> cur(child_off.begin(), child_off.end() - 1);
+    for (int64_t c = 0; c < C; ++c) {  // node order within each parent's list
+      const int64_t w = call_wf[c];
+      const int32_t p = b->parent[c];
+      if (p >= 0) child[cur[b->wf_offsets[w] + p]++] = static_cast<int32_t>(c);
+    }
+  }
+  ensure_device(cfg->device);
+  DevArena A;
+  const int NI = cfg->n_instances;
+  std::vector<int32_t> iid(NI), imb(NI);
+  std::vector<double> icap(NI), ik(NI), ipf(NI);
+  for (int i = 0; i < NI; ++i) {
+    iid[i] = cfg->instances[i].id;
+    imb[i] = cfg->instances[i].max_batch;
+    icap[i] = cfg->instances[i].capacity_tokens;
+    ik[i] = cfg->instances[i].decode_rate;
+    ipf[i] = cfg->instances[i].prefill_rate;
+  }
+  std::vector<int32_t> depth(cfg->n_agents, 1);
+  if (cfg->topo_depth) depth.assign(cfg->topo_depth, cfg->topo_depth + cfg->n_agents);
+  EngineInputs in{};
+  in.wf_base = A.upload(b->wf_base, R + 1);
+  in.call_base = A.upload(call_base.data(), R + 1);
+  in.arrival = A.upload(b->arrival, W);
+  in.wf_msg = A.upload(wf_msg.data(), W);
+  in.wf_call = A.upload(b->wf_offsets, W + 1);
+  in.call_wf = A.upload(call_wf.data(), C);
+  in.agent = A.upload(b->agent, C);
+  in.has_parent = A.upload(has_parent.data(), C);
+  in.prompt = A.upload(b->prompt_tokens, C);
+  in.target = A.upload(b->target_tokens, C);
+  in.pure = A.upload(b->pure_exec, C);
+  in.rem = A.upload(b->remaining, C);
+  in.uid = A.upload(b->uid, C);
+  in.child_off = A.upload(child_off.data(), C + 1);
+  in.child = A.upload(child.data(), C);
+  in.depth = A.upload(depth.data(), depth.size());
+  in.inst_id = A.upload(iid.data(), NI);
+  in.cap = A.upload(icap.data(), NI);
+  in.k = A.upload(ik.data(), NI);
+  in.prefill = A.upload(ipf.data(), NI);
+  in.max_batch = A.upload(imb.data(), NI);
+  const int ring = cfg->slot_ring ? cfg->slot_ring : 256;
+  require(ring >= 64 && (ring & (ring - 1)) == 0, "slot_ring must be a power of two >= 64");
+  EngineState st{};
+  st.rem_parents = A.alloc<int32_t>(C);
+  st.enqueue_time = A.alloc<double>(C);
+  st.first_enqueue = A.alloc<double>(C);
+  st.queue_seconds = A.alloc<double>(C);
+  st.kept = A.alloc<int64_t>(C);
+  st.episodes = A.alloc<int32_t>(C);
+  st.preemptions = A.alloc<int32_t>(C);
+  st.epoch = A.alloc<uint32_t>(C);
+  st.ever_preempted = A.alloc<uint8_t>(C);
+  st.run_slot = A.alloc<int32_t>(C);
+  st.wf_remaining = A.alloc<int32_t>(W);
+  st.wf_finish = A.alloc<double>(W);
+  st.wf_tokens = A.alloc<int64_t>(W);
+  st.wf_ncalls = A.alloc<int32_t>(W);
+  st.queue = A.alloc<uint32_t>(C);
+  st.waiting = A.alloc<uint32_t>(C);
+  st.waiting_inst = A.alloc<int32_t>(C);
+  const size_t RI = size_t(R) * NI;
+  st.usage = A.alloc<double>(RI * ring);
+  st.ex = A.alloc<uint8_t>(RI * ring);
+  st.base = A.alloc<int64_t>(RI);
+  st.hi = A.alloc<int64_t>(RI);
+  st.n_active = A.alloc<int32_t>(RI);
+  st.act_uid = A.alloc<uint64_t>(RI * kActiveCap);
+  st.act_P = A.alloc<double>(RI * kActiveCap);
+  st.act_k = A.alloc<double>(RI * kActiveCap);
+  st.act_t0 = A.alloc<double>(RI * kActiveCap);
+  st.act_T = A.alloc<double>(RI * kActiveCap);
+  st.out_call = A.alloc<uint32_t>(C);
+  st.out_exec_start = A.alloc<double>(C);
+  st.out_exec_end = A.alloc<double>(C);
+  st.out_inst = A.alloc<int32_t>(C);
+  st.out_wf = A.alloc<int64_t>(W);
+  st.scalars = A.alloc<double>(size_t(R) * kEngineScalars);
+  st.counts = A.alloc<int64_t>(size_t(R) * 4);
+  EngineParams prm{};
+  prm.n_inst = NI;
+  prm.sched = cfg->scheduler;
+  prm.dpolicy = dc.policy;
+  prm.oracle_T = dc.oracle_expected_time;
+  prm.ring = ring;
+  prm.heap_cap = cfg->heap_capacity ? cfg->heap_capacity : 1024;
+  prm.max_run = max_run;
+  prm.slot_len = dc.slot_len;
+  prm.watermark = dc.resume_watermark;
+  prm.static_thr = dc.static_threshold;
+  prm.default_T = dc.default_expected_time;
+  prm.period = cfg->dispatch_period > 0.0 ? cfg->dispatch_period : 0.1;
+  prm.recompute = cfg->recompute_fraction;
+  prm.max_events = cfg->max_events ? cfg->max_events : 200000000ull;
+  require(engine_smem_bytes(prm) <= 200 * 1024, "heap_capacity x instances x max_batch exceeds shared memory");
+  cudaStream_t stm = nullptr;
+  KX_CUDA(cudaStreamCreateWithFlags(&stm, cudaStreamNonBlocking));
+  struct SG {
+    cudaStream_t s;
+    ~SG() { cudaStreamDestroy(s); }
+  } sg{stm};
+  cudaEvent_t e0, e1;
+  KX_CUDA(cudaEventCreate(&e0));
+  KX_CUDA(cudaEventCreate(&e1));
+  KX_CUDA(cudaEventRecord(e0, stm));
+  launch_replica_engine(prm, in, st, R, stm);
+  KX_CUDA(cudaEventRecord(e1, stm));
+  KX_CUDA(cudaStreamSynchronize(stm));
+  float ms = 0.f;
+  KX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (device_ms) *device_ms = ms;
+  std::vector<int64_t> counts(size_t(R) * 4);
+  KX_CUDA(cudaMemcpy(counts.data(), st.counts, counts.size() * 8, cudaMemcpyDeviceToHost));
+  auto down = [&](auto* h, const auto* d, size_t n) {
+    if (h && n) KX_CUDA(cudaMemcpy(h, d, n * sizeof(*h), cudaMemcpyDeviceToHost));
+  };
+  if (out->call_order) {
+    std::vector<uint32_t> oc(C);
+    down(oc.data(), st.out_call, C);
+    for (int64_t j = 0; j < C; ++j) out->call_order[j] = oc[j];
+  }
+  down(out->exec_start, st.out_exec_start, C);
+  down(out->exec_end, st.out_exec_end, C);
+  down(out->instance, st.out_inst, C);
+  down(out->first_enqueue, st.first_enqueue, C);
+  down(out->queue_seconds, st.queue_seconds, C);
+  down(out->episodes, st.episodes, C);
+  down(out->preemptions, st.preemptions, C);
+  down(out->wf_order, st.out_wf, W);
+  down(out->wf_finish, st.wf_finish, W);
+  down(out->wf_output_tokens, st.wf_tokens, W);
+  down(out->wf_calls, st.wf_ncalls, W);
+  down(out->scalars, st.scalars, size_t(R) * kEngineScalars);
+  if (out->counts) std::memcpy(out->counts, counts.data(), counts.size() * 8);
+  for (int r = 0; r < R; ++r) {
+    const int64_t status = counts[size_t(r) * 4 + 2];
+    if (status == KX_ERR_CAPACITY) fail(KX_ERR_CAPACITY, "replica " + std::to_string(r) + ": event heap / run slots / ledger ring capacity exceeded");
+    if (status == KX_ERR_RUNTIME) throw std::runtime_error("replica " + std::to_string(r) + ": event budget exhausted; simulation stuck?");
+    if (status == KX_ERR_LOGIC) throw std::logic_error("replica " + std::to_string(r) + ": event time ran backwards");
+    if (status == KX_ERR_LIVELOCK) fail(KX_ERR_LIVELOCK, "replica " + std::to_string(r) + ": overload/resume livelock");
+    if (status != KX_OK) fail(static_cast<int>(status), "replica " + std::to_string(r) + " failed");
+  }
+}
+
+}  // namespace
+
 // ===========================================================================
 extern "C" {
 
@@ -1163,6 +1410,11 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 }
 
 int64_t kx_launch_count(void) { return kx::g_kx_launches.load(); }
+
+int kx_replicas_run(const kx_engine_config* cfg, const kx_replica_batch* batch, kx_replica_results* out,
+                    double* device_ms) {
+  return guard([&] { replicas_run_impl(cfg, batch, out, device_ms); });
+}
 
 int kx_orchestrator_dp(int64_t n_workflows, const int64_t* wf_offsets, const int32_t* parent,
                        const int64_t* prompt_tokens, const int64_t* target_tokens,

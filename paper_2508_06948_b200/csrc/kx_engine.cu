@@ -1,0 +1,763 @@
+// K6: the replica discrete-event engine, one warp per replica.
+//
+// Replays Simulator::run (engine.cpp:85-486) for many independent
+// replicas (load-trace cells, harness.cpp:166-216) at once. Each warp owns
+// one replica: its event heap lives in shared memory ordered by
+// (time, kind, seq) (engine.hpp:178-184); lane 0 performs the
+// sequential state changes and all lanes cooperate on the scans the
+// reference does in O(N) loops (ReadyQueue::best_index, select_instance over
+// instances, try_admit's waiting scan, the preemption victim arg-max).
+// Scalar replica state sits in shared memory, written by lane 0 and read by
+// every lane after __syncwarp, so control flow stays warp-uniform.
+//
+// Supported here: FCFS / TopoDepth / Oracle scheduling (scheduler.hpp:48-93)
+// with TimeSlot (oracle expected time, dispatcher.hpp:120), RoundRobin and
+// StaticThreshold dispatch. KairosScheduler's online table rebuilds
+// (W1 + MDS) and profile-based expected times are not on the device yet.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kx_common.cuh"
+#include "kx_engine.cuh"
+#include "kx_state.cuh"
+
+namespace kx {
+
+namespace {
+
+enum : int { EV_ARRIVAL = 0, EV_PREFILL = 1, EV_TOKEN = 2, EV_DONE = 3, EV_PREEMPT = 4, EV_ROUND = 5 };
+
+struct Ev {
+  double time;
+  uint64_t ks;  // kind << 56 | seq
+  uint32_t call;
+  int32_t inst;
+  uint32_t epoch;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ bool ev_less(const Ev& a, const Ev& b) {
+  return a.time < b.time || (a.time == b.time && a.ks < b.ks);
+}
+
+// Scalar replica state (shared memory, lane 0 writes).
+struct Scal {
+  double clock;
+  double prefill_seconds, decode_seconds, wasted_kv, completed_kv;
+  uint64_t next_seq, processed, preemption_events, preempted_requests;
+  int64_t next_arrival, arrivals_remaining, queue_n, waiting_n, calls_done, wf_done;
+  int32_t heap_n, round_pending, tick_scheduled, status;
+  int64_t rr_next;
+};
+
+struct RunSlot {  // RunningRequest (engine.hpp:137-145)
+  uint32_t call;
+  uint32_t epoch;
+  int64_t tokens;
+  int64_t kv;
+  double exec_start;
+  int32_t phase;  // 0 prefill, 1 decode
+  int32_t used;
+};
+
+struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_
+  double live_kv;
+  int32_t running;
+  int32_t waiting;
+  int32_t susp;
+  int32_t pad;
+  uint64_t preempted_total;
+};
+
+}  // namespace
+
+size_t engine_smem_bytes(const EngineParams& p) {
+  return sizeof(Scal) + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
+         sizeof(RunSlot) * size_t(p.n_inst) * size_t(p.max_run) + 64;
+}
+
+__global__ void __launch_bounds__(32, 16)
+k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Scal& sc = *reinterpret_cast<Scal*>(smem_raw);
+  Ev* heap = reinterpret_cast<Ev*>(smem_raw + sizeof(Scal));
+  InstS* ins = reinterpret_cast<InstS*>(heap + P.heap_cap);
+  RunSlot* runs = reinterpret_cast<RunSlot*>(ins + P.n_inst);
+
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int NI = P.n_inst;
+  const int64_t w0 = I.wf_base[r], w1 = I.wf_base[r + 1];
+  const int64_t c0 = I.call_base[r], c1 = I.call_base[r + 1];
+  const int ring = P.ring;
+  auto sync = [] { __syncwarp(); };
+
+  // ---- init --------------------------------------------------------------
+  if (lane == 0) {
+    sc = Scal{};
+    sc.next_seq = static_cast<uint64_t>(w1 - w0);  // arrivals took seq 0..n-1 (engine.cpp:86-89)
+    sc.next_arrival = w0;
+    sc.arrivals_remaining = w1 - w0;
+  }
+  for (int i = lane; i < NI; i += 32) ins[i] = InstS{};
+  for (int j = lane; j < NI * P.max_run; j += 32) runs[j].used = 0;
+  for (int64_t c = c0 + lane; c < c1; c += 32) {
+    S.first_enqueue[c] = -1.0;
+    S.queue_seconds[c] = 0.0;
+    S.kept[c] = 0;
+    S.episodes[c] = 0;
+    S.preemptions[c] = 0;
+    S.epoch[c] = 0;
+    S.ever_preempted[c] = 0;
+    S.run_slot[c] = -1;
+  }
+  const int64_t lb = int64_t(r) * NI;  // ledger / instance base of this replica
+  for (int64_t j = lane; j < int64_t(NI) * ring; j += 32) {
+    S.usage[lb * ring + j] = 0.0;
+    S.ex[lb * ring + j] = 0;
+  }
+  for (int i = lane; i < NI; i += 32) {
+    S.base[lb + i] = 0;
+    S.hi[lb + i] = -1;
+    S.n_active[lb + i] = 0;
+  }
+  sync();
+
+  // ---- helpers (uniform control flow; lane 0 writes) ------------------------
+  auto fail = [&](int code) {
+    if (lane == 0 && sc.status == KX_OK) sc.status = code;
+    sync();
+  };
+  auto push = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch) {
+    if (lane == 0) {
+      if (sc.heap_n >= P.heap_cap) {
+        sc.status = KX_ERR_CAPACITY;
+      } else {
+        Ev e{t, (uint64_t(kind) << 56) | sc.next_seq, call, inst, epoch, 0};
+        sc.next_seq += 1;
+        int k = sc.heap_n++;
+        while (k > 0) {
+          const int pk = (k - 1) >> 1;
+          if (!ev_less(e, heap[pk])) break;
+          heap[k] = heap[pk];
+          k = pk;
+        }
+        heap[k] = e;
+      }
+    }
+    sync();
+  };
+  auto pop_heap = [&]() {
+    if (lane == 0) {
+      const Ev last = heap[--sc.heap_n];
+      int k = 0;
+      const int n = sc.heap_n;
+      while (true) {
+        int c = 2 * k + 1;
+        if (c >= n) break;
+        if (c + 1 < n && ev_less(heap[c + 1], heap[c])) ++c;
+        if (!ev_less(heap[c], last)) break;
+        heap[k] = heap[c];
+        k = c;
+      }
+      if (n > 0) heap[k] = last;
+    }
+    sync();
+  };
+  auto schedule_round = [&](double t) {  // engine.cpp:79-83
+    if (sc.round_pending) return;
+    if (lane == 0) sc.round_pending = 1;
+    sync();
+    push(t, EV_ROUND, 0, -1, 0);
+  };
+  auto wf_of = [&](uint32_t c) { return I.call_wf[c]; };
+  auto enqueue_call = [&](uint32_t c, double now) {  // engine.cpp:162-175
+    if (lane == 0) {
+      S.queue[c0 + sc.queue_n] = c;
+      sc.queue_n += 1;
+      S.enqueue_time[c] = now;
+      if (S.first_enqueue[c] < 0.0) S.first_enqueue[c] = now;
+    }
+    sync();
+  };
+  // order_key (scheduler.hpp:48-93) -> tuple head (k0, k1, k2)
+  auto key0 = [&](uint32_t c) -> double {
+    switch (P.sched) {
+      case KX_SCHED_FCFS: return S.enqueue_time[c];
+      case KX_SCHED_TOPO: return static_cast<double>(I.depth[I.agent[c]]);
+      default: return I.rem[c];  // Oracle: remaining_by_uid holds every call
+    }
+  };
+  auto key1 = [&](uint32_t c) -> double {
+    return P.sched == KX_SCHED_FCFS ? I.arrival[wf_of(c)] : S.enqueue_time[c];
+  };
+  // ReadyQueue comparator (priority.hpp:95-98): (k0, k1, k2=0, app, qe, msg, uid)
+  struct Tup {
+    double k0, k1, app, qe;
+    uint64_t msg, uid;
+  };
+  auto tup = [&](uint32_t c) {
+    Tup t;
+    t.k0 = key0(c);
+    t.k1 = key1(c);
+    t.app = I.arrival[wf_of(c)];
+    t.qe = S.enqueue_time[c];
+    t.msg = I.wf_msg[wf_of(c)];
+    t.uid = I.uid[c];
+    return t;
+  };
+  auto tless = [](const Tup& a, const Tup& b) {
+    if (a.k0 != b.k0) return a.k0 < b.k0;
+    if (a.k1 != b.k1) return a.k1 < b.k1;
+    if (a.app != b.app) return a.app < b.app;
+    if (a.qe != b.qe) return a.qe < b.qe;
+    if (a.msg != b.msg) return a.msg < b.msg;
+    return a.uid < b.uid;
+  };
+  // try_admit comparator (engine.cpp:280-283): (k0, k1, k2=0, msg, uid) (H10)
+  auto wless = [](const Tup& a, const Tup& b) {
+    if (a.k0 != b.k0) return a.k0 < b.k0;
+    if (a.k1 != b.k1) return a.k1 < b.k1;
+    if (a.msg != b.msg) return a.msg < b.msg;
+    return a.uid < b.uid;
+  };
+  auto shfl_tup = [](Tup t, int src) {
+    Tup o;
+    o.k0 = __shfl_sync(0xffffffffu, t.k0, src);
+    o.k1 = __shfl_sync(0xffffffffu, t.k1, src);
+    o.app = __shfl_sync(0xffffffffu, t.app, src);
+    o.qe = __shfl_sync(0xffffffffu, t.qe, src);
+    o.msg = __shfl_sync(0xffffffffu, t.msg, src);
+    o.uid = __shfl_sync(0xffffffffu, t.uid, src);
+    return o;
+  };
+  // Warp arg-min over array entries [0, n) of `arr` (queue or waiting list)
+  // filtered by pred, under comparator `lt`. Returns the position or -1.
+  auto warp_argmin = [&](const uint32_t* arr, int64_t n, auto pred, auto lt) -> int64_t {
+    int64_t bpos = -1;
+    Tup bt{};
+    for (int64_t j = lane; j < n; j += 32) {
+      if (!pred(j)) continue;
+      const Tup t = tup(arr[j]);
+      if (bpos < 0 || lt(t, bt)) {
+        bt = t;
+        bpos = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const int src = lane ^ o;
+      const Tup ot = shfl_tup(bt, src);
+      const int64_t op = __shfl_sync(0xffffffffu, bpos, src);
+      if (op >= 0 && (bpos < 0 || lt(ot, bt))) {
+        bt = ot;
+        bpos = op;
+      }
+    }
+    return bpos;
+  };
+
+  // Slot ledger of instance i (dispatcher.cpp:44-123), global memory, owned by this warp.
+  auto ring_usage = [&](int i) { return S.usage + (lb + i) * ring; };
+  auto ring_ex = [&](int i) { return S.ex + (lb + i) * ring; };
+  // try_place, lanes over slots.
+  auto try_place = [&](int i, double Pt, double k, double t0, double T, int64_t* viol_out) -> double {
+    int64_t first, last;
+    span_bounds_dev(t0, T, P.slot_len, &first, &last);
+    const double t_end = __dadd_rn(t0, T);
+    const int64_t base = S.base[lb + i], hi = S.hi[lb + i];
+    if (last >= first && (first < base || last >= base + ring)) fail(KX_ERR_CAPACITY);
+    const double* u = ring_usage(i);
+    const uint8_t* ex = ring_ex(i);
+    const int64_t smax = hi > last ? hi : last;
+    double peak = 0.0;
+    int64_t viol = INT64_MAX;
+    const double cap = I.cap[i];
+    for (int64_t s = base + lane; s <= smax; s += 32) {
+      const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
+      const bool in_span = s >= first && s <= last;
+      const bool exists = ex[pos] != 0;
+      if (!(in_span || exists)) continue;
+      const double total = __dadd_rn(exists ? u[pos] : 0.0, peak_in_slot_dev(Pt, k, t0, t_end, s, P.slot_len));
+      if (in_span && total > cap && s < viol) viol = s;
+      peak = fmax(peak, total);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t v2 = __shfl_xor_sync(0xffffffffu, viol, o);
+      viol = v2 < viol ? v2 : viol;
+      peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    }
+    *viol_out = viol;
+    return peak;
+  };
+  auto commit = [&](int i, uint64_t uidv, double Pt, double k, double t0, double T) {
+    int64_t first, last;
+    span_bounds_dev(t0, T, P.slot_len, &first, &last);
+    const double t_end = __dadd_rn(t0, T);
+    double* u = ring_usage(i);
+    uint8_t* ex = ring_ex(i);
+    for (int64_t s = first + lane; s <= last; s += 32) {
+      const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
+      u[pos] = __dadd_rn(u[pos], peak_in_slot_dev(Pt, k, t0, t_end, s, P.slot_len));
+      ex[pos] = 1;
+    }
+    sync();
+    if (lane == 0) {
+      if (last >= first && last > S.hi[lb + i]) S.hi[lb + i] = last;
+      const int a = S.n_active[lb + i];
+      if (a >= kActiveCap) {
+        sc.status = KX_ERR_CAPACITY;
+      } else {
+        const int64_t o = (lb + i) * kActiveCap + a;
+        S.act_uid[o] = uidv;
+        S.act_P[o] = Pt;
+        S.act_k[o] = k;
+        S.act_t0[o] = t0;
+        S.act_T[o] = T;
+        S.n_active[lb + i] = a + 1;
+      }
+    }
+    sync();
+  };
+  auto finish_ledger = [&](int i, uint64_t uidv, double actual_end) {  // dispatcher.cpp:81-99,264-271
+    if (P.dpolicy != KX_DISPATCH_TIME_SLOT) return;
+    if (lane == 0) {
+      const int a = S.n_active[lb + i];
+      const int64_t o = (lb + i) * kActiveCap;
+      int j = 0;
+      for (; j < a; ++j)
+        if (S.act_uid[o + j] == uidv) break;
+      if (j < a) {
+        const double Pt = S.act_P[o + j], k = S.act_k[o + j], t0 = S.act_t0[o + j], T = S.act_T[o + j];
+        const double t_end = __dadd_rn(t0, T);
+        if (!(actual_end >= __dsub_rn(t_end, kTimeEpsilon))) {
+          const double from = actual_end > t0 ? actual_end : t0;
+          const int64_t cutoff = static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(from, kTimeEpsilon), P.slot_len)));
+          int64_t first, last;
+          span_bounds_dev(t0, T, P.slot_len, &first, &last);
+          double* u = ring_usage(i);
+          const uint8_t* ex = ring_ex(i);
+          const int64_t base = S.base[lb + i];
+          for (int64_t s = first; s <= last; ++s) {
+            if (s <= cutoff) continue;
+            const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
+            if (s < base || s >= base + ring || !ex[pos]) continue;
+            double v = __dsub_rn(u[pos], peak_in_slot_dev(Pt, k, t0, t_end, s, P.slot_len));
+            if (v < 1e-9) v = 0.0;
+            u[pos] = v;
+          }
+          S.act_T[o + j] = __dsub_rn(from, t0);
+        }
+      }
+    }
+    sync();
+  };
+  auto gc = [&](double now) {  // Dispatcher::gc (dispatcher.cpp:101-118, 295-297)
+    const int64_t current = static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(now, kTimeEpsilon), P.slot_len)));
+    for (int i = 0; i < NI; ++i) {
+      const int64_t base = S.base[lb + i];
+      if (current > base) {
+        const int64_t stop = current < base + ring ? current : base + ring;
+        double* u = ring_usage(i);
+        uint8_t* ex = ring_ex(i);
+        for (int64_t s = base + lane; s < stop; s += 32) {
+          const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
+          u[pos] = 0.0;
+          ex[pos] = 0;
+        }
+      }
+      sync();
+      if (lane == 0) {
+        if (current > base) S.base[lb + i] = current;
+        int a = S.n_active[lb + i];
+        const int64_t o = (lb + i) * kActiveCap;
+        const double lim = __dadd_rn(now, kTimeEpsilon);
+        for (int j = 0; j < a;) {
+          if (__dadd_rn(S.act_t0[o + j], S.act_T[o + j]) <= lim) {
+            --a;
+            S.act_uid[o + j] = S.act_uid[o + a];
+            S.act_P[o + j] = S.act_P[o + a];
+            S.act_k[o + j] = S.act_k[o + a];
+            S.act_t0[o + j] = S.act_t0[o + a];
+            S.act_T[o + j] = S.act_T[o + a];
+          } else {
+            ++j;
+          }
+        }
+        S.n_active[lb + i] = a;
+      }
+      sync();
+    }
+  };
+  auto on_live_usage = [&](int i) {  // dispatcher.cpp:283-289
+    if (lane == 0 && ins[i].susp && ins[i].live_kv < __dmul_rn(P.watermark, I.cap[i])) ins[i].susp = 0;
+    sync();
+  };
+  auto on_overload = [&](int i) {  // dispatcher.cpp:278-281
+    if (P.dpolicy != KX_DISPATCH_TIME_SLOT) return;
+    if (lane == 0) ins[i].susp = 1;
+    sync();
+  };
+  auto admit = [&](int i, uint32_t c) {  // engine.cpp:298-319
+    if (lane == 0) {
+      S.queue_seconds[c] = __dadd_rn(S.queue_seconds[c], __dsub_rn(sc.clock, S.enqueue_time[c]));
+      S.episodes[c] += 1;
+      int slot = -1;
+      for (int j = 0; j < P.max_run; ++j)
+        if (!runs[i * P.max_run + j].used) {
+          slot = j;
+          break;
+        }
+      if (slot < 0) {
+        sc.status = KX_ERR_CAPACITY;
+      } else {
+        RunSlot& rs = runs[i * P.max_run + slot];
+        rs.used = 1;
+        rs.call = c;
+        rs.tokens = S.kept[c];
+        rs.kv = I.prompt[c] + S.kept[c];
+        rs.phase = 0;
+        rs.exec_start = sc.clock;
+        S.epoch[c] += 1;
+        rs.epoch = S.epoch[c];
+        S.run_slot[c] = i * P.max_run + slot;
+        ins[i].live_kv = __dadd_rn(ins[i].live_kv, static_cast<double>(rs.kv));
+        ins[i].running += 1;
+      }
+    }
+    sync();
+    if (sc.status != KX_OK) return;
+    const double dur = __ddiv_rn(static_cast<double>(I.prompt[c]), I.prefill[i]);
+    if (lane == 0) sc.prefill_seconds = __dadd_rn(sc.prefill_seconds, dur);
+    sync();
+    push(__dadd_rn(sc.clock, dur), EV_PREFILL, c, i, S.epoch[c]);
+  };
+  auto try_admit = [&](int i) {  // engine.cpp:270-296
+    while (true) {
+      if (ins[i].waiting <= 0 || ins[i].running >= I.max_batch[i]) return;
+      const int64_t n = sc.waiting_n;
+      const int64_t pos = warp_argmin(S.waiting + c0, n, [&](int64_t j) { return S.waiting_inst[c0 + j] == i; }, wless);
+      if (pos < 0) return;
+      const uint32_t c = S.waiting[c0 + pos];
+      if (__dadd_rn(ins[i].live_kv, static_cast<double>(I.prompt[c])) > I.cap[i]) return;
+      if (lane == 0) {  // erase (order-free: the comparator is a total order)
+        const int64_t last = sc.waiting_n - 1;
+        S.waiting[c0 + pos] = S.waiting[c0 + last];
+        S.waiting_inst[c0 + pos] = S.waiting_inst[c0 + last];
+        sc.waiting_n = last;
+        ins[i].waiting -= 1;
+      }
+      sync();
+      admit(i, c);
+      if (sc.status != KX_OK) return;
+    }
+  };
+  auto dispatch_loop = [&]() {  // engine.cpp:220-268
+    int retries = 0;
+    while (sc.queue_n > 0 && sc.status == KX_OK) {
+      const int64_t qpos = warp_argmin(S.queue + c0, sc.queue_n, [](int64_t) { return true; }, tless);
+      const uint32_t head = S.queue[c0 + qpos];
+      const double T = P.oracle_T ? I.pure[head] : P.default_T;
+      // collect_live: watermark resume, then the live view.
+      for (int i = 0; i < NI; ++i) on_live_usage(i);
+      int target = -1;
+      if (P.dpolicy == KX_DISPATCH_ROUND_ROBIN) {
+        target = static_cast<int>(sc.rr_next % NI);
+        if (lane == 0) sc.rr_next += 1;
+        sync();
+      } else if (P.dpolicy == KX_DISPATCH_STATIC_THRESHOLD) {
+        for (int probe = 0; probe < NI; ++probe) {
+          const int i = static_cast<int>((sc.rr_next + probe) % NI);
+          const bool full = ins[i].running + ins[i].waiting >= I.max_batch[i];
+          if (ins[i].live_kv < __dmul_rn(P.static_thr, I.cap[i]) && !full) {
+            target = i;
+            break;
+          }
+        }
+        if (target >= 0) {
+          if (lane == 0) sc.rr_next = target + 1;
+          sync();
+        }
+      } else {
+        double best = 0.0;
+        for (int i = 0; i < NI; ++i) {
+          const bool full = ins[i].running + ins[i].waiting >= I.max_batch[i];
+          if (ins[i].susp || full) continue;
+          int64_t viol;
+          const double pk = try_place(i, static_cast<double>(I.prompt[head]), I.k[i], sc.clock, T, &viol);
+          if (sc.status != KX_OK) return;
+          if (viol != INT64_MAX) continue;
+          if (target < 0 || pk < best || (pk == best && I.inst_id[i] < I.inst_id[target])) {
+            best = pk;
+            target = i;
+          }
+        }
+      }
+      if (target < 0) break;  // engine.cpp:247
+      if (P.dpolicy == KX_DISPATCH_TIME_SLOT) {
+        if (__dadd_rn(ins[target].live_kv, static_cast<double>(I.prompt[head])) > I.cap[target]) {
+          on_overload(target);  // engine.cpp:254-258
+          if (++retries > NI) {  // the reference would spin forever here
+            fail(KX_ERR_LIVELOCK);
+            return;
+          }
+          continue;
+        }
+        if (lane == 0) {  // ReadyQueue::pop
+          const int64_t last = sc.queue_n - 1;
+          S.queue[c0 + qpos] = S.queue[c0 + last];
+          sc.queue_n = last;
+        }
+        sync();
+        retries = 0;
+        commit(target, I.uid[head], static_cast<double>(I.prompt[head]), I.k[target], sc.clock, T);
+        if (sc.status != KX_OK) return;
+        admit(target, head);
+      } else {
+        if (lane == 0) {
+          const int64_t last = sc.queue_n - 1;
+          S.queue[c0 + qpos] = S.queue[c0 + last];
+          sc.queue_n = last;
+          S.waiting[c0 + sc.waiting_n] = head;
+          S.waiting_inst[c0 + sc.waiting_n] = target;
+          sc.waiting_n += 1;
+          ins[target].waiting += 1;
+        }
+        sync();
+        try_admit(target);
+      }
+    }
+  };
+  auto work_pending = [&]() -> bool {  // engine.cpp:488-494
+    if (sc.arrivals_remaining > 0 || sc.queue_n > 0) return true;
+    for (int i = 0; i < NI; ++i)
+      if (ins[i].running > 0 || ins[i].waiting > 0) return true;
+    return false;
+  };
+  auto find_running = [&](const Ev& e) -> int {  // engine.cpp:321-332
+    const int rs = S.run_slot[e.call];
+    if (rs < 0 || rs / P.max_run != e.inst) return -1;
+    if (runs[rs].epoch != e.epoch) return -1;
+    return rs;
+  };
+  auto evict = [&](int i, int rs) {  // engine.cpp:464-486
+    const uint32_t c = runs[rs].call;
+    if (lane == 0) {
+      runs[rs].used = 0;
+      S.run_slot[c] = -1;
+      ins[i].running -= 1;
+      ins[i].live_kv = __dsub_rn(ins[i].live_kv, static_cast<double>(runs[rs].kv));
+      ins[i].preempted_total += 1;
+      sc.preemption_events += 1;
+      if (!S.ever_preempted[c]) {
+        S.ever_preempted[c] = 1;
+        sc.preempted_requests += 1;
+      }
+      sc.wasted_kv = __dadd_rn(sc.wasted_kv, static_cast<double>(runs[rs].kv));
+      S.preemptions[c] += 1;
+      S.epoch[c] += 1;
+      S.kept[c] = static_cast<int64_t>(floor(__dmul_rn(__dsub_rn(1.0, P.recompute), static_cast<double>(runs[rs].tokens))));
+    }
+    sync();
+    finish_ledger(i, I.uid[c], sc.clock);  // on_request_preempted
+    enqueue_call(c, sc.clock);
+  };
+
+  // ---- event loop (engine.cpp:85-123) ---------------------------------------
+  while (sc.status == KX_OK) {
+    // next event: heap top vs the next arrival (kind 0, seq = local index)
+    const bool have_arr = sc.next_arrival < w1;
+    const bool have_heap = sc.heap_n > 0;
+    if (!have_arr && !have_heap) break;
+    Ev ev;
+    bool from_heap = have_heap;
+    if (have_arr) {
+      Ev a{I.arrival[sc.next_arrival], static_cast<uint64_t>(sc.next_arrival - w0), 0, -1, 0, 0};
+      if (!have_heap || ev_less(a, heap[0])) {
+        ev = a;
+        from_heap = false;
+      }
+    }
+    if (from_heap) {
+      ev = heap[0];
+      pop_heap();
+    } else if (lane == 0) {
+      sc.next_arrival += 1;
+    }
+    sync();
+    if (ev.time < __dsub_rn(sc.clock, kTimeEpsilon)) {
+      fail(KX_ERR_LOGIC);  // event time ran backwards
+      break;
+    }
+    if (lane == 0) {
+      sc.clock = sc.clock > ev.time ? sc.clock : ev.time;
+      sc.processed += 1;
+      if (sc.processed > P.max_events) sc.status = KX_ERR_RUNTIME;  // event budget (engine.cpp:99-101)
+    }
+    sync();
+    if (sc.status != KX_OK) break;
+    const int kind = static_cast<int>(ev.ks >> 56);
+    const double clock = sc.clock;
+    if (kind == EV_ARRIVAL) {  // engine.cpp:137-160
+      const int64_t w = w0 + static_cast<int64_t>(ev.ks & ((uint64_t(1) << 56) - 1));
+      const int64_t cb = I.wf_call[w], ce = I.wf_call[w + 1];
+      for (int64_t c = cb + lane; c < ce; c += 32) S.rem_parents[c] = I.has_parent[c] ? 1 : 0;
+      if (lane == 0) {
+        S.wf_remaining[w] = static_cast<int32_t>(ce - cb);
+        S.wf_finish[w] = I.arrival[w];
+        S.wf_tokens[w] = 0;
+        S.wf_ncalls[w] = 0;
+      }
+      sync();
+      for (int64_t c = cb; c < ce; ++c)
+        if (!I.has_parent[c]) enqueue_call(static_cast<uint32_t>(c), clock);
+      if (lane == 0) sc.arrivals_remaining -= 1;
+      sync();
+      schedule_round(clock);
+    } else if (kind == EV_PREFILL) {  // engine.cpp:334-341
+      const int rs = find_running(ev);
+      if (rs < 0) continue;
+      if (lane == 0) runs[rs].phase = 1;
+      sync();
+      push(__dadd_rn(clock, __ddiv_rn(1.0, I.k[ev.inst])), EV_TOKEN, ev.call, ev.inst, ev.epoch);
+    } else if (kind == EV_TOKEN) {  // engine.cpp:343-361
+      const int rs = find_running(ev);
+      if (rs < 0) continue;
+      const int i = ev.inst;
+      const double step = __ddiv_rn(1.0, I.k[i]);
+      if (lane == 0) {
+        runs[rs].tokens += 1;
+        runs[rs].kv += 1;
+        ins[i].live_kv = __dadd_rn(ins[i].live_kv, 1.0);
+        sc.decode_seconds = __dadd_rn(sc.decode_seconds, step);
+      }
+      sync();
+      if (runs[rs].tokens >= I.target[ev.call]) push(clock, EV_DONE, ev.call, i, ev.epoch);
+      else push(__dadd_rn(clock, step), EV_TOKEN, ev.call, i, ev.epoch);
+      if (ins[i].live_kv > I.cap[i]) push(clock, EV_PREEMPT, 0, i, 0);
+    } else if (kind == EV_DONE) {  // engine.cpp:363-409
+      const int rs = find_running(ev);
+      if (rs < 0) continue;
+      const int i = ev.inst;
+      const uint32_t c = ev.call;
+      const int64_t w = wf_of(c);
+      if (lane == 0) {
+        runs[rs].used = 0;
+        S.run_slot[c] = -1;
+        ins[i].running -= 1;
+        ins[i].live_kv = __dsub_rn(ins[i].live_kv, static_cast<double>(runs[rs].kv));
+        sc.completed_kv = __dadd_rn(sc.completed_kv, static_cast<double>(runs[rs].kv));
+        const int64_t j = c0 + sc.calls_done;  // completion-order call record
+        S.out_call[j] = c;
+        S.out_exec_start[j] = runs[rs].exec_start;
+        S.out_exec_end[j] = clock;
+        S.out_inst[j] = i;
+        sc.calls_done += 1;
+        S.wf_finish[w] = S.wf_finish[w] > clock ? S.wf_finish[w] : clock;
+        S.wf_tokens[w] += I.target[c];
+        S.wf_ncalls[w] += 1;
+        S.wf_remaining[w] -= 1;
+      }
+      sync();
+      finish_ledger(i, I.uid[c], clock);
+      on_live_usage(i);
+      for (int64_t j = I.child_off[c]; j < I.child_off[c + 1]; ++j) {  // children in node order
+        const uint32_t ch = static_cast<uint32_t>(I.child[j]);
+        if (lane == 0) S.rem_parents[ch] -= 1;
+        sync();
+        if (S.rem_parents[ch] == 0) enqueue_call(ch, clock);
+      }
+      if (S.wf_remaining[w] == 0) {  // on_workflow_complete (engine.cpp:411-427)
+        if (lane == 0) {
+          S.out_wf[w0 + sc.wf_done] = w;
+          sc.wf_done += 1;
+        }
+        sync();
+      }
+      try_admit(i);
+      schedule_round(clock);
+    } else if (kind == EV_PREEMPT) {  // engine.cpp:436-462
+      const int i = ev.inst;
+      bool evicted = false;
+      while (ins[i].live_kv > I.cap[i] && ins[i].running > 0 && sc.status == KX_OK) {
+        // victim: max (victim_rank(agent), exec_start, uid) over running
+        double br = -1.0, bs = -1.0;
+        uint64_t bu = 0;
+        int brs = -1;
+        for (int j = lane; j < P.max_run; j += 32) {
+          const RunSlot& x = runs[i * P.max_run + j];
+          if (!x.used) continue;
+          const double rank = P.sched == KX_SCHED_TOPO ? static_cast<double>(I.depth[I.agent[x.call]]) : 0.0;
+          const uint64_t u = I.uid[x.call];
+          if (brs < 0 || rank > br || (rank == br && (x.exec_start > bs || (x.exec_start == bs && u > bu)))) {
+            br = rank;
+            bs = x.exec_start;
+            bu = u;
+            brs = i * P.max_run + j;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double r2 = __shfl_xor_sync(0xffffffffu, br, o);
+          const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+          const uint64_t u2 = __shfl_xor_sync(0xffffffffu, bu, o);
+          const int k2 = __shfl_xor_sync(0xffffffffu, brs, o);
+          if (k2 >= 0 && (brs < 0 || r2 > br || (r2 == br && (s2 > bs || (s2 == bs && u2 > bu))))) {
+            br = r2;
+            bs = s2;
+            bu = u2;
+            brs = k2;
+          }
+        }
+        if (brs < 0) break;
+        evict(i, brs);
+        evicted = true;
+      }
+      if (evicted) {
+        on_overload(i);
+        on_live_usage(i);
+        schedule_round(clock);
+      }
+    } else {  // EV_ROUND, engine.cpp:204-218
+      if (lane == 0) {
+        if (ev.call == 1) sc.tick_scheduled = 0;
+        else sc.round_pending = 0;
+      }
+      sync();
+      dispatch_loop();
+      for (int i = 0; i < NI; ++i) try_admit(i);
+      if (P.dpolicy == KX_DISPATCH_TIME_SLOT) gc(clock);
+      if (work_pending() && !sc.tick_scheduled) {
+        if (lane == 0) sc.tick_scheduled = 1;
+        sync();
+        push(__dadd_rn(clock, P.period), EV_ROUND, 1, -1, 0);
+      }
+    }
+  }
+  sync();
+  if (lane == 0) {
+    double* o = S.scalars + int64_t(r) * kEngineScalars;
+    o[0] = static_cast<double>(sc.preemption_events);
+    o[1] = static_cast<double>(sc.preempted_requests);
+    o[2] = sc.wasted_kv;
+    o[3] = sc.completed_kv;
+    o[4] = sc.prefill_seconds;
+    o[5] = sc.decode_seconds;
+    o[6] = static_cast<double>(sc.processed);
+    o[7] = sc.clock;
+    int64_t* n = S.counts + int64_t(r) * 4;
+    n[0] = sc.calls_done;
+    n[1] = sc.wf_done;
+    n[2] = sc.status;
+    n[3] = static_cast<int64_t>(sc.processed);
+  }
+}
+
+void launch_replica_engine(const EngineParams& p, const EngineInputs& in, const EngineState& st,
+                           int n_replicas, cudaStream_t stream) {
+  const size_t smem = engine_smem_bytes(p);
+  KX_CUDA(cudaFuncSetAttribute(k_replica_engine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  k_replica_engine<<<n_replicas, 32, smem, stream>>>(p, in, st);
+  KX_CHECK_LAUNCH();
+}
+
+}  // namespace kx

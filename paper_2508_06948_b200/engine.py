@@ -1,0 +1,87 @@
+"""Replica sweeps on the device (K6): plumbing over kx_replicas_run and the
+host realize() restatement (kx_realize_builtin)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import check
+from .sched import DispatcherConfig, InstanceProfile
+
+APPS = {"qa": 1, "rg": 2, "cg": 4, "colocated": 7}
+SCALAR_NAMES = ["preemption_events", "preempted_requests", "wasted_kv_tokens", "completed_kv_tokens",
+                "prefill_seconds", "decode_seconds", "total_events", "end_time"]
+
+
+def realize(apps="colocated", rate=3.0, duration=720.0, seed=1, prefill_rate=8000.0, decode_rate=50.0):
+    """realize() (workload.cpp:319-372) for the built-in templates."""
+    lib = _abi.load()
+    r = C.c_void_p()
+    check(lib.kx_realize_builtin(APPS[apps] if isinstance(apps, str) else apps, rate, duration, seed,
+                                 prefill_rate, decode_rate, C.byref(r)))
+    nw, nc = C.c_int64(), C.c_int64()
+    lib.kx_realization_sizes(r, C.byref(nw), C.byref(nc))
+    out = dict(arrival=np.zeros(nw.value), app=np.zeros(nw.value, np.int32),
+               wf_offsets=np.zeros(nw.value + 1, np.int64), agent=np.zeros(nc.value, np.int32),
+               parent=np.zeros(nc.value, np.int32), prompt=np.zeros(nc.value, np.int64),
+               target=np.zeros(nc.value, np.int64), pure_exec=np.zeros(nc.value),
+               remaining=np.zeros(nc.value), uid=np.zeros(nc.value, np.uint64))
+    lib.kx_realization_copy(r, *[v.ctypes.data for v in out.values()])
+    lib.kx_realization_free(r)
+    return out
+
+
+def concat(reals):
+    """Concatenate per-replica realizations into one kx_replica_batch layout."""
+    wf_base = [0]
+    arrays = {k: [] for k in ["arrival", "agent", "parent", "prompt", "target", "pure_exec", "remaining", "uid"]}
+    offs = [np.zeros(1, np.int64)]
+    c_total = 0
+    for rz in reals:
+        wf_base.append(wf_base[-1] + len(rz["arrival"]))
+        for k in arrays:
+            arrays[k].append(rz[k])
+        offs.append(rz["wf_offsets"][1:] + c_total)
+        c_total += len(rz["agent"])
+    out = {k: np.ascontiguousarray(np.concatenate(v)) for k, v in arrays.items()}
+    out["wf_base"] = np.array(wf_base, np.int64)
+    out["wf_offsets"] = np.concatenate(offs).astype(np.int64)
+    return out
+
+
+def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
+                 dispatcher: DispatcherConfig | None = None, topo_depth=None, n_agents=10,
+                 dispatch_period=0.1, recompute_fraction=1.0, heap_capacity=0, device=0):
+    lib = _abi.load()
+    d = dispatcher or DispatcherConfig()
+    arr = (_abi.kx_instance * len(instances))()
+    for i, p in enumerate(instances):
+        arr[i] = _abi.kx_instance(p.id, 0, p.capacity_tokens, p.decode_rate, p.prefill_rate, p.max_batch, 0)
+    dc = _abi.kx_dispatcher_config(_abi.DISPATCH[d.policy], int(d.oracle_expected_time), d.slot_len,
+                                   d.resume_watermark, d.static_threshold, d.default_expected_time)
+    depth = np.ascontiguousarray(topo_depth if topo_depth is not None else np.ones(n_agents), np.int32)
+    cfg = _abi.kx_engine_config(len(instances), _abi.SCHED[scheduler], arr, dc, n_agents, 0,
+                                depth.ctypes.data, dispatch_period, recompute_fraction, heap_capacity,
+                                device, 0)
+    R = len(batch["wf_base"]) - 1
+    W = int(batch["wf_base"][-1])
+    Cn = len(batch["agent"])
+    cols = [np.ascontiguousarray(batch[k], dt) for k, dt in [
+        ("wf_base", np.int64), ("arrival", np.float64), ("wf_offsets", np.int64), ("agent", np.int32),
+        ("parent", np.int32), ("prompt", np.int64), ("target", np.int64), ("pure_exec", np.float64),
+        ("remaining", np.float64), ("uid", np.uint64)]]
+    b = _abi.kx_replica_batch(R, 0, *[c.ctypes.data for c in cols])
+    res = dict(call_order=np.zeros(Cn, np.int64), exec_start=np.zeros(Cn), exec_end=np.zeros(Cn),
+               instance=np.zeros(Cn, np.int32), first_enqueue=np.zeros(Cn), queue_seconds=np.zeros(Cn),
+               episodes=np.zeros(Cn, np.int32), preemptions=np.zeros(Cn, np.int32),
+               wf_order=np.zeros(W, np.int64), wf_finish=np.zeros(W), wf_output_tokens=np.zeros(W, np.int64),
+               wf_calls=np.zeros(W, np.int32), scalars=np.zeros(R * 8), counts=np.zeros(R * 4, np.int64))
+    out = _abi.kx_replica_results(*[v.ctypes.data for v in res.values()])
+    ms = C.c_double()
+    check(lib.kx_replicas_run(C.byref(cfg), C.byref(b), C.byref(out), C.byref(ms)))
+    res["device_ms"] = ms.value
+    res["scalars"] = res["scalars"].reshape(R, 8)
+    res["counts"] = res["counts"].reshape(R, 4)
+    return res
