@@ -510,7 +510,7 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 // arg-min (REDUX), and books the target's slots of its own subset. Ledger
 // rings are staged transposed (usage[slot][instance]) so a warp's 32 lanes
 // read 32 consecutive words.
-constexpr int kLaneWarps = 4;
+constexpr int kLaneWarps = 8;
 constexpr int kLaneThreads = 32 * kLaneWarps;
 
 struct LaneLayout {
