@@ -25,7 +25,7 @@ CASES = [
     ("qa", 3.0, 120.0, insts(4), "fcfs", DispatcherConfig("round_robin"), 1.0),
     ("colocated", 4.0, 150.0, insts(4), "fcfs", DispatcherConfig("time_slot", oracle_expected_time=True), 1.0),
     ("colocated", 6.0, 120.0, insts(3, cap=1500.0), "topo_depth", DispatcherConfig("static_threshold"), 1.0),
-    ("colocated", 8.0, 100.0, insts(4, cap=1400.0, mb=12), "oracle",
+    ("colocated", 8.0, 100.0, insts(4, cap=1800.0, mb=12), "oracle",
      DispatcherConfig("time_slot", oracle_expected_time=True), 0.5),
     ("cg", 3.0, 120.0, insts(2, cap=1400.0, mb=16), "fcfs", DispatcherConfig("round_robin"), 0.25),
 ]
@@ -62,6 +62,16 @@ def test_replica_engine_matches_reference_simulator(gpu_lib, case):
         one["prompt"], one["target"] = rz["prompt"], rz["target"]
         ref = ref_sim.run(one, inst, sched, disp, DEPTH, recompute=rf)
         compare(dev, ref, b, r, int(b["wf_offsets"][b["wf_base"][r]]), int(b["wf_base"][r]))
+
+
+def test_engine_reports_the_reference_livelock(gpu_lib):
+    # prompt (<= 240) > (1 - 0.85) * cap: the reference's dispatch_loop
+    # would suspend/resume the same instance forever.
+    b = E.concat([E.realize("colocated", 8.0, 100.0, 1)])
+    with pytest.raises(Exception) as e:
+        E.run_replicas(b, insts(4, cap=1400.0, mb=12), "oracle",
+                       DispatcherConfig("time_slot", oracle_expected_time=True))
+    assert getattr(e.value, "code", None) == 6
 
 
 def test_engine_rejects_unsupported_configs(gpu_lib):
