@@ -256,6 +256,7 @@ typedef struct kx_engine_config {
   int32_t heap_capacity;          /* 0 = 1024 pending events per replica */
   int32_t device;
   uint64_t max_events;            /* 0 = 2e8 (engine.cpp:25) */
+  double warmup_seconds;          /* MetricsOptions::warmup_seconds (metrics.hpp:21-25) */
 } kx_engine_config;
 
 /* Replicas concatenated (host arrays). Replica r owns workflows
@@ -295,7 +296,18 @@ typedef struct kx_replica_results {
   double* scalars;                /* [R*8]: preemption_events, preempted_requests, wasted_kv,
                                      completed_kv, prefill_seconds, decode_seconds, events, end_time */
   int64_t* counts;                /* [R*4]: calls done, workflows done, status, events */
+  /* K7, compute_metrics (metrics.cpp:13-88) per replica, computed on the
+   * device: [R*16] = instances, requests, mean / p90 / p95 / p99 token
+   * latency, mean request token latency, mean queueing ratio, preemption
+   * rate, preempted requests, preemption events, wasted memory fraction,
+   * total queue seconds, decode time fraction, sim end time, latency count */
+  double* metrics;
+  uint32_t* histogram;            /* [R*256] token-latency bins: floor((log2 x + 16) * 8) */
 } kx_replica_results;
+
+/* aggregate_metrics (metrics.cpp:90-123) over per-replica metric rows in
+ * replica order (host arithmetic on R rows of kx_replica_results.metrics). */
+int kx_aggregate_metrics(int32_t n_rows, const double* rows, double* out);
 
 int kx_replicas_run(const kx_engine_config* cfg, const kx_replica_batch* batch,
                     kx_replica_results* out, double* device_ms);

@@ -75,7 +75,8 @@ class kx_engine_config(C.Structure):
                 ("instances", C.POINTER(kx_instance)), ("dispatcher", kx_dispatcher_config),
                 ("n_agents", C.c_int32), ("slot_ring", C.c_int32), ("topo_depth", C.c_void_p),
                 ("dispatch_period", C.c_double), ("recompute_fraction", C.c_double),
-                ("heap_capacity", C.c_int32), ("device", C.c_int32), ("max_events", C.c_uint64)]
+                ("heap_capacity", C.c_int32), ("device", C.c_int32), ("max_events", C.c_uint64),
+                ("warmup_seconds", C.c_double)]
 
 
 class kx_replica_batch(C.Structure):
@@ -88,7 +89,7 @@ class kx_replica_results(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in [
         "call_order", "exec_start", "exec_end", "instance", "first_enqueue", "queue_seconds",
         "episodes", "preemptions", "wf_order", "wf_finish", "wf_output_tokens", "wf_calls",
-        "scalars", "counts"]]
+        "scalars", "counts", "metrics", "histogram"]]
 
 
 class kx_phase_stat(C.Structure):
@@ -138,6 +139,7 @@ SIGNATURES = {
     "kx_launch_count": (C.c_int64, []),
     "kx_replicas_run": (C.c_int, [C.POINTER(kx_engine_config), C.POINTER(kx_replica_batch),
                                   C.POINTER(kx_replica_results), C.POINTER(C.c_double)]),
+    "kx_aggregate_metrics": (C.c_int, [C.c_int32, _P, _P]),
     "kx_builtin_agent_name": (C.c_char_p, [C.c_int32]),
     "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                      C.c_double, C.POINTER(_P)]),

@@ -808,6 +808,15 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   KX_CUDA(cudaEventCreate(&e1));
   KX_CUDA(cudaEventRecord(e0, stm));
   launch_replica_engine(prm, in, st, R, stm);
+  double* d_metrics = A.alloc<double>(size_t(R) * kEngineMetrics);
+  uint32_t* d_hist = A.alloc<uint32_t>(size_t(R) * kHistBins);
+  {
+    std::vector<int32_t> wf_rep(W);
+    for (int r = 0; r < R; ++r)
+      for (int64_t w = b->wf_base[r]; w < b->wf_base[r + 1]; ++w) wf_rep[w] = r;
+    const int32_t* d_rep = A.upload(wf_rep.data(), W);
+    launch_replica_metrics(in, st, d_rep, R, W, cfg->warmup_seconds, d_metrics, d_hist, stm);
+  }
   KX_CUDA(cudaEventRecord(e1, stm));
   KX_CUDA(cudaStreamSynchronize(stm));
   float ms = 0.f;
@@ -838,6 +847,8 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   down(out->wf_calls, st.wf_ncalls, W);
   down(out->scalars, st.scalars, size_t(R) * kEngineScalars);
   if (out->counts) std::memcpy(out->counts, counts.data(), counts.size() * 8);
+  down(out->metrics, d_metrics, size_t(R) * kEngineMetrics);
+  down(out->histogram, d_hist, size_t(R) * kHistBins);
   for (int r = 0; r < R; ++r) {
     const int64_t status = counts[size_t(r) * 4 + 2];
     if (status == KX_ERR_CAPACITY) fail(KX_ERR_CAPACITY, "replica " + std::to_string(r) + ": event heap / run slots / ledger ring capacity exceeded");
@@ -1410,6 +1421,28 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 }
 
 int64_t kx_launch_count(void) { return kx::g_kx_launches.load(); }
+
+int kx_aggregate_metrics(int32_t n_rows, const double* rows, double* out) {
+  return guard([&] {
+    require(n_rows >= 0 && (rows || n_rows == 0) && out, "null argument");
+    for (int k = 0; k < kEngineMetrics; ++k) out[k] = 0.0;
+    if (n_rows == 0) return;
+    // Sums for counts, plain means (accumulated as x / n in replica order,
+    // metrics.cpp:98-118) for the rates, max for the end time.
+    const double n = static_cast<double>(n_rows);
+    for (int r = 0; r < n_rows; ++r) {
+      const double* m = rows + int64_t(r) * kEngineMetrics;
+      out[0] += m[0];
+      out[1] += m[1];
+      for (int k : {2, 3, 4, 5, 6, 7, 8, 11, 13}) out[k] += m[k] / n;
+      out[9] += m[9];
+      out[10] += m[10];
+      out[12] += m[12];
+      out[14] = std::max(out[14], m[14]);
+      out[15] += m[15];
+    }
+  });
+}
 
 int kx_replicas_run(const kx_engine_config* cfg, const kx_replica_batch* batch, kx_replica_results* out,
                     double* device_ms) {

@@ -17,8 +17,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kx_common.cuh"
 #include "kx_engine.cuh"
+#include "kx_sortlib.cuh"
 #include "kx_state.cuh"
 
 namespace kx {
@@ -749,6 +752,169 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     n[2] = sc.status;
     n[3] = static_cast<int64_t>(sc.processed);
   }
+}
+
+__global__ void gather_rep(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ rep,
+                           uint32_t* __restrict__ out, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) out[j] = rep[idx[j]];
+}
+
+__global__ void gather_key(const uint64_t* __restrict__ k, const uint32_t* __restrict__ pos,
+                           uint64_t* __restrict__ out, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += stride) out[j] = k[pos[j]];
+}
+
+// ---- K7: per-replica metrics (metrics.cpp:13-88) ----------------------------
+// Token latency of each completed, measured workflow; excluded slots get
+// ~0 so they sort behind every valid latency of their replica.
+__global__ void k_token_latency(EngineInputs I, EngineState S, const int32_t* __restrict__ wf_rep,
+                                int64_t W, double warmup, uint64_t* __restrict__ key,
+                                uint32_t* __restrict__ rep) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < W; j += stride) {
+    const int r = wf_rep[j];
+    const int64_t w0 = I.wf_base[r];
+    const int64_t done = S.counts[int64_t(r) * 4 + 1];
+    uint64_t k = ~0ull;
+    if (j - w0 < done) {
+      const int64_t w = S.out_wf[j];
+      const double app = I.arrival[w];
+      const int64_t tok = S.wf_tokens[w];
+      if (app >= warmup && tok > 0) {
+        const double lat = __ddiv_rn(__dsub_rn(S.wf_finish[w], app), static_cast<double>(tok));
+        k = static_cast<uint64_t>(__double_as_longlong(lat));  // lat >= 0: raw bits are monotone
+      }
+    }
+    key[j] = k;
+    rep[j] = static_cast<uint32_t>(r);
+  }
+}
+
+__device__ double quantile_sorted_dev(const uint64_t* s, int64_t n, double p) {  // distribution.cpp:33-44
+  auto at = [&](int64_t i) { return __longlong_as_double(static_cast<long long>(s[i])); };
+  if (p <= 0.0) return at(0);
+  if (p >= 1.0) return at(n - 1);
+  const double pos = __dmul_rn(p, static_cast<double>(n - 1));
+  const int64_t lo = static_cast<int64_t>(pos);
+  const double frac = __dsub_rn(pos, static_cast<double>(lo));
+  if (lo + 1 >= n) return at(n - 1);
+  return __dadd_rn(at(lo), __dmul_rn(frac, __dsub_rn(at(lo + 1), at(lo))));
+}
+
+// One thread per replica: the sequential sums in the reference's order.
+__global__ void k_replica_metrics(EngineInputs I, EngineState S, int R, double warmup,
+                                  const uint64_t* __restrict__ sorted_lat, double* __restrict__ metrics,
+                                  uint32_t* __restrict__ hist) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int64_t w0 = I.wf_base[r];
+  const int64_t c0 = I.call_base[r];
+  const int64_t wf_done = S.counts[int64_t(r) * 4 + 1];
+  const int64_t calls_done = S.counts[int64_t(r) * 4 + 0];
+  const double* sc = S.scalars + int64_t(r) * kEngineScalars;
+  double* m = metrics + int64_t(r) * kEngineMetrics;
+  for (int k = 0; k < kEngineMetrics; ++k) m[k] = 0.0;
+  // measured instances: completed workflows with app_start >= warmup
+  int64_t measured = 0;
+  for (int64_t j = 0; j < wf_done; ++j)
+    if (I.arrival[S.out_wf[w0 + j]] >= warmup) ++measured;
+  // token latencies, ascending (sorted on the device beforehand)
+  const uint64_t* lat = sorted_lat + w0;
+  int64_t n = 0;
+  double sum = 0.0;
+  uint32_t* h = hist + int64_t(r) * kHistBins;
+  for (int b = 0; b < kHistBins; ++b) h[b] = 0;
+  while (n < (I.wf_base[r + 1] - w0) && lat[n] != ~0ull) {
+    const double v = __longlong_as_double(static_cast<long long>(lat[n]));
+    sum = __dadd_rn(sum, v);
+    const double lg = v > 0.0 ? log2(v) : -1.0e300;
+    int b = static_cast<int>(floor((lg + 16.0) * 8.0));
+    b = b < 0 ? 0 : (b >= kHistBins ? kHistBins - 1 : b);
+    h[b] += 1;
+    ++n;
+  }
+  m[0] = static_cast<double>(measured);
+  m[15] = static_cast<double>(n);
+  if (n > 0) {
+    m[2] = __ddiv_rn(sum, static_cast<double>(n));
+    m[3] = quantile_sorted_dev(lat, n, 0.90);
+    m[4] = quantile_sorted_dev(lat, n, 0.95);
+    m[5] = quantile_sorted_dev(lat, n, 0.99);
+  }
+  double queue_sum = 0.0, e2e_sum = 0.0, rtl_sum = 0.0;
+  int64_t requests = 0;
+  for (int64_t j = 0; j < calls_done; ++j) {
+    const uint32_t c = S.out_call[c0 + j];
+    const int32_t w = I.call_wf[c];
+    if (!(I.arrival[w] >= warmup) || S.wf_remaining[w] != 0) continue;
+    ++requests;
+    queue_sum = __dadd_rn(queue_sum, S.queue_seconds[c]);
+    const double e2e = __dsub_rn(S.out_exec_end[c0 + j], S.first_enqueue[c]);
+    e2e_sum = __dadd_rn(e2e_sum, e2e);
+    rtl_sum = __dadd_rn(rtl_sum, __ddiv_rn(e2e, static_cast<double>(I.target[c])));
+  }
+  m[1] = static_cast<double>(requests);
+  m[12] = queue_sum;
+  if (e2e_sum > 0.0) m[7] = __ddiv_rn(queue_sum, e2e_sum);
+  if (requests > 0) {
+    m[6] = __ddiv_rn(rtl_sum, static_cast<double>(requests));
+    m[8] = __ddiv_rn(sc[1], static_cast<double>(calls_done));
+  }
+  m[9] = sc[1];
+  m[10] = sc[0];
+  const double kv_total = __dadd_rn(sc[2], sc[3]);
+  if (kv_total > 0.0) m[11] = __ddiv_rn(sc[2], kv_total);
+  const double engine_time = __dadd_rn(sc[4], sc[5]);
+  if (engine_time > 0.0) m[13] = __ddiv_rn(sc[5], engine_time);
+  m[14] = sc[7];
+}
+
+void launch_replica_metrics(const EngineInputs& in, const EngineState& st, const int32_t* wf_rep,
+                            int R, int64_t W, double warmup, double* metrics, uint32_t* hist,
+                            cudaStream_t stream) {
+  uint64_t *key = nullptr, *key2 = nullptr;
+  uint32_t *rep = nullptr, *rep2 = nullptr, *val = nullptr, *val2 = nullptr;
+  const size_t n = static_cast<size_t>(W > 0 ? W : 1);
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&key), n * 8, stream));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&key2), n * 8, stream));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep), n * 4, stream));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep2), n * 4, stream));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&val), n * 4, stream));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&val2), n * 4, stream));
+  if (W > 0) {
+    k_token_latency<<<static_cast<int>(std::min<int64_t>((W + 255) / 256, 4096)), 256, 0, stream>>>(
+        in, st, wf_rep, W, warmup, key, rep);
+    KX_CHECK_LAUNCH();
+    // (1) all latencies ascending (stable), carrying their slot index
+    bool alt = false;
+    sort_pairs<uint64_t>(key, val, key2, val2, W, 0, 64, true, &alt, stream);
+    uint64_t* k1 = alt ? key2 : key;
+    uint32_t* v1 = alt ? val2 : val;
+    // (2) stable by replica: gather each element's replica, sort by it
+    uint64_t* kfin = alt ? key : key2;
+    gather_rep<<<static_cast<int>(std::min<int64_t>((W + 255) / 256, 4096)), 256, 0, stream>>>(
+        v1, rep, rep2, W);
+    KX_CHECK_LAUNCH();
+    int bits = 1;
+    while ((1 << bits) < R) ++bits;
+    bool alt2 = false;
+    // values = positions in the latency-sorted order
+    sort_pairs<uint32_t>(rep2, val, rep, val2, W, 0, bits, true, &alt2, stream);
+    uint32_t* pos = alt2 ? val2 : val;
+    gather_key<<<static_cast<int>(std::min<int64_t>((W + 255) / 256, 4096)), 256, 0, stream>>>(
+        k1, pos, kfin, W);
+    KX_CHECK_LAUNCH();
+    k_replica_metrics<<<(R + 127) / 128, 128, 0, stream>>>(in, st, R, warmup, kfin, metrics, hist);
+    KX_CHECK_LAUNCH();
+  }
+  KX_CUDA(cudaFreeAsync(key, stream));
+  KX_CUDA(cudaFreeAsync(key2, stream));
+  KX_CUDA(cudaFreeAsync(rep, stream));
+  KX_CUDA(cudaFreeAsync(rep2, stream));
+  KX_CUDA(cudaFreeAsync(val, stream));
+  KX_CUDA(cudaFreeAsync(val2, stream));
 }
 
 void launch_replica_engine(const EngineParams& p, const EngineInputs& in, const EngineState& st,

@@ -9,6 +9,8 @@
 namespace kx {
 
 constexpr int kEngineScalars = 8;
+constexpr int kEngineMetrics = 16;
+constexpr int kHistBins = 256;
 
 struct EngineParams {
   int32_t n_inst, sched, dpolicy, oracle_T, ring, heap_cap, max_run, pad;
@@ -86,5 +88,8 @@ struct EngineState {
 size_t engine_smem_bytes(const EngineParams& p);
 void launch_replica_engine(const EngineParams& p, const EngineInputs& in, const EngineState& st,
                            int n_replicas, cudaStream_t stream);
+void launch_replica_metrics(const EngineInputs& in, const EngineState& st, const int32_t* wf_rep,
+                            int R, int64_t W, double warmup, double* metrics, uint32_t* hist,
+                            cudaStream_t stream);
 
 }  // namespace kx

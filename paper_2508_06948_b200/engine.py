@@ -51,9 +51,16 @@ def concat(reals):
     return out
 
 
+METRIC_NAMES = ["instances", "requests", "mean_token_latency", "p90_token_latency", "p95_token_latency",
+                "p99_token_latency", "mean_request_token_latency", "mean_queueing_ratio", "preemption_rate",
+                "preempted_requests", "preemption_events", "wasted_memory_fraction", "total_queue_seconds",
+                "decode_time_fraction", "sim_end_time", "latency_count"]
+
+
 def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
                  dispatcher: DispatcherConfig | None = None, topo_depth=None, n_agents=10,
-                 dispatch_period=0.1, recompute_fraction=1.0, heap_capacity=0, device=0):
+                 dispatch_period=0.1, recompute_fraction=1.0, heap_capacity=0, device=0,
+                 warmup_seconds=0.0):
     lib = _abi.load()
     d = dispatcher or DispatcherConfig()
     arr = (_abi.kx_instance * len(instances))()
@@ -64,7 +71,7 @@ def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
     depth = np.ascontiguousarray(topo_depth if topo_depth is not None else np.ones(n_agents), np.int32)
     cfg = _abi.kx_engine_config(len(instances), _abi.SCHED[scheduler], arr, dc, n_agents, 0,
                                 depth.ctypes.data, dispatch_period, recompute_fraction, heap_capacity,
-                                device, 0)
+                                device, 0, warmup_seconds)
     R = len(batch["wf_base"]) - 1
     W = int(batch["wf_base"][-1])
     Cn = len(batch["agent"])
@@ -77,11 +84,23 @@ def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
                instance=np.zeros(Cn, np.int32), first_enqueue=np.zeros(Cn), queue_seconds=np.zeros(Cn),
                episodes=np.zeros(Cn, np.int32), preemptions=np.zeros(Cn, np.int32),
                wf_order=np.zeros(W, np.int64), wf_finish=np.zeros(W), wf_output_tokens=np.zeros(W, np.int64),
-               wf_calls=np.zeros(W, np.int32), scalars=np.zeros(R * 8), counts=np.zeros(R * 4, np.int64))
+               wf_calls=np.zeros(W, np.int32), scalars=np.zeros(R * 8), counts=np.zeros(R * 4, np.int64),
+               metrics=np.zeros(R * 16), histogram=np.zeros(R * 256, np.uint32))
     out = _abi.kx_replica_results(*[v.ctypes.data for v in res.values()])
     ms = C.c_double()
     check(lib.kx_replicas_run(C.byref(cfg), C.byref(b), C.byref(out), C.byref(ms)))
     res["device_ms"] = ms.value
     res["scalars"] = res["scalars"].reshape(R, 8)
     res["counts"] = res["counts"].reshape(R, 4)
+    res["metrics"] = res["metrics"].reshape(R, 16)
+    res["histogram"] = res["histogram"].reshape(R, 256)
     return res
+
+
+def aggregate(metrics_rows):
+    """aggregate_metrics (metrics.cpp:90-123) in replica order."""
+    lib = _abi.load()
+    rows = np.ascontiguousarray(metrics_rows, np.float64)
+    out = np.zeros(16)
+    check(lib.kx_aggregate_metrics(len(rows), rows.ctypes.data, out.ctypes.data))
+    return out

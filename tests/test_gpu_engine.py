@@ -49,6 +49,12 @@ def compare(dev, ref, b, r, c0, w0):
     assert np.array_equal(bits(dev["wf_finish"][wo]), bits(ref["wf_finish"][:nw]))
     assert np.array_equal(dev["wf_output_tokens"][wo], ref["wf_output_tokens"][:nw])
     assert np.array_equal(bits(dev["scalars"][r][:8]), bits(ref["scalars"][:8]))
+    # K7: compute_metrics on the device vs the reference (metrics.cpp:13-88)
+    m = dev["metrics"][r]
+    rs = ref["scalars"]
+    pairs = [(2, 8), (3, 9), (4, 10), (5, 11), (6, 12), (7, 13), (8, 14), (11, 15), (13, 16), (12, 17)]
+    for mi, ri in pairs:
+        assert bits(m[mi]) == bits(rs[ri]), (mi, m[mi], rs[ri])
 
 
 @pytest.mark.parametrize("case", range(len(CASES)))
