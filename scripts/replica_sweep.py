@@ -1,0 +1,145 @@
+#!/usr/bin/env python
+"""Replica sweep (config C5 shape): many independent load-trace replicas of
+the co-located QA+RG+CG workload simulated on the device (K6) with their
+metrics computed on the device (K7).
+
+Single GPU:   python scripts/replica_sweep.py --replicas 296 --duration 720
+Multi GPU:    torchrun --nproc-per-node N scripts/replica_sweep.py ...
+Replica r is simulated by rank r % N (weak scaling when --replicas scales
+with N); NCCL all-gathers each rank's per-replica metric rows and latency
+histograms; rank 0 aggregates them in replica order (aggregate_metrics,
+metrics.cpp:90-123) and prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2508_06948_b200 import DispatcherConfig, InstanceProfile  # noqa: E402
+from paper_2508_06948_b200 import engine as E  # noqa: E402
+
+DEPTH = np.array([2, 1, 1, 2, 1, 5, 4, 3, 2, 1], np.int32)  # topo_depths of the templates
+
+
+def instances(n=16):
+    return [InstanceProfile(id=i, capacity_tokens=3000.0, decode_rate=50.0, prefill_rate=8000.0,
+                            max_batch=8) for i in range(n)]
+
+
+def sweep(args, rank=0, ws=1, dev=0):
+    mine = list(range(rank, args.replicas, ws))
+    t0 = time.time()
+    reals = [E.realize("colocated", args.rate, args.duration, seed=1 + r) for r in mine]
+    b = E.concat(reals)
+    t_gen = time.time() - t0
+    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=args.dispatcher == "time_slot")
+    res = E.run_replicas(b, instances(args.instances), args.scheduler, disp, topo_depth=DEPTH,
+                         device=dev, warmup_seconds=args.warmup)
+    n_calls = int(res["counts"][:, 0].sum())
+    events = int(res["counts"][:, 3].sum())
+    return mine, res, n_calls, events, t_gen, b
+
+
+def cpu_reference(args, sample):
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ref_sim  # noqa: E402  (the reference Simulator via oracle/_ref/libkxref.so)
+    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=args.dispatcher == "time_slot")
+    reals = [E.realize("colocated", args.rate, args.duration, seed=1 + r) for r in range(sample)]
+    threads = min(sample, os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        outs = list(ex.map(lambda rz: ref_sim.run(rz, instances(args.instances), args.scheduler, disp, DEPTH),
+                           reals))
+    secs = time.perf_counter() - t0
+    calls = sum(int(o["n_calls"]) for o in outs)
+    return {"value": calls / secs, "unit": "simulated requests/s", "cores": threads, "kind": "reference",
+            "sample": f"{sample} replicas through the reference Simulator (engine.cpp:85-123), "
+                      f"{threads} threads, {calls} requests, {secs:.2f}s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--replicas", type=int, default=296)
+    ap.add_argument("--rate", type=float, default=12.0)
+    ap.add_argument("--duration", type=float, default=720.0)
+    ap.add_argument("--instances", type=int, default=16)
+    ap.add_argument("--scheduler", default="fcfs")
+    ap.add_argument("--dispatcher", default="time_slot")
+    ap.add_argument("--warmup", type=float, default=0.0)
+    ap.add_argument("--cpu-sample", type=int, default=16)
+    args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    if dist:
+        dist.barrier()
+    mine, res, n_calls, events, t_gen, b = sweep(args, rank, ws, local)
+    dev_ms = res["device_ms"]
+    # NCCL gather of metric rows and histograms (the only collective).
+    m = torch.from_numpy(res["metrics"]).cuda()
+    h = torch.from_numpy(res["histogram"].astype(np.int64)).cuda()
+    if dist:
+        R_loc = torch.tensor([m.shape[0]], device="cuda")
+        sizes = [torch.zeros_like(R_loc) for _ in range(ws)]
+        dist.all_gather(sizes, R_loc)
+        mx = int(max(s.item() for s in sizes))
+        pad_m = torch.zeros((mx, 16), dtype=m.dtype, device="cuda")
+        pad_m[:m.shape[0]] = m
+        pad_h = torch.zeros((mx, 256), dtype=h.dtype, device="cuda")
+        pad_h[:h.shape[0]] = h
+        gm = [torch.zeros_like(pad_m) for _ in range(ws)]
+        gh = [torch.zeros_like(pad_h) for _ in range(ws)]
+        dist.all_gather(gm, pad_m)
+        dist.all_gather(gh, pad_h)
+        t = torch.tensor([dev_ms, float(n_calls), float(events)], device="cuda", dtype=torch.float64)
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dev_ms = float(tmax[0].item())
+        n_calls = int(t[1].item())
+        events = int(t[2].item())
+        rows = np.zeros((args.replicas, 16))
+        hist = np.zeros(256, np.int64)
+        for k in range(ws):
+            idx = list(range(k, args.replicas, ws))
+            rows[idx] = gm[k][:len(idx)].cpu().numpy()
+            hist += gh[k][:len(idx)].sum(0).cpu().numpy()
+    else:
+        rows = res["metrics"]
+        hist = res["histogram"].sum(0)
+    if rank == 0:
+        agg = E.aggregate(rows)
+        cpu = cpu_reference(args, min(args.cpu_sample, args.replicas)) if ws == 1 and args.cpu_sample > 0 else None
+        print(json.dumps({
+            "metric": "simulated requests/s (replica sweep: DES + per-replica metrics on device)",
+            "value": n_calls / (dev_ms / 1e3), "unit": "simulated requests/s", "n_gpus": ws,
+            "replicas": args.replicas, "requests": n_calls, "events": events,
+            "events_per_s": events / (dev_ms / 1e3), "device_ms": dev_ms, "scaling": "weak",
+            "config": {"workload": f"colocated QA+RG+CG, rate {args.rate}/s for {args.duration}s per replica",
+                       "instances": args.instances, "scheduler": args.scheduler, "dispatcher": args.dispatcher},
+            "aggregate": dict(zip(E.METRIC_NAMES, [float(x) for x in agg])),
+            "histogram_total": int(hist.sum()),
+            "cpu_baseline": cpu, "host_realize_s": t_gen}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
