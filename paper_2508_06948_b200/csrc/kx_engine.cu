@@ -58,17 +58,19 @@ struct RunSlot {  // RunningRequest (engine.hpp:137-145)
   uint32_t epoch;
   int64_t tokens;
   int64_t kv;
+  int64_t target;  // plan->target_tokens, cached for the token ticks
   double exec_start;
   int32_t phase;  // 0 prefill, 1 decode
   int32_t used;
 };
 
-struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_
+struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_ + profile
   double live_kv;
+  double cap, k, step;  // capacity, decode rate, 1.0 / decode rate
   int32_t running;
   int32_t waiting;
   int32_t susp;
-  int32_t pad;
+  int32_t max_batch;
   uint64_t preempted_total;
 };
 
@@ -102,7 +104,13 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     sc.next_arrival = w0;
     sc.arrivals_remaining = w1 - w0;
   }
-  for (int i = lane; i < NI; i += 32) ins[i] = InstS{};
+  for (int i = lane; i < NI; i += 32) {
+    ins[i] = InstS{};
+    ins[i].cap = I.cap[i];
+    ins[i].k = I.k[i];
+    ins[i].step = __ddiv_rn(1.0, I.k[i]);
+    ins[i].max_batch = I.max_batch[i];
+  }
   for (int j = lane; j < NI * P.max_run; j += 32) runs[j].used = 0;
   for (int64_t c = c0 + lane; c < c1; c += 32) {
     S.first_enqueue[c] = -1.0;
@@ -274,7 +282,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     const int64_t smax = hi > last ? hi : last;
     double peak = 0.0;
     int64_t viol = INT64_MAX;
-    const double cap = I.cap[i];
+    const double cap = ins[i].cap;
     for (int64_t s = base + lane; s <= smax; s += 32) {
       const uint32_t pos = static_cast<uint32_t>(s) & (ring - 1);
       const bool in_span = s >= first && s <= last;
@@ -392,7 +400,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     }
   };
   auto on_live_usage = [&](int i) {  // dispatcher.cpp:283-289
-    if (lane == 0 && ins[i].susp && ins[i].live_kv < __dmul_rn(P.watermark, I.cap[i])) ins[i].susp = 0;
+    if (lane == 0 && ins[i].susp && ins[i].live_kv < __dmul_rn(P.watermark, ins[i].cap)) ins[i].susp = 0;
     sync();
   };
   auto on_overload = [&](int i) {  // dispatcher.cpp:278-281
@@ -416,6 +424,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         RunSlot& rs = runs[i * P.max_run + slot];
         rs.used = 1;
         rs.call = c;
+        rs.target = I.target[c];
         rs.tokens = S.kept[c];
         rs.kv = I.prompt[c] + S.kept[c];
         rs.phase = 0;
@@ -432,16 +441,18 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     const double dur = __ddiv_rn(static_cast<double>(I.prompt[c]), I.prefill[i]);
     if (lane == 0) sc.prefill_seconds = __dadd_rn(sc.prefill_seconds, dur);
     sync();
-    push(__dadd_rn(sc.clock, dur), EV_PREFILL, c, i, S.epoch[c]);
+    // events of a running request carry its run slot (find_running is a
+    // shared-memory check: slot in use, same call, same epoch)
+    push(__dadd_rn(sc.clock, dur), EV_PREFILL, c, S.run_slot[c], S.epoch[c]);
   };
   auto try_admit = [&](int i) {  // engine.cpp:270-296
     while (true) {
-      if (ins[i].waiting <= 0 || ins[i].running >= I.max_batch[i]) return;
+      if (ins[i].waiting <= 0 || ins[i].running >= ins[i].max_batch) return;
       const int64_t n = sc.waiting_n;
       const int64_t pos = warp_argmin(S.waiting + c0, n, [&](int64_t j) { return S.waiting_inst[c0 + j] == i; }, wless);
       if (pos < 0) return;
       const uint32_t c = S.waiting[c0 + pos];
-      if (__dadd_rn(ins[i].live_kv, static_cast<double>(I.prompt[c])) > I.cap[i]) return;
+      if (__dadd_rn(ins[i].live_kv, static_cast<double>(I.prompt[c])) > ins[i].cap) return;
       if (lane == 0) {  // erase (order-free: the comparator is a total order)
         const int64_t last = sc.waiting_n - 1;
         S.waiting[c0 + pos] = S.waiting[c0 + last];
@@ -470,8 +481,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       } else if (P.dpolicy == KX_DISPATCH_STATIC_THRESHOLD) {
         for (int probe = 0; probe < NI; ++probe) {
           const int i = static_cast<int>((sc.rr_next + probe) % NI);
-          const bool full = ins[i].running + ins[i].waiting >= I.max_batch[i];
-          if (ins[i].live_kv < __dmul_rn(P.static_thr, I.cap[i]) && !full) {
+          const bool full = ins[i].running + ins[i].waiting >= ins[i].max_batch;
+          if (ins[i].live_kv < __dmul_rn(P.static_thr, ins[i].cap) && !full) {
             target = i;
             break;
           }
@@ -483,10 +494,10 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       } else {
         double best = 0.0;
         for (int i = 0; i < NI; ++i) {
-          const bool full = ins[i].running + ins[i].waiting >= I.max_batch[i];
+          const bool full = ins[i].running + ins[i].waiting >= ins[i].max_batch;
           if (ins[i].susp || full) continue;
           int64_t viol;
-          const double pk = try_place(i, static_cast<double>(I.prompt[head]), I.k[i], sc.clock, T, &viol);
+          const double pk = try_place(i, static_cast<double>(I.prompt[head]), ins[i].k, sc.clock, T, &viol);
           if (sc.status != KX_OK) return;
           if (viol != INT64_MAX) continue;
           if (target < 0 || pk < best || (pk == best && I.inst_id[i] < I.inst_id[target])) {
@@ -497,7 +508,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       }
       if (target < 0) break;  // engine.cpp:247
       if (P.dpolicy == KX_DISPATCH_TIME_SLOT) {
-        if (__dadd_rn(ins[target].live_kv, static_cast<double>(I.prompt[head])) > I.cap[target]) {
+        if (__dadd_rn(ins[target].live_kv, static_cast<double>(I.prompt[head])) > ins[target].cap) {
           on_overload(target);  // engine.cpp:254-258
           if (++retries > NI) {  // the reference would spin forever here
             fail(KX_ERR_LIVELOCK);
@@ -512,7 +523,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         }
         sync();
         retries = 0;
-        commit(target, I.uid[head], static_cast<double>(I.prompt[head]), I.k[target], sc.clock, T);
+        commit(target, I.uid[head], static_cast<double>(I.prompt[head]), ins[target].k, sc.clock, T);
         if (sc.status != KX_OK) return;
         admit(target, head);
       } else {
@@ -537,10 +548,9 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     return false;
   };
   auto find_running = [&](const Ev& e) -> int {  // engine.cpp:321-332
-    const int rs = S.run_slot[e.call];
-    if (rs < 0 || rs / P.max_run != e.inst) return -1;
-    if (runs[rs].epoch != e.epoch) return -1;
-    return rs;
+    const RunSlot& x = runs[e.inst];
+    if (!x.used || x.call != e.call || x.epoch != e.epoch) return -1;
+    return e.inst;
   };
   auto evict = [&](int i, int rs) {  // engine.cpp:464-486
     const uint32_t c = runs[rs].call;
@@ -621,12 +631,12 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (rs < 0) continue;
       if (lane == 0) runs[rs].phase = 1;
       sync();
-      push(__dadd_rn(clock, __ddiv_rn(1.0, I.k[ev.inst])), EV_TOKEN, ev.call, ev.inst, ev.epoch);
+      push(__dadd_rn(clock, ins[rs / P.max_run].step), EV_TOKEN, ev.call, rs, ev.epoch);
     } else if (kind == EV_TOKEN) {  // engine.cpp:343-361
       const int rs = find_running(ev);
       if (rs < 0) continue;
-      const int i = ev.inst;
-      const double step = __ddiv_rn(1.0, I.k[i]);
+      const int i = rs / P.max_run;
+      const double step = ins[i].step;
       if (lane == 0) {
         runs[rs].tokens += 1;
         runs[rs].kv += 1;
@@ -634,13 +644,13 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         sc.decode_seconds = __dadd_rn(sc.decode_seconds, step);
       }
       sync();
-      if (runs[rs].tokens >= I.target[ev.call]) push(clock, EV_DONE, ev.call, i, ev.epoch);
-      else push(__dadd_rn(clock, step), EV_TOKEN, ev.call, i, ev.epoch);
-      if (ins[i].live_kv > I.cap[i]) push(clock, EV_PREEMPT, 0, i, 0);
+      if (runs[rs].tokens >= runs[rs].target) push(clock, EV_DONE, ev.call, rs, ev.epoch);
+      else push(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+      if (ins[i].live_kv > ins[i].cap) push(clock, EV_PREEMPT, 0, i, 0);
     } else if (kind == EV_DONE) {  // engine.cpp:363-409
       const int rs = find_running(ev);
       if (rs < 0) continue;
-      const int i = ev.inst;
+      const int i = rs / P.max_run;
       const uint32_t c = ev.call;
       const int64_t w = wf_of(c);
       if (lane == 0) {
@@ -681,7 +691,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     } else if (kind == EV_PREEMPT) {  // engine.cpp:436-462
       const int i = ev.inst;
       bool evicted = false;
-      while (ins[i].live_kv > I.cap[i] && ins[i].running > 0 && sc.status == KX_OK) {
+      while (ins[i].live_kv > ins[i].cap && ins[i].running > 0 && sc.status == KX_OK) {
         // victim: max (victim_rank(agent), exec_start, uid) over running
         double br = -1.0, bs = -1.0;
         uint64_t bu = 0;

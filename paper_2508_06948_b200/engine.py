@@ -104,3 +104,33 @@ def aggregate(metrics_rows):
     out = np.zeros(16)
     check(lib.kx_aggregate_metrics(len(rows), rows.ctypes.data, out.ctypes.data))
     return out
+
+
+def shard(n_replicas: int, rank: int, world: int) -> list[int]:
+    """Replica r runs on rank r % world (independent replicas: no exchange)."""
+    return list(range(rank, n_replicas, world))
+
+
+def gather_rows(dist, rows, hist, n_replicas: int, world: int, device):
+    """All-gather per-replica metric rows [R_local, 16] and latency
+    histograms [R_local, 256] (NCCL on CUDA tensors, gloo on CPU) and return
+    (rows in replica order [R, 16], summed histogram [256]) on every rank."""
+    import torch
+    m = torch.as_tensor(np.asarray(rows, np.float64), device=device)
+    h = torch.as_tensor(np.asarray(hist, np.int64), device=device)
+    mx = max(len(shard(n_replicas, k, world)) for k in range(world))
+    pm = torch.zeros((mx, 16), dtype=torch.float64, device=device)
+    ph = torch.zeros((mx, 256), dtype=torch.int64, device=device)
+    pm[:m.shape[0]] = m
+    ph[:h.shape[0]] = h
+    gm = [torch.zeros_like(pm) for _ in range(world)]
+    gh = [torch.zeros_like(ph) for _ in range(world)]
+    dist.all_gather(gm, pm)
+    dist.all_gather(gh, ph)
+    out = np.zeros((n_replicas, 16))
+    tot = np.zeros(256, np.int64)
+    for k in range(world):
+        idx = shard(n_replicas, k, world)
+        out[idx] = gm[k][:len(idx)].cpu().numpy()
+        tot += gh[k][:len(idx)].sum(0).cpu().numpy()
+    return out, tot

@@ -38,7 +38,7 @@ def instances(n=16):
 
 
 def sweep(args, rank=0, ws=1, dev=0):
-    mine = list(range(rank, args.replicas, ws))
+    mine = E.shard(args.replicas, rank, ws)
     t0 = time.time()
     reals = [E.realize("colocated", args.rate, args.duration, seed=1 + r) for r in mine]
     b = E.concat(reals)
@@ -93,21 +93,8 @@ def main():
     mine, res, n_calls, events, t_gen, b = sweep(args, rank, ws, local)
     dev_ms = res["device_ms"]
     # NCCL gather of metric rows and histograms (the only collective).
-    m = torch.from_numpy(res["metrics"]).cuda()
-    h = torch.from_numpy(res["histogram"].astype(np.int64)).cuda()
     if dist:
-        R_loc = torch.tensor([m.shape[0]], device="cuda")
-        sizes = [torch.zeros_like(R_loc) for _ in range(ws)]
-        dist.all_gather(sizes, R_loc)
-        mx = int(max(s.item() for s in sizes))
-        pad_m = torch.zeros((mx, 16), dtype=m.dtype, device="cuda")
-        pad_m[:m.shape[0]] = m
-        pad_h = torch.zeros((mx, 256), dtype=h.dtype, device="cuda")
-        pad_h[:h.shape[0]] = h
-        gm = [torch.zeros_like(pad_m) for _ in range(ws)]
-        gh = [torch.zeros_like(pad_h) for _ in range(ws)]
-        dist.all_gather(gm, pad_m)
-        dist.all_gather(gh, pad_h)
+        rows, hist = E.gather_rows(dist, res["metrics"], res["histogram"], args.replicas, ws, "cuda")
         t = torch.tensor([dev_ms, float(n_calls), float(events)], device="cuda", dtype=torch.float64)
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -115,12 +102,6 @@ def main():
         dev_ms = float(tmax[0].item())
         n_calls = int(t[1].item())
         events = int(t[2].item())
-        rows = np.zeros((args.replicas, 16))
-        hist = np.zeros(256, np.int64)
-        for k in range(ws):
-            idx = list(range(k, args.replicas, ws))
-            rows[idx] = gm[k][:len(idx)].cpu().numpy()
-            hist += gh[k][:len(idx)].sum(0).cpu().numpy()
     else:
         rows = res["metrics"]
         hist = res["histogram"].sum(0)
