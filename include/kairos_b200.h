@@ -312,6 +312,18 @@ int kx_aggregate_metrics(int32_t n_rows, const double* rows, double* out);
 int kx_replicas_run(const kx_engine_config* cfg, const kx_replica_batch* batch,
                     kx_replica_results* out, double* device_ms);
 
+/* ---- K8: pairwise sorting accuracy ---------------------------------------- */
+/* pairwise_sorting_accuracy (priority.cpp:165-189) of a schedule given in
+ * schedule order: agent[i], remaining[i] (true remaining latency) and
+ * present[i] (0 = uid absent from true_remaining, skipped; NULL = all).
+ * scope_all = 0: cross-agent pairs (PairScope::CrossAgent), 1: all pairs.
+ * Exact integer counting on the device in O(N log^2 N). *pairs = compared
+ * pairs, *correct = the reference's sum of 1.0 / 0.5 terms, *accuracy =
+ * correct / pairs, or NaN when pairs == 0 (the reference's nullopt). */
+int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining,
+                        const uint8_t* present, int32_t scope_all, uint64_t* pairs,
+                        double* correct, double* accuracy);
+
 /* ---- workload synthesis (host) ------------------------------------------ */
 /* realize() (workload.cpp:319-372) for the built-in templates
  * (workload.cpp:462-560); app_mask selects QA/RG/CG in that order

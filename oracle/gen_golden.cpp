@@ -747,6 +747,45 @@ void gen_remaining(const std::string& dir) {
   std::printf("  remaining.kxf, stats.kxf\n");
 }
 
+// ---- pairwise_sorting_accuracy (priority.cpp:165-189) -----------------------
+void gen_accuracy(const std::string& dir) {
+  Rng rng(99);
+  Kxf k;
+  std::vector<int64_t> off{0};
+  std::vector<int32_t> agent;
+  std::vector<double> rem, acc_cross, acc_all;
+  std::vector<uint8_t> present;
+  for (int t = 0; t < 40; ++t) {
+    const int n = 1 + static_cast<int>(rng.next_u64() % 400);
+    const int A = 1 + static_cast<int>(rng.next_u64() % 6);
+    std::vector<PendingRequest> order;
+    std::map<uint64_t, double> remaining;
+    for (int i = 0; i < n; ++i) {
+      const int a = static_cast<int>(rng.next_u64() % A);
+      order.push_back(req("m-" + std::to_string(i), "a" + std::to_string(a), 0, 0, i + 1));
+      const double v = (t % 3 == 0) ? std::floor(rng.uniform(0.0, 5.0)) : rng.uniform(0.0, 10.0);
+      const bool has = rng.uniform() < 0.9;
+      if (has) remaining[i + 1] = v;
+      agent.push_back(a);
+      rem.push_back(v);
+      present.push_back(has ? 1 : 0);
+    }
+    off.push_back(static_cast<int64_t>(agent.size()));
+    const auto c = pairwise_sorting_accuracy(order, remaining, PairScope::CrossAgent);
+    const auto a2 = pairwise_sorting_accuracy(order, remaining, PairScope::All);
+    acc_cross.push_back(c ? *c : std::nan(""));
+    acc_all.push_back(a2 ? *a2 : std::nan(""));
+  }
+  k.i64("offsets", off);
+  k.i32("agent", agent);
+  k.f64("remaining", rem);
+  k.u8("present", present);
+  k.f64("acc_cross", acc_cross);
+  k.f64("acc_all", acc_all);
+  k.write(dir + "/accuracy.kxf");
+  std::printf("  accuracy.kxf\n");
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -774,5 +813,6 @@ int main(int argc, char** argv) {
     gen_dp(dir, "dp_wide.kxf", cfg, ReferenceRates{8000.0, 50.0}, 4);
   }
   gen_remaining(dir);
+  gen_accuracy(dir);
   return 0;
 }

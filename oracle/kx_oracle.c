@@ -466,6 +466,27 @@ int64_t kxo_dispatch_round(kxo_pool* p, const kxo_queue* q, const kxo_tables* t,
   return nrows;
 }
 
+/* ---- pairwise_sorting_accuracy (priority.cpp:165-189) ------------------------ */
+int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,
+                          int32_t scope_all, double* acc, uint64_t* pairs_out) {
+  double correct = 0.0;
+  uint64_t pairs = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (present && !present[i]) continue;
+    for (int64_t j = i + 1; j < n; ++j) {
+      if (!scope_all && agent[i] == agent[j]) continue;
+      if (present && !present[j]) continue;
+      ++pairs;
+      if (rem[i] < rem[j]) correct += 1.0;
+      else if (rem[i] == rem[j]) correct += 0.5;
+    }
+  }
+  *pairs_out = pairs;
+  if (pairs == 0) return 1;
+  *acc = correct / (double)pairs;
+  return 0;
+}
+
 /* ---- finalize_instance (workload.cpp:292-315) -------------------------------- */
 int kxo_finalize(int64_t n_wf, const int64_t* off, const int32_t* parent, const int64_t* prompt,
                  const int64_t* target, double prefill_rate, double decode_rate, uint64_t uid_base,

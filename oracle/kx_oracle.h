@@ -107,6 +107,11 @@ int64_t kxo_dispatch_round(kxo_pool* p, const kxo_queue* q, const kxo_tables* t,
                            const uint32_t* perm, int64_t m, double now, int32_t pool_index,
                            kxo_decision* rows, double* cand, int64_t row_cap, int32_t* status);
 
+/* pairwise_sorting_accuracy (priority.cpp:165-189), O(N^2): returns 0 and
+ * sets *acc when pairs > 0, returns 1 (nullopt) otherwise. */
+int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,
+                          int32_t scope_all, double* acc, uint64_t* pairs_out);
+
 /* finalize_instance (workload.cpp:292-315) for many workflows. */
 int kxo_finalize(int64_t n_wf, const int64_t* off, const int32_t* parent, const int64_t* prompt,
                  const int64_t* target, double prefill_rate, double decode_rate, uint64_t uid_base,

@@ -22,6 +22,9 @@
 
 namespace kx {
 std::atomic<long long> g_kx_launches{0};
+void sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining, const uint8_t* present,
+                      int32_t scope_all, uint64_t* pairs_out, double* correct_out, int sms,
+                      cudaStream_t st);
 
 void launch_orchestrator_dp(int64_t n_wf, const int64_t* off, const int32_t* parent,
                             const int64_t* prompt, const int64_t* target, double prefill,
@@ -1421,6 +1424,31 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 }
 
 int64_t kx_launch_count(void) { return kx::g_kx_launches.load(); }
+
+int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining,
+                        const uint8_t* present, int32_t scope_all, uint64_t* pairs, double* correct,
+                        double* accuracy) {
+  return guard([&] {
+    require(n >= 0, "negative size");
+    require(n == 0 || (agent && remaining), "null argument");
+    for (int64_t i = 0; i < n; ++i) require(agent[i] >= 0, "negative agent index");
+    ensure_device(0);
+    int dev = 0;
+    KX_CUDA(cudaGetDevice(&dev));
+    cudaStream_t st = nullptr;
+    KX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    uint64_t p = 0;
+    double c = 0.0;
+    sorting_accuracy(n, agent, remaining, present, scope_all, &p, &c, sm_count(dev), st);
+    if (pairs) *pairs = p;
+    if (correct) *correct = c;
+    if (accuracy) *accuracy = p ? c / static_cast<double>(p) : std::nan("");
+  });
+}
 
 int kx_aggregate_metrics(int32_t n_rows, const double* rows, double* out) {
   return guard([&] {

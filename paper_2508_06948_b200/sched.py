@@ -276,3 +276,16 @@ def record_remaining(rec_offsets, exec_start, exec_end):
     check(lib.kx_record_remaining(len(off) - 1, ptr(off), ptr(es), ptr(ee), ptr(fin), ptr(smp),
                                   _abi.KX_MEM_HOST))
     return fin, smp
+
+
+def sorting_accuracy(agent, remaining, present=None, scope="cross_agent"):
+    """K8: pairwise_sorting_accuracy (priority.cpp:165-189); returns
+    (accuracy or None, pairs, correct)."""
+    lib = _abi.load()
+    a = np.ascontiguousarray(agent, np.int32)
+    r = np.ascontiguousarray(remaining, np.float64)
+    pr = None if present is None else np.ascontiguousarray(present, np.uint8)
+    pairs, correct, acc = C.c_uint64(), C.c_double(), C.c_double()
+    check(lib.kx_sorting_accuracy(len(a), ptr(a), ptr(r), ptr(pr), 1 if scope == "all" else 0,
+                                  C.byref(pairs), C.byref(correct), C.byref(acc)))
+    return (None if pairs.value == 0 else acc.value), pairs.value, correct.value

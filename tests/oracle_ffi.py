@@ -80,6 +80,8 @@ def lib():
         L.kxo_dispatch_round.argtypes = [C.POINTER(Pool), C.POINTER(Queue), C.POINTER(Tables), P,
                                          C.c_int64, C.c_double, C.c_int32, P, P, C.c_int64,
                                          C.POINTER(C.c_int32)]
+        L.kxo_pairwise_accuracy.argtypes = [C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_uint64)]
         L.kxo_finalize.argtypes = [C.c_int64, P, P, P, P, C.c_double, C.c_double, C.c_uint64, P, P, P]
         L.kxo_record_remaining.argtypes = [C.c_int64, P, P, P, P, P]
         _lib = L
@@ -252,3 +254,12 @@ def wasserstein(a, b):
 def median_anchor_distance(coords, anchor):
     c = np.ascontiguousarray(coords, np.float64)
     return lib().kxo_median_anchor_distance(_p(c), len(c), anchor)
+
+
+def pairwise_accuracy(agent, rem, present=None, scope_all=False):
+    a = np.ascontiguousarray(agent, np.int32)
+    r = np.ascontiguousarray(rem, np.float64)
+    p = None if present is None else np.ascontiguousarray(present, np.uint8)
+    acc, pairs = C.c_double(), C.c_uint64()
+    rc = lib().kxo_pairwise_accuracy(len(a), _p(a), _p(r), _p(p), int(scope_all), C.byref(acc), C.byref(pairs))
+    return (None if rc else acc.value), pairs.value

@@ -138,3 +138,17 @@ def test_ledger_unit_values():
     assert L2.try_place(300.0, 50.0, 0.0, 2.0)[1] == pytest.approx(800.0)
     L2.commit(2, 300.0, 50.0, 0.0, 2.0)
     assert not L2.try_place(300.0, 50.0, 0.0, 2.0)[0]
+
+
+def test_pairwise_accuracy_matches_reference():
+    d = kxf.read("accuracy.kxf")
+    off = d["offsets"]
+    for t in range(len(off) - 1):
+        sl = slice(off[t], off[t + 1])
+        for scope_all, key in ((False, "acc_cross"), (True, "acc_all")):
+            acc, _ = O.pairwise_accuracy(d["agent"][sl], d["remaining"][sl], d["present"][sl], scope_all)
+            exp = d[key][t]
+            if np.isnan(exp):
+                assert acc is None
+            else:
+                assert bits(acc) == bits(exp)
