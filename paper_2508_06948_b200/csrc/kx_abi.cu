@@ -790,7 +790,10 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   prm.dpolicy = dc.policy;
   prm.oracle_T = dc.oracle_expected_time;
   prm.ring = ring;
-  prm.heap_cap = cfg->heap_capacity ? cfg->heap_capacity : 1024;
+  // Pending events: at most one per running request, the stale ones of
+  // preempted episodes, two dispatch rounds and the preempt checks.
+  prm.heap_cap = cfg->heap_capacity ? cfg->heap_capacity
+                                    : std::max(128, 2 * cfg->n_instances * max_run + 64);
   prm.max_run = max_run;
   prm.slot_len = dc.slot_len;
   prm.watermark = dc.resume_watermark;

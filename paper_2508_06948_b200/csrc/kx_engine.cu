@@ -49,6 +49,7 @@ struct Scal {
   double prefill_seconds, decode_seconds, wasted_kv, completed_kv;
   uint64_t next_seq, processed, preemption_events, preempted_requests;
   int64_t next_arrival, arrivals_remaining, queue_n, waiting_n, calls_done, wf_done;
+  double next_arrival_time;  // arrival[next_arrival], cached
   int32_t heap_n, round_pending, tick_scheduled, status;
   int64_t rr_next;
 };
@@ -103,6 +104,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     sc.next_seq = static_cast<uint64_t>(w1 - w0);  // arrivals took seq 0..n-1 (engine.cpp:86-89)
     sc.next_arrival = w0;
     sc.arrivals_remaining = w1 - w0;
+    sc.next_arrival_time = w1 > w0 ? I.arrival[w0] : 0.0;
   }
   for (int i = lane; i < NI; i += 32) {
     ins[i] = InstS{};
@@ -584,7 +586,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     Ev ev;
     bool from_heap = have_heap;
     if (have_arr) {
-      Ev a{I.arrival[sc.next_arrival], static_cast<uint64_t>(sc.next_arrival - w0), 0, -1, 0, 0};
+      Ev a{sc.next_arrival_time, static_cast<uint64_t>(sc.next_arrival - w0), 0, -1, 0, 0};
       if (!have_heap || ev_less(a, heap[0])) {
         ev = a;
         from_heap = false;
@@ -595,6 +597,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       pop_heap();
     } else if (lane == 0) {
       sc.next_arrival += 1;
+      if (sc.next_arrival < w1) sc.next_arrival_time = I.arrival[sc.next_arrival];
     }
     sync();
     if (ev.time < __dsub_rn(sc.clock, kTimeEpsilon)) {
