@@ -239,6 +239,15 @@ struct kx_sched {
   int64_t* compact_total = nullptr;
 
   PhaseProfiler prof;
+
+  // Sort/dispatch overlap (tick): top-K order prefix + dispatch phase 1 on
+  // `side` while the full sort runs on `stream`.
+  bool overlap = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_keys = nullptr, ev_released = nullptr, ev_disp = nullptr;
+  Blob topk_blob;
+  TopKWork topk{};
+  DispResume* resume = nullptr;
 };
 
 namespace {
@@ -473,6 +482,28 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->compact_counts = at<uint32_t>(b, o_cc);
     s->compact_total = at<int64_t>(b, o_ct);
   }
+  // overlap workspace
+  if (s->n_pools <= kTopKMaxPools && dispatch_can_overlap(max_pp, ring) && !getenv("KX_NO_OVERLAP")) {
+    const size_t P = static_cast<size_t>(s->n_pools);
+    Layout L;
+    const size_t o_st = L.take<TopKState>(P), o_h = L.take<uint32_t>(P * 256),
+                 o_c = L.take<uint32_t>(P * kTopKMax), o_hd = L.take<uint32_t>(P * kTopKMax),
+                 o_r = L.take<DispResume>(P);
+    alloc_blob(s->topk_blob, L.off);
+    auto& b = s->topk_blob;
+    s->topk.state = at<TopKState>(b, o_st);
+    s->topk.hist = at<uint32_t>(b, o_h);
+    s->topk.cand = at<uint32_t>(b, o_c);
+    s->topk.heads = at<uint32_t>(b, o_hd);
+    s->resume = at<DispResume>(b, o_r);
+    if (const char* e = getenv("KX_TOPK_NEED"))  // test knob: force short prefixes
+      s->topk.max_need = static_cast<uint32_t>(std::clamp(atoi(e), 1, kTopKMax));
+    KX_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    KX_CUDA(cudaEventCreateWithFlags(&s->ev_keys, cudaEventDisableTiming));
+    KX_CUDA(cudaEventCreateWithFlags(&s->ev_released, cudaEventDisableTiming));
+    KX_CUDA(cudaEventCreateWithFlags(&s->ev_disp, cudaEventDisableTiming));
+    s->overlap = true;
+  }
   // decision log
   {
     int64_t per_pool = cfg->log_capacity_per_pool;
@@ -514,6 +545,13 @@ void destroy_impl(kx_sched* s) {
   free_blob(s->inst_ckpt_blob);
   free_blob(s->ws_blob);
   free_blob(s->log_blob);
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    cudaStreamDestroy(s->side);
+  }
+  free_blob(s->topk_blob);
+  for (cudaEvent_t e : {s->ev_keys, s->ev_released, s->ev_disp})
+    if (e) cudaEventDestroy(e);
   if (s->rem_table) cudaFree(s->rem_table);
   if (s->rem_present) cudaFree(s->rem_present);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -575,13 +613,7 @@ void order_impl(kx_sched* s) {
   s->dispatch_valid = false;
 }
 
-void dispatch_impl(kx_sched* s, double now) {
-  if (!s->order_valid || s->order_n != s->n)
-    throw std::logic_error("dispatch round needs a current queue order (call kx_order first)");
-  if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT)
-    fail(KX_ERR_INVALID, "only the time_slot dispatch policy runs on the device in this build");
-  require(s->n_agents > 0 || s->n == 0, "agent tables not set");
-  if (s->n > 0) KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
+DispatchParams dispatch_params(const kx_sched* s, double now) {
   DispatchParams dp{};
   dp.oracle_T = s->dcfg.oracle_expected_time;
   dp.ring = s->ring;
@@ -591,10 +623,80 @@ void dispatch_impl(kx_sched* s, double now) {
   dp.slot_len = s->dcfg.slot_len;
   dp.watermark = s->dcfg.resume_watermark;
   dp.now = now;
+  return dp;
+}
+
+void dispatch_checks(const kx_sched* s) {
+  if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT)
+    fail(KX_ERR_INVALID, "only the time_slot dispatch policy runs on the device in this build");
+  require(s->n_agents > 0 || s->n == 0, "agent tables not set");
+}
+
+void dispatch_impl(kx_sched* s, double now) {
+  if (!s->order_valid || s->order_n != s->n)
+    throw std::logic_error("dispatch round needs a current queue order (call kx_order first)");
+  dispatch_checks(s);
+  if (s->n > 0) KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
+  const DispatchParams dp = dispatch_params(s, now);
   s->prof.begin("dispatch", 0.0, s->stream);
   launch_dispatch(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp,
                   s->n_pools, s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count, s->pool_status,
                   s->stream);
+  s->prof.end(s->stream);
+  s->dispatch_valid = true;
+}
+
+// One scheduling tick = order + dispatch round. With the overlap workspace
+// the round starts before the full sort ends: once the compact keys exist,
+// the side stream selects each pool's top-K order prefix (radix select on
+// the keys, exact sort of the few candidates) and runs the dispatch round
+// over it (phase 1) while the main stream sorts; a pool whose round needs
+// more heads than its prefix resumes over the full order (phase 2). The
+// decisions are identical to order + dispatch_round: the prefix is exactly
+// the head of the pool's order, and the round state carries over.
+void tick_impl(kx_sched* s, double now) {
+  if (!s->overlap || s->n == 0) {
+    order_impl(s);
+    dispatch_impl(s, now);
+    return;
+  }
+  require(s->n_agents > 0, "agent tables not set");
+  dispatch_checks(s);
+  const OrderParams op = order_params(s);
+  if (op.pool_bits > 8) {  // pools beyond the first radix digit: no prefix select
+    order_impl(s);
+    dispatch_impl(s, now);
+    return;
+  }
+  const DispatchParams dp = dispatch_params(s, now);
+  const int passes = op.key_bits / 8;
+  const uint32_t* final_perm = s->ws.vals[passes & 1];
+  OrderHooks hooks;
+  hooks.after_keys = [&] {
+    KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
+    KX_CUDA(cudaEventRecord(s->ev_keys, s->stream));
+    KX_CUDA(cudaStreamWaitEvent(s->side, s->ev_keys, 0));
+    s->prof.begin("topk_select", 0.0, s->side);
+    launch_topk(s->q, s->in, s->pool_begin, op, s->n, s->ws, s->topk, s->sms, s->side,
+                s->ev_released);
+    s->prof.end(s->side);
+    s->prof.begin("dispatch_prefix", 0.0, s->side);
+    launch_dispatch(s->q, s->a, s->in, s->pool_begin, final_perm, s->ws.pool_offsets, dp, s->n_pools,
+                    s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count,
+                    s->pool_status, s->side,
+                    DispPhase{1, 0, s->topk.heads, s->topk.state, s->resume});
+    s->prof.end(s->side);
+    KX_CUDA(cudaEventRecord(s->ev_disp, s->side));
+  };
+  hooks.before_key_overwrite = [&] { KX_CUDA(cudaStreamWaitEvent(s->stream, s->ev_released, 0)); };
+  s->order = launch_order(s->q, s->a, op, s->n, s->ws, s->sms, s->stream, &s->prof, &hooks);
+  s->order_valid = true;
+  s->order_n = s->n;
+  KX_CUDA(cudaStreamWaitEvent(s->stream, s->ev_disp, 0));
+  s->prof.begin("dispatch_rest", 0.0, s->stream);
+  launch_dispatch(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp, s->n_pools,
+                  s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count,
+                  s->pool_status, s->stream, DispPhase{2, 0, nullptr, nullptr, s->resume});
   s->prof.end(s->stream);
   s->dispatch_valid = true;
 }
@@ -1144,8 +1246,7 @@ int kx_tick(kx_sched* s, double now) {
   return guard([&] {
     require(s, "null handle");
     KX_CUDA(cudaSetDevice(s->device));
-    order_impl(s);
-    dispatch_impl(s, now);
+    tick_impl(s, now);
   });
 }
 

@@ -21,6 +21,7 @@
 
 #include "kx_common.cuh"
 #include "kx_dispatch.cuh"
+#include "kx_order.cuh"
 #include "kx_state.cuh"
 
 namespace kx {
@@ -550,10 +551,32 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
                  const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
                  DispatchParams dp, LaneLayout lay, kx_decision* __restrict__ rows,
                  double* __restrict__ cand, int64_t* __restrict__ row_count,
-                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status) {
+                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
+                 DispPhase ph) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_status;
   const int pool = blockIdx.x;
+  // Head source: the pool's full order (phase 0), its top-K prefix (phase 1,
+  // overlapping the full sort), or the full order from where phase 1
+  // stopped (phase 2).
+  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
+  const uint32_t* hp = perm + pool_offsets[pool];
+  int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
+  if (ph.phase == 1) {
+    const TopKState t = ph.tk[pool];
+    if (t.defer) {  // too many ties at the boundary key: wait for the full order
+      if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
+      return;
+    }
+    hp = ph.heads + int64_t(pool) * kTopKMax;
+    q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
+  } else if (ph.phase == 2) {
+    const DispResume r = ph.resume[pool];
+    if (!r.need) return;
+    pos0 = r.start;
+    nrows0 = r.nrows;
+    nadm0 = r.nadm;
+  }
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ib = pool_begin[pool];
@@ -591,12 +614,12 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   if (threadIdx.x == 0) s_status = KX_OK;
   __syncthreads();
 
-  const int64_t q_end = pool_offsets[pool + 1];
-  int64_t pos = pool_offsets[pool];
+  int64_t pos = pos0;
   int64_t hb_start = pos, hb_n = 0;
-  int64_t nrows = 0, nadm = 0;
+  int64_t nrows = nrows0, nadm = nadm0;
   int retries = 0;
   int par = 0;
+  bool broke = false;
   const double t0e = __dadd_rn(now, kTimeEpsilon);
   uint32_t* pv = SL(uint32_t, part_viol);
   uint64_t* pp = SL(uint64_t, part_peak);
@@ -608,7 +631,7 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       hb_n = q_end - pos < kHeadBatch ? q_end - pos : kHeadBatch;
       if (threadIdx.x < hb_n) {
         const int t = threadIdx.x;
-        const uint32_t idx = perm[pos + t];
+        const uint32_t idx = hp[pos + t];
         const int32_t a = q.agent[idx];
         const double T = dp.oracle_T ? q.pure_exec[idx] : ag.T[a];
         SL(uint32_t, h_idx)[t] = idx;
@@ -688,7 +711,10 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     pp[(par * kLaneWarps + warp) * 32 + lane] = peak;
     if (overflow) atomicExch(&s_status, KX_ERR_CAPACITY);
     __syncthreads();
-    if (s_status != KX_OK) break;
+    if (s_status != KX_OK) {
+      broke = true;
+      break;
+    }
 
     // Combine the partials of all warps for this lane's instance.
 #pragma unroll
@@ -739,11 +765,15 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
     ++nrows;
-    if (bl < 0) break;  // head keeps its place (engine.cpp:247)
+    if (bl < 0) {  // head keeps its place (engine.cpp:247)
+      broke = true;
+      break;
+    }
     if (overload) {
       if (lane == bl) susp = true;  // Dispatcher::on_overload
       if (++retries > ni) {
         if (threadIdx.x == 0) s_status = KX_ERR_LIVELOCK;
+        broke = true;
         break;
       }
       par ^= 1;
@@ -786,21 +816,26 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     par ^= 1;
   }
   __syncthreads();
-  // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
-  const int64_t current =
-      static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(now, kTimeEpsilon), dp.slot_len)));
-  if (act && current > base) {
-    const int64_t stop = current < base + ring ? current : base + ring;
-    for (int64_t s = base + warp; s < stop; s += kLaneWarps) {
-      const int p2 = static_cast<int>(s & (ring - 1));
-      su[p2 * 32 + lane] = 0.0;
-      se[p2 * 32 + lane] = 0;
+  // Phase 1 ran out of prefix heads without finishing the round: hand the
+  // state to the continuation (no gc yet: the round is not over).
+  const bool defer_rest = ph.phase == 1 && !broke && s_status == KX_OK && pos >= q_end && q_end < pool_n;
+  if (!defer_rest) {
+    // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
+    const int64_t current =
+        static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(now, kTimeEpsilon), dp.slot_len)));
+    if (act && current > base) {
+      const int64_t stop = current < base + ring ? current : base + ring;
+      for (int64_t s = base + warp; s < stop; s += kLaneWarps) {
+        const int p2 = static_cast<int>(s & (ring - 1));
+        su[p2 * 32 + lane] = 0.0;
+        se[p2 * 32 + lane] = 0;
+      }
+      base = current;
     }
-    base = current;
   }
   if (warp == 0 && act) {
     in.n_active[i] = nact;
-    active_gc(in, i, now);
+    if (!defer_rest) active_gc(in, i, now);
   }
   __syncthreads();
   if (warp == 0 && act) {
@@ -818,9 +853,12 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     }
   }
   if (threadIdx.x == 0) {
-    row_count[pool] = nrows;
-    admitted_count[pool] = nadm;
-    pool_status[pool] = s_status;
+    if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
+    if (!defer_rest) {
+      row_count[pool] = nrows;
+      admitted_count[pool] = nadm;
+      pool_status[pool] = s_status;
+    }
   }
 }
 
@@ -949,18 +987,22 @@ void configure_dispatch_kernels() {
                                kDispSmemLimit));
 }
 
+bool dispatch_can_overlap(int max_inst_per_pool, int ring) {
+  return max_inst_per_pool <= 32 && lane_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
+}
+
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      const int32_t* pool_begin, const uint32_t* perm, const int64_t* pool_offsets,
                      const DispatchParams& dp, int n_pools, int max_inst_per_pool, kx_decision* rows,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
-                     cudaStream_t st) {
+                     cudaStream_t st, DispPhase phase) {
   if (max_inst_per_pool <= 32) {
     const LaneLayout ll = lane_layout(dp.ring);
     if (ll.total <= static_cast<uint32_t>(kDispSmemLimit)) {
       k_dispatch_lanes<<<n_pools, kLaneThreads, ll.total, st>>>(q, a, in, pool_begin, perm,
                                                                pool_offsets, dp, ll, rows, cand,
                                                                row_count, admitted_count,
-                                                               pool_status);
+                                                               pool_status, phase);
       KX_CHECK_LAUNCH();
       return;
     }

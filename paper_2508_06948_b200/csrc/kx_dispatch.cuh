@@ -22,13 +22,32 @@ struct DispatchParams {
   double now;
 };
 
+struct TopKState;
+
+// Resumable dispatch round (k_dispatch_lanes): phase 1 walks a pool's top-K
+// order prefix while the full sort runs; phase 2 continues from `start`
+// over the full order when phase 1 ran out of prefix heads.
+struct DispResume {
+  int64_t start, nrows, nadm;
+  int32_t need, pad;
+};
+
+struct DispPhase {
+  int32_t phase;               // 0 full order, 1 top-K prefix, 2 continuation
+  int32_t pad;
+  const uint32_t* heads;       // [P * kTopKMax] (phase 1)
+  const TopKState* tk;         // (phase 1)
+  DispResume* resume;          // [P] (phases 1, 2)
+};
+
 void configure_dispatch_kernels();
+bool dispatch_can_overlap(int max_inst_per_pool, int ring);
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      const int32_t* pool_begin, const uint32_t* perm, const int64_t* pool_offsets,
                      const DispatchParams& dp, int n_pools, int max_inst_per_pool, kx_decision* rows,
                      double* cand,
                      int64_t* row_count, int64_t* admitted_count, int* pool_status,
-                     cudaStream_t st);
+                     cudaStream_t st, DispPhase phase = DispPhase{});
 void launch_ledger_try_place(const InstDev& in, int i, int ring, double P, double k, double t0,
                              double T, double slot_len, double* out_peak, int64_t* out_viol,
                              int* out_state, cudaStream_t st);

@@ -503,6 +503,219 @@ k_tie_fix_big(QueueDev q, int policy, uint32_t* __restrict__ perm, uint32_t* __r
   }
 }
 
+// ---- per-pool top-K prefix (overlaps the dispatch with the full sort) -------
+// A dispatch round consumes at most (free batch slots + 1) heads of each
+// pool (every admission takes a slot; the round stops at the first head
+// with no target, engine.cpp:247). Radix-select finds, per pool, the
+// smallest compact-key bound whose prefix holds at least that many
+// requests; those candidates are exactly the first entries of the pool's
+// order (every other request has a larger compact key), and sorting them
+// by (key, exact tuple) gives that prefix in reference order.
+__global__ void k_topk_init(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
+                            int64_t n, const uint32_t* __restrict__ hist_excl,
+                            const int64_t* __restrict__ pool_offsets, uint32_t max_need,
+                            TopKState* __restrict__ st) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= op.n_pools) return;
+  TopKState t{};
+  const int64_t cnt = pool_offsets[p + 1] - pool_offsets[p];
+  int64_t free_slots = 0;
+  for (int i = pool_begin[p]; i < pool_begin[p + 1]; ++i) {
+    const int64_t f = int64_t(in.max_batch[i]) - in.running[i] - in.waiting[i];
+    free_slots += f > 0 ? f : 0;
+  }
+  int64_t need = free_slots + 1;
+  need = need < cnt ? need : cnt;
+  need = need < int64_t(max_need) ? need : int64_t(max_need);  // the continuation covers the rest
+  t.need = static_cast<uint32_t>(need);
+  t.pool_count = static_cast<uint32_t>(cnt);
+  if (need == 0) {  // empty pool
+    t.done = 1;
+    t.bound = 0;
+    t.empty = 1;
+    st[p] = t;
+    return;
+  }
+  const int TS = op.key_bits - 8;
+  const int lo_d = op.pool_bits ? (p << (8 - op.pool_bits)) : 0;
+  const int hi_d = op.pool_bits ? ((p + 1) << (8 - op.pool_bits)) : 256;
+  int64_t cum = 0, c = 0;
+  int d = lo_d;
+  for (; d < hi_d; ++d) {
+    c = (d + 1 < 256 ? int64_t(hist_excl[d + 1]) : n) - int64_t(hist_excl[d]);
+    if (cum + c >= need) break;
+    cum += c;
+  }
+  t.below = static_cast<uint32_t>(cum);
+  t.count = static_cast<uint32_t>(c);
+  t.prefix = static_cast<uint32_t>(d) << TS;
+  t.mask = 0xFFu << TS;
+  if (cum + c <= kTopKMax) {
+    t.done = 1;
+    t.bound = t.prefix | ((1u << TS) - 1u);
+  } else if (TS == 0) {  // single-digit keys: stop below the boundary key
+    t.done = 1;
+    if (cum > 0) t.bound = t.prefix - 1u;
+    else t.defer = 1;
+  }
+  st[p] = t;
+}
+
+__device__ __forceinline__ int pool_of_key(uint32_t key, const OrderParams& op) {
+  return op.pool_bits ? static_cast<int>(key >> (op.key_bits - op.pool_bits)) : 0;
+}
+
+__global__ void k_topk_hist(const uint32_t* __restrict__ keys, int64_t n, OrderParams op, int shift,
+                            const TopKState* __restrict__ st, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[kTopKMaxPools * kRadix];
+  __shared__ uint32_t s_mask[kTopKMaxPools], s_prefix[kTopKMaxPools], s_live[kTopKMaxPools];
+  for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x) sh[i] = 0;
+  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
+    s_mask[p] = st[p].mask;
+    s_prefix[p] = st[p].prefix;
+    s_live[p] = !st[p].done;
+  }
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = keys[i];
+    const int p = pool_of_key(k, op);
+    if (s_live[p] && (k & s_mask[p]) == s_prefix[p]) atomicAdd(&sh[p * kRadix + ((k >> shift) & 0xFF)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void k_topk_pick(OrderParams op, int shift, TopKState* __restrict__ st,
+                            uint32_t* __restrict__ hist) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= op.n_pools) return;
+  TopKState t = st[p];
+  uint32_t* h = hist + p * kRadix;
+  if (!t.done) {
+    const int64_t need = int64_t(t.need) - t.below;
+    int64_t cum = 0, c = 0;
+    int d = 0;
+    for (; d < kRadix; ++d) {
+      c = h[d];
+      if (cum + c >= need) break;
+      cum += c;
+    }
+    t.below += static_cast<uint32_t>(cum);
+    t.count = static_cast<uint32_t>(c);
+    t.prefix |= static_cast<uint32_t>(d) << shift;
+    t.mask |= 0xFFu << shift;
+    if (int64_t(t.below) + c <= kTopKMax) {
+      t.done = 1;
+      t.bound = t.prefix | ((1u << shift) - 1u);
+    } else if (shift == 0) {  // > kTopKMax requests share the boundary key:
+      t.done = 1;             // the strictly smaller keys are still a prefix
+      if (t.below > 0) t.bound = t.prefix - 1u;
+      else t.defer = 1;
+    }
+    st[p] = t;
+  }
+  for (int d = 0; d < kRadix; ++d) h[d] = 0;  // ready for the next round
+}
+
+__global__ void k_topk_compact(const uint32_t* __restrict__ keys, int64_t n, OrderParams op,
+                               TopKState* __restrict__ st, uint32_t* __restrict__ cand) {
+  __shared__ uint32_t s_bound[kTopKMaxPools], s_ok[kTopKMaxPools];
+  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
+    s_bound[p] = st[p].bound;
+    s_ok[p] = !st[p].defer && !st[p].empty;
+  }
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = keys[i];
+    const int p = pool_of_key(k, op);
+    if (s_ok[p] && k <= s_bound[p]) {
+      const uint32_t slot = atomicAdd(&st[p].n_cand, 1u);
+      if (slot < kTopKMax) cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(i);
+    }
+  }
+}
+
+// CTA per pool: exact order of the candidates (compact key, then the tuple).
+__global__ void __launch_bounds__(1024)
+k_topk_sort(QueueDev q, int policy, const uint32_t* __restrict__ keys, OrderParams op,
+            const TopKState* __restrict__ st, const uint32_t* __restrict__ cand,
+            uint32_t* __restrict__ heads) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int p = blockIdx.x;
+  const TopKState t = st[p];
+  if (t.defer || t.empty) return;
+  const int n = static_cast<int>(t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
+  uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw);
+  TRec* sr = reinterpret_cast<TRec*>(smem_raw + sizeof(uint32_t) * kTopKMax);
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+    if (i < n) {
+      const uint32_t idx = cand[int64_t(p) * kTopKMax + i];
+      sk[i] = keys[idx];
+      sr[i] = load_rec(q, policy, idx);
+    } else {
+      sk[i] = 0xffffffffu;
+      sr[i].w0 = sr[i].w1 = sr[i].w2 = sr[i].msg = sr[i].uid = ~0ull;
+      sr[i].idx = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int kk = 2; kk <= p2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & kk) == 0;
+          const bool lt_li = sk[l] < sk[i] || (sk[l] == sk[i] && rec_less(sr[l], sr[i]));
+          const bool lt_il = sk[i] < sk[l] || (sk[i] == sk[l] && rec_less(sr[i], sr[l]));
+          if (up ? lt_li : lt_il) {
+            const uint32_t tk = sk[i];
+            sk[i] = sk[l];
+            sk[l] = tk;
+            const TRec tr = sr[i];
+            sr[i] = sr[l];
+            sr[l] = tr;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = sr[i].idx;
+}
+
+void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
+                 const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
+                 cudaStream_t st, cudaEvent_t keys_released) {
+  const uint32_t* keys = ws.keys[0];
+  const int passes = op.key_bits / kRadixBits;
+  const int pb = (op.n_pools + 31) / 32;
+  k_topk_init<<<pb, 32, 0, st>>>(in, pool_begin, op, n, ws.hist + (passes - 1) * kRadix,
+                                 ws.pool_offsets, w.max_need, w.state);
+  KX_CHECK_LAUNCH();
+  KX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * op.n_pools * kRadix, st));
+  const int grid = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, int64_t(sms) * 4));
+  for (int r = 1; r < passes && n > 0; ++r) {
+    const int shift = op.key_bits - 8 - 8 * r;
+    k_topk_hist<<<grid, 256, 0, st>>>(keys, n, op, shift, w.state, w.hist);
+    KX_CHECK_LAUNCH();
+    k_topk_pick<<<pb, 32, 0, st>>>(op, shift, w.state, w.hist);
+    KX_CHECK_LAUNCH();
+  }
+  if (n > 0) {
+    k_topk_compact<<<grid, 256, 0, st>>>(keys, n, op, w.state, w.cand);
+    KX_CHECK_LAUNCH();
+  }
+  KX_CUDA(cudaEventRecord(keys_released, st));  // the original keys are no longer read
+  const size_t smem = sizeof(uint32_t) * kTopKMax + sizeof(TRec) * kTopKMax;
+  k_topk_sort<<<op.n_pools, 1024, smem, st>>>(q, op.policy, keys, op, w.state, w.cand, w.heads);
+  KX_CHECK_LAUNCH();
+}
+
 // ---- host orchestration --------------------------------------------------
 size_t order_lookback_bytes(int64_t cap) {
   const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
@@ -519,7 +732,7 @@ void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, 
 
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
-                            PhaseProfiler* prof) {
+                            PhaseProfiler* prof, const OrderHooks* hooks) {
   PhaseProfiler dummy;
   PhaseProfiler& P = prof ? *prof : dummy;
   const double N = static_cast<double>(n);
@@ -532,6 +745,8 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   if (n == 0) {
     k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
     KX_CHECK_LAUNCH();
+    if (hooks && hooks->after_keys) hooks->after_keys();
+    if (hooks && hooks->before_key_overwrite) hooks->before_key_overwrite();
     res.perm = ws.vals[0];
     res.keys = ws.keys[0];
     return res;
@@ -555,6 +770,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   KX_CHECK_LAUNCH();
   k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
   KX_CHECK_LAUNCH();
+  if (hooks && hooks->after_keys) hooks->after_keys();  // compact keys + histograms ready
 
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   const size_t smem = sort_dyn_smem<uint32_t>();
@@ -569,6 +785,8 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     KX_CHECK_LAUNCH();
     P.end(st);
     cur ^= 1;
+    // pass 1 overwrites keys[0]: readers of the original keys finish first
+    if (p == 0 && hooks && hooks->before_key_overwrite) hooks->before_key_overwrite();
   }
   res.keys = ws.keys[cur];
   res.perm = ws.vals[cur];
@@ -603,6 +821,8 @@ void init_ranges(PoolRange* r, int n, cudaStream_t st) {
 }
 
 void configure_sort_kernels() {
+  KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(uint32_t) * kTopKMax + sizeof(TRec) * kTopKMax)));
   KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sort_dyn_smem<uint32_t>())));
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+
 #include "kx_common.cuh"
 #include "kx_state.cuh"
 
@@ -41,8 +43,34 @@ void init_ranges(PoolRange* r, int n, cudaStream_t st);
 void configure_sort_kernels();
 void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, double* k0,
                   double* k1, double* k2, int sms, cudaStream_t st);
+constexpr int kTopKMax = 2048;      // candidate heads per pool
+constexpr int kTopKMaxPools = 32;   // overlap path limit
+
+// Per-pool radix-select state of the dispatch prefix (k_topk_*).
+struct TopKState {
+  uint32_t need, prefix, mask, below, count, done, bound, n_cand;
+  uint32_t pool_count, defer, empty, pad;
+};
+
+struct TopKWork {
+  TopKState* state;  // [P]
+  uint32_t* hist;    // [P * 256]
+  uint32_t* cand;    // [P * kTopKMax] candidate queue indices (unordered)
+  uint32_t max_need = kTopKMax;  // prefix length cap (lowered by tests via KX_TOPK_NEED)
+  uint32_t* heads;   // [P * kTopKMax] the pool's order prefix
+};
+
+struct OrderHooks {
+  std::function<void()> after_keys;            // compact keys, histograms, pool offsets ready
+  std::function<void()> before_key_overwrite;  // after radix pass 0, before pass 1
+};
+
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
-                            PhaseProfiler* prof);
+                            PhaseProfiler* prof, const OrderHooks* hooks = nullptr);
+
+void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
+                 const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
+                 cudaStream_t st, cudaEvent_t keys_released);
 
 }  // namespace kx

@@ -61,14 +61,37 @@ def build_pools(rng, n_pools, per_pool, cap=3000.0, max_batch=8):
     return inst
 
 
-@pytest.mark.parametrize("n_pools,per_pool,n,rounds", [(1, 4, 500, 4), (8, 32, 20000, 3), (3, 17, 5000, 5)])
-def test_dispatch_multi_pool_matches_oracle(gpu_lib, n_pools, per_pool, n, rounds):
+# Tick modes: "overlap" = top-K order prefix + dispatch on a side stream while
+# the full sort runs (the default for <= 32 instances per pool), "serial" =
+# order then dispatch, "short1"/"short5" = overlap with prefixes capped at 1
+# / 5 heads so every round resumes over the full order (phase 2).
+TICK_MODES = {"overlap": {}, "serial": {"KX_NO_OVERLAP": "1"}, "short1": {"KX_TOPK_NEED": "1"},
+              "short5": {"KX_TOPK_NEED": "5"}}
+
+
+def set_mode(monkeypatch, mode):
+    for k in ("KX_NO_OVERLAP", "KX_TOPK_NEED"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in TICK_MODES[mode].items():
+        monkeypatch.setenv(k, v)
+
+
+@pytest.mark.parametrize("mode", list(TICK_MODES))
+@pytest.mark.parametrize("n_pools,per_pool,n,rounds,ties", [(1, 4, 500, 4, 0), (8, 32, 20000, 3, 0),
+                                                             (3, 17, 5000, 5, 0), (2, 8, 6000, 3, 1), (2, 8, 6000, 3, 2)])
+def test_dispatch_multi_pool_matches_oracle(gpu_lib, monkeypatch, mode, n_pools, per_pool, n, rounds, ties):
+    set_mode(monkeypatch, mode)
     rng = np.random.default_rng(n_pools * 100 + per_pool)
     inst = build_pools(rng, n_pools, per_pool)
     s = kx.DeviceScheduler(inst, n_pools=n_pools, queue_capacity=n, max_agents=64)
     q, t = random_queue(rng, n, n_agents=30, n_pools=n_pools)
     q.prompt[:] = rng.integers(1, 400, n)
     q.view.prompt = q.prompt.ctypes.data
+    if ties:  # > kTopKMax equal compact keys per pool: a prefix cut below them (1)
+        t.pk[:] = 1.0  # or none at all (2, the whole pool waits for the full order)
+        q.app_start[:] = np.where(rng.random(n) < 0.9, 0.25, q.app_start)
+        if ties == 2:
+            q.app_start[:] = np.maximum(q.app_start, 0.25)
     s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
     s.set_scheduler("kairos")
     pools = []
@@ -158,7 +181,9 @@ def test_remove_admitted_compacts_queue(gpu_lib):
     assert np.array_equal(perm, O.sort("fcfs", sub, t, 1)[0])
 
 
-def test_checkpoint_restore_replays_identically(gpu_lib):
+@pytest.mark.parametrize("mode", ["overlap", "short1"])
+def test_checkpoint_restore_replays_identically(gpu_lib, monkeypatch, mode):
+    set_mode(monkeypatch, mode)
     rng = np.random.default_rng(9)
     inst = build_pools(rng, 2, 6)
     s = kx.DeviceScheduler(inst, n_pools=2, queue_capacity=3000, max_agents=16)
