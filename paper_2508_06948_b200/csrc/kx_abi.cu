@@ -498,7 +498,11 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->resume = at<DispResume>(b, o_r);
     if (const char* e = getenv("KX_TOPK_NEED"))  // test knob: force short prefixes
       s->topk.max_need = static_cast<uint32_t>(std::clamp(atoi(e), 1, kTopKMax));
-    KX_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    // The prefix select + dispatch chain is the tick's critical path: its
+    // stream outranks the full sort's for SM slots.
+    int prio_lo = 0, prio_hi = 0;
+    KX_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    KX_CUDA(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
     KX_CUDA(cudaEventCreateWithFlags(&s->ev_keys, cudaEventDisableTiming));
     KX_CUDA(cudaEventCreateWithFlags(&s->ev_released, cudaEventDisableTiming));
     KX_CUDA(cudaEventCreateWithFlags(&s->ev_disp, cudaEventDisableTiming));

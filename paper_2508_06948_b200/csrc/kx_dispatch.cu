@@ -501,60 +501,105 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 
 #undef SM
 
-// ---- K5 fast path: pools of <= 32 instances ----------------------------------
-// Lanes = instances, warps = interleaved slot subsets (warp w owns absolute
-// slots s with s % kLaneWarps == w). Every warp keeps an identical register
-// copy of each lane-instance's live state (it is updated deterministically),
-// evaluates its slot subset for all instances at once, publishes per-instance
-// partial (first violating slot, peak) to shared memory, and after the single
-// barrier of the decision every warp combines the partials, computes the same
-// arg-min (REDUX), and books the target's slots of its own subset. Ledger
-// rings are staged transposed (usage[slot][instance]) so a warp's 32 lanes
-// read 32 consecutive words.
-constexpr int kLaneWarps = 8;
-constexpr int kLaneThreads = 32 * kLaneWarps;
+// ---- K5 fast path: pools of <= 32 instances, one warp per decision chain ----
+// The decisions of a pool form one sequential chain (each commit changes the
+// ledger the next head is placed against), so the chain runs on ONE warp with
+// lanes = instances and no block barrier per decision; the CTA's other warps
+// only stage the rings into shared memory and write them back. Lanes are
+// assigned in increasing InstanceId order, so select_instance's tie rule
+// (smaller id) is the lowest lane among equal peaks.
+//
+// try_place's slot walk (dispatcher.cpp:52-68) is split in three. With
+// c = floor((now + eps) / L) every head's span is [c, last]. When
+// peak_in_slot (dispatcher.cpp:33-42) is zero on every slot outside the span
+// (checked per head on the two neighbouring slots each side; the reference's
+// floors make it zero further out), a stored slot outside the span
+// contributes exactly `used` to the predicted peak, so:
+//   * stored slots below c (stale past slots before the end-of-round gc, H5)
+//     are one per-instance max, fixed for the round;
+//   * stored slots above the span are a per-instance suffix max over the
+//     ring, refreshed for the target after each commit;
+//   * the span is evaluated slot by slot with the reference's
+//     used + (P + k * dt), correctly rounded; (P + k * dt) comes from a
+//     per-head table built when the head batch is loaded (per lane when the
+//     pool's decode rates differ).
+// Heads outside that shape (T <= 0, negative prompt, a non-zero margin slot,
+// spans longer than the table) take the generic slot walk. Ledger rings are
+// staged transposed (usage[slot][lane]). Invariant: a slot that is not
+// stored holds usage +0.0 (gc and the initial state write 0.0).
+constexpr int kWarpThreads = 128;
+constexpr int kWHB = 32;       // head batch (lane = head while loading)
+constexpr int kDtSlots = 64;   // span slots tabulated per head
 
-struct LaneLayout {
-  uint32_t part_viol, part_peak, h_T, h_prompt, h_kept, h_uid, h_agent, h_idx, h_first, h_last,
-      h_tend, usage, ex, total;
+struct WarpLayout {
+  uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
+      usage, ex, sufm, total;
 };
 
-LaneLayout lane_layout(int ring) {
-  LaneLayout L{};
+WarpLayout warp_layout(int ring) {
+  WarpLayout L{};
   uint32_t o = 0;
   auto take = [&](size_t bytes) {
     const uint32_t at = o;
     o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
     return at;
   };
-  L.part_viol = take(4 * 2 * kLaneWarps * 32);
-  L.part_peak = take(8 * 2 * kLaneWarps * 32);
-  L.h_T = take(8 * kHeadBatch);
-  L.h_prompt = take(8 * kHeadBatch);
-  L.h_kept = take(8 * kHeadBatch);
-  L.h_uid = take(8 * kHeadBatch);
-  L.h_agent = take(4 * kHeadBatch);
-  L.h_idx = take(4 * kHeadBatch);
-  L.h_first = take(8 * kHeadBatch);
-  L.h_last = take(8 * kHeadBatch);
-  L.h_tend = take(8 * kHeadBatch);
+  L.h_idx = take(4 * kWHB);
+  L.h_agent = take(4 * kWHB);
+  L.h_prompt = take(8 * kWHB);
+  L.h_kept = take(8 * kWHB);
+  L.h_uid = take(8 * kWHB);
+  L.h_T = take(8 * kWHB);
+  L.h_first = take(8 * kWHB);
+  L.h_last = take(8 * kWHB);
+  L.h_mode = take(4 * kWHB);
+  L.tab = take(8 * kWHB * kDtSlots);
+  L.lane_inst = take(4 * 32);
   L.usage = take(size_t(8) * 32 * ring);
   L.ex = take(size_t(32) * ring);
+  L.sufm = take(size_t(8) * 32 * ring);
   L.total = o;
   return L;
 }
 
-#define SL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
+// (eval_t - t0) of peak_in_slot (dispatcher.cpp:33-42) for one slot, NaN
+// when the slot takes the zero branch.
+__device__ __forceinline__ double slot_dt(double t0, double t0e, double t_end, double tee,
+                                          int64_t slot, double slot_len) {
+  const double slot_start = __dmul_rn(static_cast<double>(slot), slot_len);
+  const double slot_end = __dadd_rn(slot_start, slot_len);
+  if (slot_end <= t0e || slot_start >= tee) return __longlong_as_double(0x7ff8000000000000ll);
+  const double eval_t = (t_end < slot_end) ? t_end : slot_end;
+  return __dsub_rn(eval_t, t0);
+}
 
-__global__ void __launch_bounds__(kLaneThreads)
-k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
-                 const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
-                 DispatchParams dp, LaneLayout lay, kx_decision* __restrict__ rows,
-                 double* __restrict__ cand, int64_t* __restrict__ row_count,
-                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
-                 DispPhase ph) {
+__device__ __forceinline__ double pk_of(double P, double k, double dt) {
+  return dt == dt ? __dadd_rn(P, __dmul_rn(k, dt)) : 0.0;
+}
+
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
+  const uint32_t lo = __shfl_up_sync(0xffffffffu, static_cast<uint32_t>(v), d);
+  const uint32_t hi = __shfl_up_sync(0xffffffffu, static_cast<uint32_t>(v >> 32), d);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(v), src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(v >> 32), src);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// Head modes (per head, warp-uniform).
+enum : int32_t { kModeTabPk = 0, kModeTabDt = 1, kModeGeneric = 2 };
+
+__global__ void __launch_bounds__(kWarpThreads)
+k_dispatch_warp(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
+                const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
+                DispatchParams dp, WarpLayout lay, kx_decision* __restrict__ rows,
+                double* __restrict__ cand, int64_t* __restrict__ row_count,
+                int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
+                DispPhase ph) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int s_status;
   const int pool = blockIdx.x;
   // Head source: the pool's full order (phase 0), its top-K prefix (phase 1,
   // overlapping the full sort), or the full order from where phase 1
@@ -562,193 +607,300 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
   const uint32_t* hp = perm + pool_offsets[pool];
   int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
+  bool skip = false;
   if (ph.phase == 1) {
     const TopKState t = ph.tk[pool];
     if (t.defer) {  // too many ties at the boundary key: wait for the full order
       if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
-      return;
+      skip = true;
     }
     hp = ph.heads + int64_t(pool) * kTopKMax;
     q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
   } else if (ph.phase == 2) {
     const DispResume r = ph.resume[pool];
-    if (!r.need) return;
+    skip = !r.need;
     pos0 = r.start;
     nrows0 = r.nrows;
     nadm0 = r.nadm;
   }
+  if (skip) return;  // uniform over the CTA
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ib = pool_begin[pool];
   const int ni = pool_begin[pool + 1] - ib;
   const int ring = dp.ring;
-  const double now = dp.now;
-  const bool act = lane < ni;
-  const int i = ib + (act ? lane : 0);
+  const int rmask = ring - 1;
+  double* const su = reinterpret_cast<double*>(smem_raw + lay.usage);
+  uint8_t* const se = reinterpret_cast<uint8_t*>(smem_raw + lay.ex);
+  uint64_t* const sm = reinterpret_cast<uint64_t*>(smem_raw + lay.sufm);
+  int32_t* const s_li = reinterpret_cast<int32_t*>(smem_raw + lay.lane_inst);
+  const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
 
-  // Per-lane instance state (identical copies in every warp).
-  const double cap = act ? in.cap[i] : 0.0;
-  const double kr = act ? in.decode_rate[i] : 0.0;
-  const int32_t mb = act ? in.max_batch[i] : 0;
-  const int32_t id = act ? in.id[i] : 0x7fffffff;
-  const int32_t waiting = act ? in.waiting[i] : 0;
-  double live = act ? in.live_kv[i] : 0.0;
-  int32_t running = act ? in.running[i] : 0;
-  bool susp = act ? in.suspended[i] != 0 : false;
-  int64_t base = act ? in.base_slot[i] : 0;
-  int64_t hi = act ? in.hi_slot[i] : -1;
-  int32_t nact = act ? in.n_active[i] : 0;  // active_ size, kept in a register
-  // Common slot origin of the pool (bases are equal after any gc; the
-  // per-lane base still bounds what each instance retains).
-  const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
-
-  // Stage the rings transposed: usage[pos][lane].
-  double* su = SL(double, usage);
-  uint8_t* se = SL(uint8_t, ex);
-  for (int j = threadIdx.x; j < 32 * ring; j += kLaneThreads) {
-    const int li = j % 32, pos = j / 32;
-    const bool a = li < ni;
-    su[j] = a ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
-    se[j] = a ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+  // Lane of each instance: rank of its InstanceId within the pool.
+  if (warp == 0) {
+    const int32_t myid = lane < ni ? in.id[ib + lane] : 0x7fffffff;
+    int rank = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t o = __shfl_sync(0xffffffffu, myid, l);
+      rank += (l < ni) && (o < myid || (o == myid && l < lane));
+    }
+    s_li[lane] = -1;
+    __syncwarp();
+    if (lane < ni) s_li[rank] = lane;
   }
-  if (threadIdx.x == 0) s_status = KX_OK;
+  __syncthreads();
+  // Stage the rings transposed: usage[pos][lane] (all warps).
+  for (int j = threadIdx.x; j < 32 * ring; j += kWarpThreads) {
+    const int l = j & 31, pos = j >> 5;
+    const int li = s_li[l];
+    su[j] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
+    se[j] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+  }
   __syncthreads();
 
-  int64_t pos = pos0;
-  int64_t hb_start = pos, hb_n = 0;
-  int64_t nrows = nrows0, nadm = nadm0;
-  int retries = 0;
-  int par = 0;
-  bool broke = false;
-  const double t0e = __dadd_rn(now, kTimeEpsilon);
-  uint32_t* pv = SL(uint32_t, part_viol);
-  uint64_t* pp = SL(uint64_t, part_peak);
+  if (warp == 0) {
+    uint32_t* const h_idx = reinterpret_cast<uint32_t*>(smem_raw + lay.h_idx);
+    int32_t* const h_agent = reinterpret_cast<int32_t*>(smem_raw + lay.h_agent);
+    int64_t* const h_prompt = reinterpret_cast<int64_t*>(smem_raw + lay.h_prompt);
+    int64_t* const h_kept = reinterpret_cast<int64_t*>(smem_raw + lay.h_kept);
+    uint64_t* const h_uid = reinterpret_cast<uint64_t*>(smem_raw + lay.h_uid);
+    double* const h_T = reinterpret_cast<double*>(smem_raw + lay.h_T);
+    int64_t* const h_first = reinterpret_cast<int64_t*>(smem_raw + lay.h_first);
+    int64_t* const h_last = reinterpret_cast<int64_t*>(smem_raw + lay.h_last);
+    int32_t* const h_mode = reinterpret_cast<int32_t*>(smem_raw + lay.h_mode);
+    double* const stab = reinterpret_cast<double*>(smem_raw + lay.tab);
+    const double now = dp.now;
+    const double L = dp.slot_len;
+    const int li = s_li[lane];
+    const bool act = li >= 0;
+    const int i = ib + (act ? li : 0);
+    const double cap = act ? in.cap[i] : 0.0;
+    const double kr = act ? in.decode_rate[i] : 0.0;
+    const int32_t mb = act ? in.max_batch[i] : 0;
+    const int32_t id = act ? in.id[i] : 0x7fffffff;
+    const int32_t waiting = act ? in.waiting[i] : 0;
+    const double wcap = __dmul_rn(dp.watermark, cap);
+    double live = act ? in.live_kv[i] : 0.0;
+    int32_t running = act ? in.running[i] : 0;
+    bool susp = act ? in.suspended[i] != 0 : false;
+    int64_t base = act ? in.base_slot[i] : 0;
+    int64_t hi = act ? in.hi_slot[i] : -1;
+    int32_t nact = act ? in.n_active[i] : 0;
+    // One decode rate for the whole pool: the (P + k * dt) table is shared.
+    const double k0 = __shfl_sync(0xffffffffu, kr, 0);
+    const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
+    // Common slot origin of the pool (bases are equal after any gc; the
+    // per-lane base still bounds what each instance retains).
+    const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
+    const int32_t lo_off = static_cast<int32_t>(base - B);
+    const double t0e = __dadd_rn(now, kTimeEpsilon);
+    const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
+    const int32_t c_off = static_cast<int32_t>(cslot - B);
+    int32_t hi_off = static_cast<int32_t>(hi - B);  // lane's top stored offset
+    int status = KX_OK;
 
-  while (pos < q_end) {
-    if (pos >= hb_start + hb_n) {  // refill the head batch (prefix of the pool's order)
-      __syncthreads();
-      hb_start = pos;
-      hb_n = q_end - pos < kHeadBatch ? q_end - pos : kHeadBatch;
-      if (threadIdx.x < hb_n) {
-        const int t = threadIdx.x;
-        const uint32_t idx = hp[pos + t];
-        const int32_t a = q.agent[idx];
-        const double T = dp.oracle_T ? q.pure_exec[idx] : ag.T[a];
-        SL(uint32_t, h_idx)[t] = idx;
-        SL(int32_t, h_agent)[t] = a;
-        SL(int64_t, h_prompt)[t] = q.prompt[idx];
-        SL(int64_t, h_kept)[t] = q.kept[idx];
-        SL(uint64_t, h_uid)[t] = q.uid[idx];
-        SL(double, h_T)[t] = T;
-        int64_t f, l;
-        span_bounds_dev(now, T, dp.slot_len, &f, &l);
-        SL(int64_t, h_first)[t] = f;
-        SL(int64_t, h_last)[t] = l;
-        SL(double, h_tend)[t] = __dadd_rn(now, T);
+    // Max of the stored slots below c, and the suffix max of the stored
+    // slots from each offset > c up to hi.
+    uint64_t lomax = kZeroBits;
+    for (int32_t o = lo_off; o < c_off && o <= hi_off; ++o) {
+      const int p2 = static_cast<int>((B + o) & rmask);
+      if (se[p2 * 32 + lane]) {
+        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+        lomax = tb > lomax ? tb : lomax;
       }
-      __syncthreads();
     }
-    const int h = static_cast<int>(pos - hb_start);
-    const int64_t prompt = SL(int64_t, h_prompt)[h];
-    const double P = static_cast<double>(prompt);
-    Span sp;
-    sp.first = SL(int64_t, h_first)[h];
-    sp.last = SL(int64_t, h_last)[h];
-    sp.t0 = now;
-    sp.t_end = SL(double, h_tend)[h];
-    sp.t0e = t0e;
-    sp.tee = __dsub_rn(sp.t_end, kTimeEpsilon);
-    const bool nonempty = sp.last >= sp.first;
-
-    // collect_live (engine.cpp:187-202): watermark resume, batch_full.
-    if (susp && live < __dmul_rn(dp.watermark, cap)) susp = false;
-    const bool full = running + waiting >= mb;
-    const bool eligible = act && !susp && !full;
-    const bool overflow = eligible && nonempty && (sp.first < base || sp.last >= base + ring);
-
-    // Partial try_place over this warp's slots s_m = B + warp + kLaneWarps*m.
-    // The instance-independent part of peak_in_slot (the in-slot test and
-    // dt = eval_t - t0, dispatcher.cpp:34-41) is computed once per slot by
-    // lane m and broadcast; each lane then adds its instance's P + k*dt.
-    uint32_t viol = 0xffffffffu;
-    uint64_t peak = 0;  // raw bits: totals are non-negative (prompt >= 0, k > 0)
     {
-      // 32-bit slot offsets from the pool origin B (the ring spans < 2^31).
-      const int32_t lo_off = static_cast<int32_t>(base - B);
-      const int32_t first_off = static_cast<int32_t>(sp.first - B);
-      const int32_t last_off = static_cast<int32_t>(sp.last - B);
-      const int32_t my_top = eligible ? static_cast<int32_t>((hi > sp.last ? hi : sp.last) - B) : -1;
-      const int32_t top = static_cast<int32_t>(__reduce_max_sync(0xffffffffu, static_cast<uint32_t>(my_top + 1))) - 1;
-      const int32_t nslots = top >= warp ? (top - warp) / kLaneWarps + 1 : 0;
-      for (int32_t m0 = 0; m0 < nslots; m0 += 32) {
-        // lane j describes slot offset o_j = warp + kLaneWarps * (m0 + j)
-        const int32_t oj = warp + kLaneWarps * (m0 + lane);
-        const double slot_start = __dmul_rn(static_cast<double>(B + oj), dp.slot_len);
-        const double slot_end = __dadd_rn(slot_start, dp.slot_len);
-        const bool zero = slot_end <= sp.t0e || slot_start >= sp.tee;
-        const double eval_t = (sp.t_end < slot_end) ? sp.t_end : slot_end;
-        const double dtj = zero ? -1.0 : __dsub_rn(eval_t, sp.t0);  // dt >= 0 when not zero
-        const int cnt = nslots - m0 < 32 ? nslots - m0 : 32;
+      uint64_t run = kZeroBits;
+      for (int32_t o = hi_off; o > c_off && o >= lo_off; --o) {
+        const int p2 = static_cast<int>((B + o) & rmask);
+        if (se[p2 * 32 + lane]) {
+          const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+          run = tb > run ? tb : run;
+        }
+        sm[p2 * 32 + lane] = run;
+      }
+    }
+
+    // Head prefetch (registers, lane = head of the next batch): queue index
+    // first, the request fields two decisions later, the agent's T after
+    // that, so the dependent global loads overlap the decisions.
+    int64_t nx_start = pos0, nx_n = 0;
+    uint32_t nx_idx = 0;
+    int32_t nx_agent = 0;
+    int64_t nx_prompt = 0, nx_kept = 0;
+    uint64_t nx_uid = 0;
+    double nx_T = 0.0;
+    int stage = 0;
+    auto issue_idx = [&](int64_t start) {
+      nx_start = start;
+      nx_n = q_end - start < kWHB ? q_end - start : kWHB;
+      if (nx_n < 0) nx_n = 0;
+      nx_idx = lane < nx_n ? hp[start + lane] : 0u;
+      stage = 0;
+    };
+    auto issue_fields = [&]() {
+      if (lane < nx_n) {
+        nx_agent = q.agent[nx_idx];
+        nx_prompt = q.prompt[nx_idx];
+        nx_kept = q.kept[nx_idx];
+        nx_uid = q.uid[nx_idx];
+        if (dp.oracle_T) nx_T = q.pure_exec[nx_idx];
+      }
+      stage = 1;
+    };
+    auto issue_T = [&]() {
+      if (!dp.oracle_T && lane < nx_n) nx_T = ag.T[nx_agent];
+      stage = 2;
+    };
+    issue_idx(pos0);
+
+    int64_t pos = pos0, hb_start = pos0, hb_n = 0;
+    int64_t nrows = nrows0, nadm = nadm0;
+    int retries = 0;
+    bool broke = false;
+
+    while (pos < q_end) {
+      if (pos >= hb_start + hb_n) {  // next head batch (a prefix of the pool's order)
+        if (stage < 1) issue_fields();
+        if (stage < 2) issue_T();
+        hb_start = nx_start;
+        hb_n = nx_n;
+        if (lane < hb_n) {
+          h_idx[lane] = nx_idx;
+          h_agent[lane] = nx_agent;
+          h_prompt[lane] = nx_prompt;
+          h_kept[lane] = nx_kept;
+          h_uid[lane] = nx_uid;
+          h_T[lane] = nx_T;
+          int64_t f, l;
+          span_bounds_dev(now, nx_T, L, &f, &l);
+          h_first[lane] = f;
+          h_last[lane] = l;
+          // Fast shape: T > 0, P >= 0, span [c, last] within the table, and
+          // peak_in_slot zero on the two slots each side of the span.
+          bool fast = nx_T > 0.0 && nx_prompt >= 0 && f == cslot && l >= f && l - f + 1 <= kDtSlots;
+          if (fast) {
+            const double te = __dadd_rn(now, nx_T);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            const double m0 = slot_dt(now, t0e, te, tee, f - 2, L);
+            const double m1 = slot_dt(now, t0e, te, tee, f - 1, L);
+            const double m2 = slot_dt(now, t0e, te, tee, l + 1, L);
+            const double m3 = slot_dt(now, t0e, te, tee, l + 2, L);
+            fast = m0 != m0 && m1 != m1 && m2 != m2 && m3 != m3;
+          }
+          h_mode[lane] = fast ? (k_uniform ? kModeTabPk : kModeTabDt) : kModeGeneric;
+        }
+        __syncwarp();
+        // (P + k * dt) (or dt) table of every fast head's span, lanes over slots.
+        for (int hh = 0; hh < hb_n; ++hh) {
+          const int mode = h_mode[hh];
+          if (mode == kModeGeneric) continue;
+          const double Th = h_T[hh];
+          const double Ph = static_cast<double>(h_prompt[hh]);
+          const double te = __dadd_rn(now, Th);
+          const double tee = __dsub_rn(te, kTimeEpsilon);
+          const int tn = static_cast<int>(h_last[hh] - h_first[hh] + 1);
+          for (int j = lane; j < tn; j += 32) {
+            const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
+            stab[hh * kDtSlots + j] = mode == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
+          }
+        }
+        __syncwarp();
+        issue_idx(hb_start + hb_n);
+      }
+      const int h = static_cast<int>(pos - hb_start);
+      if (stage == 0 && h >= 2) issue_fields();
+      else if (stage == 1 && h >= 4) issue_T();
+
+      const int64_t prompt = h_prompt[h];
+      const double P = static_cast<double>(prompt);
+      const int64_t first = h_first[h];
+      const int64_t last = h_last[h];
+      const int mode = h_mode[h];
+      const bool nonempty = last >= first;
+
+      // collect_live (engine.cpp:187-202): watermark resume, batch_full.
+      if (susp && live < wcap) susp = false;
+      const bool full = running + waiting >= mb;
+      const bool eligible = act && !susp && !full;
+      const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
+      if (__any_sync(0xffffffffu, overflow)) {
+        status = KX_ERR_CAPACITY;
+        broke = true;
+        break;
+      }
+
+      // try_place (dispatcher.cpp:52-68) for this lane's instance.
+      uint32_t viol = 0xffffffffu;  // first violating slot offset from B
+      uint64_t peak = kZeroBits;    // ordered bits
+      const int32_t fo = static_cast<int32_t>(first - B);
+      const int32_t lo = static_cast<int32_t>(last - B);
+      if (mode != kModeGeneric) {
+        if (eligible) {
+          const int32_t qo = lo + 1;
+          const uint64_t above = (qo <= hi_off) ? sm[static_cast<int>((B + qo) & rmask) * 32 + lane] : kZeroBits;
+          peak = lomax > above ? lomax : above;
+          const double* tab = stab + h * kDtSlots;
+          const int tn = lo - fo + 1;
+          int p2 = static_cast<int>((B + fo) & rmask);
+          if (mode == kModeTabPk) {
 #pragma unroll 4
-        for (int j = 0; j < cnt; ++j) {
-          const double dt = __shfl_sync(0xffffffffu, dtj, j);  // all lanes take part
-          const int32_t o = warp + kLaneWarps * (m0 + j);
-          if (!eligible || o < lo_off) continue;
-          const int p2 = static_cast<int>((B + o) & (ring - 1));
-          const bool in_span = o >= first_off && o <= last_off;
-          const bool exists = se[p2 * 32 + lane] != 0;
-          if (!(in_span || exists)) continue;
-          const double used = exists ? su[p2 * 32 + lane] : 0.0;
-          const double pk = dt < 0.0 ? 0.0 : __dadd_rn(P, __dmul_rn(kr, dt));
-          const double total = __dadd_rn(used, pk);
+            for (int j = 0; j < tn; ++j) {
+              const double total = __dadd_rn(su[p2 * 32 + lane], tab[j]);
+              if (total > cap && viol == 0xffffffffu) viol = static_cast<uint32_t>(fo + j);
+              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+              peak = tb > peak ? tb : peak;
+              p2 = (p2 + 1) & rmask;
+            }
+          } else {
+#pragma unroll 4
+            for (int j = 0; j < tn; ++j) {
+              const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[j]));
+              if (total > cap && viol == 0xffffffffu) viol = static_cast<uint32_t>(fo + j);
+              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+              peak = tb > peak ? tb : peak;
+              p2 = (p2 + 1) & rmask;
+            }
+          }
+        }
+      } else if (eligible) {  // generic slot walk over the whole window
+        const double te = __dadd_rn(now, h_T[h]);
+        const double tee = __dsub_rn(te, kTimeEpsilon);
+        const int32_t top = hi_off > lo ? hi_off : lo;
+        for (int32_t o = lo_off; o <= top; ++o) {
+          const int p2 = static_cast<int>((B + o) & rmask);
+          const bool e = se[p2 * 32 + lane] != 0;
+          const bool in_span = o >= fo && o <= lo;
+          if (!(e || in_span)) continue;
+          const double used = e ? su[p2 * 32 + lane] : 0.0;
+          const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
           if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
-          const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total));
+          const uint64_t tb = ordered_bits(total);
           peak = tb > peak ? tb : peak;
         }
       }
-    }
-    pv[(par * kLaneWarps + warp) * 32 + lane] = viol;
-    pp[(par * kLaneWarps + warp) * 32 + lane] = peak;
-    if (overflow) atomicExch(&s_status, KX_ERR_CAPACITY);
-    __syncthreads();
-    if (s_status != KX_OK) {
-      broke = true;
-      break;
-    }
+      const bool fits = eligible && viol == 0xffffffffu;
+      // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
+      const uint64_t key = fits ? peak : ~0ull;
+      const uint64_t wkey = warp_min_u64(key);
+      const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
+      const int bl = winners ? __ffs(winners) - 1 : -1;
+      const int bsrc = bl >= 0 ? bl : 0;
+      const double bpeak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
+      const double blive = __shfl_sync(0xffffffffu, live, bsrc);
+      const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
+      const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
+      const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
 
-    // Combine the partials of all warps for this lane's instance.
-#pragma unroll
-    for (int w = 0; w < kLaneWarps; ++w) {
-      if (w == warp) continue;
-      const uint32_t v2 = pv[(par * kLaneWarps + w) * 32 + lane];
-      const uint64_t p2 = pp[(par * kLaneWarps + w) * 32 + lane];
-      viol = v2 < viol ? v2 : viol;
-      peak = p2 > peak ? p2 : peak;
-    }
-    const bool fits = eligible && viol == 0xffffffffu;
-    // select_instance: min (peak, InstanceId) (H9), all warps identically.
-    const uint64_t key = fits ? peak : ~0ull;
-    const uint64_t wkey = warp_min_u64(key);
-    const uint32_t uid_ = static_cast<uint32_t>(id) ^ 0x80000000u;
-    const uint32_t wid = __reduce_min_sync(0xffffffffu, (fits && key == wkey) ? uid_ : 0xffffffffu);
-    const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey && uid_ == wid);
-    const int bl = winners ? __ffs(winners) - 1 : -1;
-    const double bpeak = bl >= 0 ? __longlong_as_double(static_cast<long long>(wkey)) : 0.0;
-    const double blive = __shfl_sync(0xffffffffu, live, bl >= 0 ? bl : 0);
-    const double bcap = __shfl_sync(0xffffffffu, cap, bl >= 0 ? bl : 0);
-    const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
-    const int32_t bid = __shfl_sync(0xffffffffu, id, bl >= 0 ? bl : 0);
-
-    if (warp == 0) {  // decision log (engine.cpp:242-246)
-      if (nrows < dp.log_cap) {
+      if (nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
         const int64_t r = int64_t(pool) * dp.log_cap + nrows;
         if (lane == 0) {
           kx_decision d;
           d.time = now;
           d.predicted_peak = bpeak;
-          d.uid = SL(uint64_t, h_uid)[h];
-          d.queue_index = SL(uint32_t, h_idx)[h];
-          d.agent = SL(int32_t, h_agent)[h];
+          d.uid = h_uid[h];
+          d.queue_index = h_idx[h];
+          d.agent = h_agent[h];
           d.target = bl >= 0 ? bid : -1;
           d.pool = pool;
           d.admitted = (bl >= 0 && !overload) ? 1 : 0;
@@ -757,112 +909,135 @@ k_dispatch_lanes(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         if (act) {
           double v = -1.0;
           if (eligible) {
-            v = fits ? __longlong_as_double(static_cast<long long>(peak))
+            v = fits ? from_ordered_bits(peak)
                      : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
           }
-          cand[r * dp.peak_stride + lane] = v;
+          cand[r * dp.peak_stride + li] = v;
         }
       }
-    }
-    ++nrows;
-    if (bl < 0) {  // head keeps its place (engine.cpp:247)
-      broke = true;
-      break;
-    }
-    if (overload) {
-      if (lane == bl) susp = true;  // Dispatcher::on_overload
-      if (++retries > ni) {
-        if (threadIdx.x == 0) s_status = KX_ERR_LIVELOCK;
+      ++nrows;
+      if (bl < 0) {  // head keeps its place (engine.cpp:247)
         broke = true;
         break;
       }
-      par ^= 1;
-      continue;
-    }
-    retries = 0;
-    // Dispatcher::commit: each warp books the target's span slots it owns.
-    {
-      const double kt = __shfl_sync(0xffffffffu, kr, bl);
-      const int64_t f0 = sp.first + ((((B + warp) - sp.first) % kLaneWarps) + kLaneWarps) % kLaneWarps;
-      for (int64_t s = f0 + int64_t(lane) * kLaneWarps; s <= sp.last; s += 32 * kLaneWarps) {
-        const int p2 = static_cast<int>(s & (ring - 1));
-        su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pis(sp, P, kt, s, dp.slot_len));
-        se[p2 * 32 + bl] = 1;
+      if (overload) {
+        if (lane == bl) susp = true;  // Dispatcher::on_overload
+        if (++retries > ni) {
+          status = KX_ERR_LIVELOCK;
+          broke = true;
+          break;
+        }
+        continue;
       }
-      if (lane == bl) {
-        if (nonempty && sp.last > hi) hi = sp.last;
-        live = __dadd_rn(live, static_cast<double>(prompt + SL(int64_t, h_kept)[h]));  // admit
-        running += 1;
-      }
-      if (lane == bl) {
-        if (nact < kActiveCap) {
-          if (warp == 0) {  // active_[uid] = m (dispatcher.cpp:78): stores only
-            q.admitted[SL(uint32_t, h_idx)[h]] = 1;
+      retries = 0;
+      // Dispatcher::commit: book the target's span slots (lanes = slots),
+      // then refresh the target's suffix max from the span's end down.
+      {
+        const double kt = __shfl_sync(0xffffffffu, kr, bl);
+        const int32_t bhi = __shfl_sync(0xffffffffu, hi_off, bl);
+        const double T = h_T[h];
+        if (mode != kModeGeneric) {
+          const double* tab = stab + h * kDtSlots;
+          for (int64_t s = first + lane; s <= last; s += 32) {
+            const int p2 = static_cast<int>(s & rmask);
+            const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
+            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk);
+            se[p2 * 32 + bl] = 1;
+          }
+        } else {
+          const double te = __dadd_rn(now, T);
+          const double tee = __dsub_rn(te, kTimeEpsilon);
+          for (int64_t s = first + lane; s <= last; s += 32) {
+            const int p2 = static_cast<int>(s & rmask);
+            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
+            se[p2 * 32 + bl] = 1;
+          }
+        }
+        __syncwarp();
+        if (lane == bl && nonempty && lo > c_off) {
+          // the target's suffix max over offsets (c, lo], walking down from lo
+          uint64_t run = (lo + 1 <= bhi) ? sm[static_cast<int>((B + lo + 1) & rmask) * 32 + bl] : kZeroBits;
+          for (int32_t o = lo; o > c_off && o >= lo_off; --o) {
+            const int p2 = static_cast<int>((B + o) & rmask);
+            if (se[p2 * 32 + bl]) {
+              const uint64_t tb = ordered_bits(su[p2 * 32 + bl]);
+              run = tb > run ? tb : run;
+            }
+            sm[p2 * 32 + bl] = run;
+          }
+        }
+        if (lane == bl) {
+          if (nonempty && last > hi) {
+            hi = last;
+            hi_off = lo;
+          }
+          live = __dadd_rn(live, static_cast<double>(prompt + h_kept[h]));  // admit
+          running += 1;
+          if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78)
+            q.admitted[h_idx[h]] = 1;
             const int64_t o = int64_t(i) * kActiveCap + nact;
-            in.act_uid[o] = SL(uint64_t, h_uid)[h];
+            in.act_uid[o] = h_uid[h];
             in.act_P[o] = P;
             in.act_k[o] = kt;
             in.act_t0[o] = now;
-            in.act_T[o] = SL(double, h_T)[h];
+            in.act_T[o] = T;
+            ++nact;
+          } else {
+            status = KX_ERR_CAPACITY;
           }
-          ++nact;
-        } else if (warp == 0) {
-          s_status = KX_ERR_CAPACITY;
+        }
+        if (__any_sync(0xffffffffu, status != KX_OK)) {
+          status = KX_ERR_CAPACITY;
+          broke = true;
+          break;
         }
       }
+      ++nadm;
+      ++pos;
     }
-    ++nadm;
-    ++pos;
-    par ^= 1;
-  }
-  __syncthreads();
-  // Phase 1 ran out of prefix heads without finishing the round: hand the
-  // state to the continuation (no gc yet: the round is not over).
-  const bool defer_rest = ph.phase == 1 && !broke && s_status == KX_OK && pos >= q_end && q_end < pool_n;
-  if (!defer_rest) {
-    // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
-    const int64_t current =
-        static_cast<int64_t>(floor(__ddiv_rn(__dadd_rn(now, kTimeEpsilon), dp.slot_len)));
-    if (act && current > base) {
-      const int64_t stop = current < base + ring ? current : base + ring;
-      for (int64_t s = base + warp; s < stop; s += kLaneWarps) {
-        const int p2 = static_cast<int>(s & (ring - 1));
-        su[p2 * 32 + lane] = 0.0;
-        se[p2 * 32 + lane] = 0;
+    // Phase 1 ran out of prefix heads without finishing the round: hand the
+    // state to the continuation (no gc yet: the round is not over).
+    const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
+    if (!defer_rest) {
+      // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
+      if (act && cslot > base) {
+        const int64_t stop = cslot < base + ring ? cslot : base + ring;
+        for (int64_t s = base; s < stop; ++s) {
+          const int p2 = static_cast<int>(s & rmask);
+          su[p2 * 32 + lane] = 0.0;
+          se[p2 * 32 + lane] = 0;
+        }
+        base = cslot;
       }
-      base = current;
+    }
+    if (act) {
+      in.n_active[i] = nact;
+      if (!defer_rest) active_gc(in, i, now);
+      in.live_kv[i] = live;
+      in.base_slot[i] = base;
+      in.hi_slot[i] = hi;
+      in.running[i] = running;
+      in.suspended[i] = susp ? 1 : 0;
+    }
+    if (lane == 0) {
+      if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
+      if (!defer_rest) {
+        row_count[pool] = nrows;
+        admitted_count[pool] = nadm;
+        pool_status[pool] = status;
+      }
     }
   }
-  if (warp == 0 && act) {
-    in.n_active[i] = nact;
-    if (!defer_rest) active_gc(in, i, now);
-  }
   __syncthreads();
-  if (warp == 0 && act) {
-    in.live_kv[i] = live;
-    in.base_slot[i] = base;
-    in.hi_slot[i] = hi;
-    in.running[i] = running;
-    in.suspended[i] = susp ? 1 : 0;
-  }
-  for (int j = threadIdx.x; j < 32 * ring; j += kLaneThreads) {
-    const int li = j % 32, p2 = j / 32;
-    if (li < ni) {
+  for (int j = threadIdx.x; j < 32 * ring; j += kWarpThreads) {
+    const int l = j & 31, p2 = j >> 5;
+    const int li = s_li[l];
+    if (li >= 0) {
       in.usage[int64_t(ib + li) * ring + p2] = su[j];
       in.exists[int64_t(ib + li) * ring + p2] = se[j];
     }
   }
-  if (threadIdx.x == 0) {
-    if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
-    if (!defer_rest) {
-      row_count[pool] = nrows;
-      admitted_count[pool] = nadm;
-      pool_status[pool] = s_status;
-    }
-  }
 }
-
-#undef SL
 
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
 __global__ void k_ledger_try_place(InstDev in, int i, int ring, double P, double k, double t0,
@@ -979,7 +1154,7 @@ __global__ void k_gc_all(InstDev in, int n_inst, int ring, double now, double sl
 
 // ---- host wrappers -------------------------------------------------------
 void configure_dispatch_kernels() {
-  KX_CUDA(cudaFuncSetAttribute(k_dispatch_lanes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
@@ -988,7 +1163,7 @@ void configure_dispatch_kernels() {
 }
 
 bool dispatch_can_overlap(int max_inst_per_pool, int ring) {
-  return max_inst_per_pool <= 32 && lane_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
+  return max_inst_per_pool <= 32 && warp_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
 }
 
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
@@ -997,12 +1172,12 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st, DispPhase phase) {
   if (max_inst_per_pool <= 32) {
-    const LaneLayout ll = lane_layout(dp.ring);
-    if (ll.total <= static_cast<uint32_t>(kDispSmemLimit)) {
-      k_dispatch_lanes<<<n_pools, kLaneThreads, ll.total, st>>>(q, a, in, pool_begin, perm,
-                                                               pool_offsets, dp, ll, rows, cand,
-                                                               row_count, admitted_count,
-                                                               pool_status, phase);
+    const WarpLayout wl = warp_layout(dp.ring);
+    if (wl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+      k_dispatch_warp<<<n_pools, kWarpThreads, wl.total, st>>>(q, a, in, pool_begin, perm,
+                                                              pool_offsets, dp, wl, rows, cand,
+                                                              row_count, admitted_count,
+                                                              pool_status, phase);
       KX_CHECK_LAUNCH();
       return;
     }

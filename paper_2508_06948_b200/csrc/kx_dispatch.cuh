@@ -24,7 +24,7 @@ struct DispatchParams {
 
 struct TopKState;
 
-// Resumable dispatch round (k_dispatch_lanes): phase 1 walks a pool's top-K
+// Resumable dispatch round (k_dispatch_warp): phase 1 walks a pool's top-K
 // order prefix while the full sort runs; phase 2 continues from `start`
 // over the full order when phase 1 ran out of prefix heads.
 struct DispResume {

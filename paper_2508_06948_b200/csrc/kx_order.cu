@@ -638,54 +638,123 @@ __global__ void k_topk_compact(const uint32_t* __restrict__ keys, int64_t n, Ord
   }
 }
 
-// CTA per pool: exact order of the candidates (compact key, then the tuple).
-__global__ void __launch_bounds__(1024)
+// CTA per pool: exact order of the candidates. A bitonic sort of the
+// composite (compact key << 32 | candidate slot) in shared memory orders them
+// by compact key; runs of equal compact keys (whole runs: the candidate set
+// is a union of complete key values) are then re-sorted by the exact tuple,
+// short runs by one thread in registers, long runs by the CTA (exact records
+// staged in shared memory, rank by counting).
+constexpr int kTopKThreads = 1024;
+constexpr int kTopKShortRun = 16;
+constexpr int kTopKLongRuns = 64;
+
+size_t topk_sort_smem() {
+  return sizeof(uint64_t) * kTopKMax + sizeof(uint32_t) * kTopKMax + sizeof(uint32_t) * kTopKMax +
+         sizeof(TRec) * kTopKMax;
+}
+
+__global__ void __launch_bounds__(kTopKThreads)
 k_topk_sort(QueueDev q, int policy, const uint32_t* __restrict__ keys, OrderParams op,
             const TopKState* __restrict__ st, const uint32_t* __restrict__ cand,
             uint32_t* __restrict__ heads) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint32_t s_ls[kTopKLongRuns], s_ll[kTopKLongRuns];
+  __shared__ int s_nlong;
   const int p = blockIdx.x;
   const TopKState t = st[p];
   if (t.defer || t.empty) return;
   const int n = static_cast<int>(t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
-  uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw);
-  TRec* sr = reinterpret_cast<TRec*>(smem_raw + sizeof(uint32_t) * kTopKMax);
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* so = reinterpret_cast<uint32_t*>(sk + kTopKMax);
+  uint32_t* tmp = so + kTopKMax;
+  TRec* rec = reinterpret_cast<TRec*>(tmp + kTopKMax);
+  const uint32_t* pc = cand + int64_t(p) * kTopKMax;
   int p2 = 1;
   while (p2 < n) p2 <<= 1;
-  for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-    if (i < n) {
-      const uint32_t idx = cand[int64_t(p) * kTopKMax + i];
-      sk[i] = keys[idx];
-      sr[i] = load_rec(q, policy, idx);
-    } else {
-      sk[i] = 0xffffffffu;
-      sr[i].w0 = sr[i].w1 = sr[i].w2 = sr[i].msg = sr[i].uid = ~0ull;
-      sr[i].idx = 0xffffffffu;
-    }
-  }
+  for (int i = threadIdx.x; i < p2; i += blockDim.x)
+    sk[i] = i < n ? ((static_cast<uint64_t>(keys[pc[i]]) << 32) | static_cast<uint32_t>(i)) : ~0ull;
+  if (threadIdx.x == 0) s_nlong = 0;
   __syncthreads();
   for (int kk = 2; kk <= p2; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
       for (int i = threadIdx.x; i < p2; i += blockDim.x) {
         const int l = i ^ j;
         if (l > i) {
-          const bool up = (i & kk) == 0;
-          const bool lt_li = sk[l] < sk[i] || (sk[l] == sk[i] && rec_less(sr[l], sr[i]));
-          const bool lt_il = sk[i] < sk[l] || (sk[i] == sk[l] && rec_less(sr[i], sr[l]));
-          if (up ? lt_li : lt_il) {
-            const uint32_t tk = sk[i];
-            sk[i] = sk[l];
-            sk[l] = tk;
-            const TRec tr = sr[i];
-            sr[i] = sr[l];
-            sr[l] = tr;
+          const uint64_t a = sk[i], b = sk[l];
+          if ((a > b) == ((i & kk) == 0)) {
+            sk[i] = b;
+            sk[l] = a;
           }
         }
       }
       __syncthreads();
     }
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = sr[i].idx;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) so[i] = pc[static_cast<uint32_t>(sk[i])];
+  __syncthreads();
+  // Runs of equal compact keys: the exact tuple decides.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t k = static_cast<uint32_t>(sk[i] >> 32);
+    const bool start = (i == 0 || static_cast<uint32_t>(sk[i - 1] >> 32) != k) &&
+                       (i + 1 < n && static_cast<uint32_t>(sk[i + 1] >> 32) == k);
+    if (!start) continue;
+    int e = i + 2;
+    while (e < n && static_cast<uint32_t>(sk[e] >> 32) == k) ++e;
+    const int len = e - i;
+    if (len <= kTopKShortRun) {
+      TKey r[kTopKShortRun];
+      for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, so[i + j]);
+      for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
+        const TKey x = r[j];
+        int m = j - 1;
+        while (m >= 0 && tkey_less(q, x, r[m])) {
+          r[m + 1] = r[m];
+          --m;
+        }
+        r[m + 1] = x;
+      }
+      for (int j = 0; j < len; ++j) so[i + j] = r[j].idx;
+    } else {
+      const int slot = atomicAdd(&s_nlong, 1);
+      if (slot < kTopKLongRuns) {
+        s_ls[slot] = static_cast<uint32_t>(i);
+        s_ll[slot] = static_cast<uint32_t>(len);
+      }
+    }
+  }
+  __syncthreads();
+  const int nlong = s_nlong;
+  for (int r = 0; r < nlong; ++r) {
+    int st0, len;
+    if (nlong <= kTopKLongRuns) {
+      st0 = static_cast<int>(s_ls[r]);
+      len = static_cast<int>(s_ll[r]);
+    } else {  // more long runs than listed: one pass over the whole set
+      if (r > 0) break;
+      st0 = 0;
+      len = n;
+    }
+    for (int j = threadIdx.x; j < len; j += blockDim.x) rec[j] = load_rec(q, policy, so[st0 + j]);
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      const TRec x = rec[j];
+      int rank = 0;
+      if (nlong <= kTopKLongRuns) {
+        for (int m = 0; m < len; ++m) rank += rec_less(rec[m], x);
+      } else {  // whole set: compact key first
+        const uint32_t kx = static_cast<uint32_t>(sk[st0 + j] >> 32);
+        for (int m = 0; m < len; ++m) {
+          const uint32_t km = static_cast<uint32_t>(sk[m] >> 32);
+          rank += km < kx || (km == kx && rec_less(rec[m], x));
+        }
+      }
+      tmp[rank] = x.idx;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) so[st0 + j] = tmp[j];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = so[i];
 }
 
 void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
@@ -711,8 +780,7 @@ void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin
     KX_CHECK_LAUNCH();
   }
   KX_CUDA(cudaEventRecord(keys_released, st));  // the original keys are no longer read
-  const size_t smem = sizeof(uint32_t) * kTopKMax + sizeof(TRec) * kTopKMax;
-  k_topk_sort<<<op.n_pools, 1024, smem, st>>>(q, op.policy, keys, op, w.state, w.cand, w.heads);
+  k_topk_sort<<<op.n_pools, kTopKThreads, topk_sort_smem(), st>>>(q, op.policy, keys, op, w.state, w.cand, w.heads);
   KX_CHECK_LAUNCH();
 }
 
@@ -822,7 +890,7 @@ void init_ranges(PoolRange* r, int n, cudaStream_t st) {
 
 void configure_sort_kernels() {
   KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sizeof(uint32_t) * kTopKMax + sizeof(TRec) * kTopKMax)));
+                               static_cast<int>(topk_sort_smem())));
   KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sort_dyn_smem<uint32_t>())));
 }
