@@ -17,6 +17,7 @@
 // ring, and every warp reduces the same arg-min over (peak, InstanceId)
 // (SURVEY H9), so one __syncthreads per decision suffices.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "kx_common.cuh"
@@ -1039,6 +1040,658 @@ k_dispatch_warp(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
   }
 }
 
+// ---- K5 pipelined: decider warp + look-ahead evaluator warp ----------------
+// Same decisions as k_dispatch_warp, with the chain's work split over two
+// warps that meet at one 64-thread named barrier per decision:
+//   * warp 1 (evaluator) runs one head ahead: it evaluates try_place for
+//     head pos + 1 for every instance against the state at the start of the
+//     step (lanes = instances), maintains the suffix maxima and loads the
+//     head batches;
+//   * warp 0 (decider) takes that row for head pos; only the instance the
+//     previous step committed to (or suspended) is stale, and it re-evaluates
+//     just that one (lanes = slots), then runs select_instance, the overload
+//     check, the decision log and the commit.
+// A step that ends in an overload retry keeps the decider's own row for the
+// next step (only the suspended instance changes). The evaluator's reads of
+// the column the decider is committing to in the same step are discarded by
+// construction (that lane is the one re-evaluated next step).
+constexpr int kPipeThreads = 128;
+constexpr int kHR = 64;  // head ring: two batches of kWHB
+
+struct PipeLayout {
+  uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
+      st_live, st_run, st_susp, st_hi, r_viol, r_peak, r_flag, usage, ex, sufm, total;
+};
+
+PipeLayout pipe_layout(int ring) {
+  PipeLayout L{};
+  uint32_t o = 0;
+  auto take = [&](size_t bytes) {
+    const uint32_t at = o;
+    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
+    return at;
+  };
+  L.h_idx = take(4 * kHR);
+  L.h_agent = take(4 * kHR);
+  L.h_prompt = take(8 * kHR);
+  L.h_kept = take(8 * kHR);
+  L.h_uid = take(8 * kHR);
+  L.h_T = take(8 * kHR);
+  L.h_first = take(8 * kHR);
+  L.h_last = take(8 * kHR);
+  L.h_mode = take(4 * kHR);
+  L.tab = take(size_t(8) * kHR * kDtSlots);
+  L.lane_inst = take(4 * 32);
+  L.st_live = take(8 * 32);
+  L.st_run = take(4 * 32);
+  L.st_susp = take(4 * 32);
+  L.st_hi = take(4 * 32);
+  L.r_viol = take(4 * 64);
+  L.r_peak = take(8 * 64);
+  L.r_flag = take(4 * 64);
+  L.usage = take(size_t(8) * 32 * ring);
+  L.ex = take(size_t(32) * ring);
+  L.sufm = take(size_t(8) * 32 * ring);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void pipe_sync() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+struct PipeCtl {
+  int64_t pos;      // head the decider takes next
+  int32_t stop;     // 1: the round is over
+  int32_t commit;   // lane committed in the last step (-1: none)
+};
+
+__global__ void __launch_bounds__(kPipeThreads)
+k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
+                const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
+                DispatchParams dp, PipeLayout lay, kx_decision* __restrict__ rows,
+                double* __restrict__ cand, int64_t* __restrict__ row_count,
+                int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
+                DispPhase ph) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ PipeCtl ctl[2];  // double-buffered by step parity
+  const int pool = blockIdx.x;
+  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
+  const uint32_t* hp = perm + pool_offsets[pool];
+  int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
+  bool skip = false;
+  if (ph.phase == 1) {
+    const TopKState t = ph.tk[pool];
+    if (t.defer) {  // too many ties at the boundary key: wait for the full order
+      if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
+      skip = true;
+    }
+    hp = ph.heads + int64_t(pool) * kTopKMax;
+    q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
+  } else if (ph.phase == 2) {
+    const DispResume r = ph.resume[pool];
+    skip = !r.need;
+    pos0 = r.start;
+    nrows0 = r.nrows;
+    nadm0 = r.nadm;
+  }
+  if (skip) return;  // uniform over the CTA
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ib = pool_begin[pool];
+  const int ni = pool_begin[pool + 1] - ib;
+  const int ring = dp.ring;
+  const int rmask = ring - 1;
+#define PL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
+  double* const su = PL(double, usage);
+  uint8_t* const se = PL(uint8_t, ex);
+  uint64_t* const sm = PL(uint64_t, sufm);
+  int32_t* const s_li = PL(int32_t, lane_inst);
+  uint32_t* const h_idx = PL(uint32_t, h_idx);
+  int32_t* const h_agent = PL(int32_t, h_agent);
+  int64_t* const h_prompt = PL(int64_t, h_prompt);
+  int64_t* const h_kept = PL(int64_t, h_kept);
+  uint64_t* const h_uid = PL(uint64_t, h_uid);
+  double* const h_T = PL(double, h_T);
+  int64_t* const h_first = PL(int64_t, h_first);
+  int64_t* const h_last = PL(int64_t, h_last);
+  int32_t* const h_mode = PL(int32_t, h_mode);
+  double* const stab = PL(double, tab);
+  double* const st_live = PL(double, st_live);
+  int32_t* const st_run = PL(int32_t, st_run);
+  int32_t* const st_susp = PL(int32_t, st_susp);
+  int32_t* const st_hi = PL(int32_t, st_hi);
+  uint32_t* const r_viol = PL(uint32_t, r_viol);
+  uint64_t* const r_peak = PL(uint64_t, r_peak);
+  uint32_t* const r_flag = PL(uint32_t, r_flag);
+#undef PL
+  const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
+  constexpr uint32_t kNone = 0xffffffffu;
+
+  // Lane of each instance: rank of its InstanceId within the pool (H9).
+  if (warp == 0) {
+    const int32_t myid = lane < ni ? in.id[ib + lane] : 0x7fffffff;
+    int rank = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t o = __shfl_sync(0xffffffffu, myid, l);
+      rank += (l < ni) && (o < myid || (o == myid && l < lane));
+    }
+    s_li[lane] = -1;
+    __syncwarp();
+    if (lane < ni) s_li[rank] = lane;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 32 * ring; j += kPipeThreads) {
+    const int l = j & 31, pos = j >> 5;
+    const int li = s_li[l];
+    su[j] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
+    se[j] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+  }
+  __syncthreads();
+
+  if (warp < 2) {
+    // ---- per-lane instance constants (both warps) ----
+    const double now = dp.now;
+    const double L = dp.slot_len;
+    const int li = s_li[lane];
+    const bool act = li >= 0;
+    const int i = ib + (act ? li : 0);
+    const double cap = act ? in.cap[i] : 0.0;
+    const double kr = act ? in.decode_rate[i] : 0.0;
+    const int32_t mb = act ? in.max_batch[i] : 0;
+    const int32_t id = act ? in.id[i] : 0x7fffffff;
+    const int32_t waiting = act ? in.waiting[i] : 0;
+    const double wcap = __dmul_rn(dp.watermark, cap);
+    const int64_t base = act ? in.base_slot[i] : 0;
+    const int64_t hi0 = act ? in.hi_slot[i] : -1;
+    const double k0 = __shfl_sync(0xffffffffu, kr, 0);
+    const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
+    const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
+    const int32_t lo_off = static_cast<int32_t>(base - B);
+    const double t0e = __dadd_rn(now, kTimeEpsilon);
+    const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
+    const int32_t c_off = static_cast<int32_t>(cslot - B);
+    // stored slots below c: one max per instance, fixed for the round
+    uint64_t lomax = kZeroBits;
+    for (int32_t o = lo_off; o < c_off && o <= static_cast<int32_t>(hi0 - B); ++o) {
+      const int p2 = static_cast<int>((B + o) & rmask);
+      if (se[p2 * 32 + lane]) {
+        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+        lomax = tb > lomax ? tb : lomax;
+      }
+    }
+
+    if (warp == 1) {
+      // =========================== evaluator ===========================
+      // initial suffix maxima over offsets (c, hi]
+      {
+        uint64_t run = kZeroBits;
+        for (int32_t o = static_cast<int32_t>(hi0 - B); o > c_off && o >= lo_off; --o) {
+          const int p2 = static_cast<int>((B + o) & rmask);
+          if (se[p2 * 32 + lane]) {
+            const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+            run = tb > run ? tb : run;
+          }
+          sm[p2 * 32 + lane] = run;
+        }
+      }
+      // head prefetch registers (lane = head of the next batch)
+      int64_t nx_start = pos0, nx_n = 0;
+      uint32_t nx_idx = 0;
+      int32_t nx_agent = 0;
+      int64_t nx_prompt = 0, nx_kept = 0;
+      uint64_t nx_uid = 0;
+      double nx_T = 0.0;
+      int stage = 0;
+      auto issue_idx = [&](int64_t start) {
+        nx_start = start;
+        nx_n = q_end - start < kWHB ? q_end - start : kWHB;
+        if (nx_n < 0) nx_n = 0;
+        nx_idx = lane < nx_n ? hp[start + lane] : 0u;
+        stage = 0;
+      };
+      auto issue_fields = [&]() {
+        if (lane < nx_n) {
+          nx_agent = q.agent[nx_idx];
+          nx_prompt = q.prompt[nx_idx];
+          nx_kept = q.kept[nx_idx];
+          nx_uid = q.uid[nx_idx];
+          if (dp.oracle_T) nx_T = q.pure_exec[nx_idx];
+        }
+        stage = 1;
+      };
+      auto issue_T = [&]() {
+        if (!dp.oracle_T && lane < nx_n) nx_T = ag.T[nx_agent];
+        stage = 2;
+      };
+      int64_t loaded_end = pos0;  // heads [.., loaded_end) are in the ring
+      // Move the prefetched batch into its ring half and build its tables.
+      auto land_batch = [&]() {
+        if (stage < 1) issue_fields();
+        if (stage < 2) issue_T();
+        const int half = static_cast<int>(((nx_start - pos0) / kWHB) & 1);
+        const int hb = half * kWHB;
+        const int n = static_cast<int>(nx_n);
+        if (lane < n) {
+          const int hs = hb + lane;
+          h_idx[hs] = nx_idx;
+          h_agent[hs] = nx_agent;
+          h_prompt[hs] = nx_prompt;
+          h_kept[hs] = nx_kept;
+          h_uid[hs] = nx_uid;
+          h_T[hs] = nx_T;
+          int64_t f, l;
+          span_bounds_dev(now, nx_T, L, &f, &l);
+          h_first[hs] = f;
+          h_last[hs] = l;
+          bool fast = nx_T > 0.0 && nx_prompt >= 0 && f == cslot && l >= f && l - f + 1 <= kDtSlots;
+          if (fast) {
+            const double te = __dadd_rn(now, nx_T);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            const double m0 = slot_dt(now, t0e, te, tee, f - 2, L);
+            const double m1 = slot_dt(now, t0e, te, tee, f - 1, L);
+            const double m2 = slot_dt(now, t0e, te, tee, l + 1, L);
+            const double m3 = slot_dt(now, t0e, te, tee, l + 2, L);
+            fast = m0 != m0 && m1 != m1 && m2 != m2 && m3 != m3;
+          }
+          h_mode[hs] = fast ? (k_uniform ? kModeTabPk : kModeTabDt) : kModeGeneric;
+        }
+        __syncwarp();
+        for (int hh = 0; hh < n; ++hh) {
+          const int hs = hb + hh;
+          const int mode = h_mode[hs];
+          if (mode == kModeGeneric) continue;
+          const double Th = h_T[hs];
+          const double Ph = static_cast<double>(h_prompt[hs]);
+          const double te = __dadd_rn(now, Th);
+          const double tee = __dsub_rn(te, kTimeEpsilon);
+          const int tn = static_cast<int>(h_last[hs] - h_first[hs] + 1);
+          for (int j = lane; j < tn; j += 32) {
+            const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
+            stab[hs * kDtSlots + j] = mode == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
+          }
+        }
+        __syncwarp();
+        loaded_end = nx_start + nx_n;
+        issue_idx(loaded_end);
+      };
+      // try_place of head `hpos` for this lane's instance against the
+      // current state (published by the decider) -> row[par].
+      auto evaluate = [&](int64_t hpos, int par) {
+        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
+        const int mode = h_mode[hs];
+        const int64_t first = h_first[hs];
+        const int64_t last = h_last[hs];
+        const double P = static_cast<double>(h_prompt[hs]);
+        const int32_t fo = static_cast<int32_t>(first - B);
+        const int32_t lo = static_cast<int32_t>(last - B);
+        const bool nonempty = last >= first;
+        const double live = st_live[lane];
+        const bool susp = st_susp[lane] != 0 && !(live < wcap);
+        const bool eligible = act && !susp && !(st_run[lane] + waiting >= mb);
+        const int32_t hi_off = st_hi[lane];
+        uint32_t viol = kNone;
+        uint64_t peak = kZeroBits;
+        const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
+        if (eligible) {
+          if (mode != kModeGeneric) {
+            const int32_t qo = lo + 1;
+            const uint64_t above = (qo <= hi_off) ? sm[static_cast<int>((B + qo) & rmask) * 32 + lane] : kZeroBits;
+            peak = lomax > above ? lomax : above;
+            const double* tab = stab + hs * kDtSlots;
+            const int tn = lo - fo + 1;
+            int p2 = static_cast<int>((B + fo) & rmask);
+            if (mode == kModeTabPk) {
+#pragma unroll 4
+              for (int j = 0; j < tn; ++j) {
+                const double total = __dadd_rn(su[p2 * 32 + lane], tab[j]);
+                if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + j);
+                const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+                peak = tb > peak ? tb : peak;
+                p2 = (p2 + 1) & rmask;
+              }
+            } else {
+#pragma unroll 4
+              for (int j = 0; j < tn; ++j) {
+                const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[j]));
+                if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + j);
+                const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+                peak = tb > peak ? tb : peak;
+                p2 = (p2 + 1) & rmask;
+              }
+            }
+          } else {  // generic slot walk over the whole window
+            const double te = __dadd_rn(now, h_T[hs]);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            const int32_t top = hi_off > lo ? hi_off : lo;
+            for (int32_t o = lo_off; o <= top; ++o) {
+              const int p2 = static_cast<int>((B + o) & rmask);
+              const bool e = se[p2 * 32 + lane] != 0;
+              const bool in_span = o >= fo && o <= lo;
+              if (!(e || in_span)) continue;
+              const double used = e ? su[p2 * 32 + lane] : 0.0;
+              const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
+              if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
+              const uint64_t tb = ordered_bits(total);
+              peak = tb > peak ? tb : peak;
+            }
+          }
+        }
+        r_viol[par * 32 + lane] = viol;
+        r_peak[par * 32 + lane] = peak;
+        r_flag[par * 32 + lane] = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+      };
+
+      issue_idx(pos0);
+      pipe_sync();  // the decider's state is published
+      if (pos0 < q_end) {
+        land_batch();
+        evaluate(pos0, 0);
+      }
+      pipe_sync();
+      int step = 0;
+      while (true) {
+        // Iteration j runs beside the decider's step j - 1 and reads what
+        // the decider published in step j - 2 (ctl[j & 1]).
+        const int j = step + 1;
+        const PipeCtl c = ctl[j & 1];
+        if (c.stop) break;
+        step = j;
+        if (c.commit >= 0) {
+          // the committed instance's suffix max over (c, hi], from hi down
+          const int t = c.commit;
+          const int32_t hi_t = st_hi[t];
+          uint64_t carry = kZeroBits;
+          for (int32_t top = hi_t; top > c_off; top -= 32) {
+            const int32_t o = top - lane;
+            const bool valid = o > c_off;
+            const int p2 = static_cast<int>((B + o) & rmask);
+            uint64_t v = (valid && se[p2 * 32 + t]) ? ordered_bits(su[p2 * 32 + t]) : kZeroBits;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint64_t w = shfl_up_u64(v, d);
+              if (lane >= d && w > v) v = w;
+            }
+            v = carry > v ? carry : v;
+            if (valid) sm[p2 * 32 + t] = v;
+            carry = shfl_u64(v, 31);
+          }
+          __syncwarp();
+        }
+        const int64_t epos = c.pos + 1;  // speculate: the decider admits head pos
+        if (epos < q_end) {
+          if (epos >= loaded_end) land_batch();
+          else if (stage == 0 && epos >= nx_start - kWHB + 2) issue_fields();
+          else if (stage == 1 && epos >= nx_start - kWHB + 4) issue_T();
+          evaluate(epos, step & 1);
+        }
+        pipe_sync();
+      }
+    } else {
+      // ============================ decider ============================
+      double live = act ? in.live_kv[i] : 0.0;
+      int32_t running = act ? in.running[i] : 0;
+      bool susp = act ? in.suspended[i] != 0 : false;
+      int64_t hi = hi0;
+      int32_t hi_off = static_cast<int32_t>(hi0 - B);
+      int32_t nact = act ? in.n_active[i] : 0;
+      st_live[lane] = live;
+      st_run[lane] = running;
+      st_susp[lane] = susp ? 1 : 0;
+      st_hi[lane] = hi_off;
+      if (lane == 0) ctl[1] = PipeCtl{pos0, 0, -1};
+      pipe_sync();
+      pipe_sync();  // the evaluator's row for pos0 is ready
+      int64_t pos = pos0;
+      int64_t nrows = nrows0, nadm = nadm0;
+      int retries = 0;
+      bool broke = false;
+      int status = KX_OK;
+      int step = 0;
+      int tfix = -1;        // lane whose row entry is stale
+      bool own_row = false; // retry: keep the decider's row
+      uint32_t viol = kNone;
+      uint64_t peak = kZeroBits;
+      bool elig = false, ovf = false;
+      while (pos < q_end) {
+        const int hs = static_cast<int>((pos - pos0) & (kHR - 1));
+        const int64_t prompt = h_prompt[hs];
+        const double P = static_cast<double>(prompt);
+        const int64_t first = h_first[hs];
+        const int64_t last = h_last[hs];
+        const int mode = h_mode[hs];
+        const double T = h_T[hs];
+        const bool nonempty = last >= first;
+        const int32_t fo = static_cast<int32_t>(first - B);
+        const int32_t lo = static_cast<int32_t>(last - B);
+        // collect_live (engine.cpp:187-202): watermark resume, batch_full.
+        if (susp && live < wcap) {
+          susp = false;
+          st_susp[lane] = 0;
+        }
+        const bool my_elig = act && !susp && !(running + waiting >= mb);
+        if (!own_row) {
+          viol = r_viol[(step & 1) * 32 + lane];
+          peak = r_peak[(step & 1) * 32 + lane];
+          const uint32_t f = r_flag[(step & 1) * 32 + lane];
+          elig = f & 1u;
+          ovf = (f & 2u) != 0;
+        }
+        if (tfix >= 0) {
+          // re-evaluate the stale instance (lanes = slots)
+          const int t = tfix;
+          const bool e_t = __shfl_sync(0xffffffffu, my_elig, t);
+          uint32_t v_t = kNone;
+          uint64_t p_t = kZeroBits;
+          bool o_t = false;
+          if (e_t) {
+            const int32_t lo_t = __shfl_sync(0xffffffffu, lo_off, t);
+            const int32_t hio_t = __shfl_sync(0xffffffffu, hi_off, t);
+            const double cap_t = __shfl_sync(0xffffffffu, cap, t);
+            const double k_t = __shfl_sync(0xffffffffu, kr, t);
+            const int64_t base_t = B + lo_t;
+            o_t = nonempty && (first < base_t || last >= base_t + ring);
+            const bool fast = mode != kModeGeneric;
+            const int32_t w0 = fast ? fo : lo_t;
+            const int32_t w1 = hio_t > lo ? hio_t : lo;
+            const double* tab = stab + hs * kDtSlots;
+            const double te = __dadd_rn(now, T);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            uint32_t vv = kNone;
+            uint64_t pp = fast ? shfl_u64(lomax, t) : kZeroBits;
+            for (int32_t o0 = w0; o0 <= w1; o0 += 32) {
+              const int32_t o = o0 + lane;
+              if (o <= w1) {
+                const int p2 = static_cast<int>((B + o) & rmask);
+                const bool e = se[p2 * 32 + t] != 0;
+                const bool in_span = o >= fo && o <= lo;
+                if (e || in_span) {
+                  const double used = e ? su[p2 * 32 + t] : 0.0;
+                  double pk;
+                  if (fast) pk = in_span ? (mode == kModeTabPk ? tab[o - fo] : pk_of(P, k_t, tab[o - fo])) : 0.0;
+                  else pk = pk_of(P, k_t, slot_dt(now, t0e, te, tee, B + o, L));
+                  const double total = __dadd_rn(used, pk);
+                  if (in_span && total > cap_t) vv = static_cast<uint32_t>(o);
+                  const uint64_t tb = ordered_bits(total);
+                  pp = tb > pp ? tb : pp;
+                }
+              }
+            }
+            v_t = __reduce_min_sync(0xffffffffu, vv);
+            p_t = warp_max_u64(pp);
+          }
+          if (lane == t) {
+            viol = v_t;
+            peak = p_t;
+            elig = e_t;
+            ovf = o_t;
+          }
+        }
+        if (__any_sync(0xffffffffu, ovf)) {
+          status = KX_ERR_CAPACITY;
+          broke = true;
+          break;
+        }
+        const bool fits = elig && viol == kNone;
+        // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
+        const uint64_t key = fits ? peak : ~0ull;
+        const uint64_t wkey = warp_min_u64(key);
+        const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
+        const int bl = winners ? __ffs(winners) - 1 : -1;
+        const int bsrc = bl >= 0 ? bl : 0;
+        const double bpeak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
+        const double blive = __shfl_sync(0xffffffffu, live, bsrc);
+        const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
+        const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
+        const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
+        if (nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
+          const int64_t r = int64_t(pool) * dp.log_cap + nrows;
+          if (lane == 0) {
+            kx_decision d;
+            d.time = now;
+            d.predicted_peak = bpeak;
+            d.uid = h_uid[hs];
+            d.queue_index = h_idx[hs];
+            d.agent = h_agent[hs];
+            d.target = bl >= 0 ? bid : -1;
+            d.pool = pool;
+            d.admitted = (bl >= 0 && !overload) ? 1 : 0;
+            rows[r] = d;
+          }
+          if (act) {
+            double v = -1.0;
+            if (elig) {
+              v = fits ? from_ordered_bits(peak)
+                       : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
+            }
+            cand[r * dp.peak_stride + li] = v;
+          }
+        }
+        ++nrows;
+        if (bl < 0) {  // head keeps its place (engine.cpp:247)
+          broke = true;
+          break;
+        }
+        if (overload) {
+          if (lane == bl) {  // Dispatcher::on_overload
+            susp = true;
+            st_susp[lane] = 1;
+          }
+          if (++retries > ni) {
+            status = KX_ERR_LIVELOCK;
+            broke = true;
+            break;
+          }
+          tfix = bl;
+          own_row = true;
+          if (lane == 0) ctl[step & 1] = PipeCtl{pos, 0, -1};
+          ++step;
+          pipe_sync();
+          continue;
+        }
+        retries = 0;
+        // Dispatcher::commit: book the target's span slots (lanes = slots).
+        const double kt = __shfl_sync(0xffffffffu, kr, bl);
+        if (mode != kModeGeneric) {
+          const double* tab = stab + hs * kDtSlots;
+          for (int64_t s = first + lane; s <= last; s += 32) {
+            const int p2 = static_cast<int>(s & rmask);
+            const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
+            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk);
+            se[p2 * 32 + bl] = 1;
+          }
+        } else {
+          const double te = __dadd_rn(now, T);
+          const double tee = __dsub_rn(te, kTimeEpsilon);
+          for (int64_t s = first + lane; s <= last; s += 32) {
+            const int p2 = static_cast<int>(s & rmask);
+            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
+            se[p2 * 32 + bl] = 1;
+          }
+        }
+        if (lane == bl) {
+          if (nonempty && last > hi) {
+            hi = last;
+            hi_off = lo;
+          }
+          live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
+          running += 1;
+          st_live[lane] = live;
+          st_run[lane] = running;
+          st_hi[lane] = hi_off;
+          if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78)
+            q.admitted[h_idx[hs]] = 1;
+            const int64_t o = int64_t(i) * kActiveCap + nact;
+            in.act_uid[o] = h_uid[hs];
+            in.act_P[o] = P;
+            in.act_k[o] = kt;
+            in.act_t0[o] = now;
+            in.act_T[o] = T;
+            ++nact;
+          } else {
+            status = KX_ERR_CAPACITY;
+          }
+        }
+        if (__any_sync(0xffffffffu, status != KX_OK)) {
+          status = KX_ERR_CAPACITY;
+          broke = true;
+          break;
+        }
+        ++nadm;
+        ++pos;
+        tfix = bl;
+        own_row = false;
+        if (lane == 0) ctl[step & 1] = PipeCtl{pos, 0, bl};
+        ++step;
+        pipe_sync();
+      }
+      // release the evaluator
+      if (lane == 0) ctl[step & 1] = PipeCtl{pos, 1, -1};
+      pipe_sync();
+      // Phase 1 ran out of prefix heads without finishing the round: hand the
+      // state to the continuation (no gc yet: the round is not over).
+      const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
+      int64_t nbase = base;
+      if (!defer_rest) {
+        // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
+        if (act && cslot > base) {
+          const int64_t stop = cslot < base + ring ? cslot : base + ring;
+          for (int64_t s = base; s < stop; ++s) {
+            const int p2 = static_cast<int>(s & rmask);
+            su[p2 * 32 + lane] = 0.0;
+            se[p2 * 32 + lane] = 0;
+          }
+          nbase = cslot;
+        }
+      }
+      if (act) {
+        in.n_active[i] = nact;
+        if (!defer_rest) active_gc(in, i, now);
+        in.live_kv[i] = live;
+        in.base_slot[i] = nbase;
+        in.hi_slot[i] = hi;
+        in.running[i] = running;
+        in.suspended[i] = susp ? 1 : 0;
+      }
+      if (lane == 0) {
+        if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
+        if (!defer_rest) {
+          row_count[pool] = nrows;
+          admitted_count[pool] = nadm;
+          pool_status[pool] = status;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < 32 * ring; j += kPipeThreads) {
+    const int l = j & 31, p2 = j >> 5;
+    const int li = s_li[l];
+    if (li >= 0) {
+      in.usage[int64_t(ib + li) * ring + p2] = su[j];
+      in.exists[int64_t(ib + li) * ring + p2] = se[j];
+    }
+  }
+}
+
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
 __global__ void k_ledger_try_place(InstDev in, int i, int ring, double P, double k, double t0,
                                    double T, double slot_len, double* out_peak, int64_t* out_viol,
@@ -1156,6 +1809,8 @@ __global__ void k_gc_all(InstDev in, int n_inst, int ring, double now, double sl
 void configure_dispatch_kernels() {
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
+  KX_CUDA(cudaFuncSetAttribute(k_dispatch_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1163,7 +1818,8 @@ void configure_dispatch_kernels() {
 }
 
 bool dispatch_can_overlap(int max_inst_per_pool, int ring) {
-  return max_inst_per_pool <= 32 && warp_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
+  return max_inst_per_pool <= 32 && pipe_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
+         warp_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
 }
 
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
@@ -1172,6 +1828,15 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st, DispPhase phase) {
   if (max_inst_per_pool <= 32) {
+    const PipeLayout pl = pipe_layout(dp.ring);
+    if (!getenv("KX_DISPATCH_SINGLE_WARP") && pl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+      k_dispatch_pipe<<<n_pools, kPipeThreads, pl.total, st>>>(q, a, in, pool_begin, perm,
+                                                              pool_offsets, dp, pl, rows, cand,
+                                                              row_count, admitted_count,
+                                                              pool_status, phase);
+      KX_CHECK_LAUNCH();
+      return;
+    }
     const WarpLayout wl = warp_layout(dp.ring);
     if (wl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
       k_dispatch_warp<<<n_pools, kWarpThreads, wl.total, st>>>(q, a, in, pool_begin, perm,
