@@ -588,6 +588,27 @@ std::vector<uint32_t> dense_rank(const std::vector<double>& v) {
   return r;
 }
 
+// Dense rank of each agent's value among the agents of its own pool: the
+// compact key compares classes only within a pool (the pool id is its top
+// field), so per-pool ranks need the fewest class bits and leave the most
+// bits for the quantised time.
+std::vector<uint32_t> pool_dense_rank(const std::vector<double>& v, const int32_t* pool, int n_pools) {
+  std::vector<uint32_t> r(v.size(), 0);
+  for (int p = 0; p < n_pools; ++p) {
+    std::vector<double> sub;
+    std::vector<size_t> idx;
+    for (size_t i = 0; i < v.size(); ++i)
+      if (pool[i] == p) {
+        sub.push_back(v[i]);
+        idx.push_back(i);
+      }
+    if (sub.empty()) continue;
+    const auto rr = dense_rank(sub);
+    for (size_t j = 0; j < idx.size(); ++j) r[idx[j]] = rr[j];
+  }
+  return r;
+}
+
 OrderParams order_params(const kx_sched* s) {
   OrderParams op{};
   op.policy = s->sched_kind;
@@ -1038,7 +1059,8 @@ int kx_set_agent_tables(kx_sched* s, int32_t n_agents, const int32_t* agent_pool
     KX_CUDA(cudaMemcpyAsync(s->a.pool, agent_pool, A * 4, cudaMemcpyHostToDevice, s->stream));
     if (priority_key) {
       const std::vector<double> pk(priority_key, priority_key + A);
-      const auto r = dense_rank(pk);
+      for (double x : pk) require(x == x, "NaN in agent table");
+      const auto r = pool_dense_rank(pk, agent_pool, s->n_pools);
       s->n_pk_classes = 1 + static_cast<int32_t>(*std::max_element(r.begin(), r.end()));
       KX_CUDA(cudaMemcpyAsync(s->a.pk, priority_key, A * 8, cudaMemcpyHostToDevice, s->stream));
       KX_CUDA(cudaMemcpyAsync(s->a.pk_rank, r.data(), A * 4, cudaMemcpyHostToDevice, s->stream));
@@ -1051,7 +1073,7 @@ int kx_set_agent_tables(kx_sched* s, int32_t n_agents, const int32_t* agent_pool
     if (topo_depth) {
       std::vector<double> d(A);
       for (size_t i = 0; i < A; ++i) d[i] = static_cast<double>(topo_depth[i]);
-      const auto r = dense_rank(d);
+      const auto r = pool_dense_rank(d, agent_pool, s->n_pools);
       s->n_depth_classes = 1 + static_cast<int32_t>(*std::max_element(r.begin(), r.end()));
       KX_CUDA(cudaMemcpyAsync(s->a.depth, topo_depth, A * 4, cudaMemcpyHostToDevice, s->stream));
       KX_CUDA(cudaMemcpyAsync(s->a.depth_rank, r.data(), A * 4, cudaMemcpyHostToDevice, s->stream));

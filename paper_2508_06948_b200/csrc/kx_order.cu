@@ -341,78 +341,144 @@ __device__ __forceinline__ bool tkey_less(const QueueDev& q, const TKey& a, cons
 
 }  // namespace
 
-__global__ void k_tie_runs(QueueDev q, int policy, const uint32_t* __restrict__ keys,
-                           uint32_t* __restrict__ perm, int64_t n,
-                           uint32_t* __restrict__ small_starts, uint32_t* __restrict__ n_small,
-                           uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
-                           uint32_t* __restrict__ n_big, uint32_t cap) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
-    const bool start = (i == 0 || keys[i - 1] != k) && (i + 1 < n && keys[i + 1] == k);
-    if (!start) continue;
-    int64_t e = i + 2;
-    while (e < n && e - i <= 32 && keys[e] == k) ++e;
-    const int len = static_cast<int>(e - i);
-    if (len <= kThreadRun) {
-      TKey r[kThreadRun];
-      for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
-      for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
-        const TKey x = r[j];
-        int m = j - 1;
-        while (m >= 0 && tkey_less(q, x, r[m])) {
-          r[m + 1] = r[m];
-          --m;
-        }
-        r[m + 1] = x;
-      }
-      for (int j = 0; j < len; ++j) perm[i + j] = r[j].idx;
-    } else if (len <= 32) {
-      const uint32_t slot = atomicAdd(n_small, 1u);
-      if (slot < cap) small_starts[slot] = static_cast<uint32_t>(i);
-    } else {
-      while (e < n && keys[e] == k) ++e;
-      const uint32_t slot = atomicAdd(n_big, 1u);
-      if (slot < cap) {
-        big_starts[slot] = static_cast<uint32_t>(i);
-        big_lens[slot] = static_cast<uint32_t>(e - i);
-      }
+// Run detection: a coalesced scan of the sorted keys (four per thread) lists
+// the run starts, short runs (<= kThreadRun) for the thread-per-run fixer and
+// longer ones for the CTA fixer; warp-aggregated list appends.
+__device__ __forceinline__ void list_append(bool want, uint32_t value, uint32_t* list,
+                                            uint32_t* count, uint32_t cap, uint32_t* lens = nullptr,
+                                            uint32_t len = 0) {
+  const uint32_t m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, static_cast<uint32_t>(__popc(m)));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (want) {
+    const uint32_t slot = base + __popc(m & lanemask_lt());
+    if (slot < cap) {
+      list[slot] = value;
+      if (lens) lens[slot] = len;
     }
   }
 }
 
-// Runs of 2..32: one warp each, bitonic sort of exact records in registers.
-__global__ void k_tie_fix_small(QueueDev q, int policy, const uint32_t* __restrict__ keys,
-                                uint32_t* __restrict__ perm, int64_t n,
-                                const uint32_t* __restrict__ starts, const uint32_t* __restrict__ n_small,
-                                uint32_t cap) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t total = min(*n_small, cap);
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += warps) {
-    const int64_t s = starts[w];
-    const uint32_t k = keys[s];
-    const bool in = (s + lane < n) && keys[s + lane] == k;
-    const uint32_t len = __popc(__ballot_sync(0xffffffffu, in));  // run is contiguous from s
-    TRec r;
-    if (lane < static_cast<int>(len)) {
-      r = load_rec(q, policy, perm[s + lane]);
-    } else {
-      r.w0 = r.w1 = r.w2 = r.msg = r.uid = ~0ull;
-      r.idx = 0xffffffffu;
+// Run detection streams the sorted keys (uint4 loads, two per thread per
+// iteration) and lists every run start; the run length is measured by the
+// fixer, which hands runs longer than kThreadRun to the CTA fixer.
+__global__ void __launch_bounds__(256)
+k_tie_runs(const uint32_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ starts,
+           uint32_t* __restrict__ n_starts, uint32_t cap) {
+  // Block-aggregated appends: one global atomic per block per iteration
+  // (a single list counter hit once per warp serialises at L2).
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nv = (n + 3) >> 2;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  constexpr int U = 2;
+  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x; v0 < nv; v0 += U * stride) {
+    uint32_t k[U][6];  // keys[4v - 1 .. 4v + 4]
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * stride + threadIdx.x;
+      const int64_t b = 4 * v;
+      if (v < nv && b + 3 < n) {
+        const uint4 x = reinterpret_cast<const uint4*>(keys)[v];
+        k[u][1] = x.x; k[u][2] = x.y; k[u][3] = x.z; k[u][4] = x.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[u][1 + j] = (v < nv && b + j < n) ? keys[b + j] : 0u;
+      }
+      k[u][0] = (v < nv && b > 0) ? keys[b - 1] : 0u;
+      k[u][5] = (v < nv && b + 4 < n) ? keys[b + 4] : 0u;
     }
-    for (int kk = 2; kk <= 32; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
-        const TRec o = shfl_rec(r, lane ^ j);
-        const bool up = (lane & kk) == 0;
-        const bool lower = (lane & j) == 0;
-        const bool o_less = rec_less(o, r);
-        // lower lane keeps min when ascending, max when descending
-        const bool take = (lower == up) ? o_less : !o_less;
-        if (take) r = o;
+    uint32_t mask = 0;  // bit u*4+j: element 4v+j of vector u starts a run
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * stride + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t i = 4 * v + j;
+        const bool start = v < nv && i + 1 < n && (i == 0 || k[u][j] != k[u][j + 1]) && k[u][j + 2] == k[u][j + 1];
+        mask |= start ? (1u << (u * 4 + j)) : 0u;
       }
     }
-    if (lane < static_cast<int>(len)) perm[s + lane] = r.idx;
+    // block-wide exclusive prefix of the per-thread counts
+    const uint32_t c = __popc(mask);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t t = s_warp[w];
+        s_warp[w] = tot;
+        tot += t;
+      }
+      s_base = tot ? atomicAdd(n_starts, tot) : 0u;
+    }
+    __syncthreads();
+    uint32_t slot = s_base + s_warp[warp] + x - c;
+    while (mask) {
+      const int bit = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int u = bit >> 2, j = bit & 3;
+      if (slot < cap) starts[slot] = static_cast<uint32_t>(4 * (v0 + u * stride + threadIdx.x) + j);
+      ++slot;
+    }
+    __syncthreads();
+  }
+}
+
+// Runs of 2..kThreadRun: one thread each, insertion sort by the exact
+// tuple (msg/uid fetched only when the time fields tie); only a run whose
+// order changes is written back. Longer runs go to the CTA fixer's list.
+__global__ void k_tie_fix_small(QueueDev q, int policy, const uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ perm, int64_t n,
+                                const uint32_t* __restrict__ starts, const uint32_t* __restrict__ n_starts,
+                                uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
+                                uint32_t* __restrict__ n_big, uint32_t cap) {
+  const uint32_t total = min(*n_starts, cap);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t w0 = blockIdx.x * blockDim.x; w0 < total; w0 += stride) {
+    const uint32_t w = w0 + threadIdx.x;
+    int64_t i = 0, e = 0;
+    bool big = false;
+    if (w < total) {
+      i = starts[w];
+      const uint32_t kk = keys[i];
+      e = i + 2;
+      while (e < n && e - i <= kThreadRun && keys[e] == kk) ++e;
+      if (e - i > kThreadRun) {
+        while (e < n && keys[e] == kk) ++e;
+        big = true;
+      }
+    }
+    list_append(big, static_cast<uint32_t>(i), big_starts, n_big, cap, big_lens,
+                static_cast<uint32_t>(e - i));
+    if (w >= total || big) continue;
+    const int len = static_cast<int>(e - i);
+    TKey r[kThreadRun];
+    for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
+    bool moved = false;
+    for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
+      const TKey x = r[j];
+      int m = j - 1;
+      while (m >= 0 && tkey_less(q, x, r[m])) {
+        r[m + 1] = r[m];
+        --m;
+        moved = true;
+      }
+      r[m + 1] = x;
+    }
+    if (moved)
+      for (int j = 0; j < len; ++j) perm[i + j] = r[j].idx;
   }
 }
 
@@ -565,6 +631,11 @@ __device__ __forceinline__ int pool_of_key(uint32_t key, const OrderParams& op) 
   return op.pool_bits ? static_cast<int>(key >> (op.key_bits - op.pool_bits)) : 0;
 }
 
+// Keys are read as uint4 (four per load, four loads in flight per thread):
+// the select passes stream the key array at HBM rate instead of one
+// dependent 4-byte load per iteration.
+constexpr int kSelU = 4;
+
 __global__ void k_topk_hist(const uint32_t* __restrict__ keys, int64_t n, OrderParams op, int shift,
                             const TopKState* __restrict__ st, uint32_t* __restrict__ hist) {
   __shared__ uint32_t sh[kTopKMaxPools * kRadix];
@@ -576,12 +647,31 @@ __global__ void k_topk_hist(const uint32_t* __restrict__ keys, int64_t n, OrderP
     s_live[p] = !st[p].done;
   }
   __syncthreads();
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
+  auto take = [&](uint32_t k) {
     const int p = pool_of_key(k, op);
     if (s_live[p] && (k & s_mask[p]) == s_prefix[p]) atomicAdd(&sh[p * kRadix + ((k >> shift) & 0xFF)], 1u);
+  };
+  const int64_t nv = n >> 2;
+  const uint4* kv = reinterpret_cast<const uint4*>(keys);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += kSelU * stride) {
+    uint4 x[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int64_t v = v0 + u * stride;
+      x[u] = v < nv ? kv[v] : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      if (v0 + u * stride >= nv) continue;
+      take(x[u].x);
+      take(x[u].y);
+      take(x[u].z);
+      take(x[u].w);
+    }
   }
+  if (blockIdx.x == 0)
+    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(keys[i]);
   __syncthreads();
   for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
@@ -627,15 +717,35 @@ __global__ void k_topk_compact(const uint32_t* __restrict__ keys, int64_t n, Ord
     s_ok[p] = !st[p].defer && !st[p].empty;
   }
   __syncthreads();
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
+  auto take = [&](uint32_t k, int64_t i) {
     const int p = pool_of_key(k, op);
     if (s_ok[p] && k <= s_bound[p]) {
       const uint32_t slot = atomicAdd(&st[p].n_cand, 1u);
       if (slot < kTopKMax) cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(i);
     }
+  };
+  const int64_t nv = n >> 2;
+  const uint4* kv = reinterpret_cast<const uint4*>(keys);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += kSelU * stride) {
+    uint4 x[kSelU];
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int64_t v = v0 + u * stride;
+      x[u] = v < nv ? kv[v] : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kSelU; ++u) {
+      const int64_t v = v0 + u * stride;
+      if (v >= nv) continue;
+      take(x[u].x, 4 * v);
+      take(x[u].y, 4 * v + 1);
+      take(x[u].z, 4 * v + 2);
+      take(x[u].w, 4 * v + 3);
+    }
   }
+  if (blockIdx.x == 0)
+    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(keys[i], i);
 }
 
 // CTA per pool: exact order of the candidates. A bitonic sort of the
@@ -767,7 +877,7 @@ void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin
                                  ws.pool_offsets, w.max_need, w.state);
   KX_CHECK_LAUNCH();
   KX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * op.n_pools * kRadix, st));
-  const int grid = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, int64_t(sms) * 4));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, int64_t(sms) * 4)));
   for (int r = 1; r < passes && n > 0; ++r) {
     const int shift = op.key_bits - 8 - 8 * r;
     k_topk_hist<<<grid, 256, 0, st>>>(keys, n, op, shift, w.state, w.hist);
@@ -859,14 +969,14 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   res.keys = ws.keys[cur];
   res.perm = ws.vals[cur];
 
-  const int tgrid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(sms) * 8));
+  const int tgrid = static_cast<int>(std::min<int64_t>((n / 4 + 256) / 256, int64_t(sms) * 8));
   // reads the sorted keys (4 B); tie runs gather their exact tuples
   P.begin("tie_fix", N * 4.0, st);
-  k_tie_runs<<<tgrid, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts, ws.n_small,
-                                     ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);
+  k_tie_runs<<<tgrid, 256, 0, st>>>(res.keys, n, ws.small_starts, ws.n_small, ws.tie_cap);
   KX_CHECK_LAUNCH();
   k_tie_fix_small<<<sms * 8, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
-                                           ws.n_small, ws.tie_cap);
+                                           ws.n_small, ws.big_starts, ws.big_lens, ws.n_big,
+                                           ws.tie_cap);
   KX_CHECK_LAUNCH();
   k_tie_fix_big<<<sms, kBigThreads, 0, st>>>(q, op.policy, res.perm, ws.vals[cur ^ 1],
                                              ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);

@@ -27,10 +27,11 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 12;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 6144 elements
+constexpr int kSortTile = kSortThreads * kSortItems;  // 3072 elements
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
+constexpr int kLookBatch = 8;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -179,18 +180,27 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     uint32_t add = 0;
     for (int w = 0; w < warp; ++w) add += s_warp_sums[w];
     sm.digit_start[tid] += add;
-    // Decoupled look-back for digit `tid`.
+    // Decoupled look-back for digit `tid`, kLookBatch predecessors per
+    // round trip: the walk over tiles that have only published their
+    // aggregate costs one L2 latency per batch instead of per tile.
     uint32_t excl = 0;
     if (tile > 0) {
       volatile uint32_t* lb = lookback;
       int64_t p = int64_t(tile) - 1;
-      while (true) {
-        const uint32_t v = lb[p * kRadix + tid];
-        const uint32_t flag = v & ~kCountMask;
-        if (flag == 0) continue;  // predecessor not published yet
-        excl += v & kCountMask;
-        if (flag == kFlagIncl) break;
-        --p;
+      bool done = false;
+      while (!done) {
+        uint32_t v[kLookBatch];
+#pragma unroll
+        for (int j = 0; j < kLookBatch; ++j) v[j] = (p - j >= 0) ? uint32_t(lb[(p - j) * kRadix + tid]) : uint32_t(kFlagIncl);
+#pragma unroll
+        for (int j = 0; j < kLookBatch; ++j) {
+          if (done) break;
+          const uint32_t flag = v[j] & ~kCountMask;
+          if (flag == 0) break;  // not published yet: reload from here
+          excl += v[j] & kCountMask;
+          --p;
+          if (flag == kFlagIncl) done = true;
+        }
       }
       lb[int64_t(tile) * kRadix + tid] = kFlagIncl | (excl + total);
     }
