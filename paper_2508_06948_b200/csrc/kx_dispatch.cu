@@ -1040,27 +1040,33 @@ k_dispatch_warp(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
   }
 }
 
-// ---- K5 pipelined: decider warp + look-ahead evaluator warp ----------------
-// Same decisions as k_dispatch_warp, with the chain's work split over two
-// warps that meet at one 64-thread named barrier per decision:
-//   * warp 1 (evaluator) runs one head ahead: it evaluates try_place for
-//     head pos + 1 for every instance against the state at the start of the
-//     step (lanes = instances), maintains the suffix maxima and loads the
-//     head batches;
-//   * warp 0 (decider) takes that row for head pos; only the instance the
-//     previous step committed to (or suspended) is stale, and it re-evaluates
-//     just that one (lanes = slots), then runs select_instance, the overload
-//     check, the decision log and the commit.
-// A step that ends in an overload retry keeps the decider's own row for the
-// next step (only the suspended instance changes). The evaluator's reads of
-// the column the decider is committing to in the same step are discarded by
-// construction (that lane is the one re-evaluated next step).
+// ---- K5 pipelined: decider warp <-> evaluator warp ping-pong --------------
+// Same decisions as k_dispatch_warp, with the chain split over two warps
+// that hand off through two 64-thread named barriers (producer bar.arrive,
+// consumer bar.sync):
+//   * warp 1 (evaluator) keeps try_place rows (lanes = instances) for the
+//     current head and the next one, evaluated ahead of time; when the
+//     decider reports a commit or a suspension it re-evaluates only the
+//     instances changed since a row was computed (lanes = slots), publishes
+//     the current row, and evaluates the following head while the decider
+//     works. It also loads the head batches.
+//   * warp 0 (decider) runs select_instance, the overload check and the
+//     commit, reports the outcome, and writes the decision log and the
+//     admission bookkeeping while the evaluator fixes the next row.
+// The predicted peak needs no slot walk outside the span: for a head whose
+// peak_in_slot is zero off its span (the fast shape above), every stored
+// slot contributes `used` and every span slot used + pk >= used, so
+//   peak = max(max over all stored slots of used, max over the span of used + pk)
+// and the first term is one per-instance maximum, raised by each commit.
+// The evaluator's reads of a column the decider is committing to at the same
+// time are discarded by construction: that lane is marked changed by the
+// decider's next report and re-evaluated before the row is used.
 constexpr int kPipeThreads = 128;
 constexpr int kHR = 64;  // head ring: two batches of kWHB
 
 struct PipeLayout {
   uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
-      st_live, st_run, st_susp, st_hi, r_viol, r_peak, r_flag, usage, ex, sufm, total;
+      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, usage, ex, total;
 };
 
 PipeLayout pipe_layout(int ring) {
@@ -1086,23 +1092,29 @@ PipeLayout pipe_layout(int ring) {
   L.st_run = take(4 * 32);
   L.st_susp = take(4 * 32);
   L.st_hi = take(4 * 32);
-  L.r_viol = take(4 * 64);
-  L.r_peak = take(8 * 64);
-  L.r_flag = take(4 * 64);
+  L.st_umax = take(8 * 32);
+  L.r_viol = take(4 * 32);
+  L.r_peak = take(8 * 32);
+  L.r_flag = take(4 * 32);
   L.usage = take(size_t(8) * 32 * ring);
   L.ex = take(size_t(32) * ring);
-  L.sufm = take(size_t(8) * 32 * ring);
   L.total = o;
   return L;
 }
 
-__device__ __forceinline__ void pipe_sync() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 
-struct PipeCtl {
-  int64_t pos;      // head the decider takes next
-  int32_t stop;     // 1: the round is over
-  int32_t commit;   // lane committed in the last step (-1: none)
+struct PipeMsg {
+  int32_t type;     // 0 commit, 1 suspension (overload retry), 2 stop
+  int32_t lane;     // instance lane changed by the decision
 };
+
+__device__ __forceinline__ void pp_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void pp_arrive(int id) {
+  __threadfence_block();  // the consumer reads what this warp wrote to shared memory
+  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+constexpr int kBarDecided = 1;   // decider -> evaluator
+constexpr int kBarRowReady = 2;  // evaluator -> decider
 
 __global__ void __launch_bounds__(kPipeThreads)
 k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
@@ -1112,7 +1124,8 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
                 DispPhase ph) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ PipeCtl ctl[2];  // double-buffered by step parity
+  __shared__ PipeMsg msg;
+  __shared__ int64_t s_win[3];  // staged slot window [B, top]; top after the round
   const int pool = blockIdx.x;
   const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
   const uint32_t* hp = perm + pool_offsets[pool];
@@ -1143,7 +1156,6 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
 #define PL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
   double* const su = PL(double, usage);
   uint8_t* const se = PL(uint8_t, ex);
-  uint64_t* const sm = PL(uint64_t, sufm);
   int32_t* const s_li = PL(int32_t, lane_inst);
   uint32_t* const h_idx = PL(uint32_t, h_idx);
   int32_t* const h_agent = PL(int32_t, h_agent);
@@ -1159,6 +1171,7 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
   int32_t* const st_run = PL(int32_t, st_run);
   int32_t* const st_susp = PL(int32_t, st_susp);
   int32_t* const st_hi = PL(int32_t, st_hi);
+  uint64_t* const st_umax = PL(uint64_t, st_umax);
   uint32_t* const r_viol = PL(uint32_t, r_viol);
   uint64_t* const r_peak = PL(uint64_t, r_peak);
   uint32_t* const r_flag = PL(uint32_t, r_flag);
@@ -1177,13 +1190,52 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
     s_li[lane] = -1;
     __syncwarp();
     if (lane < ni) s_li[rank] = lane;
+    // the pool's slot window [B, top]: the only ring positions that can hold
+    // stored slots (everything else is +0.0 / not stored)
+    const bool a0 = lane < ni;
+    const int64_t bb = a0 ? in.base_slot[ib + lane] : INT64_MAX;
+    const int64_t hh = a0 ? in.hi_slot[ib + lane] : INT64_MIN;
+    const uint64_t bmin = warp_min_u64(static_cast<uint64_t>(bb) ^ 0x8000000000000000ull);
+    const uint64_t hmax = warp_max_u64(static_cast<uint64_t>(hh) ^ 0x8000000000000000ull);
+    if (lane == 0) {
+      s_win[0] = static_cast<int64_t>(bmin ^ 0x8000000000000000ull);
+      s_win[1] = static_cast<int64_t>(hmax ^ 0x8000000000000000ull);
+    }
   }
   __syncthreads();
+  // Stage the rings transposed (usage[pos][lane]): zero everywhere, then copy
+  // the window's positions with four independent loads in flight per thread.
+  const int64_t wB = s_win[0];
+  const int64_t wtop = s_win[1];
+  const int win = wtop < wB ? 0 : static_cast<int>(wtop - wB + 1 < ring ? wtop - wB + 1 : ring);
   for (int j = threadIdx.x; j < 32 * ring; j += kPipeThreads) {
-    const int l = j & 31, pos = j >> 5;
-    const int li = s_li[l];
-    su[j] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
-    se[j] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+    su[j] = 0.0;
+    se[j] = 0;
+  }
+  __syncthreads();
+  {
+    const int total = win * 32;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kPipeThreads) {
+      double u[4];
+      uint8_t x[4];
+      int dst[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + k * kPipeThreads;
+        const int l = e & 31;
+        const int li = e < total ? s_li[l] : -1;
+        const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
+        dst[k] = li >= 0 ? pos * 32 + l : -1;
+        u[k] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
+        x[k] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (dst[k] >= 0) {
+          su[dst[k]] = u[k];
+          se[dst[k]] = x[k];
+        }
+    }
   }
   __syncthreads();
 
@@ -1208,31 +1260,18 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
     const int32_t lo_off = static_cast<int32_t>(base - B);
     const double t0e = __dadd_rn(now, kTimeEpsilon);
     const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
-    const int32_t c_off = static_cast<int32_t>(cslot - B);
-    // stored slots below c: one max per instance, fixed for the round
-    uint64_t lomax = kZeroBits;
-    for (int32_t o = lo_off; o < c_off && o <= static_cast<int32_t>(hi0 - B); ++o) {
+    // max stored usage of the instance over its whole ledger window
+    uint64_t umax0 = kZeroBits;
+    for (int32_t o = lo_off; o <= static_cast<int32_t>(hi0 - B); ++o) {
       const int p2 = static_cast<int>((B + o) & rmask);
       if (se[p2 * 32 + lane]) {
         const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-        lomax = tb > lomax ? tb : lomax;
+        umax0 = tb > umax0 ? tb : umax0;
       }
     }
 
     if (warp == 1) {
       // =========================== evaluator ===========================
-      // initial suffix maxima over offsets (c, hi]
-      {
-        uint64_t run = kZeroBits;
-        for (int32_t o = static_cast<int32_t>(hi0 - B); o > c_off && o >= lo_off; --o) {
-          const int p2 = static_cast<int>((B + o) & rmask);
-          if (se[p2 * 32 + lane]) {
-            const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-            run = tb > run ? tb : run;
-          }
-          sm[p2 * 32 + lane] = run;
-        }
-      }
       // head prefetch registers (lane = head of the next batch)
       int64_t nx_start = pos0, nx_n = 0;
       uint32_t nx_idx = 0;
@@ -1313,9 +1352,19 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
         loaded_end = nx_start + nx_n;
         issue_idx(loaded_end);
       };
-      // try_place of head `hpos` for this lane's instance against the
-      // current state (published by the decider) -> row[par].
-      auto evaluate = [&](int64_t hpos, int par) {
+      auto ensure_loaded = [&](int64_t hpos) {
+        if (hpos >= loaded_end) land_batch();
+        else if (stage == 0 && hpos >= nx_start - kWHB + 2) issue_fields();
+        else if (stage == 1 && hpos >= nx_start - kWHB + 4) issue_T();
+      };
+      // One row entry: try_place of head `hpos` for this lane's instance
+      // against the published state (lanes = instances).
+      struct Row {
+        uint32_t viol;
+        uint64_t peak;
+        uint32_t flag;  // bit 0 eligible, bit 1 ring overflow
+      };
+      auto evaluate = [&](int64_t hpos) {
         const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
         const int mode = h_mode[hs];
         const int64_t first = h_first[hs];
@@ -1327,15 +1376,12 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
         const double live = st_live[lane];
         const bool susp = st_susp[lane] != 0 && !(live < wcap);
         const bool eligible = act && !susp && !(st_run[lane] + waiting >= mb);
-        const int32_t hi_off = st_hi[lane];
-        uint32_t viol = kNone;
-        uint64_t peak = kZeroBits;
+        Row r{kNone, kZeroBits, 0u};
         const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
         if (eligible) {
           if (mode != kModeGeneric) {
-            const int32_t qo = lo + 1;
-            const uint64_t above = (qo <= hi_off) ? sm[static_cast<int>((B + qo) & rmask) * 32 + lane] : kZeroBits;
-            peak = lomax > above ? lomax : above;
+            uint64_t peak = st_umax[lane];
+            uint32_t viol = kNone;
             const double* tab = stab + hs * kDtSlots;
             const int tn = lo - fo + 1;
             int p2 = static_cast<int>((B + fo) & rmask);
@@ -1358,10 +1404,15 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
                 p2 = (p2 + 1) & rmask;
               }
             }
+            r.viol = viol;
+            r.peak = peak;
           } else {  // generic slot walk over the whole window
             const double te = __dadd_rn(now, h_T[hs]);
             const double tee = __dsub_rn(te, kTimeEpsilon);
+            const int32_t hi_off = st_hi[lane];
             const int32_t top = hi_off > lo ? hi_off : lo;
+            uint64_t peak = kZeroBits;
+            uint32_t viol = kNone;
             for (int32_t o = lo_off; o <= top; ++o) {
               const int p2 = static_cast<int>((B + o) & rmask);
               const bool e = se[p2 * 32 + lane] != 0;
@@ -1373,130 +1424,51 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
               const uint64_t tb = ordered_bits(total);
               peak = tb > peak ? tb : peak;
             }
+            r.viol = viol;
+            r.peak = peak;
           }
         }
-        r_viol[par * 32 + lane] = viol;
-        r_peak[par * 32 + lane] = peak;
-        r_flag[par * 32 + lane] = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+        r.flag = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+        return r;
       };
-
-      issue_idx(pos0);
-      pipe_sync();  // the decider's state is published
-      if (pos0 < q_end) {
-        land_batch();
-        evaluate(pos0, 0);
-      }
-      pipe_sync();
-      int step = 0;
-      while (true) {
-        // Iteration j runs beside the decider's step j - 1 and reads what
-        // the decider published in step j - 2 (ctl[j & 1]).
-        const int j = step + 1;
-        const PipeCtl c = ctl[j & 1];
-        if (c.stop) break;
-        step = j;
-        if (c.commit >= 0) {
-          // the committed instance's suffix max over (c, hi], from hi down
-          const int t = c.commit;
-          const int32_t hi_t = st_hi[t];
-          uint64_t carry = kZeroBits;
-          for (int32_t top = hi_t; top > c_off; top -= 32) {
-            const int32_t o = top - lane;
-            const bool valid = o > c_off;
-            const int p2 = static_cast<int>((B + o) & rmask);
-            uint64_t v = (valid && se[p2 * 32 + t]) ? ordered_bits(su[p2 * 32 + t]) : kZeroBits;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-              const uint64_t w = shfl_up_u64(v, d);
-              if (lane >= d && w > v) v = w;
-            }
-            v = carry > v ? carry : v;
-            if (valid) sm[p2 * 32 + t] = v;
-            carry = shfl_u64(v, 31);
-          }
-          __syncwarp();
-        }
-        const int64_t epos = c.pos + 1;  // speculate: the decider admits head pos
-        if (epos < q_end) {
-          if (epos >= loaded_end) land_batch();
-          else if (stage == 0 && epos >= nx_start - kWHB + 2) issue_fields();
-          else if (stage == 1 && epos >= nx_start - kWHB + 4) issue_T();
-          evaluate(epos, step & 1);
-        }
-        pipe_sync();
-      }
-    } else {
-      // ============================ decider ============================
-      double live = act ? in.live_kv[i] : 0.0;
-      int32_t running = act ? in.running[i] : 0;
-      bool susp = act ? in.suspended[i] != 0 : false;
-      int64_t hi = hi0;
-      int32_t hi_off = static_cast<int32_t>(hi0 - B);
-      int32_t nact = act ? in.n_active[i] : 0;
-      st_live[lane] = live;
-      st_run[lane] = running;
-      st_susp[lane] = susp ? 1 : 0;
-      st_hi[lane] = hi_off;
-      if (lane == 0) ctl[1] = PipeCtl{pos0, 0, -1};
-      pipe_sync();
-      pipe_sync();  // the evaluator's row for pos0 is ready
-      int64_t pos = pos0;
-      int64_t nrows = nrows0, nadm = nadm0;
-      int retries = 0;
-      bool broke = false;
-      int status = KX_OK;
-      int step = 0;
-      int tfix = -1;        // lane whose row entry is stale
-      bool own_row = false; // retry: keep the decider's row
-      uint32_t viol = kNone;
-      uint64_t peak = kZeroBits;
-      bool elig = false, ovf = false;
-      while (pos < q_end) {
-        const int hs = static_cast<int>((pos - pos0) & (kHR - 1));
-        const int64_t prompt = h_prompt[hs];
-        const double P = static_cast<double>(prompt);
+      // Re-evaluate the row entries of the lanes in `dirty` (lanes = slots).
+      auto fix = [&](Row& r, int64_t hpos, uint32_t dirty) {
+        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
+        const int mode = h_mode[hs];
         const int64_t first = h_first[hs];
         const int64_t last = h_last[hs];
-        const int mode = h_mode[hs];
-        const double T = h_T[hs];
-        const bool nonempty = last >= first;
+        const double P = static_cast<double>(h_prompt[hs]);
         const int32_t fo = static_cast<int32_t>(first - B);
         const int32_t lo = static_cast<int32_t>(last - B);
-        // collect_live (engine.cpp:187-202): watermark resume, batch_full.
-        if (susp && live < wcap) {
-          susp = false;
-          st_susp[lane] = 0;
-        }
-        const bool my_elig = act && !susp && !(running + waiting >= mb);
-        if (!own_row) {
-          viol = r_viol[(step & 1) * 32 + lane];
-          peak = r_peak[(step & 1) * 32 + lane];
-          const uint32_t f = r_flag[(step & 1) * 32 + lane];
-          elig = f & 1u;
-          ovf = (f & 2u) != 0;
-        }
-        if (tfix >= 0) {
-          // re-evaluate the stale instance (lanes = slots)
-          const int t = tfix;
-          const bool e_t = __shfl_sync(0xffffffffu, my_elig, t);
+        const bool nonempty = last >= first;
+        const bool fast = mode != kModeGeneric;
+        const double* tab = stab + hs * kDtSlots;
+        while (dirty) {
+          const int t = __ffs(dirty) - 1;
+          dirty &= dirty - 1;
+          const double live_t = st_live[t];
+          const double wcap_t = __shfl_sync(0xffffffffu, wcap, t);
+          const bool susp_t = st_susp[t] != 0 && !(live_t < wcap_t);
+          const bool act_t = __shfl_sync(0xffffffffu, act, t);
+          const int32_t mb_t = __shfl_sync(0xffffffffu, mb, t);
+          const int32_t wait_t = __shfl_sync(0xffffffffu, waiting, t);
+          const bool e_t = act_t && !susp_t && !(st_run[t] + wait_t >= mb_t);
           uint32_t v_t = kNone;
           uint64_t p_t = kZeroBits;
           bool o_t = false;
           if (e_t) {
             const int32_t lo_t = __shfl_sync(0xffffffffu, lo_off, t);
-            const int32_t hio_t = __shfl_sync(0xffffffffu, hi_off, t);
+            const int32_t hio_t = st_hi[t];
             const double cap_t = __shfl_sync(0xffffffffu, cap, t);
             const double k_t = __shfl_sync(0xffffffffu, kr, t);
             const int64_t base_t = B + lo_t;
             o_t = nonempty && (first < base_t || last >= base_t + ring);
-            const bool fast = mode != kModeGeneric;
             const int32_t w0 = fast ? fo : lo_t;
-            const int32_t w1 = hio_t > lo ? hio_t : lo;
-            const double* tab = stab + hs * kDtSlots;
-            const double te = __dadd_rn(now, T);
+            const int32_t w1 = fast ? lo : (hio_t > lo ? hio_t : lo);
+            const double te = __dadd_rn(now, h_T[hs]);
             const double tee = __dsub_rn(te, kTimeEpsilon);
             uint32_t vv = kNone;
-            uint64_t pp = fast ? shfl_u64(lomax, t) : kZeroBits;
+            uint64_t pp = fast ? st_umax[t] : kZeroBits;
             for (int32_t o0 = w0; o0 <= w1; o0 += 32) {
               const int32_t o = o0 + lane;
               if (o <= w1) {
@@ -1509,7 +1481,7 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
                   if (fast) pk = in_span ? (mode == kModeTabPk ? tab[o - fo] : pk_of(P, k_t, tab[o - fo])) : 0.0;
                   else pk = pk_of(P, k_t, slot_dt(now, t0e, te, tee, B + o, L));
                   const double total = __dadd_rn(used, pk);
-                  if (in_span && total > cap_t) vv = static_cast<uint32_t>(o);
+                  if (in_span && total > cap_t && static_cast<uint32_t>(o) < vv) vv = static_cast<uint32_t>(o);
                   const uint64_t tb = ordered_bits(total);
                   pp = tb > pp ? tb : pp;
                 }
@@ -1519,15 +1491,111 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
             p_t = warp_max_u64(pp);
           }
           if (lane == t) {
-            viol = v_t;
-            peak = p_t;
-            elig = e_t;
-            ovf = o_t;
+            r.viol = v_t;
+            r.peak = e_t ? p_t : kZeroBits;
+            r.flag = (e_t ? 1u : 0u) | (o_t ? 2u : 0u);
           }
         }
-        if (__any_sync(0xffffffffu, ovf)) {
+      };
+      auto publish = [&](const Row& r) {
+        r_viol[lane] = r.viol;
+        r_peak[lane] = r.peak;
+        r_flag[lane] = r.flag;
+      };
+
+      issue_idx(pos0);
+      pp_sync(kBarDecided);  // the decider's state is published
+      int64_t h = pos0;
+      Row rc{kNone, kZeroBits, 0u}, rn{kNone, kZeroBits, 0u};
+      uint32_t dirty_n = 0;
+      if (h < q_end) {
+        ensure_loaded(h);
+        rc = evaluate(h);
+        publish(rc);
+      }
+      pp_arrive(kBarRowReady);
+      if (h + 1 < q_end) {
+        ensure_loaded(h + 1);
+        rn = evaluate(h + 1);
+      }
+      while (true) {
+        pp_sync(kBarDecided);
+        const PipeMsg m = msg;
+        if (m.type == 2) break;
+        const uint32_t bit = 1u << m.lane;
+        uint32_t dirty_c;
+        if (m.type == 0) {  // committed: the next head becomes current
+          ++h;
+          rc = rn;
+          dirty_c = dirty_n | bit;
+          dirty_n = 0;
+        } else {            // suspended: same head again
+          dirty_c = bit;
+          dirty_n |= bit;
+        }
+        if (h < q_end) {
+          fix(rc, h, dirty_c);
+          publish(rc);
+        }
+        pp_arrive(kBarRowReady);
+        if (m.type == 0 && h + 1 < q_end) {
+          ensure_loaded(h + 1);
+          rn = evaluate(h + 1);
+        }
+      }
+    } else {
+      // ============================ decider ============================
+      double live = act ? in.live_kv[i] : 0.0;
+      int32_t running = act ? in.running[i] : 0;
+      bool susp = act ? in.suspended[i] != 0 : false;
+      int64_t hi = hi0;
+      int32_t hi_off = static_cast<int32_t>(hi0 - B);
+      int32_t nact = act ? in.n_active[i] : 0;
+      uint64_t umax = umax0;
+      st_live[lane] = live;
+      st_run[lane] = running;
+      st_susp[lane] = susp ? 1 : 0;
+      st_hi[lane] = hi_off;
+      st_umax[lane] = umax;
+      pp_arrive(kBarDecided);
+      int64_t pos = pos0;
+      int64_t nrows = nrows0, nadm = nadm0;
+      int retries = 0;
+      bool broke = false;
+      int status = KX_OK;
+      auto report = [&](int type, int l) {
+        if (lane == 0) msg = PipeMsg{type, l};
+        pp_arrive(kBarDecided);
+      };
+      while (true) {
+        pp_sync(kBarRowReady);
+        if (pos >= q_end) {
+          report(2, 0);
+          break;
+        }
+        const uint32_t viol = r_viol[lane];
+        const uint64_t peak = r_peak[lane];
+        const uint32_t flg = r_flag[lane];
+        const bool elig = flg & 1u;
+        const int hs = static_cast<int>((pos - pos0) & (kHR - 1));
+        const int64_t prompt = h_prompt[hs];
+        const double P = static_cast<double>(prompt);
+        const int64_t first = h_first[hs];
+        const int64_t last = h_last[hs];
+        const int mode = h_mode[hs];
+        const double T = h_T[hs];
+        const bool nonempty = last >= first;
+        const int32_t lo = static_cast<int32_t>(last - B);
+        // collect_live (engine.cpp:187-202): the watermark resume (the
+        // evaluator applies the same rule to the published state).
+        if (susp && live < wcap) {
+          susp = false;
+          st_susp[lane] = 0;
+        }
+        if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
           status = KX_ERR_CAPACITY;
           broke = true;
+          report(2, 0);
           break;
         }
         const bool fits = elig && viol == kNone;
@@ -1537,17 +1605,76 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
         const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
         const int bl = winners ? __ffs(winners) - 1 : -1;
         const int bsrc = bl >= 0 ? bl : 0;
-        const double bpeak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
         const double blive = __shfl_sync(0xffffffffu, live, bsrc);
         const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
         const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
-        const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
+        if (bl < 0) {  // head keeps its place (engine.cpp:247)
+          broke = true;
+          report(2, 0);
+        } else if (overload) {
+          if (lane == bl) {  // Dispatcher::on_overload
+            susp = true;
+            st_susp[lane] = 1;
+          }
+          if (retries + 1 > ni) {
+            status = KX_ERR_LIVELOCK;  // SURVEY H6
+            broke = true;
+            report(2, 0);
+          } else {
+            report(1, bl);
+          }
+        } else {
+          // Dispatcher::commit: book the target's span slots (lanes = slots)
+          // and raise the target's maximum stored usage.
+          const double kt = __shfl_sync(0xffffffffu, kr, bl);
+          uint64_t nb = kZeroBits;
+          if (mode != kModeGeneric) {
+            const double* tab = stab + hs * kDtSlots;
+            for (int64_t s = first + lane; s <= last; s += 32) {
+              const int p2 = static_cast<int>(s & rmask);
+              const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
+              const double nu = __dadd_rn(su[p2 * 32 + bl], pk);
+              su[p2 * 32 + bl] = nu;
+              se[p2 * 32 + bl] = 1;
+              const uint64_t tb = ordered_bits(nu);
+              nb = tb > nb ? tb : nb;
+            }
+          } else {
+            const double te = __dadd_rn(now, T);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            for (int64_t s = first + lane; s <= last; s += 32) {
+              const int p2 = static_cast<int>(s & rmask);
+              const double nu = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
+              su[p2 * 32 + bl] = nu;
+              se[p2 * 32 + bl] = 1;
+              const uint64_t tb = ordered_bits(nu);
+              nb = tb > nb ? tb : nb;
+            }
+          }
+          nb = warp_max_u64(nb);
+          if (lane == bl) {
+            if (nonempty && last > hi) {
+              hi = last;
+              hi_off = lo;
+            }
+            live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
+            running += 1;
+            umax = nb > umax ? nb : umax;
+            st_live[lane] = live;
+            st_run[lane] = running;
+            st_hi[lane] = hi_off;
+            st_umax[lane] = umax;
+          }
+          report(0, bl);
+        }
+        // ---- bookkeeping while the evaluator fixes the next row ----
         if (nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
           const int64_t r = int64_t(pool) * dp.log_cap + nrows;
+          const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
           if (lane == 0) {
             kx_decision d;
             d.time = now;
-            d.predicted_peak = bpeak;
+            d.predicted_peak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
             d.uid = h_uid[hs];
             d.queue_index = h_idx[hs];
             d.agent = h_agent[hs];
@@ -1566,63 +1693,19 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
           }
         }
         ++nrows;
-        if (bl < 0) {  // head keeps its place (engine.cpp:247)
-          broke = true;
-          break;
-        }
+        if (broke) break;
         if (overload) {
-          if (lane == bl) {  // Dispatcher::on_overload
-            susp = true;
-            st_susp[lane] = 1;
-          }
-          if (++retries > ni) {
-            status = KX_ERR_LIVELOCK;  // SURVEY H6
-            broke = true;
-            break;
-          }
-          tfix = bl;
-          own_row = true;
-          if (lane == 0) ctl[step & 1] = PipeCtl{pos, 0, -1};
-          ++step;
-          pipe_sync();
+          ++retries;
           continue;
         }
         retries = 0;
-        // Dispatcher::commit: book the target's span slots (lanes = slots).
-        const double kt = __shfl_sync(0xffffffffu, kr, bl);
-        if (mode != kModeGeneric) {
-          const double* tab = stab + hs * kDtSlots;
-          for (int64_t s = first + lane; s <= last; s += 32) {
-            const int p2 = static_cast<int>(s & rmask);
-            const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
-            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk);
-            se[p2 * 32 + bl] = 1;
-          }
-        } else {
-          const double te = __dadd_rn(now, T);
-          const double tee = __dsub_rn(te, kTimeEpsilon);
-          for (int64_t s = first + lane; s <= last; s += 32) {
-            const int p2 = static_cast<int>(s & rmask);
-            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
-            se[p2 * 32 + bl] = 1;
-          }
-        }
         if (lane == bl) {
-          if (nonempty && last > hi) {
-            hi = last;
-            hi_off = lo;
-          }
-          live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
-          running += 1;
-          st_live[lane] = live;
-          st_run[lane] = running;
-          st_hi[lane] = hi_off;
           if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78)
             q.admitted[h_idx[hs]] = 1;
             const int64_t o = int64_t(i) * kActiveCap + nact;
             in.act_uid[o] = h_uid[hs];
             in.act_P[o] = P;
-            in.act_k[o] = kt;
+            in.act_k[o] = kr;
             in.act_t0[o] = now;
             in.act_T[o] = T;
             ++nact;
@@ -1630,22 +1713,17 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
             status = KX_ERR_CAPACITY;
           }
         }
+        ++nadm;
+        ++pos;
         if (__any_sync(0xffffffffu, status != KX_OK)) {
           status = KX_ERR_CAPACITY;
           broke = true;
+          // the evaluator is waiting for the next report
+          pp_sync(kBarRowReady);
+          report(2, 0);
           break;
         }
-        ++nadm;
-        ++pos;
-        tfix = bl;
-        own_row = false;
-        if (lane == 0) ctl[step & 1] = PipeCtl{pos, 0, bl};
-        ++step;
-        pipe_sync();
       }
-      // release the evaluator
-      if (lane == 0) ctl[step & 1] = PipeCtl{pos, 1, -1};
-      pipe_sync();
       // Phase 1 ran out of prefix heads without finishing the round: hand the
       // state to the continuation (no gc yet: the round is not over).
       const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
@@ -1671,6 +1749,10 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
         in.running[i] = running;
         in.suspended[i] = susp ? 1 : 0;
       }
+      {
+        const uint64_t hm = warp_max_u64(static_cast<uint64_t>(act ? hi : INT64_MIN) ^ 0x8000000000000000ull);
+        if (lane == 0) s_win[2] = static_cast<int64_t>(hm ^ 0x8000000000000000ull);
+      }
       if (lane == 0) {
         if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
         if (!defer_rest) {
@@ -1682,12 +1764,17 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
     }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < 32 * ring; j += kPipeThreads) {
-    const int l = j & 31, p2 = j >> 5;
-    const int li = s_li[l];
-    if (li >= 0) {
-      in.usage[int64_t(ib + li) * ring + p2] = su[j];
-      in.exists[int64_t(ib + li) * ring + p2] = se[j];
+  {
+    // write back the window (booked slots only grow hi; gc only clears inside it)
+    const int64_t top = s_win[2] > wtop ? s_win[2] : wtop;
+    const int wn = top < wB ? 0 : static_cast<int>(top - wB + 1 < ring ? top - wB + 1 : ring);
+    for (int e = threadIdx.x; e < wn * 32; e += kPipeThreads) {
+      const int l = e & 31;
+      const int li = s_li[l];
+      if (li < 0) continue;
+      const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
+      in.usage[int64_t(ib + li) * ring + pos] = su[pos * 32 + l];
+      in.exists[int64_t(ib + li) * ring + pos] = se[pos * 32 + l];
     }
   }
 }
@@ -1830,7 +1917,7 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
   if (max_inst_per_pool <= 32) {
     const PipeLayout pl = pipe_layout(dp.ring);
     if (!getenv("KX_DISPATCH_SINGLE_WARP") && pl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
-      k_dispatch_pipe<<<n_pools, kPipeThreads, pl.total, st>>>(q, a, in, pool_begin, perm,
+      k_dispatch_pipe<<<n_pools, kPipeThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
                                                               pool_offsets, dp, pl, rows, cand,
                                                               row_count, admitted_count,
                                                               pool_status, phase);

@@ -9,7 +9,10 @@
 namespace kx {
 
 constexpr int kMaxInstPerPool = 512;
-constexpr int kDispSmemLimit = 200 * 1024;  // dynamic shared memory of the dispatch CTA
+constexpr int kDispSmemLimit = 220 * 1024;  // dynamic shared memory of the dispatch CTA
+// The sequential dispatch CTAs reserve a whole SM's shared memory so no other
+// kernel's CTAs (the concurrent sort) share their SM's issue slots.
+constexpr int kDispSmemExclusive = 220 * 1024;
 
 struct DispatchParams {
   int32_t oracle_T;

@@ -25,3 +25,15 @@ rows, _ = s.fetch_dispatch()
 print("decisions", sum(len(r) for r in rows), "admitted", sum(int(r["admitted"].sum()) for r in rows))
 for k, v in s.profile_read().items():
     print(f"{k:14s} {v['ms'] / ticks:8.3f} ms/tick  launches {v['launches'] / ticks:.0f}")
+
+# the same round without the overlap: full order first, then the dispatch alone
+s.profile(False)
+s.profile(True)
+for _ in range(ticks):
+    s.restore()
+    s.order()
+    s.dispatch_round(bench.NOW)
+s.synchronize()
+print("-- order, then dispatch (no overlap)")
+for k, v in s.profile_read().items():
+    print(f"{k:14s} {v['ms'] / ticks:8.3f} ms/tick  launches {v['launches'] / ticks:.0f}")

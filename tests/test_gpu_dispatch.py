@@ -34,7 +34,7 @@ def test_dispatch_matches_reference_fixture(gpu_lib, name):
         rows, cand = s.fetch_dispatch()
         rows, cand = rows[0], cand[0]
         assert len(rows) == len(rd["dec_uid"]), f"round {r}"
-        assert np.array_equal(rows["uid"], rd["dec_uid"])
+        assert np.array_equal(rows["uid"], rd["dec_uid"]), f"round {r}"
         assert np.array_equal(rows["target"], rd["dec_target"])
         assert np.array_equal(rows["admitted"], rd["dec_admitted"])
         assert np.array_equal(bits(rows["predicted_peak"]), bits(rd["dec_peak"]))
