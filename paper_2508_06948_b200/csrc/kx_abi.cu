@@ -1555,6 +1555,11 @@ int kx_profile_read(kx_sched* s, kx_phase_stat* out, int32_t cap, int32_t* n_out
 
 int64_t kx_launch_count(void) { return kx::g_kx_launches.load(); }
 
+// Diagnostics: globaltimer stamps of the last batched dispatch kernel (pool 0).
+int kx_debug_dispatch_timers(uint64_t* out16) {
+  return guard([&] { kx::read_dispatch_debug(reinterpret_cast<unsigned long long*>(out16)); });
+}
+
 int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining,
                         const uint8_t* present, int32_t scope_all, uint64_t* pairs, double* correct,
                         double* accuracy) {

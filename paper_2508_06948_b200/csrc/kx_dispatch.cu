@@ -18,6 +18,7 @@
 // (SURVEY H9), so one __syncthreads per decision suffices.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstring>
 #include <stdint.h>
 
 #include "kx_common.cuh"
@@ -1779,6 +1780,789 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
   }
 }
 
+// ---- K5 batched: parallel look-ahead rows + one resolver warp ---------------
+// Same decisions as k_dispatch_warp. The heads of a round are taken in
+// batches of kBatchEval: each evaluator warp computes the try_place row of
+// one head of the batch (lanes = instances) against the state at the start
+// of the batch, all in parallel; then the resolver warp walks the batch in
+// priority order. A head's row is exact except for the instances changed by
+// the batch's earlier decisions (a commit, or a suspension on overload);
+// the resolver re-evaluates just those (eight slot-lanes per instance, four
+// instances per pass), then runs select_instance, the overload check, the
+// decision log and the commit. Rows and state live in shared memory; the
+// phases are separated by CTA barriers, two per batch.
+__device__ unsigned long long g_disp_dbg[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr int kBatchEval = 8;
+constexpr int kBatchThreads = 32 * (kBatchEval + 1);
+
+struct BatchLayout {
+  uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
+      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_peak, g_cand, usage,
+      ex, total;
+};
+
+// Decision records staged by the resolver and written to global memory by
+// it during the next evaluation phase (off the decision chain).
+constexpr int kStage = 64;
+struct StageMeta {
+  int32_t hs;      // head ring slot
+  int32_t target;  // lane of the target, -1 none
+  int32_t admitted;
+  int32_t act_slot;  // active-table slot of an admission
+};
+
+BatchLayout batch_layout(int ring) {
+  BatchLayout L{};
+  uint32_t o = 0;
+  auto take = [&](size_t bytes) {
+    const uint32_t at = o;
+    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
+    return at;
+  };
+  L.h_idx = take(4 * kHR);
+  L.h_agent = take(4 * kHR);
+  L.h_prompt = take(8 * kHR);
+  L.h_kept = take(8 * kHR);
+  L.h_uid = take(8 * kHR);
+  L.h_T = take(8 * kHR);
+  L.h_first = take(8 * kHR);
+  L.h_last = take(8 * kHR);
+  L.h_mode = take(4 * kHR);
+  L.tab = take(size_t(8) * kHR * kDtSlots);
+  L.lane_inst = take(4 * 32);
+  L.st_live = take(8 * 32);
+  L.st_run = take(4 * 32);
+  L.st_susp = take(4 * 32);
+  L.st_hi = take(4 * 32);
+  L.st_umax = take(8 * 32);
+  L.r_viol = take(4 * 32 * kBatchEval);
+  L.r_peak = take(8 * 32 * kBatchEval);
+  L.r_flag = take(4 * 32 * kBatchEval);
+  L.g_meta = take(sizeof(StageMeta) * kStage);
+  L.g_peak = take(8 * kStage);
+  L.g_cand = take(size_t(8) * 32 * kStage);
+  L.usage = take(size_t(8) * 32 * ring);
+  L.ex = take(size_t(32) * ring);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void batch_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kBatchThreads) : "memory"); }
+
+__global__ void __launch_bounds__(kBatchThreads)
+k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
+                 const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
+                 DispatchParams dp, BatchLayout lay, kx_decision* __restrict__ rows,
+                 double* __restrict__ cand, int64_t* __restrict__ row_count,
+                 int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
+                 DispPhase ph) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int64_t s_win[3];   // staged slot window [B, top]; top after the round
+  __shared__ int64_t s_next;     // first head of the next batch (resolver -> all)
+  __shared__ int32_t s_stop;     // resolver: round over
+  __shared__ int32_t s_ids[32];  // InstanceId per lane
+  const int pool = blockIdx.x;
+  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
+  const uint32_t* hp = perm + pool_offsets[pool];
+  int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
+  bool skip = false;
+  if (ph.phase == 1) {
+    const TopKState t = ph.tk[pool];
+    if (t.defer) {  // too many ties at the boundary key: wait for the full order
+      if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
+      skip = true;
+    }
+    hp = ph.heads + int64_t(pool) * kTopKMax;
+    q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
+  } else if (ph.phase == 2) {
+    const DispResume r = ph.resume[pool];
+    skip = !r.need;
+    pos0 = r.start;
+    nrows0 = r.nrows;
+    nadm0 = r.nadm;
+  }
+  if (skip) return;  // uniform over the CTA
+  const bool dbg = blockIdx.x == 0 && threadIdx.x == 0;
+  if (dbg) g_disp_dbg[0] = gtimer();
+  unsigned long long acc_a = 0, acc_b = 0, acc_fix = 0, acc_sel = 0, acc_com = 0, tA = 0, nb = 0;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ib = pool_begin[pool];
+  const int ni = pool_begin[pool + 1] - ib;
+  const int ring = dp.ring;
+  const int rmask = ring - 1;
+#define BL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
+  double* const su = BL(double, usage);
+  uint8_t* const se = BL(uint8_t, ex);
+  int32_t* const s_li = BL(int32_t, lane_inst);
+  uint32_t* const h_idx = BL(uint32_t, h_idx);
+  int32_t* const h_agent = BL(int32_t, h_agent);
+  int64_t* const h_prompt = BL(int64_t, h_prompt);
+  int64_t* const h_kept = BL(int64_t, h_kept);
+  uint64_t* const h_uid = BL(uint64_t, h_uid);
+  double* const h_T = BL(double, h_T);
+  int64_t* const h_first = BL(int64_t, h_first);
+  int64_t* const h_last = BL(int64_t, h_last);
+  int32_t* const h_mode = BL(int32_t, h_mode);
+  double* const stab = BL(double, tab);
+  double* const st_live = BL(double, st_live);
+  int32_t* const st_run = BL(int32_t, st_run);
+  int32_t* const st_susp = BL(int32_t, st_susp);
+  int32_t* const st_hi = BL(int32_t, st_hi);
+  uint64_t* const st_umax = BL(uint64_t, st_umax);
+  uint32_t* const r_viol = BL(uint32_t, r_viol);
+  uint64_t* const r_peak = BL(uint64_t, r_peak);
+  uint32_t* const r_flag = BL(uint32_t, r_flag);
+  StageMeta* const g_meta = BL(StageMeta, g_meta);
+  double* const g_peak = BL(double, g_peak);
+  double* const g_cand = BL(double, g_cand);
+#undef BL
+  const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
+  constexpr uint32_t kNone = 0xffffffffu;
+
+  // Lane of each instance: rank of its InstanceId within the pool (H9).
+  if (warp == 0) {
+    const int32_t myid = lane < ni ? in.id[ib + lane] : 0x7fffffff;
+    int rank = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t o = __shfl_sync(0xffffffffu, myid, l);
+      rank += (l < ni) && (o < myid || (o == myid && l < lane));
+    }
+    s_li[lane] = -1;
+    __syncwarp();
+    if (lane < ni) s_li[rank] = lane;
+    const bool a0 = lane < ni;
+    const int64_t bb = a0 ? in.base_slot[ib + lane] : INT64_MAX;
+    const int64_t hh = a0 ? in.hi_slot[ib + lane] : INT64_MIN;
+    const uint64_t bmin = warp_min_u64(static_cast<uint64_t>(bb) ^ 0x8000000000000000ull);
+    const uint64_t hmax = warp_max_u64(static_cast<uint64_t>(hh) ^ 0x8000000000000000ull);
+    if (lane == 0) {
+      s_win[0] = static_cast<int64_t>(bmin ^ 0x8000000000000000ull);
+      s_win[1] = static_cast<int64_t>(hmax ^ 0x8000000000000000ull);
+      s_stop = 0;
+      s_next = pos0;
+    }
+  }
+  __syncthreads();
+  // Stage the rings transposed (usage[pos][lane]): zero everywhere, then copy
+  // the slot window's positions, four independent loads in flight per thread.
+  const int64_t wB = s_win[0];
+  const int64_t wtop = s_win[1];
+  const int win = wtop < wB ? 0 : static_cast<int>(wtop - wB + 1 < ring ? wtop - wB + 1 : ring);
+  for (int j = threadIdx.x; j < 32 * ring; j += kBatchThreads) {
+    su[j] = 0.0;
+    se[j] = 0;
+  }
+  __syncthreads();
+  {
+    const int total = win * 32;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kBatchThreads) {
+      double u[4];
+      uint8_t x[4];
+      int dst[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + k * kBatchThreads;
+        const int l = e & 31;
+        const int li = e < total ? s_li[l] : -1;
+        const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
+        dst[k] = li >= 0 ? pos * 32 + l : -1;
+        u[k] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
+        x[k] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (dst[k] >= 0) {
+          su[dst[k]] = u[k];
+          se[dst[k]] = x[k];
+        }
+    }
+  }
+  __syncthreads();
+
+  // ---- per-lane instance constants (every warp) ----
+  if (dbg) g_disp_dbg[1] = gtimer();
+  const double now = dp.now;
+  const double L = dp.slot_len;
+  const int li = s_li[lane];
+  const bool act = li >= 0;
+  const int i = ib + (act ? li : 0);
+  const double cap = act ? in.cap[i] : 0.0;
+  const double kr = act ? in.decode_rate[i] : 0.0;
+  const int32_t mb = act ? in.max_batch[i] : 0;
+  const int32_t id = act ? in.id[i] : 0x7fffffff;
+  const int32_t waiting = act ? in.waiting[i] : 0;
+  const double wcap = __dmul_rn(dp.watermark, cap);
+  const int64_t base = act ? in.base_slot[i] : 0;
+  const int64_t hi0 = act ? in.hi_slot[i] : -1;
+  const double k0 = __shfl_sync(0xffffffffu, kr, 0);
+  const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
+  const int64_t B = wB;
+  if (warp == 0) s_ids[lane] = id;
+  const int32_t lo_off = static_cast<int32_t>(base - B);
+  const double t0e = __dadd_rn(now, kTimeEpsilon);
+  const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
+
+  // ---- head ring (warp 1 loads 32-head blocks ahead of use) ----
+  int64_t nx_start = pos0, nx_n = 0;
+  uint32_t nx_idx = 0;
+  int32_t nx_agent = 0;
+  int64_t nx_prompt = 0, nx_kept = 0;
+  uint64_t nx_uid = 0;
+  double nx_T = 0.0;
+  int stage = 0;
+  int64_t loaded_end = pos0;
+  auto issue_idx = [&](int64_t start) {
+    nx_start = start;
+    nx_n = q_end - start < kWHB ? q_end - start : kWHB;
+    if (nx_n < 0) nx_n = 0;
+    nx_idx = lane < nx_n ? hp[start + lane] : 0u;
+    stage = 0;
+  };
+  auto issue_fields = [&]() {
+    if (lane < nx_n) {
+      nx_agent = q.agent[nx_idx];
+      nx_prompt = q.prompt[nx_idx];
+      nx_kept = q.kept[nx_idx];
+      nx_uid = q.uid[nx_idx];
+      if (dp.oracle_T) nx_T = q.pure_exec[nx_idx];
+    }
+    stage = 1;
+  };
+  auto issue_T = [&]() {
+    if (!dp.oracle_T && lane < nx_n) nx_T = ag.T[nx_agent];
+    stage = 2;
+  };
+  auto land_block = [&]() {
+    if (stage < 1) issue_fields();
+    if (stage < 2) issue_T();
+    const int half = static_cast<int>(((nx_start - pos0) / kWHB) & 1);
+    const int hb = half * kWHB;
+    const int n = static_cast<int>(nx_n);
+    if (lane < n) {
+      const int hs = hb + lane;
+      h_idx[hs] = nx_idx;
+      h_agent[hs] = nx_agent;
+      h_prompt[hs] = nx_prompt;
+      h_kept[hs] = nx_kept;
+      h_uid[hs] = nx_uid;
+      h_T[hs] = nx_T;
+      int64_t f, l;
+      span_bounds_dev(now, nx_T, L, &f, &l);
+      h_first[hs] = f;
+      h_last[hs] = l;
+      bool fast = nx_T > 0.0 && nx_prompt >= 0 && f == cslot && l >= f && l - f + 1 <= kDtSlots;
+      if (fast) {
+        const double te = __dadd_rn(now, nx_T);
+        const double tee = __dsub_rn(te, kTimeEpsilon);
+        const double m0 = slot_dt(now, t0e, te, tee, f - 2, L);
+        const double m1 = slot_dt(now, t0e, te, tee, f - 1, L);
+        const double m2 = slot_dt(now, t0e, te, tee, l + 1, L);
+        const double m3 = slot_dt(now, t0e, te, tee, l + 2, L);
+        fast = m0 != m0 && m1 != m1 && m2 != m2 && m3 != m3;
+      }
+      h_mode[hs] = fast ? (k_uniform ? kModeTabPk : kModeTabDt) : kModeGeneric;
+    }
+    __syncwarp();
+    for (int hh = 0; hh < n; ++hh) {
+      const int hs = hb + hh;
+      const int mode = h_mode[hs];
+      if (mode == kModeGeneric) continue;
+      const double Th = h_T[hs];
+      const double Ph = static_cast<double>(h_prompt[hs]);
+      const double te = __dadd_rn(now, Th);
+      const double tee = __dsub_rn(te, kTimeEpsilon);
+      const int tn = static_cast<int>(h_last[hs] - h_first[hs] + 1);
+      for (int j = lane; j < tn; j += 32) {
+        const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
+        stab[hs * kDtSlots + j] = mode == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
+      }
+    }
+    __syncwarp();
+    loaded_end = nx_start + nx_n;
+    issue_idx(loaded_end);
+  };
+  if (warp == 1) {
+    issue_idx(pos0);
+    if (pos0 < q_end) land_block();
+  }
+
+  // ---- resolver state (warp 0) ----
+  double live = act ? in.live_kv[i] : 0.0;
+  int32_t running = act ? in.running[i] : 0;
+  bool susp = act ? in.suspended[i] != 0 : false;
+  int64_t hi = hi0;
+  int32_t hi_off = static_cast<int32_t>(hi0 - B);
+  int32_t nact = act ? in.n_active[i] : 0;
+  uint64_t umax = kZeroBits;  // max stored usage over the whole ledger window
+  for (int32_t o = lo_off; o <= hi_off; ++o) {
+    const int p2 = static_cast<int>((B + o) & rmask);
+    if (se[p2 * 32 + lane]) {
+      const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+      umax = tb > umax ? tb : umax;
+    }
+  }
+  if (warp == 0) {
+    st_live[lane] = live;
+    st_run[lane] = running;
+    st_susp[lane] = susp ? 1 : 0;
+    st_hi[lane] = hi_off;
+    st_umax[lane] = umax;
+  }
+  int64_t pos = pos0;
+  int64_t nrows = nrows0, nadm = nadm0;
+  int retries = 0;
+  bool broke = false;
+  int status = KX_OK;
+  int n_stage = 0;          // staged decision records (resolver)
+  int64_t stage_row0 = nrows0;  // log row of the first staged record
+  // Write the staged records: decision log rows + candidate peaks
+  // (engine.cpp:242-246), admitted flags and active_ entries
+  // (dispatcher.cpp:78).
+  auto flush = [&]() {
+    __syncwarp();
+    for (int r = 0; r < n_stage; ++r) {
+      const StageMeta m = g_meta[r];
+      const int64_t row = stage_row0 + r;
+      if (row < dp.log_cap) {
+        const int64_t ro = int64_t(pool) * dp.log_cap + row;
+        if (lane == 0) {
+          kx_decision d;
+          d.time = now;
+          d.predicted_peak = g_peak[r];
+          d.uid = h_uid[m.hs];
+          d.queue_index = h_idx[m.hs];
+          d.agent = h_agent[m.hs];
+          d.target = m.target >= 0 ? s_ids[m.target] : -1;
+          d.pool = pool;
+          d.admitted = m.admitted;
+          rows[ro] = d;
+        }
+        if (act) cand[ro * dp.peak_stride + li] = g_cand[r * 32 + lane];
+      }
+      if (m.admitted && lane == m.target) {
+        q.admitted[h_idx[m.hs]] = 1;
+        if (m.act_slot >= 0) {
+          const int64_t o = int64_t(i) * kActiveCap + m.act_slot;
+          in.act_uid[o] = h_uid[m.hs];
+          in.act_P[o] = static_cast<double>(h_prompt[m.hs]);
+          in.act_k[o] = kr;
+          in.act_t0[o] = now;
+          in.act_T[o] = h_T[m.hs];
+        }
+      }
+    }
+    stage_row0 += n_stage;
+    n_stage = 0;
+  };
+  __syncthreads();
+
+  while (true) {
+    const int64_t b0 = s_next;
+    if (s_stop || b0 >= q_end) break;
+    const int kb = static_cast<int>(q_end - b0 < kBatchEval ? q_end - b0 : kBatchEval);
+    // ---------------- phase A: rows of the batch's heads ----------------
+    if (dbg) tA = clock64();
+    if (warp == 0) flush();  // the previous batch's records, beside the evaluators
+    if (warp >= 1 && warp - 1 < kb) {
+      const int j = warp - 1;
+      const int64_t hpos = b0 + j;
+      const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
+      const int mode = h_mode[hs];
+      const int64_t first = h_first[hs];
+      const int64_t last = h_last[hs];
+      const double P = static_cast<double>(h_prompt[hs]);
+      const int32_t fo = static_cast<int32_t>(first - B);
+      const int32_t lo = static_cast<int32_t>(last - B);
+      const bool nonempty = last >= first;
+      const double lv = st_live[lane];
+      const bool sp = st_susp[lane] != 0 && !(lv < wcap);
+      const bool eligible = act && !sp && !(st_run[lane] + waiting >= mb);
+      uint32_t viol = kNone;
+      uint64_t peak = kZeroBits;
+      const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
+      if (eligible) {
+        if (mode != kModeGeneric) {
+          peak = st_umax[lane];
+          const double* tab = stab + hs * kDtSlots;
+          const int tn = lo - fo + 1;
+          int p2 = static_cast<int>((B + fo) & rmask);
+          if (mode == kModeTabPk) {
+#pragma unroll 4
+            for (int jj = 0; jj < tn; ++jj) {
+              const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
+              if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
+              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+              peak = tb > peak ? tb : peak;
+              p2 = (p2 + 1) & rmask;
+            }
+          } else {
+#pragma unroll 4
+            for (int jj = 0; jj < tn; ++jj) {
+              const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[jj]));
+              if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
+              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+              peak = tb > peak ? tb : peak;
+              p2 = (p2 + 1) & rmask;
+            }
+          }
+        } else {  // generic slot walk over the whole window
+          const double te = __dadd_rn(now, h_T[hs]);
+          const double tee = __dsub_rn(te, kTimeEpsilon);
+          const int32_t top = st_hi[lane] > lo ? st_hi[lane] : lo;
+          for (int32_t o = lo_off; o <= top; ++o) {
+            const int p2 = static_cast<int>((B + o) & rmask);
+            const bool e = se[p2 * 32 + lane] != 0;
+            const bool in_span = o >= fo && o <= lo;
+            if (!(e || in_span)) continue;
+            const double used = e ? su[p2 * 32 + lane] : 0.0;
+            const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
+            if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
+            const uint64_t tb = ordered_bits(total);
+            peak = tb > peak ? tb : peak;
+          }
+        }
+      }
+      r_viol[j * 32 + lane] = viol;
+      r_peak[j * 32 + lane] = peak;
+      r_flag[j * 32 + lane] = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+    }
+    batch_sync();
+    if (dbg) { const unsigned long long t = clock64(); acc_a += t - tA; tA = t; ++nb; }
+    // ---------------- phase B: resolve the batch in order ----------------
+    if (warp == 1) {
+      // the next batch's heads [b0 + kb, b0 + kb + kBatchEval) must be landed
+      const int64_t need_end = b0 + kb + kBatchEval;
+      if (loaded_end < q_end && need_end > loaded_end) land_block();
+      else if (stage == 0) issue_fields();
+      else if (stage == 1) issue_T();
+    } else if (warp == 0) {
+      uint32_t dirty = 0;  // lanes changed since the batch's rows were computed
+      int j = 0;
+      while (j < kb) {
+        const int64_t hpos = b0 + j;
+        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
+        uint32_t viol = r_viol[j * 32 + lane];
+        uint64_t peak = r_peak[j * 32 + lane];
+        uint32_t flg = r_flag[j * 32 + lane];
+        const int64_t prompt = h_prompt[hs];
+        const double P = static_cast<double>(prompt);
+        const int64_t first = h_first[hs];
+        const int64_t last = h_last[hs];
+        const int mode = h_mode[hs];
+        const double T = h_T[hs];
+        const bool nonempty = last >= first;
+        const int32_t fo = static_cast<int32_t>(first - B);
+        const int32_t lo = static_cast<int32_t>(last - B);
+        const bool fast = mode != kModeGeneric;
+        const int tn = lo - fo + 1;
+        const double* tab = stab + hs * kDtSlots;
+        uint32_t fixm = dirty;
+        bool done_head = false;
+        while (!done_head) {
+          // collect_live (engine.cpp:187-202), every loop iteration:
+          // watermark resume (the evaluators applied the same rule to the
+          // state published at the start of the batch).
+          if (susp && live < wcap) {
+            susp = false;
+            st_susp[lane] = 0;
+          }
+          // ---- re-evaluate the changed instances for this head ----
+          const bool my_elig = act && !susp && !(running + waiting >= mb);
+          unsigned long long tf0 = dbg ? clock64() : 0;
+          if (fixm) {
+            if (fast && tn <= 8) {
+              // four instances per pass, eight slot-lanes each
+              uint32_t rem = fixm;
+              while (rem) {
+                const int g = lane >> 3, s = lane & 7;
+                // the first four set lanes of rem, group g takes the g-th
+                uint32_t r1 = rem & (rem - 1), r2 = r1 & (r1 - 1), r3 = r2 & (r2 - 1);
+                const uint32_t pick = g == 0 ? rem : g == 1 ? r1 : g == 2 ? r2 : r3;
+                const int dl = pick ? __ffs(pick) - 1 : -1;
+                const int dsrc = dl >= 0 ? dl : 0;
+                const bool e_d = __shfl_sync(0xffffffffu, my_elig, dsrc) && dl >= 0;
+                const double cap_d = __shfl_sync(0xffffffffu, cap, dsrc);
+                const double k_d = __shfl_sync(0xffffffffu, kr, dsrc);
+                const uint64_t um_d = shfl_u64(umax, dsrc);
+                uint32_t vv = kNone;
+                uint64_t pp = kZeroBits;
+                if (e_d && s < tn) {
+                  const int p2 = static_cast<int>((B + fo + s) & rmask);
+                  const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, k_d, tab[s]);
+                  const double total = __dadd_rn(su[p2 * 32 + dl], pk);
+                  if (total > cap_d) vv = static_cast<uint32_t>(fo + s);
+                  pp = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+                }
+#pragma unroll
+                for (int m = 1; m < 8; m <<= 1) {
+                  const uint32_t v2 = __shfl_xor_sync(0xffffffffu, vv, m, 8);
+                  const uint64_t p2 = (static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(pp >> 32), m, 8)) << 32) |
+                                      __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(pp), m, 8);
+                  vv = v2 < vv ? v2 : vv;
+                  pp = p2 > pp ? p2 : pp;
+                }
+                pp = um_d > pp ? um_d : pp;
+                // hand each group's result to its instance lane
+                const bool mine = (rem >> lane) & 1u;
+                const int myg = __popc(rem & ((1u << lane) - 1u));
+                const bool take = mine && myg < 4;
+                const int src = take ? myg * 8 : lane;
+                const uint32_t v_t = __shfl_sync(0xffffffffu, vv, src);
+                const uint64_t p_t = shfl_u64(pp, src);
+                const bool e_t = __shfl_sync(0xffffffffu, e_d, src);
+                if (take) {
+                  viol = e_t ? v_t : kNone;
+                  peak = e_t ? p_t : kZeroBits;
+                  flg = (e_t ? 1u : 0u) | (e_t && nonempty && (first < base || last >= base + ring) ? 2u : 0u);
+                }
+                // drop the (up to) four lanes just handled
+                rem = r3 & (r3 - 1);
+              }
+            } else {
+              // one instance at a time, lanes over its window
+              uint32_t rem = fixm;
+              while (rem) {
+                const int t = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const bool e_t = __shfl_sync(0xffffffffu, my_elig, t);
+                uint32_t v_t = kNone;
+                uint64_t p_t = kZeroBits;
+                bool o_t = false;
+                if (e_t) {
+                  const int32_t lo_t = __shfl_sync(0xffffffffu, lo_off, t);
+                  const int32_t hio_t = __shfl_sync(0xffffffffu, hi_off, t);
+                  const double cap_t = __shfl_sync(0xffffffffu, cap, t);
+                  const double k_t = __shfl_sync(0xffffffffu, kr, t);
+                  const int64_t base_t = B + lo_t;
+                  o_t = nonempty && (first < base_t || last >= base_t + ring);
+                  const int32_t w0 = fast ? fo : lo_t;
+                  const int32_t w1 = fast ? lo : (hio_t > lo ? hio_t : lo);
+                  const double te = __dadd_rn(now, T);
+                  const double tee = __dsub_rn(te, kTimeEpsilon);
+                  uint32_t vv = kNone;
+                  uint64_t pp = fast ? shfl_u64(umax, t) : kZeroBits;
+                  for (int32_t o0 = w0; o0 <= w1; o0 += 32) {
+                    const int32_t o = o0 + lane;
+                    if (o <= w1) {
+                      const int p2 = static_cast<int>((B + o) & rmask);
+                      const bool e = se[p2 * 32 + t] != 0;
+                      const bool in_span = o >= fo && o <= lo;
+                      if (e || in_span) {
+                        const double used = e ? su[p2 * 32 + t] : 0.0;
+                        double pk;
+                        if (fast) pk = in_span ? (mode == kModeTabPk ? tab[o - fo] : pk_of(P, k_t, tab[o - fo])) : 0.0;
+                        else pk = pk_of(P, k_t, slot_dt(now, t0e, te, tee, B + o, L));
+                        const double total = __dadd_rn(used, pk);
+                        if (in_span && total > cap_t && static_cast<uint32_t>(o) < vv) vv = static_cast<uint32_t>(o);
+                        const uint64_t tb = ordered_bits(total);
+                        pp = tb > pp ? tb : pp;
+                      }
+                    }
+                  }
+                  v_t = __reduce_min_sync(0xffffffffu, vv);
+                  p_t = warp_max_u64(pp);
+                }
+                if (lane == t) {
+                  viol = v_t;
+                  peak = e_t ? p_t : kZeroBits;
+                  flg = (e_t ? 1u : 0u) | (o_t ? 2u : 0u);
+                }
+              }
+            }
+            fixm = 0;
+          }
+          unsigned long long tf1 = dbg ? clock64() : 0;
+          if (dbg) acc_fix += tf1 - tf0;
+          if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
+            status = KX_ERR_CAPACITY;
+            broke = true;
+            break;
+          }
+          const bool elig = flg & 1u;
+          const bool fits = elig && viol == kNone;
+          // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
+          const uint64_t key = fits ? peak : ~0ull;
+          const uint64_t wkey = warp_min_u64(key);
+          const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
+          const int bl = winners ? __ffs(winners) - 1 : -1;
+          const int bsrc = bl >= 0 ? bl : 0;
+          const double blive = __shfl_sync(0xffffffffu, live, bsrc);
+          const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
+          const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
+          const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
+          {  // stage the decision record (engine.cpp:242-246); flushed later
+            if (n_stage == kStage) flush();
+            const int r = n_stage;
+            if (lane == 0) {
+              g_meta[r] = StageMeta{hs, bl, (bl >= 0 && !overload) ? 1 : 0, -1};
+              g_peak[r] = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
+            }
+            double v = -1.0;
+            if (elig) {
+              v = fits ? from_ordered_bits(peak)
+                       : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
+            }
+            g_cand[r * 32 + lane] = v;
+            ++n_stage;
+          }
+          unsigned long long ts1 = dbg ? clock64() : 0;
+          if (dbg) acc_sel += ts1 - tf1;
+          ++nrows;
+          if (bl < 0) {  // head keeps its place (engine.cpp:247)
+            broke = true;
+            break;
+          }
+          if (overload) {
+            if (lane == bl) {  // Dispatcher::on_overload
+              susp = true;
+              st_susp[lane] = 1;
+            }
+            if (++retries > ni) {
+              status = KX_ERR_LIVELOCK;
+              broke = true;
+              break;
+            }
+            dirty |= 1u << bl;
+            fixm = 1u << bl;
+            continue;
+          }
+          retries = 0;
+          // Dispatcher::commit: book the target's span slots (lanes = slots)
+          // and raise the target's maximum stored usage.
+          const double kt = __shfl_sync(0xffffffffu, kr, bl);
+          uint64_t nb = kZeroBits;
+          if (fast) {
+            for (int s = lane; s < tn; s += 32) {
+              const int p2 = static_cast<int>((B + fo + s) & rmask);
+              const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, kt, tab[s]);
+              const double nu = __dadd_rn(su[p2 * 32 + bl], pk);
+              su[p2 * 32 + bl] = nu;
+              se[p2 * 32 + bl] = 1;
+              const uint64_t tb = ordered_bits(nu);
+              nb = tb > nb ? tb : nb;
+            }
+          } else {
+            const double te = __dadd_rn(now, T);
+            const double tee = __dsub_rn(te, kTimeEpsilon);
+            for (int64_t s = first + lane; s <= last; s += 32) {
+              const int p2 = static_cast<int>(s & rmask);
+              const double nu = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
+              su[p2 * 32 + bl] = nu;
+              se[p2 * 32 + bl] = 1;
+              const uint64_t tb = ordered_bits(nu);
+              nb = tb > nb ? tb : nb;
+            }
+          }
+          nb = warp_max_u64(nb);
+          __syncwarp();
+          if (lane == bl) {
+            if (nonempty && last > hi) {
+              hi = last;
+              hi_off = lo;
+            }
+            live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
+            running += 1;
+            umax = nb > umax ? nb : umax;
+            st_live[lane] = live;
+            st_run[lane] = running;
+            st_hi[lane] = hi_off;
+            st_umax[lane] = umax;
+            if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78), written at flush
+              g_meta[n_stage - 1].act_slot = nact;
+              ++nact;
+            } else {
+              status = KX_ERR_CAPACITY;
+            }
+          }
+          if (__any_sync(0xffffffffu, status != KX_OK)) {
+            status = KX_ERR_CAPACITY;
+            broke = true;
+            break;
+          }
+          if (dbg) acc_com += clock64() - ts1;
+          dirty |= 1u << bl;
+          ++nadm;
+          ++pos;
+          done_head = true;
+        }
+        if (broke) break;
+        ++j;
+      }
+      if (lane == 0) {
+        s_next = pos;
+        s_stop = broke ? 1 : 0;
+      }
+    }
+    if (dbg) acc_b += clock64() - tA;
+    batch_sync();
+  }
+
+  if (dbg) g_disp_dbg[2] = gtimer();
+  if (warp == 0) {
+    flush();
+    // Phase 1 ran out of prefix heads without finishing the round: hand the
+    // state to the continuation (no gc yet: the round is not over).
+    const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
+    int64_t nbase = base;
+    if (!defer_rest) {
+      // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
+      if (act && cslot > base) {
+        const int64_t stop = cslot < base + ring ? cslot : base + ring;
+        for (int64_t s = base; s < stop; ++s) {
+          const int p2 = static_cast<int>(s & rmask);
+          su[p2 * 32 + lane] = 0.0;
+          se[p2 * 32 + lane] = 0;
+        }
+        nbase = cslot;
+      }
+    }
+    if (act) {
+      in.n_active[i] = nact;
+      if (!defer_rest) active_gc(in, i, now);
+      in.live_kv[i] = live;
+      in.base_slot[i] = nbase;
+      in.hi_slot[i] = hi;
+      in.running[i] = running;
+      in.suspended[i] = susp ? 1 : 0;
+    }
+    {
+      const uint64_t hm = warp_max_u64(static_cast<uint64_t>(act ? hi : INT64_MIN) ^ 0x8000000000000000ull);
+      if (lane == 0) s_win[2] = static_cast<int64_t>(hm ^ 0x8000000000000000ull);
+    }
+    if (lane == 0) {
+      if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
+      if (!defer_rest) {
+        row_count[pool] = nrows;
+        admitted_count[pool] = nadm;
+        pool_status[pool] = status;
+      }
+    }
+  }
+  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; g_disp_dbg[6] = acc_a; g_disp_dbg[7] = acc_b;
+             g_disp_dbg[8] = acc_fix; g_disp_dbg[9] = acc_sel; g_disp_dbg[10] = acc_com; g_disp_dbg[11] = nb; }
+  __syncthreads();
+  {
+    // write back the window (booked slots only grow hi; gc only clears inside it)
+    const int64_t top = s_win[2] > wtop ? s_win[2] : wtop;
+    const int wn = top < wB ? 0 : static_cast<int>(top - wB + 1 < ring ? top - wB + 1 : ring);
+    for (int e = threadIdx.x; e < wn * 32; e += kBatchThreads) {
+      const int l = e & 31;
+      const int lj = s_li[l];
+      if (lj < 0) continue;
+      const int p2 = static_cast<int>((wB + (e >> 5)) & rmask);
+      in.usage[int64_t(ib + lj) * ring + p2] = su[p2 * 32 + l];
+      in.exists[int64_t(ib + lj) * ring + p2] = se[p2 * 32 + l];
+    }
+  if (dbg) g_disp_dbg[4] = gtimer();
+  }
+}
+
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
 __global__ void k_ledger_try_place(InstDev in, int i, int ring, double P, double k, double t0,
                                    double T, double slot_len, double* out_peak, int64_t* out_viol,
@@ -1893,10 +2677,16 @@ __global__ void k_gc_all(InstDev in, int n_inst, int ring, double now, double sl
 }
 
 // ---- host wrappers -------------------------------------------------------
+void read_dispatch_debug(unsigned long long* out) {
+  KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_dbg, sizeof(unsigned long long) * 16));
+}
+
 void configure_dispatch_kernels() {
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kDispSmemLimit));
+  KX_CUDA(cudaFuncSetAttribute(k_dispatch_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
@@ -1905,7 +2695,8 @@ void configure_dispatch_kernels() {
 }
 
 bool dispatch_can_overlap(int max_inst_per_pool, int ring) {
-  return max_inst_per_pool <= 32 && pipe_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
+  return max_inst_per_pool <= 32 && batch_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
+         pipe_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
          warp_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
 }
 
@@ -1915,8 +2706,18 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st, DispPhase phase) {
   if (max_inst_per_pool <= 32) {
+    const char* variant = getenv("KX_DISPATCH");  // test knob: batch (default) | pipe | warp
+    const BatchLayout bl = batch_layout(dp.ring);
+    if ((!variant || !strcmp(variant, "batch")) && bl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+      k_dispatch_batch<<<n_pools, kBatchThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
+                                                                         pool_offsets, dp, bl, rows, cand,
+                                                                         row_count, admitted_count,
+                                                                         pool_status, phase);
+      KX_CHECK_LAUNCH();
+      return;
+    }
     const PipeLayout pl = pipe_layout(dp.ring);
-    if (!getenv("KX_DISPATCH_SINGLE_WARP") && pl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+    if ((!variant || !strcmp(variant, "pipe")) && pl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
       k_dispatch_pipe<<<n_pools, kPipeThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
                                                               pool_offsets, dp, pl, rows, cand,
                                                               row_count, admitted_count,

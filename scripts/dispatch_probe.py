@@ -37,3 +37,12 @@ s.synchronize()
 print("-- order, then dispatch (no overlap)")
 for k, v in s.profile_read().items():
     print(f"{k:14s} {v['ms'] / ticks:8.3f} ms/tick  launches {v['launches'] / ticks:.0f}")
+
+import ctypes as C
+buf = (C.c_uint64 * 16)()
+if hasattr(s.lib, "kx_debug_dispatch_timers"):
+    s.lib.kx_debug_dispatch_timers(buf)
+    t = list(buf)
+    print("batch kernel (pool 0) us: stage", (t[1] - t[0]) / 1e3, "loop", (t[2] - t[1]) / 1e3,
+          "epilogue", (t[3] - t[2]) / 1e3, "writeback", (t[4] - t[3]) / 1e3, "rows", t[5])
+    print("cycles: phaseA", t[6], "phaseB", t[7], "fix", t[8], "select+log", t[9], "commit", t[10], "batches", t[11])
