@@ -1784,13 +1784,17 @@ k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict_
 // Same decisions as k_dispatch_warp. The heads of a round are taken in
 // batches of kBatchEval: each evaluator warp computes the try_place row of
 // one head of the batch (lanes = instances) against the state at the start
-// of the batch, all in parallel; then the resolver warp walks the batch in
-// priority order. A head's row is exact except for the instances changed by
-// the batch's earlier decisions (a commit, or a suspension on overload);
-// the resolver re-evaluates just those (eight slot-lanes per instance, four
-// instances per pass), then runs select_instance, the overload check, the
-// decision log and the commit. Rows and state live in shared memory; the
-// phases are separated by CTA barriers, two per batch.
+// of the batch, all in parallel (phase A). The resolver warp then walks the
+// batch in priority order (phase B). A head's row is exact except for the
+// instances changed by the batch's earlier decisions (a commit, or a
+// suspension on overload); those lanes re-evaluate themselves from the
+// resolver's registers, all at once. select_instance is one 64-bit warp min,
+// the overload check a ballot, the commit a loop in the target's own lane.
+// Decision records are staged in shared memory and written to global memory
+// by another warp during the next batch's phase B.
+#ifndef KX_DISPATCH_TIMERS
+#define KX_DISPATCH_TIMERS 0
+#endif
 __device__ unsigned long long g_disp_dbg[16];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -1799,21 +1803,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 constexpr int kBatchEval = 8;
 constexpr int kBatchThreads = 32 * (kBatchEval + 1);
+constexpr int kStage = 64;  // staged decision records per batch buffer
+constexpr int kFlushWarp = 2;
+
+struct StageMeta {
+  int32_t hs;        // head ring slot
+  int32_t target;    // lane of the target, -1 none
+  int32_t admitted;
+  int32_t act_slot;  // active-table slot of an admission (-1 none)
+  double peak;       // predicted peak of the decision
+};
 
 struct BatchLayout {
   uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
-      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_peak, g_cand, usage,
-      ex, total;
-};
-
-// Decision records staged by the resolver and written to global memory by
-// it during the next evaluation phase (off the decision chain).
-constexpr int kStage = 64;
-struct StageMeta {
-  int32_t hs;      // head ring slot
-  int32_t target;  // lane of the target, -1 none
-  int32_t admitted;
-  int32_t act_slot;  // active-table slot of an admission
+      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_viol, g_peak, g_flag,
+      usage, ex, total;
 };
 
 BatchLayout batch_layout(int ring) {
@@ -1843,9 +1847,10 @@ BatchLayout batch_layout(int ring) {
   L.r_viol = take(4 * 32 * kBatchEval);
   L.r_peak = take(8 * 32 * kBatchEval);
   L.r_flag = take(4 * 32 * kBatchEval);
-  L.g_meta = take(sizeof(StageMeta) * kStage);
-  L.g_peak = take(8 * kStage);
-  L.g_cand = take(size_t(8) * 32 * kStage);
+  L.g_meta = take(sizeof(StageMeta) * 2 * kStage);
+  L.g_viol = take(size_t(4) * 32 * 2 * kStage);
+  L.g_peak = take(size_t(8) * 32 * 2 * kStage);
+  L.g_flag = take(size_t(1) * 32 * 2 * kStage);
   L.usage = take(size_t(8) * 32 * ring);
   L.ex = take(size_t(32) * ring);
   L.total = o;
@@ -1866,6 +1871,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   __shared__ int64_t s_next;     // first head of the next batch (resolver -> all)
   __shared__ int32_t s_stop;     // resolver: round over
   __shared__ int32_t s_ids[32];  // InstanceId per lane
+  __shared__ int32_t s_nstage[2];
+  __shared__ int64_t s_row0[2];  // log row of each staging buffer's first record
   const int pool = blockIdx.x;
   const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
   const uint32_t* hp = perm + pool_offsets[pool];
@@ -1887,9 +1894,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     nadm0 = r.nadm;
   }
   if (skip) return;  // uniform over the CTA
-  const bool dbg = blockIdx.x == 0 && threadIdx.x == 0;
+  const bool dbg = KX_DISPATCH_TIMERS && blockIdx.x == 0 && threadIdx.x == 0;
   if (dbg) g_disp_dbg[0] = gtimer();
-  unsigned long long acc_a = 0, acc_b = 0, acc_fix = 0, acc_sel = 0, acc_com = 0, tA = 0, nb = 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ib = pool_begin[pool];
@@ -1919,8 +1925,9 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   uint64_t* const r_peak = BL(uint64_t, r_peak);
   uint32_t* const r_flag = BL(uint32_t, r_flag);
   StageMeta* const g_meta = BL(StageMeta, g_meta);
-  double* const g_peak = BL(double, g_peak);
-  double* const g_cand = BL(double, g_cand);
+  uint32_t* const g_viol = BL(uint32_t, g_viol);
+  uint64_t* const g_peak = BL(uint64_t, g_peak);
+  uint8_t* const g_flag = BL(uint8_t, g_flag);
 #undef BL
   const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
   constexpr uint32_t kNone = 0xffffffffu;
@@ -1946,6 +1953,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       s_win[1] = static_cast<int64_t>(hmax ^ 0x8000000000000000ull);
       s_stop = 0;
       s_next = pos0;
+      s_nstage[0] = s_nstage[1] = 0;
     }
   }
   __syncthreads();
@@ -1984,9 +1992,9 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     }
   }
   __syncthreads();
+  if (dbg) g_disp_dbg[1] = gtimer();
 
   // ---- per-lane instance constants (every warp) ----
-  if (dbg) g_disp_dbg[1] = gtimer();
   const double now = dp.now;
   const double L = dp.slot_len;
   const int li = s_li[lane];
@@ -2003,10 +2011,82 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   const double k0 = __shfl_sync(0xffffffffu, kr, 0);
   const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
   const int64_t B = wB;
-  if (warp == 0) s_ids[lane] = id;
   const int32_t lo_off = static_cast<int32_t>(base - B);
   const double t0e = __dadd_rn(now, kTimeEpsilon);
   const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
+  if (warp == 0) s_ids[lane] = id;
+
+  // try_place of the head in ring slot hs for this lane's instance, given
+  // its live state (lanes = instances). Returns the row entry.
+  struct Row {
+    uint32_t viol;
+    uint64_t peak;
+    uint32_t flag;  // bit 0 eligible, bit 1 ring overflow
+  };
+  auto evaluate = [&](int hs, double live_, int32_t run_, bool susp_, uint64_t umax_, int32_t hi_off_) {
+    const int mode = h_mode[hs];
+    const int64_t first = h_first[hs];
+    const int64_t last = h_last[hs];
+    const double P = static_cast<double>(h_prompt[hs]);
+    const int32_t fo = static_cast<int32_t>(first - B);
+    const int32_t lo = static_cast<int32_t>(last - B);
+    const bool nonempty = last >= first;
+    const bool sp = susp_ && !(live_ < wcap);  // collect_live's watermark resume
+    const bool eligible = act && !sp && !(run_ + waiting >= mb);
+    Row r{kNone, kZeroBits, 0u};
+    const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
+    if (eligible) {
+      if (mode != kModeGeneric) {
+        uint64_t peak = umax_;
+        uint32_t viol = kNone;
+        const double* tab = stab + hs * kDtSlots;
+        const int tn = lo - fo + 1;
+        int p2 = static_cast<int>((B + fo) & rmask);
+        if (mode == kModeTabPk) {
+#pragma unroll 4
+          for (int jj = 0; jj < tn; ++jj) {
+            const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
+            if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
+            const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+            peak = tb > peak ? tb : peak;
+            p2 = (p2 + 1) & rmask;
+          }
+        } else {
+#pragma unroll 4
+          for (int jj = 0; jj < tn; ++jj) {
+            const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[jj]));
+            if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
+            const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+            peak = tb > peak ? tb : peak;
+            p2 = (p2 + 1) & rmask;
+          }
+        }
+        r.viol = viol;
+        r.peak = peak;
+      } else {  // generic slot walk over the whole window
+        const double te = __dadd_rn(now, h_T[hs]);
+        const double tee = __dsub_rn(te, kTimeEpsilon);
+        const int32_t top = hi_off_ > lo ? hi_off_ : lo;
+        uint64_t peak = kZeroBits;
+        uint32_t viol = kNone;
+        for (int32_t o = lo_off; o <= top; ++o) {
+          const int p2 = static_cast<int>((B + o) & rmask);
+          const bool e = se[p2 * 32 + lane] != 0;
+          const bool in_span = o >= fo && o <= lo;
+          if (!(e || in_span)) continue;
+          const double used = e ? su[p2 * 32 + lane] : 0.0;
+          const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
+          if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
+          const uint64_t tb = ordered_bits(total);
+          peak = tb > peak ? tb : peak;
+        }
+        r.viol = viol;
+        r.peak = peak;
+      }
+    }
+    r.flag = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+    return r;
+  };
 
   // ---- head ring (warp 1 loads 32-head blocks ahead of use) ----
   int64_t nx_start = pos0, nx_n = 0;
@@ -2092,49 +2172,22 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     if (pos0 < q_end) land_block();
   }
 
-  // ---- resolver state (warp 0) ----
-  double live = act ? in.live_kv[i] : 0.0;
-  int32_t running = act ? in.running[i] : 0;
-  bool susp = act ? in.suspended[i] != 0 : false;
-  int64_t hi = hi0;
-  int32_t hi_off = static_cast<int32_t>(hi0 - B);
-  int32_t nact = act ? in.n_active[i] : 0;
-  uint64_t umax = kZeroBits;  // max stored usage over the whole ledger window
-  for (int32_t o = lo_off; o <= hi_off; ++o) {
-    const int p2 = static_cast<int>((B + o) & rmask);
-    if (se[p2 * 32 + lane]) {
-      const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-      umax = tb > umax ? tb : umax;
-    }
-  }
-  if (warp == 0) {
-    st_live[lane] = live;
-    st_run[lane] = running;
-    st_susp[lane] = susp ? 1 : 0;
-    st_hi[lane] = hi_off;
-    st_umax[lane] = umax;
-  }
-  int64_t pos = pos0;
-  int64_t nrows = nrows0, nadm = nadm0;
-  int retries = 0;
-  bool broke = false;
-  int status = KX_OK;
-  int n_stage = 0;          // staged decision records (resolver)
-  int64_t stage_row0 = nrows0;  // log row of the first staged record
-  // Write the staged records: decision log rows + candidate peaks
-  // (engine.cpp:242-246), admitted flags and active_ entries
-  // (dispatcher.cpp:78).
-  auto flush = [&]() {
-    __syncwarp();
-    for (int r = 0; r < n_stage; ++r) {
-      const StageMeta m = g_meta[r];
-      const int64_t row = stage_row0 + r;
+  // Write staged decision records of buffer `buf` (one warp): decision log
+  // rows + candidate peaks (engine.cpp:242-246, dispatcher.cpp:143-147),
+  // admitted flags and active_ entries (dispatcher.cpp:78).
+  auto flush = [&](int buf) {
+    const int n = s_nstage[buf];
+    const int64_t row0 = s_row0[buf];
+    for (int r = 0; r < n; ++r) {
+      const int g = buf * kStage + r;
+      const StageMeta m = g_meta[g];
+      const int64_t row = row0 + r;
       if (row < dp.log_cap) {
         const int64_t ro = int64_t(pool) * dp.log_cap + row;
         if (lane == 0) {
           kx_decision d;
           d.time = now;
-          d.predicted_peak = g_peak[r];
+          d.predicted_peak = m.peak;
           d.uid = h_uid[m.hs];
           d.queue_index = h_idx[m.hs];
           d.agent = h_agent[m.hs];
@@ -2143,7 +2196,15 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           d.admitted = m.admitted;
           rows[ro] = d;
         }
-        if (act) cand[ro * dp.peak_stride + li] = g_cand[r * 32 + lane];
+        if (act) {
+          const uint8_t f = g_flag[g * 32 + lane];
+          const uint32_t v = g_viol[g * 32 + lane];
+          double c = -1.0;
+          if (f & 1u)
+            c = v == kNone ? from_ordered_bits(g_peak[g * 32 + lane])
+                           : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(v)), 1.0);
+          cand[ro * dp.peak_stride + li] = c;
+        }
       }
       if (m.admitted && lane == m.target) {
         q.admitted[h_idx[m.hs]] = 1;
@@ -2157,9 +2218,36 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         }
       }
     }
-    stage_row0 += n_stage;
-    n_stage = 0;
   };
+
+  // ---- resolver state (warp 0, lane = instance) ----
+  double live = act ? in.live_kv[i] : 0.0;
+  int32_t running = act ? in.running[i] : 0;
+  bool susp = act ? in.suspended[i] != 0 : false;
+  int64_t hi = hi0;
+  int32_t hi_off = static_cast<int32_t>(hi0 - B);
+  int32_t nact = act ? in.n_active[i] : 0;
+  uint64_t umax = kZeroBits;  // max stored usage over the whole ledger window
+  if (warp == 0) {
+    for (int32_t o = lo_off; o <= hi_off; ++o) {
+      const int p2 = static_cast<int>((B + o) & rmask);
+      if (se[p2 * 32 + lane]) {
+        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+        umax = tb > umax ? tb : umax;
+      }
+    }
+    st_live[lane] = live;
+    st_run[lane] = running;
+    st_susp[lane] = susp ? 1 : 0;
+    st_hi[lane] = hi_off;
+    st_umax[lane] = umax;
+  }
+  int64_t pos = pos0;
+  int64_t nrows = nrows0, nadm = nadm0;
+  int retries = 0;
+  bool broke = false;
+  int status = KX_OK;
+  int sbuf = 0;
   __syncthreads();
 
   while (true) {
@@ -2167,73 +2255,15 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     if (s_stop || b0 >= q_end) break;
     const int kb = static_cast<int>(q_end - b0 < kBatchEval ? q_end - b0 : kBatchEval);
     // ---------------- phase A: rows of the batch's heads ----------------
-    if (dbg) tA = clock64();
-    if (warp == 0) flush();  // the previous batch's records, beside the evaluators
     if (warp >= 1 && warp - 1 < kb) {
       const int j = warp - 1;
-      const int64_t hpos = b0 + j;
-      const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
-      const int mode = h_mode[hs];
-      const int64_t first = h_first[hs];
-      const int64_t last = h_last[hs];
-      const double P = static_cast<double>(h_prompt[hs]);
-      const int32_t fo = static_cast<int32_t>(first - B);
-      const int32_t lo = static_cast<int32_t>(last - B);
-      const bool nonempty = last >= first;
-      const double lv = st_live[lane];
-      const bool sp = st_susp[lane] != 0 && !(lv < wcap);
-      const bool eligible = act && !sp && !(st_run[lane] + waiting >= mb);
-      uint32_t viol = kNone;
-      uint64_t peak = kZeroBits;
-      const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
-      if (eligible) {
-        if (mode != kModeGeneric) {
-          peak = st_umax[lane];
-          const double* tab = stab + hs * kDtSlots;
-          const int tn = lo - fo + 1;
-          int p2 = static_cast<int>((B + fo) & rmask);
-          if (mode == kModeTabPk) {
-#pragma unroll 4
-            for (int jj = 0; jj < tn; ++jj) {
-              const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
-              if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
-              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-              peak = tb > peak ? tb : peak;
-              p2 = (p2 + 1) & rmask;
-            }
-          } else {
-#pragma unroll 4
-            for (int jj = 0; jj < tn; ++jj) {
-              const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[jj]));
-              if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
-              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-              peak = tb > peak ? tb : peak;
-              p2 = (p2 + 1) & rmask;
-            }
-          }
-        } else {  // generic slot walk over the whole window
-          const double te = __dadd_rn(now, h_T[hs]);
-          const double tee = __dsub_rn(te, kTimeEpsilon);
-          const int32_t top = st_hi[lane] > lo ? st_hi[lane] : lo;
-          for (int32_t o = lo_off; o <= top; ++o) {
-            const int p2 = static_cast<int>((B + o) & rmask);
-            const bool e = se[p2 * 32 + lane] != 0;
-            const bool in_span = o >= fo && o <= lo;
-            if (!(e || in_span)) continue;
-            const double used = e ? su[p2 * 32 + lane] : 0.0;
-            const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
-            if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
-            const uint64_t tb = ordered_bits(total);
-            peak = tb > peak ? tb : peak;
-          }
-        }
-      }
-      r_viol[j * 32 + lane] = viol;
-      r_peak[j * 32 + lane] = peak;
-      r_flag[j * 32 + lane] = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
+      const int hs = static_cast<int>((b0 + j - pos0) & (kHR - 1));
+      const Row r = evaluate(hs, st_live[lane], st_run[lane], st_susp[lane] != 0, st_umax[lane], st_hi[lane]);
+      r_viol[j * 32 + lane] = r.viol;
+      r_peak[j * 32 + lane] = r.peak;
+      r_flag[j * 32 + lane] = r.flag;
     }
     batch_sync();
-    if (dbg) { const unsigned long long t = clock64(); acc_a += t - tA; tA = t; ++nb; }
     // ---------------- phase B: resolve the batch in order ----------------
     if (warp == 1) {
       // the next batch's heads [b0 + kb, b0 + kb + kBatchEval) must be landed
@@ -2241,12 +2271,17 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       if (loaded_end < q_end && need_end > loaded_end) land_block();
       else if (stage == 0) issue_fields();
       else if (stage == 1) issue_T();
+    } else if (warp == kFlushWarp) {
+      flush(sbuf ^ 1);  // the previous batch's records
     } else if (warp == 0) {
+      if (lane == 0) {
+        s_nstage[sbuf] = 0;
+        s_row0[sbuf] = nrows;
+      }
+      int ns = 0;
       uint32_t dirty = 0;  // lanes changed since the batch's rows were computed
-      int j = 0;
-      while (j < kb) {
-        const int64_t hpos = b0 + j;
-        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
+      for (int j = 0; j < kb && !broke; ++j) {
+        const int hs = static_cast<int>((b0 + j - pos0) & (kHR - 1));
         uint32_t viol = r_viol[j * 32 + lane];
         uint64_t peak = r_peak[j * 32 + lane];
         uint32_t flg = r_flag[j * 32 + lane];
@@ -2255,164 +2290,51 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         const int64_t first = h_first[hs];
         const int64_t last = h_last[hs];
         const int mode = h_mode[hs];
-        const double T = h_T[hs];
         const bool nonempty = last >= first;
-        const int32_t fo = static_cast<int32_t>(first - B);
-        const int32_t lo = static_cast<int32_t>(last - B);
-        const bool fast = mode != kModeGeneric;
-        const int tn = lo - fo + 1;
-        const double* tab = stab + hs * kDtSlots;
         uint32_t fixm = dirty;
-        bool done_head = false;
-        while (!done_head) {
-          // collect_live (engine.cpp:187-202), every loop iteration:
-          // watermark resume (the evaluators applied the same rule to the
-          // state published at the start of the batch).
+        while (true) {
+          // collect_live (engine.cpp:187-202), every iteration: watermark resume
           if (susp && live < wcap) {
             susp = false;
             st_susp[lane] = 0;
           }
-          // ---- re-evaluate the changed instances for this head ----
-          const bool my_elig = act && !susp && !(running + waiting >= mb);
-          unsigned long long tf0 = dbg ? clock64() : 0;
-          if (fixm) {
-            if (fast && tn <= 8) {
-              // four instances per pass, eight slot-lanes each
-              uint32_t rem = fixm;
-              while (rem) {
-                const int g = lane >> 3, s = lane & 7;
-                // the first four set lanes of rem, group g takes the g-th
-                uint32_t r1 = rem & (rem - 1), r2 = r1 & (r1 - 1), r3 = r2 & (r2 - 1);
-                const uint32_t pick = g == 0 ? rem : g == 1 ? r1 : g == 2 ? r2 : r3;
-                const int dl = pick ? __ffs(pick) - 1 : -1;
-                const int dsrc = dl >= 0 ? dl : 0;
-                const bool e_d = __shfl_sync(0xffffffffu, my_elig, dsrc) && dl >= 0;
-                const double cap_d = __shfl_sync(0xffffffffu, cap, dsrc);
-                const double k_d = __shfl_sync(0xffffffffu, kr, dsrc);
-                const uint64_t um_d = shfl_u64(umax, dsrc);
-                uint32_t vv = kNone;
-                uint64_t pp = kZeroBits;
-                if (e_d && s < tn) {
-                  const int p2 = static_cast<int>((B + fo + s) & rmask);
-                  const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, k_d, tab[s]);
-                  const double total = __dadd_rn(su[p2 * 32 + dl], pk);
-                  if (total > cap_d) vv = static_cast<uint32_t>(fo + s);
-                  pp = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-                }
-#pragma unroll
-                for (int m = 1; m < 8; m <<= 1) {
-                  const uint32_t v2 = __shfl_xor_sync(0xffffffffu, vv, m, 8);
-                  const uint64_t p2 = (static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(pp >> 32), m, 8)) << 32) |
-                                      __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(pp), m, 8);
-                  vv = v2 < vv ? v2 : vv;
-                  pp = p2 > pp ? p2 : pp;
-                }
-                pp = um_d > pp ? um_d : pp;
-                // hand each group's result to its instance lane
-                const bool mine = (rem >> lane) & 1u;
-                const int myg = __popc(rem & ((1u << lane) - 1u));
-                const bool take = mine && myg < 4;
-                const int src = take ? myg * 8 : lane;
-                const uint32_t v_t = __shfl_sync(0xffffffffu, vv, src);
-                const uint64_t p_t = shfl_u64(pp, src);
-                const bool e_t = __shfl_sync(0xffffffffu, e_d, src);
-                if (take) {
-                  viol = e_t ? v_t : kNone;
-                  peak = e_t ? p_t : kZeroBits;
-                  flg = (e_t ? 1u : 0u) | (e_t && nonempty && (first < base || last >= base + ring) ? 2u : 0u);
-                }
-                // drop the (up to) four lanes just handled
-                rem = r3 & (r3 - 1);
-              }
-            } else {
-              // one instance at a time, lanes over its window
-              uint32_t rem = fixm;
-              while (rem) {
-                const int t = __ffs(rem) - 1;
-                rem &= rem - 1;
-                const bool e_t = __shfl_sync(0xffffffffu, my_elig, t);
-                uint32_t v_t = kNone;
-                uint64_t p_t = kZeroBits;
-                bool o_t = false;
-                if (e_t) {
-                  const int32_t lo_t = __shfl_sync(0xffffffffu, lo_off, t);
-                  const int32_t hio_t = __shfl_sync(0xffffffffu, hi_off, t);
-                  const double cap_t = __shfl_sync(0xffffffffu, cap, t);
-                  const double k_t = __shfl_sync(0xffffffffu, kr, t);
-                  const int64_t base_t = B + lo_t;
-                  o_t = nonempty && (first < base_t || last >= base_t + ring);
-                  const int32_t w0 = fast ? fo : lo_t;
-                  const int32_t w1 = fast ? lo : (hio_t > lo ? hio_t : lo);
-                  const double te = __dadd_rn(now, T);
-                  const double tee = __dsub_rn(te, kTimeEpsilon);
-                  uint32_t vv = kNone;
-                  uint64_t pp = fast ? shfl_u64(umax, t) : kZeroBits;
-                  for (int32_t o0 = w0; o0 <= w1; o0 += 32) {
-                    const int32_t o = o0 + lane;
-                    if (o <= w1) {
-                      const int p2 = static_cast<int>((B + o) & rmask);
-                      const bool e = se[p2 * 32 + t] != 0;
-                      const bool in_span = o >= fo && o <= lo;
-                      if (e || in_span) {
-                        const double used = e ? su[p2 * 32 + t] : 0.0;
-                        double pk;
-                        if (fast) pk = in_span ? (mode == kModeTabPk ? tab[o - fo] : pk_of(P, k_t, tab[o - fo])) : 0.0;
-                        else pk = pk_of(P, k_t, slot_dt(now, t0e, te, tee, B + o, L));
-                        const double total = __dadd_rn(used, pk);
-                        if (in_span && total > cap_t && static_cast<uint32_t>(o) < vv) vv = static_cast<uint32_t>(o);
-                        const uint64_t tb = ordered_bits(total);
-                        pp = tb > pp ? tb : pp;
-                      }
-                    }
-                  }
-                  v_t = __reduce_min_sync(0xffffffffu, vv);
-                  p_t = warp_max_u64(pp);
-                }
-                if (lane == t) {
-                  viol = v_t;
-                  peak = e_t ? p_t : kZeroBits;
-                  flg = (e_t ? 1u : 0u) | (o_t ? 2u : 0u);
-                }
-              }
-            }
-            fixm = 0;
+          if ((fixm >> lane) & 1u) {  // changed lanes re-evaluate themselves
+            const Row r = evaluate(hs, live, running, susp, umax, hi_off);
+            viol = r.viol;
+            peak = r.peak;
+            flg = r.flag;
           }
-          unsigned long long tf1 = dbg ? clock64() : 0;
-          if (dbg) acc_fix += tf1 - tf0;
           if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
             status = KX_ERR_CAPACITY;
             broke = true;
             break;
           }
-          const bool elig = flg & 1u;
-          const bool fits = elig && viol == kNone;
+          const bool fits = (flg & 1u) && viol == kNone;
           // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
           const uint64_t key = fits ? peak : ~0ull;
           const uint64_t wkey = warp_min_u64(key);
           const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
+          const uint32_t ovm = __ballot_sync(0xffffffffu, fits && __dadd_rn(live, P) > cap);  // engine.cpp:254-258
           const int bl = winners ? __ffs(winners) - 1 : -1;
-          const int bsrc = bl >= 0 ? bl : 0;
-          const double blive = __shfl_sync(0xffffffffu, live, bsrc);
-          const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
-          const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
-          const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
-          {  // stage the decision record (engine.cpp:242-246); flushed later
-            if (n_stage == kStage) flush();
-            const int r = n_stage;
-            if (lane == 0) {
-              g_meta[r] = StageMeta{hs, bl, (bl >= 0 && !overload) ? 1 : 0, -1};
-              g_peak[r] = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
-            }
-            double v = -1.0;
-            if (elig) {
-              v = fits ? from_ordered_bits(peak)
-                       : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
-            }
-            g_cand[r * 32 + lane] = v;
-            ++n_stage;
+          const bool overload = bl >= 0 && ((ovm >> bl) & 1u);
+          // stage the decision record (flushed by another warp later)
+          if (ns == kStage) {  // buffer full: write it out here
+            if (lane == 0) s_nstage[sbuf] = ns;
+            __syncwarp();
+            flush(sbuf);
+            if (lane == 0) s_row0[sbuf] = nrows;
+            ns = 0;
           }
-          unsigned long long ts1 = dbg ? clock64() : 0;
-          if (dbg) acc_sel += ts1 - tf1;
+          {
+            const int g = sbuf * kStage + ns;
+            if (lane == 0)
+              g_meta[g] = StageMeta{hs, bl, (bl >= 0 && !overload) ? 1 : 0, -1,
+                                    bl >= 0 ? from_ordered_bits(wkey) : 0.0};
+            g_viol[g * 32 + lane] = viol;
+            g_peak[g * 32 + lane] = peak;
+            g_flag[g * 32 + lane] = static_cast<uint8_t>(flg);
+          }
+          ++ns;
           ++nrows;
           if (bl < 0) {  // head keeps its place (engine.cpp:247)
             broke = true;
@@ -2433,48 +2355,46 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             continue;
           }
           retries = 0;
-          // Dispatcher::commit: book the target's span slots (lanes = slots)
-          // and raise the target's maximum stored usage.
-          const double kt = __shfl_sync(0xffffffffu, kr, bl);
-          uint64_t nb = kZeroBits;
-          if (fast) {
-            for (int s = lane; s < tn; s += 32) {
-              const int p2 = static_cast<int>((B + fo + s) & rmask);
-              const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, kt, tab[s]);
-              const double nu = __dadd_rn(su[p2 * 32 + bl], pk);
-              su[p2 * 32 + bl] = nu;
-              se[p2 * 32 + bl] = 1;
-              const uint64_t tb = ordered_bits(nu);
-              nb = tb > nb ? tb : nb;
-            }
-          } else {
-            const double te = __dadd_rn(now, T);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            for (int64_t s = first + lane; s <= last; s += 32) {
-              const int p2 = static_cast<int>(s & rmask);
-              const double nu = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
-              su[p2 * 32 + bl] = nu;
-              se[p2 * 32 + bl] = 1;
-              const uint64_t tb = ordered_bits(nu);
-              nb = tb > nb ? tb : nb;
-            }
-          }
-          nb = warp_max_u64(nb);
-          __syncwarp();
+          // Dispatcher::commit, in the target's own lane: book the span
+          // slots, raise its maximum stored usage, admit (engine.cpp:298-319).
+          const double T = h_T[hs];
           if (lane == bl) {
+            if (mode != kModeGeneric) {
+              const double* tab = stab + hs * kDtSlots;
+              int p2 = static_cast<int>(first & rmask);
+              for (int s = 0; s <= static_cast<int>(last - first); ++s) {
+                const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, kr, tab[s]);
+                const double nu = __dadd_rn(su[p2 * 32 + lane], pk);
+                su[p2 * 32 + lane] = nu;
+                se[p2 * 32 + lane] = 1;
+                const uint64_t tb = ordered_bits(nu);
+                umax = tb > umax ? tb : umax;
+                p2 = (p2 + 1) & rmask;
+              }
+            } else {
+              const double te = __dadd_rn(now, T);
+              const double tee = __dsub_rn(te, kTimeEpsilon);
+              for (int64_t s = first; s <= last; ++s) {
+                const int p2 = static_cast<int>(s & rmask);
+                const double nu = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, slot_dt(now, t0e, te, tee, s, L)));
+                su[p2 * 32 + lane] = nu;
+                se[p2 * 32 + lane] = 1;
+                const uint64_t tb = ordered_bits(nu);
+                umax = tb > umax ? tb : umax;
+              }
+            }
             if (nonempty && last > hi) {
               hi = last;
-              hi_off = lo;
+              hi_off = static_cast<int32_t>(last - B);
             }
-            live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
+            live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));
             running += 1;
-            umax = nb > umax ? nb : umax;
             st_live[lane] = live;
             st_run[lane] = running;
             st_hi[lane] = hi_off;
             st_umax[lane] = umax;
             if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78), written at flush
-              g_meta[n_stage - 1].act_slot = nact;
+              g_meta[sbuf * kStage + ns - 1].act_slot = nact;
               ++nact;
             } else {
               status = KX_ERR_CAPACITY;
@@ -2485,27 +2405,26 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             broke = true;
             break;
           }
-          if (dbg) acc_com += clock64() - ts1;
           dirty |= 1u << bl;
           ++nadm;
           ++pos;
-          done_head = true;
+          break;
         }
-        if (broke) break;
-        ++j;
       }
       if (lane == 0) {
+        s_nstage[sbuf] = ns;
         s_next = pos;
         s_stop = broke ? 1 : 0;
       }
     }
-    if (dbg) acc_b += clock64() - tA;
     batch_sync();
+    sbuf ^= 1;
   }
-
   if (dbg) g_disp_dbg[2] = gtimer();
+
   if (warp == 0) {
-    flush();
+    __syncwarp();
+    flush(sbuf ^ 1);  // the last batch's records
     // Phase 1 ran out of prefix heads without finishing the round: hand the
     // state to the continuation (no gc yet: the round is not over).
     const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
@@ -2544,8 +2463,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
   }
-  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; g_disp_dbg[6] = acc_a; g_disp_dbg[7] = acc_b;
-             g_disp_dbg[8] = acc_fix; g_disp_dbg[9] = acc_sel; g_disp_dbg[10] = acc_com; g_disp_dbg[11] = nb; }
+  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; }
   __syncthreads();
   {
     // write back the window (booked slots only grow hi; gc only clears inside it)
@@ -2559,8 +2477,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       in.usage[int64_t(ib + lj) * ring + p2] = su[p2 * 32 + l];
       in.exists[int64_t(ib + lj) * ring + p2] = se[p2 * 32 + l];
     }
-  if (dbg) g_disp_dbg[4] = gtimer();
   }
+  if (dbg) g_disp_dbg[4] = gtimer();
 }
 
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
