@@ -8,7 +8,7 @@
 NVCC     ?= nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 \
-            -Xptxas -warn-spills
+            -Xptxas -warn-spills $(NVFLAGS_EXTRA)
 PKG      := paper_2508_06948_b200
 SRC      := $(PKG)/csrc
 OUT      := $(PKG)/_lib

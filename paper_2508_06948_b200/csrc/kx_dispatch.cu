@@ -1896,6 +1896,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   if (skip) return;  // uniform over the CTA
   const bool dbg = KX_DISPATCH_TIMERS && blockIdx.x == 0 && threadIdx.x == 0;
   if (dbg) g_disp_dbg[0] = gtimer();
+  unsigned long long acc_a = 0, acc_b = 0, tA = 0, nbat = 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ib = pool_begin[pool];
@@ -2255,6 +2256,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     if (s_stop || b0 >= q_end) break;
     const int kb = static_cast<int>(q_end - b0 < kBatchEval ? q_end - b0 : kBatchEval);
     // ---------------- phase A: rows of the batch's heads ----------------
+    if (dbg) tA = clock64();
     if (warp >= 1 && warp - 1 < kb) {
       const int j = warp - 1;
       const int hs = static_cast<int>((b0 + j - pos0) & (kHR - 1));
@@ -2264,6 +2266,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       r_flag[j * 32 + lane] = r.flag;
     }
     batch_sync();
+    if (dbg) { const uint32_t dep = *(volatile uint32_t*)&r_flag[0]; const unsigned long long t = clock64() + (dep & 0u); acc_a += t - tA; tA = t; ++nbat; }
     // ---------------- phase B: resolve the batch in order ----------------
     if (warp == 1) {
       // the next batch's heads [b0 + kb, b0 + kb + kBatchEval) must be landed
@@ -2291,6 +2294,10 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         const int64_t last = h_last[hs];
         const int mode = h_mode[hs];
         const bool nonempty = last >= first;
+        const int32_t fo = static_cast<int32_t>(first - B);
+        const int tn = static_cast<int>(last - first + 1);
+        const int pbase = static_cast<int>((B + fo) & rmask);
+        const double* tab = stab + hs * kDtSlots;
         uint32_t fixm = dirty;
         while (true) {
           // collect_live (engine.cpp:187-202), every iteration: watermark resume
@@ -2299,10 +2306,29 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             st_susp[lane] = 0;
           }
           if ((fixm >> lane) & 1u) {  // changed lanes re-evaluate themselves
-            const Row r = evaluate(hs, live, running, susp, umax, hi_off);
-            viol = r.viol;
-            peak = r.peak;
-            flg = r.flag;
+            if (mode == kModeTabPk) {  // the common shape, inline
+              const bool el = act && !susp && !(running + waiting >= mb);
+              viol = kNone;
+              peak = kZeroBits;
+              flg = el ? 1u : 0u;
+              if (el) {
+                if (first < base || last >= base + ring) flg |= 2u;
+                peak = umax;
+                int p2 = pbase;
+                for (int jj = 0; jj < tn; ++jj) {
+                  const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
+                  if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
+                  const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
+                  peak = tb > peak ? tb : peak;
+                  p2 = (p2 + 1) & rmask;
+                }
+              }
+            } else {
+              const Row r = evaluate(hs, live, running, susp, umax, hi_off);
+              viol = r.viol;
+              peak = r.peak;
+              flg = r.flag;
+            }
           }
           if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
             status = KX_ERR_CAPACITY;
@@ -2359,15 +2385,14 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           // slots, raise its maximum stored usage, admit (engine.cpp:298-319).
           const double T = h_T[hs];
           if (lane == bl) {
-            if (mode != kModeGeneric) {
-              const double* tab = stab + hs * kDtSlots;
+            if (mode != kModeGeneric) {  // usage + pk >= 0: raw bits order
               int p2 = static_cast<int>(first & rmask);
-              for (int s = 0; s <= static_cast<int>(last - first); ++s) {
+              for (int s = 0; s < tn; ++s) {
                 const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, kr, tab[s]);
                 const double nu = __dadd_rn(su[p2 * 32 + lane], pk);
                 su[p2 * 32 + lane] = nu;
                 se[p2 * 32 + lane] = 1;
-                const uint64_t tb = ordered_bits(nu);
+                const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(nu)) | kZeroBits;
                 umax = tb > umax ? tb : umax;
                 p2 = (p2 + 1) & rmask;
               }
@@ -2417,6 +2442,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         s_stop = broke ? 1 : 0;
       }
     }
+    if (dbg) acc_b += clock64() - tA;
     batch_sync();
     sbuf ^= 1;
   }
@@ -2463,7 +2489,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
   }
-  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; }
+  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; g_disp_dbg[6] = acc_a; g_disp_dbg[7] = acc_b; g_disp_dbg[11] = nbat; }
   __syncthreads();
   {
     // write back the window (booked slots only grow hi; gc only clears inside it)
