@@ -641,12 +641,17 @@ __global__ void k_topk_hist(const uint32_t* __restrict__ keys, int64_t n, OrderP
   __shared__ uint32_t sh[kTopKMaxPools * kRadix];
   __shared__ uint32_t s_mask[kTopKMaxPools], s_prefix[kTopKMaxPools], s_live[kTopKMaxPools];
   for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x) sh[i] = 0;
+  __shared__ int s_any;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
   for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
     s_mask[p] = st[p].mask;
     s_prefix[p] = st[p].prefix;
     s_live[p] = !st[p].done;
+    if (s_live[p]) s_any = 1;
   }
   __syncthreads();
+  if (!s_any) return;  // every pool's prefix bound is already known
   auto take = [&](uint32_t k) {
     const int p = pool_of_key(k, op);
     if (s_live[p] && (k & s_mask[p]) == s_prefix[p]) atomicAdd(&sh[p * kRadix + ((k >> shift) & 0xFF)], 1u);

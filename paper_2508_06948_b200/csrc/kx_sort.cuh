@@ -25,9 +25,15 @@ namespace kx {
 
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 12;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 3072 elements
+#ifndef KX_SORT_THREADS
+#define KX_SORT_THREADS 256
+#endif
+#ifndef KX_SORT_ITEMS
+#define KX_SORT_ITEMS 12
+#endif
+constexpr int kSortThreads = KX_SORT_THREADS;
+constexpr int kSortItems = KX_SORT_ITEMS;
+constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
@@ -102,7 +108,11 @@ __global__ void __launch_bounds__(kSortThreads)
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                 int64_t n, int shift, const uint32_t* __restrict__ global_excl,
-                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter) {
+                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter
+#ifdef KX_PROBE_NO_LOOKBACK_SWITCH
+                , int probe_no_lookback = 0
+#endif
+                ) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<K>& sm = *reinterpret_cast<SortSmem<K>*>(smem_raw);
   K* s_keys = reinterpret_cast<K*>(smem_raw + sizeof(SortSmem<K>));
@@ -184,6 +194,10 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     // round trip: the walk over tiles that have only published their
     // aggregate costs one L2 latency per batch instead of per tile.
     uint32_t excl = 0;
+#ifdef KX_PROBE_NO_LOOKBACK_SWITCH
+    if (probe_no_lookback) lookback[int64_t(tile) * kRadix + tid] = kFlagIncl | total;
+    else
+#endif
     if (tile > 0) {
       volatile uint32_t* lb = lookback;
       int64_t p = int64_t(tile) - 1;
