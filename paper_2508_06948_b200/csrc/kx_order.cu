@@ -44,14 +44,6 @@ __global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes) {
 
 namespace {
 
-__device__ __forceinline__ double primary_time(const QueueDev& q, int policy, int64_t i) {
-  switch (policy) {
-    case KX_SCHED_KAIROS: return q.app_start[i];
-    case KX_SCHED_ORACLE: return q.rem[i];
-    default: return q.queue_enter[i];  // FCFS, Topo
-  }
-}
-
 __device__ __forceinline__ uint32_t class_of(const AgentsDev& a, int policy, int32_t agent) {
   if (policy == KX_SCHED_KAIROS) return a.pk_rank[agent];
   if (policy == KX_SCHED_TOPO) return a.depth_rank[agent];
@@ -100,16 +92,6 @@ __device__ __forceinline__ bool rec_less(const TRec& a, const TRec& b) {
   return a.idx < b.idx;  // identical tuples: first-enqueued wins (best_index uses strict <)
 }
 
-__device__ __forceinline__ TRec shfl_rec(const TRec& r, int src) {
-  TRec o;
-  o.w0 = __shfl_sync(0xffffffffu, r.w0, src);
-  o.w1 = __shfl_sync(0xffffffffu, r.w1, src);
-  o.w2 = __shfl_sync(0xffffffffu, r.w2, src);
-  o.msg = __shfl_sync(0xffffffffu, r.msg, src);
-  o.uid = __shfl_sync(0xffffffffu, r.uid, src);
-  o.idx = __shfl_sync(0xffffffffu, r.idx, src);
-  return o;
-}
 
 }  // namespace
 
@@ -134,8 +116,15 @@ __global__ void k_score(QueueDev q, AgentsDev a, int policy, int64_t n, double* 
 
 // ---- per-pool range of the primary time ------------------------------
 // Also validates agent indices and rejects NaN (error_flags bit 0 / bit 1).
-__global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
-                             PoolRange* __restrict__ ranges, int* __restrict__ error_flags) {
+// Streams the queue with 16-byte loads: four agents (int4) and four times
+// (two double2) per thread per step, two steps in flight.
+__device__ __forceinline__ const double* primary_ptr(const QueueDev& q, int policy) {
+  return policy == KX_SCHED_KAIROS ? q.app_start : policy == KX_SCHED_ORACLE ? q.rem : q.queue_enter;
+}
+
+__global__ void __launch_bounds__(256)
+k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n, PoolRange* __restrict__ ranges,
+             int* __restrict__ error_flags) {
   extern __shared__ uint64_t s_rng[];  // [2 * n_pools]: lo, hi
   for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
     s_rng[2 * p] = ~0ull;
@@ -154,45 +143,55 @@ __global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
       atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur + 1]), (unsigned long long)hi);
     }
   };
-  // Four independent elements per thread per iteration keep enough loads in
-  // flight to stream at HBM rate.
-  constexpr int U = 4;
+  auto take = [&](int32_t ag, double t) {
+    if (ag < 0 || ag >= op.n_agents) {
+      err |= 1;
+      return;
+    }
+    if (t != t) {
+      err |= 2;
+      return;
+    }
+    const int32_t p = a.pool[ag];
+    const uint64_t bb = ordered_bits(t);
+    if (p != cur) {
+      flush();
+      cur = p;
+      lo = ~0ull;
+      hi = 0ull;
+    }
+    lo = bb < lo ? bb : lo;
+    hi = bb > hi ? bb : hi;
+  };
+  const double* tp = primary_ptr(q, op.policy);
+  const int4* av = reinterpret_cast<const int4*>(q.agent);
+  const double2* tv = reinterpret_cast<const double2*>(tp);
+  const int64_t nv = n >> 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
-    int32_t ags[U];
-    double ts[U];
+  constexpr int U = 2;
+  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += U * stride) {
+    int4 ag[U];
+    double2 t0[U], t1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u * stride;
-      ags[u] = i < n ? q.agent[i] : -1;
-      ts[u] = i < n ? primary_time(q, op.policy, i) : 0.0;
+      const int64_t v = v0 + u * stride;
+      if (v < nv) {
+        ag[u] = av[v];
+        t0[u] = tv[2 * v];
+        t1[u] = tv[2 * v + 1];
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u * stride;
-      if (i >= n) continue;
-      const int32_t ag = ags[u];
-      if (ag < 0 || ag >= op.n_agents) {
-        err |= 1;
-        continue;
-      }
-      const double t = ts[u];
-      if (t != t) {
-        err |= 2;
-        continue;
-      }
-      const int32_t p = a.pool[ag];
-      const uint64_t bb = ordered_bits(t);
-      if (p != cur) {
-        flush();
-        cur = p;
-        lo = ~0ull;
-        hi = 0ull;
-      }
-      lo = bb < lo ? bb : lo;
-      hi = bb > hi ? bb : hi;
+      if (v0 + u * stride >= nv) continue;
+      take(ag[u].x, t0[u].x);
+      take(ag[u].y, t0[u].y);
+      take(ag[u].z, t1[u].x);
+      take(ag[u].w, t1[u].y);
     }
   }
+  if (blockIdx.x == 0)
+    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(q.agent[i], tp[i]);
   flush();
   if (err) atomicOr(error_flags, err);
   __syncthreads();
@@ -204,6 +203,51 @@ __global__ void k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
   }
 }
 
+// ---- sampled quantisation window ---------------------------------------
+// The compact key only needs the quantisation to be monotone: any window
+// [lo, hi] works (values outside clamp to the ends and tie, and ties are
+// resolved by the exact tuple), the window only sets the time resolution.
+// So it comes from a sample: kSampleLen contiguous requests out of every
+// `stride` (all of them for small queues), per-pool min / max of the primary
+// time. Validation of every request happens in k_keygen.
+constexpr int kSampleLen = 64;
+
+__global__ void __launch_bounds__(kSampleLen)
+k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
+              PoolRange* __restrict__ ranges) {
+  const int64_t i = int64_t(blockIdx.x) * stride + threadIdx.x;
+  int32_t p = -1;
+  uint64_t lo = ~0ull, hi = 0ull;
+  if (i < n) {
+    const int32_t ag = q.agent[i];
+    const double t = primary_ptr(q, op.policy)[i];
+    if (ag >= 0 && ag < op.n_agents && t == t) {
+      p = a.pool[ag];
+      lo = hi = ordered_bits(t);
+    }
+  }
+  // one atomic pair per warp when the warp's samples share a pool (pools
+  // are mostly contiguous), one per sample otherwise
+  const uint32_t valid = __ballot_sync(0xffffffffu, p >= 0);
+  if (!valid) return;
+  const int32_t p0 = __shfl_sync(0xffffffffu, p, __ffs(valid) - 1);
+  if (__all_sync(0xffffffffu, p < 0 || p == p0)) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+      const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p0].lo_bits), (unsigned long long)lo);
+      atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p0].hi_bits), (unsigned long long)hi);
+    }
+  } else if (p >= 0) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p].lo_bits), (unsigned long long)lo);
+    atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p].hi_bits), (unsigned long long)hi);
+  }
+}
+
 __global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pools) return;
@@ -212,8 +256,13 @@ __global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
     r.lo = 0.0;
     r.scale = 0.0;
   } else {
-    const double lo = from_ordered_bits(r.lo_bits);
-    const double hi = from_ordered_bits(r.hi_bits);
+    double lo = from_ordered_bits(r.lo_bits);
+    double hi = from_ordered_bits(r.hi_bits);
+    // The sampled extremes sit inside the true ones: widen by 1/64 of the
+    // span each side so unsampled tails rarely clamp (clamped values only tie).
+    const double m = __dmul_rn(__dsub_rn(hi, lo), 0.015625);
+    lo = __dsub_rn(lo, m);
+    hi = __dadd_rn(hi, m);
     const double span = __dsub_rn(hi, lo);
     const double qmax = static_cast<double>((uint64_t(1) << q_bits) - 1);
     r.lo = lo;
@@ -225,9 +274,11 @@ __global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
 }
 
 // ---- compact key + upfront digit histograms + pool counts -------------
-__global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
-                         const PoolRange* __restrict__ ranges, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts) {
+// 16-byte loads (four requests per thread per step), keys stored as uint4.
+__global__ void __launch_bounds__(256)
+k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
+         uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
+         int* __restrict__ error_flags) {
   __shared__ uint32_t sh[4 * kRadix];
   extern __shared__ uint32_t s_pool[];
   const int passes = op.key_bits / kRadixBits;
@@ -237,50 +288,92 @@ __global__ void k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n,
   const uint32_t qmax = (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
   int32_t cur_pool = -1;
   uint32_t cur_cnt = 0;
-  constexpr int U = 4;
+  int err = 0;
+  auto make_key = [&](int32_t ag, double t) {
+    if (ag < 0 || ag >= op.n_agents) {  // reported at order fetch; key 0 in pool 0
+      err |= 1;
+      ag = 0;
+    }
+    if (t != t) {
+      err |= 2;
+      t = 0.0;
+    }
+    const int32_t p = a.pool[ag];
+    const uint32_t cls = class_of(a, op.policy, ag);
+    const PoolRange r = ranges[p];
+    // Monotone: (t - lo) and the product are correctly rounded, floor and
+    // the clamp are monotone, so t1 <= t2 implies q1 <= q2.
+    const double x = __dmul_rn(__dsub_rn(t, r.lo), r.scale);
+    uint32_t qv;
+    if (!(x > 0.0)) qv = 0;
+    else if (x >= static_cast<double>(qmax)) qv = qmax;
+    else qv = static_cast<uint32_t>(x);
+    uint32_t key = qv;
+    if (op.class_bits) key |= cls << op.q_bits;
+    if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+    if (p != cur_pool) {
+      if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
+      cur_pool = p;
+      cur_cnt = 0;
+    }
+    ++cur_cnt;
+    return key;
+  };
+  const double* tp = primary_ptr(q, op.policy);
+  const int4* av = reinterpret_cast<const int4*>(q.agent);
+  const double2* tv = reinterpret_cast<const double2*>(tp);
+  uint4* kv = reinterpret_cast<uint4*>(keys);
+  const int64_t nv = n >> 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t b0 = int64_t(blockIdx.x) * blockDim.x; b0 < n; b0 += U * stride) {
-    int32_t ags[U];
-    double ts[U];
+  constexpr int U = 2;
+  // the loop trip count is uniform over the block (hist_add is warp-collective)
+  for (int64_t b0 = int64_t(blockIdx.x) * blockDim.x; b0 < nv; b0 += U * stride) {
+    int4 ag[U];
+    double2 t0[U], t1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t i = b0 + u * stride + threadIdx.x;
-      ags[u] = i < n ? q.agent[i] : 0;
-      ts[u] = i < n ? primary_time(q, op.policy, i) : 0.0;
+      const int64_t v = b0 + u * stride + threadIdx.x;
+      if (v < nv) {
+        ag[u] = av[v];
+        t0[u] = tv[2 * v];
+        t1[u] = tv[2 * v + 1];
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t i = b0 + u * stride + threadIdx.x;
+      const int64_t v = b0 + u * stride + threadIdx.x;
+      const bool valid = v < nv;
+      uint4 k4 = make_uint4(0, 0, 0, 0);
+      if (valid) {
+        k4.x = make_key(ag[u].x, t0[u].x);
+        k4.y = make_key(ag[u].y, t0[u].y);
+        k4.z = make_key(ag[u].z, t1[u].x);
+        k4.w = make_key(ag[u].w, t1[u].y);
+        kv[v] = k4;
+      }
+      for (int pz = 0; pz < passes; ++pz) {
+        const int sh_ = pz * kRadixBits;
+        hist_add(&sh[pz * kRadix], digit_of(k4.x, sh_), valid);
+        hist_add(&sh[pz * kRadix], digit_of(k4.y, sh_), valid);
+        hist_add(&sh[pz * kRadix], digit_of(k4.z, sh_), valid);
+        hist_add(&sh[pz * kRadix], digit_of(k4.w, sh_), valid);
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (int64_t base = nv << 2; base < n; base += blockDim.x) {
+      const int64_t i = base + threadIdx.x;
       const bool valid = i < n;
       uint32_t key = 0;
       if (valid) {
-        const int32_t ag = ags[u];
-        const int32_t p = a.pool[ag];
-        const uint32_t cls = class_of(a, op.policy, ag);
-        const PoolRange r = ranges[p];
-        // Monotone: (t - lo) and the product are correctly rounded, floor
-        // and the clamp are monotone, so t1 <= t2 implies q1 <= q2.
-        const double x = __dmul_rn(__dsub_rn(ts[u], r.lo), r.scale);
-        uint32_t qv;
-        if (!(x > 0.0)) qv = 0;
-        else if (x >= static_cast<double>(qmax)) qv = qmax;
-        else qv = static_cast<uint32_t>(x);
-        key = qv;
-        if (op.class_bits) key |= cls << op.q_bits;
-        if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+        key = make_key(q.agent[i], tp[i]);
         keys[i] = key;
-        if (p != cur_pool) {
-          if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
-          cur_pool = p;
-          cur_cnt = 0;
-        }
-        ++cur_cnt;
       }
-      // every lane reaches hist_add (warp-collective)
       for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
     }
   }
   if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
+  if (err) atomicOr(error_flags, err);
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
@@ -934,19 +1027,23 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     res.keys = ws.keys[0];
     return res;
   }
-  const int grid = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, int64_t(sms) * 8));
-  // reads agent (4 B) + primary time (8 B) per request
-  P.begin("pool_range", N * 12.0, st);
-  k_pool_range<<<grid, 256, sizeof(uint64_t) * 2 * op.n_pools, st>>>(q, a, op, n, ws.ranges,
-                                                                       ws.error_flags);
-  KX_CHECK_LAUNCH();
-  P.end(st);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
+  {
+    // sampled window: ~256K requests (every request below that)
+    const int64_t target = int64_t(1) << 18;
+    const int64_t stride = n <= target ? kSampleLen : kSampleLen * ((n + target - 1) / target);
+    const int64_t blocks = (n + stride - 1) / stride;
+    P.begin("pool_sample", double(blocks) * kSampleLen * 12.0, st);
+    k_pool_sample<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges);
+    KX_CHECK_LAUNCH();
+    P.end(st);
+  }
   k_range_finalize<<<(op.n_pools + 127) / 128, 128, 0, st>>>(ws.ranges, op.n_pools, op.q_bits);
   KX_CHECK_LAUNCH();
   // reads agent + primary time (12 B), writes the compact key (4 B)
   P.begin("keygen_hist", N * 16.0, st);
   k_keygen<<<grid, 256, sizeof(uint32_t) * op.n_pools, st>>>(q, a, op, n, ws.ranges, ws.keys[0],
-                                                              ws.hist, ws.pool_counts);
+                                                              ws.hist, ws.pool_counts, ws.error_flags);
   KX_CHECK_LAUNCH();
   P.end(st);
   k_scan_hist<<<1, 32 * passes, 0, st>>>(ws.hist, passes);
