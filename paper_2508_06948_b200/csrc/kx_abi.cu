@@ -488,7 +488,10 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     Layout L;
     const size_t o_st = L.take<TopKState>(P), o_h = L.take<uint32_t>(P * 256),
                  o_c = L.take<uint32_t>(P * kTopKMax), o_hd = L.take<uint32_t>(P * kTopKMax),
-                 o_r = L.take<DispResume>(P);
+                 o_r = L.take<DispResume>(P), o_sb = L.take<uint32_t>(P), o_so = L.take<uint32_t>(P),
+                 o_sc = L.take<uint32_t>(P);
+    const int64_t ns = spec_sample_capacity(std::max<int64_t>(s->cap, 1));
+    const size_t o_sk = L.take<uint32_t>(ns), o_sp = L.take<int32_t>(ns);
     alloc_blob(s->topk_blob, L.off);
     auto& b = s->topk_blob;
     s->topk.state = at<TopKState>(b, o_st);
@@ -496,6 +499,11 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->topk.cand = at<uint32_t>(b, o_c);
     s->topk.heads = at<uint32_t>(b, o_hd);
     s->resume = at<DispResume>(b, o_r);
+    s->topk.spec_bound = at<uint32_t>(b, o_sb);
+    s->topk.spec_on = at<uint32_t>(b, o_so);
+    s->topk.spec_count = at<uint32_t>(b, o_sc);
+    s->topk.sample_key = at<uint32_t>(b, o_sk);
+    s->topk.sample_pool = at<int32_t>(b, o_sp);
     if (const char* e = getenv("KX_TOPK_NEED"))  // test knob: force short prefixes
       s->topk.max_need = static_cast<uint32_t>(std::clamp(atoi(e), 1, kTopKMax));
     // The prefix select + dispatch chain is the tick's critical path: its
@@ -697,6 +705,12 @@ void tick_impl(kx_sched* s, double now) {
   const int passes = op.key_bits / 8;
   const uint32_t* final_perm = s->ws.vals[passes & 1];
   OrderHooks hooks;
+  // the dispatch prefix is collected during key generation (speculative
+  // bound from the sample; launch_topk falls back to the radix select)
+  hooks.before_keygen = [&] {
+    launch_spec_bound(s->q, s->a, s->in, s->pool_begin, op, s->n, s->ws, s->topk, s->stream);
+  };
+  hooks.spec = KeygenSpec{s->topk.spec_bound, s->topk.spec_on, s->topk.spec_count, s->topk.cand};
   hooks.after_keys = [&] {
     KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
     KX_CUDA(cudaEventRecord(s->ev_keys, s->stream));

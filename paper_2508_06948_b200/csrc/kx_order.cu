@@ -212,6 +212,12 @@ k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n, PoolRange* __re
 // time. Validation of every request happens in k_keygen.
 constexpr int kSampleLen = 64;
 
+// Sample stride for n requests: ~256K samples (every request below that).
+__host__ __device__ inline int64_t sample_stride(int64_t n) {
+  const int64_t target = int64_t(1) << 18;
+  return n <= target ? kSampleLen : kSampleLen * ((n + target - 1) / target);
+}
+
 __global__ void __launch_bounds__(kSampleLen)
 k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
               PoolRange* __restrict__ ranges) {
@@ -273,23 +279,195 @@ __global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
   ranges[p] = r;
 }
 
+// Compact key of one request: [pool | class rank | q(primary time)].
+// Monotone: (t - lo) and the product are correctly rounded, floor and the
+// clamp are monotone, so t1 <= t2 implies q1 <= q2.
+__device__ __forceinline__ uint32_t compact_key(const AgentsDev& a, const OrderParams& op,
+                                                const PoolRange& r, int32_t p, int32_t ag, double t,
+                                                uint32_t qmax) {
+  const double x = __dmul_rn(__dsub_rn(t, r.lo), r.scale);
+  uint32_t qv;
+  if (!(x > 0.0)) qv = 0;
+  else if (x >= static_cast<double>(qmax)) qv = qmax;
+  else qv = static_cast<uint32_t>(x);
+  uint32_t key = qv;
+  if (op.class_bits) key |= class_of(a, op.policy, ag) << op.q_bits;
+  if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+  return key;
+}
+
+__device__ __forceinline__ uint32_t q_max(const OrderParams& op) {
+  return (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
+}
+
+// ---- speculative dispatch-prefix bound (CTA per pool) --------------------
+// The dispatch round of pool p reads at most `need` heads (free batch slots
+// + 1). From the sampled requests of p (a uniform subsample of <=
+// kSpecMax), take the k-th smallest compact key with k ~ 1.5 * need * the
+// sampling fraction: about 1.5 * need of the pool's keys are <= it. Key
+// generation then collects exactly the keys <= bound - a prefix of the
+// pool's order by construction (equal keys are all in or all out) - and the
+// prefix select needs no pass of its own. If the collection overflows the
+// candidate buffer the pool falls back to the radix select; if it is short
+// of `need`, the dispatch continues over the full order (phase 2).
+constexpr int kSpecMax = 32768;
+constexpr int kSpecThreads = 1024;
+
+// Compact keys of the sampled requests (same positions as k_pool_sample),
+// pool id per sample (-1 = invalid), for k_spec_bound.
+__global__ void __launch_bounds__(kSampleLen)
+k_sample_keys(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
+              const PoolRange* __restrict__ ranges, uint32_t* __restrict__ skey,
+              int32_t* __restrict__ spool) {
+  const int64_t e = int64_t(blockIdx.x) * kSampleLen + threadIdx.x;
+  const int64_t i = int64_t(blockIdx.x) * stride + threadIdx.x;
+  int32_t p = -1;
+  uint32_t key = 0xffffffffu;
+  if (i < n) {
+    const int32_t ag = q.agent[i];
+    const double t = primary_ptr(q, op.policy)[i];
+    if (ag >= 0 && ag < op.n_agents && t == t) {
+      p = a.pool[ag];
+      key = compact_key(a, op, ranges[p], p, ag, t, q_max(op));
+    }
+  }
+  skey[e] = key;
+  spool[e] = p;
+}
+
+__global__ void __launch_bounds__(kSpecThreads)
+k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op, int64_t n,
+             int64_t stride, int64_t n_samples, const uint32_t* __restrict__ skey,
+             const int32_t* __restrict__ spool, uint32_t max_need, uint32_t* __restrict__ spec_bound,
+             uint32_t* __restrict__ spec_on, uint32_t* __restrict__ spec_count) {
+  extern __shared__ uint32_t s_keys[];  // [kSpecMax]
+  __shared__ uint32_t s_hist[kRadix];
+  __shared__ uint32_t s_cnt, s_n;
+  __shared__ uint32_t s_prefix, s_mask, s_rank, s_ok;
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_cnt = 0;
+    s_n = 0;
+    spec_count[p] = 0;
+  }
+  __syncthreads();
+  // pass 1: samples of pool p (int4 loads, four in flight per thread)
+  uint32_t c = 0;
+  const int64_t nv = n_samples >> 2;  // n_samples is a multiple of kSampleLen
+  const int4* pv = reinterpret_cast<const int4*>(spool);
+  for (int64_t v0 = tid; v0 < nv; v0 += 4 * kSpecThreads) {
+    int4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t v = v0 + u * kSpecThreads;
+      x[u] = v < nv ? pv[v] : make_int4(-1, -1, -1, -1);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c += (x[u].x == p) + (x[u].y == p) + (x[u].z == p) + (x[u].w == p);
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((tid & 31) == 0 && c) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  const uint32_t S = s_cnt;
+  const int64_t m = S > kSpecMax ? (S + kSpecMax - 1) / kSpecMax : 1;
+  // pass 2: keys of every m-th sample position (a uniform subsample)
+  const uint4* kv4 = reinterpret_cast<const uint4*>(skey);
+  for (int64_t v0 = tid; v0 < nv; v0 += 4 * kSpecThreads) {
+    int4 x[4];
+    uint4 k[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t v = v0 + u * kSpecThreads;
+      x[u] = v < nv ? pv[v] : make_int4(-1, -1, -1, -1);
+      k[u] = v < nv ? kv4[v] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e0 = 4 * (v0 + u * kSpecThreads);
+      const int32_t pp[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+      const uint32_t kk[4] = {k[u].x, k[u].y, k[u].z, k[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (pp[j] != p || (m > 1 && (e0 + j) % m)) continue;
+        const uint32_t slot = atomicAdd(&s_n, 1u);
+        if (slot < kSpecMax) s_keys[slot] = kk[j];
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t Sp = s_n < kSpecMax ? s_n : kSpecMax;
+    int64_t free_slots = 0;
+    for (int k = pool_begin[p]; k < pool_begin[p + 1]; ++k) {
+      const int64_t f = int64_t(in.max_batch[k]) - in.running[k] - in.waiting[k];
+      free_slots += f > 0 ? f : 0;
+    }
+    int64_t need = free_slots + 1;
+    need = need < int64_t(max_need) ? need : int64_t(max_need);
+    // pool size estimate: S samples cover kSampleLen / stride of the queue
+    const double Np = double(S) * double(stride) / double(kSampleLen);
+    const double frac = Np > 0.0 ? double(Sp) / Np : 0.0;
+    const uint32_t k = static_cast<uint32_t>(ceil(1.5 * double(need) * frac)) + 3u;
+    s_ok = (Sp >= k && Sp >= 64) ? 1u : 0u;
+    s_rank = k;
+    s_prefix = 0;
+    s_mask = 0;
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (tid == 0) spec_on[p] = 0;
+    return;
+  }
+  const uint32_t Sp = s_n < kSpecMax ? s_n : kSpecMax;
+  // k-th smallest sampled key: MSD radix select over the four bytes
+  for (int d = 3; d >= 0; --d) {
+    for (int j = tid; j < kRadix; j += kSpecThreads) s_hist[j] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix, mask = s_mask;
+    // warp-aggregated: the high digits of one pool's keys are mostly equal
+    for (uint32_t j0 = 0; j0 < Sp; j0 += kSpecThreads) {
+      const uint32_t j = j0 + tid;
+      const uint32_t key = j < Sp ? s_keys[j] : 0u;
+      hist_add(s_hist, (key >> (8 * d)) & 0xFF, j < Sp && (key & mask) == prefix);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t rank = s_rank, cum = 0;
+      int dg = 0;
+      for (; dg < kRadix; ++dg) {
+        if (cum + s_hist[dg] >= rank) break;
+        cum += s_hist[dg];
+      }
+      s_prefix = prefix | (static_cast<uint32_t>(dg) << (8 * d));
+      s_mask = mask | (0xFFu << (8 * d));
+      s_rank = rank - cum;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    spec_bound[p] = s_prefix;
+    spec_on[p] = 1;
+  }
+}
+
 // ---- compact key + upfront digit histograms + pool counts -------------
 // 16-byte loads (four requests per thread per step), keys stored as uint4.
 __global__ void __launch_bounds__(256)
 k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
          uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
-         int* __restrict__ error_flags) {
+         int* __restrict__ error_flags, KeygenSpec spec) {
   __shared__ uint32_t sh[4 * kRadix];
   extern __shared__ uint32_t s_pool[];
   const int passes = op.key_bits / kRadixBits;
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) sh[i] = 0;
   for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) s_pool[i] = 0;
   __syncthreads();
-  const uint32_t qmax = (op.q_bits >= 32) ? 0xffffffffu : ((1u << op.q_bits) - 1u);
+  const uint32_t qmax = q_max(op);
   int32_t cur_pool = -1;
   uint32_t cur_cnt = 0;
   int err = 0;
-  auto make_key = [&](int32_t ag, double t) {
+  auto make_key = [&](int32_t ag, double t, int64_t idx) {
     if (ag < 0 || ag >= op.n_agents) {  // reported at order fetch; key 0 in pool 0
       err |= 1;
       ag = 0;
@@ -299,24 +477,17 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
       t = 0.0;
     }
     const int32_t p = a.pool[ag];
-    const uint32_t cls = class_of(a, op.policy, ag);
-    const PoolRange r = ranges[p];
-    // Monotone: (t - lo) and the product are correctly rounded, floor and
-    // the clamp are monotone, so t1 <= t2 implies q1 <= q2.
-    const double x = __dmul_rn(__dsub_rn(t, r.lo), r.scale);
-    uint32_t qv;
-    if (!(x > 0.0)) qv = 0;
-    else if (x >= static_cast<double>(qmax)) qv = qmax;
-    else qv = static_cast<uint32_t>(x);
-    uint32_t key = qv;
-    if (op.class_bits) key |= cls << op.q_bits;
-    if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
+    const uint32_t key = compact_key(a, op, ranges[p], p, ag, t, qmax);
     if (p != cur_pool) {
       if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
       cur_pool = p;
       cur_cnt = 0;
     }
     ++cur_cnt;
+    if (spec.bound && spec.on[p] && key <= spec.bound[p]) {  // dispatch-prefix candidate
+      const uint32_t slot = atomicAdd(&spec.count[p], 1u);
+      if (slot < kTopKMax) spec.cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(idx);
+    }
     return key;
   };
   const double* tp = primary_ptr(q, op.policy);
@@ -345,10 +516,10 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
       const bool valid = v < nv;
       uint4 k4 = make_uint4(0, 0, 0, 0);
       if (valid) {
-        k4.x = make_key(ag[u].x, t0[u].x);
-        k4.y = make_key(ag[u].y, t0[u].y);
-        k4.z = make_key(ag[u].z, t1[u].x);
-        k4.w = make_key(ag[u].w, t1[u].y);
+        k4.x = make_key(ag[u].x, t0[u].x, 4 * v);
+        k4.y = make_key(ag[u].y, t0[u].y, 4 * v + 1);
+        k4.z = make_key(ag[u].z, t1[u].x, 4 * v + 2);
+        k4.w = make_key(ag[u].w, t1[u].y, 4 * v + 3);
         kv[v] = k4;
       }
       for (int pz = 0; pz < passes; ++pz) {
@@ -366,7 +537,7 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
       const bool valid = i < n;
       uint32_t key = 0;
       if (valid) {
-        key = make_key(q.agent[i], tp[i]);
+        key = make_key(q.agent[i], tp[i], i);
         keys[i] = key;
       }
       for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
@@ -673,11 +844,24 @@ k_tie_fix_big(QueueDev q, int policy, uint32_t* __restrict__ perm, uint32_t* __r
 __global__ void k_topk_init(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
                             int64_t n, const uint32_t* __restrict__ hist_excl,
                             const int64_t* __restrict__ pool_offsets, uint32_t max_need,
-                            TopKState* __restrict__ st) {
+                            TopKState* __restrict__ st, const uint32_t* __restrict__ spec_on,
+                            const uint32_t* __restrict__ spec_bound,
+                            const uint32_t* __restrict__ spec_count) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= op.n_pools) return;
   TopKState t{};
   const int64_t cnt = pool_offsets[p + 1] - pool_offsets[p];
+  if (spec_on && spec_on[p] && spec_count[p] <= uint32_t(kTopKMax) && cnt > 0) {
+    // candidates collected by key generation: every key <= spec_bound
+    t.need = 0;
+    t.pool_count = static_cast<uint32_t>(cnt);
+    t.done = 1;
+    t.spec = 1;
+    t.bound = spec_bound[p];
+    t.n_cand = spec_count[p];
+    st[p] = t;
+    return;
+  }
   int64_t free_slots = 0;
   for (int i = pool_begin[p]; i < pool_begin[p + 1]; ++i) {
     const int64_t f = int64_t(in.max_batch[i]) - in.running[i] - in.waiting[i];
@@ -810,11 +994,16 @@ __global__ void k_topk_pick(OrderParams op, int shift, TopKState* __restrict__ s
 __global__ void k_topk_compact(const uint32_t* __restrict__ keys, int64_t n, OrderParams op,
                                TopKState* __restrict__ st, uint32_t* __restrict__ cand) {
   __shared__ uint32_t s_bound[kTopKMaxPools], s_ok[kTopKMaxPools];
+  __shared__ int s_any;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
   for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
     s_bound[p] = st[p].bound;
-    s_ok[p] = !st[p].defer && !st[p].empty;
+    s_ok[p] = !st[p].defer && !st[p].empty && !st[p].spec;
+    if (s_ok[p]) s_any = 1;
   }
   __syncthreads();
+  if (!s_any) return;  // every pool's candidates are already collected
   auto take = [&](uint32_t k, int64_t i) {
     const int p = pool_of_key(k, op);
     if (s_ok[p] && k <= s_bound[p]) {
@@ -965,6 +1154,25 @@ k_topk_sort(QueueDev q, int policy, const uint32_t* __restrict__ keys, OrderPara
   for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = so[i];
 }
 
+int64_t spec_sample_capacity(int64_t cap) {
+  const int64_t stride = sample_stride(cap);
+  return ((cap + stride - 1) / stride + 1) * kSampleLen;
+}
+
+void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
+                       const int32_t* pool_begin, const OrderParams& op, int64_t n,
+                       const OrderWorkspace& ws, TopKWork& w, cudaStream_t st) {
+  const int64_t stride = sample_stride(n);
+  const int64_t blocks = (n + stride - 1) / stride;
+  k_sample_keys<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges,
+                                                                     w.sample_key, w.sample_pool);
+  KX_CHECK_LAUNCH();
+  k_spec_bound<<<op.n_pools, kSpecThreads, sizeof(uint32_t) * kSpecMax, st>>>(
+      in, pool_begin, op, n, stride, blocks * kSampleLen, w.sample_key, w.sample_pool, w.max_need,
+      w.spec_bound, w.spec_on, w.spec_count);
+  KX_CHECK_LAUNCH();
+}
+
 void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
                  const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
                  cudaStream_t st, cudaEvent_t keys_released) {
@@ -972,7 +1180,8 @@ void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin
   const int passes = op.key_bits / kRadixBits;
   const int pb = (op.n_pools + 31) / 32;
   k_topk_init<<<pb, 32, 0, st>>>(in, pool_begin, op, n, ws.hist + (passes - 1) * kRadix,
-                                 ws.pool_offsets, w.max_need, w.state);
+                                 ws.pool_offsets, w.max_need, w.state, w.spec_on, w.spec_bound,
+                                 w.spec_count);
   KX_CHECK_LAUNCH();
   KX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * op.n_pools * kRadix, st));
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, int64_t(sms) * 4)));
@@ -1030,8 +1239,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
   {
     // sampled window: ~256K requests (every request below that)
-    const int64_t target = int64_t(1) << 18;
-    const int64_t stride = n <= target ? kSampleLen : kSampleLen * ((n + target - 1) / target);
+    const int64_t stride = sample_stride(n);
     const int64_t blocks = (n + stride - 1) / stride;
     P.begin("pool_sample", double(blocks) * kSampleLen * 12.0, st);
     k_pool_sample<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges);
@@ -1040,10 +1248,12 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   }
   k_range_finalize<<<(op.n_pools + 127) / 128, 128, 0, st>>>(ws.ranges, op.n_pools, op.q_bits);
   KX_CHECK_LAUNCH();
+  if (hooks && hooks->before_keygen) hooks->before_keygen();
   // reads agent + primary time (12 B), writes the compact key (4 B)
   P.begin("keygen_hist", N * 16.0, st);
   k_keygen<<<grid, 256, sizeof(uint32_t) * op.n_pools, st>>>(q, a, op, n, ws.ranges, ws.keys[0],
-                                                              ws.hist, ws.pool_counts, ws.error_flags);
+                                                              ws.hist, ws.pool_counts, ws.error_flags,
+                                                              hooks ? hooks->spec : KeygenSpec{});
   KX_CHECK_LAUNCH();
   P.end(st);
   k_scan_hist<<<1, 32 * passes, 0, st>>>(ws.hist, passes);
@@ -1101,6 +1311,8 @@ void init_ranges(PoolRange* r, int n, cudaStream_t st) {
 }
 
 void configure_sort_kernels() {
+  KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(uint32_t) * kSpecMax)));
   KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(topk_sort_smem())));
   KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,

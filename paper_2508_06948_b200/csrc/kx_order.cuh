@@ -49,7 +49,7 @@ constexpr int kTopKMaxPools = 32;   // overlap path limit
 // Per-pool radix-select state of the dispatch prefix (k_topk_*).
 struct TopKState {
   uint32_t need, prefix, mask, below, count, done, bound, n_cand;
-  uint32_t pool_count, defer, empty, pad;
+  uint32_t pool_count, defer, empty, spec;  // spec: candidates came from key generation
 };
 
 struct TopKWork {
@@ -58,9 +58,29 @@ struct TopKWork {
   uint32_t* cand;    // [P * kTopKMax] candidate queue indices (unordered)
   uint32_t max_need = kTopKMax;  // prefix length cap (lowered by tests via KX_TOPK_NEED)
   uint32_t* heads;   // [P * kTopKMax] the pool's order prefix
+  // speculative prefix bound from the sample (k_spec_bound), candidates
+  // collected by k_keygen
+  uint32_t* spec_bound;  // [P]
+  uint32_t* spec_on;     // [P]
+  uint32_t* spec_count;  // [P]
+  uint32_t* sample_key;  // [spec_sample_capacity] compact keys of the sampled requests
+  int32_t* sample_pool;  // [spec_sample_capacity] their pools (-1 invalid)
+};
+
+int64_t spec_sample_capacity(int64_t cap);
+
+// Speculative top-K: key generation collects every key <= spec_bound[p] of
+// the pools with spec_on[p] into cand / spec_count (see k_spec_bound).
+struct KeygenSpec {
+  const uint32_t* bound;
+  const uint32_t* on;
+  uint32_t* count;
+  uint32_t* cand;
 };
 
 struct OrderHooks {
+  std::function<void()> before_keygen;         // quantisation window ready, keys not yet built
+  KeygenSpec spec{};                           // speculative prefix collection (bound != nullptr)
   std::function<void()> after_keys;            // compact keys, histograms, pool offsets ready
   std::function<void()> before_key_overwrite;  // after radix pass 0, before pass 1
 };
@@ -68,6 +88,10 @@ struct OrderHooks {
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
                             PhaseProfiler* prof, const OrderHooks* hooks = nullptr);
+
+void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
+                       const int32_t* pool_begin, const OrderParams& op, int64_t n,
+                       const OrderWorkspace& ws, TopKWork& w, cudaStream_t st);
 
 void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
                  const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
