@@ -491,7 +491,8 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
                  o_r = L.take<DispResume>(P), o_sb = L.take<uint32_t>(P), o_so = L.take<uint32_t>(P),
                  o_sc = L.take<uint32_t>(P);
     const int64_t ns = spec_sample_capacity(std::max<int64_t>(s->cap, 1));
-    const size_t o_sk = L.take<uint32_t>(ns), o_sp = L.take<int32_t>(ns);
+    const size_t o_sk = L.take<uint32_t>(ns), o_sp = L.take<int32_t>(ns),
+                 o_ck = L.take<uint32_t>(P * kTopKMax);
     alloc_blob(s->topk_blob, L.off);
     auto& b = s->topk_blob;
     s->topk.state = at<TopKState>(b, o_st);
@@ -504,6 +505,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->topk.spec_count = at<uint32_t>(b, o_sc);
     s->topk.sample_key = at<uint32_t>(b, o_sk);
     s->topk.sample_pool = at<int32_t>(b, o_sp);
+    s->topk.cand_key = at<uint32_t>(b, o_ck);
     if (const char* e = getenv("KX_TOPK_NEED"))  // test knob: force short prefixes
       s->topk.max_need = static_cast<uint32_t>(std::clamp(atoi(e), 1, kTopKMax));
     // The prefix select + dispatch chain is the tick's critical path: its
@@ -702,32 +704,38 @@ void tick_impl(kx_sched* s, double now) {
     return;
   }
   const DispatchParams dp = dispatch_params(s, now);
-  const int passes = op.key_bits / 8;
-  const uint32_t* final_perm = s->ws.vals[passes & 1];
+  // Key generation also collects each pool's order prefix (every key below a
+  // bound taken from the sample); right after it, the dispatch CTAs (high
+  // priority stream) sort their prefix and run the round while the main
+  // stream sorts the whole queue. A round that outlasts its prefix resumes
+  // over the full order (phase 2).
+  KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
   OrderHooks hooks;
-  // the dispatch prefix is collected during key generation (speculative
-  // bound from the sample; launch_topk falls back to the radix select)
   hooks.before_keygen = [&] {
     launch_spec_bound(s->q, s->a, s->in, s->pool_begin, op, s->n, s->ws, s->topk, s->stream);
   };
-  hooks.spec = KeygenSpec{s->topk.spec_bound, s->topk.spec_on, s->topk.spec_count, s->topk.cand};
+  hooks.spec = KeygenSpec{s->topk.spec_bound, s->topk.spec_on, s->topk.spec_count, s->topk.cand,
+                          s->topk.cand_key};
   hooks.after_keys = [&] {
-    KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
     KX_CUDA(cudaEventRecord(s->ev_keys, s->stream));
     KX_CUDA(cudaStreamWaitEvent(s->side, s->ev_keys, 0));
-    s->prof.begin("topk_select", 0.0, s->side);
-    launch_topk(s->q, s->in, s->pool_begin, op, s->n, s->ws, s->topk, s->sms, s->side,
-                s->ev_released);
-    s->prof.end(s->side);
+    DispPhase ph{};
+    ph.phase = 3;
+    ph.pad = op.policy;
+    ph.resume = s->resume;
+    ph.spec_on = s->topk.spec_on;
+    ph.spec_count = s->topk.spec_count;
+    ph.cand = s->topk.cand;
+    ph.cand_key = s->topk.cand_key;
+    ph.pool_counts = s->ws.pool_counts;
+    ph.heads_out = s->topk.heads;
     s->prof.begin("dispatch_prefix", 0.0, s->side);
-    launch_dispatch(s->q, s->a, s->in, s->pool_begin, final_perm, s->ws.pool_offsets, dp, s->n_pools,
+    launch_dispatch(s->q, s->a, s->in, s->pool_begin, nullptr, s->ws.pool_offsets, dp, s->n_pools,
                     s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count,
-                    s->pool_status, s->side,
-                    DispPhase{1, 0, s->topk.heads, s->topk.state, s->resume});
+                    s->pool_status, s->side, ph);
     s->prof.end(s->side);
     KX_CUDA(cudaEventRecord(s->ev_disp, s->side));
   };
-  hooks.before_key_overwrite = [&] { KX_CUDA(cudaStreamWaitEvent(s->stream, s->ev_released, 0)); };
   s->order = launch_order(s->q, s->a, op, s->n, s->ws, s->sms, s->stream, &s->prof, &hooks);
   s->order_valid = true;
   s->order_n = s->n;

@@ -25,6 +25,7 @@
 #include "kx_dispatch.cuh"
 #include "kx_order.cuh"
 #include "kx_state.cuh"
+#include "kx_tuple.cuh"
 
 namespace kx {
 
@@ -1817,7 +1818,7 @@ struct StageMeta {
 struct BatchLayout {
   uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
       st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_viol, g_peak, g_flag,
-      usage, ex, total;
+      c_key, c_idx, usage, ex, total;
 };
 
 BatchLayout batch_layout(int ring) {
@@ -1851,10 +1852,79 @@ BatchLayout batch_layout(int ring) {
   L.g_viol = take(size_t(4) * 32 * 2 * kStage);
   L.g_peak = take(size_t(8) * 32 * 2 * kStage);
   L.g_flag = take(size_t(1) * 32 * 2 * kStage);
+  L.c_key = take(size_t(8) * kTopKMax);
+  L.c_idx = take(size_t(4) * kTopKMax);
   L.usage = take(size_t(8) * 32 * ring);
   L.ex = take(size_t(32) * ring);
   L.total = o;
   return L;
+}
+
+// The collected prefix of one pool in order (all threads of the CTA): a
+// bitonic sort of (compact key << 32 | slot) in shared memory, then runs of
+// equal compact keys re-sorted by the exact tuple (one thread per run).
+// Returns false when a run is longer than kRunMax (degenerate keys): the
+// caller then dispatches from the full order instead.
+constexpr int kRunMax = 16;
+
+__device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __restrict__ cand,
+                            const uint32_t* __restrict__ ckey, int n, uint32_t* __restrict__ heads,
+                            uint64_t* sk, uint32_t* so) {
+  __shared__ int s_long;
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = threadIdx.x; i < p2; i += blockDim.x)
+    sk[i] = i < n ? ((static_cast<uint64_t>(__ldcg(ckey + i)) << 32) | static_cast<uint32_t>(i)) : ~0ull;
+  if (threadIdx.x == 0) s_long = 0;
+  __syncthreads();
+  for (int kk = 2; kk <= p2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint64_t x = sk[i], y = sk[l];
+          if ((x > y) == ((i & kk) == 0)) {
+            sk[i] = y;
+            sk[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) so[i] = __ldcg(cand + static_cast<uint32_t>(sk[i]));
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t k = static_cast<uint32_t>(sk[i] >> 32);
+    const bool start = (i == 0 || static_cast<uint32_t>(sk[i - 1] >> 32) != k) &&
+                       (i + 1 < n && static_cast<uint32_t>(sk[i + 1] >> 32) == k);
+    if (!start) continue;
+    int e = i + 2;
+    while (e < n && e - i <= kRunMax && static_cast<uint32_t>(sk[e] >> 32) == k) ++e;
+    const int len = e - i;
+    if (len > kRunMax) {
+      s_long = 1;
+      continue;
+    }
+    TKey r[kRunMax];
+    for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, so[i + j]);
+    for (int j = 1; j < len; ++j) {
+      const TKey x = r[j];
+      int m = j - 1;
+      while (m >= 0 && tkey_less(q, x, r[m])) {
+        r[m + 1] = r[m];
+        --m;
+      }
+      r[m + 1] = x;
+    }
+    for (int j = 0; j < len; ++j) so[i + j] = r[j].idx;
+  }
+  __syncthreads();
+  if (s_long) return false;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) heads[i] = so[i];
+  __threadfence_block();
+  __syncthreads();
+  return true;
 }
 
 __device__ __forceinline__ void batch_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kBatchThreads) : "memory"); }
@@ -1874,8 +1944,10 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   __shared__ int32_t s_nstage[2];
   __shared__ int64_t s_row0[2];  // log row of each staging buffer's first record
   const int pool = blockIdx.x;
-  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
-  const uint32_t* hp = perm + pool_offsets[pool];
+  // phase 3 learns its heads (and the pool size) only once key generation
+  // has finished, below
+  int64_t pool_n = ph.phase == 3 ? 0 : pool_offsets[pool + 1] - pool_offsets[pool];
+  const uint32_t* hp = ph.phase == 3 ? ph.heads_out + int64_t(pool) * kTopKMax : perm + pool_offsets[pool];
   int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
   bool skip = false;
   if (ph.phase == 1) {
@@ -2168,11 +2240,6 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     loaded_end = nx_start + nx_n;
     issue_idx(loaded_end);
   };
-  if (warp == 1) {
-    issue_idx(pos0);
-    if (pos0 < q_end) land_block();
-  }
-
   // Write staged decision records of buffer `buf` (one warp): decision log
   // rows + candidate peaks (engine.cpp:242-246, dispatcher.cpp:143-147),
   // admitted flags and active_ entries (dispatcher.cpp:78).
@@ -2220,6 +2287,23 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
   };
+
+  // ---- phase 3: the prefix collected by key generation, sorted here ----
+  if (ph.phase == 3) {
+    pool_n = ph.pool_counts[pool];
+    const uint32_t on = ph.spec_on[pool], cnt = ph.spec_count[pool];
+    const bool ok = on && cnt > 0 && cnt <= uint32_t(kTopKMax) &&
+                    sort_prefix(q, ph.pad, ph.cand + int64_t(pool) * kTopKMax,
+                                ph.cand_key + int64_t(pool) * kTopKMax, static_cast<int>(cnt),
+                                ph.heads_out + int64_t(pool) * kTopKMax,
+                                reinterpret_cast<uint64_t*>(smem_raw + lay.c_key),
+                                reinterpret_cast<uint32_t*>(smem_raw + lay.c_idx));
+    q_end = ok ? cnt : 0;
+  }
+  if (warp == 1) {
+    issue_idx(pos0);
+    if (pos0 < q_end) land_block();
+  }
 
   // ---- resolver state (warp 0, lane = instance) ----
   double live = act ? in.live_kv[i] : 0.0;
@@ -2453,7 +2537,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     flush(sbuf ^ 1);  // the last batch's records
     // Phase 1 ran out of prefix heads without finishing the round: hand the
     // state to the continuation (no gc yet: the round is not over).
-    const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
+    const bool defer_rest = (ph.phase == 1 || ph.phase == 3) && !broke && status == KX_OK && pos >= q_end &&
+                            q_end < pool_n;
     int64_t nbase = base;
     if (!defer_rest) {
       // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
@@ -2626,6 +2711,9 @@ void read_dispatch_debug(unsigned long long* out) {
 }
 
 void configure_dispatch_kernels() {
+  cudaFuncAttributes attr;  // load eagerly (see configure_sort_kernels)
+  KX_CUDA(cudaFuncGetAttributes(&attr, k_dispatch_batch));
+  KX_CUDA(cudaFuncGetAttributes(&attr, k_gc_all));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2652,7 +2740,8 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
   if (max_inst_per_pool <= 32) {
     const char* variant = getenv("KX_DISPATCH");  // test knob: batch (default) | pipe | warp
     const BatchLayout bl = batch_layout(dp.ring);
-    if ((!variant || !strcmp(variant, "batch")) && bl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+    if ((!variant || !strcmp(variant, "batch") || phase.phase == 3) &&
+        bl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
       k_dispatch_batch<<<n_pools, kBatchThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
                                                                          pool_offsets, dp, bl, rows, cand,
                                                                          row_count, admitted_count,

@@ -36,11 +36,19 @@ struct DispResume {
 };
 
 struct DispPhase {
-  int32_t phase;               // 0 full order, 1 top-K prefix, 2 continuation
+  int32_t phase;               // 0 full order, 1 top-K prefix, 2 continuation, 3 overlapped tick
   int32_t pad;
-  const uint32_t* heads;       // [P * kTopKMax] (phase 1)
+  const uint32_t* heads;       // [P * kTopKMax] (phase 1; phase 3 writes it)
   const TopKState* tk;         // (phase 1)
   DispResume* resume;          // [P] (phases 1, 2)
+  // phase 3: like phase 1, with the prefix collected by key generation and
+  // sorted in the dispatch CTA (launched after key generation)
+  const uint32_t* spec_on;      // [P] speculative prefix collected
+  const uint32_t* spec_count;   // [P]
+  const uint32_t* cand;         // [P * kTopKMax] candidate queue indices
+  const uint32_t* cand_key;     // [P * kTopKMax] their compact keys
+  const uint32_t* pool_counts;  // [P] from key generation
+  uint32_t* heads_out;          // [P * kTopKMax]
 };
 
 void configure_dispatch_kernels();

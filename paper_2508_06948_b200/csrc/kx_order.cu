@@ -22,6 +22,7 @@
 #include "kx_order.cuh"
 #include "kx_sort.cuh"
 #include "kx_state.cuh"
+#include "kx_tuple.cuh"
 
 namespace kx {
 
@@ -486,7 +487,10 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
     ++cur_cnt;
     if (spec.bound && spec.on[p] && key <= spec.bound[p]) {  // dispatch-prefix candidate
       const uint32_t slot = atomicAdd(&spec.count[p], 1u);
-      if (slot < kTopKMax) spec.cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(idx);
+      if (slot < kTopKMax) {
+        spec.cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(idx);
+        spec.cand_key[int64_t(p) * kTopKMax + slot] = key;
+      }
     }
     return key;
   };
@@ -573,35 +577,6 @@ __global__ void k_pool_offsets(const uint32_t* __restrict__ counts, int n_pools,
 constexpr int kThreadRun = 16;
 
 namespace {
-
-struct TKey {
-  uint64_t w0, w1, w2;
-  uint32_t idx;
-};
-
-__device__ __forceinline__ TKey load_tkey(const QueueDev& q, int policy, uint32_t idx) {
-  TKey r;
-  const double app = q.app_start[idx];
-  const double qe = q.queue_enter[idx];
-  switch (policy) {
-    case KX_SCHED_KAIROS: r.w0 = ordered_bits(app); r.w1 = ordered_bits(qe); r.w2 = 0; break;
-    case KX_SCHED_ORACLE: r.w0 = ordered_bits(q.rem[idx]); r.w1 = ordered_bits(qe); r.w2 = ordered_bits(app); break;
-    default: r.w0 = ordered_bits(qe); r.w1 = ordered_bits(app); r.w2 = 0; break;
-  }
-  r.idx = idx;
-  return r;
-}
-
-__device__ __forceinline__ bool tkey_less(const QueueDev& q, const TKey& a, const TKey& b) {
-  if (a.w0 != b.w0) return a.w0 < b.w0;
-  if (a.w1 != b.w1) return a.w1 < b.w1;
-  if (a.w2 != b.w2) return a.w2 < b.w2;
-  const uint64_t ma = q.msg[a.idx], mb = q.msg[b.idx];
-  if (ma != mb) return ma < mb;
-  const uint64_t ua = q.uid[a.idx], ub = q.uid[b.idx];
-  if (ua != ub) return ua < ub;
-  return a.idx < b.idx;
-}
 
 }  // namespace
 
@@ -1215,6 +1190,10 @@ void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, 
   KX_CHECK_LAUNCH();
 }
 
+int keygen_grid(int64_t n, int sms) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
+}
+
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
                             PhaseProfiler* prof, const OrderHooks* hooks) {
@@ -1236,7 +1215,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     res.keys = ws.keys[0];
     return res;
   }
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
+  const int grid = keygen_grid(n, sms);
   {
     // sampled window: ~256K requests (every request below that)
     const int64_t stride = sample_stride(n);
@@ -1310,7 +1289,29 @@ void init_ranges(PoolRange* r, int n, cudaStream_t st) {
   KX_CHECK_LAUNCH();
 }
 
+// Module lazy loading (CUDA 12 default) loads a kernel at its first launch
+// and may wait for the device to drain while doing so; the overlapped tick
+// has CTAs that wait on other kernels, so every kernel of the tick is
+// loaded up front.
+template <typename F>
+static void preload(F f) {
+  cudaFuncAttributes attr;
+  KX_CUDA(cudaFuncGetAttributes(&attr, f));
+}
+
 void configure_sort_kernels() {
+  preload(k_scan_hist);
+  preload(k_pool_sample);
+  preload(k_range_finalize);
+  preload(k_sample_keys);
+  preload(k_spec_bound);
+  preload(k_keygen);
+  preload(k_pool_offsets);
+  preload(k_tie_runs);
+  preload(k_tie_fix_small);
+  preload(k_tie_fix_big);
+  preload(k_init_ranges);
+  preload(k_onesweep_pass<uint32_t>);
   KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(uint32_t) * kSpecMax)));
   KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,

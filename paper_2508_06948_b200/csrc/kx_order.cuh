@@ -65,7 +65,10 @@ struct TopKWork {
   uint32_t* spec_count;  // [P]
   uint32_t* sample_key;  // [spec_sample_capacity] compact keys of the sampled requests
   int32_t* sample_pool;  // [spec_sample_capacity] their pools (-1 invalid)
+  uint32_t* cand_key;    // [P * kTopKMax]
 };
+
+int keygen_grid(int64_t n, int sms);
 
 int64_t spec_sample_capacity(int64_t cap);
 
@@ -76,6 +79,7 @@ struct KeygenSpec {
   const uint32_t* on;
   uint32_t* count;
   uint32_t* cand;
+  uint32_t* cand_key;  // compact key of each candidate
 };
 
 struct OrderHooks {
