@@ -433,16 +433,33 @@ k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
       hist_add(s_hist, (key >> (8 * d)) & 0xFF, j < Sp && (key & mask) == prefix);
     }
     __syncthreads();
-    if (tid == 0) {
-      uint32_t rank = s_rank, cum = 0;
-      int dg = 0;
-      for (; dg < kRadix; ++dg) {
-        if (cum + s_hist[dg] >= rank) break;
-        cum += s_hist[dg];
+    if (tid < 32) {  // warp 0: bucket of the rank-th key (eight bins per lane)
+      const uint32_t rank = s_rank;
+      uint32_t h[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        h[j] = s_hist[tid * 8 + j];
+        sum += h[j];
       }
-      s_prefix = prefix | (static_cast<uint32_t>(dg) << (8 * d));
-      s_mask = mask | (0xFFu << (8 * d));
-      s_rank = rank - cum;
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const uint32_t hit = __ballot_sync(0xffffffffu, incl >= rank);
+      const int lane_hit = __ffs(hit) - 1;
+      if (tid == lane_hit) {
+        uint32_t cum = incl - sum;
+        int j = 0;
+        for (; j < 8; ++j) {
+          if (cum + h[j] >= rank) break;
+          cum += h[j];
+        }
+        s_prefix = prefix | (static_cast<uint32_t>(tid * 8 + j) << (8 * d));
+        s_mask = mask | (0xFFu << (8 * d));
+        s_rank = rank - cum;
+      }
     }
     __syncthreads();
   }
@@ -526,12 +543,24 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
         k4.w = make_key(ag[u].w, t1[u].y, 4 * v + 3);
         kv[v] = k4;
       }
+      // the two low digits are spread (plain shared atomics); the high ones
+      // are often equal across a warp (aggregated increments)
       for (int pz = 0; pz < passes; ++pz) {
         const int sh_ = pz * kRadixBits;
-        hist_add(&sh[pz * kRadix], digit_of(k4.x, sh_), valid);
-        hist_add(&sh[pz * kRadix], digit_of(k4.y, sh_), valid);
-        hist_add(&sh[pz * kRadix], digit_of(k4.z, sh_), valid);
-        hist_add(&sh[pz * kRadix], digit_of(k4.w, sh_), valid);
+        uint32_t* h = &sh[pz * kRadix];
+        if (pz < 2) {
+          if (valid) {
+            atomicAdd(&h[digit_of(k4.x, sh_)], 1u);
+            atomicAdd(&h[digit_of(k4.y, sh_)], 1u);
+            atomicAdd(&h[digit_of(k4.z, sh_)], 1u);
+            atomicAdd(&h[digit_of(k4.w, sh_)], 1u);
+          }
+        } else {
+          hist_add(h, digit_of(k4.x, sh_), valid);
+          hist_add(h, digit_of(k4.y, sh_), valid);
+          hist_add(h, digit_of(k4.z, sh_), valid);
+          hist_add(h, digit_of(k4.w, sh_), valid);
+        }
       }
     }
   }
