@@ -490,8 +490,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
                  o_c = L.take<uint32_t>(P * kTopKMax), o_hd = L.take<uint32_t>(P * kTopKMax),
                  o_r = L.take<DispResume>(P), o_sb = L.take<uint32_t>(P), o_so = L.take<uint32_t>(P),
                  o_sc = L.take<uint32_t>(P);
-    const int64_t ns = spec_sample_capacity(std::max<int64_t>(s->cap, 1));
-    const size_t o_sk = L.take<uint32_t>(ns), o_sp = L.take<int32_t>(ns),
+    const size_t o_sk = L.take<uint32_t>(spec_list_words(s->n_pools)), o_sp = L.take<uint32_t>(P),
                  o_ck = L.take<uint32_t>(P * kTopKMax);
     alloc_blob(s->topk_blob, L.off);
     auto& b = s->topk_blob;
@@ -503,8 +502,8 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->topk.spec_bound = at<uint32_t>(b, o_sb);
     s->topk.spec_on = at<uint32_t>(b, o_so);
     s->topk.spec_count = at<uint32_t>(b, o_sc);
-    s->topk.sample_key = at<uint32_t>(b, o_sk);
-    s->topk.sample_pool = at<int32_t>(b, o_sp);
+    s->topk.plist = at<uint32_t>(b, o_sk);
+    s->topk.plist_count = at<uint32_t>(b, o_sp);
     s->topk.cand_key = at<uint32_t>(b, o_ck);
     if (const char* e = getenv("KX_TOPK_NEED"))  // test knob: force short prefixes
       s->topk.max_need = static_cast<uint32_t>(std::clamp(atoi(e), 1, kTopKMax));

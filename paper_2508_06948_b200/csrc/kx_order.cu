@@ -314,16 +314,17 @@ __device__ __forceinline__ uint32_t q_max(const OrderParams& op) {
 constexpr int kSpecMax = 32768;
 constexpr int kSpecThreads = 1024;
 
-// Compact keys of the sampled requests (same positions as k_pool_sample),
-// pool id per sample (-1 = invalid), for k_spec_bound.
+// Compact keys of the sampled requests (every m-th block of k_pool_sample's
+// positions), appended to per-pool lists of at most kSpecMax (block-
+// aggregated: a block's requests mostly share one pool). plist_count[p]
+// counts every sample of p, kept or not.
 __global__ void __launch_bounds__(kSampleLen)
-k_sample_keys(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
-              const PoolRange* __restrict__ ranges, uint32_t* __restrict__ skey,
-              int32_t* __restrict__ spool) {
-  const int64_t e = int64_t(blockIdx.x) * kSampleLen + threadIdx.x;
-  const int64_t i = int64_t(blockIdx.x) * stride + threadIdx.x;
+k_sample_keys(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride, int64_t m,
+              const PoolRange* __restrict__ ranges, uint32_t* __restrict__ plist,
+              uint32_t* __restrict__ plist_count) {
+  const int64_t i = int64_t(blockIdx.x) * m * stride + threadIdx.x;
   int32_t p = -1;
-  uint32_t key = 0xffffffffu;
+  uint32_t key = 0;
   if (i < n) {
     const int32_t ag = q.agent[i];
     const double t = primary_ptr(q, op.policy)[i];
@@ -332,70 +333,42 @@ k_sample_keys(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
       key = compact_key(a, op, ranges[p], p, ag, t, q_max(op));
     }
   }
-  skey[e] = key;
-  spool[e] = p;
+  const int lane = threadIdx.x & 31;
+  const uint32_t valid = __ballot_sync(0xffffffffu, p >= 0);
+  const int32_t p0 = valid ? __shfl_sync(0xffffffffu, p, __ffs(valid) - 1) : -1;
+  if (__all_sync(0xffffffffu, p < 0 || p == p0)) {  // one reservation per warp
+    uint32_t base = 0;
+    if (lane == 0 && valid) base = atomicAdd(&plist_count[p0], static_cast<uint32_t>(__popc(valid)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t slot = base + __popc(valid & lanemask_lt());
+    if (p >= 0 && slot < kSpecMax) plist[int64_t(p) * kSpecMax + slot] = key;
+  } else if (p >= 0) {
+    const uint32_t slot = atomicAdd(&plist_count[p], 1u);
+    if (slot < kSpecMax) plist[int64_t(p) * kSpecMax + slot] = key;
+  }
 }
 
 __global__ void __launch_bounds__(kSpecThreads)
 k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op, int64_t n,
-             int64_t stride, int64_t n_samples, const uint32_t* __restrict__ skey,
-             const int32_t* __restrict__ spool, uint32_t max_need, uint32_t* __restrict__ spec_bound,
-             uint32_t* __restrict__ spec_on, uint32_t* __restrict__ spec_count) {
+             int64_t stride, int64_t m, const uint32_t* __restrict__ plist,
+             const uint32_t* __restrict__ plist_count, uint32_t max_need,
+             uint32_t* __restrict__ spec_bound, uint32_t* __restrict__ spec_on,
+             uint32_t* __restrict__ spec_count) {
   extern __shared__ uint32_t s_keys[];  // [kSpecMax]
   __shared__ uint32_t s_hist[kRadix];
-  __shared__ uint32_t s_cnt, s_n;
+  __shared__ uint32_t s_n;
   __shared__ uint32_t s_prefix, s_mask, s_rank, s_ok;
   const int p = blockIdx.x;
   const int tid = threadIdx.x;
+  const uint32_t S = plist_count[p];
+  const uint32_t Sk = S < kSpecMax ? S : kSpecMax;
   if (tid == 0) {
-    s_cnt = 0;
-    s_n = 0;
+    s_n = Sk;
     spec_count[p] = 0;
   }
-  __syncthreads();
-  // pass 1: samples of pool p (int4 loads, four in flight per thread)
-  uint32_t c = 0;
-  const int64_t nv = n_samples >> 2;  // n_samples is a multiple of kSampleLen
-  const int4* pv = reinterpret_cast<const int4*>(spool);
-  for (int64_t v0 = tid; v0 < nv; v0 += 4 * kSpecThreads) {
-    int4 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t v = v0 + u * kSpecThreads;
-      x[u] = v < nv ? pv[v] : make_int4(-1, -1, -1, -1);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) c += (x[u].x == p) + (x[u].y == p) + (x[u].z == p) + (x[u].w == p);
-  }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((tid & 31) == 0 && c) atomicAdd(&s_cnt, c);
-  __syncthreads();
-  const uint32_t S = s_cnt;
-  const int64_t m = S > kSpecMax ? (S + kSpecMax - 1) / kSpecMax : 1;
-  // pass 2: keys of every m-th sample position (a uniform subsample)
-  const uint4* kv4 = reinterpret_cast<const uint4*>(skey);
-  for (int64_t v0 = tid; v0 < nv; v0 += 4 * kSpecThreads) {
-    int4 x[4];
-    uint4 k[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t v = v0 + u * kSpecThreads;
-      x[u] = v < nv ? pv[v] : make_int4(-1, -1, -1, -1);
-      k[u] = v < nv ? kv4[v] : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e0 = 4 * (v0 + u * kSpecThreads);
-      const int32_t pp[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-      const uint32_t kk[4] = {k[u].x, k[u].y, k[u].z, k[u].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (pp[j] != p || (m > 1 && (e0 + j) % m)) continue;
-        const uint32_t slot = atomicAdd(&s_n, 1u);
-        if (slot < kSpecMax) s_keys[slot] = kk[j];
-      }
-    }
-  }
+  const uint4* src = reinterpret_cast<const uint4*>(plist + int64_t(p) * kSpecMax);
+  uint4* dst = reinterpret_cast<uint4*>(s_keys);
+  for (uint32_t v = tid; v < (Sk + 3) / 4; v += kSpecThreads) dst[v] = src[v];
   __syncthreads();
   if (tid == 0) {
     const uint32_t Sp = s_n < kSpecMax ? s_n : kSpecMax;
@@ -406,8 +379,8 @@ k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
     }
     int64_t need = free_slots + 1;
     need = need < int64_t(max_need) ? need : int64_t(max_need);
-    // pool size estimate: S samples cover kSampleLen / stride of the queue
-    const double Np = double(S) * double(stride) / double(kSampleLen);
+    // pool size estimate: the S samples cover kSampleLen / (m * stride) of the queue
+    const double Np = double(S) * double(m) * double(stride) / double(kSampleLen);
     const double frac = Np > 0.0 ? double(Sp) / Np : 0.0;
     const uint32_t k = static_cast<uint32_t>(ceil(1.5 * double(need) * frac)) + 3u;
     s_ok = (Sp >= k && Sp >= 64) ? 1u : 0u;
@@ -1158,24 +1131,26 @@ k_topk_sort(QueueDev q, int policy, const uint32_t* __restrict__ keys, OrderPara
   for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = so[i];
 }
 
-int64_t spec_sample_capacity(int64_t cap) {
-  const int64_t stride = sample_stride(cap);
-  return ((cap + stride - 1) / stride + 1) * kSampleLen;
-}
-
 void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                        const int32_t* pool_begin, const OrderParams& op, int64_t n,
                        const OrderWorkspace& ws, TopKWork& w, cudaStream_t st) {
   const int64_t stride = sample_stride(n);
   const int64_t blocks = (n + stride - 1) / stride;
-  k_sample_keys<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges,
-                                                                     w.sample_key, w.sample_pool);
+  // every m-th sample block: about kSpecMax / 2 samples per pool when the
+  // pools are balanced
+  const int64_t per = int64_t(kSpecMax / 2) * op.n_pools;
+  const int64_t m = std::max<int64_t>(1, (blocks * kSampleLen + per - 1) / per);
+  KX_CUDA(cudaMemsetAsync(w.plist_count, 0, sizeof(uint32_t) * op.n_pools, st));
+  k_sample_keys<<<static_cast<unsigned>((blocks + m - 1) / m), kSampleLen, 0, st>>>(
+      q, a, op, n, stride, m, ws.ranges, w.plist, w.plist_count);
   KX_CHECK_LAUNCH();
   k_spec_bound<<<op.n_pools, kSpecThreads, sizeof(uint32_t) * kSpecMax, st>>>(
-      in, pool_begin, op, n, stride, blocks * kSampleLen, w.sample_key, w.sample_pool, w.max_need,
-      w.spec_bound, w.spec_on, w.spec_count);
+      in, pool_begin, op, n, stride, m, w.plist, w.plist_count, w.max_need, w.spec_bound, w.spec_on,
+      w.spec_count);
   KX_CHECK_LAUNCH();
 }
+
+size_t spec_list_words(int n_pools) { return size_t(n_pools) * kSpecMax; }
 
 void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
                  const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,

@@ -63,14 +63,14 @@ struct TopKWork {
   uint32_t* spec_bound;  // [P]
   uint32_t* spec_on;     // [P]
   uint32_t* spec_count;  // [P]
-  uint32_t* sample_key;  // [spec_sample_capacity] compact keys of the sampled requests
-  int32_t* sample_pool;  // [spec_sample_capacity] their pools (-1 invalid)
+  uint32_t* plist;        // [P * kSpecMax] compact keys of each pool's sampled requests
+  uint32_t* plist_count;  // [P]
   uint32_t* cand_key;    // [P * kTopKMax]
 };
 
 int keygen_grid(int64_t n, int sms);
 
-int64_t spec_sample_capacity(int64_t cap);
+size_t spec_list_words(int n_pools);
 
 // Speculative top-K: key generation collects every key <= spec_bound[p] of
 // the pools with spec_on[p] into cand / spec_count (see k_spec_bound).
