@@ -58,39 +58,65 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling around the timed region (B200_PROFILING.md): started
+    before the warm-up, 50 ms period, and only the samples whose timestamp falls
+    inside the timed region are summarised (the nearest one if the region is
+    shorter than the period)."""
 
     def __init__(self, index: int):
         self.path = Path("/tmp") / f"kx_clocks_{os.getpid()}.csv"
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.t0 = self.t1 = None
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def stop(self):
         if self.p is None:
             return None
+        time.sleep(0.15)  # let the sample after the region land
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
         except Exception:
             self.p.kill()
         self.f.close()
-        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.count(",") >= 8]
+        import datetime
+        rows = []
+        for r in self.path.read_text().strip().splitlines():
+            c = [x.strip() for x in r.split(",")]
+            if len(c) < 10:
+                continue
+            try:
+                ts = datetime.datetime.strptime(c[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            rows.append((ts, c))
         if not rows:
             return None
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        t0 = self.t0 or rows[0][0]
+        t1 = self.t1 or rows[-1][0]
+        inside = [c for ts, c in rows if t0 <= ts <= t1]
+        if not inside:  # region shorter than the period: nearest sample
+            inside = [min(rows, key=lambda r: abs(r[0] - (t0 + t1) / 2))[1]]
+        sm = [float(c[2]) for c in inside if c[2].replace(".", "").isdigit()]
+        mx = [float(c[3]) for c in inside if c[3].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        reasons = sorted({n for c in inside for n, v in zip(names, c[6:10]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(inside)}
 
 
 def build_c4(rank: int):
@@ -140,6 +166,7 @@ def run_mine(args):
         s.restore()
         s.tick(NOW)
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step()
     s.synchronize()
@@ -148,7 +175,6 @@ def run_mine(args):
     decisions = int(sum(len(r) for r in rows))
 
     # ---- timed region: device-resident inputs ---------------------------
-    clocks = Clocks(local)
     s.profile(True)
     if dist:
         dist.barrier()
@@ -157,11 +183,13 @@ def run_mine(args):
     launches0 = lib.kx_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark(True)
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
     ev1.synchronize()
+    clocks.mark(False)
     s.synchronize()
     torch.cuda.synchronize(dev)
     launches = lib.kx_launch_count() - launches0
@@ -409,7 +437,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -12,7 +12,7 @@ if [[ $STAGE == all || $STAGE == tests ]]; then
   timeout 900 python -m pytest tests -q -m gpu -x ${PYTEST_ARGS:-} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 fi
 if [[ $STAGE == all || $STAGE == bench ]]; then
-  timeout 900 python bench.py --steps ${STEPS:-20} --warmup ${WARMUP:-5} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+  timeout 900 python bench.py --steps ${STEPS:-200} --warmup ${WARMUP:-5} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 fi
 if [[ $STAGE == all || $STAGE == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" --csv \
