@@ -1806,6 +1806,9 @@ constexpr int kBatchEval = 8;
 constexpr int kBatchThreads = 32 * (kBatchEval + 1);
 constexpr int kStage = 64;  // staged decision records per batch buffer
 constexpr int kFlushWarp = 2;
+// Ledger rows of 33 words: lanes = instances read a row conflict-free, and
+// lanes = slots read one instance's column conflict-free too.
+constexpr int kRow = 33;
 
 struct StageMeta {
   int32_t hs;        // head ring slot
@@ -1968,7 +1971,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   if (skip) return;  // uniform over the CTA
   const bool dbg = KX_DISPATCH_TIMERS && blockIdx.x == 0 && threadIdx.x == 0;
   if (dbg) g_disp_dbg[0] = gtimer();
-  unsigned long long acc_a = 0, acc_b = 0, tA = 0, nbat = 0;
+  unsigned long long acc_a = 0, acc_b = 0, tA = 0, nbat = 0, acc_fix = 0, acc_sel = 0, acc_stg = 0, acc_com = 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ib = pool_begin[pool];
@@ -2035,7 +2038,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   const int64_t wB = s_win[0];
   const int64_t wtop = s_win[1];
   const int win = wtop < wB ? 0 : static_cast<int>(wtop - wB + 1 < ring ? wtop - wB + 1 : ring);
-  for (int j = threadIdx.x; j < 32 * ring; j += kBatchThreads) {
+  for (int j = threadIdx.x; j < kRow * ring; j += kBatchThreads) {
     su[j] = 0.0;
     se[j] = 0;
   }
@@ -2052,7 +2055,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         const int l = e & 31;
         const int li = e < total ? s_li[l] : -1;
         const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
-        dst[k] = li >= 0 ? pos * 32 + l : -1;
+        dst[k] = li >= 0 ? pos * kRow + l : -1;
         u[k] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
         x[k] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
       }
@@ -2118,7 +2121,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         if (mode == kModeTabPk) {
 #pragma unroll 4
           for (int jj = 0; jj < tn; ++jj) {
-            const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
+            const double total = __dadd_rn(su[p2 * kRow + lane], tab[jj]);
             if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
             const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
             peak = tb > peak ? tb : peak;
@@ -2127,7 +2130,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         } else {
 #pragma unroll 4
           for (int jj = 0; jj < tn; ++jj) {
-            const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[jj]));
+            const double total = __dadd_rn(su[p2 * kRow + lane], pk_of(P, kr, tab[jj]));
             if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
             const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
             peak = tb > peak ? tb : peak;
@@ -2144,10 +2147,10 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         uint32_t viol = kNone;
         for (int32_t o = lo_off; o <= top; ++o) {
           const int p2 = static_cast<int>((B + o) & rmask);
-          const bool e = se[p2 * 32 + lane] != 0;
+          const bool e = se[p2 * kRow + lane] != 0;
           const bool in_span = o >= fo && o <= lo;
           if (!(e || in_span)) continue;
-          const double used = e ? su[p2 * 32 + lane] : 0.0;
+          const double used = e ? su[p2 * kRow + lane] : 0.0;
           const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
           if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
           const uint64_t tb = ordered_bits(total);
@@ -2316,8 +2319,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   if (warp == 0) {
     for (int32_t o = lo_off; o <= hi_off; ++o) {
       const int p2 = static_cast<int>((B + o) & rmask);
-      if (se[p2 * 32 + lane]) {
-        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
+      if (se[p2 * kRow + lane]) {
+        const uint64_t tb = ordered_bits(su[p2 * kRow + lane]);
         umax = tb > umax ? tb : umax;
       }
     }
@@ -2389,6 +2392,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             susp = false;
             st_susp[lane] = 0;
           }
+          unsigned long long tq0 = dbg ? clock64() : 0;
           if ((fixm >> lane) & 1u) {  // changed lanes re-evaluate themselves
             if (mode == kModeTabPk) {  // the common shape, inline
               const bool el = act && !susp && !(running + waiting >= mb);
@@ -2399,8 +2403,9 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
                 if (first < base || last >= base + ring) flg |= 2u;
                 peak = umax;
                 int p2 = pbase;
+#pragma unroll 4
                 for (int jj = 0; jj < tn; ++jj) {
-                  const double total = __dadd_rn(su[p2 * 32 + lane], tab[jj]);
+                  const double total = __dadd_rn(su[p2 * kRow + lane], tab[jj]);
                   if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
                   const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
                   peak = tb > peak ? tb : peak;
@@ -2419,6 +2424,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             broke = true;
             break;
           }
+          unsigned long long tq1 = dbg ? clock64() : 0;
+          if (dbg) acc_fix += tq1 - tq0;
           const bool fits = (flg & 1u) && viol == kNone;
           // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
           const uint64_t key = fits ? peak : ~0ull;
@@ -2427,6 +2434,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           const uint32_t ovm = __ballot_sync(0xffffffffu, fits && __dadd_rn(live, P) > cap);  // engine.cpp:254-258
           const int bl = winners ? __ffs(winners) - 1 : -1;
           const bool overload = bl >= 0 && ((ovm >> bl) & 1u);
+          unsigned long long tq2 = dbg ? clock64() + (bl & 0) : 0;
+          if (dbg) acc_sel += tq2 - tq1;
           // stage the decision record (flushed by another warp later)
           if (ns == kStage) {  // buffer full: write it out here
             if (lane == 0) s_nstage[sbuf] = ns;
@@ -2444,6 +2453,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             g_peak[g * 32 + lane] = peak;
             g_flag[g * 32 + lane] = static_cast<uint8_t>(flg);
           }
+          unsigned long long tq3 = dbg ? clock64() : 0;
+          if (dbg) acc_stg += tq3 - tq2;
           ++ns;
           ++nrows;
           if (bl < 0) {  // head keeps its place (engine.cpp:247)
@@ -2468,14 +2479,29 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           // Dispatcher::commit, in the target's own lane: book the span
           // slots, raise its maximum stored usage, admit (engine.cpp:298-319).
           const double T = h_T[hs];
-          if (lane == bl) {
+          if (mode == kModeTabPk && tn <= 32) {
+            // the common shape: lanes = span slots, one pass; the target's
+            // new maximum stored usage is a warp max of the booked slots
+            uint64_t tb = kZeroBits;
+            if (lane < tn) {
+              const int p2 = (pbase + lane) & rmask;
+              const double nu = __dadd_rn(su[p2 * kRow + bl], tab[lane]);
+              su[p2 * kRow + bl] = nu;
+              se[p2 * kRow + bl] = 1;
+              tb = static_cast<uint64_t>(__double_as_longlong(nu)) | kZeroBits;
+            }
+            const uint64_t nb = warp_max_u64(tb);
+            if (lane == bl) umax = nb > umax ? nb : umax;
+            __syncwarp();  // the target's lane reads these slots next
+          } else if (lane == bl) {
             if (mode != kModeGeneric) {  // usage + pk >= 0: raw bits order
               int p2 = static_cast<int>(first & rmask);
+#pragma unroll 4
               for (int s = 0; s < tn; ++s) {
                 const double pk = mode == kModeTabPk ? tab[s] : pk_of(P, kr, tab[s]);
-                const double nu = __dadd_rn(su[p2 * 32 + lane], pk);
-                su[p2 * 32 + lane] = nu;
-                se[p2 * 32 + lane] = 1;
+                const double nu = __dadd_rn(su[p2 * kRow + lane], pk);
+                su[p2 * kRow + lane] = nu;
+                se[p2 * kRow + lane] = 1;
                 const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(nu)) | kZeroBits;
                 umax = tb > umax ? tb : umax;
                 p2 = (p2 + 1) & rmask;
@@ -2485,13 +2511,15 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
               const double tee = __dsub_rn(te, kTimeEpsilon);
               for (int64_t s = first; s <= last; ++s) {
                 const int p2 = static_cast<int>(s & rmask);
-                const double nu = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, slot_dt(now, t0e, te, tee, s, L)));
-                su[p2 * 32 + lane] = nu;
-                se[p2 * 32 + lane] = 1;
+                const double nu = __dadd_rn(su[p2 * kRow + lane], pk_of(P, kr, slot_dt(now, t0e, te, tee, s, L)));
+                su[p2 * kRow + lane] = nu;
+                se[p2 * kRow + lane] = 1;
                 const uint64_t tb = ordered_bits(nu);
                 umax = tb > umax ? tb : umax;
               }
             }
+          }
+          if (lane == bl) {
             if (nonempty && last > hi) {
               hi = last;
               hi_off = static_cast<int32_t>(last - B);
@@ -2514,6 +2542,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             broke = true;
             break;
           }
+          if (dbg) acc_com += clock64() - tq3;
           dirty |= 1u << bl;
           ++nadm;
           ++pos;
@@ -2546,8 +2575,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         const int64_t stop = cslot < base + ring ? cslot : base + ring;
         for (int64_t s = base; s < stop; ++s) {
           const int p2 = static_cast<int>(s & rmask);
-          su[p2 * 32 + lane] = 0.0;
-          se[p2 * 32 + lane] = 0;
+          su[p2 * kRow + lane] = 0.0;
+          se[p2 * kRow + lane] = 0;
         }
         nbase = cslot;
       }
@@ -2574,7 +2603,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
   }
-  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; g_disp_dbg[6] = acc_a; g_disp_dbg[7] = acc_b; g_disp_dbg[11] = nbat; }
+  if (dbg) { g_disp_dbg[3] = gtimer(); g_disp_dbg[5] = nrows; g_disp_dbg[6] = acc_a; g_disp_dbg[7] = acc_b; g_disp_dbg[11] = nbat; g_disp_dbg[8] = acc_fix; g_disp_dbg[9] = acc_sel; g_disp_dbg[10] = acc_stg; g_disp_dbg[12] = acc_com; }
   __syncthreads();
   {
     // write back the window (booked slots only grow hi; gc only clears inside it)
@@ -2585,8 +2614,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       const int lj = s_li[l];
       if (lj < 0) continue;
       const int p2 = static_cast<int>((wB + (e >> 5)) & rmask);
-      in.usage[int64_t(ib + lj) * ring + p2] = su[p2 * 32 + l];
-      in.exists[int64_t(ib + lj) * ring + p2] = se[p2 * 32 + l];
+      in.usage[int64_t(ib + lj) * ring + p2] = su[p2 * kRow + l];
+      in.exists[int64_t(ib + lj) * ring + p2] = se[p2 * kRow + l];
     }
   }
   if (dbg) g_disp_dbg[4] = gtimer();
