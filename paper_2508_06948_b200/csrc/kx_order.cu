@@ -444,15 +444,33 @@ k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
 
 // ---- compact key + upfront digit histograms + pool counts -------------
 // 16-byte loads (four requests per thread per step), keys stored as uint4.
+// The per-agent (pool, class) pairs and the per-pool window and prefix
+// bound are staged in shared memory when the agent table is small.
+constexpr int kKeygenAgents = 2048;
+
+template <bool kSmemTables>
 __global__ void __launch_bounds__(256)
 k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
          uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
          int* __restrict__ error_flags, KeygenSpec spec) {
   __shared__ uint32_t sh[4 * kRadix];
-  extern __shared__ uint32_t s_pool[];
+  __shared__ uint32_t s_ag[kSmemTables ? kKeygenAgents : 1];  // pool << 16 | class
+  extern __shared__ __align__(16) unsigned char kg_dyn[];
+  double* s_lo = reinterpret_cast<double*>(kg_dyn);                 // [P]
+  double* s_scale = s_lo + op.n_pools;                              // [P]
+  int64_t* s_bnd = reinterpret_cast<int64_t*>(s_scale + op.n_pools);  // [P] prefix bound, -1 off
+  uint32_t* s_pool = reinterpret_cast<uint32_t*>(s_bnd + op.n_pools);  // [P] counts
   const int passes = op.key_bits / kRadixBits;
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) sh[i] = 0;
-  for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) s_pool[i] = 0;
+  for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) {
+    s_pool[i] = 0;
+    s_lo[i] = ranges[i].lo;
+    s_scale[i] = ranges[i].scale;
+    s_bnd[i] = (spec.bound && spec.on[i]) ? int64_t(spec.bound[i]) : int64_t(-1);
+  }
+  if (kSmemTables)
+    for (int i = threadIdx.x; i < op.n_agents; i += blockDim.x)
+      s_ag[i] = (static_cast<uint32_t>(a.pool[i]) << 16) | class_of(a, op.policy, i);
   __syncthreads();
   const uint32_t qmax = q_max(op);
   int32_t cur_pool = -1;
@@ -467,15 +485,32 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
       err |= 2;
       t = 0.0;
     }
-    const int32_t p = a.pool[ag];
-    const uint32_t key = compact_key(a, op, ranges[p], p, ag, t, qmax);
+    int32_t p;
+    uint32_t cls;
+    if (kSmemTables) {
+      const uint32_t pc = s_ag[ag];
+      p = static_cast<int32_t>(pc >> 16);
+      cls = pc & 0xFFFFu;
+    } else {
+      p = a.pool[ag];
+      cls = class_of(a, op.policy, ag);
+    }
+    // monotone quantisation (see compact_key)
+    const double x = __dmul_rn(__dsub_rn(t, s_lo[p]), s_scale[p]);
+    uint32_t qv;
+    if (!(x > 0.0)) qv = 0;
+    else if (x >= static_cast<double>(qmax)) qv = qmax;
+    else qv = static_cast<uint32_t>(x);
+    uint32_t key = qv;
+    if (op.class_bits) key |= cls << op.q_bits;
+    if (op.pool_bits) key |= static_cast<uint32_t>(p) << (op.class_bits + op.q_bits);
     if (p != cur_pool) {
       if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
       cur_pool = p;
       cur_cnt = 0;
     }
     ++cur_cnt;
-    if (spec.bound && spec.on[p] && key <= spec.bound[p]) {  // dispatch-prefix candidate
+    if (int64_t(key) <= s_bnd[p]) {  // dispatch-prefix candidate
       const uint32_t slot = atomicAdd(&spec.count[p], 1u);
       if (slot < kTopKMax) {
         spec.cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(idx);
@@ -1234,9 +1269,17 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   if (hooks && hooks->before_keygen) hooks->before_keygen();
   // reads agent + primary time (12 B), writes the compact key (4 B)
   P.begin("keygen_hist", N * 16.0, st);
-  k_keygen<<<grid, 256, sizeof(uint32_t) * op.n_pools, st>>>(q, a, op, n, ws.ranges, ws.keys[0],
-                                                              ws.hist, ws.pool_counts, ws.error_flags,
-                                                              hooks ? hooks->spec : KeygenSpec{});
+  {
+    const size_t dyn = size_t(op.n_pools) * (8 + 8 + 8 + 4);
+    const KeygenSpec sp = hooks ? hooks->spec : KeygenSpec{};
+    // class ranks must fit 16 bits for the packed shared table
+    if (op.n_agents <= kKeygenAgents && op.class_bits <= 16 && op.n_pools <= 65536)
+      k_keygen<true><<<grid, 256, dyn, st>>>(q, a, op, n, ws.ranges, ws.keys[0], ws.hist,
+                                             ws.pool_counts, ws.error_flags, sp);
+    else
+      k_keygen<false><<<grid, 256, dyn, st>>>(q, a, op, n, ws.ranges, ws.keys[0], ws.hist,
+                                              ws.pool_counts, ws.error_flags, sp);
+  }
   KX_CHECK_LAUNCH();
   P.end(st);
   k_scan_hist<<<1, 32 * passes, 0, st>>>(ws.hist, passes);
@@ -1309,7 +1352,8 @@ void configure_sort_kernels() {
   preload(k_range_finalize);
   preload(k_sample_keys);
   preload(k_spec_bound);
-  preload(k_keygen);
+  preload(k_keygen<true>);
+  preload(k_keygen<false>);
   preload(k_pool_offsets);
   preload(k_tie_runs);
   preload(k_tie_fix_small);
