@@ -324,6 +324,16 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
                         const uint8_t* present, int32_t scope_all, uint64_t* pairs,
                         double* correct, double* accuracy);
 
+/* ---- priority table: W1 distance matrix ------------------------------------ */
+/* Replaces build_distance_matrix_from_samples (priority.cpp:60-65) ->
+ * build_matrix (priority.cpp:15-46): samples holds each agent's sorted sample
+ * set back to back (offsets[0..n_agents]); out receives the (n_agents + 1)^2
+ * row-major matrix whose last label is the anchor (a single sample 0.0),
+ * d[i][j] = wasserstein_1d (distribution.cpp:9-31), bit-identical. Errors as
+ * the reference: no agents / an empty set -> KX_ERR_INVALID. Host pointers.
+ * The 1-D classical MDS of the matrix (priority.cpp:67-112) stays on the host. */
+int kx_w1_matrix(int32_t n_agents, const int64_t* offsets, const double* samples, double* out);
+
 /* ---- workload synthesis (host) ------------------------------------------ */
 /* realize() (workload.cpp:319-372) for the built-in templates
  * (workload.cpp:462-560); app_mask selects QA/RG/CG in that order

@@ -788,6 +788,53 @@ void gen_accuracy(const std::string& dir) {
 
 }  // namespace
 
+// W1 distance matrix (priority.cpp:15-65): per-agent sorted sample sets of
+// varied sizes (singletons, ties, a large set), the reference's
+// build_distance_matrix_from_samples over them (agents named so the map
+// order is the index order; the anchor {0.0} is the last label).
+void gen_w1matrix(const std::string& dir) {
+  Rng rng(4242);
+  Kxf k;
+  std::vector<int64_t> set_off{0}, case_off{0}, mat_off{0};
+  std::vector<double> samples, mat;
+  const int sizes[][6] = {{1, 1, 1, 0, 0, 0}, {3, 7, 1, 12, 0, 0}, {64, 200, 33, 5, 400, 17},
+                          {1000, 999, 1, 2, 3, 4096}};
+  for (int c = 0; c < 6; ++c) {
+    std::map<AgentId, std::vector<double>> sets;
+    const int na = c < 4 ? 6 : (c == 4 ? 9 : 14);
+    for (int a = 0; a < na; ++a) {
+      int sz = c < 4 ? sizes[c][a] : 1 + static_cast<int>(rng.next_u64() % 300);
+      if (sz == 0) continue;
+      std::vector<double> v;
+      for (int j = 0; j < sz; ++j) {
+        // mix of continuous values and heavy ties (the reference's remaining
+        // times often repeat)
+        const double x = (j % 3 == 0) ? std::floor(rng.uniform(0.0, 8.0)) : rng.uniform(0.0, 30.0);
+        v.push_back(x);
+      }
+      std::sort(v.begin(), v.end());
+      char name[16];
+      std::snprintf(name, sizeof(name), "a%02d", a);
+      sets[name] = v;
+    }
+    for (const auto& [nm, v] : sets) {
+      samples.insert(samples.end(), v.begin(), v.end());
+      set_off.push_back(static_cast<int64_t>(samples.size()));
+    }
+    case_off.push_back(static_cast<int64_t>(set_off.size() - 1));
+    const DistanceMatrix m = build_distance_matrix_from_samples(sets);
+    for (const auto& row : m.d) mat.insert(mat.end(), row.begin(), row.end());
+    mat_off.push_back(static_cast<int64_t>(mat.size()));
+  }
+  k.i64("set_offsets", set_off);
+  k.i64("case_sets", case_off);
+  k.f64("samples", samples);
+  k.i64("matrix_offsets", mat_off);
+  k.f64("matrix", mat);
+  k.write(dir + "/w1_matrix.kxf");
+  std::printf("  w1_matrix.kxf\n");
+}
+
 int main(int argc, char** argv) {
   const std::string dir = argc > 1 ? argv[1] : "tests/golden";
   std::filesystem::create_directories(dir);
@@ -814,5 +861,6 @@ int main(int argc, char** argv) {
   }
   gen_remaining(dir);
   gen_accuracy(dir);
+  gen_w1matrix(dir);
   return 0;
 }

@@ -7,7 +7,7 @@ the tests and bench.py.
 """
 from ._abi import KxError, LIB_PATH, load  # noqa: F401
 from .sched import (DeviceScheduler, DispatcherConfig, InstanceProfile,  # noqa: F401
-                    orchestrator_dp, record_remaining)
+                    orchestrator_dp, record_remaining, w1_matrix)
 
 __all__ = ["KxError", "LIB_PATH", "load", "DeviceScheduler", "DispatcherConfig",
-           "InstanceProfile", "orchestrator_dp", "record_remaining"]
+           "InstanceProfile", "orchestrator_dp", "record_remaining", "w1_matrix"]

@@ -21,6 +21,8 @@
 #include "kx_state.cuh"
 
 namespace kx {
+void launch_w1_matrix(int32_t n_agents, const int64_t* off, const double* samples, double* d, int sms,
+                      cudaStream_t st);
 std::atomic<long long> g_kx_launches{0};
 void sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining, const uint8_t* present,
                       int32_t scope_all, uint64_t* pairs_out, double* correct_out, int sms,
@@ -1603,6 +1605,43 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
     if (pairs) *pairs = p;
     if (correct) *correct = c;
     if (accuracy) *accuracy = p ? c / static_cast<double>(p) : std::nan("");
+  });
+}
+
+int kx_w1_matrix(int32_t n_agents, const int64_t* offsets, const double* samples, double* out) {
+  return guard([&] {
+    require(n_agents >= 0, "negative agent count");
+    require(offsets && out, "null argument");
+    // build_matrix's checks (priority.cpp:17-27): no agents, empty set
+    if (n_agents == 0) fail(KX_ERR_INVALID, "no converged agent distributions");
+    require(offsets[0] == 0, "offsets must start at 0");
+    for (int32_t a = 0; a < n_agents; ++a)
+      if (offsets[a + 1] <= offsets[a]) fail(KX_ERR_INVALID, "empty distribution for agent " + std::to_string(a));
+    const int64_t ns = offsets[n_agents];
+    require(ns == 0 || samples, "null samples");
+    ensure_device(0);
+    int dev = 0;
+    KX_CUDA(cudaGetDevice(&dev));
+    cudaStream_t st = nullptr;
+    KX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    const int64_t m = int64_t(n_agents) + 1;
+    int64_t* d_off = nullptr;
+    double *d_s = nullptr, *d_m = nullptr;
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_off), size_t(m) * 8, st));
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_s), size_t(std::max<int64_t>(ns, 1)) * 8, st));
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_m), size_t(m * m) * 8, st));
+    KX_CUDA(cudaMemcpyAsync(d_off, offsets, size_t(m) * 8, cudaMemcpyHostToDevice, st));
+    if (ns) KX_CUDA(cudaMemcpyAsync(d_s, samples, size_t(ns) * 8, cudaMemcpyHostToDevice, st));
+    launch_w1_matrix(n_agents, d_off, d_s, d_m, sm_count(dev), st);
+    KX_CUDA(cudaMemcpyAsync(out, d_m, size_t(m * m) * 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaFreeAsync(d_off, st));
+    KX_CUDA(cudaFreeAsync(d_s, st));
+    KX_CUDA(cudaFreeAsync(d_m, st));
+    KX_CUDA(cudaStreamSynchronize(st));
   });
 }
 

@@ -289,3 +289,19 @@ def sorting_accuracy(agent, remaining, present=None, scope="cross_agent"):
     check(lib.kx_sorting_accuracy(len(a), ptr(a), ptr(r), ptr(pr), 1 if scope == "all" else 0,
                                   C.byref(pairs), C.byref(correct), C.byref(acc)))
     return (None if pairs.value == 0 else acc.value), pairs.value, correct.value
+
+
+def w1_matrix(sample_sets):
+    """§8(f)2: build_distance_matrix_from_samples (priority.cpp:15-65) on the
+    device. sample_sets: per-agent sorted sample arrays in label order; returns
+    the (n + 1) x (n + 1) matrix with the anchor {0.0} as the last label,
+    bit-identical to the reference."""
+    lib = _abi.load()
+    sets = [np.ascontiguousarray(x, np.float64) for x in sample_sets]
+    off = np.zeros(len(sets) + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in sets]) if sets else []
+    flat = np.concatenate(sets) if sets else np.zeros(0)
+    m = len(sets) + 1
+    out = np.zeros((m, m), np.float64)
+    check(lib.kx_w1_matrix(len(sets), ptr(off), ptr(flat), ptr(out)))
+    return out
