@@ -737,7 +737,10 @@ void tick_impl(kx_sched* s, double now) {
     s->prof.end(s->side);
     KX_CUDA(cudaEventRecord(s->ev_disp, s->side));
   };
-  s->order = launch_order(s->q, s->a, op, s->n, s->ws, s->sms, s->stream, &s->prof, &hooks);
+  // the dispatch CTAs hold one SM per pool while the sort runs: size the
+  // sort's grid-stride launches for the rest (no partial second wave)
+  const int sort_sms = std::max(1, s->sms - s->n_pools);
+  s->order = launch_order(s->q, s->a, op, s->n, s->ws, sort_sms, s->stream, &s->prof, &hooks);
   s->order_valid = true;
   s->order_n = s->n;
   KX_CUDA(cudaStreamWaitEvent(s->stream, s->ev_disp, 0));
