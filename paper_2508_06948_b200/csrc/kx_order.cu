@@ -17,6 +17,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "kx_common.cuh"
 #include "kx_order.cuh"
@@ -1216,6 +1218,12 @@ void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin
 }
 
 // ---- host orchestration --------------------------------------------------
+// Warp ranking per radix pass (kx_sort.cuh kRank), chosen by measurement
+// on the C4 keys (profiles/r01_sort_rank.md): MATCH.ANY with a leader
+// broadcast for the spread low digits, ballots for the top
+// digit (few distinct values).
+constexpr int kSortRankDefault[4] = {2, 2, 2, 1};
+
 size_t order_lookback_bytes(int64_t cap) {
   const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
   return size_t(tiles) * kRadix * sizeof(uint32_t);
@@ -1295,9 +1303,21 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     KX_CUDA(cudaMemsetAsync(ws.lookback, 0, size_t(tiles) * kRadix * sizeof(uint32_t), st));
     // key (4 B) [+ index (4 B) after the first pass] in, key + index out
     P.begin("radix_pass", N * (p == 0 ? 12.0 : 16.0), st);
-    k_onesweep_pass<uint32_t><<<static_cast<unsigned>(tiles), kSortThreads, smem, st>>>(
-        ws.keys[cur], ws.keys[cur ^ 1], p == 0 ? nullptr : ws.vals[cur], ws.vals[cur ^ 1], n,
-        p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+    {
+      static const char* variants = getenv("KX_SORT_RANK");  // experiment knob, per pass
+      const int v = (variants && int(strlen(variants)) > p) ? variants[p] - '0' : kSortRankDefault[p < 4 ? p : 3];
+      const uint32_t* vin = p == 0 ? nullptr : ws.vals[cur];
+      const unsigned g = static_cast<unsigned>(tiles);
+      if (v == 1)
+        k_onesweep_pass<uint32_t, 1><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+      else if (v == 2)
+        k_onesweep_pass<uint32_t, 2><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+      else
+        k_onesweep_pass<uint32_t, 0><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+    }
     KX_CHECK_LAUNCH();
     P.end(st);
     cur ^= 1;
@@ -1359,13 +1379,16 @@ void configure_sort_kernels() {
   preload(k_tie_fix_small);
   preload(k_tie_fix_big);
   preload(k_init_ranges);
-  preload(k_onesweep_pass<uint32_t>);
+  preload(k_onesweep_pass<uint32_t, 0>);
+  preload(k_onesweep_pass<uint32_t, 1>);
+  preload(k_onesweep_pass<uint32_t, 2>);
   KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(uint32_t) * kSpecMax)));
   KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(topk_sort_smem())));
-  KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sort_dyn_smem<uint32_t>())));
+  for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>})
+    KX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sort_dyn_smem<uint32_t>())));
 }
 
 }  // namespace kx

@@ -45,6 +45,20 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Lanes holding the same 8-bit digit: eight ballots instead of MATCH.ANY
+// (MATCH issues through the MIO pipe at a fraction of the ballot rate and
+// was the top stall of the ranking loop).
+__device__ __forceinline__ uint32_t warp_match8(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t vote = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? vote : ~vote;
+  }
+  return peers;
+}
+
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return static_cast<uint32_t>(key >> shift) & (kRadix - 1);
@@ -103,7 +117,10 @@ constexpr size_t sort_dyn_smem() {
 
 // One stable LSD digit pass. vals_in == nullptr means "value = element index"
 // (first pass). global_excl: this pass's exclusive digit offsets.
-template <typename K>
+// kRank selects the warp ranking: 0 = MATCH.ANY peers, every peer reads the
+// running count; 1 = eight-ballot peers, same update; 2 = MATCH.ANY peers,
+// the leader reads and broadcasts the count.
+template <typename K, int kRank = 0>
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
@@ -149,15 +166,24 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = digit_of(key[i], shift);
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader) {
-      old = wh[d];
-      wh[d] = old + __popc(peers);
+    const uint32_t peers = kRank == 1 ? warp_match8(d) : __match_any_sync(0xffffffffu, d);
+    if (kRank == 2) {
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        old = wh[d];
+        wh[d] = old + __popc(peers);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rank[i] = old + __popc(peers & lanemask_lt());
+    } else {
+      // every peer reads the running count (broadcast), the lowest one bumps it
+      const uint32_t old = wh[d];
+      __syncwarp();
+      if ((peers & lanemask_lt()) == 0) wh[d] = old + __popc(peers);
+      __syncwarp();
+      rank[i] = old + __popc(peers & lanemask_lt());
     }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    rank[i] = old + __popc(peers & lanemask_lt());
   }
   __syncthreads();
 
