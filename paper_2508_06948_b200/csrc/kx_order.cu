@@ -1329,9 +1329,11 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
 
   const int tgrid = static_cast<int>(std::min<int64_t>((n / 4 + 256) / 256, int64_t(sms) * 8));
   // reads the sorted keys (4 B); tie runs gather their exact tuples
-  P.begin("tie_fix", N * 4.0, st);
+  P.begin("tie_runs", N * 4.0, st);
   k_tie_runs<<<tgrid, 256, 0, st>>>(res.keys, n, ws.small_starts, ws.n_small, ws.tie_cap);
   KX_CHECK_LAUNCH();
+  P.end(st);
+  P.begin("tie_fix", 0.0, st);
   k_tie_fix_small<<<sms * 8, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
                                            ws.n_small, ws.big_starts, ws.big_lens, ws.n_big,
                                            ws.tie_cap);
