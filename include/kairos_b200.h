@@ -324,6 +324,13 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
                         const uint8_t* present, int32_t scope_all, uint64_t* pairs,
                         double* correct, double* accuracy);
 
+/* ---- CUDA graph of a repeated step (e.g. kx_state_restore + kx_tick) ------ */
+/* Calls between begin and end are captured (asynchronous calls only: no
+ * fetches, profiling off) and replayed by kx_graph_launch with one launch. */
+int kx_graph_capture_begin(kx_sched* s);
+int kx_graph_capture_end(kx_sched* s);
+int kx_graph_launch(kx_sched* s);
+
 /* ---- priority table: W1 distance matrix ------------------------------------ */
 /* Replaces build_distance_matrix_from_samples (priority.cpp:60-65) ->
  * build_matrix (priority.cpp:15-46): samples holds each agent's sorted sample

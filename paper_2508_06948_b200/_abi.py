@@ -143,6 +143,9 @@ SIGNATURES = {
                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "kx_aggregate_metrics": (C.c_int, [C.c_int32, _P, _P]),
     "kx_w1_matrix": (C.c_int, [C.c_int32, _P, _P, _P]),
+    "kx_graph_capture_begin": (C.c_int, [_P]),
+    "kx_graph_capture_end": (C.c_int, [_P]),
+    "kx_graph_launch": (C.c_int, [_P]),
     "kx_builtin_agent_name": (C.c_char_p, [C.c_int32]),
     "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                      C.c_double, C.POINTER(_P)]),

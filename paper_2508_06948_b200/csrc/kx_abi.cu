@@ -246,6 +246,8 @@ struct kx_sched {
   // `side` while the full sort runs on `stream`.
   bool overlap = false;
   cudaStream_t side = nullptr;
+  cudaGraph_t graph = nullptr;          // captured step (kx_graph_*)
+  cudaGraphExec_t graph_exec = nullptr;
   cudaEvent_t ev_keys = nullptr, ev_released = nullptr, ev_disp = nullptr;
   Blob topk_blob;
   TopKWork topk{};
@@ -567,6 +569,8 @@ void destroy_impl(kx_sched* s) {
   free_blob(s->topk_blob);
   for (cudaEvent_t e : {s->ev_keys, s->ev_released, s->ev_disp})
     if (e) cudaEventDestroy(e);
+  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
   if (s->rem_table) cudaFree(s->rem_table);
   if (s->rem_present) cudaFree(s->rem_present);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -1549,6 +1553,47 @@ int kx_state_restore(kx_sched* s) {
     KX_CUDA(cudaSetDevice(s->device));
     KX_CUDA(cudaMemcpyAsync(s->inst_mut_blob.base, s->inst_ckpt_blob.base, s->inst_mut_blob.size,
                             cudaMemcpyDeviceToDevice, s->stream));
+  });
+}
+
+// CUDA graph of a repeated step: every call between begin and end (on this
+// handle, from this thread) is captured from the handle's stream, including
+// the side stream's overlapped dispatch, and kx_graph_launch replays it with
+// one launch. The captured calls must be asynchronous (no fetches, no
+// profiling); the graph is valid while the queue size and handle state
+// shapes stay the same.
+int kx_graph_capture_begin(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    if (s->prof.enabled) throw std::logic_error("disable profiling before capturing a graph");
+    if (s->graph_exec) {
+      cudaGraphExecDestroy(s->graph_exec);
+      s->graph_exec = nullptr;
+    }
+    if (s->graph) {
+      cudaGraphDestroy(s->graph);
+      s->graph = nullptr;
+    }
+    KX_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int kx_graph_capture_end(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    KX_CUDA(cudaStreamEndCapture(s->stream, &s->graph));
+    KX_CUDA(cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+  });
+}
+
+int kx_graph_launch(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->graph_exec) throw std::logic_error("no captured graph");
+    KX_CUDA(cudaSetDevice(s->device));
+    KX_CUDA(cudaGraphLaunch(s->graph_exec, s->stream));
   });
 }
 

@@ -240,6 +240,17 @@ class DeviceScheduler:
         return {arr[i].name.decode(): {"ms": arr[i].total_ms, "launches": arr[i].launches,
                                        "alg_bytes": arr[i].alg_bytes} for i in range(n.value)}
 
+    def capture_begin(self):
+        """Start capturing this handle's asynchronous calls into a CUDA graph."""
+        check(self.lib.kx_graph_capture_begin(self.h))
+
+    def capture_end(self):
+        check(self.lib.kx_graph_capture_end(self.h))
+
+    def graph_launch(self):
+        """Replay the captured calls (one launch)."""
+        check(self.lib.kx_graph_launch(self.h))
+
     def checkpoint(self):
         check(self.lib.kx_state_checkpoint(self.h))
 

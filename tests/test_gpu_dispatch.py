@@ -198,3 +198,33 @@ def test_checkpoint_restore_replays_identically(gpu_lib, monkeypatch, mode):
     b = s.fetch_dispatch()[0]
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_graph_replay_matches_direct_tick(gpu_lib):
+    # kx_graph_*: the captured step (restore + tick) replays the same kernels
+    rng = np.random.default_rng(17)
+    inst = build_pools(rng, 3, 8)
+    s = kx.DeviceScheduler(inst, n_pools=3, queue_capacity=20000, max_agents=32)
+    q, t = random_queue(rng, 20000, n_agents=20, n_pools=3)
+    s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
+    s.set_scheduler("kairos")
+    s.upload(q.agent, q.prompt, q.app_start, q.queue_enter, q.msg_key, q.uid)
+    s.checkpoint()
+    s.restore()
+    s.tick(3.0)
+    ref_rows, ref_cand = s.fetch_dispatch()
+    ref_perm, ref_offs = s.fetch_order()
+    s.capture_begin()
+    s.restore()
+    s.tick(3.0)
+    s.capture_end()
+    for _ in range(3):
+        s.graph_launch()
+        s.synchronize()
+        rows, cand = s.fetch_dispatch()
+        perm, offs = s.fetch_order()
+        assert np.array_equal(perm, ref_perm) and np.array_equal(offs, ref_offs)
+        for a, b in zip(rows, ref_rows):
+            assert np.array_equal(a, b)
+        for a, b in zip(cand, ref_cand):
+            assert np.array_equal(bits(a), bits(b))
