@@ -1815,13 +1815,19 @@ struct StageMeta {
   int32_t target;    // lane of the target, -1 none
   int32_t admitted;
   int32_t act_slot;  // active-table slot of an admission (-1 none)
-  double peak;       // predicted peak of the decision
+};
+
+// One instance's try_place result for a staged decision (one 16-byte store).
+struct __align__(16) StageRow {
+  uint32_t viol;
+  uint32_t flag;
+  uint64_t peak;
 };
 
 struct BatchLayout {
   uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
-      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_viol, g_peak, g_flag,
-      c_key, c_idx, usage, ex, total;
+      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, g_meta, g_row, c_key, c_idx,
+      usage, ex, total;
 };
 
 BatchLayout batch_layout(int ring) {
@@ -1852,9 +1858,7 @@ BatchLayout batch_layout(int ring) {
   L.r_peak = take(8 * 32 * kBatchEval);
   L.r_flag = take(4 * 32 * kBatchEval);
   L.g_meta = take(sizeof(StageMeta) * 2 * kStage);
-  L.g_viol = take(size_t(4) * 32 * 2 * kStage);
-  L.g_peak = take(size_t(8) * 32 * 2 * kStage);
-  L.g_flag = take(size_t(1) * 32 * 2 * kStage);
+  L.g_row = take(sizeof(StageRow) * 32 * 2 * kStage);
   L.c_key = take(size_t(8) * kTopKMax);
   L.c_idx = take(size_t(4) * kTopKMax);
   L.usage = take(size_t(8) * 32 * ring);
@@ -2001,9 +2005,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   uint64_t* const r_peak = BL(uint64_t, r_peak);
   uint32_t* const r_flag = BL(uint32_t, r_flag);
   StageMeta* const g_meta = BL(StageMeta, g_meta);
-  uint32_t* const g_viol = BL(uint32_t, g_viol);
-  uint64_t* const g_peak = BL(uint64_t, g_peak);
-  uint8_t* const g_flag = BL(uint8_t, g_flag);
+  StageRow* const g_row = BL(StageRow, g_row);
 #undef BL
   const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
   constexpr uint32_t kNone = 0xffffffffu;
@@ -2255,10 +2257,12 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       const int64_t row = row0 + r;
       if (row < dp.log_cap) {
         const int64_t ro = int64_t(pool) * dp.log_cap + row;
+        const StageRow w = g_row[g * 32 + lane];
+        const uint64_t wpeak = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(w.peak), m.target >= 0 ? m.target : 0);
         if (lane == 0) {
           kx_decision d;
           d.time = now;
-          d.predicted_peak = m.peak;
+          d.predicted_peak = m.target >= 0 ? from_ordered_bits(wpeak) : 0.0;
           d.uid = h_uid[m.hs];
           d.queue_index = h_idx[m.hs];
           d.agent = h_agent[m.hs];
@@ -2268,12 +2272,10 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           rows[ro] = d;
         }
         if (act) {
-          const uint8_t f = g_flag[g * 32 + lane];
-          const uint32_t v = g_viol[g * 32 + lane];
           double c = -1.0;
-          if (f & 1u)
-            c = v == kNone ? from_ordered_bits(g_peak[g * 32 + lane])
-                           : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(v)), 1.0);
+          if (w.flag & 1u)
+            c = w.viol == kNone ? from_ordered_bits(w.peak)
+                                : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(w.viol)), 1.0);
           cand[ro * dp.peak_stride + li] = c;
         }
       }
@@ -2316,6 +2318,19 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   int32_t hi_off = static_cast<int32_t>(hi0 - B);
   int32_t nact = act ? in.n_active[i] : 0;
   uint64_t umax = kZeroBits;  // max stored usage over the whole ledger window
+  int64_t pend_last = -1;     // slots [cslot, pend_last] booked since umax was folded
+  // Bring umax up to date with the slots booked by this lane's commits.
+  auto fold_pending = [&]() {
+    if (pend_last >= cslot) {
+      int p2 = static_cast<int>(cslot & rmask);
+      for (int64_t s2 = cslot; s2 <= pend_last; ++s2) {
+        const uint64_t tb = ordered_bits(su[p2 * kRow + lane]);
+        umax = tb > umax ? tb : umax;
+        p2 = (p2 + 1) & rmask;
+      }
+      pend_last = -1;
+    }
+  };
   if (warp == 0) {
     for (int32_t o = lo_off; o <= hi_off; ++o) {
       const int p2 = static_cast<int>((B + o) & rmask);
@@ -2401,37 +2416,59 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
               flg = el ? 1u : 0u;
               if (el) {
                 if (first < base || last >= base + ring) flg |= 2u;
-                peak = umax;
+                // span slots (every span starts at cslot) fold the pending
+                // commits into umax on the way; the rest of them after
+                // (usage and pk are >= 0: double max orders like the bits)
+                const int np = pend_last >= cslot ? static_cast<int>(pend_last - cslot + 1) : 0;
+                double um = __longlong_as_double(static_cast<long long>(umax & ~kZeroBits));
+                double pk_max = 0.0;
                 int p2 = pbase;
 #pragma unroll 4
                 for (int jj = 0; jj < tn; ++jj) {
-                  const double total = __dadd_rn(su[p2 * kRow + lane], tab[jj]);
+                  const double u = su[p2 * kRow + lane];
+                  const double total = __dadd_rn(u, tab[jj]);
                   if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + jj);
-                  const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-                  peak = tb > peak ? tb : peak;
+                  pk_max = fmax(pk_max, total);
+                  if (jj < np) um = fmax(um, u);
                   p2 = (p2 + 1) & rmask;
                 }
+                for (int jj = tn; jj < np; ++jj) {
+                  um = fmax(um, su[p2 * kRow + lane]);
+                  p2 = (p2 + 1) & rmask;
+                }
+                umax = static_cast<uint64_t>(__double_as_longlong(um)) | kZeroBits;
+                pend_last = -1;
+                peak = static_cast<uint64_t>(__double_as_longlong(fmax(um, pk_max))) | kZeroBits;
               }
             } else {
+              fold_pending();
               const Row r = evaluate(hs, live, running, susp, umax, hi_off);
               viol = r.viol;
               peak = r.peak;
               flg = r.flag;
             }
           }
-          if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
-            status = KX_ERR_CAPACITY;
-            broke = true;
-            break;
-          }
           unsigned long long tq1 = dbg ? clock64() : 0;
           if (dbg) acc_fix += tq1 - tq0;
           const bool fits = (flg & 1u) && viol == kNone;
           // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
-          const uint64_t key = fits ? peak : ~0ull;
-          const uint64_t wkey = warp_min_u64(key);
-          const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
+          // Min of the high words first (peaks have the top bit set, so 0
+          // flags a ring overflow); the low words only on a tie there.
+          const uint32_t khi = (flg & 2u) ? 0u : fits ? static_cast<uint32_t>(peak >> 32) : 0xffffffffu;
           const uint32_t ovm = __ballot_sync(0xffffffffu, fits && __dadd_rn(live, P) > cap);  // engine.cpp:254-258
+          const uint32_t fullm = __ballot_sync(0xffffffffu, nact >= kActiveCap);
+          const uint32_t hmin = __reduce_min_sync(0xffffffffu, khi);
+          if (hmin == 0u) {
+            status = KX_ERR_CAPACITY;
+            broke = true;
+            break;
+          }
+          uint32_t winners = __ballot_sync(0xffffffffu, fits && khi == hmin);
+          if (winners & (winners - 1)) {
+            const uint32_t klo = ((winners >> lane) & 1u) ? static_cast<uint32_t>(peak) : 0xffffffffu;
+            const uint32_t lmin = __reduce_min_sync(0xffffffffu, klo);
+            winners = __ballot_sync(0xffffffffu, ((winners >> lane) & 1u) && static_cast<uint32_t>(peak) == lmin);
+          }
           const int bl = winners ? __ffs(winners) - 1 : -1;
           const bool overload = bl >= 0 && ((ovm >> bl) & 1u);
           unsigned long long tq2 = dbg ? clock64() + (bl & 0) : 0;
@@ -2446,12 +2483,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           }
           {
             const int g = sbuf * kStage + ns;
-            if (lane == 0)
-              g_meta[g] = StageMeta{hs, bl, (bl >= 0 && !overload) ? 1 : 0, -1,
-                                    bl >= 0 ? from_ordered_bits(wkey) : 0.0};
-            g_viol[g * 32 + lane] = viol;
-            g_peak[g * 32 + lane] = peak;
-            g_flag[g * 32 + lane] = static_cast<uint8_t>(flg);
+            if (lane == 0) g_meta[g] = StageMeta{hs, bl, (bl >= 0 && !overload) ? 1 : 0, -1};
+            g_row[g * 32 + lane] = StageRow{viol, flg, peak};
           }
           unsigned long long tq3 = dbg ? clock64() : 0;
           if (dbg) acc_stg += tq3 - tq2;
@@ -2480,18 +2513,15 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           // slots, raise its maximum stored usage, admit (engine.cpp:298-319).
           const double T = h_T[hs];
           if (mode == kModeTabPk && tn <= 32) {
-            // the common shape: lanes = span slots, one pass; the target's
-            // new maximum stored usage is a warp max of the booked slots
-            uint64_t tb = kZeroBits;
+            // the common shape: lanes = span slots, one pass; the target
+            // folds the booked slots into its maximum stored usage when it
+            // next needs it (pend_last)
             if (lane < tn) {
               const int p2 = (pbase + lane) & rmask;
-              const double nu = __dadd_rn(su[p2 * kRow + bl], tab[lane]);
-              su[p2 * kRow + bl] = nu;
+              su[p2 * kRow + bl] = __dadd_rn(su[p2 * kRow + bl], tab[lane]);
               se[p2 * kRow + bl] = 1;
-              tb = static_cast<uint64_t>(__double_as_longlong(nu)) | kZeroBits;
             }
-            const uint64_t nb = warp_max_u64(tb);
-            if (lane == bl) umax = nb > umax ? nb : umax;
+            if (lane == bl) pend_last = last > pend_last ? last : pend_last;
             __syncwarp();  // the target's lane reads these slots next
           } else if (lane == bl) {
             if (mode != kModeGeneric) {  // usage + pk >= 0: raw bits order
@@ -2529,15 +2559,12 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             st_live[lane] = live;
             st_run[lane] = running;
             st_hi[lane] = hi_off;
-            st_umax[lane] = umax;
             if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78), written at flush
               g_meta[sbuf * kStage + ns - 1].act_slot = nact;
               ++nact;
-            } else {
-              status = KX_ERR_CAPACITY;
             }
           }
-          if (__any_sync(0xffffffffu, status != KX_OK)) {
+          if ((fullm >> bl) & 1u) {  // the target's active table was full
             status = KX_ERR_CAPACITY;
             broke = true;
             break;
@@ -2549,6 +2576,8 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           break;
         }
       }
+      fold_pending();
+      st_umax[lane] = umax;  // the next batch's evaluators read it
       if (lane == 0) {
         s_nstage[sbuf] = ns;
         s_next = pos;
