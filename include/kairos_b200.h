@@ -184,6 +184,38 @@ int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
 /* One scheduling tick: kx_order + kx_dispatch_round (asynchronous). */
 int kx_tick(kx_sched* s, double now);
 
+/* ---- waiting lists: round_robin / static_threshold (engine.cpp:259-296) ---
+ * Under KX_DISPATCH_ROUND_ROBIN and KX_DISPATCH_STATIC_THRESHOLD a dispatch
+ * round pops each placed head into its target instance's waiting list
+ * (engine.cpp:259-262) and runs try_admit on it (engine.cpp:270-296); after
+ * the loop every instance runs try_admit once more (engine.cpp:211). The
+ * waiting lists are device-resident between rounds. In those rounds a
+ * decision row's `admitted` = 1 means "popped into the target's waiting
+ * list", predicted_peak is 0.0 and no candidate peaks are logged (the
+ * reference's DispatchDecision carries none), and every admission out of a
+ * waiting list is logged as a kx_admission row. */
+typedef struct kx_admission {
+  double time;
+  uint64_t uid;
+  int64_t queue_index;            /* index in this round's queue, -1 = entered an earlier round */
+  int32_t instance;               /* InstanceId */
+  int32_t pool;
+} kx_admission;
+/* Entries per instance waiting list (default 1024; grows on upload). */
+int kx_waiting_reserve(kx_sched* s, int64_t per_instance);
+/* Replaces every waiting list: entry j joins the list of the instance at
+ * position instance_pos[j] (kx_sched_config.instances order), appended in
+ * array order. Host memory only. Also sets the instances' waiting counts. */
+int kx_waiting_upload(kx_sched* s, int64_t n, const int32_t* instance_pos, const kx_queue_view* q);
+/* uid[] of the waiting list of the instance at position instance_pos, in
+ * list order (at most cap entries copied; *n_out = list length). */
+int kx_waiting_fetch(kx_sched* s, int32_t instance_pos, int64_t cap, uint64_t* uid, int64_t* n_out);
+/* Admission log of the last round: per_pool_count[n_pools]; rows pool-major
+ * with *row_stride rows per pool (= the decision-log capacity). */
+int kx_admissions_fetch(kx_sched* s, int64_t* per_pool_count, kx_admission* rows, int64_t* row_stride);
+/* Dispatcher::rr_next_ per pool (dispatcher.hpp:174): get and/or set (either may be NULL). */
+int kx_rr_next(kx_sched* s, int64_t* get_per_pool, const int64_t* set_per_pool);
+
 /* ---- instance / ledger state (dispatcher.cpp:44-123, 264-297) ---------- */
 /* Engine-side live view (engine.cpp:187-202): live_kv, running, waiting,
  * indexed by position in the kx_sched_config.instances array. */

@@ -567,6 +567,207 @@ void gen_dispatch(const std::string& dir, const std::string& name, uint64_t seed
   std::printf("  %s: %d instances, %d rounds\n", name.c_str(), n_inst, rounds);
 }
 
+// ---- dispatch under RoundRobin / StaticThreshold: waiting lists ---------------
+// The dispatch_loop restatement above with the non-TimeSlot branch
+// (engine.cpp:259-262) and Simulator::try_admit (engine.cpp:270-296)
+// restated over the reference's own Dispatcher, ReadyQueue and
+// TopoDepthScheduler (whose waiting comparator (order_key, msg_id, uid)
+// differs from the queue order when depth and queue_enter tie).
+void gen_dispatch_waiting(const std::string& dir, const std::string& name, uint64_t seed,
+                          DispatchPolicy policy, int n_inst, int max_batch, double cap, int rounds,
+                          int per_round, double prompt_hi) {
+  Rng rng(seed);
+  DispatcherConfig dcfg;
+  dcfg.policy = policy;
+  std::vector<InstanceId> ids;
+  std::vector<double> caps, ks;
+  for (int i = 0; i < n_inst; ++i) {
+    ids.push_back(7 + 5 * i);
+    caps.push_back(cap * (i % 3 == 1 ? 0.7 : 1.0));
+    ks.push_back(50.0);
+  }
+  Dispatcher disp(dcfg, ids, caps, ks);
+  Names names;
+  const int A = 4;
+  std::map<AgentId, int> depths;
+  for (int a = 0; a < A; ++a) {
+    names.agent("w" + std::to_string(a));
+    if (a != 3) depths["w" + std::to_string(a)] = 1 + (a % 2);  // w3: unknown -> depth 1
+  }
+  TopoDepthScheduler sched(depths);
+  auto key = [&](const PendingRequest& r) { return sched.order_key(r); };
+  std::vector<int32_t> depth_arr;
+  for (int a = 0; a < A; ++a) {
+    auto it = depths.find("w" + std::to_string(a));
+    depth_arr.push_back(it == depths.end() ? 1 : it->second);
+  }
+  // every request of every round up front: one msg-key space for all of them
+  std::vector<std::vector<PendingRequest>> arrivals(rounds);
+  std::vector<std::string> all_msgs;
+  uint64_t next_uid = 1;
+  double now = 2.0;
+  std::vector<double> nows;
+  for (int r = 0; r < rounds; ++r) {
+    nows.push_back(now);
+    for (int j = 0; j < per_round; ++j) {
+      const int a = static_cast<int>(rng.next_u64() % A);
+      // coarse times: queue_enter ties across apps, app_start decides the
+      // queue order, msg_id the waiting order
+      const std::string msg = "m-" + std::to_string(1 + rng.next_u64() % (3 * per_round));
+      PendingRequest p = req(msg, "w" + std::to_string(a), now - 0.125 * double(rng.next_u64() % 16),
+                             now - 0.25 * double(rng.next_u64() % 4), next_uid++,
+                             1 + static_cast<int64_t>(rng.next_u64() % static_cast<uint64_t>(prompt_hi)));
+      arrivals[r].push_back(p);
+      all_msgs.push_back(msg);
+    }
+    now += rng.uniform(0.2, 1.0);
+  }
+  std::sort(all_msgs.begin(), all_msgs.end());
+  all_msgs.erase(std::unique(all_msgs.begin(), all_msgs.end()), all_msgs.end());
+  auto mkey = [&](const std::string& m) {
+    return static_cast<uint64_t>(std::lower_bound(all_msgs.begin(), all_msgs.end(), m) - all_msgs.begin());
+  };
+  auto put_reqs = [&](Kxf& k, const std::vector<PendingRequest>& q, const std::string& pre) {
+    std::vector<int32_t> agent;
+    std::vector<int64_t> prompt;
+    std::vector<double> app, qe;
+    std::vector<uint64_t> uid, msg;
+    for (const auto& r : q) {
+      agent.push_back(names.agent(r.agent));
+      prompt.push_back(r.prompt_tokens);
+      app.push_back(r.app_start);
+      qe.push_back(r.queue_enter);
+      uid.push_back(r.uid);
+      msg.push_back(mkey(r.msg_id));
+    }
+    k.i32(pre + "agent", agent);
+    k.i64(pre + "prompt", prompt);
+    k.f64(pre + "app_start", app);
+    k.f64(pre + "queue_enter", qe);
+    k.u64(pre + "msg_key", msg);
+    k.u64(pre + "uid", uid);
+  };
+
+  Kxf k;
+  k.scalar_i("n_inst", n_inst);
+  k.scalar_i("policy", static_cast<int64_t>(policy));
+  k.i32("inst_id", std::vector<int32_t>(ids.begin(), ids.end()));
+  k.f64("inst_cap", caps);
+  k.f64("inst_k", ks);
+  k.i32("inst_max_batch", std::vector<int32_t>(n_inst, max_batch));
+  k.i32("agent_depth", depth_arr);
+
+  std::vector<double> live(n_inst, 0.0);
+  std::vector<int> running(n_inst, 0);
+  std::vector<std::vector<PendingRequest>> waiting(n_inst);
+  struct Run {
+    int inst;
+    int64_t kv;
+  };
+  std::vector<Run> runs;
+  std::vector<PendingRequest> queue;
+  auto put_waiting = [&](const std::string& pre) {
+    std::vector<PendingRequest> flat;
+    std::vector<int32_t> pos;
+    for (int i = 0; i < n_inst; ++i)
+      for (const auto& r : waiting[i]) {
+        flat.push_back(r);
+        pos.push_back(i);
+      }
+    put_reqs(k, flat, pre);
+    k.i32(pre + "inst", pos);
+  };
+  for (int r = 0; r < rounds; ++r) {
+    const std::string R = "r" + std::to_string(r) + ".";
+    now = nows[r];
+    for (const auto& p : arrivals[r]) queue.push_back(p);
+    k.scalar_f(R + "now", now);
+    k.f64(R + "live_kv", live);
+    k.i32(R + "running", std::vector<int32_t>(running.begin(), running.end()));
+    put_waiting(R + "w.");
+    put_reqs(k, queue, R + "q.");
+    std::vector<uint64_t> dec_uid, adm_uid;
+    std::vector<int32_t> dec_target, dec_admitted, adm_inst;
+    auto try_admit = [&](int i) {  // engine.cpp:270-296
+      while (!waiting[i].empty() && running[i] < max_batch) {
+        std::size_t best = 0;
+        for (std::size_t j = 1; j < waiting[i].size(); ++j) {
+          const auto& a = waiting[i][j];
+          const auto& b = waiting[i][best];
+          const auto ka = key(a);
+          const auto kb = key(b);
+          if (std::tie(ka, a.msg_id, a.uid) < std::tie(kb, b.msg_id, b.uid)) best = j;
+        }
+        const PendingRequest& head = waiting[i][best];
+        if (live[i] + static_cast<double>(head.prompt_tokens) > caps[i]) break;
+        const PendingRequest h = head;
+        waiting[i].erase(waiting[i].begin() + static_cast<std::ptrdiff_t>(best));
+        live[i] += static_cast<double>(h.prompt_tokens);  // kept_tokens = 0
+        running[i] += 1;
+        runs.push_back({i, h.prompt_tokens});
+        adm_uid.push_back(h.uid);
+        adm_inst.push_back(ids[i]);
+      }
+    };
+    ReadyQueue rq;
+    for (const auto& p : queue) rq.enqueue(p);
+    while (!rq.empty()) {
+      const std::size_t idx = rq.best_index(key);
+      const PendingRequest head = rq.entries()[idx];
+      std::vector<InstanceLive> lv;
+      for (int i = 0; i < n_inst; ++i) {
+        disp.on_live_usage(ids[i], live[i]);
+        InstanceLive l;
+        l.live_kv = live[i];
+        l.running = running[i];
+        l.waiting = static_cast<int>(waiting[i].size());
+        l.batch_full = l.running + l.waiting >= max_batch;
+        lv.push_back(l);
+      }
+      DispatchDecision d = disp.choose(head, now, 1.0, lv);
+      dec_uid.push_back(head.uid);
+      dec_target.push_back(d.target ? *d.target : -1);
+      dec_admitted.push_back(d.target ? 1 : 0);
+      if (!d.target) break;
+      const int ti = static_cast<int>(std::find(ids.begin(), ids.end(), *d.target) - ids.begin());
+      PendingRequest popped = rq.pop(key);
+      waiting[ti].push_back(popped);
+      try_admit(ti);
+    }
+    for (int i = 0; i < n_inst; ++i) try_admit(i);
+    disp.gc(now);
+    k.u64(R + "dec_uid", dec_uid);
+    k.i32(R + "dec_target", dec_target);
+    k.i32(R + "dec_admitted", dec_admitted);
+    k.u64(R + "adm_uid", adm_uid);
+    k.i32(R + "adm_inst", adm_inst);
+    k.f64(R + "end_live_kv", live);
+    k.i32(R + "end_running", std::vector<int32_t>(running.begin(), running.end()));
+    put_waiting(R + "end_w.");
+    // the queue keeps what was not popped
+    std::set<uint64_t> gone;
+    for (std::size_t j = 0; j < dec_uid.size(); ++j)
+      if (dec_admitted[j]) gone.insert(dec_uid[j]);
+    std::vector<PendingRequest> rest;
+    for (const auto& p : queue)
+      if (!gone.count(p.uid)) rest.push_back(p);
+    queue = rest;
+    // some running requests finish before the next round (engine side)
+    std::vector<Run> still;
+    for (const auto& x : runs) {
+      if (rng.uniform() < 0.5) {
+        live[x.inst] -= static_cast<double>(x.kv);
+        running[x.inst] -= 1;
+      } else {
+        still.push_back(x);
+      }
+    }
+    runs = still;
+  }
+  k.write(dir + "/" + name);
+  std::printf("  %s: %d instances, %d rounds\n", name.c_str(), n_inst, rounds);
+}
+
 // ---- K1: realize() / finalize_instance ---------------------------------------
 AppSpec fan_app(int width) {
   // Parallel fan-out + choice + feedback: exercises multi-child max.
@@ -843,6 +1044,9 @@ int main(int argc, char** argv) {
   gen_dispatch(dir, "dispatch_small.kxf", 11, 4, 8, 3000.0, 6, 40, 450.0, false);
   gen_dispatch(dir, "dispatch_preload.kxf", 12, 16, 6, 3000.0, 8, 120, 400.0, true);
   gen_dispatch(dir, "dispatch_overload.kxf", 13, 5, 64, 1000.0, 5, 80, 150.0, false);
+  gen_dispatch_waiting(dir, "dispatch_rr.kxf", 21, DispatchPolicy::RoundRobin, 5, 4, 2000.0, 6, 30, 600.0);
+  gen_dispatch_waiting(dir, "dispatch_static.kxf", 22, DispatchPolicy::StaticThreshold, 6, 4, 2000.0, 6, 40,
+                       1100.0);
   gen_dp(dir, "dp_colocated.kxf", colocated_workload(3.0, 400.0, 3), ReferenceRates{8000.0, 50.0}, 3);
   gen_dp(dir, "dp_cg.kxf", cg_workload(2.0, 300.0, 11), ReferenceRates{6000.0, 40.0}, 11);
   {

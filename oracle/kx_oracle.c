@@ -466,6 +466,138 @@ int64_t kxo_dispatch_round(kxo_pool* p, const kxo_queue* q, const kxo_tables* t,
   return nrows;
 }
 
+/* ---- dispatch round, RoundRobin / StaticThreshold (engine.cpp:220-296) ------ */
+
+/* SchedulerPolicy::order_key of a waiting entry (scheduler.hpp:48-113). */
+static void wkey_of(int policy, const kxo_tables* t, const kxo_waitrec* r, double* k) {
+  switch (policy) {
+    case KXO_KAIROS: k[0] = t->pk[r->agent]; k[1] = r->app_start; k[2] = r->queue_enter; break;
+    case KXO_FCFS: k[0] = r->queue_enter; k[1] = r->app_start; k[2] = 0.0; break;
+    case KXO_TOPO: k[0] = (double)t->depth[r->agent]; k[1] = r->queue_enter; k[2] = 0.0; break;
+    default: k[0] = rem_of(t, r->uid); k[1] = r->queue_enter; k[2] = 0.0; break;
+  }
+}
+
+/* std::tie(key(a), a.msg_id, a.uid) < std::tie(key(b), ...) (engine.cpp:280-283) */
+static int wless(int policy, const kxo_tables* t, const kxo_waitrec* a, const kxo_waitrec* b) {
+  double ka[3], kb[3];
+  wkey_of(policy, t, a, ka);
+  wkey_of(policy, t, b, kb);
+  for (int j = 0; j < 3; ++j)
+    if (ka[j] != kb[j]) return ka[j] < kb[j];
+  if (a->msg != b->msg) return a->msg < b->msg;
+  return a->uid < b->uid;
+}
+
+typedef struct {
+  kxo_pool* p;
+  int sched_policy;
+  const kxo_tables* t;
+  kxo_waitrec* wrec;
+  int64_t wcap;
+  int32_t round;
+  double now;
+  int32_t pool_index;
+  kxo_admission* adm;
+  int64_t adm_cap;
+  int64_t n_adm;
+} wctx;
+
+/* Simulator::try_admit (engine.cpp:270-296), admit (298-319) bookkeeping. */
+static void try_admit_o(wctx* c, int32_t i) {
+  kxo_pool* p = c->p;
+  kxo_waitrec* L = c->wrec + (int64_t)i * c->wcap;
+  while (p->waiting[i] > 0 && p->running[i] < p->max_batch[i]) {
+    int64_t best = 0;
+    for (int64_t j = 1; j < p->waiting[i]; ++j)
+      if (wless(c->sched_policy, c->t, &L[j], &L[best])) best = j;
+    const kxo_waitrec h = L[best];
+    if (p->live_kv[i] + (double)h.prompt > p->cap[i]) break; /* head waits for memory */
+    memmove(L + best, L + best + 1, (size_t)(p->waiting[i] - best - 1) * sizeof(kxo_waitrec));
+    p->waiting[i] -= 1;
+    p->live_kv[i] += (double)(h.prompt + h.kept);
+    p->running[i] += 1;
+    if (c->n_adm < c->adm_cap) {
+      kxo_admission* a = &c->adm[c->n_adm];
+      a->time = c->now;
+      a->uid = h.uid;
+      a->queue_index = h.round == c->round ? h.qidx : -1;
+      a->instance = p->id[i];
+      a->pool = c->pool_index;
+    }
+    c->n_adm += 1;
+  }
+}
+
+int64_t kxo_dispatch_round_waiting(kxo_pool* p, int dispatch_policy, double static_thr, int sched_policy,
+                                   int64_t* rr_next, kxo_waitrec* wrec, int64_t wcap, int32_t round,
+                                   const kxo_queue* q, const kxo_tables* t, const uint32_t* perm,
+                                   int64_t m, double now, int32_t pool_index, kxo_decision* rows,
+                                   int64_t row_cap, kxo_admission* adm, int64_t adm_cap, int64_t* n_adm,
+                                   int32_t* status) {
+  const int32_t ni = p->n_inst;
+  wctx c = {p, sched_policy, t, wrec, wcap, round, now, pool_index, adm, adm_cap, 0};
+  int64_t nrows = 0;
+  *status = 0;
+  for (int64_t pos = 0; pos < m; ++pos) {
+    const uint32_t idx = perm[pos];
+    /* collect_live (engine.cpp:187-202): on_live_usage per instance */
+    for (int32_t i = 0; i < ni; ++i)
+      if (p->suspended[i] && p->live_kv[i] < p->watermark * p->cap[i]) p->suspended[i] = 0;
+    int32_t target = -1;
+    if (dispatch_policy == 1) { /* RoundRobin, dispatcher.cpp:214-218 */
+      target = (int32_t)((uint64_t)*rr_next % (uint64_t)ni);
+      *rr_next += 1;
+    } else { /* StaticThreshold, dispatcher.cpp:219-231 */
+      for (int32_t probe = 0; probe < ni; ++probe) {
+        const int32_t i = (int32_t)(((uint64_t)*rr_next + (uint64_t)probe) % (uint64_t)ni);
+        const int full = p->running[i] + p->waiting[i] >= p->max_batch[i];
+        if (p->live_kv[i] < static_thr * p->cap[i] && !full) {
+          target = i;
+          *rr_next = i + 1;
+          break;
+        }
+      }
+    }
+    if (nrows < row_cap) {
+      kxo_decision* d = &rows[nrows];
+      d->time = now;
+      d->predicted_peak = 0.0;
+      d->uid = q->uid[idx];
+      d->queue_index = idx;
+      d->agent = q->agent[idx];
+      d->target = target >= 0 ? p->id[target] : -1;
+      d->pool = pool_index;
+      d->admitted = target >= 0 ? 1 : 0;
+    }
+    ++nrows;
+    if (target < 0) break; /* engine.cpp:247 */
+    if (p->waiting[target] >= wcap) {
+      *status = 5;
+      break;
+    }
+    /* pop; inst.waiting.push_back; try_admit (engine.cpp:259-262) */
+    kxo_waitrec r;
+    r.app_start = q->app_start[idx];
+    r.queue_enter = q->queue_enter[idx];
+    r.msg = q->msg_key[idx];
+    r.uid = q->uid[idx];
+    r.prompt = q->prompt[idx];
+    r.kept = q->kept ? q->kept[idx] : 0;
+    r.qidx = idx;
+    r.agent = q->agent[idx];
+    r.round = round;
+    wrec[(int64_t)target * wcap + p->waiting[target]] = r;
+    p->waiting[target] += 1;
+    try_admit_o(&c, target);
+  }
+  if (*status == 0)
+    for (int32_t i = 0; i < ni; ++i) try_admit_o(&c, i); /* engine.cpp:211 */
+  for (int32_t i = 0; i < ni; ++i) kxo_gc(p->ledgers[i], now); /* engine.cpp:212 */
+  *n_adm = c.n_adm;
+  return nrows;
+}
+
 /* ---- pairwise_sorting_accuracy (priority.cpp:165-189) ------------------------ */
 int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,
                           int32_t scope_all, double* acc, uint64_t* pairs_out) {

@@ -107,6 +107,34 @@ int64_t kxo_dispatch_round(kxo_pool* p, const kxo_queue* q, const kxo_tables* t,
                            const uint32_t* perm, int64_t m, double now, int32_t pool_index,
                            kxo_decision* rows, double* cand, int64_t row_cap, int32_t* status);
 
+/* One request in an instance's waiting list (InstanceState::waiting). */
+typedef struct kxo_waitrec {
+  double app_start, queue_enter;
+  uint64_t msg, uid;
+  int64_t prompt, kept, qidx;
+  int32_t agent, round;
+} kxo_waitrec;
+
+typedef struct kxo_admission {
+  double time;
+  uint64_t uid;
+  int64_t queue_index;
+  int32_t instance;
+  int32_t pool;
+} kxo_admission;
+
+/* dispatch_loop (engine.cpp:220-268) under RoundRobin / StaticThreshold
+ * (dispatcher.cpp:214-231): each head popped into the target's waiting list
+ * (p->waiting[i] entries at wrec + i * wcap) and try_admit (engine.cpp:270-296);
+ * then try_admit on every instance (engine.cpp:211) and gc. *rr_next is
+ * Dispatcher::rr_next_. Returns decision rows; *status: 0 ok, 5 capacity. */
+int64_t kxo_dispatch_round_waiting(kxo_pool* p, int dispatch_policy, double static_thr, int sched_policy,
+                                   int64_t* rr_next, kxo_waitrec* wrec, int64_t wcap, int32_t round,
+                                   const kxo_queue* q, const kxo_tables* t, const uint32_t* perm,
+                                   int64_t m, double now, int32_t pool_index, kxo_decision* rows,
+                                   int64_t row_cap, kxo_admission* adm, int64_t adm_cap, int64_t* n_adm,
+                                   int32_t* status);
+
 /* pairwise_sorting_accuracy (priority.cpp:165-189), O(N^2): returns 0 and
  * sets *acc when pairs > 0, returns 1 (nullopt) otherwise. */
 int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,

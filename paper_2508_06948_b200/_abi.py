@@ -119,6 +119,11 @@ SIGNATURES = {
     "kx_dispatch_round": (C.c_int, [_P, C.c_double]),
     "kx_dispatch_fetch": (C.c_int, [_P, _P, _P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "kx_tick": (C.c_int, [_P, C.c_double]),
+    "kx_waiting_reserve": (C.c_int, [_P, C.c_int64]),
+    "kx_waiting_upload": (C.c_int, [_P, C.c_int64, _P, C.POINTER(kx_queue_view)]),
+    "kx_waiting_fetch": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.POINTER(C.c_int64)]),
+    "kx_admissions_fetch": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64)]),
+    "kx_rr_next": (C.c_int, [_P, _P, _P]),
     "kx_instances_set_live": (C.c_int, [_P, _P, _P, _P]),
     "kx_instances_get_live": (C.c_int, [_P, _P, _P, _P, _P]),
     "kx_ledger_try_place": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,

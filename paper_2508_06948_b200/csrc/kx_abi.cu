@@ -252,6 +252,15 @@ struct kx_sched {
   Blob topk_blob;
   TopKWork topk{};
   DispResume* resume = nullptr;
+
+  // waiting lists (round_robin / static_threshold rounds)
+  WaitRec* wrec = nullptr;       // [n_inst * wcap]
+  int64_t wcap = 0;
+  kx_admission* adm = nullptr;   // [n_pools * log_cap]
+  int64_t* adm_count = nullptr;  // [n_pools]
+  int32_t round = 0;
+  WaitRec* wckpt = nullptr;      // checkpoint copy
+  int64_t wckpt_cap = 0;
 };
 
 namespace {
@@ -571,6 +580,10 @@ void destroy_impl(kx_sched* s) {
     if (e) cudaEventDestroy(e);
   if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
   if (s->graph) cudaGraphDestroy(s->graph);
+  if (s->wrec) cudaFree(s->wrec);
+  if (s->wckpt) cudaFree(s->wckpt);
+  if (s->adm) cudaFree(s->adm);
+  if (s->adm_count) cudaFree(s->adm_count);
   if (s->rem_table) cudaFree(s->rem_table);
   if (s->rem_present) cudaFree(s->rem_present);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -667,9 +680,46 @@ DispatchParams dispatch_params(const kx_sched* s, double now) {
 }
 
 void dispatch_checks(const kx_sched* s) {
-  if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT)
-    fail(KX_ERR_INVALID, "only the time_slot dispatch policy runs on the device in this build");
   require(s->n_agents > 0 || s->n == 0, "agent tables not set");
+}
+
+// Waiting-list storage: `per_inst` entries per instance (contents kept).
+void ensure_waiting(kx_sched* s, int64_t per_inst) {
+  if (!s->adm) {
+    const size_t P = static_cast<size_t>(s->n_pools);
+    KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->adm), std::max<size_t>(1, P * s->log_cap) * sizeof(kx_admission)));
+    KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->adm_count), std::max<size_t>(1, P) * 8));
+    KX_CUDA(cudaMemset(s->adm_count, 0, std::max<size_t>(1, P) * 8));
+  }
+  if (per_inst <= s->wcap) return;
+  const size_t I = static_cast<size_t>(s->n_inst);
+  WaitRec* nr = nullptr;
+  KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&nr), std::max<size_t>(1, I * per_inst) * sizeof(WaitRec)));
+  if (s->wrec) {
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    KX_CUDA(cudaMemcpy2D(nr, per_inst * sizeof(WaitRec), s->wrec, s->wcap * sizeof(WaitRec),
+                         s->wcap * sizeof(WaitRec), I, cudaMemcpyDeviceToDevice));
+    KX_CUDA(cudaFree(s->wrec));
+  }
+  s->wrec = nr;
+  s->wcap = per_inst;
+}
+
+WaitDev waiting_dev(kx_sched* s) {
+  WaitDev w{};
+  w.rec = s->wrec;
+  w.cap = s->wcap;
+  w.adm = s->adm;
+  w.adm_count = s->adm_count;
+  w.rem_table = s->rem_table;
+  w.rem_present = s->rem_present;
+  w.rem_base = s->rem_base;
+  w.rem_n = s->rem_table ? s->rem_n : 0;
+  w.static_thr = s->dcfg.static_threshold;
+  w.policy = s->dcfg.policy;
+  w.sched_kind = s->sched_kind;
+  w.round = s->round;
+  return w;
 }
 
 void dispatch_impl(kx_sched* s, double now) {
@@ -678,6 +728,17 @@ void dispatch_impl(kx_sched* s, double now) {
   dispatch_checks(s);
   if (s->n > 0) KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
   const DispatchParams dp = dispatch_params(s, now);
+  if (s->dcfg.policy != KX_DISPATCH_TIME_SLOT) {  // round_robin / static_threshold
+    ensure_waiting(s, 1024);
+    ++s->round;
+    s->prof.begin("dispatch", 0.0, s->stream);
+    launch_dispatch_waiting(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp,
+                            waiting_dev(s), s->n_pools, s->max_inst_per_pool, s->rows, s->row_count,
+                            s->admitted_count, s->pool_status, s->stream);
+    s->prof.end(s->stream);
+    s->dispatch_valid = true;
+    return;
+  }
   s->prof.begin("dispatch", 0.0, s->stream);
   launch_dispatch(s->q, s->a, s->in, s->pool_begin, s->order.perm, s->ws.pool_offsets, dp,
                   s->n_pools, s->max_inst_per_pool, s->rows, s->cand, s->row_count, s->admitted_count, s->pool_status,
@@ -695,7 +756,7 @@ void dispatch_impl(kx_sched* s, double now) {
 // decisions are identical to order + dispatch_round: the prefix is exactly
 // the head of the pool's order, and the round state carries over.
 void tick_impl(kx_sched* s, double now) {
-  if (!s->overlap || s->n == 0) {
+  if (!s->overlap || s->n == 0 || s->dcfg.policy != KX_DISPATCH_TIME_SLOT) {
     order_impl(s);
     dispatch_impl(s, now);
     return;
@@ -1326,7 +1387,7 @@ int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
                                   ": overload/resume livelock (reference would spin forever)");
       if (status[p] == KX_ERR_CAPACITY)
         fail(KX_ERR_CAPACITY, "pool " + std::to_string(p) +
-                                  ": slot ring or active-request table capacity exceeded");
+                                  ": slot ring, active-request table or waiting-list capacity exceeded");
       if (status[p] != KX_OK) fail(status[p], "pool " + std::to_string(p) + ": dispatch failed");
       if (cnt[p] > s->log_cap && (rows || candidate_peaks))
         fail(KX_ERR_CAPACITY, "decision log truncated (raise log_capacity_per_pool)");
@@ -1340,6 +1401,123 @@ int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
                               P * s->log_cap * s->max_inst_per_pool * sizeof(double),
                               cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_waiting_reserve(kx_sched* s, int64_t per_instance) {
+  return guard([&] {
+    require(s, "null handle");
+    require(per_instance >= 0, "negative waiting-list capacity");
+    KX_CUDA(cudaSetDevice(s->device));
+    ensure_waiting(s, per_instance);
+  });
+}
+
+int kx_waiting_upload(kx_sched* s, int64_t n, const int32_t* instance_pos, const kx_queue_view* v) {
+  return guard([&] {
+    require(s, "null handle");
+    require(n >= 0, "negative count");
+    KX_CUDA(cudaSetDevice(s->device));
+    std::vector<int32_t> cnt(static_cast<size_t>(s->n_inst), 0);
+    if (n > 0) {
+      require(instance_pos && v && v->agent && v->prompt_tokens && v->app_start && v->queue_enter &&
+                  v->msg_key && v->uid,
+              "waiting view is missing a required array");
+      for (int64_t j = 0; j < n; ++j) {
+        require(instance_pos[j] >= 0 && instance_pos[j] < s->n_inst, "instance position out of range");
+        require(v->agent[j] >= 0 && v->agent[j] < std::max(s->n_agents, 1), "agent index out of range");
+        require(v->app_start[j] == v->app_start[j] && v->queue_enter[j] == v->queue_enter[j], "NaN time");
+        ++cnt[static_cast<size_t>(instance_pos[j])];
+      }
+    }
+    const int64_t need = cnt.empty() ? 0 : *std::max_element(cnt.begin(), cnt.end());
+    ensure_waiting(s, std::max<int64_t>(need, 1024));
+    const size_t I = static_cast<size_t>(s->n_inst);
+    std::vector<WaitRec> h(I * static_cast<size_t>(s->wcap));
+    std::vector<int32_t> fill(I, 0);
+    for (int64_t j = 0; j < n; ++j) {
+      const size_t i = static_cast<size_t>(instance_pos[j]);
+      WaitRec r{};
+      r.app_start = v->app_start[j];
+      r.queue_enter = v->queue_enter[j];
+      r.msg = v->msg_key[j];
+      r.uid = v->uid[j];
+      r.prompt = v->prompt_tokens[j];
+      r.kept = v->kept_tokens ? v->kept_tokens[j] : 0;
+      r.qidx = -1;
+      r.agent = v->agent[j];
+      r.round = -1;  // not from a dispatch round
+      h[i * static_cast<size_t>(s->wcap) + static_cast<size_t>(fill[i]++)] = r;
+    }
+    KX_CUDA(cudaMemcpyAsync(s->wrec, h.data(), h.size() * sizeof(WaitRec), cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->in.waiting, cnt.data(), I * 4, cudaMemcpyHostToDevice, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_waiting_fetch(kx_sched* s, int32_t instance_pos, int64_t cap, uint64_t* uid, int64_t* n_out) {
+  return guard([&] {
+    require(s, "null handle");
+    require(instance_pos >= 0 && instance_pos < s->n_inst, "instance position out of range");
+    KX_CUDA(cudaSetDevice(s->device));
+    int32_t n = 0;
+    KX_CUDA(cudaMemcpyAsync(&n, s->in.waiting + instance_pos, 4, cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (n_out) *n_out = n;
+    const int64_t m = std::min<int64_t>(n, cap);
+    if (!uid || m <= 0) return;
+    require(s->wrec != nullptr && n <= s->wcap, "waiting list storage missing");
+    std::vector<WaitRec> h(static_cast<size_t>(m));
+    KX_CUDA(cudaMemcpyAsync(h.data(), s->wrec + int64_t(instance_pos) * s->wcap, size_t(m) * sizeof(WaitRec),
+                            cudaMemcpyDeviceToHost, s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    for (int64_t j = 0; j < m; ++j) uid[j] = h[static_cast<size_t>(j)].uid;
+  });
+}
+
+int kx_admissions_fetch(kx_sched* s, int64_t* per_pool_count, kx_admission* rows, int64_t* row_stride) {
+  return guard([&] {
+    require(s, "null handle");
+    if (!s->dispatch_valid) throw std::logic_error("no dispatch round to fetch");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t P = static_cast<size_t>(s->n_pools);
+    if (row_stride) *row_stride = s->log_cap;
+    std::vector<int64_t> cnt(P, 0);
+    if (s->adm_count && s->dcfg.policy != KX_DISPATCH_TIME_SLOT) {
+      KX_CUDA(cudaMemcpyAsync(cnt.data(), s->adm_count, P * 8, cudaMemcpyDeviceToHost, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    for (size_t p = 0; p < P; ++p)
+      if (cnt[p] > s->log_cap && rows)
+        fail(KX_ERR_CAPACITY, "admission log truncated (raise log_capacity_per_pool)");
+    if (per_pool_count) std::memcpy(per_pool_count, cnt.data(), P * 8);
+    if (rows && s->adm)
+      KX_CUDA(cudaMemcpyAsync(rows, s->adm, P * s->log_cap * sizeof(kx_admission), cudaMemcpyDeviceToHost,
+                              s->stream));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int kx_rr_next(kx_sched* s, int64_t* get_per_pool, const int64_t* set_per_pool) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    const size_t P = static_cast<size_t>(s->n_pools);
+    std::vector<int32_t> v(P);
+    if (get_per_pool) {
+      KX_CUDA(cudaMemcpyAsync(v.data(), s->in.rr_next, P * 4, cudaMemcpyDeviceToHost, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+      for (size_t p = 0; p < P; ++p) get_per_pool[p] = v[p];
+    }
+    if (set_per_pool) {
+      for (size_t p = 0; p < P; ++p) {
+        const int64_t np = s->pool_begin_host[p + 1] - s->pool_begin_host[p];
+        require(set_per_pool[p] >= 0, "negative rr_next");
+        v[p] = static_cast<int32_t>(np > 0 ? set_per_pool[p] % np : 0);
+      }
+      KX_CUDA(cudaMemcpyAsync(s->in.rr_next, v.data(), P * 4, cudaMemcpyHostToDevice, s->stream));
+      KX_CUDA(cudaStreamSynchronize(s->stream));
+    }
   });
 }
 
@@ -1541,6 +1719,15 @@ int kx_state_checkpoint(kx_sched* s) {
     if (!s->inst_ckpt_blob.base) alloc_blob(s->inst_ckpt_blob, s->inst_mut_blob.size);
     KX_CUDA(cudaMemcpyAsync(s->inst_ckpt_blob.base, s->inst_mut_blob.base, s->inst_mut_blob.size,
                             cudaMemcpyDeviceToDevice, s->stream));
+    // waiting-list contents go with their counts
+    if (s->wrec && s->wckpt_cap != s->wcap) {
+      if (s->wckpt) KX_CUDA(cudaFree(s->wckpt));
+      KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->wckpt), size_t(s->n_inst) * s->wcap * sizeof(WaitRec)));
+      s->wckpt_cap = s->wcap;
+    }
+    if (s->wrec)
+      KX_CUDA(cudaMemcpyAsync(s->wckpt, s->wrec, size_t(s->n_inst) * s->wcap * sizeof(WaitRec),
+                              cudaMemcpyDeviceToDevice, s->stream));
     KX_CUDA(cudaStreamSynchronize(s->stream));
     s->have_ckpt = true;
   });
@@ -1553,6 +1740,9 @@ int kx_state_restore(kx_sched* s) {
     KX_CUDA(cudaSetDevice(s->device));
     KX_CUDA(cudaMemcpyAsync(s->inst_mut_blob.base, s->inst_ckpt_blob.base, s->inst_mut_blob.size,
                             cudaMemcpyDeviceToDevice, s->stream));
+    if (s->wrec && s->wckpt_cap == s->wcap)
+      KX_CUDA(cudaMemcpyAsync(s->wrec, s->wckpt, size_t(s->n_inst) * s->wcap * sizeof(WaitRec),
+                              cudaMemcpyDeviceToDevice, s->stream));
   });
 }
 

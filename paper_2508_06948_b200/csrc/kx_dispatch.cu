@@ -2763,6 +2763,254 @@ __global__ void k_gc_all(InstDev in, int n_inst, int ring, double now, double sl
   }
 }
 
+// ---- K5w: round_robin / static_threshold round with waiting lists --------
+// One warp per pool walks the pool's order: Dispatcher::choose for RR
+// (dispatcher.cpp:214-218) or StaticThreshold (219-231), the head popped into
+// the target's waiting list (engine.cpp:259-262) and try_admit on it
+// (engine.cpp:270-296); after the walk try_admit on every instance
+// (engine.cpp:211) and Dispatcher::gc. Lane-parallel parts: the collect_live
+// resume over instances, the static probe (a warp min over probe offsets),
+// the waiting-list arg-min and the erase shift. try_admit keeps each list's
+// arg-min position cached between a memory-blocked check and the next
+// change of the list (a push compares against it; an erase drops it).
+namespace {
+
+struct WKey {
+  double k0, k1, k2;
+  uint64_t msg, uid;
+};
+
+__device__ __forceinline__ WKey wait_key(const WaitRec& r, const AgentsDev& a, const WaitDev& w) {
+  WKey k;
+  k.k2 = 0.0;
+  switch (w.sched_kind) {  // SchedulerPolicy::order_key (scheduler.hpp:48-113)
+    case KX_SCHED_KAIROS: k.k0 = a.pk[r.agent]; k.k1 = r.app_start; k.k2 = r.queue_enter; break;
+    case KX_SCHED_FCFS: k.k0 = r.queue_enter; k.k1 = r.app_start; break;
+    case KX_SCHED_TOPO: k.k0 = static_cast<double>(a.depth[r.agent]); k.k1 = r.queue_enter; break;
+    default: {  // OracleScheduler: remaining_by_uid lookup, absent -> 0.0 (scheduler.hpp:85-89)
+      double rem = 0.0;
+      if (w.rem_table && r.uid >= w.rem_base && r.uid - w.rem_base < static_cast<uint64_t>(w.rem_n) &&
+          w.rem_present[r.uid - w.rem_base])
+        rem = w.rem_table[r.uid - w.rem_base];
+      k.k0 = rem;
+      k.k1 = r.queue_enter;
+    }
+  }
+  k.msg = r.msg;
+  k.uid = r.uid;
+  return k;
+}
+
+// try_admit's comparator: std::tie(order_key, msg_id, uid) < (engine.cpp:280-283).
+__device__ __forceinline__ bool wkey_less(const WKey& a, const WKey& b) {
+  if (a.k0 != b.k0) return a.k0 < b.k0;
+  if (a.k1 != b.k1) return a.k1 < b.k1;
+  if (a.k2 != b.k2) return a.k2 < b.k2;
+  if (a.msg != b.msg) return a.msg < b.msg;
+  return a.uid < b.uid;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(32)
+k_dispatch_waiting(QueueDev q, AgentsDev a, InstDev in, const int32_t* __restrict__ pool_begin,
+                   const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
+                   DispatchParams dp, WaitDev w, kx_decision* __restrict__ rows,
+                   int64_t* __restrict__ row_count, int64_t* __restrict__ admitted_count,
+                   int* __restrict__ pool_status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int pool = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int ib = pool_begin[pool];
+  const int ni = pool_begin[pool + 1] - ib;
+  double* s_live = reinterpret_cast<double*>(smem_raw);
+  double* s_cap = s_live + ni;
+  int32_t* s_run = reinterpret_cast<int32_t*>(s_cap + ni);
+  int32_t* s_wait = s_run + ni;
+  int32_t* s_mb = s_wait + ni;
+  int32_t* s_id = s_mb + ni;
+  int64_t* s_wmin = reinterpret_cast<int64_t*>(smem_raw + ((size_t(ni) * 32 + 15) & ~size_t(15)));
+  uint8_t* s_susp = reinterpret_cast<uint8_t*>(s_wmin + ni);
+  for (int li = lane; li < ni; li += 32) {
+    s_live[li] = in.live_kv[ib + li];
+    s_cap[li] = in.cap[ib + li];
+    s_run[li] = in.running[ib + li];
+    s_wait[li] = in.waiting[ib + li];
+    s_mb[li] = in.max_batch[ib + li];
+    s_id[li] = in.id[ib + li];
+    s_susp[li] = in.suspended[ib + li];
+    s_wmin[li] = -1;
+  }
+  __syncwarp();
+  const double now = dp.now;
+  int64_t rr = in.rr_next[pool];
+  int64_t nrows = 0, npop = 0, nadm = 0;
+  int status = ni > 0 ? KX_OK : KX_ERR_INVALID;
+
+  // Arg-min of instance li's waiting list under wkey_less (uid is unique, so
+  // the minimum is unique: list order never decides).
+  auto argmin = [&](int li) -> int64_t {
+    const WaitRec* L = w.rec + int64_t(ib + li) * w.cap;
+    const int64_t n = s_wait[li];
+    int64_t bp = -1;
+    WKey bk{};
+    for (int64_t j = lane; j < n; j += 32) {
+      const WKey k = wait_key(L[j], a, w);
+      if (bp < 0 || wkey_less(k, bk)) {
+        bk = k;
+        bp = j;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      WKey ok;
+      ok.k0 = __shfl_xor_sync(0xffffffffu, bk.k0, o);
+      ok.k1 = __shfl_xor_sync(0xffffffffu, bk.k1, o);
+      ok.k2 = __shfl_xor_sync(0xffffffffu, bk.k2, o);
+      ok.msg = __shfl_xor_sync(0xffffffffu, bk.msg, o);
+      ok.uid = __shfl_xor_sync(0xffffffffu, bk.uid, o);
+      const int64_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (op >= 0 && (bp < 0 || wkey_less(ok, bk))) {
+        bk = ok;
+        bp = op;
+      }
+    }
+    return bp;
+  };
+  // Simulator::try_admit (engine.cpp:270-296) + admit's live/running update (298-319).
+  auto try_admit = [&](int li) {
+    WaitRec* L = w.rec + int64_t(ib + li) * w.cap;
+    while (s_wait[li] > 0 && s_run[li] < s_mb[li]) {
+      int64_t pos = s_wmin[li];
+      if (pos < 0) pos = argmin(li);
+      const WaitRec h = L[pos];
+      if (__dadd_rn(s_live[li], static_cast<double>(h.prompt)) > s_cap[li]) {
+        __syncwarp();
+        if (lane == 0) s_wmin[li] = pos;  // strict admission order: the head waits for memory
+        __syncwarp();
+        return;
+      }
+      const int64_t n = s_wait[li];
+      for (int64_t b = pos + 1; b < n; b += 32) {  // erase, keeping list order
+        const int64_t j = b + lane;
+        WaitRec t;
+        if (j < n) t = L[j];
+        __syncwarp();
+        if (j < n) L[j - 1] = t;
+        __syncwarp();
+      }
+      if (lane == 0) {
+        s_wait[li] = static_cast<int32_t>(n - 1);
+        s_wmin[li] = -1;
+        s_live[li] = __dadd_rn(s_live[li], static_cast<double>(h.prompt + h.kept));
+        s_run[li] += 1;
+        if (nadm < dp.log_cap) {
+          kx_admission r;
+          r.time = now;
+          r.uid = h.uid;
+          r.queue_index = h.round == w.round ? h.qidx : -1;
+          r.instance = s_id[li];
+          r.pool = pool;
+          w.adm[int64_t(pool) * dp.log_cap + nadm] = r;
+        }
+      }
+      ++nadm;
+      __syncwarp();
+    }
+  };
+
+  const int64_t b0 = pool_offsets[pool], e0 = pool_offsets[pool + 1];
+  for (int64_t pos = b0; pos < e0 && status == KX_OK; ++pos) {
+    const uint32_t idx = perm[pos];
+    // collect_live: Dispatcher::on_live_usage per instance (engine.cpp:191)
+    for (int li = lane; li < ni; li += 32)
+      if (s_susp[li] && s_live[li] < __dmul_rn(dp.watermark, s_cap[li])) s_susp[li] = 0;
+    int t = -1;
+    if (w.policy == KX_DISPATCH_ROUND_ROBIN) {
+      t = static_cast<int>(rr % ni);
+      ++rr;
+    } else {  // first probe from rr_next_ below the threshold and not batch-full
+      int best = INT32_MAX;
+      for (int probe = lane; probe < ni; probe += 32) {
+        const int i = static_cast<int>((rr + probe) % ni);
+        const bool full = s_run[i] + s_wait[i] >= s_mb[i];
+        if (s_live[i] < __dmul_rn(w.static_thr, s_cap[i]) && !full) best = probe < best ? probe : best;
+      }
+      best = __reduce_min_sync(0xffffffffu, best);
+      if (best != INT32_MAX) {
+        t = static_cast<int>((rr + best) % ni);
+        rr = t + 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
+      kx_decision d;
+      d.time = now;
+      d.predicted_peak = 0.0;
+      d.uid = q.uid[idx];
+      d.queue_index = idx;
+      d.agent = q.agent[idx];
+      d.target = t >= 0 ? s_id[t] : -1;
+      d.pool = pool;
+      d.admitted = t >= 0 ? 1 : 0;
+      rows[int64_t(pool) * dp.log_cap + nrows] = d;
+    }
+    ++nrows;
+    if (t < 0) break;  // engine.cpp:247
+    if (s_wait[t] >= w.cap) {
+      status = KX_ERR_CAPACITY;
+      break;
+    }
+    if (lane == 0) {  // ReadyQueue::pop; inst.waiting.push_back (engine.cpp:260-261)
+      WaitRec r;
+      r.app_start = q.app_start[idx];
+      r.queue_enter = q.queue_enter[idx];
+      r.msg = q.msg[idx];
+      r.uid = q.uid[idx];
+      r.prompt = q.prompt[idx];
+      r.kept = q.kept[idx];
+      r.qidx = idx;
+      r.agent = q.agent[idx];
+      r.round = w.round;
+      WaitRec* L = w.rec + int64_t(ib + t) * w.cap;
+      const int64_t n = s_wait[t];
+      L[n] = r;
+      q.admitted[idx] = 1;
+      const int64_t m = s_wmin[t];
+      if (m >= 0 && wkey_less(wait_key(r, a, w), wait_key(L[m], a, w))) s_wmin[t] = n;
+      s_wait[t] = static_cast<int32_t>(n + 1);
+    }
+    ++npop;
+    __syncwarp();
+    try_admit(t);
+  }
+  if (status == KX_OK)
+    for (int li = 0; li < ni; ++li) try_admit(li);  // engine.cpp:211
+  // Dispatcher::gc (engine.cpp:212)
+  for (int li = 0; li < ni; ++li) {
+    Ring r = global_ring(in, ib + li, dp.ring);
+    warp_gc_slots(r, dp.ring, now, dp.slot_len);
+    if (lane == 0) {
+      in.base_slot[ib + li] = r.base;
+      active_gc(in, ib + li, now);
+    }
+  }
+  __syncwarp();
+  for (int li = lane; li < ni; li += 32) {
+    in.live_kv[ib + li] = s_live[li];
+    in.running[ib + li] = s_run[li];
+    in.waiting[ib + li] = s_wait[li];
+    in.suspended[ib + li] = s_susp[li];
+  }
+  if (lane == 0) {
+    // only rr mod n is ever used (RR: ids_[rr % n]; static: (rr + probe) % n)
+    in.rr_next[pool] = static_cast<int32_t>(ni > 0 ? rr % ni : 0);
+    row_count[pool] = nrows;
+    admitted_count[pool] = npop;
+    w.adm_count[pool] = nadm;
+    pool_status[pool] = status;
+  }
+}
+
 // ---- host wrappers -------------------------------------------------------
 void read_dispatch_debug(unsigned long long* out) {
   KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_dbg, sizeof(unsigned long long) * 16));
@@ -2772,6 +3020,7 @@ void configure_dispatch_kernels() {
   cudaFuncAttributes attr;  // load eagerly (see configure_sort_kernels)
   KX_CUDA(cudaFuncGetAttributes(&attr, k_dispatch_batch));
   KX_CUDA(cudaFuncGetAttributes(&attr, k_gc_all));
+  KX_CUDA(cudaFuncGetAttributes(&attr, k_dispatch_waiting));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2837,6 +3086,19 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
         q, a, in, pool_begin, perm, pool_offsets, dp, no_ring, rows, cand, row_count,
         admitted_count, pool_status);
   }
+  KX_CHECK_LAUNCH();
+}
+
+size_t waiting_smem(int ni) { return ((size_t(ni) * 32 + 15) & ~size_t(15)) + size_t(ni) * 9; }
+
+void launch_dispatch_waiting(const QueueDev& q, const AgentsDev& a, const InstDev& in,
+                             const int32_t* pool_begin, const uint32_t* perm,
+                             const int64_t* pool_offsets, const DispatchParams& dp, const WaitDev& w,
+                             int n_pools, int max_inst_per_pool, kx_decision* rows,
+                             int64_t* row_count, int64_t* admitted_count, int* pool_status,
+                             cudaStream_t st) {
+  k_dispatch_waiting<<<n_pools, 32, waiting_smem(max_inst_per_pool), st>>>(
+      q, a, in, pool_begin, perm, pool_offsets, dp, w, rows, row_count, admitted_count, pool_status);
   KX_CHECK_LAUNCH();
 }
 

@@ -51,6 +51,41 @@ struct DispPhase {
   uint32_t* heads_out;          // [P * kTopKMax]
 };
 
+// One request in an instance's waiting list (InstanceState::waiting,
+// engine.hpp:147-153): what try_admit's comparator and admit read.
+struct WaitRec {
+  double app_start, queue_enter;
+  uint64_t msg, uid;
+  int64_t prompt, kept;
+  int64_t qidx;     // queue index in the round it entered
+  int32_t agent;
+  int32_t round;    // serial of the dispatch round it entered in
+};
+
+// Waiting-list state and policy of a round_robin / static_threshold round.
+struct WaitDev {
+  WaitRec* rec;           // [n_inst * cap]
+  int64_t cap;
+  kx_admission* adm;      // [n_pools * log_cap]
+  int64_t* adm_count;     // [n_pools]
+  const double* rem_table;  // OracleScheduler remaining_by_uid (dense, see kx_set_remaining_table)
+  const uint8_t* rem_present;
+  uint64_t rem_base;
+  int64_t rem_n;
+  double static_thr;
+  int32_t policy;         // KX_DISPATCH_ROUND_ROBIN / KX_DISPATCH_STATIC_THRESHOLD
+  int32_t sched_kind;     // order_key policy for try_admit's comparator
+  int32_t round;
+  int32_t pad;
+};
+
+void launch_dispatch_waiting(const QueueDev& q, const AgentsDev& a, const InstDev& in,
+                             const int32_t* pool_begin, const uint32_t* perm,
+                             const int64_t* pool_offsets, const DispatchParams& dp, const WaitDev& w,
+                             int n_pools, int max_inst_per_pool, kx_decision* rows,
+                             int64_t* row_count, int64_t* admitted_count, int* pool_status,
+                             cudaStream_t st);
+
 void configure_dispatch_kernels();
 void read_dispatch_debug(unsigned long long* out);
 bool dispatch_can_overlap(int max_inst_per_pool, int ring);

@@ -42,6 +42,8 @@ DECISION_DTYPE = np.dtype([("time", "<f8"), ("predicted_peak", "<f8"), ("uid", "
                            ("queue_index", "<i8"), ("agent", "<i4"), ("target", "<i4"),
                            ("pool", "<i4"), ("admitted", "<i4")])
 assert DECISION_DTYPE.itemsize == C.sizeof(_abi.kx_decision)
+ADMISSION_DTYPE = np.dtype([("time", "<f8"), ("uid", "<u8"), ("queue_index", "<i8"), ("instance", "<i4"),
+                            ("pool", "<i4")])
 
 
 class DeviceScheduler:
@@ -174,6 +176,41 @@ class DeviceScheduler:
         cand = cand.reshape(self.n_pools, rs.value, ps.value)
         return [rows[p, :cnt[p]] for p in range(self.n_pools)], \
                [cand[p, :cnt[p]] for p in range(self.n_pools)]
+
+    # -- waiting lists (round_robin / static_threshold) ---------------------------
+    def set_waiting(self, instance_pos, agent, prompt_tokens, app_start, queue_enter, msg_key, uid,
+                    kept_tokens=None):
+        """Replace every waiting list: entry j joins the instance at position instance_pos[j]."""
+        pos = np.ascontiguousarray(instance_pos, np.int32)
+        cols = [np.ascontiguousarray(agent, np.int32), np.ascontiguousarray(prompt_tokens, np.int64),
+                np.ascontiguousarray(app_start, np.float64), np.ascontiguousarray(queue_enter, np.float64),
+                np.ascontiguousarray(msg_key, np.uint64), np.ascontiguousarray(uid, np.uint64),
+                None if kept_tokens is None else np.ascontiguousarray(kept_tokens, np.int64), None]
+        v = _abi.kx_queue_view(*[ptr(c) for c in cols])
+        check(self.lib.kx_waiting_upload(self.h, len(pos), ptr(pos), C.byref(v)))
+
+    def waiting_uids(self, instance_pos: int):
+        n = C.c_int64()
+        check(self.lib.kx_waiting_fetch(self.h, instance_pos, 0, None, C.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        check(self.lib.kx_waiting_fetch(self.h, instance_pos, n.value, ptr(out), C.byref(n)))
+        return out
+
+    def fetch_admissions(self):
+        """Admissions out of the waiting lists in the last round, per pool."""
+        cnt = np.zeros(self.n_pools, np.int64)
+        rs = C.c_int64()
+        check(self.lib.kx_admissions_fetch(self.h, ptr(cnt), None, C.byref(rs)))
+        rows = np.zeros(self.n_pools * rs.value, ADMISSION_DTYPE)
+        check(self.lib.kx_admissions_fetch(self.h, ptr(cnt), ptr(rows), C.byref(rs)))
+        rows = rows.reshape(self.n_pools, rs.value)
+        return [rows[p, :cnt[p]] for p in range(self.n_pools)]
+
+    def rr_next(self, set_to=None):
+        got = np.zeros(self.n_pools, np.int64)
+        st = None if set_to is None else np.ascontiguousarray(set_to, np.int64)
+        check(self.lib.kx_rr_next(self.h, ptr(got), ptr(st)))
+        return got
 
     # -- instance / ledger state ----------------------------------------------------
     def set_live(self, live_kv=None, running=None, waiting=None):

@@ -41,6 +41,13 @@ DECISION = np.dtype([("time", "<f8"), ("predicted_peak", "<f8"), ("uid", "<u8"),
                      ("queue_index", "<i8"), ("agent", "<i4"), ("target", "<i4"),
                      ("pool", "<i4"), ("admitted", "<i4")])
 
+WAITREC = np.dtype([("app_start", "<f8"), ("queue_enter", "<f8"), ("msg", "<u8"), ("uid", "<u8"),
+                    ("prompt", "<i8"), ("kept", "<i8"), ("qidx", "<i8"), ("agent", "<i4"),
+                    ("round", "<i4")])
+ADMISSION = np.dtype([("time", "<f8"), ("uid", "<u8"), ("queue_index", "<i8"), ("instance", "<i4"),
+                      ("pool", "<i4")])
+DISPATCH_POLICY = {"time_slot": 0, "round_robin": 1, "static_threshold": 2}
+
 _lib = None
 
 
@@ -80,6 +87,11 @@ def lib():
         L.kxo_dispatch_round.argtypes = [C.POINTER(Pool), C.POINTER(Queue), C.POINTER(Tables), P,
                                          C.c_int64, C.c_double, C.c_int32, P, P, C.c_int64,
                                          C.POINTER(C.c_int32)]
+        L.kxo_dispatch_round_waiting.restype = C.c_int64
+        L.kxo_dispatch_round_waiting.argtypes = [
+            C.POINTER(Pool), C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int64), P, C.c_int64, C.c_int32,
+            C.POINTER(Queue), C.POINTER(Tables), P, C.c_int64, C.c_double, C.c_int32, P, C.c_int64, P,
+            C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         L.kxo_pairwise_accuracy.argtypes = [C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_double),
                                             C.POINTER(C.c_uint64)]
         L.kxo_finalize.argtypes = [C.c_int64, P, P, P, P, C.c_double, C.c_double, C.c_uint64, P, P, P]
@@ -192,10 +204,53 @@ class PoolState:
                          _p(self.live_kv), _p(self.running), _p(self.waiting), _p(self.suspended),
                          C.cast(self._lp, C.c_void_p), slot_len, watermark, int(oracle_T))
 
-    def set_live(self, live_kv, running, waiting):
+    def set_live(self, live_kv, running, waiting=None):
         self.live_kv[:] = live_kv
         self.running[:] = running
-        self.waiting[:] = waiting
+        if waiting is not None:
+            self.waiting[:] = waiting
+
+    # ---- waiting lists (round_robin / static_threshold) ----
+    wcap = 0
+    rr_next = 0
+    round = 0
+
+    def set_waiting(self, q: "QueueArrays", inst_pos, wcap=4096):
+        """Replaces every waiting list: entry j joins instance inst_pos[j]."""
+        n = len(self.id)
+        self.wcap = wcap
+        self.wrec = np.zeros(n * wcap, WAITREC)
+        self.waiting[:] = 0
+        for j, i in enumerate(np.asarray(inst_pos)):
+            r = self.wrec[int(i) * wcap + int(self.waiting[i])]
+            r["app_start"], r["queue_enter"] = q.app_start[j], q.queue_enter[j]
+            r["msg"], r["uid"], r["prompt"] = q.msg_key[j], q.uid[j], q.prompt[j]
+            r["kept"] = 0 if q.kept is None else q.kept[j]
+            r["qidx"], r["agent"], r["round"] = -1, q.agent[j], -1
+            self.wrec[int(i) * wcap + int(self.waiting[i])] = r
+            self.waiting[i] += 1
+
+    def waiting_uids(self, i):
+        return self.wrec["uid"][i * self.wcap:i * self.wcap + int(self.waiting[i])].copy()
+
+    def dispatch_round_waiting(self, dispatch_policy, sched_policy, q: "QueueArrays", t: "TableArrays", perm,
+                               now, static_thr=0.90, pool_index=0, row_cap=1 << 16):
+        if self.wcap == 0:
+            self.set_waiting(q, [])
+        self.round += 1
+        perm = np.ascontiguousarray(perm, np.uint32)
+        rows = np.zeros(row_cap, DECISION)
+        adm = np.zeros(row_cap, ADMISSION)
+        rr = C.c_int64(self.rr_next)
+        nadm = C.c_int64()
+        st = C.c_int32()
+        n = lib().kxo_dispatch_round_waiting(
+            C.byref(self.view), DISPATCH_POLICY.get(dispatch_policy, dispatch_policy), static_thr,
+            POLICY.get(sched_policy, sched_policy), C.byref(rr), self.wrec.ctypes.data, self.wcap, self.round,
+            C.byref(q.view), C.byref(t.view), _p(perm), len(perm), now, pool_index, rows.ctypes.data, row_cap,
+            adm.ctypes.data, row_cap, C.byref(nadm), C.byref(st))
+        self.rr_next = rr.value
+        return rows[:n], adm[:nadm.value], st.value
 
     def dispatch_round(self, q: QueueArrays, t: TableArrays, perm, now, pool_index=0, row_cap=1 << 16):
         perm = np.ascontiguousarray(perm, np.uint32)

@@ -152,3 +152,44 @@ def test_pairwise_accuracy_matches_reference():
                 assert acc is None
             else:
                 assert bits(acc) == bits(exp)
+
+
+def waiting_queue(rd, pre):
+    return O.QueueArrays(rd[pre + "agent"], rd[pre + "prompt"], rd[pre + "app_start"], rd[pre + "queue_enter"],
+                         rd[pre + "msg_key"], rd[pre + "uid"])
+
+
+@pytest.mark.parametrize("name", ["dispatch_rr.kxf", "dispatch_static.kxf"])
+def test_waiting_rounds_match_reference(name):
+    """RoundRobin / StaticThreshold rounds (engine.cpp:259-296): decisions,
+    admissions out of the waiting lists and the lists themselves, with the
+    lists carried from round to round by the oracle (only the engine's live
+    state is reset from the fixture)."""
+    d = kxf.read(name)
+    ids = d["inst_id"]
+    policy = {1: "round_robin", 2: "static_threshold"}[int(d["policy"][0])]
+    pool = O.PoolState(ids, d["inst_cap"], d["inst_k"], d["inst_max_batch"])
+    depth = d["agent_depth"]
+    tables = O.TableArrays(np.zeros(len(depth), np.int32), depth=depth)
+    n_adm = 0
+    for r, rd in dispatch_rounds(d):
+        if r == 0:
+            pool.set_waiting(waiting_queue(rd, "w."), rd["w.inst"])
+        for i in range(len(ids)):  # the carried lists equal the reference's at round start
+            assert np.array_equal(pool.waiting_uids(i), rd["w.uid"][rd["w.inst"] == i]), (r, i)
+        pool.set_live(rd["live_kv"], rd["running"])
+        q = waiting_queue(rd, "q.")
+        perm, _ = O.sort("topo_depth", q, tables, 1)
+        rows, adm, st = pool.dispatch_round_waiting(policy, "topo_depth", q, tables, perm, float(rd["now"][0]))
+        assert st == 0
+        assert np.array_equal(rows["uid"], rd["dec_uid"]), r
+        assert np.array_equal(rows["target"], rd["dec_target"]), r
+        assert np.array_equal(rows["admitted"], rd["dec_admitted"]), r
+        assert np.array_equal(adm["uid"], rd["adm_uid"]), r
+        assert np.array_equal(adm["instance"], rd["adm_inst"]), r
+        assert np.array_equal(bits(pool.live_kv), bits(rd["end_live_kv"]))
+        assert np.array_equal(pool.running, rd["end_running"])
+        for i in range(len(ids)):
+            assert np.array_equal(pool.waiting_uids(i), rd["end_w.uid"][rd["end_w.inst"] == i]), (r, i)
+        n_adm += len(adm)
+    assert n_adm > 0
