@@ -1821,6 +1821,11 @@ int kx_debug_dispatch_timers(uint64_t* out16) {
   return guard([&] { kx::read_dispatch_debug(reinterpret_cast<unsigned long long*>(out16)); });
 }
 
+// Diagnostics: per-pass tile phase sums of the radix passes (KX_SORT_TIMERS builds).
+int kx_debug_sort_timers(uint64_t* out64, int32_t reset) {
+  return guard([&] { kx::read_sort_debug(reinterpret_cast<unsigned long long*>(out64), reset != 0); });
+}
+
 int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining,
                         const uint8_t* present, int32_t scope_all, uint64_t* pairs, double* correct,
                         double* accuracy) {

@@ -28,6 +28,14 @@
 
 namespace kx {
 
+void read_sort_debug(unsigned long long* out64, bool reset) {
+  KX_CUDA(cudaMemcpyFromSymbol(out64, g_sort_tim, sizeof(unsigned long long) * 64));
+  if (reset) {
+    static const unsigned long long z[64] = {};
+    KX_CUDA(cudaMemcpyToSymbol(g_sort_tim, z, sizeof(z)));
+  }
+}
+
 __global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= passes) return;
@@ -1308,7 +1316,10 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
       const int v = (variants && int(strlen(variants)) > p) ? variants[p] - '0' : kSortRankDefault[p < 4 ? p : 3];
       const uint32_t* vin = p == 0 ? nullptr : ws.vals[cur];
       const unsigned g = static_cast<unsigned>(tiles);
-      if (v == 1)
+      if (v == 3)
+        k_onesweep_pass<uint32_t, 3><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+      else if (v == 1)
         k_onesweep_pass<uint32_t, 1><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
             ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
       else if (v == 2)
@@ -1334,7 +1345,14 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   KX_CHECK_LAUNCH();
   P.end(st);
   P.begin("tie_fix", 0.0, st);
-  k_tie_fix_small<<<sms * 8, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
+  // one resident wave (grid-stride over the run starts): a partial second
+  // wave would double the latency-bound kernel's span
+  static int fix_ctas = [] {
+    int b = 0;
+    KX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tie_fix_small, 256, 0));
+    return std::max(b, 1);
+  }();
+  k_tie_fix_small<<<sms * fix_ctas, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
                                            ws.n_small, ws.big_starts, ws.big_lens, ws.n_big,
                                            ws.tie_cap);
   KX_CHECK_LAUNCH();
@@ -1384,11 +1402,13 @@ void configure_sort_kernels() {
   preload(k_onesweep_pass<uint32_t, 0>);
   preload(k_onesweep_pass<uint32_t, 1>);
   preload(k_onesweep_pass<uint32_t, 2>);
+  preload(k_onesweep_pass<uint32_t, 3>);
   KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(uint32_t) * kSpecMax)));
   KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(topk_sort_smem())));
-  for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>})
+  for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>,
+                 k_onesweep_pass<uint32_t, 3>})
     KX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sort_dyn_smem<uint32_t>())));
 }

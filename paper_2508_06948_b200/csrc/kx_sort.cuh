@@ -37,7 +37,23 @@ constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
-constexpr int kLookBatch = 8;
+#ifndef KX_LOOK_BATCH
+#define KX_LOOK_BATCH 8
+#endif
+constexpr int kLookBatch = KX_LOOK_BATCH;
+
+// Diagnostics (build with -DKX_SORT_TIMERS=1): per pass (shift / 8), sums
+// over tiles of the globaltimer spans load, rank, scan+look-back, stage,
+// write, and the tile count (read by kx_debug_sort_timers).
+#ifndef KX_SORT_TIMERS
+#define KX_SORT_TIMERS 0
+#endif
+static __device__ unsigned long long g_sort_tim[8 * 8];  // per translation unit (no -rdc)
+__device__ __forceinline__ unsigned long long sort_gclk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -105,6 +121,7 @@ __global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes);
 template <typename K>
 struct SortSmem {
   uint32_t warp_hist[kSortThreads / 32][kRadix];
+  uint32_t peer_mask[kSortThreads / 32][kRadix];  // kRank 3: lanes holding each digit
   uint32_t digit_start[kRadix];
   int64_t global_base[kRadix];
   uint32_t tile_id;
@@ -119,7 +136,11 @@ constexpr size_t sort_dyn_smem() {
 // (first pass). global_excl: this pass's exclusive digit offsets.
 // kRank selects the warp ranking: 0 = MATCH.ANY peers, every peer reads the
 // running count; 1 = eight-ballot peers, same update; 2 = MATCH.ANY peers,
-// the leader reads and broadcasts the count.
+// the leader reads and broadcasts the count; 3 = peers from a shared-memory
+// atomicOr mask per (warp, digit), the leader reads/bumps the count and
+// clears the mask. MATCH.ANY issues at a small fraction of the shared-memory
+// atomic rate on sm_100 (scripts/micro/pass_probe.cu: a tile's ranking takes
+// ~6 us with MATCH, ~3 us with the mask), so 3 wins on spread digits.
 template <typename K, int kRank = 0>
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
@@ -140,8 +161,12 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
   const int warp = tid >> 5;
   const int lane = tid & 31;
 
+  unsigned long long tt[6] = {0, 0, 0, 0, 0, 0};
+  if (KX_SORT_TIMERS && tid == 0) tt[0] = sort_gclk();
   if (tid == 0) sm.tile_id = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+  if (kRank == 3)
+    for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.peer_mask[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = sm.tile_id;
   const int64_t base = int64_t(tile) * kSortTile;
@@ -161,13 +186,44 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
       val[i] = 0;
     }
   }
+  // Every key of the tile is in registers before the ranking starts (the
+  // ranking loop then runs without load stalls between its shared-memory
+  // steps): the empty asm consumes all keys ahead of the barrier.
+  {
+    uint32_t dep = 0;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) dep ^= static_cast<uint32_t>(key[i]);
+    asm volatile("" ::"r"(dep));
+    __syncthreads();
+  }
+  if (KX_SORT_TIMERS && tid == 0) tt[1] = sort_gclk();
   // Stable warp-level ranking, processing items in element order.
   uint32_t* wh = sm.warp_hist[warp];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = digit_of(key[i], shift);
-    const uint32_t peers = kRank == 1 ? warp_match8(d) : __match_any_sync(0xffffffffu, d);
-    if (kRank == 2) {
+    uint32_t peers;
+    if (kRank == 3) {
+      uint32_t* pm = sm.peer_mask[warp];
+      atomicOr(&pm[d], 1u << lane);
+      __syncwarp();
+      peers = pm[d];
+      __syncwarp();
+    } else {
+      peers = kRank == 1 ? warp_match8(d) : __match_any_sync(0xffffffffu, d);
+    }
+    if (kRank == 3) {
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        old = wh[d];
+        wh[d] = old + __popc(peers);
+        sm.peer_mask[warp][d] = 0;
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      __syncwarp();
+      rank[i] = old + __popc(peers & lanemask_lt());
+    } else if (kRank == 2) {
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (lane == leader) {
@@ -186,6 +242,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     }
   }
   __syncthreads();
+  if (KX_SORT_TIMERS && tid == 0) tt[2] = sort_gclk();
 
   // Per digit: exclusive prefix over warps, tile total, look-back.
   uint32_t total = 0;
@@ -247,6 +304,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     sm.global_base[tid] = int64_t(global_excl[tid]) + excl - int64_t(sm.digit_start[tid]);
   }
   __syncthreads();
+  if (KX_SORT_TIMERS && tid == 0) tt[3] = sort_gclk();
 
   // Stage the tile in digit order.
 #pragma unroll
@@ -257,6 +315,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     s_vals[pos] = val[i];
   }
   __syncthreads();
+  if (KX_SORT_TIMERS && tid == 0) tt[4] = sort_gclk();
 
   const int64_t valid = (n - base) < kSortTile ? (n - base) : kSortTile;
 #pragma unroll 4
@@ -265,6 +324,15 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
     keys_out[dst] = k;
     vals_out[dst] = s_vals[j];
+  }
+  if (KX_SORT_TIMERS) {
+    __syncthreads();
+    if (tid == 0) {
+      tt[5] = sort_gclk();
+      unsigned long long* g = g_sort_tim + (shift / 8 & 7) * 8;
+      for (int k = 0; k < 5; ++k) atomicAdd(&g[k], tt[k + 1] - tt[k]);
+      atomicAdd(&g[5], 1ull);
+    }
   }
 }
 
