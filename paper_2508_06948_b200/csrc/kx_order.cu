@@ -463,15 +463,14 @@ __global__ void __launch_bounds__(256)
 k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
          uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
          int* __restrict__ error_flags, KeygenSpec spec) {
-  __shared__ uint32_t sh[4 * kRadix];
+  __shared__ uint32_t sh[kRadix];
   __shared__ uint32_t s_ag[kSmemTables ? kKeygenAgents : 1];  // pool << 16 | class
   extern __shared__ __align__(16) unsigned char kg_dyn[];
   double* s_lo = reinterpret_cast<double*>(kg_dyn);                 // [P]
   double* s_scale = s_lo + op.n_pools;                              // [P]
   int64_t* s_bnd = reinterpret_cast<int64_t*>(s_scale + op.n_pools);  // [P] prefix bound, -1 off
   uint32_t* s_pool = reinterpret_cast<uint32_t*>(s_bnd + op.n_pools);  // [P] counts
-  const int passes = op.key_bits / kRadixBits;
-  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) sh[i] = 0;
+  for (int i = threadIdx.x; i < kRadix; i += blockDim.x) sh[i] = 0;
   for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) {
     s_pool[i] = 0;
     s_lo[i] = ranges[i].lo;
@@ -561,24 +560,13 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
         k4.w = make_key(ag[u].w, t1[u].y, 4 * v + 3);
         kv[v] = k4;
       }
-      // the two low digits are spread (plain shared atomics); the high ones
-      // are often equal across a warp (aggregated increments)
-      for (int pz = 0; pz < passes; ++pz) {
-        const int sh_ = pz * kRadixBits;
-        uint32_t* h = &sh[pz * kRadix];
-        if (pz < 2) {
-          if (valid) {
-            atomicAdd(&h[digit_of(k4.x, sh_)], 1u);
-            atomicAdd(&h[digit_of(k4.y, sh_)], 1u);
-            atomicAdd(&h[digit_of(k4.z, sh_)], 1u);
-            atomicAdd(&h[digit_of(k4.w, sh_)], 1u);
-          }
-        } else {
-          hist_add(h, digit_of(k4.x, sh_), valid);
-          hist_add(h, digit_of(k4.y, sh_), valid);
-          hist_add(h, digit_of(k4.z, sh_), valid);
-          hist_add(h, digit_of(k4.w, sh_), valid);
-        }
+      // the first pass's digit (spread: plain shared atomics); each radix
+      // pass counts the next pass's digit as it writes its keys
+      if (valid) {
+        atomicAdd(&sh[digit_of(k4.x, 0)], 1u);
+        atomicAdd(&sh[digit_of(k4.y, 0)], 1u);
+        atomicAdd(&sh[digit_of(k4.z, 0)], 1u);
+        atomicAdd(&sh[digit_of(k4.w, 0)], 1u);
       }
     }
   }
@@ -591,13 +579,13 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
         key = make_key(q.agent[i], tp[i], i);
         keys[i] = key;
       }
-      for (int pz = 0; pz < passes; ++pz) hist_add(&sh[pz * kRadix], digit_of(key, pz * kRadixBits), valid);
+      hist_add(sh, digit_of(key, 0), valid);
     }
   }
   if (cur_pool >= 0) atomicAdd(&s_pool[cur_pool], cur_cnt);
   if (err) atomicOr(error_flags, err);
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
+  for (int i = threadIdx.x; i < kRadix; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
   for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x)
     if (s_pool[i]) atomicAdd(&pool_counts[i], s_pool[i]);
@@ -855,327 +843,6 @@ k_tie_fix_big(QueueDev q, int policy, uint32_t* __restrict__ perm, uint32_t* __r
   }
 }
 
-// ---- per-pool top-K prefix (overlaps the dispatch with the full sort) -------
-// A dispatch round consumes at most (free batch slots + 1) heads of each
-// pool (every admission takes a slot; the round stops at the first head
-// with no target, engine.cpp:247). Radix-select finds, per pool, the
-// smallest compact-key bound whose prefix holds at least that many
-// requests; those candidates are exactly the first entries of the pool's
-// order (every other request has a larger compact key), and sorting them
-// by (key, exact tuple) gives that prefix in reference order.
-__global__ void k_topk_init(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
-                            int64_t n, const uint32_t* __restrict__ hist_excl,
-                            const int64_t* __restrict__ pool_offsets, uint32_t max_need,
-                            TopKState* __restrict__ st, const uint32_t* __restrict__ spec_on,
-                            const uint32_t* __restrict__ spec_bound,
-                            const uint32_t* __restrict__ spec_count) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= op.n_pools) return;
-  TopKState t{};
-  const int64_t cnt = pool_offsets[p + 1] - pool_offsets[p];
-  if (spec_on && spec_on[p] && spec_count[p] <= uint32_t(kTopKMax) && cnt > 0) {
-    // candidates collected by key generation: every key <= spec_bound
-    t.need = 0;
-    t.pool_count = static_cast<uint32_t>(cnt);
-    t.done = 1;
-    t.spec = 1;
-    t.bound = spec_bound[p];
-    t.n_cand = spec_count[p];
-    st[p] = t;
-    return;
-  }
-  int64_t free_slots = 0;
-  for (int i = pool_begin[p]; i < pool_begin[p + 1]; ++i) {
-    const int64_t f = int64_t(in.max_batch[i]) - in.running[i] - in.waiting[i];
-    free_slots += f > 0 ? f : 0;
-  }
-  int64_t need = free_slots + 1;
-  need = need < cnt ? need : cnt;
-  need = need < int64_t(max_need) ? need : int64_t(max_need);  // the continuation covers the rest
-  t.need = static_cast<uint32_t>(need);
-  t.pool_count = static_cast<uint32_t>(cnt);
-  if (need == 0) {  // empty pool
-    t.done = 1;
-    t.bound = 0;
-    t.empty = 1;
-    st[p] = t;
-    return;
-  }
-  const int TS = op.key_bits - 8;
-  const int lo_d = op.pool_bits ? (p << (8 - op.pool_bits)) : 0;
-  const int hi_d = op.pool_bits ? ((p + 1) << (8 - op.pool_bits)) : 256;
-  int64_t cum = 0, c = 0;
-  int d = lo_d;
-  for (; d < hi_d; ++d) {
-    c = (d + 1 < 256 ? int64_t(hist_excl[d + 1]) : n) - int64_t(hist_excl[d]);
-    if (cum + c >= need) break;
-    cum += c;
-  }
-  t.below = static_cast<uint32_t>(cum);
-  t.count = static_cast<uint32_t>(c);
-  t.prefix = static_cast<uint32_t>(d) << TS;
-  t.mask = 0xFFu << TS;
-  if (cum + c <= kTopKMax) {
-    t.done = 1;
-    t.bound = t.prefix | ((1u << TS) - 1u);
-  } else if (TS == 0) {  // single-digit keys: stop below the boundary key
-    t.done = 1;
-    if (cum > 0) t.bound = t.prefix - 1u;
-    else t.defer = 1;
-  }
-  st[p] = t;
-}
-
-__device__ __forceinline__ int pool_of_key(uint32_t key, const OrderParams& op) {
-  return op.pool_bits ? static_cast<int>(key >> (op.key_bits - op.pool_bits)) : 0;
-}
-
-// Keys are read as uint4 (four per load, four loads in flight per thread):
-// the select passes stream the key array at HBM rate instead of one
-// dependent 4-byte load per iteration.
-constexpr int kSelU = 4;
-
-__global__ void k_topk_hist(const uint32_t* __restrict__ keys, int64_t n, OrderParams op, int shift,
-                            const TopKState* __restrict__ st, uint32_t* __restrict__ hist) {
-  __shared__ uint32_t sh[kTopKMaxPools * kRadix];
-  __shared__ uint32_t s_mask[kTopKMaxPools], s_prefix[kTopKMaxPools], s_live[kTopKMaxPools];
-  for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x) sh[i] = 0;
-  __shared__ int s_any;
-  if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
-    s_mask[p] = st[p].mask;
-    s_prefix[p] = st[p].prefix;
-    s_live[p] = !st[p].done;
-    if (s_live[p]) s_any = 1;
-  }
-  __syncthreads();
-  if (!s_any) return;  // every pool's prefix bound is already known
-  auto take = [&](uint32_t k) {
-    const int p = pool_of_key(k, op);
-    if (s_live[p] && (k & s_mask[p]) == s_prefix[p]) atomicAdd(&sh[p * kRadix + ((k >> shift) & 0xFF)], 1u);
-  };
-  const int64_t nv = n >> 2;
-  const uint4* kv = reinterpret_cast<const uint4*>(keys);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += kSelU * stride) {
-    uint4 x[kSelU];
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      const int64_t v = v0 + u * stride;
-      x[u] = v < nv ? kv[v] : make_uint4(~0u, ~0u, ~0u, ~0u);
-    }
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      if (v0 + u * stride >= nv) continue;
-      take(x[u].x);
-      take(x[u].y);
-      take(x[u].z);
-      take(x[u].w);
-    }
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(keys[i]);
-  __syncthreads();
-  for (int i = threadIdx.x; i < op.n_pools * kRadix; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-__global__ void k_topk_pick(OrderParams op, int shift, TopKState* __restrict__ st,
-                            uint32_t* __restrict__ hist) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= op.n_pools) return;
-  TopKState t = st[p];
-  uint32_t* h = hist + p * kRadix;
-  if (!t.done) {
-    const int64_t need = int64_t(t.need) - t.below;
-    int64_t cum = 0, c = 0;
-    int d = 0;
-    for (; d < kRadix; ++d) {
-      c = h[d];
-      if (cum + c >= need) break;
-      cum += c;
-    }
-    t.below += static_cast<uint32_t>(cum);
-    t.count = static_cast<uint32_t>(c);
-    t.prefix |= static_cast<uint32_t>(d) << shift;
-    t.mask |= 0xFFu << shift;
-    if (int64_t(t.below) + c <= kTopKMax) {
-      t.done = 1;
-      t.bound = t.prefix | ((1u << shift) - 1u);
-    } else if (shift == 0) {  // > kTopKMax requests share the boundary key:
-      t.done = 1;             // the strictly smaller keys are still a prefix
-      if (t.below > 0) t.bound = t.prefix - 1u;
-      else t.defer = 1;
-    }
-    st[p] = t;
-  }
-  for (int d = 0; d < kRadix; ++d) h[d] = 0;  // ready for the next round
-}
-
-__global__ void k_topk_compact(const uint32_t* __restrict__ keys, int64_t n, OrderParams op,
-                               TopKState* __restrict__ st, uint32_t* __restrict__ cand) {
-  __shared__ uint32_t s_bound[kTopKMaxPools], s_ok[kTopKMaxPools];
-  __shared__ int s_any;
-  if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
-    s_bound[p] = st[p].bound;
-    s_ok[p] = !st[p].defer && !st[p].empty && !st[p].spec;
-    if (s_ok[p]) s_any = 1;
-  }
-  __syncthreads();
-  if (!s_any) return;  // every pool's candidates are already collected
-  auto take = [&](uint32_t k, int64_t i) {
-    const int p = pool_of_key(k, op);
-    if (s_ok[p] && k <= s_bound[p]) {
-      const uint32_t slot = atomicAdd(&st[p].n_cand, 1u);
-      if (slot < kTopKMax) cand[int64_t(p) * kTopKMax + slot] = static_cast<uint32_t>(i);
-    }
-  };
-  const int64_t nv = n >> 2;
-  const uint4* kv = reinterpret_cast<const uint4*>(keys);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += kSelU * stride) {
-    uint4 x[kSelU];
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      const int64_t v = v0 + u * stride;
-      x[u] = v < nv ? kv[v] : make_uint4(~0u, ~0u, ~0u, ~0u);
-    }
-#pragma unroll
-    for (int u = 0; u < kSelU; ++u) {
-      const int64_t v = v0 + u * stride;
-      if (v >= nv) continue;
-      take(x[u].x, 4 * v);
-      take(x[u].y, 4 * v + 1);
-      take(x[u].z, 4 * v + 2);
-      take(x[u].w, 4 * v + 3);
-    }
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(keys[i], i);
-}
-
-// CTA per pool: exact order of the candidates. A bitonic sort of the
-// composite (compact key << 32 | candidate slot) in shared memory orders them
-// by compact key; runs of equal compact keys (whole runs: the candidate set
-// is a union of complete key values) are then re-sorted by the exact tuple,
-// short runs by one thread in registers, long runs by the CTA (exact records
-// staged in shared memory, rank by counting).
-constexpr int kTopKThreads = 1024;
-constexpr int kTopKShortRun = 16;
-constexpr int kTopKLongRuns = 64;
-
-size_t topk_sort_smem() {
-  return sizeof(uint64_t) * kTopKMax + sizeof(uint32_t) * kTopKMax + sizeof(uint32_t) * kTopKMax +
-         sizeof(TRec) * kTopKMax;
-}
-
-__global__ void __launch_bounds__(kTopKThreads)
-k_topk_sort(QueueDev q, int policy, const uint32_t* __restrict__ keys, OrderParams op,
-            const TopKState* __restrict__ st, const uint32_t* __restrict__ cand,
-            uint32_t* __restrict__ heads) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ uint32_t s_ls[kTopKLongRuns], s_ll[kTopKLongRuns];
-  __shared__ int s_nlong;
-  const int p = blockIdx.x;
-  const TopKState t = st[p];
-  if (t.defer || t.empty) return;
-  const int n = static_cast<int>(t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
-  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-  uint32_t* so = reinterpret_cast<uint32_t*>(sk + kTopKMax);
-  uint32_t* tmp = so + kTopKMax;
-  TRec* rec = reinterpret_cast<TRec*>(tmp + kTopKMax);
-  const uint32_t* pc = cand + int64_t(p) * kTopKMax;
-  int p2 = 1;
-  while (p2 < n) p2 <<= 1;
-  for (int i = threadIdx.x; i < p2; i += blockDim.x)
-    sk[i] = i < n ? ((static_cast<uint64_t>(keys[pc[i]]) << 32) | static_cast<uint32_t>(i)) : ~0ull;
-  if (threadIdx.x == 0) s_nlong = 0;
-  __syncthreads();
-  for (int kk = 2; kk <= p2; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const uint64_t a = sk[i], b = sk[l];
-          if ((a > b) == ((i & kk) == 0)) {
-            sk[i] = b;
-            sk[l] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) so[i] = pc[static_cast<uint32_t>(sk[i])];
-  __syncthreads();
-  // Runs of equal compact keys: the exact tuple decides.
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t k = static_cast<uint32_t>(sk[i] >> 32);
-    const bool start = (i == 0 || static_cast<uint32_t>(sk[i - 1] >> 32) != k) &&
-                       (i + 1 < n && static_cast<uint32_t>(sk[i + 1] >> 32) == k);
-    if (!start) continue;
-    int e = i + 2;
-    while (e < n && static_cast<uint32_t>(sk[e] >> 32) == k) ++e;
-    const int len = e - i;
-    if (len <= kTopKShortRun) {
-      TKey r[kTopKShortRun];
-      for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, so[i + j]);
-      for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
-        const TKey x = r[j];
-        int m = j - 1;
-        while (m >= 0 && tkey_less(q, x, r[m])) {
-          r[m + 1] = r[m];
-          --m;
-        }
-        r[m + 1] = x;
-      }
-      for (int j = 0; j < len; ++j) so[i + j] = r[j].idx;
-    } else {
-      const int slot = atomicAdd(&s_nlong, 1);
-      if (slot < kTopKLongRuns) {
-        s_ls[slot] = static_cast<uint32_t>(i);
-        s_ll[slot] = static_cast<uint32_t>(len);
-      }
-    }
-  }
-  __syncthreads();
-  const int nlong = s_nlong;
-  for (int r = 0; r < nlong; ++r) {
-    int st0, len;
-    if (nlong <= kTopKLongRuns) {
-      st0 = static_cast<int>(s_ls[r]);
-      len = static_cast<int>(s_ll[r]);
-    } else {  // more long runs than listed: one pass over the whole set
-      if (r > 0) break;
-      st0 = 0;
-      len = n;
-    }
-    for (int j = threadIdx.x; j < len; j += blockDim.x) rec[j] = load_rec(q, policy, so[st0 + j]);
-    __syncthreads();
-    for (int j = threadIdx.x; j < len; j += blockDim.x) {
-      const TRec x = rec[j];
-      int rank = 0;
-      if (nlong <= kTopKLongRuns) {
-        for (int m = 0; m < len; ++m) rank += rec_less(rec[m], x);
-      } else {  // whole set: compact key first
-        const uint32_t kx = static_cast<uint32_t>(sk[st0 + j] >> 32);
-        for (int m = 0; m < len; ++m) {
-          const uint32_t km = static_cast<uint32_t>(sk[m] >> 32);
-          rank += km < kx || (km == kx && rec_less(rec[m], x));
-        }
-      }
-      tmp[rank] = x.idx;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < len; j += blockDim.x) so[st0 + j] = tmp[j];
-    __syncthreads();
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) heads[int64_t(p) * kTopKMax + i] = so[i];
-}
-
 void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                        const int32_t* pool_begin, const OrderParams& op, int64_t n,
                        const OrderWorkspace& ws, TopKWork& w, cudaStream_t st) {
@@ -1196,34 +863,6 @@ void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
 }
 
 size_t spec_list_words(int n_pools) { return size_t(n_pools) * kSpecMax; }
-
-void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
-                 const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
-                 cudaStream_t st, cudaEvent_t keys_released) {
-  const uint32_t* keys = ws.keys[0];
-  const int passes = op.key_bits / kRadixBits;
-  const int pb = (op.n_pools + 31) / 32;
-  k_topk_init<<<pb, 32, 0, st>>>(in, pool_begin, op, n, ws.hist + (passes - 1) * kRadix,
-                                 ws.pool_offsets, w.max_need, w.state, w.spec_on, w.spec_bound,
-                                 w.spec_count);
-  KX_CHECK_LAUNCH();
-  KX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * op.n_pools * kRadix, st));
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, int64_t(sms) * 4)));
-  for (int r = 1; r < passes && n > 0; ++r) {
-    const int shift = op.key_bits - 8 - 8 * r;
-    k_topk_hist<<<grid, 256, 0, st>>>(keys, n, op, shift, w.state, w.hist);
-    KX_CHECK_LAUNCH();
-    k_topk_pick<<<pb, 32, 0, st>>>(op, shift, w.state, w.hist);
-    KX_CHECK_LAUNCH();
-  }
-  if (n > 0) {
-    k_topk_compact<<<grid, 256, 0, st>>>(keys, n, op, w.state, w.cand);
-    KX_CHECK_LAUNCH();
-  }
-  KX_CUDA(cudaEventRecord(keys_released, st));  // the original keys are no longer read
-  k_topk_sort<<<op.n_pools, kTopKThreads, topk_sort_smem(), st>>>(q, op.policy, keys, op, w.state, w.cand, w.heads);
-  KX_CHECK_LAUNCH();
-}
 
 // ---- host orchestration --------------------------------------------------
 // Warp ranking per radix pass (kx_sort.cuh kRank), chosen by measurement
@@ -1298,8 +937,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   }
   KX_CHECK_LAUNCH();
   P.end(st);
-  k_scan_hist<<<1, 32 * passes, 0, st>>>(ws.hist, passes);
-  KX_CHECK_LAUNCH();
+  // (pass p scans its raw digit counts itself; pass p counts digit p + 1)
   k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
   KX_CHECK_LAUNCH();
   if (hooks && hooks->after_keys) hooks->after_keys();  // compact keys + histograms ready
@@ -1315,19 +953,20 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
       static const char* variants = getenv("KX_SORT_RANK");  // experiment knob, per pass
       const int v = (variants && int(strlen(variants)) > p) ? variants[p] - '0' : kSortRankDefault[p < 4 ? p : 3];
       const uint32_t* vin = p == 0 ? nullptr : ws.vals[cur];
+      uint32_t* nh = p + 1 < passes ? ws.hist + (p + 1) * kRadix : nullptr;
       const unsigned g = static_cast<unsigned>(tiles);
       if (v == 3)
         k_onesweep_pass<uint32_t, 3><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else if (v == 1)
         k_onesweep_pass<uint32_t, 1><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else if (v == 2)
         k_onesweep_pass<uint32_t, 2><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else
         k_onesweep_pass<uint32_t, 0><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
     }
     KX_CHECK_LAUNCH();
     P.end(st);
@@ -1405,8 +1044,6 @@ void configure_sort_kernels() {
   preload(k_onesweep_pass<uint32_t, 3>);
   KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(uint32_t) * kSpecMax)));
-  KX_CUDA(cudaFuncSetAttribute(k_topk_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(topk_sort_smem())));
   for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>,
                  k_onesweep_pass<uint32_t, 3>})
     KX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -97,10 +97,6 @@ void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                        const int32_t* pool_begin, const OrderParams& op, int64_t n,
                        const OrderWorkspace& ws, TopKWork& w, cudaStream_t st);
 
-void launch_topk(const QueueDev& q, const InstDev& in, const int32_t* pool_begin,
-                 const OrderParams& op, int64_t n, const OrderWorkspace& ws, TopKWork& w, int sms,
-                 cudaStream_t st, cudaEvent_t keys_released);
-
 // Diagnostics: per-pass radix tile phase sums (KX_SORT_TIMERS builds).
 void read_sort_debug(unsigned long long* out64, bool reset);
 

@@ -41,6 +41,12 @@ constexpr uint32_t kCountMask = (1u << 30) - 1;
 #define KX_LOOK_BATCH 8
 #endif
 constexpr int kLookBatch = KX_LOOK_BATCH;
+// Next-digit counting: digits at or above this shift are counted with
+// warp-aggregated increments, lower ones with plain shared atomics. The
+// C4 keys' low digits cluster too (a workflow's calls share app_start), and
+// aggregated increments measured faster for every digit (0.531 vs 0.543 ms
+// for the four passes), so all digits aggregate.
+constexpr int kNextAggShift = 0;
 
 // Diagnostics (build with -DKX_SORT_TIMERS=1): per pass (shift / 8), sums
 // over tiles of the globaltimer spans load, rank, scan+look-back, stage,
@@ -122,6 +128,7 @@ template <typename K>
 struct SortSmem {
   uint32_t warp_hist[kSortThreads / 32][kRadix];
   uint32_t peer_mask[kSortThreads / 32][kRadix];  // kRank 3: lanes holding each digit
+  uint32_t next_hist[kRadix];                      // next pass's digit counts (this tile)
   uint32_t digit_start[kRadix];
   int64_t global_base[kRadix];
   uint32_t tile_id;
@@ -133,7 +140,10 @@ constexpr size_t sort_dyn_smem() {
 }
 
 // One stable LSD digit pass. vals_in == nullptr means "value = element index"
-// (first pass). global_excl: this pass's exclusive digit offsets.
+// (first pass). global_excl: this pass's exclusive digit offsets, or with
+// counts_in != 0 its raw digit counts (each CTA scans them). next_hist !=
+// nullptr: the pass also counts the digit at next_shift of every key it
+// writes (the next pass's histogram, one read of the keys saved).
 // kRank selects the warp ranking: 0 = MATCH.ANY peers, every peer reads the
 // running count; 1 = eight-ballot peers, same update; 2 = MATCH.ANY peers,
 // the leader reads and broadcasts the count; 3 = peers from a shared-memory
@@ -146,7 +156,8 @@ __global__ void __launch_bounds__(kSortThreads)
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                 int64_t n, int shift, const uint32_t* __restrict__ global_excl,
-                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter
+                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter, int counts_in,
+                uint32_t* __restrict__ next_hist, int next_shift
 #ifdef KX_PROBE_NO_LOOKBACK_SWITCH
                 , int probe_no_lookback = 0
 #endif
@@ -167,6 +178,8 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
   if (kRank == 3)
     for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.peer_mask[0][0])[i] = 0;
+  if (next_hist)
+    for (int i = tid; i < kRadix; i += kSortThreads) sm.next_hist[i] = 0;
   __syncthreads();
   const uint32_t tile = sm.tile_id;
   const int64_t base = int64_t(tile) * kSortTile;
@@ -256,23 +269,39 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     volatile uint32_t* lb = lookback;
     lb[int64_t(tile) * kRadix + tid] = (tile == 0 ? kFlagIncl : kFlagAgg) | total;
   }
-  // Exclusive scan of `total` over the 256 digits (8 warps x 32 lanes).
-  __shared__ uint32_t s_warp_sums[kRadix / 32];
+  // Exclusive scans over the 256 digits (8 warps x 32 lanes) of `total`
+  // and, with counts_in, of the pass's global digit counts.
+  __shared__ uint32_t s_warp_sums[kRadix / 32], s_warp_cnt[kRadix / 32];
+  uint32_t gcount = 0, gexcl = 0;
   if (tid < kRadix) {
     uint32_t x = total;
+    gcount = counts_in ? global_excl[tid] : 0u;
+    uint32_t c = gcount;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const uint32_t yc = __shfl_up_sync(0xffffffffu, c, o);
+      if (lane >= o) {
+        x += y;
+        c += yc;
+      }
     }
-    if (lane == 31) s_warp_sums[warp] = x;
+    if (lane == 31) {
+      s_warp_sums[warp] = x;
+      s_warp_cnt[warp] = c;
+    }
     sm.digit_start[tid] = x - total;  // warp-local exclusive
+    gexcl = c - gcount;
   }
   __syncthreads();
   if (tid < kRadix) {
-    uint32_t add = 0;
-    for (int w = 0; w < warp; ++w) add += s_warp_sums[w];
+    uint32_t add = 0, addc = 0;
+    for (int w = 0; w < warp; ++w) {
+      add += s_warp_sums[w];
+      addc += s_warp_cnt[w];
+    }
     sm.digit_start[tid] += add;
+    gexcl = counts_in ? gexcl + addc : global_excl[tid];
     // Decoupled look-back for digit `tid`, kLookBatch predecessors per
     // round trip: the walk over tiles that have only published their
     // aggregate costs one L2 latency per batch instead of per tile.
@@ -301,7 +330,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
       }
       lb[int64_t(tile) * kRadix + tid] = kFlagIncl | (excl + total);
     }
-    sm.global_base[tid] = int64_t(global_excl[tid]) + excl - int64_t(sm.digit_start[tid]);
+    sm.global_base[tid] = int64_t(gexcl) + excl - int64_t(sm.digit_start[tid]);
   }
   __syncthreads();
   if (KX_SORT_TIMERS && tid == 0) tt[3] = sort_gclk();
@@ -318,12 +347,42 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
   if (KX_SORT_TIMERS && tid == 0) tt[4] = sort_gclk();
 
   const int64_t valid = (n - base) < kSortTile ? (n - base) : kSortTile;
+  if (next_hist && next_shift >= kNextAggShift) {
+    // a high digit (often equal across a warp): aggregated increments need a
+    // uniform trip count
 #pragma unroll 4
-  for (int j = tid; j < valid; j += kSortThreads) {
-    const K k = s_keys[j];
-    const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
-    keys_out[dst] = k;
-    vals_out[dst] = s_vals[j];
+    for (int j = tid; j < kSortTile; j += kSortThreads) {
+      const bool ok = j < valid;
+      const K k = ok ? s_keys[j] : K(0);
+      if (ok) {
+        const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
+        keys_out[dst] = k;
+        vals_out[dst] = s_vals[j];
+      }
+      hist_add(sm.next_hist, digit_of(k, next_shift), ok);
+    }
+  } else if (next_hist) {  // a spread digit: plain shared atomics
+#pragma unroll 4
+    for (int j = tid; j < valid; j += kSortThreads) {
+      const K k = s_keys[j];
+      const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
+      keys_out[dst] = k;
+      vals_out[dst] = s_vals[j];
+      atomicAdd(&sm.next_hist[digit_of(k, next_shift)], 1u);
+    }
+  } else {
+#pragma unroll 4
+    for (int j = tid; j < valid; j += kSortThreads) {
+      const K k = s_keys[j];
+      const int64_t dst = sm.global_base[digit_of(k, shift)] + j;
+      keys_out[dst] = k;
+      vals_out[dst] = s_vals[j];
+    }
+  }
+  if (next_hist) {
+    __syncthreads();
+    for (int i = tid; i < kRadix; i += kSortThreads)
+      if (sm.next_hist[i]) atomicAdd(&next_hist[i], sm.next_hist[i]);
   }
   if (KX_SORT_TIMERS) {
     __syncthreads();
