@@ -180,23 +180,47 @@ __device__ void active_append(InstDev& in, int i, uint64_t uid, double P, double
 }
 
 // SlotLedger::gc's active_ part (dispatcher.cpp:111-117), owner lane only.
+__device__ __forceinline__ void prefetch_l2_last(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+// Order-preserving compaction of instance i's active table, entries loaded
+// kGcChunk at a time (one memory latency per chunk instead of per entry:
+// this runs at the end of the dispatch round, on the tick's critical path).
+constexpr int kGcChunk = 8;
 __device__ void active_gc(InstDev& in, int i, double now) {
-  int a = in.n_active[i];
+  const int a = in.n_active[i];
   const int64_t o = int64_t(i) * kActiveCap;
   const double lim = __dadd_rn(now, kTimeEpsilon);
-  for (int j = 0; j < a;) {
-    if (__dadd_rn(in.act_t0[o + j], in.act_T[o + j]) <= lim) {
-      --a;
-      in.act_uid[o + j] = in.act_uid[o + a];
-      in.act_P[o + j] = in.act_P[o + a];
-      in.act_k[o + j] = in.act_k[o + a];
-      in.act_t0[o + j] = in.act_t0[o + a];
-      in.act_T[o + j] = in.act_T[o + a];
-    } else {
-      ++j;
+  int w = 0;
+  for (int j0 = 0; j0 < a; j0 += kGcChunk) {
+    uint64_t u[kGcChunk];
+    double P[kGcChunk], k[kGcChunk], t0[kGcChunk], T[kGcChunk];
+#pragma unroll
+    for (int c = 0; c < kGcChunk; ++c) {
+      if (j0 + c < a) {
+        u[c] = in.act_uid[o + j0 + c];
+        P[c] = in.act_P[o + j0 + c];
+        k[c] = in.act_k[o + j0 + c];
+        t0[c] = in.act_t0[o + j0 + c];
+        T[c] = in.act_T[o + j0 + c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kGcChunk; ++c) {
+      if (j0 + c >= a) break;
+      if (__dadd_rn(t0[c], T[c]) <= lim) continue;  // elapsed model (dispatcher.cpp:113-117)
+      if (w != j0 + c) {
+        in.act_uid[o + w] = u[c];
+        in.act_P[o + w] = P[c];
+        in.act_k[o + w] = k[c];
+        in.act_t0[o + w] = t0[c];
+        in.act_T[o + w] = T[c];
+      }
+      ++w;
     }
   }
-  in.n_active[i] = a;
+  in.n_active[i] = w;
 }
 
 __device__ __forceinline__ Ring global_ring(const InstDev& in, int i, int ring) {
@@ -2378,6 +2402,19 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       else if (stage == 1) issue_T();
     } else if (warp == kFlushWarp) {
       flush(sbuf ^ 1);  // the previous batch's records
+      // keep the instances' active tables in L2 for the end-of-round gc
+      // (the concurrent sort streams far more than L2 holds)
+      if (act) {
+        const int64_t o = int64_t(i) * kActiveCap;
+        const int bytes = in.n_active[i] * 8;
+        for (int off = 0; off < bytes; off += 128) {
+          prefetch_l2_last(reinterpret_cast<const char*>(in.act_uid + o) + off);
+          prefetch_l2_last(reinterpret_cast<const char*>(in.act_P + o) + off);
+          prefetch_l2_last(reinterpret_cast<const char*>(in.act_k + o) + off);
+          prefetch_l2_last(reinterpret_cast<const char*>(in.act_t0 + o) + off);
+          prefetch_l2_last(reinterpret_cast<const char*>(in.act_T + o) + off);
+        }
+      }
     } else if (warp == 0) {
       if (lane == 0) {
         s_nstage[sbuf] = 0;
@@ -2593,6 +2630,7 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   if (warp == 0) {
     __syncwarp();
     flush(sbuf ^ 1);  // the last batch's records
+    if (dbg) g_disp_dbg[13] = gtimer();
     // Phase 1 ran out of prefix heads without finishing the round: hand the
     // state to the continuation (no gc yet: the round is not over).
     const bool defer_rest = (ph.phase == 1 || ph.phase == 3) && !broke && status == KX_OK && pos >= q_end &&
@@ -2612,7 +2650,11 @@ k_dispatch_batch(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     }
     if (act) {
       in.n_active[i] = nact;
+      if (dbg) g_disp_dbg[14] = gtimer();
+      if (dbg) g_disp_dbg[14] = gtimer();
       if (!defer_rest) active_gc(in, i, now);
+      if (dbg) g_disp_dbg[15] = gtimer();
+      if (dbg) g_disp_dbg[15] = gtimer();
       in.live_kv[i] = live;
       in.base_slot[i] = nbase;
       in.hi_slot[i] = hi;

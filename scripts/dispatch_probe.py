@@ -45,4 +45,6 @@ if hasattr(s.lib, "kx_debug_dispatch_timers"):
     t = list(buf)
     print("batch kernel (pool 0) us: stage", (t[1] - t[0]) / 1e3, "loop", (t[2] - t[1]) / 1e3,
           "epilogue", (t[3] - t[2]) / 1e3, "writeback", (t[4] - t[3]) / 1e3, "rows", t[5])
+    print("epilogue us: flush", (t[13] - t[2]) / 1e3, "gc slots", (t[14] - t[13]) / 1e3, "active gc",
+          (t[15] - t[14]) / 1e3, "rest", (t[3] - t[15]) / 1e3)
     print("cycles: phaseA", t[6], "phaseB", t[7], "batches", t[11], "fix", t[8], "select", t[9], "stage", t[10], "commit", t[12])
