@@ -401,6 +401,36 @@ int kx_orchestrator_dp(int64_t n_workflows, const int64_t* wf_offsets, const int
                        double prefill_rate, double decode_rate, uint64_t uid_base,
                        uint64_t* uid_out, double* pure_exec_out, double* remaining_out,
                        int32_t mem);
+/* ---- K9: profiler ingestion (distribution.cpp:91-123, profiler.cpp:20-50) ----
+ * LatencyProfiler over dense agent indices: per agent an execution and a
+ * remaining-latency EmpiricalDistribution (sorted samples, sliding window,
+ * doubling-checkpoint W1 convergence), device-resident. capacity = retained
+ * samples per distribution (>= window_cap + 1 where window_cap > 0; an
+ * unbounded kind needs room for all its samples, else KX_ERR_CAPACITY). */
+typedef struct kx_convergence_config {  /* ConvergenceConfig (distribution.hpp:36-40) */
+  uint64_t min_samples;                 /* 16 */
+  double relative_threshold;            /* 0.05 */
+  int64_t window_cap;                   /* 0 = unbounded; remaining: 4096 */
+} kx_convergence_config;
+typedef struct kx_profiler kx_profiler;
+int kx_profiler_create(int32_t n_agents, const kx_convergence_config* exec,
+                       const kx_convergence_config* remaining, int64_t capacity, int32_t device,
+                       kx_profiler** out);
+int kx_profiler_destroy(kx_profiler* p);
+/* record_execution (profiler.cpp:20-29) for n samples in order. */
+int kx_profiler_record_execution(kx_profiler* p, int64_t n, const int32_t* agent, const double* latency);
+/* record_remaining (profiler.cpp:31-50) for many completed workflows in
+ * completion order (records of workflow w: [rec_offsets[w], rec_offsets[w+1])).
+ * newly_converged[w] (nullable) = take_newly_converged() right after w. A
+ * negative sample fails the whole batch before any sample is applied. */
+int kx_profiler_record_remaining(kx_profiler* p, int64_t n_workflows, const int64_t* rec_offsets,
+                                 const int32_t* agent, const double* exec_start, const double* exec_end,
+                                 uint8_t* newly_converged);
+/* One distribution (kind 0 execution, 1 remaining): samples() (sorted, up to
+ * cap copied), size, total_added, converged, last_checkpoint_distance. */
+int kx_profiler_read(kx_profiler* p, int32_t kind, int32_t agent, int64_t cap, double* samples, int64_t* n,
+                     uint64_t* total_added, int32_t* converged, double* last_distance);
+
 /* LatencyProfiler::record_remaining's arithmetic (profiler.cpp:31-50) for
  * many completed workflows: finish = max exec_end (seeded with the first
  * record), sample[r] = finish - exec_start[r]. Synchronous. */

@@ -1036,6 +1036,82 @@ void gen_w1matrix(const std::string& dir) {
   std::printf("  w1_matrix.kxf\n");
 }
 
+// ---- K9: profiler ingestion -------------------------------------------------
+// The reference LatencyProfiler (default ProfilerConfig: remaining window
+// 4096, execution unbounded) fed workflow by workflow: after each workflow's
+// record_remaining the take_newly_converged() flag, and every record also
+// through record_execution. Agent 0 gets enough samples to slide its window;
+// agent 3 is noisy (converges late or never).
+void gen_profiler(const std::string& dir) {
+  Rng rng(909);
+  LatencyProfiler prof;
+  const int A = 4;
+  std::vector<std::string> agents;
+  for (int a = 0; a < A; ++a) agents.push_back("p" + std::to_string(a));
+  std::vector<int64_t> off{0};
+  std::vector<int32_t> agent;
+  std::vector<double> es, ee;
+  std::vector<uint8_t> newly;
+  const int W = 2600;
+  double t = 0.0;
+  for (int w = 0; w < W; ++w) {
+    std::vector<RequestRecord> recs;
+    const int nr = 1 + static_cast<int>(rng.next_u64() % 4);
+    t += rng.uniform(0.0, 0.5);
+    double cur = t;
+    for (int r = 0; r < nr; ++r) {
+      const int a = r == 0 ? 0 : static_cast<int>(rng.next_u64() % A);
+      RequestRecord rec;
+      rec.msg_id = "m-" + std::to_string(w);
+      rec.agent = agents[static_cast<std::size_t>(a)];
+      rec.exec_start = cur + rng.uniform(0.0, 0.2);
+      const double dur = a == 3 ? rng.uniform(0.01, 30.0) : 0.5 + a + rng.uniform(0.0, 0.3 * (a + 1));
+      rec.exec_end = rec.exec_start + dur;
+      cur = rec.exec_end - (r % 2 ? dur * 0.5 : 0.0);  // some overlap (parallel calls)
+      recs.push_back(rec);
+      agent.push_back(a);
+      es.push_back(rec.exec_start);
+      ee.push_back(rec.exec_end);
+      prof.record_execution(rec.agent, rec.exec_end - rec.exec_start);
+    }
+    // every fifth workflow repeats agent 0 twice more (fills its window)
+    if (w % 5 == 0) {
+      for (int r = 0; r < 2; ++r) {
+        RequestRecord rec = recs.front();
+        rec.exec_start = recs.front().exec_start + rng.uniform(0.0, 0.1);
+        recs.push_back(rec);
+        agent.push_back(0);
+        es.push_back(rec.exec_start);
+        ee.push_back(rec.exec_end);
+        prof.record_execution(rec.agent, rec.exec_end - rec.exec_start);
+      }
+    }
+    off.push_back(static_cast<int64_t>(agent.size()));
+    prof.record_remaining(recs);
+    newly.push_back(prof.take_newly_converged() ? 1 : 0);
+  }
+  Kxf k;
+  k.scalar_i("n_agents", A);
+  k.i64("off", off);
+  k.i32("agent", agent);
+  k.f64("exec_start", es);
+  k.f64("exec_end", ee);
+  k.u8("newly", newly);
+  for (int kind = 0; kind < 2; ++kind)
+    for (int a = 0; a < A; ++a) {
+      const std::string pre = std::string(kind ? "rem" : "exec") + std::to_string(a) + ".";
+      const EmpiricalDistribution* d =
+          kind ? &prof.remaining_distribution(agents[static_cast<std::size_t>(a)])->dist
+               : prof.exec_distribution(agents[static_cast<std::size_t>(a)]);
+      k.f64(pre + "samples", d->samples());
+      k.u64(pre + "total", {d->total_added()});
+      k.u8(pre + "converged", {static_cast<uint8_t>(d->converged() ? 1 : 0)});
+      k.f64(pre + "last", {d->last_checkpoint_distance()});
+    }
+  k.write(dir + "/profiler.kxf");
+  std::printf("  profiler.kxf: %d workflows, %zu records\n", W, agent.size());
+}
+
 int main(int argc, char** argv) {
   const std::string dir = argc > 1 ? argv[1] : "tests/golden";
   std::filesystem::create_directories(dir);
@@ -1066,5 +1142,6 @@ int main(int argc, char** argv) {
   gen_remaining(dir);
   gen_accuracy(dir);
   gen_w1matrix(dir);
+  gen_profiler(dir);
   return 0;
 }

@@ -598,6 +598,115 @@ int64_t kxo_dispatch_round_waiting(kxo_pool* p, int dispatch_policy, double stat
   return nrows;
 }
 
+/* ---- EmpiricalDistribution (distribution.cpp:88-123) -------------------------- */
+
+struct kxo_dist {
+  uint64_t min_samples;
+  double thr;
+  int64_t window_cap;
+  double* sorted;
+  int64_t n, cap_s;
+  double* fifo; /* arrival_order_ as a growable ring */
+  int64_t f_head, f_n, cap_f;
+  double* snap;
+  int64_t snap_n;
+  uint64_t total, next_cp;
+  int converged;
+  double last;
+};
+
+kxo_dist* kxo_dist_new(uint64_t min_samples, double relative_threshold, int64_t window_cap) {
+  kxo_dist* d = (kxo_dist*)calloc(1, sizeof(kxo_dist));
+  d->min_samples = min_samples;
+  d->thr = relative_threshold;
+  d->window_cap = window_cap;
+  d->next_cp = min_samples; /* next_checkpoint_(cfg.min_samples) */
+  d->last = -1.0;
+  return d;
+}
+
+void kxo_dist_free(kxo_dist* d) {
+  if (!d) return;
+  free(d->sorted);
+  free(d->fifo);
+  free(d->snap);
+  free(d);
+}
+
+static int64_t lower_bound_d(const double* s, int64_t n, double v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (s[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+int kxo_dist_add(kxo_dist* d, double value) {
+  if (value < 0.0) return -1; /* distribution.cpp:92-94 */
+  if (d->n == d->cap_s) {
+    d->cap_s = d->cap_s ? 2 * d->cap_s : 64;
+    d->sorted = (double*)realloc(d->sorted, (size_t)d->cap_s * sizeof(double));
+  }
+  const int64_t pos = lower_bound_d(d->sorted, d->n, value); /* sorted_.insert(lower_bound) */
+  memmove(d->sorted + pos + 1, d->sorted + pos, (size_t)(d->n - pos) * sizeof(double));
+  d->sorted[pos] = value;
+  d->n += 1;
+  if (d->window_cap > 0) {
+    if (d->f_n == d->cap_f) { /* grow the ring, oldest first */
+      const int64_t nc = d->cap_f ? 2 * d->cap_f : 64;
+      double* nf = (double*)malloc((size_t)nc * sizeof(double));
+      for (int64_t j = 0; j < d->f_n; ++j) nf[j] = d->fifo[(d->f_head + j) % d->cap_f];
+      free(d->fifo);
+      d->fifo = nf;
+      d->cap_f = nc;
+      d->f_head = 0;
+    }
+    d->fifo[(d->f_head + d->f_n) % d->cap_f] = value; /* arrival_order_.push_back */
+    d->f_n += 1;
+    if (d->f_n > d->window_cap) {
+      const double oldest = d->fifo[d->f_head];
+      d->f_head = (d->f_head + 1) % d->cap_f;
+      d->f_n -= 1;
+      const int64_t e = lower_bound_d(d->sorted, d->n, oldest);
+      memmove(d->sorted + e, d->sorted + e + 1, (size_t)(d->n - e - 1) * sizeof(double));
+      d->n -= 1;
+    }
+  }
+  d->total += 1;
+  int became = 0;
+  if (d->total == d->next_cp) { /* check_convergence, distribution.cpp:113-123 */
+    if (d->snap_n > 0) {
+      const double w = kxo_wasserstein_1d(d->snap, d->snap_n, d->sorted, d->n);
+      d->last = w;
+      double s = 0.0;
+      for (int64_t j = 0; j < d->n; ++j) s += d->sorted[j]; /* mean(), distribution.cpp:125-129 */
+      const double t = d->thr * (s / (double)d->n);
+      const double tau = t > 1e-12 ? t : 1e-12;
+      if (w < tau) {
+        became = !d->converged;
+        d->converged = 1;
+      }
+    }
+    d->snap = (double*)realloc(d->snap, (size_t)(d->n > 0 ? d->n : 1) * sizeof(double));
+    memcpy(d->snap, d->sorted, (size_t)d->n * sizeof(double));
+    d->snap_n = d->n;
+    d->next_cp *= 2;
+  }
+  return became;
+}
+
+int64_t kxo_dist_read(const kxo_dist* d, double* out, int64_t cap, uint64_t* total_added, int32_t* converged,
+                      double* last_distance) {
+  if (out)
+    for (int64_t j = 0; j < d->n && j < cap; ++j) out[j] = d->sorted[j];
+  if (total_added) *total_added = d->total;
+  if (converged) *converged = d->converged;
+  if (last_distance) *last_distance = d->last;
+  return d->n;
+}
+
 /* ---- pairwise_sorting_accuracy (priority.cpp:165-189) ------------------------ */
 int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,
                           int32_t scope_all, double* acc, uint64_t* pairs_out) {

@@ -135,6 +135,17 @@ int64_t kxo_dispatch_round_waiting(kxo_pool* p, int dispatch_policy, double stat
                                    int64_t row_cap, kxo_admission* adm, int64_t adm_cap, int64_t* n_adm,
                                    int32_t* status);
 
+/* EmpiricalDistribution (distribution.cpp:88-123): sorted samples, sliding
+ * window, doubling-checkpoint convergence. add returns -1 on a negative
+ * sample (invalid_argument), 1 when this add converged it, else 0. */
+typedef struct kxo_dist kxo_dist;
+kxo_dist* kxo_dist_new(uint64_t min_samples, double relative_threshold, int64_t window_cap);
+void kxo_dist_free(kxo_dist* d);
+int kxo_dist_add(kxo_dist* d, double value);
+/* sorted samples (up to cap copied); returns the size */
+int64_t kxo_dist_read(const kxo_dist* d, double* out, int64_t cap, uint64_t* total_added, int32_t* converged,
+                      double* last_distance);
+
 /* pairwise_sorting_accuracy (priority.cpp:165-189), O(N^2): returns 0 and
  * sets *acc when pairs > 0, returns 1 (nullopt) otherwise. */
 int kxo_pairwise_accuracy(int64_t n, const int32_t* agent, const double* rem, const uint8_t* present,

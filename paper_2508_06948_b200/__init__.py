@@ -6,8 +6,8 @@ include/kairos_b200.hpp. This Python package is a thin ctypes handle used by
 the tests and bench.py.
 """
 from ._abi import KxError, LIB_PATH, load  # noqa: F401
-from .sched import (DeviceScheduler, DispatcherConfig, InstanceProfile,  # noqa: F401
+from .sched import (DeviceScheduler, DispatcherConfig, InstanceProfile, Profiler,  # noqa: F401
                     orchestrator_dp, record_remaining, w1_matrix)
 
 __all__ = ["KxError", "LIB_PATH", "load", "DeviceScheduler", "DispatcherConfig",
-           "InstanceProfile", "orchestrator_dp", "record_remaining", "w1_matrix"]
+           "InstanceProfile", "Profiler", "orchestrator_dp", "record_remaining", "w1_matrix"]

@@ -92,6 +92,10 @@ class kx_replica_results(C.Structure):
         "scalars", "counts", "metrics", "histogram"]]
 
 
+class kx_convergence_config(C.Structure):
+    _fields_ = [("min_samples", C.c_uint64), ("relative_threshold", C.c_double), ("window_cap", C.c_int64)]
+
+
 class kx_phase_stat(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("total_ms", C.c_double), ("launches", C.c_int64),
                 ("alg_bytes", C.c_double)]
@@ -148,6 +152,13 @@ SIGNATURES = {
                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "kx_aggregate_metrics": (C.c_int, [C.c_int32, _P, _P]),
     "kx_w1_matrix": (C.c_int, [C.c_int32, _P, _P, _P]),
+    "kx_profiler_create": (C.c_int, [C.c_int32, C.POINTER(kx_convergence_config),
+                                     C.POINTER(kx_convergence_config), C.c_int64, C.c_int32, C.POINTER(_P)]),
+    "kx_profiler_destroy": (C.c_int, [_P]),
+    "kx_profiler_record_execution": (C.c_int, [_P, C.c_int64, _P, _P]),
+    "kx_profiler_record_remaining": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P]),
+    "kx_profiler_read": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _P, C.POINTER(C.c_int64),
+                                   C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
     "kx_graph_capture_begin": (C.c_int, [_P]),
     "kx_graph_capture_end": (C.c_int, [_P]),
     "kx_graph_launch": (C.c_int, [_P]),

@@ -18,6 +18,7 @@
 #include "kx_dispatch.cuh"
 #include "kx_engine.cuh"
 #include "kx_order.cuh"
+#include "kx_profiler.cuh"
 #include "kx_state.cuh"
 
 namespace kx {
@@ -1086,6 +1087,60 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
 }  // namespace
 
 // ===========================================================================
+// LatencyProfiler state on the device (K9, kx_profiler.cu): per agent an
+// execution and a remaining-latency EmpiricalDistribution.
+struct kx_profiler {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int32_t n_agents = 0;
+  int64_t cap = 0;
+  kx_convergence_config cfg[2]{};
+  DistDev dd{};
+  DistCfg* d_cfg = nullptr;
+  void* blob = nullptr;
+  int* status = nullptr;
+};
+
+namespace {
+
+// Applies a batch grouped by distribution: off[n_dist + 1], values and item
+// (the caller's record index of each value) in per-distribution arrival
+// order. Returns conv_item per distribution.
+std::vector<int64_t> profiler_ingest(kx_profiler* p, const std::vector<int64_t>& off,
+                                     const std::vector<double>& values, const std::vector<int64_t>& item) {
+  const int32_t nd = 2 * p->n_agents;
+  const size_t nv = values.size();
+  int64_t* d_off = nullptr;
+  double* d_v = nullptr;
+  int64_t* d_it = nullptr;
+  cudaStream_t st = p->stream;
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_off), off.size() * 8, st));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_v), std::max<size_t>(nv, 1) * 8, st));
+  KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_it), std::max<size_t>(nv, 1) * 8, st));
+  KX_CUDA(cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+  if (nv) {
+    KX_CUDA(cudaMemcpyAsync(d_v, values.data(), nv * 8, cudaMemcpyHostToDevice, st));
+    KX_CUDA(cudaMemcpyAsync(d_it, item.data(), nv * 8, cudaMemcpyHostToDevice, st));
+  }
+  KX_CUDA(cudaMemsetAsync(p->status, 0, sizeof(int), st));
+  KX_CUDA(cudaMemsetAsync(p->dd.conv_item, 0xff, size_t(nd) * 8, st));  // -1: untouched this batch
+  launch_dist_ingest(p->dd, nd, d_off, d_v, d_it, p->status, st);
+  std::vector<int64_t> conv(static_cast<size_t>(nd));
+  int status = 0;
+  KX_CUDA(cudaMemcpyAsync(conv.data(), p->dd.conv_item, size_t(nd) * 8, cudaMemcpyDeviceToHost, st));
+  KX_CUDA(cudaMemcpyAsync(&status, p->status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KX_CUDA(cudaFreeAsync(d_off, st));
+  KX_CUDA(cudaFreeAsync(d_v, st));
+  KX_CUDA(cudaFreeAsync(d_it, st));
+  KX_CUDA(cudaStreamSynchronize(st));
+  if (status == KX_ERR_CAPACITY)
+    fail(KX_ERR_CAPACITY, "profiler distribution exceeds its sample capacity (raise capacity)");
+  if (status != KX_OK) fail(status, "profiler ingestion failed");
+  return conv;
+}
+
+}  // namespace
+
 extern "C" {
 
 int kx_abi_version(void) { return KX_ABI_VERSION; }
@@ -1848,6 +1903,185 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
     if (pairs) *pairs = p;
     if (correct) *correct = c;
     if (accuracy) *accuracy = p ? c / static_cast<double>(p) : std::nan("");
+  });
+}
+
+int kx_profiler_create(int32_t n_agents, const kx_convergence_config* exec,
+                       const kx_convergence_config* remaining, int64_t capacity, int32_t device,
+                       kx_profiler** out) {
+  return guard([&] {
+    require(out && exec && remaining, "null argument");
+    require(n_agents > 0, "no agents");
+    require(capacity > 0, "capacity must be positive");
+    for (const kx_convergence_config* c : {exec, remaining}) {
+      require(c->window_cap >= 0, "negative window_cap");
+      if (c->window_cap > 0) require(capacity >= c->window_cap + 1, "capacity below window_cap + 1");
+    }
+    ensure_device(device);
+    auto p = std::make_unique<kx_profiler>();
+    p->device = device;
+    p->n_agents = n_agents;
+    p->cap = capacity;
+    p->cfg[0] = *exec;
+    p->cfg[1] = *remaining;
+    KX_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const size_t nd = size_t(2) * n_agents, C = static_cast<size_t>(capacity);
+    Layout L;
+    const size_t o_s = L.take<double>(nd * C), o_r = L.take<double>(nd * C), o_sn = L.take<double>(nd * C),
+                 o_n = L.take<int64_t>(nd), o_h = L.take<int64_t>(nd), o_snn = L.take<int64_t>(nd),
+                 o_t = L.take<uint64_t>(nd), o_cp = L.take<uint64_t>(nd), o_c = L.take<uint8_t>(nd),
+                 o_l = L.take<double>(nd), o_ci = L.take<int64_t>(nd), o_cfg = L.take<DistCfg>(nd),
+                 o_st = L.take<int>(1);
+    KX_CUDA(cudaMalloc(&p->blob, L.off));
+    KX_CUDA(cudaMemset(p->blob, 0, L.off));
+    char* b = static_cast<char*>(p->blob);
+    DistDev& dd = p->dd;
+    dd.cap = capacity;
+    dd.sorted = reinterpret_cast<double*>(b + o_s);
+    dd.ring = reinterpret_cast<double*>(b + o_r);
+    dd.snap = reinterpret_cast<double*>(b + o_sn);
+    dd.n = reinterpret_cast<int64_t*>(b + o_n);
+    dd.ring_head = reinterpret_cast<int64_t*>(b + o_h);
+    dd.snap_n = reinterpret_cast<int64_t*>(b + o_snn);
+    dd.total = reinterpret_cast<uint64_t*>(b + o_t);
+    dd.next_cp = reinterpret_cast<uint64_t*>(b + o_cp);
+    dd.conv = reinterpret_cast<uint8_t*>(b + o_c);
+    dd.last_dist = reinterpret_cast<double*>(b + o_l);
+    dd.conv_item = reinterpret_cast<int64_t*>(b + o_ci);
+    p->d_cfg = reinterpret_cast<DistCfg*>(b + o_cfg);
+    dd.cfg = p->d_cfg;
+    p->status = reinterpret_cast<int*>(b + o_st);
+    // EmpiricalDistribution(cfg): next_checkpoint_ = min_samples, last distance -1
+    std::vector<DistCfg> cfgs(nd);
+    std::vector<uint64_t> ncp(nd);
+    std::vector<double> last(nd, -1.0);
+    for (size_t d = 0; d < nd; ++d) {
+      const kx_convergence_config& c = p->cfg[d / size_t(n_agents)];
+      cfgs[d] = DistCfg{c.min_samples, c.relative_threshold, c.window_cap};
+      ncp[d] = c.min_samples;
+    }
+    KX_CUDA(cudaMemcpy(p->d_cfg, cfgs.data(), nd * sizeof(DistCfg), cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(dd.next_cp, ncp.data(), nd * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaMemcpy(dd.last_dist, last.data(), nd * 8, cudaMemcpyHostToDevice));
+    *out = p.release();
+  });
+}
+
+int kx_profiler_destroy(kx_profiler* p) {
+  return guard([&] {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->blob) cudaFree(p->blob);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+  });
+}
+
+int kx_profiler_record_execution(kx_profiler* p, int64_t n, const int32_t* agent, const double* latency) {
+  return guard([&] {
+    require(p, "null handle");
+    require(n >= 0, "negative count");
+    if (n == 0) return;
+    require(agent && latency, "null argument");
+    const int32_t A = p->n_agents;
+    std::vector<int64_t> off(size_t(2) * A + 1, 0);
+    for (int64_t j = 0; j < n; ++j) {
+      require(agent[j] >= 0 && agent[j] < A, "agent index out of range");
+      // LatencyProfiler::record_execution (profiler.cpp:20-29)
+      if (!(latency[j] >= 0.0)) fail(KX_ERR_INVALID, "negative execution latency");
+      ++off[size_t(agent[j]) + 1];
+    }
+    for (size_t d = 1; d < off.size(); ++d) off[d] += off[d - 1];
+    std::vector<int64_t> fill(off.begin(), off.end() - 1), item(static_cast<size_t>(n));
+    std::vector<double> values(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) {
+      const int64_t k = fill[size_t(agent[j])]++;
+      values[size_t(k)] = latency[j];
+      item[size_t(k)] = j;
+    }
+    KX_CUDA(cudaSetDevice(p->device));
+    profiler_ingest(p, off, values, item);
+  });
+}
+
+int kx_profiler_record_remaining(kx_profiler* p, int64_t n_workflows, const int64_t* rec_offsets,
+                                 const int32_t* agent, const double* exec_start, const double* exec_end,
+                                 uint8_t* newly_converged) {
+  return guard([&] {
+    require(p, "null handle");
+    require(n_workflows >= 0, "negative count");
+    if (n_workflows == 0) return;
+    require(rec_offsets && rec_offsets[0] == 0, "offsets must start at 0");
+    const int64_t nr = rec_offsets[n_workflows];
+    require(nr == 0 || (agent && exec_start && exec_end), "null argument");
+    const int32_t A = p->n_agents;
+    std::vector<double> sample(static_cast<size_t>(nr));
+    std::vector<int64_t> off(size_t(2) * A + 1, 0);
+    for (int64_t w = 0; w < n_workflows; ++w) {
+      const int64_t b = rec_offsets[w], e = rec_offsets[w + 1];
+      require(e >= b, "offsets must be non-decreasing");
+      if (b == e) continue;  // record_remaining returns on an empty instance
+      // finish = max exec_end seeded with the first record (profiler.cpp:33-35)
+      double finish = exec_end[b];
+      for (int64_t r = b; r < e; ++r) finish = finish < exec_end[r] ? exec_end[r] : finish;
+      for (int64_t r = b; r < e; ++r) {
+        require(agent[r] >= 0 && agent[r] < A, "agent index out of range");
+        sample[size_t(r)] = finish - exec_start[r];
+        // EmpiricalDistribution::add rejects negatives (distribution.cpp:92-94);
+        // the batch is validated before any sample is applied
+        if (!(sample[size_t(r)] >= 0.0)) fail(KX_ERR_INVALID, "latency sample must be non-negative");
+        ++off[size_t(A + agent[r]) + 1];
+      }
+    }
+    for (size_t d = 1; d < off.size(); ++d) off[d] += off[d - 1];
+    std::vector<int64_t> fill(off.begin(), off.end() - 1), item(static_cast<size_t>(nr));
+    std::vector<double> values(static_cast<size_t>(nr));
+    for (int64_t w = 0; w < n_workflows; ++w)
+      for (int64_t r = rec_offsets[w]; r < rec_offsets[w + 1]; ++r) {
+        const int64_t k = fill[size_t(A + agent[r])]++;
+        values[size_t(k)] = sample[size_t(r)];
+        item[size_t(k)] = w;
+      }
+    KX_CUDA(cudaSetDevice(p->device));
+    const std::vector<int64_t> conv = profiler_ingest(p, off, values, item);
+    if (newly_converged) {
+      std::memset(newly_converged, 0, size_t(n_workflows));
+      for (int32_t a = 0; a < A; ++a) {
+        const int64_t w = conv[size_t(A + a)];
+        if (w >= 0 && w < n_workflows) newly_converged[w] = 1;
+      }
+    }
+  });
+}
+
+int kx_profiler_read(kx_profiler* p, int32_t kind, int32_t agent, int64_t cap, double* samples, int64_t* n,
+                     uint64_t* total_added, int32_t* converged, double* last_distance) {
+  return guard([&] {
+    require(p, "null handle");
+    require(kind == 0 || kind == 1, "kind must be 0 (execution) or 1 (remaining)");
+    require(agent >= 0 && agent < p->n_agents, "agent index out of range");
+    KX_CUDA(cudaSetDevice(p->device));
+    const int64_t d = int64_t(kind) * p->n_agents + agent;
+    int64_t nn = 0;
+    uint64_t tot = 0;
+    uint8_t cv = 0;
+    double ld = 0.0;
+    cudaStream_t st = p->stream;
+    KX_CUDA(cudaMemcpyAsync(&nn, p->dd.n + d, 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaMemcpyAsync(&tot, p->dd.total + d, 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaMemcpyAsync(&cv, p->dd.conv + d, 1, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaMemcpyAsync(&ld, p->dd.last_dist + d, 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaStreamSynchronize(st));
+    if (n) *n = nn;
+    if (total_added) *total_added = tot;
+    if (converged) *converged = cv;
+    if (last_distance) *last_distance = ld;
+    const int64_t m = std::min(nn, cap);
+    if (samples && m > 0) {
+      KX_CUDA(cudaMemcpyAsync(samples, p->dd.sorted + d * p->cap, size_t(m) * 8, cudaMemcpyDeviceToHost, st));
+      KX_CUDA(cudaStreamSynchronize(st));
+    }
   });
 }
 

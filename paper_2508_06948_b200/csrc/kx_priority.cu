@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "kx_common.cuh"
+#include "kx_w1.cuh"
 
 namespace kx {
 
@@ -35,19 +36,7 @@ __global__ void k_w1_matrix(int32_t n_agents, const int64_t* __restrict__ off,
     const double* b = j < n_agents ? samples + off[j] : &anchor;
     const uint64_t na = i < n_agents ? uint64_t(off[i + 1] - off[i]) : 1u;
     const uint64_t nb = j < n_agents ? uint64_t(off[j + 1] - off[j]) : 1u;
-    const uint64_t total = na * nb;
-    uint64_t cur = 0, ia = 0, jb = 0;
-    double acc = 0.0;
-    while (cur < total) {
-      const uint64_t a_next = (ia + 1) * nb;
-      const uint64_t b_next = (jb + 1) * na;
-      const uint64_t nxt = a_next < b_next ? a_next : b_next;
-      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(nxt - cur), fabs(__dsub_rn(a[ia], b[jb]))));
-      if (a_next == nxt) ++ia;
-      if (b_next == nxt) ++jb;
-      cur = nxt;
-    }
-    const double w = __ddiv_rn(acc, static_cast<double>(total));
+    const double w = w1_walk(a, na, b, nb);
     d[i * m + j] = w;
     d[j * m + i] = w;
   }

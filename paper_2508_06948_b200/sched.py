@@ -339,6 +339,61 @@ def sorting_accuracy(agent, remaining, present=None, scope="cross_agent"):
     return (None if pairs.value == 0 else acc.value), pairs.value, correct.value
 
 
+class Profiler:
+    """LatencyProfiler (profiler.hpp:49-90) on the device (K9): per agent an
+    execution and a remaining-latency EmpiricalDistribution. Configs are
+    (min_samples, relative_threshold, window_cap) (distribution.hpp:36-40)."""
+
+    EXECUTION, REMAINING = 0, 1
+
+    def __init__(self, n_agents: int, exec_cfg=(16, 0.05, 0), remaining_cfg=(16, 0.05, 4096),
+                 capacity: int = 8192, device: int = 0):
+        self.lib = _abi.load()
+        self.n_agents = n_agents
+        ec = _abi.kx_convergence_config(*exec_cfg)
+        rc = _abi.kx_convergence_config(*remaining_cfg)
+        h = C.c_void_p()
+        check(self.lib.kx_profiler_create(n_agents, C.byref(ec), C.byref(rc), capacity, device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kx_profiler_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def record_execution(self, agent, latency):
+        a = np.ascontiguousarray(agent, np.int32)
+        v = np.ascontiguousarray(latency, np.float64)
+        check(self.lib.kx_profiler_record_execution(self.h, len(a), ptr(a), ptr(v)))
+
+    def record_remaining(self, rec_offsets, agent, exec_start, exec_end):
+        """Completed workflows in order; returns take_newly_converged() per workflow."""
+        off = np.ascontiguousarray(rec_offsets, np.int64)
+        a = np.ascontiguousarray(agent, np.int32)
+        es = np.ascontiguousarray(exec_start, np.float64)
+        ee = np.ascontiguousarray(exec_end, np.float64)
+        newly = np.zeros(max(len(off) - 1, 0), np.uint8)
+        check(self.lib.kx_profiler_record_remaining(self.h, len(off) - 1, ptr(off), ptr(a), ptr(es), ptr(ee),
+                                                    ptr(newly)))
+        return newly
+
+    def read(self, kind: int, agent: int):
+        """(sorted samples, total_added, converged, last_checkpoint_distance)."""
+        n, tot, cv, last = C.c_int64(), C.c_uint64(), C.c_int32(), C.c_double()
+        check(self.lib.kx_profiler_read(self.h, kind, agent, 0, None, C.byref(n), C.byref(tot), C.byref(cv),
+                                        C.byref(last)))
+        out = np.zeros(n.value, np.float64)
+        check(self.lib.kx_profiler_read(self.h, kind, agent, n.value, ptr(out), C.byref(n), C.byref(tot),
+                                        C.byref(cv), C.byref(last)))
+        return out, tot.value, bool(cv.value), last.value
+
+
 def w1_matrix(sample_sets):
     """§8(f)2: build_distance_matrix_from_samples (priority.cpp:15-65) on the
     device. sample_sets: per-agent sorted sample arrays in label order; returns

@@ -92,6 +92,13 @@ def lib():
             C.POINTER(Pool), C.c_int, C.c_double, C.c_int, C.POINTER(C.c_int64), P, C.c_int64, C.c_int32,
             C.POINTER(Queue), C.POINTER(Tables), P, C.c_int64, C.c_double, C.c_int32, P, C.c_int64, P,
             C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.kxo_dist_new.restype = P
+        L.kxo_dist_new.argtypes = [C.c_uint64, C.c_double, C.c_int64]
+        L.kxo_dist_free.argtypes = [P]
+        L.kxo_dist_add.argtypes = [P, C.c_double]
+        L.kxo_dist_read.restype = C.c_int64
+        L.kxo_dist_read.argtypes = [P, P, C.c_int64, C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_double)]
         L.kxo_pairwise_accuracy.argtypes = [C.c_int64, P, P, P, C.c_int32, C.POINTER(C.c_double),
                                             C.POINTER(C.c_uint64)]
         L.kxo_finalize.argtypes = [C.c_int64, P, P, P, P, C.c_double, C.c_double, C.c_uint64, P, P, P]
@@ -318,3 +325,48 @@ def pairwise_accuracy(agent, rem, present=None, scope_all=False):
     acc, pairs = C.c_double(), C.c_uint64()
     rc = lib().kxo_pairwise_accuracy(len(a), _p(a), _p(r), _p(p), int(scope_all), C.byref(acc), C.byref(pairs))
     return (None if rc else acc.value), pairs.value
+
+
+class Dist:
+    """EmpiricalDistribution restatement (kxo_dist)."""
+
+    def __init__(self, min_samples=16, threshold=0.05, window_cap=0):
+        self.h = lib().kxo_dist_new(min_samples, threshold, window_cap)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().kxo_dist_free(self.h)
+            self.h = None
+
+    def add(self, v):
+        return lib().kxo_dist_add(self.h, float(v))
+
+    def read(self):
+        tot, cv, last = C.c_uint64(), C.c_int32(), C.c_double()
+        n = lib().kxo_dist_read(self.h, None, 0, C.byref(tot), C.byref(cv), C.byref(last))
+        out = np.zeros(n, np.float64)
+        lib().kxo_dist_read(self.h, _p(out), n, C.byref(tot), C.byref(cv), C.byref(last))
+        return out, tot.value, cv.value, last.value
+
+
+def profiler_replay(n_agents, off, agent, es, ee, exec_cfg=(16, 0.05, 0), rem_cfg=(16, 0.05, 4096)):
+    """LatencyProfiler replay: record_execution of every record, then
+    record_remaining per workflow; returns (exec dists, rem dists, newly[w])."""
+    ex = [Dist(*exec_cfg) for _ in range(n_agents)]
+    rm = [Dist(*rem_cfg) for _ in range(n_agents)]
+    newly = np.zeros(len(off) - 1, np.uint8)
+    for w in range(len(off) - 1):
+        b, e = int(off[w]), int(off[w + 1])
+        for r in range(b, e):
+            assert ex[agent[r]].add(ee[r] - es[r]) >= 0
+        if b == e:
+            continue
+        fin = ee[b]
+        for r in range(b, e):
+            fin = ee[r] if fin < ee[r] else fin
+        for r in range(b, e):
+            got = rm[agent[r]].add(fin - es[r])
+            assert got >= 0
+            if got == 1:
+                newly[w] = 1
+    return ex, rm, newly

@@ -193,3 +193,20 @@ def test_waiting_rounds_match_reference(name):
             assert np.array_equal(pool.waiting_uids(i), rd["end_w.uid"][rd["end_w.inst"] == i]), (r, i)
         n_adm += len(adm)
     assert n_adm > 0
+
+
+def test_profiler_matches_reference():
+    """EmpiricalDistribution restatement vs the reference LatencyProfiler
+    (profiler.kxf: sliding 4096 window, doubling checkpoints, W1 convergence,
+    take_newly_converged per workflow)."""
+    d = kxf.read("profiler.kxf")
+    A = int(d["n_agents"][0])
+    ex, rm, newly = O.profiler_replay(A, d["off"], d["agent"], d["exec_start"], d["exec_end"])
+    assert np.array_equal(newly, d["newly"])
+    for kind, dists in (("exec", ex), ("rem", rm)):
+        for a in range(A):
+            s, tot, cv, last = dists[a].read()
+            p = f"{kind}{a}."
+            assert np.array_equal(bits(s), bits(d[p + "samples"])), p
+            assert tot == int(d[p + "total"][0]) and cv == int(d[p + "converged"][0]), p
+            assert bits(last) == bits(d[p + "last"][0]), p
