@@ -277,7 +277,7 @@ int64_t kx_launch_count(void);
  * StaticThreshold dispatch. */
 typedef struct kx_engine_config {
   int32_t n_instances;
-  int32_t scheduler;              /* KX_SCHED_FCFS / TOPO / ORACLE */
+  int32_t scheduler;              /* KX_SCHED_KAIROS / FCFS / TOPO / ORACLE */
   const kx_instance* instances;   /* pool ignored */
   kx_dispatcher_config dispatcher;
   int32_t n_agents;
@@ -289,6 +289,11 @@ typedef struct kx_engine_config {
   int32_t device;
   uint64_t max_events;            /* 0 = 2e8 (engine.cpp:25) */
   double warmup_seconds;          /* MetricsOptions::warmup_seconds (metrics.hpp:21-25) */
+  /* KairosScheduler (scheduler.hpp:94-133): agent indices in AgentId order
+   * (std::map<AgentId,...> iteration order, the W1 matrix's label order);
+   * NULL = index order. Rebuild every N completed workflows (0 = 256). */
+  const int32_t* agent_order;
+  uint64_t kairos_rebuild_interval;
 } kx_engine_config;
 
 /* Replicas concatenated (host arrays). Replica r owns workflows
@@ -335,6 +340,10 @@ typedef struct kx_replica_results {
    * total queue seconds, decode time fraction, sim end time, latency count */
   double* metrics;
   uint32_t* histogram;            /* [R*256] token-latency bins: floor((log2 x + 16) * 8) */
+  /* Kairos: final PriorityTable::priority_key per agent index [R*n_agents]
+   * and the number of tables built per replica [R] (NULL = not wanted) */
+  double* priority_keys;
+  int64_t* table_versions;
 } kx_replica_results;
 
 /* aggregate_metrics (metrics.cpp:90-123) over per-replica metric rows in

@@ -243,7 +243,8 @@ extern "C" int kxref_sim_run(
     uint64_t* c_uid, double* c_exec_start, double* c_exec_end, int32_t* c_instance,
     double* c_first_enqueue, double* c_queue_seconds, int32_t* c_episodes, int32_t* c_preemptions,
     int64_t* w_index, double* w_finish, int64_t* w_output_tokens, int64_t* w_calls,
-    double* scalars, int64_t* n_calls_done, int64_t* n_wf_done) {
+    double* scalars, int64_t* n_calls_done, int64_t* n_wf_done, double* pk_out,
+    int64_t* table_version_out) {
   try {
     WorkloadRealization real;
     for (int64_t w = 0; w < n_wf; ++w) {
@@ -349,6 +350,13 @@ extern "C" int kxref_sim_run(
                         m.decode_time_fraction,
                         m.total_queue_seconds};
     for (std::size_t j = 0; j < sizeof(s) / sizeof(s[0]); ++j) scalars[j] = s[j];
+    // KairosScheduler's final table (scheduler.hpp:120-122): priority_key per
+    // built-in agent index and the table version (= tables built).
+    if (const PriorityTable* t = sched->table()) {
+      if (pk_out)
+        for (int a = 0; a < 10; ++a) pk_out[a] = t->priority_key(kBuiltin[a]);
+      if (table_version_out) *table_version_out = static_cast<int64_t>(t->version);
+    }
     return 0;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "kxref_sim_run: %s\n", e.what());

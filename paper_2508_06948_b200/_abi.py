@@ -76,7 +76,8 @@ class kx_engine_config(C.Structure):
                 ("n_agents", C.c_int32), ("slot_ring", C.c_int32), ("topo_depth", C.c_void_p),
                 ("dispatch_period", C.c_double), ("recompute_fraction", C.c_double),
                 ("heap_capacity", C.c_int32), ("device", C.c_int32), ("max_events", C.c_uint64),
-                ("warmup_seconds", C.c_double)]
+                ("warmup_seconds", C.c_double), ("agent_order", C.c_void_p),
+                ("kairos_rebuild_interval", C.c_uint64)]
 
 
 class kx_replica_batch(C.Structure):
@@ -89,7 +90,7 @@ class kx_replica_results(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in [
         "call_order", "exec_start", "exec_end", "instance", "first_enqueue", "queue_seconds",
         "episodes", "preemptions", "wf_order", "wf_finish", "wf_output_tokens", "wf_calls",
-        "scalars", "counts", "metrics", "histogram"]]
+        "scalars", "counts", "metrics", "histogram", "priority_keys", "table_versions"]]
 
 
 class kx_convergence_config(C.Structure):

@@ -866,13 +866,13 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   require(cfg && b && out, "null argument");
   require(cfg->n_instances >= 1 && cfg->n_instances <= 32 && cfg->instances,
           "engine supports 1..32 instances per replica");
-  require(cfg->scheduler == KX_SCHED_FCFS || cfg->scheduler == KX_SCHED_TOPO ||
-              cfg->scheduler == KX_SCHED_ORACLE,
-          "replica engine supports the fcfs, topo_depth and oracle schedulers");
+  require(cfg->scheduler >= KX_SCHED_KAIROS && cfg->scheduler <= KX_SCHED_ORACLE, "unknown scheduler");
   const auto& dc = cfg->dispatcher;
   require(dc.policy >= 0 && dc.policy <= 2, "unknown dispatcher policy");
-  require(dc.policy != KX_DISPATCH_TIME_SLOT || dc.oracle_expected_time,
-          "time_slot dispatch in the replica engine needs oracle_expected_time");
+  const bool kairos = cfg->scheduler == KX_SCHED_KAIROS;
+  // expected_exec_time only feeds TimeSlot's try_place (dispatcher.cpp:207-250)
+  const bool profile_T = dc.policy == KX_DISPATCH_TIME_SLOT && !dc.oracle_expected_time;
+  require(!kairos || cfg->n_agents <= kKairosMaxAgents, "kairos replica engine supports up to 32 agents");
   require(dc.slot_len > 0.0, "slot_len must be positive");
   require(b->n_replicas >= 1, "no replicas");
   require(cfg->n_agents >= 1, "n_agents must be positive");
@@ -965,6 +965,33 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   in.k = A.upload(ik.data(), NI);
   in.prefill = A.upload(ipf.data(), NI);
   in.max_batch = A.upload(imb.data(), NI);
+  // Profiler layout per (replica, agent): one exec slot per call of the
+  // agent (each call completes once), a remaining window of min(calls, 4097).
+  const int NA = cfg->n_agents;
+  std::vector<int64_t> exec_off(size_t(R) * NA + 1, 0), rem_off(size_t(R) * NA + 1, 0);
+  std::vector<int32_t> agent_order(NA);
+  for (int a = 0; a < NA; ++a) agent_order[a] = cfg->agent_order ? cfg->agent_order[a] : a;
+  {
+    std::vector<uint8_t> seen(NA, 0);
+    for (int a = 0; a < NA; ++a) {
+      require(agent_order[a] >= 0 && agent_order[a] < NA && !seen[agent_order[a]],
+              "agent_order must be a permutation of the agent indices");
+      seen[agent_order[a]] = 1;
+    }
+  }
+  if (kairos || profile_T) {
+    for (int r = 0; r < R; ++r)
+      for (int64_t c = call_base[r]; c < call_base[r + 1]; ++c) exec_off[size_t(r) * NA + b->agent[c] + 1] += 1;
+    for (size_t k = 1; k < exec_off.size(); ++k) {
+      rem_off[k] = rem_off[k - 1] + std::min<int64_t>(exec_off[k], kRemWindow + 1);
+      exec_off[k] += exec_off[k - 1];
+    }
+  }
+  const int64_t exec_total = profile_T ? exec_off.back() : 0;
+  const int64_t rem_total = kairos ? rem_off.back() : 0;
+  in.agent_order = A.upload(agent_order.data(), NA);
+  in.exec_off = A.upload(exec_off.data(), exec_off.size());
+  in.rem_off = A.upload(rem_off.data(), rem_off.size());
   const int ring = cfg->slot_ring ? cfg->slot_ring : 256;
   require(ring >= 64 && (ring & (ring - 1)) == 0, "slot_ring must be a power of two >= 64");
   EngineState st{};
@@ -1003,7 +1030,28 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   st.out_wf = A.alloc<int64_t>(W);
   st.scalars = A.alloc<double>(size_t(R) * kEngineScalars);
   st.counts = A.alloc<int64_t>(size_t(R) * 4);
+  const size_t RA = size_t(R) * NA;
+  st.done_idx = A.alloc<int64_t>(C);
+  st.exec_buf = A.alloc<double>(size_t(exec_total));
+  st.exec_ns = A.alloc<int64_t>(RA);
+  st.exec_nt = A.alloc<int64_t>(RA);
+  st.exec_T = A.alloc<double>(RA);
+  st.exec_dirty = A.alloc<uint8_t>(RA);
+  st.rem_sorted = A.alloc<double>(size_t(rem_total));
+  st.rem_ring = A.alloc<double>(size_t(rem_total));
+  st.rem_snap = A.alloc<double>(size_t(rem_total));
+  st.rem_d = A.alloc<DistScal>(RA);
+  st.pk = A.alloc<double>(RA);
+  const int64_t mds_n = NA + 1;
+  const int64_t mds_stride = kairos ? 4 * mds_n * mds_n + mds_n + 8 : 0;
+  st.mds = A.alloc<double>(size_t(R) * size_t(mds_stride));
+  st.rebuilds = A.alloc<int64_t>(size_t(R));
   EngineParams prm{};
+  prm.n_agents = NA;
+  prm.profile_T = profile_T;
+  prm.kairos = kairos;
+  prm.rebuild_interval = cfg->kairos_rebuild_interval ? cfg->kairos_rebuild_interval : 256;
+  prm.mds_stride = mds_stride;
   prm.n_inst = NI;
   prm.sched = cfg->scheduler;
   prm.dpolicy = dc.policy;
@@ -1074,6 +1122,13 @@ void replicas_run_impl(const kx_engine_config* cfg, const kx_replica_batch* b, k
   if (out->counts) std::memcpy(out->counts, counts.data(), counts.size() * 8);
   down(out->metrics, d_metrics, size_t(R) * kEngineMetrics);
   down(out->histogram, d_hist, size_t(R) * kHistBins);
+  if (kairos) {
+    down(out->priority_keys, st.pk, RA);
+    down(out->table_versions, st.rebuilds, size_t(R));
+  } else {
+    if (out->priority_keys) std::fill(out->priority_keys, out->priority_keys + RA, 0.0);
+    if (out->table_versions) std::fill(out->table_versions, out->table_versions + R, int64_t(0));
+  }
   for (int r = 0; r < R; ++r) {
     const int64_t status = counts[size_t(r) * 4 + 2];
     if (status == KX_ERR_CAPACITY) fail(KX_ERR_CAPACITY, "replica " + std::to_string(r) + ": event heap / run slots / ledger ring capacity exceeded");

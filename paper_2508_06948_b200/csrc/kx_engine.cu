@@ -10,10 +10,19 @@
 // Scalar replica state sits in shared memory, written by lane 0 and read by
 // every lane after __syncwarp, so control flow stays warp-uniform.
 //
-// Supported here: FCFS / TopoDepth / Oracle scheduling (scheduler.hpp:48-93)
-// with TimeSlot (oracle expected time, dispatcher.hpp:120), RoundRobin and
-// StaticThreshold dispatch. KairosScheduler's online table rebuilds
-// (W1 + MDS) and profile-based expected times are not on the device yet.
+// Supported: all four scheduling policies (scheduler.hpp:48-133) with
+// TimeSlot, RoundRobin and StaticThreshold dispatch, TimeSlot's expected
+// time either the oracle's pure_exec or the profiler's (engine.cpp:177-185).
+// The LatencyProfiler (profiler.cpp:20-50) lives in global memory per
+// (replica, agent): execution samples as a sorted prefix plus the samples
+// recorded since the last workflow completion (the reference's snapshot
+// point, engine.cpp:423), merged at each completion, their mode
+// (mode_estimate) computed lazily when a dispatch needs it; remaining-latency
+// windows with doubling checkpoints (dist_add_warp, kx_dist.cuh). The
+// KairosScheduler rebuild (scheduler.cpp:5-24: converged agents in AgentId
+// order, W1 matrix with the anchor, classical MDS, anchor distances, median
+// for the rest) runs in the warp when a workflow completion makes an agent
+// converge or every rebuild_interval completions.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -52,6 +61,7 @@ struct Scal {
   double next_arrival_time;  // arrival[next_arrival], cached
   int32_t heap_n, round_pending, tick_scheduled, status;
   int64_t rr_next;
+  uint64_t completed_instances;
 };
 
 struct RunSlot {  // RunningRequest (engine.hpp:137-145)
@@ -96,6 +106,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   const int64_t w0 = I.wf_base[r], w1 = I.wf_base[r + 1];
   const int64_t c0 = I.call_base[r], c1 = I.call_base[r + 1];
   const int ring = P.ring;
+  const int NA = P.n_agents;
+  const int64_t ab = int64_t(r) * NA;  // profiler / priority-table base of this replica
   auto sync = [] { __syncwarp(); };
 
   // ---- init --------------------------------------------------------------
@@ -134,6 +146,17 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     S.hi[lb + i] = -1;
     S.n_active[lb + i] = 0;
   }
+  if (P.profile_T || P.kairos) {
+    for (int a = lane; a < NA; a += 32) {
+      S.exec_ns[ab + a] = 0;
+      S.exec_nt[ab + a] = 0;
+      S.exec_dirty[ab + a] = 0;
+      S.exec_T[ab + a] = P.default_T;
+      S.pk[ab + a] = 0.0;  // empty table: median_anchor_distance() = 0
+      S.rem_d[ab + a] = DistScal{0, 0, 0, 0, uint64_t(kModeMinSamples), 0, -1.0};
+    }
+  }
+  if (lane == 0 && P.kairos) S.rebuilds[r] = 0;
   sync();
 
   // ---- helpers (uniform control flow; lane 0 writes) ------------------------
@@ -198,13 +221,16 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     switch (P.sched) {
       case KX_SCHED_FCFS: return S.enqueue_time[c];
       case KX_SCHED_TOPO: return static_cast<double>(I.depth[I.agent[c]]);
+      case KX_SCHED_KAIROS: return S.pk[ab + I.agent[c]];  // table_.priority_key(agent)
       default: return I.rem[c];  // Oracle: remaining_by_uid holds every call
     }
   };
-  auto key1 = [&](uint32_t c) -> double {
-    return P.sched == KX_SCHED_FCFS ? I.arrival[wf_of(c)] : S.enqueue_time[c];
+  auto key1 = [&](uint32_t c) -> double {  // FCFS, Kairos: app_start; Topo, Oracle: queue_enter
+    return (P.sched == KX_SCHED_FCFS || P.sched == KX_SCHED_KAIROS) ? I.arrival[wf_of(c)] : S.enqueue_time[c];
   };
-  // ReadyQueue comparator (priority.hpp:95-98): (k0, k1, k2=0, app, qe, msg, uid)
+  const bool k2_qe = P.sched == KX_SCHED_KAIROS;  // Kairos' third key component is queue_enter
+  // ReadyQueue comparator (priority.hpp:95-98): (k0, k1, k2, app, qe, msg, uid);
+  // k2 is 0, or queue_enter under Kairos where k1 = app makes it the qe test
   struct Tup {
     double k0, k1, app, qe;
     uint64_t msg, uid;
@@ -227,10 +253,11 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     if (a.msg != b.msg) return a.msg < b.msg;
     return a.uid < b.uid;
   };
-  // try_admit comparator (engine.cpp:280-283): (k0, k1, k2=0, msg, uid) (H10)
-  auto wless = [](const Tup& a, const Tup& b) {
+  // try_admit comparator (engine.cpp:280-283): (k0, k1, k2, msg, uid) (H10)
+  auto wless = [k2_qe](const Tup& a, const Tup& b) {
     if (a.k0 != b.k0) return a.k0 < b.k0;
     if (a.k1 != b.k1) return a.k1 < b.k1;
+    if (k2_qe && a.qe != b.qe) return a.qe < b.qe;
     if (a.msg != b.msg) return a.msg < b.msg;
     return a.uid < b.uid;
   };
@@ -467,12 +494,167 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (sc.status != KX_OK) return;
     }
   };
+  // ---- LatencyProfiler + KairosScheduler (profiler.cpp, scheduler.cpp) ----
+  // ProfilerSnapshot::expected_exec_time (profiler.cpp:11-16) of the last
+  // snapshot: mode_estimate of the agent's execution samples, cached until
+  // the next snapshot changes them.
+  auto expected_T = [&](int a) -> double {
+    const int64_t idx = ab + a;
+    const int64_t ns = S.exec_ns[idx];
+    if (ns == 0) return P.default_T;  // no samples in the snapshot: fallback
+    if (!S.exec_dirty[idx]) return S.exec_T[idx];
+    const double T = mode_estimate_warp(S.exec_buf + I.exec_off[idx], ns, kModeMinSamples);
+    sync();
+    if (lane == 0) {
+      S.exec_T[idx] = T;
+      S.exec_dirty[idx] = 0;
+    }
+    sync();
+    return T;
+  };
+  // profiler_.snapshot() (profiler.cpp:86-102): the execution samples
+  // recorded since the last snapshot join the sorted prefix.
+  auto exec_snapshot = [&]() {
+    for (int a = 0; a < NA; ++a) {
+      const int64_t idx = ab + a;
+      int64_t ns = S.exec_ns[idx];
+      const int64_t nt = S.exec_nt[idx];
+      if (ns == nt) continue;
+      double* buf = S.exec_buf + I.exec_off[idx];
+      for (; ns < nt; ++ns) {
+        const double v = buf[ns];
+        const int64_t pos = warp_lower_bound(buf, ns, v);
+        warp_shift_up(buf, pos, ns);
+        if (lane == 0) buf[pos] = v;
+        sync();
+      }
+      if (lane == 0) {
+        S.exec_ns[idx] = ns;
+        S.exec_dirty[idx] = 1;
+      }
+      sync();
+    }
+  };
+  // LatencyProfiler::record_remaining (profiler.cpp:31-50) of workflow w:
+  // its records in completion order, sample = finish - exec_start.
+  auto record_remaining = [&](int64_t w) -> bool {
+    const int64_t cb = I.wf_call[w], ce = I.wf_call[w + 1];
+    const double finish = S.wf_finish[w];  // max(arrival, exec_end...) = max exec_end
+    const DistCfg cfg{uint64_t(kModeMinSamples), 0.05, kRemWindow};
+    bool newly = false;
+    int64_t prev = -1;
+    for (int64_t k = cb; k < ce; ++k) {
+      int64_t best = INT64_MAX;  // next record: smallest completion slot after prev
+      for (int64_t c = cb + lane; c < ce; c += 32) {
+        const int64_t j = S.done_idx[c];
+        if (j > prev && j < best) best = j;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        best = b2 < best ? b2 : best;
+      }
+      prev = best;
+      const uint32_t call = S.out_call[best];
+      const int64_t idx = ab + I.agent[call];
+      const int64_t off = I.rem_off[idx], cap = I.rem_off[idx + 1] - off;
+      DistScal d = S.rem_d[idx];
+      const double v = __dsub_rn(finish, S.out_exec_start[best]);
+      if (!dist_add_warp(S.rem_sorted + off, S.rem_ring + off, S.rem_snap + off, cap, cfg, d, v, &newly)) {
+        fail(KX_ERR_CAPACITY);
+        return false;
+      }
+      sync();
+      if (lane == 0) S.rem_d[idx] = d;
+      sync();
+    }
+    return newly;
+  };
+  // KairosScheduler::rebuild (scheduler.cpp:14-24) -> build_matrix
+  // (priority.cpp:15-46) -> mds_embed_1d (priority.cpp:102-112).
+  auto rebuild = [&]() {
+    double* scr = S.mds + int64_t(r) * P.mds_stride;
+    int m = 0;  // converged agents with samples, in AgentId order (std::map)
+    int list[kKairosMaxAgents];
+    for (int k = 0; k < NA; ++k) {
+      const int a = I.agent_order[k];
+      const DistScal d = S.rem_d[ab + a];
+      if (d.conv && d.n > 0) list[m++] = a;
+    }
+    if (m == 0) return;  // nothing to rank yet
+    const int n = m + 1;  // + the anchor (a single sample 0.0), last label
+    double* dm = scr;
+    double* coords = scr + n * n;
+    double* work = coords + n;
+    double* anchor = work + 3 * n * n;
+    if (lane == 0) *anchor = 0.0;
+    sync();
+    const int pairs = n * (n - 1) / 2;
+    for (int p = lane; p < pairs; p += 32) {
+      int i = 0, rem = p;
+      while (rem >= n - 1 - i) {
+        rem -= n - 1 - i;
+        ++i;
+      }
+      const int j = i + 1 + rem;
+      auto samples = [&](int x, int64_t* cnt) -> const double* {
+        if (x == n - 1) {
+          *cnt = 1;
+          return anchor;
+        }
+        const int64_t idx = ab + list[x];
+        *cnt = S.rem_d[idx].n;
+        return S.rem_sorted + I.rem_off[idx];
+      };
+      int64_t na, nb;
+      const double* sa = samples(i, &na);
+      const double* sb = samples(j, &nb);
+      const double w = w1_walk(sa, uint64_t(na), sb, uint64_t(nb));
+      dm[i * n + j] = w;
+      dm[j * n + i] = w;
+    }
+    for (int i = lane; i < n; i += 32) dm[i * n + i] = 0.0;
+    sync();
+    if (lane == 0) {
+      mds_1d_thread(dm, n, work, coords);
+      const double anchor_coord = coords[n - 1];
+      // anchor distances of the table's agents; the median for the rest
+      double* dist = work;  // reuse
+      for (int i = 0; i < m; ++i) dist[i] = fabs(__dsub_rn(coords[i], anchor_coord));
+      double* srt = work + m;
+      for (int i = 0; i < m; ++i) {  // insertion sort (std::sort of values)
+        const double v = dist[i];
+        int j = i;
+        while (j > 0 && srt[j - 1] > v) {
+          srt[j] = srt[j - 1];
+          --j;
+        }
+        srt[j] = v;
+      }
+      const double median = quantile_sorted_d(srt, m, 0.5);
+      for (int a = 0; a < NA; ++a) S.pk[ab + a] = median;
+      for (int i = 0; i < m; ++i) S.pk[ab + list[i]] = dist[i];
+      S.rebuilds[r] += 1;
+    }
+    sync();
+  };
+  // Simulator::on_workflow_complete (engine.cpp:411-427), profiler part.
+  auto on_workflow_complete = [&](int64_t w) {
+    bool newly = false;
+    if (P.kairos) newly = record_remaining(w);
+    if (sc.status != KX_OK) return;
+    if (P.profile_T) exec_snapshot();
+    if (lane == 0) sc.completed_instances += 1;
+    sync();
+    if (P.kairos && (newly || sc.completed_instances % P.rebuild_interval == 0)) rebuild();
+  };
   auto dispatch_loop = [&]() {  // engine.cpp:220-268
     int retries = 0;
     while (sc.queue_n > 0 && sc.status == KX_OK) {
       const int64_t qpos = warp_argmin(S.queue + c0, sc.queue_n, [](int64_t) { return true; }, tless);
       const uint32_t head = S.queue[c0 + qpos];
-      const double T = P.oracle_T ? I.pure[head] : P.default_T;
+      const double T = P.oracle_T ? I.pure[head]
+                       : (P.profile_T && sc.completed_instances > 0) ? expected_T(I.agent[head])
+                                                                     : P.default_T;
       // collect_live: watermark resume, then the live view.
       for (int i = 0; i < NI; ++i) on_live_usage(i);
       int target = -1;
@@ -667,7 +849,13 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         S.out_exec_start[j] = runs[rs].exec_start;
         S.out_exec_end[j] = clock;
         S.out_inst[j] = i;
+        S.done_idx[c] = j;
         sc.calls_done += 1;
+        if (P.profile_T) {  // record_execution (engine.cpp:389)
+          const int64_t idx = ab + I.agent[c];
+          S.exec_buf[I.exec_off[idx] + S.exec_nt[idx]] = __dsub_rn(clock, runs[rs].exec_start);
+          S.exec_nt[idx] += 1;
+        }
         S.wf_finish[w] = S.wf_finish[w] > clock ? S.wf_finish[w] : clock;
         S.wf_tokens[w] += I.target[c];
         S.wf_ncalls[w] += 1;
@@ -688,6 +876,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
           sc.wf_done += 1;
         }
         sync();
+        on_workflow_complete(w);
+        if (sc.status != KX_OK) break;
       }
       try_admit(i);
       schedule_round(clock);
@@ -702,7 +892,9 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         for (int j = lane; j < P.max_run; j += 32) {
           const RunSlot& x = runs[i * P.max_run + j];
           if (!x.used) continue;
-          const double rank = P.sched == KX_SCHED_TOPO ? static_cast<double>(I.depth[I.agent[x.call]]) : 0.0;
+          const double rank = P.sched == KX_SCHED_TOPO     ? static_cast<double>(I.depth[I.agent[x.call]])
+                              : P.sched == KX_SCHED_KAIROS ? S.pk[ab + I.agent[x.call]]
+                                                           : 0.0;
           const uint64_t u = I.uid[x.call];
           if (brs < 0 || rank > br || (rank == br && (x.exec_start > bs || (x.exec_start == bs && u > bu)))) {
             br = rank;

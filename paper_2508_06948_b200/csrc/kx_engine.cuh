@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "kx_dist.cuh"
 #include "kx_state.cuh"
 
 namespace kx {
@@ -16,7 +17,17 @@ struct EngineParams {
   int32_t n_inst, sched, dpolicy, oracle_T, ring, heap_cap, max_run, pad;
   double slot_len, watermark, static_thr, default_T, period, recompute;
   uint64_t max_events;
+  // profile-based expected times (engine.cpp:177-185) and KairosScheduler
+  // online rebuilds (scheduler.cpp:5-24)
+  int32_t n_agents, profile_T, kairos, pad2;
+  uint64_t rebuild_interval;
+  int64_t mds_stride;  // doubles of rebuild scratch per replica
 };
+
+constexpr int kKairosMaxAgents = 32;
+// ProfilerConfig::remaining (profiler.hpp:43): {16, 0.05, 4096}
+constexpr int64_t kRemWindow = 4096;
+constexpr int64_t kModeMinSamples = 16;  // mode_estimate default (distribution.hpp:33-34)
 
 // All replicas concatenated; call / workflow indices are global.
 struct EngineInputs {
@@ -41,6 +52,10 @@ struct EngineInputs {
   const double* k;
   const double* prefill;
   const int32_t* max_batch;
+  // profiler layout, per (replica, agent) index r * n_agents + a
+  const int32_t* agent_order;  // [A] agent indices in AgentId (name) order
+  const int64_t* exec_off;     // [R*A+1] exec sample buffer (one per call of the agent)
+  const int64_t* rem_off;      // [R*A+1] remaining window buffers (min(calls, 4097))
 };
 
 struct EngineState {
@@ -83,6 +98,20 @@ struct EngineState {
   int64_t* out_wf;
   double* scalars;  // [R * kEngineScalars]
   int64_t* counts;  // [R * 4]
+  // profiler (LatencyProfiler, profiler.hpp:49-88) and priority table
+  int64_t* done_idx;    // [C] completion slot of each call
+  double* exec_buf;     // exec samples: sorted prefix [0, ns) + pending [ns, nt)
+  int64_t* exec_ns;     // [R*A] samples in the last snapshot (sorted)
+  int64_t* exec_nt;     // [R*A] samples recorded
+  double* exec_T;       // [R*A] cached mode_estimate of the snapshot
+  uint8_t* exec_dirty;  // [R*A]
+  double* rem_sorted;   // remaining-latency windows (sorted_, arrival ring, snapshot_)
+  double* rem_ring;
+  double* rem_snap;
+  DistScal* rem_d;      // [R*A]
+  double* pk;           // [R*A] current priority_key per agent
+  double* mds;          // [R*mds_stride] rebuild scratch
+  int64_t* rebuilds;    // [R] priority-table versions built
 };
 
 size_t engine_smem_bytes(const EngineParams& p);

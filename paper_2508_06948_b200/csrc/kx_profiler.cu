@@ -23,58 +23,8 @@
 #include "kx_common.cuh"
 #include "kx_profiler.cuh"
 #include "../../include/kairos_b200.h"
-#include "kx_w1.cuh"
 
 namespace kx {
-
-namespace {
-
-// std::lower_bound over s[0, n): first position with s[pos] >= v.
-__device__ __forceinline__ int64_t warp_lower_bound(const double* s, int64_t n, double v) {
-  const int lane = threadIdx.x & 31;
-  int64_t lo = 0, hi = n;
-  while (hi - lo > 32) {
-    const int64_t step = (hi - lo + 31) / 32;
-    const int64_t idx = lo + lane * step;
-    const uint32_t m = __ballot_sync(0xffffffffu, idx < hi && s[idx] < v);
-    const int c = __popc(m);  // sampled positions below v: a prefix (sorted)
-    if (c == 0) return lo;
-    const int64_t nlo = lo + int64_t(c - 1) * step + 1;
-    const int64_t nhi = lo + int64_t(c) * step;
-    lo = nlo;
-    hi = nhi < hi ? nhi : hi;
-  }
-  const uint32_t m = __ballot_sync(0xffffffffu, lo + lane < hi && s[lo + lane] < v);
-  return lo + __popc(m);
-}
-
-// s[pos + 1 .. n] = s[pos .. n - 1] (order kept), top chunk first.
-__device__ __forceinline__ void warp_shift_up(double* s, int64_t pos, int64_t n) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t top = n; top > pos; top -= 32) {
-    const int64_t idx = top - 1 - lane;
-    double t = 0.0;
-    if (idx >= pos) t = s[idx];
-    __syncwarp();
-    if (idx >= pos) s[idx + 1] = t;
-    __syncwarp();
-  }
-}
-
-// s[pos .. n - 2] = s[pos + 1 .. n - 1], bottom chunk first.
-__device__ __forceinline__ void warp_shift_down(double* s, int64_t pos, int64_t n) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t b = pos + 1; b < n; b += 32) {
-    const int64_t idx = b + lane;
-    double t = 0.0;
-    if (idx < n) t = s[idx];
-    __syncwarp();
-    if (idx < n) s[idx - 1] = t;
-    __syncwarp();
-  }
-}
-
-}  // namespace
 
 // Block = one warp = one distribution. Samples of distribution d in
 // [off[d], off[d+1]) in arrival order; item[k] is the caller's index of the
@@ -104,63 +54,20 @@ k_dist_ingest(DistDev dd, int32_t n_dist, const int64_t* __restrict__ off, const
     head = 0;
     __syncwarp();
   }
-  uint64_t total = dd.total[d];
-  uint64_t next_cp = dd.next_cp[d];
-  uint8_t conv = dd.conv[d];
-  double last = dd.last_dist[d];
+  DistScal ds{n, head, dd.snap_n[d], dd.total[d], dd.next_cp[d], dd.conv[d], dd.last_dist[d]};
+  double* snap = dd.snap + int64_t(d) * cap;
   int64_t conv_item = -1;
   int st = KX_OK;
   for (int64_t k = off[d]; k < off[d + 1]; ++k) {
-    const double v = values[k];
-    if (n + 1 > cap) {  // the retained window must fit before eviction
-      st = KX_ERR_CAPACITY;
+    bool newly = false;
+    if (!dist_add_warp(s, ring, snap, cap, cfg, ds, values[k], &newly)) {
+      st = KX_ERR_CAPACITY;  // the retained window must fit before eviction
       break;
     }
-    // sorted_.insert(lower_bound(value), value)
-    const int64_t pos = warp_lower_bound(s, n, v);
-    warp_shift_up(s, pos, n);
-    if (lane == 0) s[pos] = v;
-    ++n;
-    if (windowed) {
-      if (lane == 0) ring[(head + n - 1) % cap] = v;  // arrival_order_.push_back
-      __syncwarp();
-      if (uint64_t(n) > uint64_t(cfg.window_cap)) {  // evict the oldest
-        const double oldest = ring[head];
-        head = (head + 1) % cap;
-        const int64_t ep = warp_lower_bound(s, n, oldest);
-        warp_shift_down(s, ep, n);
-        --n;
-      }
-    }
-    __syncwarp();
-    ++total;
-    if (total == next_cp) {  // check_convergence (distribution.cpp:113-123)
-      const int64_t sn = dd.snap_n[d];
-      double* snap = dd.snap + int64_t(d) * cap;
-      if (sn > 0) {
-        double w = 0.0, sum = 0.0;
-        if (lane == 0) {
-          w = w1_walk(snap, uint64_t(sn), s, uint64_t(n));
-          for (int64_t j = 0; j < n; ++j) sum = __dadd_rn(sum, s[j]);  // mean(): sequential
-        }
-        w = __shfl_sync(0xffffffffu, w, 0);
-        sum = __shfl_sync(0xffffffffu, sum, 0);
-        const double mean = __ddiv_rn(sum, static_cast<double>(n));
-        const double t = __dmul_rn(cfg.threshold, mean);
-        const double tau = t > 1e-12 ? t : 1e-12;  // std::max(t, 1e-12)
-        last = w;
-        if (w < tau) {
-          if (!conv && conv_item < 0) conv_item = item ? item[k] : k;
-          conv = 1;
-        }
-      }
-      __syncwarp();
-      for (int64_t j = lane; j < n; j += 32) snap[j] = s[j];  // snapshot_ = sorted_
-      if (lane == 0) dd.snap_n[d] = n;
-      __syncwarp();
-      next_cp *= 2;
-    }
+    if (newly && conv_item < 0) conv_item = item ? item[k] : k;
   }
+  n = ds.n;
+  head = ds.head;
   __syncwarp();
   if (kSmem) {
     for (int64_t j = lane; j < n; j += 32) {
@@ -172,10 +79,11 @@ k_dist_ingest(DistDev dd, int32_t n_dist, const int64_t* __restrict__ off, const
   if (lane == 0) {
     dd.n[d] = n;
     dd.ring_head[d] = head;
-    dd.total[d] = total;
-    dd.next_cp[d] = next_cp;
-    dd.conv[d] = conv;
-    dd.last_dist[d] = last;
+    dd.snap_n[d] = ds.snap_n;
+    dd.total[d] = ds.total;
+    dd.next_cp[d] = ds.next_cp;
+    dd.conv[d] = static_cast<uint8_t>(ds.conv);
+    dd.last_dist[d] = ds.last;
     dd.conv_item[d] = conv_item;
     if (st != KX_OK) atomicExch(status, st);
   }

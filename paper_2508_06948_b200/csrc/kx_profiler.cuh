@@ -4,14 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-namespace kx {
+#include "kx_dist.cuh"
 
-// ConvergenceConfig (distribution.hpp:36-40) of one distribution.
-struct DistCfg {
-  uint64_t min_samples;
-  double threshold;
-  int64_t window_cap;   // 0 = unbounded
-};
+namespace kx {
 
 // EmpiricalDistribution state (distribution.hpp:72-82) of n_dist
 // distributions, each with room for `cap` retained samples.

@@ -57,10 +57,21 @@ METRIC_NAMES = ["instances", "requests", "mean_token_latency", "p90_token_latenc
                 "decode_time_fraction", "sim_end_time", "latency_count"]
 
 
+def builtin_agent_order(n_agents=10):
+    """Agent indices in AgentId order (std::map iteration: byte-wise name
+    order), the label order of the reference's W1 matrix (priority.cpp:49-65)."""
+    lib = _abi.load()
+    names = [lib.kx_builtin_agent_name(a).decode() for a in range(n_agents)]
+    return np.array(sorted(range(n_agents), key=lambda a: names[a].encode()), np.int32)
+
+
 def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
                  dispatcher: DispatcherConfig | None = None, topo_depth=None, n_agents=10,
                  dispatch_period=0.1, recompute_fraction=1.0, heap_capacity=0, device=0,
-                 warmup_seconds=0.0):
+                 warmup_seconds=0.0, agent_order=None, rebuild_interval=0):
+    """Whole replica simulations on the device (K6). scheduler "kairos" runs
+    the KairosScheduler's online table rebuilds; time_slot dispatch without
+    oracle_expected_time takes T from the device profiler (engine.cpp:177-185)."""
     lib = _abi.load()
     d = dispatcher or DispatcherConfig()
     arr = (_abi.kx_instance * len(instances))()
@@ -72,6 +83,11 @@ def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
     cfg = _abi.kx_engine_config(len(instances), _abi.SCHED[scheduler], arr, dc, n_agents, 0,
                                 depth.ctypes.data, dispatch_period, recompute_fraction, heap_capacity,
                                 device, 0, warmup_seconds)
+    if agent_order is None:
+        agent_order = builtin_agent_order(n_agents) if n_agents == 10 else np.arange(n_agents)
+    order = np.ascontiguousarray(agent_order, np.int32)
+    cfg.agent_order = order.ctypes.data
+    cfg.kairos_rebuild_interval = rebuild_interval
     R = len(batch["wf_base"]) - 1
     W = int(batch["wf_base"][-1])
     Cn = len(batch["agent"])
@@ -85,7 +101,8 @@ def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
                episodes=np.zeros(Cn, np.int32), preemptions=np.zeros(Cn, np.int32),
                wf_order=np.zeros(W, np.int64), wf_finish=np.zeros(W), wf_output_tokens=np.zeros(W, np.int64),
                wf_calls=np.zeros(W, np.int32), scalars=np.zeros(R * 8), counts=np.zeros(R * 4, np.int64),
-               metrics=np.zeros(R * 16), histogram=np.zeros(R * 256, np.uint32))
+               metrics=np.zeros(R * 16), histogram=np.zeros(R * 256, np.uint32),
+               priority_keys=np.zeros(R * n_agents), table_versions=np.zeros(R, np.int64))
     out = _abi.kx_replica_results(*[v.ctypes.data for v in res.values()])
     ms = C.c_double()
     check(lib.kx_replicas_run(C.byref(cfg), C.byref(b), C.byref(out), C.byref(ms)))
@@ -94,6 +111,7 @@ def run_replicas(batch, instances: list[InstanceProfile], scheduler="fcfs",
     res["counts"] = res["counts"].reshape(R, 4)
     res["metrics"] = res["metrics"].reshape(R, 16)
     res["histogram"] = res["histogram"].reshape(R, 256)
+    res["priority_keys"] = res["priority_keys"].reshape(R, n_agents)
     return res
 
 

@@ -45,6 +45,8 @@ def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, rec
                episodes=np.zeros(Cn, np.int32), preemptions=np.zeros(Cn, np.int32),
                wf_index=np.zeros(W, np.int64), wf_finish=np.zeros(W), wf_output_tokens=np.zeros(W, np.int64),
                wf_calls=np.zeros(W, np.int64), scalars=np.zeros(18))
+    pk = np.zeros(10)
+    version = C.c_int64(0)
     nc, nw = C.c_int64(), C.c_int64()
     d = dispatcher
     P = C.c_void_p
@@ -54,9 +56,11 @@ def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, rec
         C.c_int(int(d.oracle_expected_time)), C.c_double(d.slot_len), C.c_double(d.resume_watermark),
         C.c_double(d.static_threshold), C.c_double(d.default_expected_time), C.c_double(period),
         C.c_double(recompute), P(depth.ctypes.data)] + [P(v.ctypes.data) for v in out.values()] + [
-        C.byref(nc), C.byref(nw)]
+        C.byref(nc), C.byref(nw), P(pk.ctypes.data), C.byref(version)]
     rc = lib().kxref_sim_run(*args)
     assert rc == 0, "reference simulation failed"
     out["n_calls"] = nc.value
     out["n_wf"] = nw.value
+    out["priority_keys"] = pk
+    out["table_version"] = version.value
     return out

@@ -82,7 +82,8 @@ def test_engine_reports_the_reference_livelock(gpu_lib):
 
 def test_engine_rejects_unsupported_configs(gpu_lib):
     b = E.concat([E.realize("qa", 1.0, 20.0, 1)])
-    with pytest.raises(Exception):
-        E.run_replicas(b, insts(2), "kairos", DispatcherConfig("round_robin"))
-    with pytest.raises(Exception):
-        E.run_replicas(b, insts(2), "fcfs", DispatcherConfig("time_slot"))  # profile-based T
+    with pytest.raises(Exception):  # agent index outside the agent table
+        E.run_replicas(b, insts(2), "fcfs", DispatcherConfig("round_robin"), n_agents=2,
+                       topo_depth=np.ones(2, np.int32))
+    with pytest.raises(Exception):  # agent_order is not a permutation
+        E.run_replicas(b, insts(2), "kairos", DispatcherConfig("time_slot"), agent_order=np.zeros(10))
