@@ -33,6 +33,16 @@
 #include "kx_sortlib.cuh"
 #include "kx_state.cuh"
 
+#ifndef KX_HEAP_ARITY
+#define KX_HEAP_ARITY 2  // event-heap fan-out (A/B on B200: 2 beats 4, profiles/r01_engine_ab.md)
+#endif
+#ifndef KX_FAST_TICKS
+#define KX_FAST_TICKS 1  // lane 0 runs consecutive prefill / token events without warp syncs
+#endif
+#ifndef KX_REPLACE_TOP
+#define KX_REPLACE_TOP 1  // reuse the popped root for the handler's first push
+#endif
+
 namespace kx {
 
 namespace {
@@ -60,6 +70,7 @@ struct Scal {
   int64_t next_arrival, arrivals_remaining, queue_n, waiting_n, calls_done, wf_done;
   double next_arrival_time;  // arrival[next_arrival], cached
   int32_t heap_n, round_pending, tick_scheduled, status;
+  int32_t top_free, pad;
   int64_t rr_next;
   uint64_t completed_instances;
 };
@@ -73,6 +84,8 @@ struct RunSlot {  // RunningRequest (engine.hpp:137-145)
   double exec_start;
   int32_t phase;  // 0 prefill, 1 decode
   int32_t used;
+  int32_t inst;   // owning instance (slot / max_run, kept to avoid the division)
+  int32_t pad;
 };
 
 struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_ + profile
@@ -125,7 +138,10 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     ins[i].step = __ddiv_rn(1.0, I.k[i]);
     ins[i].max_batch = I.max_batch[i];
   }
-  for (int j = lane; j < NI * P.max_run; j += 32) runs[j].used = 0;
+  for (int j = lane; j < NI * P.max_run; j += 32) {
+    runs[j].used = 0;
+    runs[j].inst = j / P.max_run;
+  }
   for (int64_t c = c0 + lane; c < c1; c += 32) {
     S.first_enqueue[c] = -1.0;
     S.queue_seconds[c] = 0.0;
@@ -164,16 +180,50 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     if (lane == 0 && sc.status == KX_OK) sc.status = code;
     sync();
   };
-  auto push = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch) {
-    if (lane == 0) {
-      if (sc.heap_n >= P.heap_cap) {
+  // Event heap: KX_HEAP_ARITY-ary (binary), (time, kind, seq) order (engine.hpp:178-184). The
+  // keys are a strict total order (seq is unique), so the pop sequence does
+  // not depend on the layout: an event popped by the loop stays at the root
+  // (sc.top_free) until the handler's first push overwrites it and sifts
+  // down once (replace-top), or the next iteration removes it.
+  auto sift_down = [&](const Ev& e) {  // lane 0: place e from the root
+    int k = 0;
+    const int n = sc.heap_n;
+    while (true) {
+      const int c0 = KX_HEAP_ARITY * k + 1;
+      if (c0 >= n) break;
+      // the smallest of up to four children, comparing (time, ks) only
+      int c = c0;
+      double bt = heap[c0].time;
+      uint64_t bk = heap[c0].ks;
+      const int ce = c0 + KX_HEAP_ARITY < n ? c0 + KX_HEAP_ARITY : n;
+      for (int j = c0 + 1; j < ce; ++j) {
+        const double t = heap[j].time;
+        const uint64_t ks = heap[j].ks;
+        if (t < bt || (t == bt && ks < bk)) {
+          bt = t;
+          bk = ks;
+          c = j;
+        }
+      }
+      if (!(bt < e.time || (bt == e.time && bk < e.ks))) break;
+      heap[k] = heap[c];
+      k = c;
+    }
+    heap[k] = e;
+  };
+  auto push_l0 = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch) {  // lane 0
+    {
+      Ev e{t, (uint64_t(kind) << 56) | sc.next_seq, call, inst, epoch, 0};
+      sc.next_seq += 1;
+      if (KX_REPLACE_TOP && sc.top_free) {  // replace-top
+        sc.top_free = 0;
+        sift_down(e);
+      } else if (sc.heap_n >= P.heap_cap) {
         sc.status = KX_ERR_CAPACITY;
       } else {
-        Ev e{t, (uint64_t(kind) << 56) | sc.next_seq, call, inst, epoch, 0};
-        sc.next_seq += 1;
         int k = sc.heap_n++;
         while (k > 0) {
-          const int pk = (k - 1) >> 1;
+          const int pk = (k - 1) / KX_HEAP_ARITY;
           if (!ev_less(e, heap[pk])) break;
           heap[k] = heap[pk];
           k = pk;
@@ -181,23 +231,18 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         heap[k] = e;
       }
     }
+  };
+  auto push = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch) {
+    if (lane == 0) push_l0(t, kind, call, inst, epoch);
     sync();
   };
+  auto pop_l0 = [&]() {  // lane 0: remove the root (deferred pop)
+    sc.top_free = 0;
+    const Ev last = heap[--sc.heap_n];
+    if (sc.heap_n > 0) sift_down(last);
+  };
   auto pop_heap = [&]() {
-    if (lane == 0) {
-      const Ev last = heap[--sc.heap_n];
-      int k = 0;
-      const int n = sc.heap_n;
-      while (true) {
-        int c = 2 * k + 1;
-        if (c >= n) break;
-        if (c + 1 < n && ev_less(heap[c + 1], heap[c])) ++c;
-        if (!ev_less(heap[c], last)) break;
-        heap[k] = heap[c];
-        k = c;
-      }
-      if (n > 0) heap[k] = last;
-    }
+    if (lane == 0) pop_l0();
     sync();
   };
   auto schedule_round = [&](double t) {  // engine.cpp:79-83
@@ -759,8 +804,57 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     enqueue_call(c, sc.clock);
   };
 
+  // PrefillDone / TokenTick events (engine.cpp:334-361, ~97% of all events)
+  // touch only shared-memory state, so lane 0 runs them back to back without
+  // warp synchronisation until the next event is of another kind or an
+  // arrival comes first (arrivals win ties: kind 0).
+  auto fast_ticks = [&]() {  // lane 0
+    while (sc.status == KX_OK) {
+      if (sc.top_free) pop_l0();
+      if (sc.heap_n == 0) return;
+      const int kind = static_cast<int>(heap[0].ks >> 56);
+      if (kind != EV_TOKEN && kind != EV_PREFILL) return;
+      if (sc.next_arrival < w1 && !(heap[0].time < sc.next_arrival_time)) return;
+      const Ev ev = heap[0];
+      sc.top_free = 1;
+      if (ev.time < __dsub_rn(sc.clock, kTimeEpsilon)) {
+        sc.status = KX_ERR_LOGIC;  // event time ran backwards
+        return;
+      }
+      sc.clock = sc.clock > ev.time ? sc.clock : ev.time;
+      sc.processed += 1;
+      if (sc.processed > P.max_events) {
+        sc.status = KX_ERR_RUNTIME;
+        return;
+      }
+      const int rs = find_running(ev);
+      if (rs < 0) continue;
+      const double clock = sc.clock;
+      const int i = runs[rs].inst;
+      const double step = ins[i].step;
+      if (kind == EV_PREFILL) {
+        runs[rs].phase = 1;
+        push_l0(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+      } else {
+        runs[rs].tokens += 1;
+        runs[rs].kv += 1;
+        ins[i].live_kv = __dadd_rn(ins[i].live_kv, 1.0);
+        sc.decode_seconds = __dadd_rn(sc.decode_seconds, step);
+        if (runs[rs].tokens >= runs[rs].target) push_l0(clock, EV_DONE, ev.call, rs, ev.epoch);
+        else push_l0(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+        if (ins[i].live_kv > ins[i].cap) push_l0(clock, EV_PREEMPT, 0, i, 0);
+      }
+    }
+  };
+
   // ---- event loop (engine.cpp:85-123) ---------------------------------------
   while (sc.status == KX_OK) {
+    if (KX_FAST_TICKS) {
+      if (lane == 0) fast_ticks();
+      sync();
+      if (sc.status != KX_OK) break;
+    }
+    if (sc.top_free) pop_heap();  // the last event's root was not reused
     // next event: heap top vs the next arrival (kind 0, seq = local index)
     const bool have_arr = sc.next_arrival < w1;
     const bool have_heap = sc.heap_n > 0;
@@ -776,7 +870,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     }
     if (from_heap) {
       ev = heap[0];
-      pop_heap();
+      if (lane == 0) sc.top_free = 1;
     } else if (lane == 0) {
       sc.next_arrival += 1;
       if (sc.next_arrival < w1) sc.next_arrival_time = I.arrival[sc.next_arrival];
@@ -816,11 +910,11 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (rs < 0) continue;
       if (lane == 0) runs[rs].phase = 1;
       sync();
-      push(__dadd_rn(clock, ins[rs / P.max_run].step), EV_TOKEN, ev.call, rs, ev.epoch);
+      push(__dadd_rn(clock, ins[runs[rs].inst].step), EV_TOKEN, ev.call, rs, ev.epoch);
     } else if (kind == EV_TOKEN) {  // engine.cpp:343-361
       const int rs = find_running(ev);
       if (rs < 0) continue;
-      const int i = rs / P.max_run;
+      const int i = runs[rs].inst;
       const double step = ins[i].step;
       if (lane == 0) {
         runs[rs].tokens += 1;
@@ -835,7 +929,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     } else if (kind == EV_DONE) {  // engine.cpp:363-409
       const int rs = find_running(ev);
       if (rs < 0) continue;
-      const int i = rs / P.max_run;
+      const int i = runs[rs].inst;
       const uint32_t c = ev.call;
       const int64_t w = wf_of(c);
       if (lane == 0) {

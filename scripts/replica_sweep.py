@@ -3,7 +3,8 @@
 the co-located QA+RG+CG workload simulated on the device (K6) with their
 metrics computed on the device (K7).
 
-Single GPU:   python scripts/replica_sweep.py --replicas 296 --duration 720
+Single GPU:   python scripts/replica_sweep.py --replicas 1024 --duration 720
+              (--scheduler kairos --profile-T: the paper's policy, online tables)
 Multi GPU:    torchrun --nproc-per-node N scripts/replica_sweep.py ...
 Replica r is simulated by rank r % N (weak scaling when --replicas scales
 with N); NCCL all-gathers each rank's per-replica metric rows and latency
@@ -43,7 +44,7 @@ def sweep(args, rank=0, ws=1, dev=0):
     reals = [E.realize("colocated", args.rate, args.duration, seed=1 + r) for r in mine]
     b = E.concat(reals)
     t_gen = time.time() - t0
-    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=args.dispatcher == "time_slot")
+    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=not args.profile_T)
     res = E.run_replicas(b, instances(args.instances), args.scheduler, disp, topo_depth=DEPTH,
                          device=dev, warmup_seconds=args.warmup)
     n_calls = int(res["counts"][:, 0].sum())
@@ -54,7 +55,7 @@ def sweep(args, rank=0, ws=1, dev=0):
 def cpu_reference(args, sample):
     sys.path.insert(0, str(ROOT / "tests"))
     import ref_sim  # noqa: E402  (the reference Simulator via oracle/_ref/libkxref.so)
-    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=args.dispatcher == "time_slot")
+    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=not args.profile_T)
     reals = [E.realize("colocated", args.rate, args.duration, seed=1 + r) for r in range(sample)]
     threads = min(sample, os.cpu_count() or 1)
     t0 = time.perf_counter()
@@ -70,7 +71,7 @@ def cpu_reference(args, sample):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--replicas", type=int, default=296)
+    ap.add_argument("--replicas", type=int, default=1024)  # C5: 1024 replicas
     ap.add_argument("--rate", type=float, default=12.0)
     ap.add_argument("--duration", type=float, default=720.0)
     ap.add_argument("--instances", type=int, default=16)
@@ -78,6 +79,8 @@ def main():
     ap.add_argument("--dispatcher", default="time_slot")
     ap.add_argument("--warmup", type=float, default=0.0)
     ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--profile-T", action="store_true",
+                    help="time_slot T from the online profiler (engine.cpp:177-185) instead of the oracle's")
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -114,7 +117,8 @@ def main():
             "replicas": args.replicas, "requests": n_calls, "events": events,
             "events_per_s": events / (dev_ms / 1e3), "device_ms": dev_ms, "scaling": "weak",
             "config": {"workload": f"colocated QA+RG+CG, rate {args.rate}/s for {args.duration}s per replica",
-                       "instances": args.instances, "scheduler": args.scheduler, "dispatcher": args.dispatcher},
+                       "instances": args.instances, "scheduler": args.scheduler, "dispatcher": args.dispatcher,
+                       "expected_T": "profiler" if args.profile_T else "oracle"},
             "aggregate": dict(zip(E.METRIC_NAMES, [float(x) for x in agg])),
             "histogram_total": int(hist.sum()),
             "cpu_baseline": cpu, "host_realize_s": t_gen}), flush=True)
