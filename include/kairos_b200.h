@@ -382,6 +382,15 @@ int kx_graph_launch(kx_sched* s);
  * The 1-D classical MDS of the matrix (priority.cpp:67-112) stays on the host. */
 int kx_w1_matrix(int32_t n_agents, const int64_t* offsets, const double* samples, double* out);
 
+/* ProfilerSnapshot::expected_exec_time (profiler.cpp:11-16) for n_agents
+ * sorted execution-sample sets back to back (offsets[0..n_agents]): out[a] =
+ * mode_estimate(set a, min_samples).value (distribution.cpp:46-86; the
+ * reference's default min_samples is 16), or `fallback` for an empty set.
+ * Bit-identical to the reference (glibc cbrt replayed on the device). Host
+ * pointers; unsorted sets -> KX_ERR_INVALID. */
+int kx_expected_exec_times(int32_t n_agents, const int64_t* offsets, const double* samples,
+                           int64_t min_samples, double fallback, double* out);
+
 /* ---- workload synthesis (host) ------------------------------------------ */
 /* realize() (workload.cpp:319-372) for the built-in templates
  * (workload.cpp:462-560); app_mask selects QA/RG/CG in that order

@@ -164,6 +164,7 @@ SIGNATURES = {
     "kx_graph_capture_end": (C.c_int, [_P]),
     "kx_graph_launch": (C.c_int, [_P]),
     "kx_builtin_agent_name": (C.c_char_p, [C.c_int32]),
+    "kx_expected_exec_times": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p]),
     "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                      C.c_double, C.POINTER(_P)]),
     "kx_realization_sizes": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

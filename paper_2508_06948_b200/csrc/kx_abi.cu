@@ -22,6 +22,8 @@
 #include "kx_state.cuh"
 
 namespace kx {
+void launch_expected_T(int32_t n_agents, const int64_t* off, const double* samples, int64_t min_samples,
+                       double fallback, double* out, cudaStream_t st);
 void launch_w1_matrix(int32_t n_agents, const int64_t* off, const double* samples, double* d, int sms,
                       cudaStream_t st);
 std::atomic<long long> g_kx_launches{0};
@@ -2173,6 +2175,42 @@ int kx_w1_matrix(int32_t n_agents, const int64_t* offsets, const double* samples
     KX_CUDA(cudaFreeAsync(d_off, st));
     KX_CUDA(cudaFreeAsync(d_s, st));
     KX_CUDA(cudaFreeAsync(d_m, st));
+    KX_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int kx_expected_exec_times(int32_t n_agents, const int64_t* offsets, const double* samples,
+                           int64_t min_samples, double fallback, double* out) {
+  return guard([&] {
+    require(n_agents >= 0, "negative agent count");
+    if (n_agents == 0) return;
+    require(offsets && out, "null argument");
+    require(offsets[0] == 0, "offsets must start at 0");
+    for (int32_t a = 0; a < n_agents; ++a) require(offsets[a + 1] >= offsets[a], "offsets must be non-decreasing");
+    const int64_t ns = offsets[n_agents];
+    require(ns == 0 || samples, "null samples");
+    for (int32_t a = 0; a < n_agents; ++a)  // mode_estimate expects a sorted set
+      for (int64_t k = offsets[a] + 1; k < offsets[a + 1]; ++k)
+        require(samples[k - 1] <= samples[k], "sample sets must be sorted ascending");
+    ensure_device(0);
+    cudaStream_t st = nullptr;
+    KX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() { cudaStreamDestroy(s); }
+    } sg{st};
+    int64_t* d_off = nullptr;
+    double *d_s = nullptr, *d_o = nullptr;
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_off), size_t(n_agents + 1) * 8, st));
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_s), size_t(std::max<int64_t>(ns, 1)) * 8, st));
+    KX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_o), size_t(n_agents) * 8, st));
+    KX_CUDA(cudaMemcpyAsync(d_off, offsets, size_t(n_agents + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (ns) KX_CUDA(cudaMemcpyAsync(d_s, samples, size_t(ns) * 8, cudaMemcpyHostToDevice, st));
+    launch_expected_T(n_agents, d_off, d_s, min_samples, fallback, d_o, st);
+    KX_CUDA(cudaMemcpyAsync(out, d_o, size_t(n_agents) * 8, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaFreeAsync(d_off, st));
+    KX_CUDA(cudaFreeAsync(d_s, st));
+    KX_CUDA(cudaFreeAsync(d_o, st));
     KX_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "kx_common.cuh"
+#include "kx_dist.cuh"
 #include "kx_w1.cuh"
 
 namespace kx {
@@ -56,6 +57,26 @@ void launch_w1_matrix(int32_t n_agents, const int64_t* off, const double* sample
   if (pairs == 0) return;
   const int grid = static_cast<int>(std::min<int64_t>((pairs + 127) / 128, int64_t(sms) * 16));
   k_w1_matrix<<<grid, 128, 0, st>>>(n_agents, off, samples, d);
+  KX_CHECK_LAUNCH();
+}
+
+// ProfilerSnapshot::expected_exec_time (profiler.cpp:11-16) for every agent
+// of a snapshot: warp per agent, mode_estimate (distribution.cpp:46-86) of
+// its sorted execution samples, `fallback` for an empty set.
+__global__ void __launch_bounds__(128)
+k_expected_T(int32_t n_agents, const int64_t* __restrict__ off, const double* __restrict__ samples,
+             int64_t min_samples, double fallback, double* __restrict__ out) {
+  const int a = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (a >= n_agents) return;
+  const int64_t n = off[a + 1] - off[a];
+  const double T = n == 0 ? fallback : mode_estimate_warp(samples + off[a], n, min_samples);
+  if ((threadIdx.x & 31) == 0) out[a] = T;
+}
+
+void launch_expected_T(int32_t n_agents, const int64_t* off, const double* samples, int64_t min_samples,
+                       double fallback, double* out, cudaStream_t st) {
+  if (n_agents == 0) return;
+  k_expected_T<<<(n_agents + 3) / 4, 128, 0, st>>>(n_agents, off, samples, min_samples, fallback, out);
   KX_CHECK_LAUNCH();
 }
 
