@@ -152,6 +152,11 @@ int kx_set_remaining_table(kx_sched* s, uint64_t uid_base, int64_t n,
 /* ---- ready queue (priority.hpp:70-116) ----------------------------------- */
 /* Replaces ReadyQueue contents with n requests (ReadyQueue::enqueue x n). */
 int kx_queue_upload(kx_sched* s, int64_t n, const kx_queue_view* q, int32_t mem);
+/* ReadyQueue::enqueue (priority.hpp:72) x n: appends n requests behind the
+ * current ones, in the given order (push_back; the order decides exact-tuple
+ * ties, priority.hpp:89-103). msg_key must rank like the keys already queued
+ * (H1: one key space per queue). Invalidates the last order / dispatch round. */
+int kx_queue_enqueue(kx_sched* s, int64_t n, const kx_queue_view* q, int32_t mem);
 int kx_queue_size(kx_sched* s, int64_t* n);
 /* Drops every request admitted by the last dispatch round (ReadyQueue::pop
  * of the placed prefix), keeping the others in their relative order. */

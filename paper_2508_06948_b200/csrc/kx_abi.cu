@@ -1329,41 +1329,62 @@ int kx_set_remaining_table(kx_sched* s, uint64_t uid_base, int64_t n, const doub
   });
 }
 
+// Writes n requests at queue positions [at, at + n) (SoA columns), checks
+// them and refreshes the Oracle key column.
+static void queue_write(kx_sched* s, int64_t at, int64_t n, const kx_queue_view* v, int32_t mem, const char* who) {
+  require(s && v, "null argument");
+  require(n >= 0 && at >= 0 && at + n <= s->cap, "queue size exceeds queue_capacity");
+  KX_CUDA(cudaSetDevice(s->device));
+  const size_t N = static_cast<size_t>(n), A = static_cast<size_t>(at);
+  if (n > 0) {
+    require(v->agent && v->prompt_tokens && v->app_start && v->queue_enter && v->msg_key && v->uid,
+            "queue view is missing a required array");
+    if (s->dcfg.oracle_expected_time)
+      require(v->pure_exec != nullptr, "oracle_expected_time needs pure_exec");
+    const cudaMemcpyKind k = kind_in(mem);
+    KX_CUDA(cudaMemcpyAsync(s->q.agent + A, v->agent, N * 4, k, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q.prompt + A, v->prompt_tokens, N * 8, k, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q.app_start + A, v->app_start, N * 8, k, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q.queue_enter + A, v->queue_enter, N * 8, k, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q.msg + A, v->msg_key, N * 8, k, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q.uid + A, v->uid, N * 8, k, s->stream));
+    if (v->kept_tokens)
+      KX_CUDA(cudaMemcpyAsync(s->q.kept + A, v->kept_tokens, N * 8, k, s->stream));
+    else
+      KX_CUDA(cudaMemsetAsync(s->q.kept + A, 0, N * 8, s->stream));
+    if (v->pure_exec) KX_CUDA(cudaMemcpyAsync(s->q.pure_exec + A, v->pure_exec, N * 8, k, s->stream));
+    KX_CUDA(cudaMemsetAsync(s->err_flag, 0, sizeof(int), s->stream));
+    QueueDev part = s->q;
+    part.agent += A;
+    part.prompt += A;
+    part.app_start += A;
+    part.queue_enter += A;
+    part.msg += A;
+    part.uid += A;
+    part.kept += A;
+    part.pure_exec += A;
+    part.rem += A;
+    part.admitted += A;
+    const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(s->sms) * 8));
+    k_validate_queue<<<grid, 256, 0, s->stream>>>(part, n, std::max(s->n_agents, 0),
+                                                  s->dcfg.oracle_expected_time ? 1 : 0, s->err_flag);
+    KX_CHECK_LAUNCH();
+  }
+  s->n = at + n;
+  refresh_rem(s);
+  s->order_valid = false;
+  s->dispatch_valid = false;
+  if (n > 0) check_err_flag(s, who);
+}
+
 int kx_queue_upload(kx_sched* s, int64_t n, const kx_queue_view* v, int32_t mem) {
+  return guard([&] { queue_write(s, 0, n, v, mem, "kx_queue_upload"); });
+}
+
+int kx_queue_enqueue(kx_sched* s, int64_t n, const kx_queue_view* v, int32_t mem) {
   return guard([&] {
-    require(s && v, "null argument");
-    require(n >= 0 && n <= s->cap, "queue size exceeds queue_capacity");
-    KX_CUDA(cudaSetDevice(s->device));
-    const size_t N = static_cast<size_t>(n);
-    if (n > 0) {
-      require(v->agent && v->prompt_tokens && v->app_start && v->queue_enter && v->msg_key && v->uid,
-              "queue view is missing a required array");
-      if (s->dcfg.oracle_expected_time)
-        require(v->pure_exec != nullptr, "oracle_expected_time needs pure_exec");
-      const cudaMemcpyKind k = kind_in(mem);
-      KX_CUDA(cudaMemcpyAsync(s->q.agent, v->agent, N * 4, k, s->stream));
-      KX_CUDA(cudaMemcpyAsync(s->q.prompt, v->prompt_tokens, N * 8, k, s->stream));
-      KX_CUDA(cudaMemcpyAsync(s->q.app_start, v->app_start, N * 8, k, s->stream));
-      KX_CUDA(cudaMemcpyAsync(s->q.queue_enter, v->queue_enter, N * 8, k, s->stream));
-      KX_CUDA(cudaMemcpyAsync(s->q.msg, v->msg_key, N * 8, k, s->stream));
-      KX_CUDA(cudaMemcpyAsync(s->q.uid, v->uid, N * 8, k, s->stream));
-      if (v->kept_tokens)
-        KX_CUDA(cudaMemcpyAsync(s->q.kept, v->kept_tokens, N * 8, k, s->stream));
-      else
-        KX_CUDA(cudaMemsetAsync(s->q.kept, 0, N * 8, s->stream));
-      if (v->pure_exec) KX_CUDA(cudaMemcpyAsync(s->q.pure_exec, v->pure_exec, N * 8, k, s->stream));
-      KX_CUDA(cudaMemsetAsync(s->err_flag, 0, sizeof(int), s->stream));
-      const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(s->sms) * 8));
-      k_validate_queue<<<grid, 256, 0, s->stream>>>(s->q, n, std::max(s->n_agents, 0),
-                                                    s->dcfg.oracle_expected_time ? 1 : 0,
-                                                    s->err_flag);
-      KX_CHECK_LAUNCH();
-    }
-    s->n = n;
-    refresh_rem(s);
-    s->order_valid = false;
-    s->dispatch_valid = false;
-    if (n > 0) check_err_flag(s, "kx_queue_upload");
+    require(s, "null handle");
+    queue_write(s, s->n, n, v, mem, "kx_queue_enqueue");
   });
 }
 

@@ -111,24 +111,34 @@ class DeviceScheduler:
                                               _abi.KX_MEM_HOST))
 
     # -- queue ---------------------------------------------------------------
+    def _view(self, agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens, pure_exec, device):
+        if device:
+            cols = [agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens, pure_exec]
+            return cols, int(agent.numel()), _abi.KX_MEM_DEVICE
+        cols = [np.ascontiguousarray(agent, np.int32), np.ascontiguousarray(prompt_tokens, np.int64),
+                np.ascontiguousarray(app_start, np.float64), np.ascontiguousarray(queue_enter, np.float64),
+                np.ascontiguousarray(msg_key, np.uint64), np.ascontiguousarray(uid, np.uint64),
+                None if kept_tokens is None else np.ascontiguousarray(kept_tokens, np.int64),
+                None if pure_exec is None else np.ascontiguousarray(pure_exec, np.float64)]
+        return cols, len(cols[0]), _abi.KX_MEM_HOST
+
     def upload(self, agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens=None,
                pure_exec=None, device: bool = False):
         """Replace the queue. Host numpy arrays, or torch CUDA tensors with device=True."""
-        if device:
-            cols = [agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens, pure_exec]
-            n = int(agent.numel())
-            mem = _abi.KX_MEM_DEVICE
-        else:
-            cols = [np.ascontiguousarray(agent, np.int32), np.ascontiguousarray(prompt_tokens, np.int64),
-                    np.ascontiguousarray(app_start, np.float64), np.ascontiguousarray(queue_enter, np.float64),
-                    np.ascontiguousarray(msg_key, np.uint64), np.ascontiguousarray(uid, np.uint64),
-                    None if kept_tokens is None else np.ascontiguousarray(kept_tokens, np.int64),
-                    None if pure_exec is None else np.ascontiguousarray(pure_exec, np.float64)]
-            n = len(cols[0])
-            mem = _abi.KX_MEM_HOST
+        cols, n, mem = self._view(agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens,
+                                  pure_exec, device)
         v = _abi.kx_queue_view(*[ptr(c) for c in cols])
         check(self.lib.kx_queue_upload(self.h, n, C.byref(v), mem))
         self.n = n
+
+    def enqueue(self, agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens=None,
+                pure_exec=None, device: bool = False):
+        """ReadyQueue::enqueue (priority.hpp:72) for each request, in order: append."""
+        cols, n, mem = self._view(agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens,
+                                  pure_exec, device)
+        v = _abi.kx_queue_view(*[ptr(c) for c in cols])
+        check(self.lib.kx_queue_enqueue(self.h, n, C.byref(v), mem))
+        self.n = self.size()
 
     def size(self) -> int:
         n = C.c_int64()

@@ -118,3 +118,38 @@ def test_order_reused_across_table_versions(gpu_lib):
         s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
         s.order()
         assert np.array_equal(s.fetch_order()[0], O.sort("kairos", q, t, 1)[0])
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_enqueue_appends_like_readyqueue(gpu_lib, policy):
+    # ReadyQueue::enqueue (priority.hpp:72) in chunks == one upload of the
+    # concatenation; exact-tuple ties keep queue (push_back) order
+    rng = np.random.default_rng(72)
+    n, pools = 90_001, 3
+    q, t = random_queue(rng, n, n_agents=37, n_pools=pools, tie_grain=0.5)
+    s = make_sched(pools, n)
+    cols = [q.agent, q.prompt, q.app_start, q.queue_enter, q.msg_key, q.uid]
+    cuts = [0, 1, 40_000, 40_000, 77_777, n]
+    s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
+    if t.rem is not None:
+        s.set_remaining_table(t.view.rem_base, t.rem, t.rem_present)
+    s.set_scheduler(policy)
+    s.upload(*[c[:cuts[1]] for c in cols])
+    for a, b in zip(cuts[1:], cuts[2:]):
+        s.enqueue(*[c[a:b] for c in cols])
+    assert s.size() == n
+    s.order()
+    perm, offs = s.fetch_order()
+    ref_perm, ref_offs = O.sort(policy, q, t, pools)
+    assert np.array_equal(offs, ref_offs)
+    assert np.array_equal(perm, ref_perm)
+
+
+def test_enqueue_beyond_capacity_fails(gpu_lib):
+    rng = np.random.default_rng(73)
+    q, t = random_queue(rng, 100, n_agents=5, n_pools=1)
+    s = make_sched(1, 100)
+    s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
+    s.upload(q.agent[:60], q.prompt[:60], q.app_start[:60], q.queue_enter[:60], q.msg_key[:60], q.uid[:60])
+    with pytest.raises(Exception):
+        s.enqueue(q.agent, q.prompt, q.app_start, q.queue_enter, q.msg_key, q.uid)
