@@ -39,6 +39,9 @@
 #ifndef KX_FAST_TICKS
 #define KX_FAST_TICKS 1  // lane 0 runs consecutive prefill / token events without warp syncs
 #endif
+#ifndef KX_FLOYD
+#define KX_FLOYD 0  // bottom-up sift-down (hole to a leaf, then sift up): measured slower
+#endif
 #ifndef KX_REPLACE_TOP
 #define KX_REPLACE_TOP 1  // reuse the popped root for the handler's first push
 #endif
@@ -49,7 +52,10 @@ namespace {
 
 enum : int { EV_ARRIVAL = 0, EV_PREFILL = 1, EV_TOKEN = 2, EV_DONE = 3, EV_PREEMPT = 4, EV_ROUND = 5 };
 
-struct Ev {
+#ifndef KX_EV_ALIGN
+#define KX_EV_ALIGN 16  // 16: heap moves are two 128-bit shared loads / stores
+#endif
+struct __align__(KX_EV_ALIGN) Ev {
   double time;
   uint64_t ks;  // kind << 56 | seq
   uint32_t call;
@@ -100,8 +106,10 @@ struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_ +
 
 }  // namespace
 
+constexpr size_t kScalBytes = (sizeof(Scal) + 15) & ~size_t(15);  // heap starts 16-byte aligned
+
 size_t engine_smem_bytes(const EngineParams& p) {
-  return sizeof(Scal) + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
+  return kScalBytes + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
          sizeof(RunSlot) * size_t(p.n_inst) * size_t(p.max_run) + 64;
 }
 
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(32, 16)
 k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Scal& sc = *reinterpret_cast<Scal*>(smem_raw);
-  Ev* heap = reinterpret_cast<Ev*>(smem_raw + sizeof(Scal));
+  Ev* heap = reinterpret_cast<Ev*>(smem_raw + kScalBytes);
   InstS* ins = reinterpret_cast<InstS*>(heap + P.heap_cap);
   RunSlot* runs = reinterpret_cast<RunSlot*>(ins + P.n_inst);
 
@@ -188,10 +196,32 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   auto sift_down = [&](const Ev& e) {  // lane 0: place e from the root
     int k = 0;
     const int n = sc.heap_n;
+    if (KX_FLOYD && KX_HEAP_ARITY == 2) {
+      // Floyd: walk the hole down the smaller-child path to a leaf (one
+      // comparison per level), then sift e up from there (e is usually a
+      // late event: a token tick's successor sinks to the bottom).
+      while (2 * k + 1 < n) {
+        int c = 2 * k + 1;
+        if (c + 1 < n) {
+          const double t0 = heap[c].time, t1 = heap[c + 1].time;
+          if (t1 < t0 || (t1 == t0 && heap[c + 1].ks < heap[c].ks)) ++c;
+        }
+        heap[k] = heap[c];
+        k = c;
+      }
+      while (k > 0) {
+        const int pk = (k - 1) >> 1;
+        if (!ev_less(e, heap[pk])) break;
+        heap[k] = heap[pk];
+        k = pk;
+      }
+      heap[k] = e;
+      return;
+    }
     while (true) {
       const int c0 = KX_HEAP_ARITY * k + 1;
       if (c0 >= n) break;
-      // the smallest of up to four children, comparing (time, ks) only
+      // the smallest of the children, comparing (time, ks) only
       int c = c0;
       double bt = heap[c0].time;
       uint64_t bk = heap[c0].ks;
