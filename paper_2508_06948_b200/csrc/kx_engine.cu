@@ -39,6 +39,9 @@
 #ifndef KX_FAST_TICKS
 #define KX_FAST_TICKS 1  // lane 0 runs consecutive prefill / token events without warp syncs
 #endif
+#ifndef KX_TOKEN_FIFO
+#define KX_TOKEN_FIFO 1  // per-instance token-event FIFOs: only each FIFO's head sits in the heap
+#endif
 #ifndef KX_FLOYD
 #define KX_FLOYD 0  // bottom-up sift-down (hole to a leaf, then sift up): measured slower
 #endif
@@ -102,15 +105,24 @@ struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_ +
   int32_t susp;
   int32_t max_batch;
   uint64_t preempted_total;
+  int32_t fh, fn;  // token FIFO: ring head, entries (the head is in the heap when fn > 0)
 };
 
 }  // namespace
 
 constexpr size_t kScalBytes = (sizeof(Scal) + 15) & ~size_t(15);  // heap starts 16-byte aligned
 
+// Token FIFO entries per instance (0 = off): running requests plus room for
+// stale events of preempted ones; a full FIFO falls back to the heap.
+__host__ __device__ inline int fifo_cap_of(int max_run) { return KX_TOKEN_FIFO ? max_run + 8 : 0; }
+__host__ __device__ inline size_t fifo_off(const EngineParams& p) {
+  const size_t end = kScalBytes + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
+                     sizeof(RunSlot) * size_t(p.n_inst) * size_t(p.max_run);
+  return (end + 15) & ~size_t(15);
+}
+
 size_t engine_smem_bytes(const EngineParams& p) {
-  return kScalBytes + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
-         sizeof(RunSlot) * size_t(p.n_inst) * size_t(p.max_run) + 64;
+  return fifo_off(p) + sizeof(Ev) * size_t(p.n_inst) * size_t(fifo_cap_of(p.max_run)) + 64;
 }
 
 __global__ void __launch_bounds__(32, 16)
@@ -120,6 +132,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   Ev* heap = reinterpret_cast<Ev*>(smem_raw + kScalBytes);
   InstS* ins = reinterpret_cast<InstS*>(heap + P.heap_cap);
   RunSlot* runs = reinterpret_cast<RunSlot*>(ins + P.n_inst);
+  const int fcap = fifo_cap_of(P.max_run);
+  Ev* fifo = reinterpret_cast<Ev*>(smem_raw + fifo_off(P));  // [NI][fcap]
 
   const int r = blockIdx.x;
   const int lane = threadIdx.x;
@@ -265,6 +279,55 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   auto push = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch) {
     if (lane == 0) push_l0(t, kind, call, inst, epoch);
     sync();
+  };
+  // A token tick of instance i (lane 0). Its time is >= every pending token
+  // event of i (all were scheduled at earlier clocks with the same step,
+  // rounding is monotone) and its seq is larger, so i's token events form a
+  // FIFO; only the FIFO's head needs to be in the heap for the heap minimum
+  // to be the global minimum. seq is taken here, at scheduling time.
+  auto push_token_l0 = [&](int i, double t, uint32_t call, int rs, uint32_t epoch) {
+    if (fcap == 0 || ins[i].fn >= fcap) {  // no FIFO room: an ordinary heap event
+      push_l0(t, EV_TOKEN, call, rs, epoch);
+      return;
+    }
+    Ev e{t, (uint64_t(EV_TOKEN) << 56) | sc.next_seq, call, rs, epoch, 1u};
+    sc.next_seq += 1;
+    const int n = ins[i].fn;
+    int slot = ins[i].fh + n;
+    if (slot >= fcap) slot -= fcap;
+    fifo[i * fcap + slot] = e;
+    ins[i].fn = n + 1;
+    if (n == 0) {  // new head: into the heap (seq already assigned)
+      if (KX_REPLACE_TOP && sc.top_free) {
+        sc.top_free = 0;
+        sift_down(e);
+      } else if (sc.heap_n >= P.heap_cap) {
+        sc.status = KX_ERR_CAPACITY;
+      } else {
+        int k = sc.heap_n++;
+        while (k > 0) {
+          const int pk = (k - 1) / KX_HEAP_ARITY;
+          if (!ev_less(e, heap[pk])) break;
+          heap[k] = heap[pk];
+          k = pk;
+        }
+        heap[k] = e;
+      }
+    }
+  };
+  // The root was just taken as the current event (sc.top_free = 1): a FIFO
+  // head hands its heap place to the next entry of its FIFO.
+  auto take_root_l0 = [&](const Ev& ev) {
+    if (ev.pad != 1u) return;
+    const int i = runs[ev.inst].inst;
+    int h = ins[i].fh + 1;
+    if (h >= fcap) h -= fcap;
+    ins[i].fh = h;
+    ins[i].fn -= 1;
+    if (ins[i].fn > 0) {
+      sc.top_free = 0;
+      sift_down(fifo[i * fcap + h]);
+    }
   };
   auto pop_l0 = [&]() {  // lane 0: remove the root (deferred pop)
     sc.top_free = 0;
@@ -847,6 +910,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (sc.next_arrival < w1 && !(heap[0].time < sc.next_arrival_time)) return;
       const Ev ev = heap[0];
       sc.top_free = 1;
+      take_root_l0(ev);
       if (ev.time < __dsub_rn(sc.clock, kTimeEpsilon)) {
         sc.status = KX_ERR_LOGIC;  // event time ran backwards
         return;
@@ -864,14 +928,14 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       const double step = ins[i].step;
       if (kind == EV_PREFILL) {
         runs[rs].phase = 1;
-        push_l0(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+        push_token_l0(i, __dadd_rn(clock, step), ev.call, rs, ev.epoch);
       } else {
         runs[rs].tokens += 1;
         runs[rs].kv += 1;
         ins[i].live_kv = __dadd_rn(ins[i].live_kv, 1.0);
         sc.decode_seconds = __dadd_rn(sc.decode_seconds, step);
         if (runs[rs].tokens >= runs[rs].target) push_l0(clock, EV_DONE, ev.call, rs, ev.epoch);
-        else push_l0(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+        else push_token_l0(i, __dadd_rn(clock, step), ev.call, rs, ev.epoch);
         if (ins[i].live_kv > ins[i].cap) push_l0(clock, EV_PREEMPT, 0, i, 0);
       }
     }
@@ -900,7 +964,10 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     }
     if (from_heap) {
       ev = heap[0];
-      if (lane == 0) sc.top_free = 1;
+      if (lane == 0) {
+        sc.top_free = 1;
+        take_root_l0(ev);
+      }
     } else if (lane == 0) {
       sc.next_arrival += 1;
       if (sc.next_arrival < w1) sc.next_arrival_time = I.arrival[sc.next_arrival];
@@ -940,7 +1007,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (rs < 0) continue;
       if (lane == 0) runs[rs].phase = 1;
       sync();
-      push(__dadd_rn(clock, ins[runs[rs].inst].step), EV_TOKEN, ev.call, rs, ev.epoch);
+      if (lane == 0) push_token_l0(runs[rs].inst, __dadd_rn(clock, ins[runs[rs].inst].step), ev.call, rs, ev.epoch);
+      sync();
     } else if (kind == EV_TOKEN) {  // engine.cpp:343-361
       const int rs = find_running(ev);
       if (rs < 0) continue;
@@ -954,7 +1022,10 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       }
       sync();
       if (runs[rs].tokens >= runs[rs].target) push(clock, EV_DONE, ev.call, rs, ev.epoch);
-      else push(__dadd_rn(clock, step), EV_TOKEN, ev.call, rs, ev.epoch);
+      else {
+        if (lane == 0) push_token_l0(i, __dadd_rn(clock, step), ev.call, rs, ev.epoch);
+        sync();
+      }
       if (ins[i].live_kv > ins[i].cap) push(clock, EV_PREEMPT, 0, i, 0);
     } else if (kind == EV_DONE) {  // engine.cpp:363-409
       const int rs = find_running(ev);
