@@ -498,12 +498,15 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   };
   auto finish_ledger = [&](int i, uint64_t uidv, double actual_end) {  // dispatcher.cpp:81-99,264-271
     if (P.dpolicy != KX_DISPATCH_TIME_SLOT) return;
+    // active_.find(uid): lanes over the table (uids are unique)
+    const int a = S.n_active[lb + i];
+    const int64_t o = (lb + i) * kActiveCap;
+    int j = a;
+    for (int j0 = 0; j0 < a && j == a; j0 += 32) {
+      const uint32_t hit = __ballot_sync(0xffffffffu, j0 + lane < a && S.act_uid[o + j0 + lane] == uidv);
+      if (hit) j = j0 + __ffs(hit) - 1;
+    }
     if (lane == 0) {
-      const int a = S.n_active[lb + i];
-      const int64_t o = (lb + i) * kActiveCap;
-      int j = 0;
-      for (; j < a; ++j)
-        if (S.act_uid[o + j] == uidv) break;
       if (j < a) {
         const double Pt = S.act_P[o + j], k = S.act_k[o + j], t0 = S.act_t0[o + j], T = S.act_T[o + j];
         const double t_end = __dadd_rn(t0, T);
@@ -544,25 +547,40 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         }
       }
       sync();
-      if (lane == 0) {
-        if (current > base) S.base[lb + i] = current;
-        int a = S.n_active[lb + i];
-        const int64_t o = (lb + i) * kActiveCap;
-        const double lim = __dadd_rn(now, kTimeEpsilon);
-        for (int j = 0; j < a;) {
-          if (__dadd_rn(S.act_t0[o + j], S.act_T[o + j]) <= lim) {
-            --a;
-            S.act_uid[o + j] = S.act_uid[o + a];
-            S.act_P[o + j] = S.act_P[o + a];
-            S.act_k[o + j] = S.act_k[o + a];
-            S.act_t0[o + j] = S.act_t0[o + a];
-            S.act_T[o + j] = S.act_T[o + a];
-          } else {
-            ++j;
-          }
+      if (lane == 0 && current > base) S.base[lb + i] = current;
+      // drop elapsed models (dispatcher.cpp:110-117): lanes over the active
+      // table, survivors compacted in place (the table is a set keyed by uid)
+      const int a = S.n_active[lb + i];
+      const int64_t o = (lb + i) * kActiveCap;
+      const double lim = __dadd_rn(now, kTimeEpsilon);
+      int w = 0;
+      for (int j0 = 0; j0 < a; j0 += 32) {
+        const int j = j0 + lane;
+        uint64_t au = 0;
+        double aP = 0.0, ak = 0.0, at0 = 0.0, aT = 0.0;
+        bool keep = false;
+        if (j < a) {
+          au = S.act_uid[o + j];
+          aP = S.act_P[o + j];
+          ak = S.act_k[o + j];
+          at0 = S.act_t0[o + j];
+          aT = S.act_T[o + j];
+          keep = !(__dadd_rn(at0, aT) <= lim);
         }
-        S.n_active[lb + i] = a;
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();  // the chunk's loads are ordered before its in-place stores
+        if (keep) {
+          const int d = w + __popc(m & ((1u << lane) - 1u));
+          S.act_uid[o + d] = au;
+          S.act_P[o + d] = aP;
+          S.act_k[o + d] = ak;
+          S.act_t0[o + d] = at0;
+          S.act_T[o + d] = aT;
+        }
+        w += __popc(m);
+        sync();
       }
+      if (lane == 0) S.n_active[lb + i] = w;
       sync();
     }
   };
