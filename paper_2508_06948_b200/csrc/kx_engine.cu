@@ -42,6 +42,12 @@
 #ifndef KX_TOKEN_FIFO
 #define KX_TOKEN_FIFO 1  // per-instance token-event FIFOs: only each FIFO's head sits in the heap
 #endif
+#ifndef KX_FAST_REG
+#define KX_FAST_REG 1  // the fast path keeps the scalar replica state in registers
+#endif
+#if KX_FAST_REG && KX_HEAP_ARITY != 2
+#error "KX_FAST_REG's sift is binary: build it with KX_HEAP_ARITY=2"
+#endif
 #ifndef KX_FLOYD
 #define KX_FLOYD 0  // bottom-up sift-down (hole to a leaf, then sift up): measured slower
 #endif
@@ -959,10 +965,141 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     }
   };
 
+  // The same fast path with the scalar state held in registers for the whole
+  // run of ticks (the shared-memory copies alias the heap and run slots, so
+  // the compiler would reload them after every store otherwise).
+  auto fast_ticks_reg = [&]() {  // lane 0
+    int heap_n = sc.heap_n, top_free = sc.top_free, status = sc.status;
+    uint64_t next_seq = sc.next_seq, processed = sc.processed;
+    double clk = sc.clock, dsec = sc.decode_seconds;
+    const bool have_arr = sc.next_arrival < w1;
+    const double t_arr = sc.next_arrival_time;
+    auto sift = [&](const Ev& e) {  // binary sift-down of e from the root
+      int k = 0;
+      while (true) {
+        int ch = 2 * k + 1;
+        if (ch >= heap_n) break;
+        double bt = heap[ch].time;
+        uint64_t bk = heap[ch].ks;
+        if (ch + 1 < heap_n) {
+          const double t1 = heap[ch + 1].time;
+          const uint64_t k1 = heap[ch + 1].ks;
+          if (t1 < bt || (t1 == bt && k1 < bk)) {
+            bt = t1;
+            bk = k1;
+            ++ch;
+          }
+        }
+        if (!(bt < e.time || (bt == e.time && bk < e.ks))) break;
+        heap[k] = heap[ch];
+        k = ch;
+      }
+      heap[k] = e;
+    };
+    auto hpush = [&](const Ev& e) {
+      if (KX_REPLACE_TOP && top_free) {
+        top_free = 0;
+        sift(e);
+      } else if (heap_n >= P.heap_cap) {
+        status = KX_ERR_CAPACITY;
+      } else {
+        int k = heap_n++;
+        while (k > 0) {
+          const int pk = (k - 1) >> 1;
+          if (!ev_less(e, heap[pk])) break;
+          heap[k] = heap[pk];
+          k = pk;
+        }
+        heap[k] = e;
+      }
+    };
+    auto push_ev = [&](double t, int kind, uint32_t call, int inst, uint32_t epoch, uint32_t fifo_flag) {
+      const Ev e{t, (uint64_t(kind) << 56) | next_seq, call, inst, epoch, fifo_flag};
+      next_seq += 1;
+      return e;
+    };
+    auto push_tok = [&](int i, double t, uint32_t call, int rs, uint32_t epoch) {
+      if (fcap == 0 || ins[i].fn >= fcap) {
+        hpush(push_ev(t, EV_TOKEN, call, rs, epoch, 0u));
+        return;
+      }
+      const Ev e = push_ev(t, EV_TOKEN, call, rs, epoch, 1u);
+      const int n = ins[i].fn;
+      int slot = ins[i].fh + n;
+      if (slot >= fcap) slot -= fcap;
+      fifo[i * fcap + slot] = e;
+      ins[i].fn = n + 1;
+      if (n == 0) hpush(e);
+    };
+    while (status == KX_OK) {
+      if (top_free) {
+        top_free = 0;
+        const Ev last = heap[--heap_n];
+        if (heap_n > 0) sift(last);
+      }
+      if (heap_n == 0) break;
+      const double t0 = heap[0].time;
+      const int kind = static_cast<int>(heap[0].ks >> 56);
+      if (kind != EV_TOKEN && kind != EV_PREFILL) break;
+      if (have_arr && !(t0 < t_arr)) break;
+      const Ev ev = heap[0];
+      top_free = 1;
+      if (ev.pad == 1u) {  // a FIFO head: the next entry takes the root
+        const int i = runs[ev.inst].inst;
+        int h = ins[i].fh + 1;
+        if (h >= fcap) h -= fcap;
+        ins[i].fh = h;
+        ins[i].fn -= 1;
+        if (ins[i].fn > 0) {
+          top_free = 0;
+          sift(fifo[i * fcap + h]);
+        }
+      }
+      if (ev.time < __dsub_rn(clk, kTimeEpsilon)) {
+        status = KX_ERR_LOGIC;  // event time ran backwards
+        break;
+      }
+      clk = clk > ev.time ? clk : ev.time;
+      processed += 1;
+      if (processed > P.max_events) {
+        status = KX_ERR_RUNTIME;
+        break;
+      }
+      const int rs = find_running(ev);
+      if (rs < 0) continue;
+      const int i = runs[rs].inst;
+      const double step = ins[i].step;
+      if (kind == EV_PREFILL) {
+        runs[rs].phase = 1;
+        push_tok(i, __dadd_rn(clk, step), ev.call, rs, ev.epoch);
+      } else {
+        const int64_t tok = runs[rs].tokens + 1;
+        runs[rs].tokens = tok;
+        runs[rs].kv += 1;
+        const double lv = __dadd_rn(ins[i].live_kv, 1.0);
+        ins[i].live_kv = lv;
+        dsec = __dadd_rn(dsec, step);
+        if (tok >= runs[rs].target) hpush(push_ev(clk, EV_DONE, ev.call, rs, ev.epoch, 0u));
+        else push_tok(i, __dadd_rn(clk, step), ev.call, rs, ev.epoch);
+        if (lv > ins[i].cap) hpush(push_ev(clk, EV_PREEMPT, 0, i, 0, 0u));
+      }
+    }
+    sc.heap_n = heap_n;
+    sc.top_free = top_free;
+    sc.status = status;
+    sc.next_seq = next_seq;
+    sc.processed = processed;
+    sc.clock = clk;
+    sc.decode_seconds = dsec;
+  };
+
   // ---- event loop (engine.cpp:85-123) ---------------------------------------
   while (sc.status == KX_OK) {
     if (KX_FAST_TICKS) {
-      if (lane == 0) fast_ticks();
+      if (lane == 0) {
+        if (KX_FAST_REG) fast_ticks_reg();
+        else fast_ticks();
+      }
       sync();
       if (sc.status != KX_OK) break;
     }
