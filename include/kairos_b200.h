@@ -182,7 +182,8 @@ int kx_dispatch_round(kx_sched* s, double now);
 /* Copies the decision log of the last round. per_pool_count[n_pools]:
  * rows written per pool; rows[] and candidate_peaks[] are pool-major with
  * `row_stride` rows per pool and `peak_stride` peaks per row (>= max
- * instances in a pool). Any output pointer may be NULL. Synchronizes. */
+ * instances in a pool); only the first per_pool_count[p] rows of each pool's
+ * block are written. Any output pointer may be NULL. Synchronizes. */
 int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
                       double* candidate_peaks, int64_t* row_stride, int64_t* peak_stride);
 

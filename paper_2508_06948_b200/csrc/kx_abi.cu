@@ -84,34 +84,80 @@ __global__ void k_flag_count(const uint8_t* __restrict__ flags, int64_t n, int c
   }
 }
 
-__global__ void k_scan_counts(uint32_t* __restrict__ c, int64_t m, int64_t* __restrict__ total) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    uint64_t acc = 0;
-    for (int64_t i = 0; i < m; ++i) {
-      const uint32_t v = c[i];
-      c[i] = static_cast<uint32_t>(acc);
-      acc += v;
-    }
-    *total = static_cast<int64_t>(acc);
+__global__ void __launch_bounds__(1024)
+k_scan_counts(uint32_t* __restrict__ c, int64_t m, int64_t* __restrict__ total) {
+  // Exclusive scan of m chunk counts in place, one CTA: each thread sums a
+  // contiguous run, a block scan of the run sums, then the runs are written.
+  __shared__ uint64_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t per = (m + blockDim.x - 1) / blockDim.x;
+  const int64_t b = int64_t(tid) * per, e = min(b + per, m);
+  uint64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += c[i];
+  uint64_t x = s;  // inclusive warp scan
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    uint64_t w = lane < nw ? wsum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  uint64_t acc = x - s + (warp > 0 ? wsum[warp - 1] : 0);
+  for (int64_t i = b; i < e; ++i) {
+    const uint32_t v = c[i];
+    c[i] = static_cast<uint32_t>(acc);
+    acc += v;
+  }
+  if (tid == blockDim.x - 1) *total = static_cast<int64_t>(wsum[(blockDim.x >> 5) - 1]);
 }
 
-template <typename T>
-__global__ void k_compact(const T* __restrict__ src, T* __restrict__ dst,
-                          const uint8_t* __restrict__ flags, int64_t n, int chunk,
-                          const uint32_t* __restrict__ offs) {
-  // One warp walks its CTA's chunk in order (stable).
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+// All queue columns of a chunk in one pass (ReadyQueue::pop of the placed
+// requests keeps the rest in order): flags read once, every kept request's
+// columns moved to its compacted position in `dst`.
+__global__ void __launch_bounds__(256)
+k_compact_queue(QueueDev src, QueueDev dst, int64_t n, int chunk, const uint32_t* __restrict__ offs) {
+  __shared__ uint32_t wcnt[2][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = int64_t(blockIdx.x) * chunk;
   const int64_t e = min(b + chunk, n);
   uint32_t out = offs[blockIdx.x];
-  for (int64_t i0 = b; i0 < e; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const bool keep = i < e && !flags[i];
+  int buf = 0;
+  for (int64_t i0 = b; i0 < e; i0 += 256) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool keep = i < e && !src.admitted[i];
     const uint32_t m = __ballot_sync(0xffffffffu, keep);
-    if (keep) dst[out + __popc(m & ((1u << lane) - 1u))] = src[i];
-    out += __popc(m);
+    if (lane == 0) wcnt[buf][warp] = __popc(m);
+    __syncthreads();
+    uint32_t excl = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = wcnt[buf][w];
+      excl += w < warp ? x : 0u;
+      total += x;
+    }
+    if (keep) {
+      const int64_t d = int64_t(out) + excl + __popc(m & ((1u << lane) - 1u));
+      dst.agent[d] = src.agent[i];
+      dst.prompt[d] = src.prompt[i];
+      dst.app_start[d] = src.app_start[i];
+      dst.queue_enter[d] = src.queue_enter[i];
+      dst.msg[d] = src.msg[i];
+      dst.uid[d] = src.uid[i];
+      dst.kept[d] = src.kept[i];
+      dst.pure_exec[d] = src.pure_exec[i];
+      dst.rem[d] = src.rem[i];
+    }
+    out += total;
+    buf ^= 1;
   }
 }
 
@@ -215,6 +261,7 @@ struct kx_sched {
   InstDev in{};
   int32_t* pool_begin = nullptr;
   Blob queue_blob, agent_blob, inst_const_blob, inst_mut_blob, inst_ckpt_blob, ws_blob, log_blob;
+  Blob queue_alt_blob;  // compaction target of kx_queue_remove_admitted (allocated on first use)
   bool have_ckpt = false;
 
   OrderWorkspace ws{};
@@ -568,6 +615,7 @@ void destroy_impl(kx_sched* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   free_blob(s->queue_blob);
+  free_blob(s->queue_alt_blob);
   free_blob(s->agent_blob);
   free_blob(s->inst_const_blob);
   free_blob(s->inst_mut_blob);
@@ -1406,29 +1454,39 @@ int kx_queue_remove_admitted(kx_sched* s) {
     k_flag_count<<<static_cast<unsigned>(chunks), 256, 0, s->stream>>>(
         s->q.admitted, n, static_cast<int>(kCompactChunk), s->compact_counts);
     KX_CHECK_LAUNCH();
-    k_scan_counts<<<1, 32, 0, s->stream>>>(s->compact_counts, chunks, s->compact_total);
+    k_scan_counts<<<1, 1024, 0, s->stream>>>(s->compact_counts, chunks, s->compact_total);
     KX_CHECK_LAUNCH();
-    // Compact each column through the (now unused) sort buffers.
-    auto compact = [&](auto* col) {
+    // All columns in one pass into the alternate queue blob (same layout),
+    // then each column's kept prefix back: the queue's addresses stay fixed,
+    // so captured graphs remain valid.
+    if (!s->queue_alt_blob.base) alloc_blob(s->queue_alt_blob, s->queue_blob.size);
+    auto alt = [&](auto* col) {
       using T = std::remove_pointer_t<decltype(col)>;
-      T* tmp = reinterpret_cast<T*>(s->ws.keys[0]);  // keys[0..1]+vals[0..1] = 16 B/elem
-      k_compact<T><<<static_cast<unsigned>(chunks), 32, 0, s->stream>>>(
-          col, tmp, s->q.admitted, n, static_cast<int>(kCompactChunk), s->compact_counts);
-      KX_CHECK_LAUNCH();
-      KX_CUDA(cudaMemcpyAsync(col, tmp, size_t(n) * sizeof(T), cudaMemcpyDeviceToDevice, s->stream));
+      return reinterpret_cast<T*>(s->queue_alt_blob.base + (reinterpret_cast<char*>(col) - s->queue_blob.base));
     };
-    compact(s->q.agent);
-    compact(s->q.prompt);
-    compact(s->q.app_start);
-    compact(s->q.queue_enter);
-    compact(s->q.msg);
-    compact(s->q.uid);
-    compact(s->q.kept);
-    compact(s->q.pure_exec);
-    compact(s->q.rem);
+    QueueDev qa{alt(s->q.agent), alt(s->q.prompt), alt(s->q.app_start), alt(s->q.queue_enter), alt(s->q.msg),
+                alt(s->q.uid),   alt(s->q.kept),   alt(s->q.pure_exec), alt(s->q.rem),         alt(s->q.admitted)};
+    k_compact_queue<<<static_cast<unsigned>(chunks), 256, 0, s->stream>>>(s->q, qa, n,
+                                                                          static_cast<int>(kCompactChunk),
+                                                                          s->compact_counts);
+    KX_CHECK_LAUNCH();
     int64_t total = 0;
     KX_CUDA(cudaMemcpyAsync(&total, s->compact_total, 8, cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaStreamSynchronize(s->stream));
+    const size_t T = static_cast<size_t>(total);
+    auto back = [&](auto* col) {
+      using E = std::remove_pointer_t<decltype(col)>;
+      if (T) KX_CUDA(cudaMemcpyAsync(col, alt(col), T * sizeof(E), cudaMemcpyDeviceToDevice, s->stream));
+    };
+    back(s->q.agent);
+    back(s->q.prompt);
+    back(s->q.app_start);
+    back(s->q.queue_enter);
+    back(s->q.msg);
+    back(s->q.uid);
+    back(s->q.kept);
+    back(s->q.pure_exec);
+    back(s->q.rem);
     s->n = total;
     s->order_valid = false;
     s->dispatch_valid = false;
@@ -1526,13 +1584,20 @@ int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
         fail(KX_ERR_CAPACITY, "decision log truncated (raise log_capacity_per_pool)");
     }
     if (per_pool_count) std::memcpy(per_pool_count, cnt.data(), P * 8);
-    if (rows)
-      KX_CUDA(cudaMemcpyAsync(rows, s->rows, P * s->log_cap * sizeof(kx_decision),
-                              cudaMemcpyDeviceToHost, s->stream));
-    if (candidate_peaks)
-      KX_CUDA(cudaMemcpyAsync(candidate_peaks, s->cand,
-                              P * s->log_cap * s->max_inst_per_pool * sizeof(double),
-                              cudaMemcpyDeviceToHost, s->stream));
+    // only each pool's filled rows travel (the layout keeps the log stride)
+    for (size_t p = 0; p < P; ++p) {
+      const size_t n = static_cast<size_t>(std::min<int64_t>(cnt[p], s->log_cap));
+      if (n == 0) continue;
+      const size_t r0 = p * static_cast<size_t>(s->log_cap);
+      if (rows)
+        KX_CUDA(cudaMemcpyAsync(rows + r0, s->rows + r0, n * sizeof(kx_decision), cudaMemcpyDeviceToHost,
+                                s->stream));
+      if (candidate_peaks) {
+        const size_t w = static_cast<size_t>(s->max_inst_per_pool);
+        KX_CUDA(cudaMemcpyAsync(candidate_peaks + r0 * w, s->cand + r0 * w, n * w * sizeof(double),
+                                cudaMemcpyDeviceToHost, s->stream));
+      }
+    }
     KX_CUDA(cudaStreamSynchronize(s->stream));
   });
 }

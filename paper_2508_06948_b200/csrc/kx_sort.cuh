@@ -152,10 +152,10 @@ constexpr size_t sort_dyn_smem() {
 // atomic rate on sm_100 (scripts/micro/pass_probe.cu: a tile's ranking takes
 // ~6 us with MATCH, ~3 us with the mask), so 3 wins on spread digits.
 #ifndef KX_SORT_MINB
-#define KX_SORT_MINB 4  // 4 blocks per SM: caps registers at 64 (unbounded, ptxas takes 119 and halves occupancy)
+#define KX_SORT_MINB 4  // 32-bit keys: 4 blocks per SM caps registers at 64 (unbounded, ptxas takes 119)
 #endif
 template <typename K, int kRank = 0>
-__global__ void __launch_bounds__(kSortThreads, KX_SORT_MINB)
+__global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? KX_SORT_MINB : 2)
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                 int64_t n, int shift, const uint32_t* __restrict__ global_excl,

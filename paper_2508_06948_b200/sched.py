@@ -178,8 +178,9 @@ class DeviceScheduler:
         cnt = np.zeros(self.n_pools, np.int64)
         rs, ps = C.c_int64(), C.c_int64()
         check(self.lib.kx_dispatch_fetch(self.h, ptr(cnt), None, None, C.byref(rs), C.byref(ps)))
-        rows = np.zeros(self.n_pools * rs.value, DECISION_DTYPE)
-        cand = np.zeros(self.n_pools * rs.value * ps.value, np.float64)
+        # only each pool's first cnt[p] rows are written (and returned)
+        rows = np.empty(self.n_pools * rs.value, DECISION_DTYPE)
+        cand = np.empty(self.n_pools * rs.value * ps.value, np.float64)
         check(self.lib.kx_dispatch_fetch(self.h, ptr(cnt), ptr(rows), ptr(cand), C.byref(rs),
                                          C.byref(ps)))
         rows = rows.reshape(self.n_pools, rs.value)
