@@ -228,3 +228,42 @@ def test_graph_replay_matches_direct_tick(gpu_lib):
             assert np.array_equal(a, b)
         for a, b in zip(cand, ref_cand):
             assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("policy", ["kairos", "oracle"])
+def test_serving_loop_pop_and_enqueue(gpu_lib, policy):
+    # ReadyQueue across rounds: the placed prefix is popped (vector::erase,
+    # order kept) and new arrivals are pushed back; the device queue (many
+    # 8192-element compaction chunks) must order exactly like the same
+    # logical queue sorted by the oracle.
+    rng = np.random.default_rng(31)
+    n0, n_new, pools = 120_000, 3_000, 3
+    q, t = random_queue(rng, n0 + 4 * n_new, n_agents=12, n_pools=pools, tie_grain=0.25)
+    inst = [kx.InstanceProfile(id=i, pool=i // 3, capacity_tokens=6000.0, max_batch=64)
+            for i in range(3 * pools)]
+    s = kx.DeviceScheduler(inst, n_pools=pools, queue_capacity=n0 + 4 * n_new, max_agents=16)
+    s.set_agent_tables(t.pool, t.pk, t.depth, t.T)
+    if t.rem is not None:
+        s.set_remaining_table(t.view.rem_base, t.rem, t.rem_present)
+    s.set_scheduler(policy)
+    cols = [q.agent, q.prompt, q.app_start, q.queue_enter, q.msg_key, q.uid]
+    s.upload(*[c[:n0] for c in cols])
+    logical = np.arange(n0)  # indices into q, in queue order
+    nxt = n0
+    for rnd in range(4):
+        s.restore() if rnd else s.checkpoint()
+        s.tick(5.0)
+        rows, _ = s.fetch_dispatch()
+        gone = np.concatenate([r["queue_index"][r["admitted"] == 1] for r in rows])
+        assert len(gone) > 0
+        s.remove_admitted()
+        logical = np.delete(logical, gone)
+        s.enqueue(*[c[nxt:nxt + n_new] for c in cols])
+        logical = np.concatenate([logical, np.arange(nxt, nxt + n_new)])
+        nxt += n_new
+        assert s.size() == len(logical)
+        s.order()
+        perm, offs = s.fetch_order()
+        sub = O.QueueArrays(*[c[logical] for c in cols])
+        ref_perm, ref_offs = O.sort(policy, sub, t, pools)
+        assert np.array_equal(offs, ref_offs) and np.array_equal(perm, ref_perm), f"round {rnd}"
