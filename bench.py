@@ -274,6 +274,7 @@ def run_mine(args):
             (arr.agent.astype(np.int32), arr.prompt, arr.app_start, arr.queue_enter,
              arr.msg_key.view(np.int64), arr.uid.view(np.int64))]
     a_bytes_per_req = sum(t.element_size() for t in apin)
+    s.graph_release()  # the timed replays are done: the pop may swap the queue's double buffer
     kx._abi.check(lib.kx_queue_upload(s.h, snap.n, C.byref(view), kx._abi.KX_MEM_HOST))
     a_pos = [0]
 

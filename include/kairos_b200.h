@@ -159,7 +159,9 @@ int kx_queue_upload(kx_sched* s, int64_t n, const kx_queue_view* q, int32_t mem)
 int kx_queue_enqueue(kx_sched* s, int64_t n, const kx_queue_view* q, int32_t mem);
 int kx_queue_size(kx_sched* s, int64_t* n);
 /* Drops every request admitted by the last dispatch round (ReadyQueue::pop
- * of the placed prefix), keeping the others in their relative order. */
+ * of the placed prefix), keeping the others in their relative order. The
+ * queue is double-buffered: without a captured graph the buffers swap;
+ * with one, the kept prefix is copied back so the graph's addresses hold. */
 int kx_queue_remove_admitted(kx_sched* s);
 
 /* K2: per-request OrderKey (SchedulerPolicy::order_key, scheduler.hpp:17-27),
@@ -377,6 +379,9 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
 int kx_graph_capture_begin(kx_sched* s);
 int kx_graph_capture_end(kx_sched* s);
 int kx_graph_launch(kx_sched* s);
+/* Drops the captured graph (kx_queue_remove_admitted then compacts by
+ * swapping the queue's double buffer instead of copying back). */
+int kx_graph_release(kx_sched* s);
 
 /* ---- priority table: W1 distance matrix ------------------------------------ */
 /* Replaces build_distance_matrix_from_samples (priority.cpp:60-65) ->

@@ -117,6 +117,7 @@ SIGNATURES = {
     "kx_set_remaining_table": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P, C.c_int32]),
     "kx_queue_upload": (C.c_int, [_P, C.c_int64, C.POINTER(kx_queue_view), C.c_int32]),
     "kx_queue_enqueue": (C.c_int, [_P, C.c_int64, C.POINTER(kx_queue_view), C.c_int32]),
+    "kx_graph_release": (C.c_int, [_P]),
     "kx_queue_size": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "kx_queue_remove_admitted": (C.c_int, [_P]),
     "kx_score": (C.c_int, [_P, _P, _P, _P, C.c_int32]),

@@ -1474,6 +1474,14 @@ int kx_queue_remove_admitted(kx_sched* s) {
     KX_CUDA(cudaMemcpyAsync(&total, s->compact_total, 8, cudaMemcpyDeviceToHost, s->stream));
     KX_CUDA(cudaStreamSynchronize(s->stream));
     const size_t T = static_cast<size_t>(total);
+    if (!s->graph_exec) {  // no captured graph holds the queue's addresses: swap the blobs
+      std::swap(s->queue_blob, s->queue_alt_blob);
+      s->q = qa;
+      s->n = total;
+      s->order_valid = false;
+      s->dispatch_valid = false;
+      return;
+    }
     auto back = [&](auto* col) {
       using E = std::remove_pointer_t<decltype(col)>;
       if (T) KX_CUDA(cudaMemcpyAsync(col, alt(col), T * sizeof(E), cudaMemcpyDeviceToDevice, s->stream));
@@ -1973,6 +1981,22 @@ int kx_graph_capture_end(kx_sched* s) {
     KX_CUDA(cudaSetDevice(s->device));
     KX_CUDA(cudaStreamEndCapture(s->stream, &s->graph));
     KX_CUDA(cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+  });
+}
+
+int kx_graph_release(kx_sched* s) {
+  return guard([&] {
+    require(s, "null handle");
+    KX_CUDA(cudaSetDevice(s->device));
+    KX_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->graph_exec) {
+      cudaGraphExecDestroy(s->graph_exec);
+      s->graph_exec = nullptr;
+    }
+    if (s->graph) {
+      cudaGraphDestroy(s->graph);
+      s->graph = nullptr;
+    }
   });
 }
 

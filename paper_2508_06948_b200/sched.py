@@ -295,6 +295,9 @@ class DeviceScheduler:
     def capture_end(self):
         check(self.lib.kx_graph_capture_end(self.h))
 
+    def graph_release(self):
+        check(self.lib.kx_graph_release(self.h))
+
     def graph_launch(self):
         """Replay the captured calls (one launch)."""
         check(self.lib.kx_graph_launch(self.h))

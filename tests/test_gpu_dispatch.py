@@ -230,8 +230,8 @@ def test_graph_replay_matches_direct_tick(gpu_lib):
             assert np.array_equal(bits(a), bits(b))
 
 
-@pytest.mark.parametrize("policy", ["kairos", "oracle"])
-def test_serving_loop_pop_and_enqueue(gpu_lib, policy):
+@pytest.mark.parametrize("policy,graph", [("kairos", False), ("oracle", False), ("kairos", True)])
+def test_serving_loop_pop_and_enqueue(gpu_lib, policy, graph):
     # ReadyQueue across rounds: the placed prefix is popped (vector::erase,
     # order kept) and new arrivals are pushed back; the device queue (many
     # 8192-element compaction chunks) must order exactly like the same
@@ -248,6 +248,12 @@ def test_serving_loop_pop_and_enqueue(gpu_lib, policy):
     s.set_scheduler(policy)
     cols = [q.agent, q.prompt, q.app_start, q.queue_enter, q.msg_key, q.uid]
     s.upload(*[c[:n0] for c in cols])
+    if graph:  # a captured graph pins the queue's addresses: the pop copies back
+        s.checkpoint()
+        s.capture_begin()
+        s.restore()
+        s.tick(5.0)
+        s.capture_end()
     logical = np.arange(n0)  # indices into q, in queue order
     nxt = n0
     for rnd in range(4):
