@@ -262,6 +262,8 @@ struct kx_sched {
   int32_t* pool_begin = nullptr;
   Blob queue_blob, agent_blob, inst_const_blob, inst_mut_blob, inst_ckpt_blob, ws_blob, log_blob;
   Blob queue_alt_blob;  // compaction target of kx_queue_remove_admitted (allocated on first use)
+  char* fetch_pinned = nullptr;  // pinned staging of kx_dispatch_fetch (allocated on first use)
+  size_t fetch_pinned_size = 0;
   bool have_ckpt = false;
 
   OrderWorkspace ws{};
@@ -616,6 +618,7 @@ void destroy_impl(kx_sched* s) {
   if (s->stream) cudaStreamSynchronize(s->stream);
   free_blob(s->queue_blob);
   free_blob(s->queue_alt_blob);
+  if (s->fetch_pinned) cudaFreeHost(s->fetch_pinned);
   free_blob(s->agent_blob);
   free_blob(s->inst_const_blob);
   free_blob(s->inst_mut_blob);
@@ -1592,21 +1595,47 @@ int kx_dispatch_fetch(kx_sched* s, int64_t* per_pool_count, kx_decision* rows,
         fail(KX_ERR_CAPACITY, "decision log truncated (raise log_capacity_per_pool)");
     }
     if (per_pool_count) std::memcpy(per_pool_count, cnt.data(), P * 8);
-    // only each pool's filled rows travel (the layout keeps the log stride)
+    // Only each pool's filled rows travel (the layout keeps the log stride),
+    // through a pinned staging buffer, then one host copy per block.
+    const size_t w = static_cast<size_t>(s->max_inst_per_pool);
+    size_t need = 0;
+    for (size_t p = 0; p < P; ++p) {
+      const size_t n = static_cast<size_t>(std::min<int64_t>(cnt[p], s->log_cap));
+      need += (rows ? n * sizeof(kx_decision) : 0) + (candidate_peaks ? n * w * sizeof(double) : 0);
+    }
+    if (need > s->fetch_pinned_size) {
+      if (s->fetch_pinned) cudaFreeHost(s->fetch_pinned);
+      s->fetch_pinned = nullptr;
+      s->fetch_pinned_size = 0;
+      const size_t full = P * static_cast<size_t>(s->log_cap) * (sizeof(kx_decision) + w * sizeof(double));
+      KX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&s->fetch_pinned), full));
+      s->fetch_pinned_size = full;
+    }
+    struct Piece {
+      char* dst;
+      size_t off, bytes;
+    };
+    std::vector<Piece> pieces;
+    size_t off = 0;
     for (size_t p = 0; p < P; ++p) {
       const size_t n = static_cast<size_t>(std::min<int64_t>(cnt[p], s->log_cap));
       if (n == 0) continue;
       const size_t r0 = p * static_cast<size_t>(s->log_cap);
-      if (rows)
-        KX_CUDA(cudaMemcpyAsync(rows + r0, s->rows + r0, n * sizeof(kx_decision), cudaMemcpyDeviceToHost,
-                                s->stream));
+      if (rows) {
+        const size_t b = n * sizeof(kx_decision);
+        KX_CUDA(cudaMemcpyAsync(s->fetch_pinned + off, s->rows + r0, b, cudaMemcpyDeviceToHost, s->stream));
+        pieces.push_back({reinterpret_cast<char*>(rows + r0), off, b});
+        off += b;
+      }
       if (candidate_peaks) {
-        const size_t w = static_cast<size_t>(s->max_inst_per_pool);
-        KX_CUDA(cudaMemcpyAsync(candidate_peaks + r0 * w, s->cand + r0 * w, n * w * sizeof(double),
-                                cudaMemcpyDeviceToHost, s->stream));
+        const size_t b = n * w * sizeof(double);
+        KX_CUDA(cudaMemcpyAsync(s->fetch_pinned + off, s->cand + r0 * w, b, cudaMemcpyDeviceToHost, s->stream));
+        pieces.push_back({reinterpret_cast<char*>(candidate_peaks + r0 * w), off, b});
+        off += b;
       }
     }
     KX_CUDA(cudaStreamSynchronize(s->stream));
+    for (const Piece& pc : pieces) std::memcpy(pc.dst, s->fetch_pinned + pc.off, pc.bytes);
   });
 }
 
