@@ -120,7 +120,12 @@ constexpr size_t kScalBytes = (sizeof(Scal) + 15) & ~size_t(15);  // heap starts
 
 // Token FIFO entries per instance (0 = off): running requests plus room for
 // stale events of preempted ones; a full FIFO falls back to the heap.
-__host__ __device__ inline int fifo_cap_of(int max_run) { return KX_TOKEN_FIFO ? max_run + 8 : 0; }
+#ifndef KX_FIFO_EXTRA
+#define KX_FIFO_EXTRA 8  // FIFO room beyond max_batch (tests shrink it to force the heap fallback)
+#endif
+__host__ __device__ inline int fifo_cap_of(int max_run) {
+  return KX_TOKEN_FIFO ? (max_run + KX_FIFO_EXTRA > 1 ? max_run + KX_FIFO_EXTRA : 1) : 0;
+}
 __host__ __device__ inline size_t fifo_off(const EngineParams& p) {
   const size_t end = kScalBytes + sizeof(Ev) * size_t(p.heap_cap) + sizeof(InstS) * size_t(p.n_inst) +
                      sizeof(RunSlot) * size_t(p.n_inst) * size_t(p.max_run);
