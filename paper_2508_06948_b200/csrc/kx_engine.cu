@@ -567,26 +567,32 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       int w = 0;
       for (int j0 = 0; j0 < a; j0 += 32) {
         const int j = j0 + lane;
-        uint64_t au = 0;
-        double aP = 0.0, ak = 0.0, at0 = 0.0, aT = 0.0;
         bool keep = false;
+        double at0 = 0.0, aT = 0.0;
         if (j < a) {
-          au = S.act_uid[o + j];
-          aP = S.act_P[o + j];
-          ak = S.act_k[o + j];
           at0 = S.act_t0[o + j];
           aT = S.act_T[o + j];
           keep = !(__dadd_rn(at0, aT) <= lim);
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();  // the chunk's loads are ordered before its in-place stores
-        if (keep) {
-          const int d = w + __popc(m & ((1u << lane) - 1u));
-          S.act_uid[o + d] = au;
-          S.act_P[o + d] = aP;
-          S.act_k[o + d] = ak;
-          S.act_t0[o + d] = at0;
-          S.act_T[o + d] = aT;
+        const int d = w + __popc(m & ((1u << lane) - 1u));
+        const bool move = keep && d != j;  // survivors ahead of every drop stay put
+        if (__any_sync(0xffffffffu, move)) {
+          uint64_t au = 0;
+          double aP = 0.0, ak = 0.0;
+          if (move) {
+            au = S.act_uid[o + j];
+            aP = S.act_P[o + j];
+            ak = S.act_k[o + j];
+          }
+          __syncwarp();  // the chunk's loads are ordered before its in-place stores
+          if (move) {
+            S.act_uid[o + d] = au;
+            S.act_P[o + d] = aP;
+            S.act_k[o + d] = ak;
+            S.act_t0[o + d] = at0;
+            S.act_T[o + d] = aT;
+          }
         }
         w += __popc(m);
         sync();
