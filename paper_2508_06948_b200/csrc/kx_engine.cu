@@ -112,6 +112,7 @@ struct InstS {  // InstanceState (engine.hpp:147-153) + Dispatcher::suspended_ +
   int32_t max_batch;
   uint64_t preempted_total;
   int32_t fh, fn;  // token FIFO: ring head, entries (the head is in the heap when fn > 0)
+  double act_min_end;  // min over the active table of t0 + T (gc skips the sweep above it)
 };
 
 }  // namespace
@@ -170,6 +171,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
     ins[i].k = I.k[i];
     ins[i].step = __ddiv_rn(1.0, I.k[i]);
     ins[i].max_batch = I.max_batch[i];
+    ins[i].act_min_end = __longlong_as_double(0x7ff0000000000000ll);  // +inf: empty table
   }
   for (int j = lane; j < NI * P.max_run; j += 32) {
     runs[j].used = 0;
@@ -503,6 +505,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         S.act_t0[o] = t0;
         S.act_T[o] = T;
         S.n_active[lb + i] = a + 1;
+        const double e = __dadd_rn(t0, T);
+        if (e < ins[i].act_min_end) ins[i].act_min_end = e;
       }
     }
     sync();
@@ -538,6 +542,8 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
             u[pos] = v;
           }
           S.act_T[o + j] = __dsub_rn(from, t0);
+          const double e = __dadd_rn(t0, S.act_T[o + j]);
+          if (e < ins[i].act_min_end) ins[i].act_min_end = e;
         }
       }
     }
@@ -561,10 +567,12 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
       if (lane == 0 && current > base) S.base[lb + i] = current;
       // drop elapsed models (dispatcher.cpp:110-117): lanes over the active
       // table, survivors compacted in place (the table is a set keyed by uid)
+      const double lim = __dadd_rn(now, kTimeEpsilon);
+      if (!(ins[i].act_min_end <= lim)) continue;  // nothing has elapsed (all lanes read the same)
       const int a = S.n_active[lb + i];
       const int64_t o = (lb + i) * kActiveCap;
-      const double lim = __dadd_rn(now, kTimeEpsilon);
       int w = 0;
+      double kept_min = __longlong_as_double(0x7ff0000000000000ll);
       for (int j0 = 0; j0 < a; j0 += 32) {
         const int j = j0 + lane;
         bool keep = false;
@@ -575,6 +583,7 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
           keep = !(__dadd_rn(at0, aT) <= lim);
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (keep) kept_min = fmin(kept_min, __dadd_rn(at0, aT));
         const int d = w + __popc(m & ((1u << lane) - 1u));
         const bool move = keep && d != j;  // survivors ahead of every drop stay put
         if (__any_sync(0xffffffffu, move)) {
@@ -597,7 +606,11 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         w += __popc(m);
         sync();
       }
-      if (lane == 0) S.n_active[lb + i] = w;
+      for (int off = 16; off > 0; off >>= 1) kept_min = fmin(kept_min, __shfl_xor_sync(0xffffffffu, kept_min, off));
+      if (lane == 0) {
+        S.n_active[lb + i] = w;
+        ins[i].act_min_end = kept_min;
+      }
       sync();
     }
   };
