@@ -451,9 +451,10 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
   auto ring_usage = [&](int i) { return S.usage + (lb + i) * ring; };
   auto ring_ex = [&](int i) { return S.ex + (lb + i) * ring; };
   // try_place, lanes over slots.
-  auto try_place = [&](int i, double Pt, double k, double t0, double T, int64_t* viol_out) -> double {
-    int64_t first, last;
-    span_bounds_dev(t0, T, P.slot_len, &first, &last);
+  // (first, last) = span_bounds(t0, T): the same for every instance of a
+  // head, so the caller computes it once.
+  auto try_place = [&](int i, double Pt, double k, double t0, double T, int64_t first, int64_t last,
+                       int64_t* viol_out) -> double {
     const double t_end = __dadd_rn(t0, T);
     const int64_t base = S.base[lb + i], hi = S.hi[lb + i];
     if (last >= first && (first < base || last >= base + ring)) fail(KX_ERR_CAPACITY);
@@ -863,11 +864,14 @@ k_replica_engine(EngineParams P, EngineInputs I, EngineState S) {
         }
       } else {
         double best = 0.0;
+        int64_t sfirst, slast;
+        span_bounds_dev(sc.clock, T, P.slot_len, &sfirst, &slast);
         for (int i = 0; i < NI; ++i) {
           const bool full = ins[i].running + ins[i].waiting >= ins[i].max_batch;
           if (ins[i].susp || full) continue;
           int64_t viol;
-          const double pk = try_place(i, static_cast<double>(I.prompt[head]), ins[i].k, sc.clock, T, &viol);
+          const double pk = try_place(i, static_cast<double>(I.prompt[head]), ins[i].k, sc.clock, T, sfirst,
+                                      slast, &viol);
           if (sc.status != KX_OK) return;
           if (viol != INT64_MAX) continue;
           if (target < 0 || pk < best || (pk == best && I.inst_id[i] < I.inst_id[target])) {
