@@ -1,19 +1,33 @@
 #!/usr/bin/env python
-"""Benchmark: scheduled requests/s (score + sort + dispatch) of one scheduling
-tick over a 16M-request queue (config C4: 8 LLM pools x 32 instances, 2M
-queued requests per pool, pre-loaded ledgers), Kairos policy + time-slot
-dispatch, on 1..N B200s (one process per GPU, weak scaling: every rank owns
-its own 8 pools).
+"""Benchmark: scheduled requests/s (score + sort + dispatch) of one
+scheduling tick, Kairos priority + time-slot dispatch, on 1..N B200s (one
+process per GPU, weak scaling: every rank owns its own pools and queue).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+  python bench.py [--config C1|C2|C3|C4] [--gpus N] [--steps K] [--warmup W]
+                  [--impl mine|reference]
+
+Configs (BASELINE.json `configs`; paper_2508_06948_b200/workload.py):
+  C1  QA app, 1 pool x 4 instances, 1K queued requests
+  C2  QA+RG+CG co-located, 1 pool x 16 instances, 64K queued requests
+  C3  100 generated apps (choice/parallel/feedback, 500 agents), 1 pool x 64
+      instances, 1M queued requests
+  C4  (default, the headline) 16M queued requests, 8 pools x 32 instances,
+      max_batch 64, pre-loaded ledgers
+C1-C3 queues are the product's realize() of the config's WorkloadConfig
+(bit-identical to the reference's realize(), tests/test_workload_general.py);
+C4 is a numpy draw of the co-located shapes at 16M.
 
 One step = restore the pre-tick instance/ledger state (device copy) + kx_tick
-(order the whole queue, dispatch every pool) on the handle's stream. Inputs
-are resident in HBM and larger than L2 (16M requests x 44 B = 704 MB). `e2e`
-runs the same step through the C ABI from pinned HOST buffers (queue upload
-H2D + tick + decision-log D2H inside the timed region). `--impl reference`
-times the reference's own CPU implementation (oracle/_ref/libkxref.so, built
-from the unmodified reference sources) on this host's cores.
+(order the whole queue, dispatch every pool) on the handle's stream, replayed
+as one CUDA graph. `value` times it with the queue resident in HBM (L2
+flushed between steps when the queue is smaller than L2). `e2e` runs the same
+step through the C ABI from pinned HOST buffers (queue upload H2D + tick +
+decision-log D2H inside the timed region). `parity` compares every decision
+of the measured tick (target, admitted, predicted peak bits, candidate peak
+bits) and the full queue order with the UNMODIFIED reference (Dispatcher +
+comparator sort, oracle/_ref/libkxref.so) run on the same inputs on the host
+in the cpu_baseline leg. `--impl reference` times that reference CPU path
+alone on this host's cores.
 """
 from __future__ import annotations
 
@@ -34,8 +48,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "scheduled requests/sec (score+sort+dispatch) at 1M–16M queue depth; % HBM roofline"
 UNIT = "requests/s"
-N_POOLS, PER_POOL, INST_PER_POOL = 8, 2_000_000, 32
-NOW = 10.0
+L2_BYTES = 126 << 20
+REF_BUDGET_S = 300.0  # the --impl reference run (warm-up + steps) fits in ~5 minutes
+SURVEY_B_ALG = 238.0
 
 
 def log(*a):
@@ -119,28 +134,31 @@ class Clocks:
                 "reasons": reasons, "samples": len(inside)}
 
 
-def build_c4(rank: int):
-    from paper_2508_06948_b200 import workload as W
-    t0 = time.time()
-    snap = W.snapshot(n_pools=N_POOLS, per_pool=PER_POOL, seed=1 + rank,
-                      msg_base=rank * 10_000_000, uid_base=1 + rank * 10 ** 9)
-    insts = W.instances(N_POOLS, INST_PER_POOL)
-    live, running, commits = W.preload(insts, seed=7 + rank, now=NOW)
-    log(f"[rank {rank}] synthetic C4 queue: {snap.n} requests, {len(insts)} instances "
-        f"({time.time() - t0:.1f}s)")
-    return snap, insts, live, running, commits
+def config_dict(w, ws):
+    snap = w.snap
+    qbytes = snap.n * 44
+    return {"workload": w.desc, "config": w.name, "queue_depth_per_gpu": snap.n, "pools": snap.n_pools,
+            "instances": len(w.insts), "agents": len(snap.agent_names), "policy": "kairos+time_slot",
+            "max_batch": w.insts[0].max_batch, "capacity_tokens": w.insts[0].capacity_tokens,
+            "l2": ("inputs (%d MB) larger than L2" % (qbytes >> 20)) if qbytes > L2_BYTES else
+                  ("L2 flushed between steps (queue %.1f MB < L2)" % (qbytes / 2 ** 20)),
+            "step": "state restore + kx_tick (order + dispatch), replayed as one CUDA graph",
+            "parallelism": f"pools per rank, weak scaling over {ws} GPU(s)"}
 
 
-def make_sched(snap, insts, live, running, commits, device):
+def make_sched(w, device):
     import paper_2508_06948_b200 as kx
-    s = kx.DeviceScheduler(insts, n_pools=N_POOLS, queue_capacity=snap.n, max_agents=len(snap.agent_pool),
-                           device=device)
+    snap = w.snap
+    s = kx.DeviceScheduler(w.insts, n_pools=snap.n_pools, queue_capacity=snap.n + w.arrivals.n,
+                           max_agents=len(snap.agent_pool), device=device)
     s.set_agent_tables(snap.agent_pool, snap.priority_key, snap.topo_depth, snap.expected_T)
     s.set_scheduler("kairos")
-    c = np.array(commits, dtype=np.float64).T if commits else np.zeros((6, 0))
-    s.commit_batch(c[0].astype(np.int32), np.array([x[1] for x in commits], np.uint64), c[2], c[3], c[4], c[5])
-    s.set_live(live, running, np.zeros(len(insts), np.int32))
-    s.gc(NOW)  # the pre-loaded state is the end of the previous round (engine.cpp:212)
+    cm = w.commits
+    if cm:
+        c = np.array(cm, dtype=np.float64).T
+        s.commit_batch(c[0].astype(np.int32), np.array([x[1] for x in cm], np.uint64), c[2], c[3], c[4], c[5])
+    s.set_live(w.live, w.running, np.zeros(len(w.insts), np.int32))
+    s.gc(w.now)  # the pre-loaded state is the end of the previous round (engine.cpp:212)
     s.checkpoint()
     return s
 
@@ -148,6 +166,7 @@ def make_sched(snap, insts, live, running, commits, device):
 def run_mine(args):
     import torch
     import paper_2508_06948_b200 as kx
+    from paper_2508_06948_b200 import workload as W
 
     ws, rank, local = dist_env()
     dist = None
@@ -156,11 +175,16 @@ def run_mine(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    snap, insts, live, running, commits = build_c4(rank)
-    s = make_sched(snap, insts, live, running, commits, local)
+    t0 = time.time()
+    w = W.build_workload(args.config, rank)
+    snap = w.snap
+    log(f"[rank {rank}] {w.name}: {snap.n} requests, {len(w.insts)} instances, "
+        f"{len(snap.agent_names)} agents ({time.time() - t0:.1f}s)")
+    s = make_sched(w, local)
     s.upload(snap.agent, snap.prompt, snap.app_start, snap.queue_enter, snap.msg_key, snap.uid)
     stream = torch.cuda.ExternalStream(s.stream_ptr(), device=dev)
     lib = s.lib
+    NOW = w.now
 
     def step():
         s.restore()
@@ -170,9 +194,11 @@ def run_mine(args):
     for _ in range(args.warmup):
         step()
     s.synchronize()
-    rows, _ = s.fetch_dispatch()
-    admitted = int(sum(int(r["admitted"].sum()) for r in rows))
-    decisions = int(sum(len(r) for r in rows))
+    gpu_rows, gpu_cand = s.fetch_dispatch()
+    admitted = int(sum(int(r["admitted"].sum()) for r in gpu_rows))
+    decisions = int(sum(len(r) for r in gpu_rows))
+    s.order()
+    gpu_perm, gpu_offs = s.fetch_order()
 
     # The step (state restore + tick) is captured once into a CUDA graph and
     # replayed: same kernels, one launch per step instead of ~30.
@@ -186,6 +212,9 @@ def run_mine(args):
     assert int(sum(int(r["admitted"].sum()) for r in r2)) == admitted, "graph replay differs"
 
     # ---- timed region: device-resident inputs, graph replays ---------------
+    flush = None
+    if snap.n * 44 <= L2_BYTES:  # queue fits in L2: flush it between steps (not timed)
+        flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -193,15 +222,26 @@ def run_mine(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     clocks.mark(True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        s.graph_launch()
-    ev1.record(stream)
-    ev1.synchronize()
+    if flush is None:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            s.graph_launch()
+        ev1.record(stream)
+        ev1.synchronize()
+        ms_total = ev0.elapsed_time(ev1)
+    else:
+        ms_total = 0.0
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                flush.zero_()
+                ev0.record(stream)
+                s.graph_launch()
+                ev1.record(stream)
+                ev1.synchronize()
+                ms_total += ev0.elapsed_time(ev1)
     clocks.mark(False)
     s.synchronize()
     torch.cuda.synchronize(dev)
-    ms_total = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if dist:
         t = torch.tensor([ms_total], device=dev)
@@ -212,8 +252,11 @@ def run_mine(args):
     # ---- per-kernel CUDA-event timing: the same K steps, launched directly ----
     s.profile(True)
     launches0 = lib.kx_launch_count()
-    for _ in range(args.steps):
-        step()
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            step()
     s.synchronize()
     launches = lib.kx_launch_count() - launches0  # the graph replays exactly these kernels
     phases = s.profile_read()
@@ -267,9 +310,7 @@ def run_mine(args):
     # pinned host memory (kx_queue_enqueue), ticks, reads the decision log
     # back and pops the placed requests (kx_queue_remove_admitted); the queue
     # stays at its depth because as many requests arrive as were placed.
-    from paper_2508_06948_b200 import workload as W
-    arr = W.snapshot(n_pools=N_POOLS, per_pool=8192, seed=101 + rank, msg_base=rank * 10_000_000 + 8_000_000,
-                     uid_base=1 + rank * 10 ** 9 + 100_000_000)
+    arr = w.arrivals
     apin = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for v in
             (arr.agent.astype(np.int32), arr.prompt, arr.app_start, arr.queue_enter,
              arr.msg_key.view(np.int64), arr.uid.view(np.int64))]
@@ -329,27 +370,26 @@ def run_mine(args):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom_name)
+            traffic = json.loads(tf.read_text()).get(args.config, {}).get(dom_name)
         except Exception:
             traffic = None
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(snap, insts, live, running, commits, sample_pools=args.cpu_pools)
+        cpu, parity = cpu_baseline(w, gpu_rows, gpu_cand, gpu_perm, gpu_offs)
 
     if rank == 0:
+        cfg = config_dict(w, ws)
+        cfg.update(admitted_per_step=admitted, decisions_per_step=decisions)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (co-located QA/RG/CG workflow shapes, workload.py; C4 snapshot)",
-            "config": {"workload": "C4: 16M queued requests, 8 LLM pools x 32 instances, Kairos "
-                                   "priority + time-slot dispatch, pre-loaded ledgers",
-                       "queue_depth_per_gpu": snap.n, "pools": N_POOLS, "instances": len(insts),
-                       "policy": "kairos+time_slot", "l2": "inputs (704 MB) larger than L2",
-                       "step": "state restore + kx_tick (order + dispatch), replayed as one CUDA graph; "
-                               "per-kernel times from the same K steps launched directly",
-                       "admitted_per_step": admitted, "decisions_per_step": decisions},
+            "data": ("synthetic: the product's realize() of the config's WorkloadConfig (seed 1+rank), "
+                     "first N calls queued" if w.name != "C4" else
+                     "synthetic (co-located QA/RG/CG workflow shapes drawn with numpy, workload.snapshot)"),
+            "config": cfg,
+            "parity": parity,
             "e2e": {"value": n_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms},
             # the serving loop with the queue resident: only arrivals go up
@@ -365,10 +405,9 @@ def run_mine(args):
                          "tick_frac": (tick_bytes / (ms_step / 1e3) / 1e9) / hbm,
                          # SURVEY §8(d)'s north-star accounting of score + sort: a 64-bit key
                          # through 8 LSD passes, B_alg = 38 + 8 + 192 = 238 B/request. This path
-                         # moves fewer bytes (32-bit compact key, 4 passes; tick_alg_bytes), so
-                         # this is the requests/s the target is stated in, not measured traffic.
+                         # moves fewer bytes (32-bit compact key; tick_alg_bytes), so this is the
+                         # requests/s the target is stated in, not measured traffic.
                          "survey_b_alg_per_request": SURVEY_B_ALG,
-                         "survey_achieved": value * SURVEY_B_ALG / 1e9,
                          "survey_frac": value * SURVEY_B_ALG / 1e9 / hbm},
             "kernels": kernels,
             "gpu_launches": int(launches),
@@ -378,9 +417,6 @@ def run_mine(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-
-
-SURVEY_B_ALG = 238.0
 
 
 # ---- the reference's CPU path ------------------------------------------------
@@ -403,22 +439,30 @@ def _ref_lib():
     L.kxref_pool_tick.argtypes = [P, C.c_double]
     L.kxref_pools_tick.restype = C.c_double
     L.kxref_pools_tick.argtypes = [C.POINTER(P), C.c_int, C.c_double, C.c_int]
+    L.kxref_pool_record.argtypes = [P, C.c_int]
+    L.kxref_pool_log.restype = C.c_int64
+    L.kxref_pool_log.argtypes = [P, P, P, P, P, P]
+    L.kxref_pool_order.restype = C.c_int64
+    L.kxref_pool_order.argtypes = [P, P]
     return L
 
 
 class RefPools:
-    """The reference's data structures for `pools` pools of the workload."""
+    """The reference's data structures (Dispatcher with pre-loaded ledgers,
+    PendingRequest queue, policy table) for `pools` pools of the workload."""
 
-    def __init__(self, L, snap, insts, live, running, commits, pools):
+    def __init__(self, L, w, pools):
         self.L = L
+        snap, insts = w.snap, w.insts
         names = [n.encode() for n in snap.agent_names]
         self.cnames = (C.c_char_p * len(names))(*names)
-        self.handles = []
+        self.handles, self.pools, self.ni = [], list(pools), []
         self.n = 0
         self._keep = []
+        all_ids = np.array([i.id for i in insts])
         for p in pools:
-            ids = np.array([i.id for i in insts if i.pool == p], np.int32)
-            sel = np.isin(np.array([i.id for i in insts]), ids)
+            sel = np.array([i.pool == p for i in insts])
+            ids = all_ids[sel].astype(np.int32)
             caps = np.array([i.capacity_tokens for i in insts])[sel]
             ks = np.array([i.decode_rate for i in insts])[sel]
             mb = np.array([i.max_batch for i in insts], np.int32)[sel]
@@ -428,12 +472,12 @@ class RefPools:
                                  0.5, 0.85, 0, len(names), C.cast(self.cnames, C.c_void_p),
                                  snap.priority_key.ctypes.data, snap.pk_known.ctypes.data,
                                  snap.topo_depth.ctypes.data, snap.expected_T.ctypes.data)
-            for (iid, uid, P, k, t0, T) in commits:
+            for (iid, uid, P, k, t0, T) in w.commits:
                 if iid in ids:
                     L.kxref_pool_commit(h, int(iid), int(uid), int(P), t0, T)
-            L.kxref_pool_gc(h, NOW)
-            lv = np.ascontiguousarray(live[sel])
-            rn = np.ascontiguousarray(running[sel], np.int32)
+            L.kxref_pool_gc(h, w.now)
+            lv = np.ascontiguousarray(w.live[sel])
+            rn = np.ascontiguousarray(w.running[sel], np.int32)
             wt = np.zeros(len(ids), np.int32)
             self._keep += [lv, rn, wt]
             L.kxref_pool_set_live(h, lv.ctypes.data, rn.ctypes.data, wt.ctypes.data)
@@ -443,33 +487,95 @@ class RefPools:
             L.kxref_pool_set_queue(h, len(cols[0]), *[c.ctypes.data for c in cols], C.cast(self.cnames, C.c_void_p))
             self.n += len(cols[0])
             self.handles.append(h)
+            self.ni.append(len(ids))
         self.arr = (C.c_void_p * len(self.handles))(*self.handles)
 
-    def tick(self, threads):
-        return self.L.kxref_pools_tick(self.arr, len(self.handles), NOW, threads)
+    def tick(self, threads, now):
+        return self.L.kxref_pools_tick(self.arr, len(self.handles), now, threads)
+
+    def record(self, on: bool):
+        for h in self.handles:
+            self.L.kxref_pool_record(h, int(on))
+
+    def log(self, j):
+        h, ni = self.handles[j], self.ni[j]
+        n = self.L.kxref_pool_log(h, None, None, None, None, None)
+        uid = np.zeros(n, np.uint64)
+        tgt = np.zeros(n, np.int32)
+        adm = np.zeros(n, np.int32)
+        peak = np.zeros(n)
+        cand = np.zeros((n, ni))
+        self.L.kxref_pool_log(h, uid.ctypes.data, tgt.ctypes.data, adm.ctypes.data, peak.ctypes.data,
+                              cand.ctypes.data)
+        return uid, tgt, adm, peak, cand
+
+    def order(self, j):
+        n = self.L.kxref_pool_order(self.handles[j], None)
+        out = np.zeros(n, np.uint64)
+        self.L.kxref_pool_order(self.handles[j], out.ctypes.data)
+        return out
 
     def close(self):
         for h in self.handles:
             self.L.kxref_pool_free(h)
 
 
-def cpu_baseline(snap, insts, live, running, commits, sample_pools=None):
+def compare_decisions(ref, j, rows, cand):
+    """Mismatching decision rows of pool ref.pools[j]: uid, target, admitted,
+    predicted_peak bits, candidate_peaks bits (engine.cpp:242-246)."""
+    uid, tgt, adm, peak, rc = ref.log(j)
+    n = min(len(uid), len(rows))
+    ni = rc.shape[1]
+    bad = np.zeros(n, bool)
+    if n:
+        bad |= rows["uid"][:n] != uid[:n]
+        bad |= rows["target"][:n] != tgt[:n]
+        bad |= rows["admitted"][:n] != adm[:n]
+        bad |= rows["predicted_peak"][:n].view(np.uint64) != peak[:n].view(np.uint64)
+        bad |= (np.ascontiguousarray(cand[:n, :ni]).view(np.uint64) != rc[:n].view(np.uint64)).any(axis=1)
+    return len(uid), int(bad.sum()) + abs(len(uid) - len(rows))
+
+
+def cpu_baseline(w, gpu_rows=None, gpu_cand=None, gpu_perm=None, gpu_offs=None):
+    """One tick of the reference's own CPU path (every pool on its own host
+    thread), timed; with the GPU's decisions/order given, also their parity."""
     L = _ref_lib()
     if L is None:
-        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                "sample": "unavailable: oracle/_ref/libkxref.so not built"}
+        return ({"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                 "sample": "unavailable: oracle/_ref/libkxref.so not built"}, None)
     ncpu = os.cpu_count() or 1
-    k = sample_pools or min(N_POOLS, ncpu)
+    P = w.snap.n_pools
+    k = min(P, ncpu)
     t0 = time.time()
-    ref = RefPools(L, snap, insts, live, running, commits, list(range(k)))
+    ref = RefPools(L, w, list(range(k)))
     log(f"cpu baseline: built reference queues for {k} pools ({ref.n} requests) in {time.time() - t0:.1f}s")
-    secs = ref.tick(min(k, ncpu))
+    ref.record(gpu_rows is not None)
+    threads = min(k, ncpu)
+    secs = ref.tick(threads, w.now)
+    cpu = {"value": ref.n / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+           "sample": f"one tick of {k} of the {P} pool(s) ({ref.n} requests), one pool per host thread: "
+                     f"reference comparator std::sort (harness.cpp:92-100) + Dispatcher choose/commit over "
+                     f"the dispatched prefix (engine.cpp:220-268) + gc, decision log recorded "
+                     f"({secs:.2f}s)", "seconds": secs, "host_cpus": ncpu}
+    parity = None
+    if gpu_rows is not None:
+        t1 = time.time()
+        dec = mis = omis = 0
+        for j, p in enumerate(ref.pools):
+            d, m = compare_decisions(ref, j, gpu_rows[p], gpu_cand[p])
+            dec += d
+            mis += m
+            ro = ref.order(j)
+            go = w.snap.uid[gpu_perm[gpu_offs[p]:gpu_offs[p + 1]]]
+            omis += int((ro != go).sum()) if len(ro) == len(go) else max(len(ro), len(go))
+        parity = {"pools_checked": k, "pools": P, "decisions": dec, "mismatches": mis,
+                  "order_checked": int(ref.n), "order_mismatches": omis,
+                  "checked": "target, admitted, predicted_peak bits, candidate_peaks bits per decision; "
+                             "full per-pool queue order (uids)",
+                  "reference": "unmodified reference Dispatcher + ReadyQueue comparator (oracle/_ref)",
+                  "seconds": time.time() - t1}
     ref.close()
-    return {"value": ref.n / secs, "unit": UNIT, "cores": min(k, ncpu), "kind": "reference",
-            "sample": f"one tick of {k} of the 8 C4 pools ({ref.n} requests, 2M per pool), one pool per "
-                      f"thread: reference comparator std::sort + Dispatcher choose/commit over the "
-                      f"dispatched prefix + gc ({secs:.2f}s)",
-            "seconds": secs, "host_cpus": ncpu}
+    return cpu, parity
 
 
 def run_reference(args):
@@ -481,36 +587,41 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libkxref.so is not built"}))
         return
     from paper_2508_06948_b200 import workload as W
-    snap = W.snapshot(n_pools=N_POOLS, per_pool=PER_POOL, seed=1)
-    insts = W.instances(N_POOLS, INST_PER_POOL)
-    live, running, commits = W.preload(insts, seed=7, now=NOW)
+    w = W.build_workload(args.config, 0)
     ncpu = os.cpu_count() or 1
-    pools = list(range(N_POOLS))
-    ref = RefPools(L, snap, insts, live, running, commits, pools)
-    threads = min(N_POOLS, ncpu)
-    first = ref.tick(threads)  # warm-up 1, also sizes the sample
-    budget = 150.0
-    per_pool = first / max(1, -(-N_POOLS // threads))
-    k = N_POOLS
-    if first * (args.steps + args.warmup) > budget:
-        k = max(1, min(N_POOLS, int(budget / (args.steps + args.warmup) / per_pool) * threads))
-    if k < N_POOLS:
+    P = w.snap.n_pools
+    ref = RefPools(L, w, list(range(P)))
+    threads = min(P, ncpu)
+    first = ref.tick(threads, w.now)  # warm-up 1, also sizes the sample
+    per_round = first
+    k = P
+    if first * (args.steps + args.warmup) > REF_BUDGET_S:
+        # bounded sample: fewer pools per step (each pool keeps its full queue)
+        rounds = -(-P // threads)
+        per_pool_round = first / rounds
+        k = max(1, min(P, int(REF_BUDGET_S / (args.steps + args.warmup) / per_pool_round) * threads))
+    if k < P:
         ref.close()
-        ref = RefPools(L, snap, insts, live, running, commits, list(range(k)))
+        ref = RefPools(L, w, list(range(k)))
         threads = min(k, ncpu)
     for _ in range(max(0, args.warmup - 1)):
-        ref.tick(threads)
-    times = [ref.tick(threads) for _ in range(args.steps)]
+        ref.tick(threads, w.now)
+    times = [ref.tick(threads, w.now) for _ in range(args.steps)]
     ms = 1e3 * sum(times) / len(times)
     value = ref.n / (ms / 1e3)
-    sample = (f"{k} of 8 C4 pools per step ({ref.n} requests), {threads} threads: reference comparator "
-              f"std::sort (harness.cpp:92-100) + reference Dispatcher over the dispatched prefix + gc")
+    sample = (f"{k} of {P} pool(s) per step ({ref.n} requests), {threads} host threads (one pool per "
+              f"thread, the reference's one-Simulator-per-thread model, harness.cpp:189-206): reference "
+              f"comparator std::sort (harness.cpp:92-100) + reference Dispatcher over the dispatched "
+              f"prefix + gc. The prefix walk replaces the reference's O(N) best_index scan per placement "
+              f"(priority.hpp:89-103), so this baseline is faster than the stock path")
+    cfg = config_dict(w, ws)
+    del per_round
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (workload.py C4)",
-        "config": {"workload": "C4: 16M queued requests, 8 LLM pools x 32 instances, Kairos "
-                               "priority + time-slot dispatch, pre-loaded ledgers"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, the same inputs as the mine arm (workload.build_workload)",
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -520,12 +631,12 @@ def run_reference(args):
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pools", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

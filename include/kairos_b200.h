@@ -375,7 +375,11 @@ int kx_sorting_accuracy(int64_t n, const int32_t* agent, const double* remaining
 
 /* ---- CUDA graph of a repeated step (e.g. kx_state_restore + kx_tick) ------ */
 /* Calls between begin and end are captured (asynchronous calls only: no
- * fetches, profiling off) and replayed by kx_graph_launch with one launch. */
+ * fetches, profiling off) and replayed by kx_graph_launch with one launch.
+ * The captured kernels carry the queue size of the capture: after a
+ * kx_queue_remove_admitted / kx_queue_enqueue that changed the size,
+ * kx_graph_launch fails with KX_ERR_LOGIC (capture again). After a replay
+ * the last order / dispatch round is fetchable as after the captured calls. */
 int kx_graph_capture_begin(kx_sched* s);
 int kx_graph_capture_end(kx_sched* s);
 int kx_graph_launch(kx_sched* s);
@@ -412,6 +416,56 @@ typedef struct kx_realization kx_realization;
 const char* kx_builtin_agent_name(int32_t agent);
 int kx_realize_builtin(uint32_t app_mask, double rate, double duration, uint64_t seed,
                        double prefill_rate, double decode_rate, kx_realization** out);
+/* realize() (workload.cpp:319-372) for a general WorkloadConfig
+ * (workload.hpp:69-83): agents are dense indices 0..n_agents-1 (the caller
+ * keeps the names), AgentSpec (workload.hpp:39-52) with a choice list,
+ * a parallel list and an optional feedback edge; AppSpec (workload.hpp:55-60)
+ * lists its member agents (the validate() cycle check walks from them).
+ * TraceFile arrivals are passed as the file's raw timestamps
+ * (ingest_arrival_trace's parse is the caller's; scale_arrival_gaps and the
+ * duration cut are applied here). validate()'s errors -> KX_ERR_INVALID. */
+enum kx_length_kind { KX_LEN_FIXED = 0, KX_LEN_UNIFORM = 1, KX_LEN_LOGNORMAL = 2 };
+typedef struct kx_length_spec {   /* LengthSpec (workload.hpp:18-33) */
+  int32_t kind;                   /* kx_length_kind */
+  int32_t _pad;
+  double a;                       /* Fixed: value; Uniform: lo; Lognormal: mu = log(median) */
+  double b;                       /* Uniform: hi; Lognormal: sigma */
+  int64_t min_tokens, max_tokens;
+} kx_length_spec;
+typedef struct kx_agent_spec {
+  kx_length_spec prompt_len, output_len;
+  int32_t n_choice;               /* choice: (choice_to[j], choice_p[j]) */
+  int32_t n_parallel;
+  const int32_t* choice_to;
+  const double* choice_p;
+  const int32_t* parallel_to;
+  int32_t feedback_target;        /* -1 = no feedback */
+  int32_t feedback_max_iterations;
+  double feedback_probability;
+} kx_agent_spec;
+typedef struct kx_app_spec {
+  int32_t entry;                  /* agent index */
+  int32_t n_members;
+  const int32_t* members;         /* the app's agents */
+  double weight;
+} kx_app_spec;
+enum kx_arrival_kind { KX_ARRIVAL_POISSON = 0, KX_ARRIVAL_TRACE = 1 };
+enum kx_entry_selection { KX_ENTRY_WEIGHTED = 0, KX_ENTRY_CYCLE = 1 };
+typedef struct kx_workload_config {
+  int32_t n_agents;
+  int32_t n_apps;
+  const kx_agent_spec* agents;
+  const kx_app_spec* apps;
+  int32_t arrival_kind;           /* kx_arrival_kind */
+  int32_t entry_selection;        /* kx_entry_selection */
+  double rate;                    /* Poisson arrivals per second */
+  int64_t n_trace;                /* TraceFile: raw timestamps */
+  const double* trace;
+  double trace_scale;             /* inter-arrival scaling factor */
+  double duration;                /* arrival window, seconds */
+} kx_workload_config;
+int kx_realize(const kx_workload_config* config, uint64_t seed, double prefill_rate, double decode_rate,
+               kx_realization** out);
 int kx_realization_sizes(const kx_realization* r, int64_t* n_workflows, int64_t* n_calls);
 /* Any output may be NULL; wf_offsets has n_workflows + 1 entries. */
 int kx_realization_copy(const kx_realization* r, double* arrival, int32_t* app, int64_t* wf_offsets,

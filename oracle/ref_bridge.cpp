@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <string>
@@ -51,6 +52,13 @@ struct RefPool {
   std::vector<PendingRequest> queue0, queue;
   int64_t last_admitted = 0;
   int64_t last_decisions = 0;
+  // Decision log of the last tick (engine.cpp:242-246 DecisionLogRow plus
+  // DispatchDecision::candidate_peaks), filled only when `record` is set so
+  // the timed baseline does not pay for it.
+  bool record = false;
+  std::vector<uint64_t> log_uid;
+  std::vector<int32_t> log_target, log_admitted;
+  std::vector<double> log_peak, log_cand;
 };
 
 }  // namespace
@@ -153,6 +161,11 @@ void kxref_pool_reset(void* h) {
 int64_t kxref_pool_tick(void* h, double now) {
   auto* p = static_cast<RefPool*>(h);
   const SchedulerPolicy& s = *p->policy;
+  p->log_uid.clear();
+  p->log_target.clear();
+  p->log_admitted.clear();
+  p->log_peak.clear();
+  p->log_cand.clear();
   std::sort(p->queue.begin(), p->queue.end(), [&](const PendingRequest& a, const PendingRequest& b) {
     const auto ka = s.order_key(a);
     const auto kb = s.order_key(b);
@@ -176,6 +189,14 @@ int64_t kxref_pool_tick(void* h, double now) {
     }
     DispatchDecision d = p->disp->choose(head, now, T, live);
     ++decisions;
+    if (p->record) {
+      p->log_uid.push_back(head.uid);
+      p->log_target.push_back(d.target ? *d.target : -1);
+      p->log_peak.push_back(d.target ? d.predicted_peak : 0.0);
+      p->log_admitted.push_back(0);
+      for (std::size_t i = 0; i < ni; ++i)
+        p->log_cand.push_back(i < d.candidate_peaks.size() ? d.candidate_peaks[i] : -1.0);
+    }
     if (!d.target) break;
     const std::size_t ti =
         static_cast<std::size_t>(std::find(p->ids.begin(), p->ids.end(), *d.target) - p->ids.begin());
@@ -185,6 +206,7 @@ int64_t kxref_pool_tick(void* h, double now) {
       continue;
     }
     p->disp->commit(d, now, T);
+    if (p->record) p->log_admitted.back() = 1;
     p->live[ti] += static_cast<double>(head.prompt_tokens);
     p->running[ti] += 1;
     ++admitted;
@@ -197,6 +219,36 @@ int64_t kxref_pool_tick(void* h, double now) {
 }
 
 int64_t kxref_pool_last_decisions(void* h) { return static_cast<RefPool*>(h)->last_decisions; }
+
+// Decision logging for parity checks (off by default: the timed baseline
+// does not record).
+void kxref_pool_record(void* h, int on) { static_cast<RefPool*>(h)->record = on != 0; }
+
+// Rows logged by the last tick; copies them out (any pointer may be NULL;
+// cand is rows x n_inst, Dispatcher ids_ order).
+int64_t kxref_pool_log(void* h, uint64_t* uid, int32_t* target, int32_t* admitted, double* peak,
+                       double* cand) {
+  auto* p = static_cast<RefPool*>(h);
+  const std::size_t n = p->log_uid.size();
+  for (std::size_t j = 0; j < n; ++j) {
+    if (uid) uid[j] = p->log_uid[j];
+    if (target) target[j] = p->log_target[j];
+    if (admitted) admitted[j] = p->log_admitted[j];
+    if (peak) peak[j] = p->log_peak[j];
+  }
+  if (cand)
+    for (std::size_t j = 0; j < p->log_cand.size(); ++j) cand[j] = p->log_cand[j];
+  return static_cast<int64_t>(n);
+}
+
+// uids of the queue in the order the last tick sorted it (the reference
+// comparator's permutation, harness.cpp:92-100); returns the queue length.
+int64_t kxref_pool_order(void* h, uint64_t* uid) {
+  auto* p = static_cast<RefPool*>(h);
+  if (uid)
+    for (std::size_t j = 0; j < p->queue.size(); ++j) uid[j] = p->queue[j].uid;
+  return static_cast<int64_t>(p->queue.size());
+}
 
 // Ticks `n` pools concurrently on up to `threads` threads (the reference's
 // std::async-per-cell model, harness.cpp:189-206); returns wall seconds.
@@ -363,3 +415,140 @@ extern "C" int kxref_sim_run(
     return 1;
   }
 }
+
+// ---- realize() for a general WorkloadConfig (tests of kx_realize) -------
+// Builds the reference WorkloadConfig (workload.hpp:69-83) from the C ABI's
+// flat description (include/kairos_b200.h kx_workload_config), agent i named
+// "a<i>", app k named "app<k>", and runs the reference realize()
+// (workload.cpp:319-372). TraceFile arrivals go through a temporary file so
+// the reference's own ingest_arrival_trace parses them.
+#include <cstdlib>
+#include <fstream>
+#include <unistd.h>
+
+#include "kairos/workload.hpp"
+#include "../include/kairos_b200.h"
+
+namespace {
+LengthSpec ref_length(const kx_length_spec& l) {
+  LengthSpec s;
+  s.kind = static_cast<LengthSpec::Kind>(l.kind);
+  s.a = l.a;
+  s.b = l.b;
+  s.min_tokens = l.min_tokens;
+  s.max_tokens = l.max_tokens;
+  return s;
+}
+struct RefRealization {
+  std::vector<double> arrival;
+  std::vector<int64_t> wf_offsets{0};
+  std::vector<int32_t> agent, parent;
+  std::vector<int64_t> prompt, target;
+  std::vector<double> pure, rem, rem_map;
+  std::vector<uint64_t> uid;
+  std::string error;
+};
+}  // namespace
+
+extern "C" void* kxref_realize(const kx_workload_config* c, uint64_t seed, double prefill, double decode) {
+  auto* out = new RefRealization();
+  std::string trace_path;
+  try {
+    WorkloadConfig cfg;
+    auto name = [](int i) { return "a" + std::to_string(i); };
+    for (int k = 0; k < c->n_apps; ++k) {
+      AppSpec app;
+      app.name = "app" + std::to_string(k);
+      app.entry = name(c->apps[k].entry);
+      app.weight = c->apps[k].weight;
+      for (int j = 0; j < c->apps[k].n_members; ++j) {
+        const int i = c->apps[k].members[j];
+        const kx_agent_spec& s = c->agents[i];
+        AgentSpec a;
+        a.name = name(i);
+        a.prompt_len = ref_length(s.prompt_len);
+        a.output_len = ref_length(s.output_len);
+        for (int t = 0; t < s.n_choice; ++t) a.choice.emplace_back(name(s.choice_to[t]), s.choice_p[t]);
+        for (int t = 0; t < s.n_parallel; ++t) a.parallel.push_back(name(s.parallel_to[t]));
+        if (s.feedback_target >= 0)
+          a.feedback = AgentSpec::Feedback{name(s.feedback_target), s.feedback_probability,
+                                           s.feedback_max_iterations};
+        app.agents.push_back(std::move(a));
+      }
+      cfg.apps.push_back(std::move(app));
+    }
+    if (c->arrival_kind == KX_ARRIVAL_TRACE) {
+      char tmpl[] = "/tmp/kxref_traceXXXXXX";
+      const int fd = mkstemp(tmpl);
+      if (fd < 0) throw std::runtime_error("mkstemp");
+      close(fd);
+      trace_path = tmpl;
+      std::FILE* f = std::fopen(tmpl, "w");
+      for (int64_t j = 0; j < c->n_trace; ++j) std::fprintf(f, "%.17g\n", c->trace[j]);
+      std::fclose(f);
+      cfg.arrival.kind = ArrivalSpec::Kind::TraceFile;
+      cfg.arrival.path = trace_path;
+      cfg.arrival.scale = c->trace_scale;
+    } else {
+      cfg.arrival.kind = ArrivalSpec::Kind::Poisson;
+      cfg.arrival.rate = c->rate;
+    }
+    cfg.duration = c->duration;
+    cfg.seed = seed;
+    cfg.entry_selection = c->entry_selection == KX_ENTRY_CYCLE ? WorkloadConfig::EntrySelection::Cycle
+                                                               : WorkloadConfig::EntrySelection::Weighted;
+    ReferenceRates rates;
+    rates.prefill_rate = prefill;
+    rates.decode_rate = decode;
+    const WorkloadRealization real = realize(cfg, rates, seed);
+    for (const auto& inst : real.instances) {
+      out->arrival.push_back(inst.arrival);
+      for (const auto& call : inst.calls) {
+        out->agent.push_back(std::stoi(call.agent.substr(1)));
+        out->parent.push_back(call.parents.empty() ? -1 : call.parents[0]);
+        out->prompt.push_back(call.prompt_tokens);
+        out->target.push_back(call.target_tokens);
+        out->pure.push_back(call.pure_exec);
+        out->rem.push_back(call.remaining_exec);
+        out->uid.push_back(call.uid);
+        out->rem_map.push_back(real.remaining_by_uid.at(call.uid));
+      }
+      out->wf_offsets.push_back(static_cast<int64_t>(out->agent.size()));
+    }
+  } catch (const std::exception& e) {
+    out->error = e.what();
+  }
+  if (!trace_path.empty()) std::remove(trace_path.c_str());
+  return out;
+}
+
+// "" on success, else the exception the reference threw.
+extern "C" const char* kxref_realize_error(void* h) { return static_cast<RefRealization*>(h)->error.c_str(); }
+
+extern "C" void kxref_realize_sizes(void* h, int64_t* n_wf, int64_t* n_calls) {
+  auto* r = static_cast<RefRealization*>(h);
+  *n_wf = static_cast<int64_t>(r->arrival.size());
+  *n_calls = static_cast<int64_t>(r->agent.size());
+}
+
+// rem_map = remaining_by_uid[uid] (must equal remaining_exec).
+extern "C" void kxref_realize_copy(void* h, double* arrival, int64_t* wf_offsets, int32_t* agent,
+                                   int32_t* parent, int64_t* prompt, int64_t* target, double* pure,
+                                   double* rem, uint64_t* uid, double* rem_map) {
+  auto* r = static_cast<RefRealization*>(h);
+  auto cp = [](auto* dst, const auto& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  cp(arrival, r->arrival);
+  cp(wf_offsets, r->wf_offsets);
+  cp(agent, r->agent);
+  cp(parent, r->parent);
+  cp(prompt, r->prompt);
+  cp(target, r->target);
+  cp(pure, r->pure);
+  cp(rem, r->rem);
+  cp(uid, r->uid);
+  cp(rem_map, r->rem_map);
+}
+
+extern "C" void kxref_realize_free(void* h) { delete static_cast<RefRealization*>(h); }

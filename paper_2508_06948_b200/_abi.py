@@ -102,6 +102,30 @@ class kx_phase_stat(C.Structure):
                 ("alg_bytes", C.c_double)]
 
 
+class kx_length_spec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("_pad", C.c_int32), ("a", C.c_double), ("b", C.c_double),
+                ("min_tokens", C.c_int64), ("max_tokens", C.c_int64)]
+
+
+class kx_agent_spec(C.Structure):
+    _fields_ = [("prompt_len", kx_length_spec), ("output_len", kx_length_spec),
+                ("n_choice", C.c_int32), ("n_parallel", C.c_int32), ("choice_to", C.c_void_p),
+                ("choice_p", C.c_void_p), ("parallel_to", C.c_void_p), ("feedback_target", C.c_int32),
+                ("feedback_max_iterations", C.c_int32), ("feedback_probability", C.c_double)]
+
+
+class kx_app_spec(C.Structure):
+    _fields_ = [("entry", C.c_int32), ("n_members", C.c_int32), ("members", C.c_void_p),
+                ("weight", C.c_double)]
+
+
+class kx_workload_config(C.Structure):
+    _fields_ = [("n_agents", C.c_int32), ("n_apps", C.c_int32), ("agents", C.POINTER(kx_agent_spec)),
+                ("apps", C.POINTER(kx_app_spec)), ("arrival_kind", C.c_int32),
+                ("entry_selection", C.c_int32), ("rate", C.c_double), ("n_trace", C.c_int64),
+                ("trace", C.c_void_p), ("trace_scale", C.c_double), ("duration", C.c_double)]
+
+
 # name -> (restype, argtypes)
 _P = C.c_void_p
 SIGNATURES = {
@@ -169,6 +193,8 @@ SIGNATURES = {
     "kx_expected_exec_times": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_void_p]),
     "kx_realize_builtin": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_double,
                                      C.c_double, C.POINTER(_P)]),
+    "kx_realize": (C.c_int, [C.POINTER(kx_workload_config), C.c_uint64, C.c_double, C.c_double,
+                             C.POINTER(_P)]),
     "kx_realization_sizes": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "kx_realization_copy": (C.c_int, [_P] + [_P] * 10),
     "kx_realization_free": (None, [_P]),

@@ -195,6 +195,16 @@ int guard(F&& f) {
 
 [[noreturn]] void fail(int code, const std::string& m) { throw KxError(code, m); }
 
+}  // namespace
+
+// kx_last_error's message for entry points defined in other translation
+// units (kx_workload.cpp).
+namespace kx {
+void set_last_error(const char* m) { g_last_error = m ? m : ""; }
+}  // namespace kx
+
+namespace {
+
 void require(bool ok, const std::string& m) {
   if (!ok) throw std::invalid_argument(m);
 }
@@ -300,6 +310,12 @@ struct kx_sched {
   cudaStream_t side = nullptr;
   cudaGraph_t graph = nullptr;          // captured step (kx_graph_*)
   cudaGraphExec_t graph_exec = nullptr;
+  // what the captured calls were recorded against (launch-time checks) and
+  // the handle state they leave behind (restored after each replay)
+  int64_t graph_n = 0;
+  const char* graph_queue_base = nullptr;
+  bool graph_order_valid = false, graph_dispatch_valid = false;
+  OrderResultDev graph_order{};
   cudaEvent_t ev_keys = nullptr, ev_released = nullptr, ev_disp = nullptr;
   Blob topk_blob;
   TopKWork topk{};
@@ -2010,6 +2026,11 @@ int kx_graph_capture_end(kx_sched* s) {
     KX_CUDA(cudaSetDevice(s->device));
     KX_CUDA(cudaStreamEndCapture(s->stream, &s->graph));
     KX_CUDA(cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+    s->graph_n = s->n;
+    s->graph_queue_base = s->queue_blob.base;
+    s->graph_order_valid = s->order_valid;
+    s->graph_dispatch_valid = s->dispatch_valid;
+    s->graph_order = s->order;
   });
 }
 
@@ -2033,8 +2054,16 @@ int kx_graph_launch(kx_sched* s) {
   return guard([&] {
     require(s, "null handle");
     if (!s->graph_exec) throw std::logic_error("no captured graph");
+    // The captured kernels carry the queue size and buffer addresses of the
+    // capture: a pop or an enqueue that changed the size needs a new capture.
+    if (s->n != s->graph_n || s->queue_blob.base != s->graph_queue_base)
+      throw std::logic_error("queue size changed since the graph was captured: capture again");
     KX_CUDA(cudaSetDevice(s->device));
     KX_CUDA(cudaGraphLaunch(s->graph_exec, s->stream));
+    s->order = s->graph_order;
+    s->order_valid = s->graph_order_valid;
+    s->order_n = s->n;
+    s->dispatch_valid = s->graph_dispatch_valid;
   });
 }
 

@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -32,6 +33,18 @@ struct KxError : std::runtime_error {
   } while (0)
 
 extern std::atomic<long long> g_kx_launches;  // diagnostics: kernels launched
+
+// Runs `f` once per CUDA device of the calling thread's current context,
+// race-free across threads (kernel attributes and occupancy are per device;
+// handles on several devices and threads share no other state).
+constexpr int kMaxDevices = 64;
+template <typename F>
+void once_per_device(std::once_flag (&flags)[kMaxDevices], F&& f) {
+  int dev = 0;
+  KX_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw KxError(4, "device ordinal out of range");
+  std::call_once(flags[dev], f);
+}
 
 #define KX_CHECK_LAUNCH()                                  \
   do {                                                     \

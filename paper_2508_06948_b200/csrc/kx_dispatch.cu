@@ -528,13 +528,12 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 
 #undef SM
 
-// ---- K5 fast path: pools of <= 32 instances, one warp per decision chain ----
+// ---- K5 fast path (pools of <= 32 instances): shared definitions ----------
 // The decisions of a pool form one sequential chain (each commit changes the
-// ledger the next head is placed against), so the chain runs on ONE warp with
-// lanes = instances and no block barrier per decision; the CTA's other warps
-// only stage the rings into shared memory and write them back. Lanes are
-// assigned in increasing InstanceId order, so select_instance's tie rule
-// (smaller id) is the lowest lane among equal peaks.
+// ledger the next head is placed against). The batched kernel below runs
+// that chain on one resolver warp with lanes = instances, assigned in
+// increasing InstanceId order, so select_instance's tie rule (smaller id,
+// SURVEY H9) is the lowest lane among equal peaks.
 //
 // try_place's slot walk (dispatcher.cpp:52-68) is split in three. With
 // c = floor((now + eps) / L) every head's span is [c, last]. When
@@ -554,40 +553,9 @@ k_dispatch_timeslot(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restr
 // spans longer than the table) take the generic slot walk. Ledger rings are
 // staged transposed (usage[slot][lane]). Invariant: a slot that is not
 // stored holds usage +0.0 (gc and the initial state write 0.0).
-constexpr int kWarpThreads = 128;
 constexpr int kWHB = 32;       // head batch (lane = head while loading)
 constexpr int kDtSlots = 64;   // span slots tabulated per head
 
-struct WarpLayout {
-  uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
-      usage, ex, sufm, total;
-};
-
-WarpLayout warp_layout(int ring) {
-  WarpLayout L{};
-  uint32_t o = 0;
-  auto take = [&](size_t bytes) {
-    const uint32_t at = o;
-    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
-    return at;
-  };
-  L.h_idx = take(4 * kWHB);
-  L.h_agent = take(4 * kWHB);
-  L.h_prompt = take(8 * kWHB);
-  L.h_kept = take(8 * kWHB);
-  L.h_uid = take(8 * kWHB);
-  L.h_T = take(8 * kWHB);
-  L.h_first = take(8 * kWHB);
-  L.h_last = take(8 * kWHB);
-  L.h_mode = take(4 * kWHB);
-  L.tab = take(8 * kWHB * kDtSlots);
-  L.lane_inst = take(4 * 32);
-  L.usage = take(size_t(8) * 32 * ring);
-  L.ex = take(size_t(32) * ring);
-  L.sufm = take(size_t(8) * 32 * ring);
-  L.total = o;
-  return L;
-}
 
 // (eval_t - t0) of peak_in_slot (dispatcher.cpp:33-42) for one slot, NaN
 // when the slot takes the zero branch.
@@ -619,1194 +587,12 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
 // Head modes (per head, warp-uniform).
 enum : int32_t { kModeTabPk = 0, kModeTabDt = 1, kModeGeneric = 2 };
 
-__global__ void __launch_bounds__(kWarpThreads)
-k_dispatch_warp(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
-                const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
-                DispatchParams dp, WarpLayout lay, kx_decision* __restrict__ rows,
-                double* __restrict__ cand, int64_t* __restrict__ row_count,
-                int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
-                DispPhase ph) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int pool = blockIdx.x;
-  // Head source: the pool's full order (phase 0), its top-K prefix (phase 1,
-  // overlapping the full sort), or the full order from where phase 1
-  // stopped (phase 2).
-  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
-  const uint32_t* hp = perm + pool_offsets[pool];
-  int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
-  bool skip = false;
-  if (ph.phase == 1) {
-    const TopKState t = ph.tk[pool];
-    if (t.defer) {  // too many ties at the boundary key: wait for the full order
-      if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
-      skip = true;
-    }
-    hp = ph.heads + int64_t(pool) * kTopKMax;
-    q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
-  } else if (ph.phase == 2) {
-    const DispResume r = ph.resume[pool];
-    skip = !r.need;
-    pos0 = r.start;
-    nrows0 = r.nrows;
-    nadm0 = r.nadm;
-  }
-  if (skip) return;  // uniform over the CTA
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int ib = pool_begin[pool];
-  const int ni = pool_begin[pool + 1] - ib;
-  const int ring = dp.ring;
-  const int rmask = ring - 1;
-  double* const su = reinterpret_cast<double*>(smem_raw + lay.usage);
-  uint8_t* const se = reinterpret_cast<uint8_t*>(smem_raw + lay.ex);
-  uint64_t* const sm = reinterpret_cast<uint64_t*>(smem_raw + lay.sufm);
-  int32_t* const s_li = reinterpret_cast<int32_t*>(smem_raw + lay.lane_inst);
-  const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
 
-  // Lane of each instance: rank of its InstanceId within the pool.
-  if (warp == 0) {
-    const int32_t myid = lane < ni ? in.id[ib + lane] : 0x7fffffff;
-    int rank = 0;
-    for (int l = 0; l < 32; ++l) {
-      const int32_t o = __shfl_sync(0xffffffffu, myid, l);
-      rank += (l < ni) && (o < myid || (o == myid && l < lane));
-    }
-    s_li[lane] = -1;
-    __syncwarp();
-    if (lane < ni) s_li[rank] = lane;
-  }
-  __syncthreads();
-  // Stage the rings transposed: usage[pos][lane] (all warps).
-  for (int j = threadIdx.x; j < 32 * ring; j += kWarpThreads) {
-    const int l = j & 31, pos = j >> 5;
-    const int li = s_li[l];
-    su[j] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
-    se[j] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    uint32_t* const h_idx = reinterpret_cast<uint32_t*>(smem_raw + lay.h_idx);
-    int32_t* const h_agent = reinterpret_cast<int32_t*>(smem_raw + lay.h_agent);
-    int64_t* const h_prompt = reinterpret_cast<int64_t*>(smem_raw + lay.h_prompt);
-    int64_t* const h_kept = reinterpret_cast<int64_t*>(smem_raw + lay.h_kept);
-    uint64_t* const h_uid = reinterpret_cast<uint64_t*>(smem_raw + lay.h_uid);
-    double* const h_T = reinterpret_cast<double*>(smem_raw + lay.h_T);
-    int64_t* const h_first = reinterpret_cast<int64_t*>(smem_raw + lay.h_first);
-    int64_t* const h_last = reinterpret_cast<int64_t*>(smem_raw + lay.h_last);
-    int32_t* const h_mode = reinterpret_cast<int32_t*>(smem_raw + lay.h_mode);
-    double* const stab = reinterpret_cast<double*>(smem_raw + lay.tab);
-    const double now = dp.now;
-    const double L = dp.slot_len;
-    const int li = s_li[lane];
-    const bool act = li >= 0;
-    const int i = ib + (act ? li : 0);
-    const double cap = act ? in.cap[i] : 0.0;
-    const double kr = act ? in.decode_rate[i] : 0.0;
-    const int32_t mb = act ? in.max_batch[i] : 0;
-    const int32_t id = act ? in.id[i] : 0x7fffffff;
-    const int32_t waiting = act ? in.waiting[i] : 0;
-    const double wcap = __dmul_rn(dp.watermark, cap);
-    double live = act ? in.live_kv[i] : 0.0;
-    int32_t running = act ? in.running[i] : 0;
-    bool susp = act ? in.suspended[i] != 0 : false;
-    int64_t base = act ? in.base_slot[i] : 0;
-    int64_t hi = act ? in.hi_slot[i] : -1;
-    int32_t nact = act ? in.n_active[i] : 0;
-    // One decode rate for the whole pool: the (P + k * dt) table is shared.
-    const double k0 = __shfl_sync(0xffffffffu, kr, 0);
-    const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
-    // Common slot origin of the pool (bases are equal after any gc; the
-    // per-lane base still bounds what each instance retains).
-    const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
-    const int32_t lo_off = static_cast<int32_t>(base - B);
-    const double t0e = __dadd_rn(now, kTimeEpsilon);
-    const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
-    const int32_t c_off = static_cast<int32_t>(cslot - B);
-    int32_t hi_off = static_cast<int32_t>(hi - B);  // lane's top stored offset
-    int status = KX_OK;
-
-    // Max of the stored slots below c, and the suffix max of the stored
-    // slots from each offset > c up to hi.
-    uint64_t lomax = kZeroBits;
-    for (int32_t o = lo_off; o < c_off && o <= hi_off; ++o) {
-      const int p2 = static_cast<int>((B + o) & rmask);
-      if (se[p2 * 32 + lane]) {
-        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-        lomax = tb > lomax ? tb : lomax;
-      }
-    }
-    {
-      uint64_t run = kZeroBits;
-      for (int32_t o = hi_off; o > c_off && o >= lo_off; --o) {
-        const int p2 = static_cast<int>((B + o) & rmask);
-        if (se[p2 * 32 + lane]) {
-          const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-          run = tb > run ? tb : run;
-        }
-        sm[p2 * 32 + lane] = run;
-      }
-    }
-
-    // Head prefetch (registers, lane = head of the next batch): queue index
-    // first, the request fields two decisions later, the agent's T after
-    // that, so the dependent global loads overlap the decisions.
-    int64_t nx_start = pos0, nx_n = 0;
-    uint32_t nx_idx = 0;
-    int32_t nx_agent = 0;
-    int64_t nx_prompt = 0, nx_kept = 0;
-    uint64_t nx_uid = 0;
-    double nx_T = 0.0;
-    int stage = 0;
-    auto issue_idx = [&](int64_t start) {
-      nx_start = start;
-      nx_n = q_end - start < kWHB ? q_end - start : kWHB;
-      if (nx_n < 0) nx_n = 0;
-      nx_idx = lane < nx_n ? hp[start + lane] : 0u;
-      stage = 0;
-    };
-    auto issue_fields = [&]() {
-      if (lane < nx_n) {
-        nx_agent = q.agent[nx_idx];
-        nx_prompt = q.prompt[nx_idx];
-        nx_kept = q.kept[nx_idx];
-        nx_uid = q.uid[nx_idx];
-        if (dp.oracle_T) nx_T = q.pure_exec[nx_idx];
-      }
-      stage = 1;
-    };
-    auto issue_T = [&]() {
-      if (!dp.oracle_T && lane < nx_n) nx_T = ag.T[nx_agent];
-      stage = 2;
-    };
-    issue_idx(pos0);
-
-    int64_t pos = pos0, hb_start = pos0, hb_n = 0;
-    int64_t nrows = nrows0, nadm = nadm0;
-    int retries = 0;
-    bool broke = false;
-
-    while (pos < q_end) {
-      if (pos >= hb_start + hb_n) {  // next head batch (a prefix of the pool's order)
-        if (stage < 1) issue_fields();
-        if (stage < 2) issue_T();
-        hb_start = nx_start;
-        hb_n = nx_n;
-        if (lane < hb_n) {
-          h_idx[lane] = nx_idx;
-          h_agent[lane] = nx_agent;
-          h_prompt[lane] = nx_prompt;
-          h_kept[lane] = nx_kept;
-          h_uid[lane] = nx_uid;
-          h_T[lane] = nx_T;
-          int64_t f, l;
-          span_bounds_dev(now, nx_T, L, &f, &l);
-          h_first[lane] = f;
-          h_last[lane] = l;
-          // Fast shape: T > 0, P >= 0, span [c, last] within the table, and
-          // peak_in_slot zero on the two slots each side of the span.
-          bool fast = nx_T > 0.0 && nx_prompt >= 0 && f == cslot && l >= f && l - f + 1 <= kDtSlots;
-          if (fast) {
-            const double te = __dadd_rn(now, nx_T);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            const double m0 = slot_dt(now, t0e, te, tee, f - 2, L);
-            const double m1 = slot_dt(now, t0e, te, tee, f - 1, L);
-            const double m2 = slot_dt(now, t0e, te, tee, l + 1, L);
-            const double m3 = slot_dt(now, t0e, te, tee, l + 2, L);
-            fast = m0 != m0 && m1 != m1 && m2 != m2 && m3 != m3;
-          }
-          h_mode[lane] = fast ? (k_uniform ? kModeTabPk : kModeTabDt) : kModeGeneric;
-        }
-        __syncwarp();
-        // (P + k * dt) (or dt) table of every fast head's span, lanes over slots.
-        for (int hh = 0; hh < hb_n; ++hh) {
-          const int mode = h_mode[hh];
-          if (mode == kModeGeneric) continue;
-          const double Th = h_T[hh];
-          const double Ph = static_cast<double>(h_prompt[hh]);
-          const double te = __dadd_rn(now, Th);
-          const double tee = __dsub_rn(te, kTimeEpsilon);
-          const int tn = static_cast<int>(h_last[hh] - h_first[hh] + 1);
-          for (int j = lane; j < tn; j += 32) {
-            const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
-            stab[hh * kDtSlots + j] = mode == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
-          }
-        }
-        __syncwarp();
-        issue_idx(hb_start + hb_n);
-      }
-      const int h = static_cast<int>(pos - hb_start);
-      if (stage == 0 && h >= 2) issue_fields();
-      else if (stage == 1 && h >= 4) issue_T();
-
-      const int64_t prompt = h_prompt[h];
-      const double P = static_cast<double>(prompt);
-      const int64_t first = h_first[h];
-      const int64_t last = h_last[h];
-      const int mode = h_mode[h];
-      const bool nonempty = last >= first;
-
-      // collect_live (engine.cpp:187-202): watermark resume, batch_full.
-      if (susp && live < wcap) susp = false;
-      const bool full = running + waiting >= mb;
-      const bool eligible = act && !susp && !full;
-      const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
-      if (__any_sync(0xffffffffu, overflow)) {
-        status = KX_ERR_CAPACITY;
-        broke = true;
-        break;
-      }
-
-      // try_place (dispatcher.cpp:52-68) for this lane's instance.
-      uint32_t viol = 0xffffffffu;  // first violating slot offset from B
-      uint64_t peak = kZeroBits;    // ordered bits
-      const int32_t fo = static_cast<int32_t>(first - B);
-      const int32_t lo = static_cast<int32_t>(last - B);
-      if (mode != kModeGeneric) {
-        if (eligible) {
-          const int32_t qo = lo + 1;
-          const uint64_t above = (qo <= hi_off) ? sm[static_cast<int>((B + qo) & rmask) * 32 + lane] : kZeroBits;
-          peak = lomax > above ? lomax : above;
-          const double* tab = stab + h * kDtSlots;
-          const int tn = lo - fo + 1;
-          int p2 = static_cast<int>((B + fo) & rmask);
-          if (mode == kModeTabPk) {
-#pragma unroll 4
-            for (int j = 0; j < tn; ++j) {
-              const double total = __dadd_rn(su[p2 * 32 + lane], tab[j]);
-              if (total > cap && viol == 0xffffffffu) viol = static_cast<uint32_t>(fo + j);
-              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-              peak = tb > peak ? tb : peak;
-              p2 = (p2 + 1) & rmask;
-            }
-          } else {
-#pragma unroll 4
-            for (int j = 0; j < tn; ++j) {
-              const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[j]));
-              if (total > cap && viol == 0xffffffffu) viol = static_cast<uint32_t>(fo + j);
-              const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-              peak = tb > peak ? tb : peak;
-              p2 = (p2 + 1) & rmask;
-            }
-          }
-        }
-      } else if (eligible) {  // generic slot walk over the whole window
-        const double te = __dadd_rn(now, h_T[h]);
-        const double tee = __dsub_rn(te, kTimeEpsilon);
-        const int32_t top = hi_off > lo ? hi_off : lo;
-        for (int32_t o = lo_off; o <= top; ++o) {
-          const int p2 = static_cast<int>((B + o) & rmask);
-          const bool e = se[p2 * 32 + lane] != 0;
-          const bool in_span = o >= fo && o <= lo;
-          if (!(e || in_span)) continue;
-          const double used = e ? su[p2 * 32 + lane] : 0.0;
-          const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
-          if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
-          const uint64_t tb = ordered_bits(total);
-          peak = tb > peak ? tb : peak;
-        }
-      }
-      const bool fits = eligible && viol == 0xffffffffu;
-      // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
-      const uint64_t key = fits ? peak : ~0ull;
-      const uint64_t wkey = warp_min_u64(key);
-      const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
-      const int bl = winners ? __ffs(winners) - 1 : -1;
-      const int bsrc = bl >= 0 ? bl : 0;
-      const double bpeak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
-      const double blive = __shfl_sync(0xffffffffu, live, bsrc);
-      const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
-      const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
-      const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
-
-      if (nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
-        const int64_t r = int64_t(pool) * dp.log_cap + nrows;
-        if (lane == 0) {
-          kx_decision d;
-          d.time = now;
-          d.predicted_peak = bpeak;
-          d.uid = h_uid[h];
-          d.queue_index = h_idx[h];
-          d.agent = h_agent[h];
-          d.target = bl >= 0 ? bid : -1;
-          d.pool = pool;
-          d.admitted = (bl >= 0 && !overload) ? 1 : 0;
-          rows[r] = d;
-        }
-        if (act) {
-          double v = -1.0;
-          if (eligible) {
-            v = fits ? from_ordered_bits(peak)
-                     : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
-          }
-          cand[r * dp.peak_stride + li] = v;
-        }
-      }
-      ++nrows;
-      if (bl < 0) {  // head keeps its place (engine.cpp:247)
-        broke = true;
-        break;
-      }
-      if (overload) {
-        if (lane == bl) susp = true;  // Dispatcher::on_overload
-        if (++retries > ni) {
-          status = KX_ERR_LIVELOCK;
-          broke = true;
-          break;
-        }
-        continue;
-      }
-      retries = 0;
-      // Dispatcher::commit: book the target's span slots (lanes = slots),
-      // then refresh the target's suffix max from the span's end down.
-      {
-        const double kt = __shfl_sync(0xffffffffu, kr, bl);
-        const int32_t bhi = __shfl_sync(0xffffffffu, hi_off, bl);
-        const double T = h_T[h];
-        if (mode != kModeGeneric) {
-          const double* tab = stab + h * kDtSlots;
-          for (int64_t s = first + lane; s <= last; s += 32) {
-            const int p2 = static_cast<int>(s & rmask);
-            const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
-            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk);
-            se[p2 * 32 + bl] = 1;
-          }
-        } else {
-          const double te = __dadd_rn(now, T);
-          const double tee = __dsub_rn(te, kTimeEpsilon);
-          for (int64_t s = first + lane; s <= last; s += 32) {
-            const int p2 = static_cast<int>(s & rmask);
-            su[p2 * 32 + bl] = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
-            se[p2 * 32 + bl] = 1;
-          }
-        }
-        __syncwarp();
-        if (lane == bl && nonempty && lo > c_off) {
-          // the target's suffix max over offsets (c, lo], walking down from lo
-          uint64_t run = (lo + 1 <= bhi) ? sm[static_cast<int>((B + lo + 1) & rmask) * 32 + bl] : kZeroBits;
-          for (int32_t o = lo; o > c_off && o >= lo_off; --o) {
-            const int p2 = static_cast<int>((B + o) & rmask);
-            if (se[p2 * 32 + bl]) {
-              const uint64_t tb = ordered_bits(su[p2 * 32 + bl]);
-              run = tb > run ? tb : run;
-            }
-            sm[p2 * 32 + bl] = run;
-          }
-        }
-        if (lane == bl) {
-          if (nonempty && last > hi) {
-            hi = last;
-            hi_off = lo;
-          }
-          live = __dadd_rn(live, static_cast<double>(prompt + h_kept[h]));  // admit
-          running += 1;
-          if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78)
-            q.admitted[h_idx[h]] = 1;
-            const int64_t o = int64_t(i) * kActiveCap + nact;
-            in.act_uid[o] = h_uid[h];
-            in.act_P[o] = P;
-            in.act_k[o] = kt;
-            in.act_t0[o] = now;
-            in.act_T[o] = T;
-            ++nact;
-          } else {
-            status = KX_ERR_CAPACITY;
-          }
-        }
-        if (__any_sync(0xffffffffu, status != KX_OK)) {
-          status = KX_ERR_CAPACITY;
-          broke = true;
-          break;
-        }
-      }
-      ++nadm;
-      ++pos;
-    }
-    // Phase 1 ran out of prefix heads without finishing the round: hand the
-    // state to the continuation (no gc yet: the round is not over).
-    const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
-    if (!defer_rest) {
-      // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
-      if (act && cslot > base) {
-        const int64_t stop = cslot < base + ring ? cslot : base + ring;
-        for (int64_t s = base; s < stop; ++s) {
-          const int p2 = static_cast<int>(s & rmask);
-          su[p2 * 32 + lane] = 0.0;
-          se[p2 * 32 + lane] = 0;
-        }
-        base = cslot;
-      }
-    }
-    if (act) {
-      in.n_active[i] = nact;
-      if (!defer_rest) active_gc(in, i, now);
-      in.live_kv[i] = live;
-      in.base_slot[i] = base;
-      in.hi_slot[i] = hi;
-      in.running[i] = running;
-      in.suspended[i] = susp ? 1 : 0;
-    }
-    if (lane == 0) {
-      if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
-      if (!defer_rest) {
-        row_count[pool] = nrows;
-        admitted_count[pool] = nadm;
-        pool_status[pool] = status;
-      }
-    }
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < 32 * ring; j += kWarpThreads) {
-    const int l = j & 31, p2 = j >> 5;
-    const int li = s_li[l];
-    if (li >= 0) {
-      in.usage[int64_t(ib + li) * ring + p2] = su[j];
-      in.exists[int64_t(ib + li) * ring + p2] = se[j];
-    }
-  }
-}
-
-// ---- K5 pipelined: decider warp <-> evaluator warp ping-pong --------------
-// Same decisions as k_dispatch_warp, with the chain split over two warps
-// that hand off through two 64-thread named barriers (producer bar.arrive,
-// consumer bar.sync):
-//   * warp 1 (evaluator) keeps try_place rows (lanes = instances) for the
-//     current head and the next one, evaluated ahead of time; when the
-//     decider reports a commit or a suspension it re-evaluates only the
-//     instances changed since a row was computed (lanes = slots), publishes
-//     the current row, and evaluates the following head while the decider
-//     works. It also loads the head batches.
-//   * warp 0 (decider) runs select_instance, the overload check and the
-//     commit, reports the outcome, and writes the decision log and the
-//     admission bookkeeping while the evaluator fixes the next row.
-// The predicted peak needs no slot walk outside the span: for a head whose
-// peak_in_slot is zero off its span (the fast shape above), every stored
-// slot contributes `used` and every span slot used + pk >= used, so
-//   peak = max(max over all stored slots of used, max over the span of used + pk)
-// and the first term is one per-instance maximum, raised by each commit.
-// The evaluator's reads of a column the decider is committing to at the same
-// time are discarded by construction: that lane is marked changed by the
-// decider's next report and re-evaluated before the row is used.
-constexpr int kPipeThreads = 128;
 constexpr int kHR = 64;  // head ring: two batches of kWHB
 
-struct PipeLayout {
-  uint32_t h_idx, h_agent, h_prompt, h_kept, h_uid, h_T, h_first, h_last, h_mode, tab, lane_inst,
-      st_live, st_run, st_susp, st_hi, st_umax, r_viol, r_peak, r_flag, usage, ex, total;
-};
-
-PipeLayout pipe_layout(int ring) {
-  PipeLayout L{};
-  uint32_t o = 0;
-  auto take = [&](size_t bytes) {
-    const uint32_t at = o;
-    o = static_cast<uint32_t>((o + bytes + 15) & ~size_t(15));
-    return at;
-  };
-  L.h_idx = take(4 * kHR);
-  L.h_agent = take(4 * kHR);
-  L.h_prompt = take(8 * kHR);
-  L.h_kept = take(8 * kHR);
-  L.h_uid = take(8 * kHR);
-  L.h_T = take(8 * kHR);
-  L.h_first = take(8 * kHR);
-  L.h_last = take(8 * kHR);
-  L.h_mode = take(4 * kHR);
-  L.tab = take(size_t(8) * kHR * kDtSlots);
-  L.lane_inst = take(4 * 32);
-  L.st_live = take(8 * 32);
-  L.st_run = take(4 * 32);
-  L.st_susp = take(4 * 32);
-  L.st_hi = take(4 * 32);
-  L.st_umax = take(8 * 32);
-  L.r_viol = take(4 * 32);
-  L.r_peak = take(8 * 32);
-  L.r_flag = take(4 * 32);
-  L.usage = take(size_t(8) * 32 * ring);
-  L.ex = take(size_t(32) * ring);
-  L.total = o;
-  return L;
-}
-
-
-struct PipeMsg {
-  int32_t type;     // 0 commit, 1 suspension (overload retry), 2 stop
-  int32_t lane;     // instance lane changed by the decision
-};
-
-__device__ __forceinline__ void pp_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void pp_arrive(int id) {
-  __threadfence_block();  // the consumer reads what this warp wrote to shared memory
-  asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
-}
-constexpr int kBarDecided = 1;   // decider -> evaluator
-constexpr int kBarRowReady = 2;  // evaluator -> decider
-
-__global__ void __launch_bounds__(kPipeThreads)
-k_dispatch_pipe(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict__ pool_begin,
-                const uint32_t* __restrict__ perm, const int64_t* __restrict__ pool_offsets,
-                DispatchParams dp, PipeLayout lay, kx_decision* __restrict__ rows,
-                double* __restrict__ cand, int64_t* __restrict__ row_count,
-                int64_t* __restrict__ admitted_count, int* __restrict__ pool_status,
-                DispPhase ph) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ PipeMsg msg;
-  __shared__ int64_t s_win[3];  // staged slot window [B, top]; top after the round
-  const int pool = blockIdx.x;
-  const int64_t pool_n = pool_offsets[pool + 1] - pool_offsets[pool];
-  const uint32_t* hp = perm + pool_offsets[pool];
-  int64_t q_end = pool_n, pos0 = 0, nrows0 = 0, nadm0 = 0;
-  bool skip = false;
-  if (ph.phase == 1) {
-    const TopKState t = ph.tk[pool];
-    if (t.defer) {  // too many ties at the boundary key: wait for the full order
-      if (threadIdx.x == 0) ph.resume[pool] = DispResume{0, 0, 0, 1, 0};
-      skip = true;
-    }
-    hp = ph.heads + int64_t(pool) * kTopKMax;
-    q_end = t.empty ? 0 : (t.n_cand < kTopKMax ? t.n_cand : kTopKMax);
-  } else if (ph.phase == 2) {
-    const DispResume r = ph.resume[pool];
-    skip = !r.need;
-    pos0 = r.start;
-    nrows0 = r.nrows;
-    nadm0 = r.nadm;
-  }
-  if (skip) return;  // uniform over the CTA
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int ib = pool_begin[pool];
-  const int ni = pool_begin[pool + 1] - ib;
-  const int ring = dp.ring;
-  const int rmask = ring - 1;
-#define PL(type, field) reinterpret_cast<type*>(smem_raw + lay.field)
-  double* const su = PL(double, usage);
-  uint8_t* const se = PL(uint8_t, ex);
-  int32_t* const s_li = PL(int32_t, lane_inst);
-  uint32_t* const h_idx = PL(uint32_t, h_idx);
-  int32_t* const h_agent = PL(int32_t, h_agent);
-  int64_t* const h_prompt = PL(int64_t, h_prompt);
-  int64_t* const h_kept = PL(int64_t, h_kept);
-  uint64_t* const h_uid = PL(uint64_t, h_uid);
-  double* const h_T = PL(double, h_T);
-  int64_t* const h_first = PL(int64_t, h_first);
-  int64_t* const h_last = PL(int64_t, h_last);
-  int32_t* const h_mode = PL(int32_t, h_mode);
-  double* const stab = PL(double, tab);
-  double* const st_live = PL(double, st_live);
-  int32_t* const st_run = PL(int32_t, st_run);
-  int32_t* const st_susp = PL(int32_t, st_susp);
-  int32_t* const st_hi = PL(int32_t, st_hi);
-  uint64_t* const st_umax = PL(uint64_t, st_umax);
-  uint32_t* const r_viol = PL(uint32_t, r_viol);
-  uint64_t* const r_peak = PL(uint64_t, r_peak);
-  uint32_t* const r_flag = PL(uint32_t, r_flag);
-#undef PL
-  const uint64_t kZeroBits = 0x8000000000000000ull;  // ordered_bits(0.0)
-  constexpr uint32_t kNone = 0xffffffffu;
-
-  // Lane of each instance: rank of its InstanceId within the pool (H9).
-  if (warp == 0) {
-    const int32_t myid = lane < ni ? in.id[ib + lane] : 0x7fffffff;
-    int rank = 0;
-    for (int l = 0; l < 32; ++l) {
-      const int32_t o = __shfl_sync(0xffffffffu, myid, l);
-      rank += (l < ni) && (o < myid || (o == myid && l < lane));
-    }
-    s_li[lane] = -1;
-    __syncwarp();
-    if (lane < ni) s_li[rank] = lane;
-    // the pool's slot window [B, top]: the only ring positions that can hold
-    // stored slots (everything else is +0.0 / not stored)
-    const bool a0 = lane < ni;
-    const int64_t bb = a0 ? in.base_slot[ib + lane] : INT64_MAX;
-    const int64_t hh = a0 ? in.hi_slot[ib + lane] : INT64_MIN;
-    const uint64_t bmin = warp_min_u64(static_cast<uint64_t>(bb) ^ 0x8000000000000000ull);
-    const uint64_t hmax = warp_max_u64(static_cast<uint64_t>(hh) ^ 0x8000000000000000ull);
-    if (lane == 0) {
-      s_win[0] = static_cast<int64_t>(bmin ^ 0x8000000000000000ull);
-      s_win[1] = static_cast<int64_t>(hmax ^ 0x8000000000000000ull);
-    }
-  }
-  __syncthreads();
-  // Stage the rings transposed (usage[pos][lane]): zero everywhere, then copy
-  // the window's positions with four independent loads in flight per thread.
-  const int64_t wB = s_win[0];
-  const int64_t wtop = s_win[1];
-  const int win = wtop < wB ? 0 : static_cast<int>(wtop - wB + 1 < ring ? wtop - wB + 1 : ring);
-  for (int j = threadIdx.x; j < 32 * ring; j += kPipeThreads) {
-    su[j] = 0.0;
-    se[j] = 0;
-  }
-  __syncthreads();
-  {
-    const int total = win * 32;
-    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kPipeThreads) {
-      double u[4];
-      uint8_t x[4];
-      int dst[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int e = e0 + k * kPipeThreads;
-        const int l = e & 31;
-        const int li = e < total ? s_li[l] : -1;
-        const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
-        dst[k] = li >= 0 ? pos * 32 + l : -1;
-        u[k] = li >= 0 ? in.usage[int64_t(ib + li) * ring + pos] : 0.0;
-        x[k] = li >= 0 ? in.exists[int64_t(ib + li) * ring + pos] : 0;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (dst[k] >= 0) {
-          su[dst[k]] = u[k];
-          se[dst[k]] = x[k];
-        }
-    }
-  }
-  __syncthreads();
-
-  if (warp < 2) {
-    // ---- per-lane instance constants (both warps) ----
-    const double now = dp.now;
-    const double L = dp.slot_len;
-    const int li = s_li[lane];
-    const bool act = li >= 0;
-    const int i = ib + (act ? li : 0);
-    const double cap = act ? in.cap[i] : 0.0;
-    const double kr = act ? in.decode_rate[i] : 0.0;
-    const int32_t mb = act ? in.max_batch[i] : 0;
-    const int32_t id = act ? in.id[i] : 0x7fffffff;
-    const int32_t waiting = act ? in.waiting[i] : 0;
-    const double wcap = __dmul_rn(dp.watermark, cap);
-    const int64_t base = act ? in.base_slot[i] : 0;
-    const int64_t hi0 = act ? in.hi_slot[i] : -1;
-    const double k0 = __shfl_sync(0xffffffffu, kr, 0);
-    const bool k_uniform = __all_sync(0xffffffffu, !act || kr == k0);
-    const int64_t B = static_cast<int64_t>(warp_min_u64(act ? static_cast<uint64_t>(base) : ~0ull));
-    const int32_t lo_off = static_cast<int32_t>(base - B);
-    const double t0e = __dadd_rn(now, kTimeEpsilon);
-    const int64_t cslot = static_cast<int64_t>(floor(__ddiv_rn(t0e, L)));
-    // max stored usage of the instance over its whole ledger window
-    uint64_t umax0 = kZeroBits;
-    for (int32_t o = lo_off; o <= static_cast<int32_t>(hi0 - B); ++o) {
-      const int p2 = static_cast<int>((B + o) & rmask);
-      if (se[p2 * 32 + lane]) {
-        const uint64_t tb = ordered_bits(su[p2 * 32 + lane]);
-        umax0 = tb > umax0 ? tb : umax0;
-      }
-    }
-
-    if (warp == 1) {
-      // =========================== evaluator ===========================
-      // head prefetch registers (lane = head of the next batch)
-      int64_t nx_start = pos0, nx_n = 0;
-      uint32_t nx_idx = 0;
-      int32_t nx_agent = 0;
-      int64_t nx_prompt = 0, nx_kept = 0;
-      uint64_t nx_uid = 0;
-      double nx_T = 0.0;
-      int stage = 0;
-      auto issue_idx = [&](int64_t start) {
-        nx_start = start;
-        nx_n = q_end - start < kWHB ? q_end - start : kWHB;
-        if (nx_n < 0) nx_n = 0;
-        nx_idx = lane < nx_n ? hp[start + lane] : 0u;
-        stage = 0;
-      };
-      auto issue_fields = [&]() {
-        if (lane < nx_n) {
-          nx_agent = q.agent[nx_idx];
-          nx_prompt = q.prompt[nx_idx];
-          nx_kept = q.kept[nx_idx];
-          nx_uid = q.uid[nx_idx];
-          if (dp.oracle_T) nx_T = q.pure_exec[nx_idx];
-        }
-        stage = 1;
-      };
-      auto issue_T = [&]() {
-        if (!dp.oracle_T && lane < nx_n) nx_T = ag.T[nx_agent];
-        stage = 2;
-      };
-      int64_t loaded_end = pos0;  // heads [.., loaded_end) are in the ring
-      // Move the prefetched batch into its ring half and build its tables.
-      auto land_batch = [&]() {
-        if (stage < 1) issue_fields();
-        if (stage < 2) issue_T();
-        const int half = static_cast<int>(((nx_start - pos0) / kWHB) & 1);
-        const int hb = half * kWHB;
-        const int n = static_cast<int>(nx_n);
-        if (lane < n) {
-          const int hs = hb + lane;
-          h_idx[hs] = nx_idx;
-          h_agent[hs] = nx_agent;
-          h_prompt[hs] = nx_prompt;
-          h_kept[hs] = nx_kept;
-          h_uid[hs] = nx_uid;
-          h_T[hs] = nx_T;
-          int64_t f, l;
-          span_bounds_dev(now, nx_T, L, &f, &l);
-          h_first[hs] = f;
-          h_last[hs] = l;
-          bool fast = nx_T > 0.0 && nx_prompt >= 0 && f == cslot && l >= f && l - f + 1 <= kDtSlots;
-          if (fast) {
-            const double te = __dadd_rn(now, nx_T);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            const double m0 = slot_dt(now, t0e, te, tee, f - 2, L);
-            const double m1 = slot_dt(now, t0e, te, tee, f - 1, L);
-            const double m2 = slot_dt(now, t0e, te, tee, l + 1, L);
-            const double m3 = slot_dt(now, t0e, te, tee, l + 2, L);
-            fast = m0 != m0 && m1 != m1 && m2 != m2 && m3 != m3;
-          }
-          h_mode[hs] = fast ? (k_uniform ? kModeTabPk : kModeTabDt) : kModeGeneric;
-        }
-        __syncwarp();
-        for (int hh = 0; hh < n; ++hh) {
-          const int hs = hb + hh;
-          const int mode = h_mode[hs];
-          if (mode == kModeGeneric) continue;
-          const double Th = h_T[hs];
-          const double Ph = static_cast<double>(h_prompt[hs]);
-          const double te = __dadd_rn(now, Th);
-          const double tee = __dsub_rn(te, kTimeEpsilon);
-          const int tn = static_cast<int>(h_last[hs] - h_first[hs] + 1);
-          for (int j = lane; j < tn; j += 32) {
-            const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
-            stab[hs * kDtSlots + j] = mode == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
-          }
-        }
-        __syncwarp();
-        loaded_end = nx_start + nx_n;
-        issue_idx(loaded_end);
-      };
-      auto ensure_loaded = [&](int64_t hpos) {
-        if (hpos >= loaded_end) land_batch();
-        else if (stage == 0 && hpos >= nx_start - kWHB + 2) issue_fields();
-        else if (stage == 1 && hpos >= nx_start - kWHB + 4) issue_T();
-      };
-      // One row entry: try_place of head `hpos` for this lane's instance
-      // against the published state (lanes = instances).
-      struct Row {
-        uint32_t viol;
-        uint64_t peak;
-        uint32_t flag;  // bit 0 eligible, bit 1 ring overflow
-      };
-      auto evaluate = [&](int64_t hpos) {
-        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
-        const int mode = h_mode[hs];
-        const int64_t first = h_first[hs];
-        const int64_t last = h_last[hs];
-        const double P = static_cast<double>(h_prompt[hs]);
-        const int32_t fo = static_cast<int32_t>(first - B);
-        const int32_t lo = static_cast<int32_t>(last - B);
-        const bool nonempty = last >= first;
-        const double live = st_live[lane];
-        const bool susp = st_susp[lane] != 0 && !(live < wcap);
-        const bool eligible = act && !susp && !(st_run[lane] + waiting >= mb);
-        Row r{kNone, kZeroBits, 0u};
-        const bool overflow = eligible && nonempty && (first < base || last >= base + ring);
-        if (eligible) {
-          if (mode != kModeGeneric) {
-            uint64_t peak = st_umax[lane];
-            uint32_t viol = kNone;
-            const double* tab = stab + hs * kDtSlots;
-            const int tn = lo - fo + 1;
-            int p2 = static_cast<int>((B + fo) & rmask);
-            if (mode == kModeTabPk) {
-#pragma unroll 4
-              for (int j = 0; j < tn; ++j) {
-                const double total = __dadd_rn(su[p2 * 32 + lane], tab[j]);
-                if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + j);
-                const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-                peak = tb > peak ? tb : peak;
-                p2 = (p2 + 1) & rmask;
-              }
-            } else {
-#pragma unroll 4
-              for (int j = 0; j < tn; ++j) {
-                const double total = __dadd_rn(su[p2 * 32 + lane], pk_of(P, kr, tab[j]));
-                if (total > cap && viol == kNone) viol = static_cast<uint32_t>(fo + j);
-                const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(total)) | kZeroBits;
-                peak = tb > peak ? tb : peak;
-                p2 = (p2 + 1) & rmask;
-              }
-            }
-            r.viol = viol;
-            r.peak = peak;
-          } else {  // generic slot walk over the whole window
-            const double te = __dadd_rn(now, h_T[hs]);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            const int32_t hi_off = st_hi[lane];
-            const int32_t top = hi_off > lo ? hi_off : lo;
-            uint64_t peak = kZeroBits;
-            uint32_t viol = kNone;
-            for (int32_t o = lo_off; o <= top; ++o) {
-              const int p2 = static_cast<int>((B + o) & rmask);
-              const bool e = se[p2 * 32 + lane] != 0;
-              const bool in_span = o >= fo && o <= lo;
-              if (!(e || in_span)) continue;
-              const double used = e ? su[p2 * 32 + lane] : 0.0;
-              const double total = __dadd_rn(used, pk_of(P, kr, slot_dt(now, t0e, te, tee, B + o, L)));
-              if (in_span && total > cap) viol = static_cast<uint32_t>(o) < viol ? static_cast<uint32_t>(o) : viol;
-              const uint64_t tb = ordered_bits(total);
-              peak = tb > peak ? tb : peak;
-            }
-            r.viol = viol;
-            r.peak = peak;
-          }
-        }
-        r.flag = (eligible ? 1u : 0u) | (overflow ? 2u : 0u);
-        return r;
-      };
-      // Re-evaluate the row entries of the lanes in `dirty` (lanes = slots).
-      auto fix = [&](Row& r, int64_t hpos, uint32_t dirty) {
-        const int hs = static_cast<int>((hpos - pos0) & (kHR - 1));
-        const int mode = h_mode[hs];
-        const int64_t first = h_first[hs];
-        const int64_t last = h_last[hs];
-        const double P = static_cast<double>(h_prompt[hs]);
-        const int32_t fo = static_cast<int32_t>(first - B);
-        const int32_t lo = static_cast<int32_t>(last - B);
-        const bool nonempty = last >= first;
-        const bool fast = mode != kModeGeneric;
-        const double* tab = stab + hs * kDtSlots;
-        while (dirty) {
-          const int t = __ffs(dirty) - 1;
-          dirty &= dirty - 1;
-          const double live_t = st_live[t];
-          const double wcap_t = __shfl_sync(0xffffffffu, wcap, t);
-          const bool susp_t = st_susp[t] != 0 && !(live_t < wcap_t);
-          const bool act_t = __shfl_sync(0xffffffffu, act, t);
-          const int32_t mb_t = __shfl_sync(0xffffffffu, mb, t);
-          const int32_t wait_t = __shfl_sync(0xffffffffu, waiting, t);
-          const bool e_t = act_t && !susp_t && !(st_run[t] + wait_t >= mb_t);
-          uint32_t v_t = kNone;
-          uint64_t p_t = kZeroBits;
-          bool o_t = false;
-          if (e_t) {
-            const int32_t lo_t = __shfl_sync(0xffffffffu, lo_off, t);
-            const int32_t hio_t = st_hi[t];
-            const double cap_t = __shfl_sync(0xffffffffu, cap, t);
-            const double k_t = __shfl_sync(0xffffffffu, kr, t);
-            const int64_t base_t = B + lo_t;
-            o_t = nonempty && (first < base_t || last >= base_t + ring);
-            const int32_t w0 = fast ? fo : lo_t;
-            const int32_t w1 = fast ? lo : (hio_t > lo ? hio_t : lo);
-            const double te = __dadd_rn(now, h_T[hs]);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            uint32_t vv = kNone;
-            uint64_t pp = fast ? st_umax[t] : kZeroBits;
-            for (int32_t o0 = w0; o0 <= w1; o0 += 32) {
-              const int32_t o = o0 + lane;
-              if (o <= w1) {
-                const int p2 = static_cast<int>((B + o) & rmask);
-                const bool e = se[p2 * 32 + t] != 0;
-                const bool in_span = o >= fo && o <= lo;
-                if (e || in_span) {
-                  const double used = e ? su[p2 * 32 + t] : 0.0;
-                  double pk;
-                  if (fast) pk = in_span ? (mode == kModeTabPk ? tab[o - fo] : pk_of(P, k_t, tab[o - fo])) : 0.0;
-                  else pk = pk_of(P, k_t, slot_dt(now, t0e, te, tee, B + o, L));
-                  const double total = __dadd_rn(used, pk);
-                  if (in_span && total > cap_t && static_cast<uint32_t>(o) < vv) vv = static_cast<uint32_t>(o);
-                  const uint64_t tb = ordered_bits(total);
-                  pp = tb > pp ? tb : pp;
-                }
-              }
-            }
-            v_t = __reduce_min_sync(0xffffffffu, vv);
-            p_t = warp_max_u64(pp);
-          }
-          if (lane == t) {
-            r.viol = v_t;
-            r.peak = e_t ? p_t : kZeroBits;
-            r.flag = (e_t ? 1u : 0u) | (o_t ? 2u : 0u);
-          }
-        }
-      };
-      auto publish = [&](const Row& r) {
-        r_viol[lane] = r.viol;
-        r_peak[lane] = r.peak;
-        r_flag[lane] = r.flag;
-      };
-
-      issue_idx(pos0);
-      pp_sync(kBarDecided);  // the decider's state is published
-      int64_t h = pos0;
-      Row rc{kNone, kZeroBits, 0u}, rn{kNone, kZeroBits, 0u};
-      uint32_t dirty_n = 0;
-      if (h < q_end) {
-        ensure_loaded(h);
-        rc = evaluate(h);
-        publish(rc);
-      }
-      pp_arrive(kBarRowReady);
-      if (h + 1 < q_end) {
-        ensure_loaded(h + 1);
-        rn = evaluate(h + 1);
-      }
-      while (true) {
-        pp_sync(kBarDecided);
-        const PipeMsg m = msg;
-        if (m.type == 2) break;
-        const uint32_t bit = 1u << m.lane;
-        uint32_t dirty_c;
-        if (m.type == 0) {  // committed: the next head becomes current
-          ++h;
-          rc = rn;
-          dirty_c = dirty_n | bit;
-          dirty_n = 0;
-        } else {            // suspended: same head again
-          dirty_c = bit;
-          dirty_n |= bit;
-        }
-        if (h < q_end) {
-          fix(rc, h, dirty_c);
-          publish(rc);
-        }
-        pp_arrive(kBarRowReady);
-        if (m.type == 0 && h + 1 < q_end) {
-          ensure_loaded(h + 1);
-          rn = evaluate(h + 1);
-        }
-      }
-    } else {
-      // ============================ decider ============================
-      double live = act ? in.live_kv[i] : 0.0;
-      int32_t running = act ? in.running[i] : 0;
-      bool susp = act ? in.suspended[i] != 0 : false;
-      int64_t hi = hi0;
-      int32_t hi_off = static_cast<int32_t>(hi0 - B);
-      int32_t nact = act ? in.n_active[i] : 0;
-      uint64_t umax = umax0;
-      st_live[lane] = live;
-      st_run[lane] = running;
-      st_susp[lane] = susp ? 1 : 0;
-      st_hi[lane] = hi_off;
-      st_umax[lane] = umax;
-      pp_arrive(kBarDecided);
-      int64_t pos = pos0;
-      int64_t nrows = nrows0, nadm = nadm0;
-      int retries = 0;
-      bool broke = false;
-      int status = KX_OK;
-      auto report = [&](int type, int l) {
-        if (lane == 0) msg = PipeMsg{type, l};
-        pp_arrive(kBarDecided);
-      };
-      while (true) {
-        pp_sync(kBarRowReady);
-        if (pos >= q_end) {
-          report(2, 0);
-          break;
-        }
-        const uint32_t viol = r_viol[lane];
-        const uint64_t peak = r_peak[lane];
-        const uint32_t flg = r_flag[lane];
-        const bool elig = flg & 1u;
-        const int hs = static_cast<int>((pos - pos0) & (kHR - 1));
-        const int64_t prompt = h_prompt[hs];
-        const double P = static_cast<double>(prompt);
-        const int64_t first = h_first[hs];
-        const int64_t last = h_last[hs];
-        const int mode = h_mode[hs];
-        const double T = h_T[hs];
-        const bool nonempty = last >= first;
-        const int32_t lo = static_cast<int32_t>(last - B);
-        // collect_live (engine.cpp:187-202): the watermark resume (the
-        // evaluator applies the same rule to the published state).
-        if (susp && live < wcap) {
-          susp = false;
-          st_susp[lane] = 0;
-        }
-        if (__any_sync(0xffffffffu, (flg & 2u) != 0)) {
-          status = KX_ERR_CAPACITY;
-          broke = true;
-          report(2, 0);
-          break;
-        }
-        const bool fits = elig && viol == kNone;
-        // select_instance: min (peak, InstanceId) (H9); lanes are in id order.
-        const uint64_t key = fits ? peak : ~0ull;
-        const uint64_t wkey = warp_min_u64(key);
-        const uint32_t winners = __ballot_sync(0xffffffffu, fits && key == wkey);
-        const int bl = winners ? __ffs(winners) - 1 : -1;
-        const int bsrc = bl >= 0 ? bl : 0;
-        const double blive = __shfl_sync(0xffffffffu, live, bsrc);
-        const double bcap = __shfl_sync(0xffffffffu, cap, bsrc);
-        const bool overload = bl >= 0 && __dadd_rn(blive, P) > bcap;  // engine.cpp:254-258
-        if (bl < 0) {  // head keeps its place (engine.cpp:247)
-          broke = true;
-          report(2, 0);
-        } else if (overload) {
-          if (lane == bl) {  // Dispatcher::on_overload
-            susp = true;
-            st_susp[lane] = 1;
-          }
-          if (retries + 1 > ni) {
-            status = KX_ERR_LIVELOCK;
-            broke = true;
-            report(2, 0);
-          } else {
-            report(1, bl);
-          }
-        } else {
-          // Dispatcher::commit: book the target's span slots (lanes = slots)
-          // and raise the target's maximum stored usage.
-          const double kt = __shfl_sync(0xffffffffu, kr, bl);
-          uint64_t nb = kZeroBits;
-          if (mode != kModeGeneric) {
-            const double* tab = stab + hs * kDtSlots;
-            for (int64_t s = first + lane; s <= last; s += 32) {
-              const int p2 = static_cast<int>(s & rmask);
-              const double pk = mode == kModeTabPk ? tab[s - first] : pk_of(P, kt, tab[s - first]);
-              const double nu = __dadd_rn(su[p2 * 32 + bl], pk);
-              su[p2 * 32 + bl] = nu;
-              se[p2 * 32 + bl] = 1;
-              const uint64_t tb = ordered_bits(nu);
-              nb = tb > nb ? tb : nb;
-            }
-          } else {
-            const double te = __dadd_rn(now, T);
-            const double tee = __dsub_rn(te, kTimeEpsilon);
-            for (int64_t s = first + lane; s <= last; s += 32) {
-              const int p2 = static_cast<int>(s & rmask);
-              const double nu = __dadd_rn(su[p2 * 32 + bl], pk_of(P, kt, slot_dt(now, t0e, te, tee, s, L)));
-              su[p2 * 32 + bl] = nu;
-              se[p2 * 32 + bl] = 1;
-              const uint64_t tb = ordered_bits(nu);
-              nb = tb > nb ? tb : nb;
-            }
-          }
-          nb = warp_max_u64(nb);
-          if (lane == bl) {
-            if (nonempty && last > hi) {
-              hi = last;
-              hi_off = lo;
-            }
-            live = __dadd_rn(live, static_cast<double>(prompt + h_kept[hs]));  // admit
-            running += 1;
-            umax = nb > umax ? nb : umax;
-            st_live[lane] = live;
-            st_run[lane] = running;
-            st_hi[lane] = hi_off;
-            st_umax[lane] = umax;
-          }
-          report(0, bl);
-        }
-        // ---- bookkeeping while the evaluator fixes the next row ----
-        if (nrows < dp.log_cap) {  // decision log (engine.cpp:242-246)
-          const int64_t r = int64_t(pool) * dp.log_cap + nrows;
-          const int32_t bid = __shfl_sync(0xffffffffu, id, bsrc);
-          if (lane == 0) {
-            kx_decision d;
-            d.time = now;
-            d.predicted_peak = bl >= 0 ? from_ordered_bits(wkey) : 0.0;
-            d.uid = h_uid[hs];
-            d.queue_index = h_idx[hs];
-            d.agent = h_agent[hs];
-            d.target = bl >= 0 ? bid : -1;
-            d.pool = pool;
-            d.admitted = (bl >= 0 && !overload) ? 1 : 0;
-            rows[r] = d;
-          }
-          if (act) {
-            double v = -1.0;
-            if (elig) {
-              v = fits ? from_ordered_bits(peak)
-                       : __dsub_rn(-static_cast<double>(B + static_cast<int64_t>(viol)), 1.0);
-            }
-            cand[r * dp.peak_stride + li] = v;
-          }
-        }
-        ++nrows;
-        if (broke) break;
-        if (overload) {
-          ++retries;
-          continue;
-        }
-        retries = 0;
-        if (lane == bl) {
-          if (nact < kActiveCap) {  // active_[uid] = m (dispatcher.cpp:78)
-            q.admitted[h_idx[hs]] = 1;
-            const int64_t o = int64_t(i) * kActiveCap + nact;
-            in.act_uid[o] = h_uid[hs];
-            in.act_P[o] = P;
-            in.act_k[o] = kr;
-            in.act_t0[o] = now;
-            in.act_T[o] = T;
-            ++nact;
-          } else {
-            status = KX_ERR_CAPACITY;
-          }
-        }
-        ++nadm;
-        ++pos;
-        if (__any_sync(0xffffffffu, status != KX_OK)) {
-          status = KX_ERR_CAPACITY;
-          broke = true;
-          // the evaluator is waiting for the next report
-          pp_sync(kBarRowReady);
-          report(2, 0);
-          break;
-        }
-      }
-      // Phase 1 ran out of prefix heads without finishing the round: hand the
-      // state to the continuation (no gc yet: the round is not over).
-      const bool defer_rest = ph.phase == 1 && !broke && status == KX_OK && pos >= q_end && q_end < pool_n;
-      int64_t nbase = base;
-      if (!defer_rest) {
-        // Dispatcher::gc (engine.cpp:212): slots below the current one, elapsed models.
-        if (act && cslot > base) {
-          const int64_t stop = cslot < base + ring ? cslot : base + ring;
-          for (int64_t s = base; s < stop; ++s) {
-            const int p2 = static_cast<int>(s & rmask);
-            su[p2 * 32 + lane] = 0.0;
-            se[p2 * 32 + lane] = 0;
-          }
-          nbase = cslot;
-        }
-      }
-      if (act) {
-        in.n_active[i] = nact;
-        if (!defer_rest) active_gc(in, i, now);
-        in.live_kv[i] = live;
-        in.base_slot[i] = nbase;
-        in.hi_slot[i] = hi;
-        in.running[i] = running;
-        in.suspended[i] = susp ? 1 : 0;
-      }
-      {
-        const uint64_t hm = warp_max_u64(static_cast<uint64_t>(act ? hi : INT64_MIN) ^ 0x8000000000000000ull);
-        if (lane == 0) s_win[2] = static_cast<int64_t>(hm ^ 0x8000000000000000ull);
-      }
-      if (lane == 0) {
-        if (ph.resume) ph.resume[pool] = DispResume{pos, nrows, nadm, defer_rest ? 1 : 0, 0};
-        if (!defer_rest) {
-          row_count[pool] = nrows;
-          admitted_count[pool] = nadm;
-          pool_status[pool] = status;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  {
-    // write back the window (booked slots only grow hi; gc only clears inside it)
-    const int64_t top = s_win[2] > wtop ? s_win[2] : wtop;
-    const int wn = top < wB ? 0 : static_cast<int>(top - wB + 1 < ring ? top - wB + 1 : ring);
-    for (int e = threadIdx.x; e < wn * 32; e += kPipeThreads) {
-      const int l = e & 31;
-      const int li = s_li[l];
-      if (li < 0) continue;
-      const int pos = static_cast<int>((wB + (e >> 5)) & rmask);
-      in.usage[int64_t(ib + li) * ring + pos] = su[pos * 32 + l];
-      in.exists[int64_t(ib + li) * ring + pos] = se[pos * 32 + l];
-    }
-  }
-}
 
 // ---- K5 batched: parallel look-ahead rows + one resolver warp ---------------
-// Same decisions as k_dispatch_warp. The heads of a round are taken in
+// The heads of a round are taken in
 // batches of kBatchEval: each evaluator warp computes the try_place row of
 // one head of the batch (lanes = instances) against the state at the start
 // of the batch, all in parallel (phase A). The resolver warp then walks the
@@ -3063,10 +1849,6 @@ void configure_dispatch_kernels() {
   KX_CUDA(cudaFuncGetAttributes(&attr, k_dispatch_batch));
   KX_CUDA(cudaFuncGetAttributes(&attr, k_gc_all));
   KX_CUDA(cudaFuncGetAttributes(&attr, k_dispatch_waiting));
-  KX_CUDA(cudaFuncSetAttribute(k_dispatch_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kDispSmemLimit));
-  KX_CUDA(cudaFuncSetAttribute(k_dispatch_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kDispSmemLimit));
   KX_CUDA(cudaFuncSetAttribute(k_dispatch_timeslot<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3076,9 +1858,7 @@ void configure_dispatch_kernels() {
 }
 
 bool dispatch_can_overlap(int max_inst_per_pool, int ring) {
-  return max_inst_per_pool <= 32 && batch_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
-         pipe_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit) &&
-         warp_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
+  return max_inst_per_pool <= 32 && batch_layout(ring).total <= static_cast<uint32_t>(kDispSmemLimit);
 }
 
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
@@ -3087,32 +1867,12 @@ void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,
                      double* cand, int64_t* row_count, int64_t* admitted_count, int* pool_status,
                      cudaStream_t st, DispPhase phase) {
   if (max_inst_per_pool <= 32) {
-    const char* variant = getenv("KX_DISPATCH");  // test knob: batch (default) | pipe | warp
     const BatchLayout bl = batch_layout(dp.ring);
-    if ((!variant || !strcmp(variant, "batch") || phase.phase == 3) &&
-        bl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
+    if (bl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
       k_dispatch_batch<<<n_pools, kBatchThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
                                                                          pool_offsets, dp, bl, rows, cand,
                                                                          row_count, admitted_count,
                                                                          pool_status, phase);
-      KX_CHECK_LAUNCH();
-      return;
-    }
-    const PipeLayout pl = pipe_layout(dp.ring);
-    if ((!variant || !strcmp(variant, "pipe")) && pl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
-      k_dispatch_pipe<<<n_pools, kPipeThreads, kDispSmemExclusive, st>>>(q, a, in, pool_begin, perm,
-                                                              pool_offsets, dp, pl, rows, cand,
-                                                              row_count, admitted_count,
-                                                              pool_status, phase);
-      KX_CHECK_LAUNCH();
-      return;
-    }
-    const WarpLayout wl = warp_layout(dp.ring);
-    if (wl.total <= static_cast<uint32_t>(kDispSmemLimit)) {
-      k_dispatch_warp<<<n_pools, kWarpThreads, wl.total, st>>>(q, a, in, pool_begin, perm,
-                                                              pool_offsets, dp, wl, rows, cand,
-                                                              row_count, admitted_count,
-                                                              pool_status, phase);
       KX_CHECK_LAUNCH();
       return;
     }

@@ -986,11 +986,16 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   P.begin("tie_fix", 0.0, st);
   // one resident wave (grid-stride over the run starts): a partial second
   // wave would double the latency-bound kernel's span
-  static int fix_ctas = [] {
+  static std::once_flag fix_once[kMaxDevices];
+  static int fix_ctas_dev[kMaxDevices];
+  int dev = 0;
+  KX_CUDA(cudaGetDevice(&dev));
+  once_per_device(fix_once, [dev] {
     int b = 0;
     KX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tie_fix_small, 256, 0));
-    return std::max(b, 1);
-  }();
+    fix_ctas_dev[dev] = std::max(b, 1);
+  });
+  const int fix_ctas = fix_ctas_dev[dev];
   k_tie_fix_small<<<sms * fix_ctas, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
                                            ws.n_small, ws.big_starts, ws.big_lens, ws.n_big,
                                            ws.tie_cap);

@@ -96,12 +96,11 @@ void launch_dist_ingest(const DistDev& dd, int32_t n_dist, const int64_t* off, c
   if (n_dist == 0) return;
   const size_t smem = dist_smem_bytes(dd.cap);
   if (smem <= size_t(kDistSmemMax)) {
-    static bool configured = false;
-    if (!configured) {
+    static std::once_flag configured[kMaxDevices];
+    once_per_device(configured, [] {
       KX_CUDA(cudaFuncSetAttribute(k_dist_ingest<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kDistSmemMax));
-      configured = true;
-    }
+    });
     k_dist_ingest<true><<<n_dist, 32, smem, st>>>(dd, n_dist, off, values, item, status);
   } else {
     k_dist_ingest<false><<<n_dist, 32, 0, st>>>(dd, n_dist, off, values, item, status);

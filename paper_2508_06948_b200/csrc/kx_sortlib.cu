@@ -18,12 +18,11 @@ void sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_
   if (n <= 0 || end_bit <= begin_bit) return;
   const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
   if (passes > 8) throw KxError(KX_ERR_INVALID, "sort_pairs: at most 64 key bits");
-  static bool configured = false;
-  if (!configured) {
+  static std::once_flag configured[kMaxDevices];
+  once_per_device(configured, [] {
     KX_CUDA(cudaFuncSetAttribute(k_onesweep_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sort_dyn_smem<K>())));
-    configured = true;
-  }
+  });
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   uint32_t* hist = nullptr;
   uint32_t* lookback = nullptr;

@@ -91,7 +91,11 @@ def full(args):
         wb = float(r[col["dram__bytes_write.sum"]].replace(",", "")) * TO_BYTES.get(units[col["dram__bytes_write.sum"]], 1)
         dur = float(r[col["gpu__time_duration.sum"]].replace(",", ""))
         dunit = units[col["gpu__time_duration.sum"]]
-        dur_s = dur * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-6)
+        scale = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3,
+                 "s": 1.0, "second": 1.0}
+        if dunit not in scale:
+            raise SystemExit(f"unknown duration unit {dunit!r}")
+        dur_s = dur * scale[dunit]
         stalls = []
         for h, i in col.items():
             if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):

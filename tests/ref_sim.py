@@ -64,3 +64,37 @@ def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, rec
     out["priority_keys"] = pk
     out["table_version"] = version.value
     return out
+
+
+def realize(cfg, prefill=8000.0, decode=50.0):
+    """The reference realize() (workload.cpp:319-372) on the same
+    WorkloadConfig (built through the C ABI struct, agent i named "a<i>");
+    returns a dict of flat arrays, or raises ValueError with the reference's
+    exception message."""
+    from paper_2508_06948_b200 import workload as W
+    L = lib()
+    P = C.c_void_p
+    L.kxref_realize.restype = P
+    L.kxref_realize.argtypes = [P, C.c_uint64, C.c_double, C.c_double]
+    L.kxref_realize_error.restype = C.c_char_p
+    L.kxref_realize_error.argtypes = [P]
+    L.kxref_realize_sizes.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.kxref_realize_copy.argtypes = [P] * 11
+    L.kxref_realize_free.argtypes = [P]
+    c, keep, names = W.workload_abi(cfg)
+    h = L.kxref_realize(C.addressof(c), cfg.seed, prefill, decode)
+    try:
+        err = L.kxref_realize_error(h).decode()
+        if err:
+            raise ValueError(err)
+        nw, nc = C.c_int64(), C.c_int64()
+        L.kxref_realize_sizes(h, C.byref(nw), C.byref(nc))
+        Wn, N = nw.value, nc.value
+        out = dict(arrival=np.zeros(Wn), wf_offsets=np.zeros(Wn + 1, np.int64), agent=np.zeros(N, np.int32),
+                   parent=np.zeros(N, np.int32), prompt=np.zeros(N, np.int64), target=np.zeros(N, np.int64),
+                   pure_exec=np.zeros(N), remaining=np.zeros(N), uid=np.zeros(N, np.uint64),
+                   rem_map=np.zeros(N))
+        L.kxref_realize_copy(h, *[v.ctypes.data for v in out.values()])
+    finally:
+        L.kxref_realize_free(h)
+    return out
