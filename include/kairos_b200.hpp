@@ -189,6 +189,7 @@ class DeviceScheduler {
     cfg.slot_ring = 256;
     cfg.device = device;
     default_T_ = dcfg.default_expected_time;
+    time_slot_ = dcfg.policy == KX_DISPATCH_TIME_SLOT;
     check(kx_sched_create(&cfg, &h_));
   }
   ~DeviceScheduler() {
@@ -228,13 +229,24 @@ class DeviceScheduler {
     T_ = T;
     tables_dirty_ = true;
   }
-  // OracleScheduler's remaining_by_uid.
+  // Priority keys computed by the caller's own SchedulerPolicy (e.g.
+  // KairosScheduler::order_key(r).k0 = PriorityTable::priority_key(agent),
+  // scheduler.hpp:111-113): used instead of the coord table when non-empty.
+  void set_agent_keys(const std::map<std::string, double>& pk) {
+    keys_ = pk;
+    tables_dirty_ = true;
+  }
+  // OracleScheduler's remaining_by_uid. The device table is dense over
+  // [min uid, max uid]; a span far wider than the map (hashed uids) is
+  // refused rather than allocated.
   void set_remaining(const std::map<uint64_t, double>& rem) {
     if (rem.empty()) {
       check(kx_set_remaining_table(h_, 0, 0, nullptr, nullptr, KX_MEM_HOST));
       return;
     }
     const uint64_t lo = rem.begin()->first, hi = rem.rbegin()->first;
+    if (hi - lo >= 64 * static_cast<uint64_t>(rem.size()) + (uint64_t(1) << 24))
+      throw std::invalid_argument("set_remaining: uid span too sparse for the dense device table");
     std::vector<double> v(hi - lo + 1, 0.0);
     std::vector<uint8_t> p(hi - lo + 1, 0);
     for (const auto& [u, r] : rem) {
@@ -245,9 +257,38 @@ class DeviceScheduler {
   }
 
   // Replaces the device queue (ReadyQueue::enqueue for every request).
+  // kept: retained tokens per request (admit's kv_tokens = prompt + kept,
+  // engine.cpp:306); pure_exec: the oracle T per request
+  // (oracle_expected_time, engine.cpp:178-180).
   template <typename Request>
   void upload(const std::vector<Request>& q, const std::vector<int64_t>* kept = nullptr,
               const std::vector<double>* pure_exec = nullptr) {
+    const kx_queue_view v = view(q, kept, pure_exec);
+    check(kx_queue_upload(h_, static_cast<int64_t>(q.size()), &v, KX_MEM_HOST));
+    n_ = static_cast<int64_t>(q.size());
+  }
+  // ReadyQueue::enqueue (priority.hpp:72) of n requests behind the queued
+  // ones. msg_id keys must come from the same key space as the queued ones:
+  // MessageIdFactory ids with one prefix (the MsgKeyer fast path).
+  template <typename Request>
+  void enqueue(const std::vector<Request>& q, const std::vector<int64_t>* kept = nullptr,
+               const std::vector<double>* pure_exec = nullptr) {
+    const kx_queue_view v = view(q, kept, pure_exec);
+    check(kx_queue_enqueue(h_, static_cast<int64_t>(q.size()), &v, KX_MEM_HOST));
+    check(kx_queue_size(h_, &n_));
+  }
+  // ReadyQueue::pop of every request the last dispatch round admitted
+  // (engine.cpp:259), keeping the rest in their relative order.
+  void remove_admitted() {
+    check(kx_queue_remove_admitted(h_));
+    check(kx_queue_size(h_, &n_));
+  }
+  int64_t size() const { return n_; }
+
+ private:
+  template <typename Request>
+  kx_queue_view view(const std::vector<Request>& q, const std::vector<int64_t>* kept,
+                     const std::vector<double>* pure_exec) {
     flush_tables();
     const std::size_t n = q.size();
     agent_.resize(n);
@@ -265,11 +306,13 @@ class DeviceScheduler {
       uid_[i] = q[i].uid;
     }
     msg_ = MsgKeyer().keys(q);
-    kx_queue_view v{agent_.data(), prompt_.data(), app_.data(), qe_.data(), msg_.data(), uid_.data(),
-                    kept ? kept->data() : nullptr, pure_exec ? pure_exec->data() : nullptr};
-    check(kx_queue_upload(h_, static_cast<int64_t>(n), &v, KX_MEM_HOST));
-    n_ = static_cast<int64_t>(n);
+    if (kept && kept->size() != n) throw std::invalid_argument("kept: one entry per request");
+    if (pure_exec && pure_exec->size() != n) throw std::invalid_argument("pure_exec: one entry per request");
+    return kx_queue_view{agent_.data(), prompt_.data(), app_.data(), qe_.data(), msg_.data(), uid_.data(),
+                         kept ? kept->data() : nullptr, pure_exec ? pure_exec->data() : nullptr};
   }
+
+ public:
 
   // Full queue order per pool (ReadyQueue pop order): indices into the
   // uploaded vector, pool-major, with pool offsets.
@@ -283,7 +326,11 @@ class DeviceScheduler {
   }
 
   // One dispatch round (engine.cpp:220-268 + gc): order + place. Returns the
-  // decision log in pool order; admitted rows were popped and committed.
+  // decision log in pool order. Admitted rows are committed to the device
+  // ledgers and flagged; they stay queued on the device until
+  // remove_admitted() (or the next upload). candidate_peaks are filled for
+  // the time-slot policy only (Dispatcher::choose logs none otherwise,
+  // dispatcher.cpp:207-250).
   std::vector<DecisionLogRow> dispatch_round(double now) {
     check(kx_tick(h_, now));
     std::vector<int64_t> cnt(static_cast<std::size_t>(n_pools_));
@@ -293,7 +340,6 @@ class DeviceScheduler {
     std::vector<double> cand(static_cast<std::size_t>(n_pools_ * rs * ps));
     check(kx_dispatch_fetch(h_, cnt.data(), rows.data(), cand.data(), &rs, &ps));
     std::vector<DecisionLogRow> out;
-    int64_t inst_begin = 0;
     for (int32_t p = 0; p < n_pools_; ++p) {
       int64_t ni = 0;
       for (const auto& ip : instances_) ni += ip.pool == p ? 1 : 0;
@@ -305,13 +351,14 @@ class DeviceScheduler {
         row.agent = agents_[static_cast<std::size_t>(d.agent)];
         if (d.target >= 0) row.target = d.target;
         row.predicted_peak = d.predicted_peak;
-        const double* c = cand.data() + (p * rs + r) * ps;
-        row.candidate_peaks.assign(c, c + ni);
+        if (time_slot_) {
+          const double* c = cand.data() + (p * rs + r) * ps;
+          row.candidate_peaks.assign(c, c + ni);
+        }
         row.queue_index = d.queue_index;
         row.admitted = d.admitted != 0;
         out.push_back(std::move(row));
       }
-      inst_begin += ni;
     }
     return out;
   }
@@ -342,7 +389,12 @@ class DeviceScheduler {
   void flush_tables() {
     if (!tables_dirty_) return;
     if (agents_.empty()) throw std::invalid_argument("no agents registered");
-    const auto pk = priority_keys(agents_, coord_, anchor_);
+    std::vector<double> pk = priority_keys(agents_, coord_, anchor_);
+    if (!keys_.empty())
+      for (std::size_t i = 0; i < agents_.size(); ++i) {
+        auto k = keys_.find(agents_[i]);
+        pk[i] = k == keys_.end() ? 0.0 : k->second;
+      }
     std::vector<int32_t> depth;
     std::vector<double> T;
     for (const auto& a : agents_) {
@@ -366,7 +418,9 @@ class DeviceScheduler {
   double anchor_ = 0.0;
   std::map<std::string, int> depths_;
   std::map<std::string, double> T_;
+  std::map<std::string, double> keys_;
   double default_T_ = 1.0;
+  bool time_slot_ = true;
   bool tables_dirty_ = true;
   uint64_t table_version_ = 0;
   int64_t n_ = 0;

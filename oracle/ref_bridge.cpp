@@ -280,6 +280,10 @@ double kxref_pools_tick(void** pools, int n, double now, int threads) {
 #include "kairos/metrics.hpp"
 #include "kairos/workflow.hpp"
 
+#ifdef KX_DROPIN
+extern "C" void kx_dropin_release(const void* dispatcher);
+#endif
+
 namespace {
 const char* kBuiltin[10] = {"Router", "Math", "Humanities", "Researcher", "Writer",
                             "ProductManager", "Architect", "ProjectManager", "Engineer", "QAEngineer"};
@@ -362,6 +366,9 @@ extern "C" int kxref_sim_run(
     WorkflowAnalyzer analyzer;
     Simulator sim(ecfg, real, *sched, disp, profiler, analyzer);
     RunResult run = sim.run();
+#ifdef KX_DROPIN
+    kx_dropin_release(&disp);  // the drop-in build's device state of this Dispatcher
+#endif
     for (std::size_t j = 0; j < run.calls.size(); ++j) {
       const auto& c = run.calls[j];
       c_uid[j] = c.uid;

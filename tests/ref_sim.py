@@ -10,23 +10,28 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parents[1]
 SO = ROOT / "oracle" / "_ref" / "libkxref.so"
+# the drop-in build: the same reference Simulator with its time-slot dispatch
+# round and Dispatcher events on the B200 (oracle/dropin_sim.cpp)
+DROPIN_SO = ROOT / "oracle" / "_ref" / "libkxdropin.so"
 SCHED = {"kairos": 0, "fcfs": 1, "topo_depth": 2, "oracle": 3}
 DISPATCH = {"time_slot": 0, "round_robin": 1, "static_threshold": 2}
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not SO.exists():
+def lib(so=SO):
+    if so not in _libs:
+        if not Path(so).exists():
             subprocess.run(["make", "-C", str(ROOT / "oracle")], check=True, capture_output=True)
-        _lib = C.CDLL(str(SO))
-        _lib.kxref_sim_run.restype = C.c_int
-    return _lib
+        L = C.CDLL(str(so))
+        L.kxref_sim_run.restype = C.c_int
+        _libs[so] = L
+    return _libs[so]
 
 
-def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, recompute=1.0):
-    """One replica through the reference Simulator; returns a dict like engine.run_replicas."""
+def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, recompute=1.0, so=SO):
+    """One replica through the reference Simulator (the stock build, or
+    with so=DROPIN_SO the drop-in build); returns a dict like
+    engine.run_replicas."""
     b = batch_one
     W = len(b["arrival"])
     Cn = len(b["agent"])
@@ -57,7 +62,7 @@ def run(batch_one, instances, scheduler, dispatcher, topo_depth, period=0.1, rec
         C.c_double(d.static_threshold), C.c_double(d.default_expected_time), C.c_double(period),
         C.c_double(recompute), P(depth.ctypes.data)] + [P(v.ctypes.data) for v in out.values()] + [
         C.byref(nc), C.byref(nw), P(pk.ctypes.data), C.byref(version)]
-    rc = lib().kxref_sim_run(*args)
+    rc = lib(so).kxref_sim_run(*args)
     assert rc == 0, "reference simulation failed"
     out["n_calls"] = nc.value
     out["n_wf"] = nw.value
