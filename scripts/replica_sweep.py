@@ -45,11 +45,60 @@ def sweep(args, rank=0, ws=1, dev=0):
     b = E.concat(reals)
     t_gen = time.time() - t0
     disp = DispatcherConfig(args.dispatcher, oracle_expected_time=not args.profile_T)
+    sys.path.insert(0, str(ROOT))
+    from bench import Clocks  # nvidia-smi sampling over the device run
+    clocks = Clocks(dev)
+    clocks.mark(True)
     res = E.run_replicas(b, instances(args.instances), args.scheduler, disp, topo_depth=DEPTH,
                          device=dev, warmup_seconds=args.warmup)
+    clocks.mark(False)
+    res["clocks"] = clocks.stop()
     n_calls = int(res["counts"][:, 0].sum())
     events = int(res["counts"][:, 3].sum())
     return mine, res, n_calls, events, t_gen, b
+
+
+def parity(args, mine, res, b, n_check):
+    """Bit-exact comparison of n_check replicas (spread over the sweep) with
+    the UNMODIFIED reference Simulator on the same realize() output:
+    completion order, per-call exec times, counters and compute_metrics."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ref_sim  # noqa: E402  (oracle/_ref/libkxref.so)
+    disp = DispatcherConfig(args.dispatcher, oracle_expected_time=not args.profile_T)
+    picks = sorted({int(round(x)) for x in np.linspace(0, len(mine) - 1, n_check)})
+
+    def one(j):
+        r = mine[j]
+        rz = E.realize("colocated", args.rate, args.duration, seed=1 + r)
+        ref = ref_sim.run(rz, instances(args.instances), args.scheduler, disp, DEPTH)
+        c0 = int(b["wf_offsets"][b["wf_base"][j]])
+        n = int(ref["n_calls"])
+        bad = []
+        if int(res["counts"][j][0]) != n:
+            return r, n, ["call count"]
+        order = res["call_order"][c0:c0 + n]
+        bits = lambda a: np.ascontiguousarray(a).view(np.uint64)  # noqa: E731
+        if not np.array_equal(b["uid"][order], ref["uid"][:n]):
+            bad.append("completion order")
+        for k in ("exec_start", "exec_end"):
+            if not np.array_equal(bits(res[k][c0:c0 + n]), bits(ref[k][:n])):
+                bad.append(k)
+        if not np.array_equal(bits(res["scalars"][j][:8]), bits(ref["scalars"][:8])):
+            bad.append("counters")
+        m, rs = res["metrics"][j], ref["scalars"]
+        for mi, ri in [(2, 8), (3, 9), (4, 10), (5, 11), (6, 12), (7, 13), (8, 14), (11, 15), (13, 16), (12, 17)]:
+            if bits(np.array([m[mi]]))[0] != bits(np.array([rs[ri]]))[0]:
+                bad.append(f"metric {mi}")
+        return r, n, bad
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(min(len(picks), os.cpu_count() or 1)) as ex:
+        outs = list(ex.map(one, picks))
+    return {"replicas_checked": [o[0] for o in outs], "requests_checked": sum(o[1] for o in outs),
+            "mismatches": sum(len(o[2]) for o in outs), "details": {o[0]: o[2] for o in outs if o[2]},
+            "checked": "completion order, exec_start/exec_end bits per call, counters, compute_metrics bits",
+            "reference": "unmodified reference Simulator (oracle/_ref/libkxref.so)",
+            "seconds": time.perf_counter() - t0}
 
 
 def cpu_reference(args, sample):
@@ -79,6 +128,8 @@ def main():
     ap.add_argument("--dispatcher", default="time_slot")
     ap.add_argument("--warmup", type=float, default=0.0)
     ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--parity", type=int, default=0,
+                    help="compare this many replicas bit-exact with the reference Simulator")
     ap.add_argument("--profile-T", action="store_true",
                     help="time_slot T from the online profiler (engine.cpp:177-185) instead of the oracle's")
     args = ap.parse_args()
@@ -111,6 +162,7 @@ def main():
     if rank == 0:
         agg = E.aggregate(rows)
         cpu = cpu_reference(args, min(args.cpu_sample, args.replicas)) if ws == 1 and args.cpu_sample > 0 else None
+        par = parity(args, mine, res, b, args.parity) if ws == 1 and args.parity > 0 else None
         print(json.dumps({
             "metric": "simulated requests/s (replica sweep: DES + per-replica metrics on device)",
             "value": n_calls / (dev_ms / 1e3), "unit": "simulated requests/s", "n_gpus": ws,
@@ -121,7 +173,8 @@ def main():
                        "expected_T": "profiler" if args.profile_T else "oracle"},
             "aggregate": dict(zip(E.METRIC_NAMES, [float(x) for x in agg])),
             "histogram_total": int(hist.sum()),
-            "cpu_baseline": cpu, "host_realize_s": t_gen}), flush=True)
+            "cpu_baseline": cpu, "parity": par, "clocks": res.get("clocks"),
+            "host_realize_s": t_gen}), flush=True)
     if dist:
         dist.destroy_process_group()
 
