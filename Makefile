@@ -12,7 +12,8 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcom
 PKG      := paper_2508_06948_b200
 SRC      := $(PKG)/csrc
 OUT      := $(PKG)/_lib
-CU       := kx_abi kx_order kx_dispatch kx_orchestrator kx_engine kx_sortlib kx_accuracy kx_priority kx_profiler
+CU       := kx_abi kx_order kx_dispatch kx_orchestrator kx_engine kx_sortlib kx_accuracy kx_priority kx_profiler \
+            kx_trace
 CPP      := kx_workload
 OBJS     := $(patsubst %,$(OUT)/obj/%.o,$(CU)) $(patsubst %,$(OUT)/obj/%.cpp.o,$(CPP))
 CXXFLAGS := -std=c++20 -O2 -ffp-contract=off -fPIC -Wall -Wextra

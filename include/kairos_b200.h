@@ -473,6 +473,50 @@ int kx_realization_copy(const kx_realization* r, double* arrival, int32_t* app, 
                         double* pure_exec, double* remaining, uint64_t* uid);
 void kx_realization_free(kx_realization* r);
 
+/* ---- trace CSV I/O + workflow reconstruction ------------- */
+/* read_trace (trace.cpp:111-127) of a whole CSV on the device: lines split on
+ * '\n' (std::getline), the header line (kTraceHeader, trace.cpp:10-12)
+ * skipped on line 1, empty lines skipped, every line parsed and validated
+ * as parse_trace_line + validate (trace.cpp:14-27, 90-109). The first bad
+ * line fails with KX_ERR_INVALID and the reference's message ("trace line N:
+ * ..."). Numbers: correctly rounded like strtod for decimal forms with <= 19
+ * significant digits and a power of ten within +-22 (every format_seconds
+ * output below 1e10 s); other std::stod forms (hex, inf, nan, longer
+ * significands, larger exponents) are refused, never approximated. Agents are ranked
+ * in std::string order (the graph's std::map/std::set order); msg ids keep
+ * an internal index. */
+typedef struct kx_trace kx_trace;
+int kx_trace_parse(const char* bytes, int64_t n_bytes, int32_t device, kx_trace** out);
+void kx_trace_free(kx_trace* t);
+int kx_trace_sizes(const kx_trace* t, int64_t* n_records, int32_t* n_agents, int64_t* n_msgs,
+                   int64_t* agent_name_bytes);
+/* Agent names, concatenated; offsets[n_agents + 1]. */
+int kx_trace_agents(const kx_trace* t, char* names, int64_t* offsets);
+/* RequestRecord fields (types.hpp) in file order; upstream = -1 when empty.
+ * Any output may be NULL. */
+int kx_trace_columns(const kx_trace* t, int64_t* msg, int32_t* agent, int32_t* upstream, double* exec_start,
+                     double* exec_end, int64_t* prompt_tokens, int64_t* output_tokens, double* app_start);
+int kx_trace_msg_id(const kx_trace* t, int64_t msg, char* buf, int64_t cap, int64_t* len);
+/* write_trace (trace.cpp:44-48) of the parsed records, formatted on the
+ * device (format_seconds' "%.9f" exact); out = NULL returns the size. */
+int kx_trace_format(kx_trace* t, char* out, int64_t cap, int64_t* n_out);
+/* WorkflowAnalyzer::ingest_trace (workflow.cpp:319-343): every msg_id group
+ * folded by WorkflowGraph::ingest_instance (workflow.cpp:59-111). */
+typedef struct kx_workflow_sizes {
+  int64_t n_edges;        /* distinct (upstream, agent) edges */
+  int64_t n_diagnostics;  /* conflicting-entry diagnostics */
+  int64_t instances;      /* instances_ingested */
+} kx_workflow_sizes;
+int kx_workflow_reconstruct(kx_trace* t, kx_workflow_sizes* sizes);
+/* Edges in (from, to) name order with their observation counts; per agent:
+ * entry flag and the fan-out tallies (parallel, sequential, single
+ * observations; an agent with none is no fan-out node); diagnostics in
+ * ingest order (msg index, the instance's entry, the conflicting entry).
+ * Any output may be NULL. */
+int kx_workflow_fetch(const kx_trace* t, int32_t* edge_from, int32_t* edge_to, uint64_t* edge_count,
+                      uint8_t* is_entry, uint64_t* fan_parallel, uint64_t* fan_sequential, uint64_t* fan_single,
+                      int64_t* diag_msg, int32_t* diag_entry, int32_t* diag_other);
+
 /* ---- K1: orchestrator DP ------------------------------------------------ */
 /* finalize_instance (workload.cpp:292-315) for many workflow instances at
  * once: calls of workflow w are [wf_offsets[w], wf_offsets[w+1]), in node_id

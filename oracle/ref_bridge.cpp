@@ -559,3 +559,68 @@ extern "C" void kxref_realize_copy(void* h, double* arrival, int64_t* wf_offsets
 }
 
 extern "C" void kxref_realize_free(void* h) { delete static_cast<RefRealization*>(h); }
+
+// ---- trace CSV + workflow reconstruction (tests of kx_trace_* / workflow) --
+// read_trace (trace.cpp:111-127) of a byte buffer; WorkflowAnalyzer's
+// ingest_trace + the graph's report(), topo_depth and downstream_paths per
+// node; write_trace of the parsed records. Errors come back as the
+// reference's exception text with a negative length.
+#include <sstream>
+
+#include "kairos/trace.hpp"
+#include "kairos/workflow.hpp"
+
+namespace {
+int64_t put_text(const std::string& s, char* out, int64_t cap) {
+  const int64_t n = static_cast<int64_t>(s.size());
+  if (out && cap >= n) std::memcpy(out, s.data(), s.size());
+  return n;
+}
+}  // namespace
+
+extern "C" int64_t kxref_trace_report(const char* bytes, int64_t n, int max_loop, char* out, int64_t cap) {
+  try {
+    std::istringstream in(std::string(bytes, static_cast<size_t>(n)));
+    const auto recs = read_trace(in);
+    WorkflowAnalyzer a;
+    a.ingest_trace(recs);
+    const auto g = a.snapshot();
+    std::string s = g->report();
+    for (const auto& node : g->nodes()) {
+      s += "depth " + node + " " + std::to_string(g->topo_depth(node)) + "\n";
+      for (const auto& p : g->downstream_paths(node, max_loop)) {
+        s += "path " + node + ":";
+        for (const auto& x : p) s += " " + x;
+        s += "\n";
+      }
+    }
+    return put_text(s, out, cap);
+  } catch (const std::exception& e) {
+    return -put_text(e.what(), out, cap) - 1;
+  }
+}
+
+extern "C" int64_t kxref_trace_write(const char* bytes, int64_t n, char* out, int64_t cap) {
+  try {
+    std::istringstream in(std::string(bytes, static_cast<size_t>(n)));
+    std::ostringstream o;
+    write_trace(o, read_trace(in));
+    return put_text(o.str(), out, cap);
+  } catch (const std::exception& e) {
+    return -put_text(e.what(), out, cap) - 1;
+  }
+}
+
+extern "C" int64_t kxref_trace_columns(const char* bytes, int64_t n, int64_t cap, double* es, double* ee,
+                                       double* as, int64_t* pt, int64_t* ot) {
+  std::istringstream in(std::string(bytes, static_cast<size_t>(n)));
+  const auto recs = read_trace(in);
+  for (size_t i = 0; i < recs.size() && static_cast<int64_t>(i) < cap; ++i) {
+    es[i] = recs[i].exec_start;
+    ee[i] = recs[i].exec_end;
+    as[i] = recs[i].app_start;
+    pt[i] = recs[i].prompt_tokens;
+    ot[i] = recs[i].output_tokens;
+  }
+  return static_cast<int64_t>(recs.size());
+}

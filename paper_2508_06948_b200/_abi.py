@@ -38,6 +38,10 @@ class KxError(RuntimeError):
         self.code = code
 
 
+class kx_workflow_sizes(C.Structure):
+    _fields_ = [("n_edges", C.c_int64), ("n_diagnostics", C.c_int64), ("instances", C.c_int64)]
+
+
 class kx_instance(C.Structure):
     _fields_ = [("id", C.c_int32), ("pool", C.c_int32), ("capacity_tokens", C.c_double),
                 ("decode_rate", C.c_double), ("prefill_rate", C.c_double),
@@ -201,6 +205,16 @@ SIGNATURES = {
     "kx_orchestrator_dp": (C.c_int, [C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, C.c_uint64,
                                      _P, _P, _P, C.c_int32]),
     "kx_record_remaining": (C.c_int, [C.c_int64, _P, _P, _P, _P, _P, C.c_int32]),
+    "kx_trace_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(_P)]),
+    "kx_trace_free": (None, [_P]),
+    "kx_trace_sizes": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64)]),
+    "kx_trace_agents": (C.c_int, [_P, _P, _P]),
+    "kx_trace_columns": (C.c_int, [_P] + [_P] * 8),
+    "kx_trace_msg_id": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "kx_trace_format": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "kx_workflow_reconstruct": (C.c_int, [_P, C.POINTER(kx_workflow_sizes)]),
+    "kx_workflow_fetch": (C.c_int, [_P] + [_P] * 10),
 }
 
 _lib = None

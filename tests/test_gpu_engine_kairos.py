@@ -55,3 +55,22 @@ def test_kairos_rebuild_interval(gpu_lib):
                          rebuild_interval=16)
     dev256 = E.run_replicas(b, insts(4), "kairos", DispatcherConfig("time_slot"), topo_depth=DEPTH)
     assert int(dev["table_versions"][0]) > int(dev256["table_versions"][0])
+
+
+def test_c5_shape_replicas_match_reference_simulator(gpu_lib):
+    """BASELINE C5's replica shape: the co-located workload at
+    12 workflows/s for 720 s on 16 instances, Kairos + profiler T, two
+    replicas of a sweep, each bit-exact against the reference Simulator."""
+    from paper_2508_06948_b200 import InstanceProfile
+    inst = [InstanceProfile(id=i, capacity_tokens=3000.0, decode_rate=50.0, prefill_rate=8000.0, max_batch=8)
+            for i in range(16)]
+    disp = DispatcherConfig("time_slot")
+    reals = [E.realize("colocated", 12.0, 720.0, seed) for seed in (1, 5)]
+    b = E.concat(reals)
+    dev = E.run_replicas(b, inst, "kairos", disp, topo_depth=DEPTH)
+    for r, rz in enumerate(reals):
+        ref = ref_sim.run(dict(rz), inst, "kairos", disp, DEPTH)
+        assert ref["n_calls"] > 20000
+        compare(dev, ref, b, r, int(b["wf_offsets"][b["wf_base"][r]]), int(b["wf_base"][r]))
+        assert int(dev["table_versions"][r]) == ref["table_version"] > 0
+        assert np.array_equal(bits(dev["priority_keys"][r]), bits(ref["priority_keys"]))
