@@ -2101,6 +2101,16 @@ int kx_debug_dispatch_timers(uint64_t* out16) {
   return guard([&] { kx::read_dispatch_debug(reinterpret_cast<unsigned long long*>(out16)); });
 }
 
+// Diagnostics: per-stage resolver cycles of pool 0 (KX_DISPATCH_TIMERS=2 builds).
+int kx_debug_dispatch_stages(uint64_t* out16) {
+  return guard([&] { kx::read_dispatch_stages(reinterpret_cast<unsigned long long*>(out16)); });
+}
+
+// Diagnostics: clock stamps of 8 register-resolver steps of pool 0 (KX_DISPATCH_TIMERS=3 builds).
+int kx_debug_dispatch_trace(uint64_t* out128) {
+  return guard([&] { kx::read_dispatch_trace(reinterpret_cast<unsigned long long*>(out128)); });
+}
+
 // Diagnostics: per-pass tile phase sums of the radix passes (KX_SORT_TIMERS builds).
 int kx_debug_sort_timers(uint64_t* out64, int32_t reset) {
   return guard([&] { kx::read_sort_debug(reinterpret_cast<unsigned long long*>(out64), reset != 0); });

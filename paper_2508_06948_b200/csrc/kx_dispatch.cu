@@ -660,12 +660,20 @@ __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __res
 #define KX_DISPATCH_TIMERS 0
 #endif
 __device__ unsigned long long g_disp_dbg[16];
+__device__ unsigned long long g_disp_st[16];
+__device__ unsigned long long g_disp_tr[8 * 16];  // KX_DISPATCH_TIMERS=3: clock stamps of 8 rr steps (pool 0)  // KX_DISPATCH_TIMERS=2: per-stage resolver cycles (pool 0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
+#ifndef KX_REG_RESOLVER
+#define KX_REG_RESOLVER 1
+#endif
+#ifndef KX_RR_PUBLISH
+#define KX_RR_PUBLISH 16  // rr: records staged per publication (one fence each)
+#endif
 #ifndef KX_CHAIN_HELPERS
 #define KX_CHAIN_HELPERS 4
 #endif
@@ -679,7 +687,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // prologue (staging, the prefix sort) and the write-back.
 constexpr int kHelpers = KX_CHAIN_HELPERS;
 constexpr int kLead = KX_CHAIN_LEAD;         // a helper starts head j when the resolver is at j - kLead
-constexpr int kChainThreads = 384;
+constexpr int kChainThreads = 256;  // 8 warps: 4 helpers, loader, flush, resolver (+1 idle)
 constexpr int kResolverWarp = kChainThreads / 32 - 1;
 __host__ __device__ constexpr int role_warp(int h) { return h + h / 3; }  // skips wid % 4 == 3
 constexpr int kLoaderWarp = role_warp(kHelpers);
@@ -953,6 +961,11 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
 #pragma unroll
   for (int s = 0; s < NI; ++s) kuni = kuni && (!act_[s] || kr_[s] == k0);
   const bool k_uniform = __all_sync(0xffffffffu, kuni);
+  // Register-resident resolver (uniform decode rates: every fast head's pk
+  // table is instance-independent): the resolver keeps each instance's usage
+  // of the next kRegSlots slots in registers and needs no helper rows.
+  constexpr int kRegSlots = 16;  // the configs' spans are <= 16 slots; longer spans take the exact path
+  const bool rr = KX_REG_RESOLVER && NI == 1 && k_uniform && ring >= kRegSlots;
 
   // ---- phase 3: the prefix collected by key generation, sorted here ----
   if (ph.phase == 3) {
@@ -1073,7 +1086,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           }
         }
     }
-  } else if (warp < kLoaderWarp && warp % 4 != 3) {
+  } else if (warp < kLoaderWarp && warp % 4 != 3 && !rr) {
     // ---- helpers: the row of head j, (first violating span slot, span max
     //      of used + pk) per instance, against a snapshot of commit count v ----
     const int h = warp - warp / 4;  // helper index (inverse of role_warp)
@@ -1211,10 +1224,13 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     int hs = 0, mode = 0, tn = 0, pbase = 0;
     int32_t fo = 0;
     int64_t first = 0, last = -1, prompt = 0, kept = 0;
+    int64_t known_loaded = pos0;  // heads below it are landed (fenced)
     auto load_head = [&](int64_t pp) {
-      while (s_loaded <= pp) {
+      if (pp >= known_loaded) {
+        while ((known_loaded = s_loaded) <= pp) {
+        }
+        smem_order();
       }
-      smem_order();
       hs = static_cast<int>((pp - pos0) & (kHR - 1));
       mode = h_mode[hs];
       first = h_first[hs];
@@ -1226,17 +1242,227 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       pbase = static_cast<int>((B + fo) & rmask);
     };
     if (p < q_end) load_head(p);
+    // ---- register-resident state (rr): usage of slots cslot + j, j < kRegSlots ----
+    double ru[NI][kRegSlots];
+    uint32_t rbook[NI];  // slots booked this round (written back to the shared ledger)
+    // (macros, not lambdas: a lambda capturing the register arrays by
+    // reference can push them to local memory)
+#define KX_RR_RELOAD()                                                                      \
+  do {                                                                                      \
+    _Pragma("unroll") for (int s_ = 0; s_ < NI; ++s_) {                                     \
+      rbook[s_] = 0;                                                                        \
+      _Pragma("unroll") for (int j_ = 0; j_ < kRegSlots; ++j_)                              \
+        ru[s_][j_] = su[((cslot + j_) & rmask) * kRW + lane + 32 * s_];                     \
+    }                                                                                       \
+  } while (0)
+#define KX_RR_FLUSH()                                                                       \
+  do {                                                                                      \
+    _Pragma("unroll") for (int s_ = 0; s_ < NI; ++s_) {                                     \
+      _Pragma("unroll") for (int j_ = 0; j_ < kRegSlots; ++j_)                              \
+        if ((rbook[s_] >> j_) & 1u) {                                                       \
+          const int p2_ = static_cast<int>((cslot + j_) & rmask);                           \
+          su[p2_ * kRW + lane + 32 * s_] = ru[s_][j_];                                      \
+          se[p2_ * kRW + lane + 32 * s_] = 1;                                               \
+        }                                                                                   \
+      rbook[s_] = 0;                                                                        \
+    }                                                                                       \
+    __syncwarp();                                                                           \
+  } while (0)
+    // the current head's span table (pk, instance-independent under rr)
+    double c_pk[kRegSlots];
+#define KX_LOAD_PK(dst, hs_)                                                           \
+  do {                                                                                      \
+    const double* t_ = stab + (hs_) * kDtSlots;                                             \
+    _Pragma("unroll") for (int j_ = 0; j_ < kRegSlots; j_ += 2) {                           \
+      const double2 v_ = *reinterpret_cast<const double2*>(t_ + j_);                       \
+      dst[j_] = v_.x;                                                                       \
+      dst[j_ + 1] = v_.y;                                                                   \
+    }                                                                                       \
+  } while (0)
+    if (rr) {
+      KX_RR_RELOAD();
+      if (p < q_end) KX_LOAD_PK(c_pk, hs);
+    }
+    int32_t rr_pub = staged;  // records staged but not yet published (rr publishes in batches)
+    auto rr_publish = [&]() {
+      smem_order();
+      __syncwarp();
+      if (lane == 0) {
+        s_staged = staged;
+        s_cur = p;
+      }
+      rr_pub = staged;
+    };
+#if KX_DISPATCH_TIMERS >= 2
+    long long st_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long st_prev = clock64();
+#define STAMP(k) do { const long long _c = clock64(); st_acc[k] += _c - st_prev; st_prev = _c; } while (0)
+#else
+#define STAMP(k) do { } while (0)
+#endif
+#if KX_DISPATCH_TIMERS == 3
+#define TRACE(k)                                                                            \
+  do {                                                                                      \
+    if (pool == 0 && tr_it >= 0 && tr_it < 8 && lane == 0) g_disp_tr[tr_it * 16 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(k) do { } while (0)
+#endif
     while (p < q_end) {
+      STAMP(0);  // load_head + loop overhead
+      const int64_t tr_it = p - pos0 - 100;
+      (void)tr_it;
+      TRACE(0);
+      if constexpr (NI == 1) {
+      if (rr && mode == kModeTabPk && tn <= kRegSlots) {
+        // ---- one head, all instances in registers (lane = instance) ----
+        // Prefetch the next head (fields + span table): independent of this
+        // decision, so its shared-memory latency hides under the evaluation.
+        // (raw loads only: in-order issue stalls at the first consumer, which
+        // is the copy at the end of the step)
+        const bool has_next = p + 1 < q_end;
+        if (has_next && p + 1 >= known_loaded) {
+          if (staged != rr_pub) rr_publish();  // the loader may wait for the published position
+          while ((known_loaded = s_loaded) <= p + 1) {
+          }
+          smem_order();
+        }
+        const int n_hs = static_cast<int>((p + 1 - pos0) & (kHR - 1));
+        const int n_mode = h_mode[n_hs];
+        const int64_t n_first = h_first[n_hs];
+        const int64_t n_last = h_last[n_hs];
+        const int64_t n_prompt = h_prompt[n_hs];
+        const int64_t n_kept = h_kept[n_hs];
+        double n_pk[kRegSlots];
+#pragma unroll
+        for (int j = 0; j < kRegSlots; j += 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(stab + n_hs * kDtSlots + j);
+          n_pk[j] = v2.x;
+          n_pk[j + 1] = v2.y;
+        }
+        TRACE(1);
+        // try_place (dispatcher.cpp:52-68) for the common shape: span
+        // [cslot, last], peak = max(stored max, max over the span of used + pk);
+        // the flags that do not read the ledger first
+        const double P = static_cast<double>(prompt);
+        const bool elig = act_[0] && !susp_[0] && !(run_[0] + wait_[0] >= mb_[0]);
+        const uint32_t ovfm = __ballot_sync(0xffffffffu, elig && (first < base_[0] || last >= base_[0] + ring));
+        const uint32_t ovrm = __ballot_sync(0xffffffffu, __dadd_rn(live_[0], P) > cap_[0]);
+        const uint32_t fullm = __ballot_sync(0xffffffffu, nact_[0] >= kActiveCap);
+        // span totals: violations as a slot mask, the max as a tree
+        uint32_t vm = 0;
+        double t[kRegSlots];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double x = __dadd_rn(ru[0][j], c_pk[j]);
+          vm |= (j < tn && x > cap_[0]) ? (1u << j) : 0u;
+          t[j] = j < tn ? x : 0.0;
+        }
+        if (tn > 8) {
+#pragma unroll
+          for (int j = 8; j < kRegSlots; ++j) {
+            const double x = __dadd_rn(ru[0][j], c_pk[j]);
+            vm |= (j < tn && x > cap_[0]) ? (1u << j) : 0u;
+            t[j] = j < tn ? x : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = t[j + 8] > t[j] ? t[j + 8] : t[j];
+        }
+#pragma unroll
+        for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+          for (int j = 0; j < w; ++j) t[j] = t[j + w] > t[j] ? t[j + w] : t[j];
+        const uint64_t sm = nonneg_bits(t[0]);
+        const uint64_t peak = umax_[0] > sm ? umax_[0] : sm;
+        const uint64_t key = (elig && vm == 0) ? peak : ~0ull;
+        // this head's candidate peak (dispatcher.cpp:143-147), staged below
+        const double cval = !elig ? -1.0
+                            : vm == 0 ? from_ordered_bits(peak)
+                                      : __dsub_rn(-static_cast<double>(cslot + __ffs(vm) - 1), 1.0);
+        TRACE(2);
+        // select_instance: min (peak, InstanceId rank) over the fitting instances
+        const uint64_t kmin = warp_min_u64(key);
+        const uint32_t wb = __ballot_sync(0xffffffffu, key == kmin);
+        const int bl = wb ? __ffs(wb) - 1 : -1;
+        const bool wovr = bl >= 0 && ((ovrm >> bl) & 1u);
+        const bool wfull = bl >= 0 && ((fullm >> bl) & 1u);
+        STAMP(3);
+        TRACE(3);
+        if (ovfm == 0 && kmin != ~0ull && !wovr && !wfull) {
+          // stage the decision record
+          if ((staged & (kStage / 2 - 1)) == 0) {
+            if (staged != rr_pub) rr_publish();
+            while (staged - s_flushed > kStage / 2) {
+            }
+          }
+          const int sl = staged & (kStage - 1);
+          st_cand[sl * kR + lane] = cval;
+          if (lane == 0) st_meta[sl] = (static_cast<uint32_t>(p - pos0) << 9) | 256u | static_cast<uint32_t>(bl + 1);
+          ++staged;
+          ++nrows;
+          TRACE(4);
+          // Dispatcher::commit + admit (engine.cpp:298-319) in the target's lane
+          const bool me = lane == bl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ru[0][j] = (me && j < tn) ? __dadd_rn(ru[0][j], c_pk[j]) : ru[0][j];
+          if (tn > 8) {
+#pragma unroll
+            for (int j = 8; j < kRegSlots; ++j) ru[0][j] = (me && j < tn) ? __dadd_rn(ru[0][j], c_pk[j]) : ru[0][j];
+          }
+          TRACE(5);
+          rbook[0] |= me ? (1u << tn) - 1u : 0u;
+          live_[0] = me ? __dadd_rn(live_[0], static_cast<double>(prompt + kept)) : live_[0];
+          run_[0] += me ? 1 : 0;
+          umax_[0] = me ? kmin : umax_[0];
+          hi_[0] = (me && last > hi_[0]) ? last : hi_[0];
+          lm_[0] = me ? commits : lm_[0];
+          nact_[0] += (me && nact_[0] < kActiveCap) ? 1 : 0;
+          ++commits;
+          retries = 0;
+          TRACE(6);
+          ++p;
+          if (staged - rr_pub >= KX_RR_PUBLISH) rr_publish();
+          TRACE(7);
+          if (has_next) {  // the prefetched head becomes the current one
+            hs = n_hs;
+            mode = n_mode;
+            first = n_first;
+            last = n_last;
+            prompt = n_prompt;
+            kept = n_kept;
+            fo = static_cast<int32_t>(first - B);
+            tn = static_cast<int>(last - first + 1);
+            pbase = static_cast<int>((B + fo) & rmask);
+#pragma unroll
+            for (int j = 0; j < kRegSlots; ++j) c_pk[j] = n_pk[j];
+          }
+          TRACE(8);
+          STAMP(4);
+#if KX_DISPATCH_TIMERS >= 2
+          st_acc[9] += 1;
+#endif
+          continue;
+        }
+      }
+      }
+#if KX_DISPATCH_TIMERS >= 2
+      st_acc[10] += 1;
+#endif
+      if (rr) {  // anything unusual: the exact path over the shared ledger
+        if (staged != rr_pub) rr_publish();
+        KX_RR_FLUSH();
+      }
 #if KX_DISPATCH_TIMERS
       long long tA = clock64();
 #endif
       const double P = static_cast<double>(prompt);
       const double* tab = stab + hs * kDtSlots;
       const bool nonempty = last >= first;
-      if (mode != kModeGeneric) {
+      if (mode != kModeGeneric && !rr) {
         const int slot = static_cast<int>((p - pos0) & (kRowRing - 1));
         while (s_tag[slot] != p) {
         }
+        STAMP(1);  // helper row wait
         smem_order();
         const int32_t v = s_rver[slot];
         uint64_t smax[NI];
@@ -1247,6 +1473,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           smax[s] = r_smax[slot * kR + lane + 32 * s];
           dm[s] = __ballot_sync(0xffffffffu, lm_[s] >= v);
         }
+        STAMP(2);  // fence + row loads
 #if KX_DISPATCH_TIMERS
         const long long tB = clock64();
         acc[0] += tB - tA;
@@ -1290,6 +1517,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           }
           rpeak[s] = umax_[s] > smax[s] ? umax_[s] : smax[s];
         }
+        STAMP(3);  // fix
 #if KX_DISPATCH_TIMERS
         acc[1] += clock64() - tB;
 #endif
@@ -1379,6 +1607,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           }
         const bool admit = bl >= 0 && !overload;
         ++nrows;
+        STAMP(4);  // select
 #if KX_DISPATCH_TIMERS
         const long long tD = clock64();
         acc[2] += tD - tC;
@@ -1401,6 +1630,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         if (lane == 0)
           st_meta[sl] = (static_cast<uint32_t>(p - pos0) << 9) | (admit ? 256u : 0u) | static_cast<uint32_t>(bl + 1);
         ++staged;
+        STAMP(5);  // staging
         if (admit) {
           // Dispatcher::commit: book the span slots of the target
           uint64_t umax_new = shfl_u64(bs == 0 ? rpeak[0] : rpeak[NI - 1], bln);
@@ -1447,6 +1677,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
             }
             umax_new = shfl_u64(um, bln);
           }
+          STAMP(6);  // ledger booking
           // admit (engine.cpp:298-319) in the target's lane
 #pragma unroll
           for (int s = 0; s < NI; ++s)
@@ -1459,6 +1690,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
               nact_[s] += nact_[s] < kActiveCap ? 1 : 0;
             }
           ++commits;
+          STAMP(7);  // admit state
         }
         // publish: the staged record, and with a commit the next position
         // (helpers snapshot it; the loader reuses ring slots below it)
@@ -1468,6 +1700,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           s_staged = staged;
           if (admit) s_cur = p + 1;
         }
+        STAMP(8);  // fence + publish
 #if KX_DISPATCH_TIMERS
         acc[3] += clock64() - tD;
 #endif
@@ -1495,14 +1728,37 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         next = true;
         break;
       }
+      if (rr) KX_RR_RELOAD();
       if (!next) break;
       ++p;
-      if (p < q_end) load_head(p);
+      rr_pub = staged;  // the exact path publishes every record
+      if (p < q_end) {
+        load_head(p);
+        if (rr) KX_LOAD_PK(c_pk, hs);
+      }
+    }
+    if (rr) {
+      KX_RR_FLUSH();
+      smem_order();
+      __syncwarp();
+      if (lane == 0) {
+        s_staged = staged;
+        s_cur = p;
+      }
     }
     smem_order();
     if (lane == 0) s_stop = 1;
     f_rows = nrows;
     f_adm = commits;
+#if KX_DISPATCH_TIMERS >= 2
+    if (pool == 0 && lane == 0)
+      for (int k = 0; k < 12; ++k) g_disp_st[k] = static_cast<unsigned long long>(st_acc[k]);
+#endif
+#undef STAMP
+#undef TRACE
+#undef KX_RR_RELOAD
+#undef KX_LOAD_PK
+#undef KX_RR_FLUSH
 #if KX_DISPATCH_TIMERS
     if (pool == 0 && lane == 0)
       for (int k = 0; k < 4; ++k) g_disp_dbg[6 + k] = static_cast<unsigned long long>(acc[k]);
@@ -1940,6 +2196,14 @@ k_dispatch_waiting(QueueDev q, AgentsDev a, InstDev in, const int32_t* __restric
 }
 
 // ---- host wrappers -------------------------------------------------------
+void read_dispatch_trace(unsigned long long* out) {
+  KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_tr, sizeof(unsigned long long) * 128));
+}
+
+void read_dispatch_stages(unsigned long long* out) {
+  KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_st, sizeof(unsigned long long) * 16));
+}
+
 void read_dispatch_debug(unsigned long long* out) {
   KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_dbg, sizeof(unsigned long long) * 16));
 }

@@ -23,8 +23,38 @@ snap = w.snap
 s.upload(snap.agent, snap.prompt, snap.app_start, snap.queue_enter, snap.msg_key, snap.uid)
 
 
+STAGES = ["load_head+loop", "row wait", "fence+row loads", "fix / rr eval+select", "select / rr commit", "staging",
+          "ledger booking", "admit state", "fence+publish", "rr decisions", "exact-path heads"]
+
+
+def trace():
+    if not hasattr(s.lib, "kx_debug_dispatch_trace"):
+        return
+    buf = (C.c_uint64 * 128)()
+    s.lib.kx_debug_dispatch_trace(buf)
+    t = list(buf)
+    if not any(t):
+        return
+    names = ["top", "eval", "flags", "argmin", "staging", "commit", "admit", "publish", "load_head"]
+    for it in range(8):
+        row = t[it * 16: it * 16 + 9]
+        if not all(row):
+            continue
+        d = [row[k] - row[k - 1] for k in range(1, 9)]
+        nxt = t[(it + 1) * 16] - row[8] if it < 7 and t[(it + 1) * 16] else 0
+        print("  step trace cycles: " + " ".join(f"{n} {v}" for n, v in zip(names[1:], d)) + f" | to next top {nxt}")
+
+
 def timers():
+    trace()
     buf = (C.c_uint64 * 16)()
+    if hasattr(s.lib, "kx_debug_dispatch_stages"):
+        s.lib.kx_debug_dispatch_stages(buf)
+        st = list(buf)
+        if any(st):
+            s.lib.kx_debug_dispatch_timers(buf)
+            n = max(1, list(buf)[5])
+            print("  resolver stage cycles per record: " + ", ".join(f"{k} {v / n:.0f}" for k, v in zip(STAGES, st)))
     if hasattr(s.lib, "kx_debug_dispatch_timers"):
         s.lib.kx_debug_dispatch_timers(buf)
         t = list(buf)

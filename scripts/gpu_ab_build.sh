@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 : > gpurun_out/abb.log
 for spec in $VARIANTS; do
   name=${spec%%:*}; flags=${spec#*:}; flags=${flags//,/ }
-  touch paper_2508_06948_b200/csrc/*.cu
+  touch ${TOUCH:-paper_2508_06948_b200/csrc/*.cu}
   make NVFLAGS_EXTRA="$flags" > gpurun_out/abb_build_$name.log 2>&1 || { echo "$name build failed" >> gpurun_out/abb.log; continue; }
   if [[ ${TESTS:-1} == 1 ]]; then
     timeout 300 python -m pytest tests/test_gpu_order.py tests/test_gpu_dispatch.py -q -x > gpurun_out/abb_t_$name.log 2>&1

@@ -9,12 +9,11 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2508_06948_b200 import workload as W  # noqa: E402
 
-per_pool = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
+config = sys.argv[1] if len(sys.argv) > 1 else "C4"
 ticks = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-snap = W.snapshot(n_pools=8, per_pool=per_pool, seed=1)
-insts = W.instances(8, 32)
-live, running, commits = W.preload(insts, seed=7, now=bench.NOW)
-s = bench.make_sched(snap, insts, live, running, commits, 0)
+w = W.build_workload(config, 0, arrivals=1024)
+s = bench.make_sched(w, 0)
+snap = w.snap
 s.upload(snap.agent, snap.prompt, snap.app_start, snap.queue_enter, snap.msg_key, snap.uid)
 buf = (C.c_uint64 * 64)()
 for overlap in (True, False):
@@ -22,7 +21,7 @@ for overlap in (True, False):
     for _ in range(ticks):
         s.restore()
         if overlap:
-            s.tick(bench.NOW)
+            s.tick(w.now)
         else:
             s.order()
     s.synchronize()
