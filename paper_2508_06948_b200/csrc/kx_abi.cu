@@ -2106,6 +2106,12 @@ int kx_debug_dispatch_stages(uint64_t* out16) {
   return guard([&] { kx::read_dispatch_stages(reinterpret_cast<unsigned long long*>(out16)); });
 }
 
+// Diagnostics: decisions taken by the register-resident resolver and heads
+// on the exact path, summed over chain-kernel launches (read, then reset).
+int kx_debug_dispatch_counts(uint64_t* out2, int32_t reset) {
+  return guard([&] { kx::read_dispatch_counts(reinterpret_cast<unsigned long long*>(out2), reset != 0); });
+}
+
 // Diagnostics: clock stamps of 8 register-resolver steps of pool 0 (KX_DISPATCH_TIMERS=3 builds).
 int kx_debug_dispatch_trace(uint64_t* out128) {
   return guard([&] { kx::read_dispatch_trace(reinterpret_cast<unsigned long long*>(out128)); });

@@ -661,6 +661,7 @@ __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __res
 #endif
 __device__ unsigned long long g_disp_dbg[16];
 __device__ unsigned long long g_disp_st[16];
+__device__ unsigned long long g_disp_cnt[2];  // decisions by the register resolver / heads on the exact path (all pools)
 __device__ unsigned long long g_disp_tr[8 * 16];  // KX_DISPATCH_TIMERS=3: clock stamps of 8 rr steps (pool 0)  // KX_DISPATCH_TIMERS=2: per-stage resolver cycles (pool 0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -1284,6 +1285,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       if (p < q_end) KX_LOAD_PK(c_pk, hs);
     }
     int32_t rr_pub = staged;  // records staged but not yet published (rr publishes in batches)
+    uint32_t n_rr = 0, n_exact = 0;
     auto rr_publish = [&]() {
       smem_order();
       __syncwarp();
@@ -1441,6 +1443,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
 #if KX_DISPATCH_TIMERS >= 2
           st_acc[9] += 1;
 #endif
+          ++n_rr;
           continue;
         }
       }
@@ -1448,6 +1451,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
 #if KX_DISPATCH_TIMERS >= 2
       st_acc[10] += 1;
 #endif
+      ++n_exact;
       if (rr) {  // anything unusual: the exact path over the shared ledger
         if (staged != rr_pub) rr_publish();
         KX_RR_FLUSH();
@@ -1747,7 +1751,11 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
     smem_order();
-    if (lane == 0) s_stop = 1;
+    if (lane == 0) {
+      s_stop = 1;
+      if (n_rr) atomicAdd(&g_disp_cnt[0], static_cast<unsigned long long>(n_rr));
+      if (n_exact) atomicAdd(&g_disp_cnt[1], static_cast<unsigned long long>(n_exact));
+    }
     f_rows = nrows;
     f_adm = commits;
 #if KX_DISPATCH_TIMERS >= 2
@@ -2196,6 +2204,14 @@ k_dispatch_waiting(QueueDev q, AgentsDev a, InstDev in, const int32_t* __restric
 }
 
 // ---- host wrappers -------------------------------------------------------
+void read_dispatch_counts(unsigned long long* out, bool reset) {
+  KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_cnt, sizeof(unsigned long long) * 2));
+  if (reset) {
+    const unsigned long long z[2] = {0, 0};
+    KX_CUDA(cudaMemcpyToSymbol(g_disp_cnt, z, sizeof(z)));
+  }
+}
+
 void read_dispatch_trace(unsigned long long* out) {
   KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_tr, sizeof(unsigned long long) * 128));
 }

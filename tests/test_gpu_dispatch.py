@@ -1,6 +1,8 @@
 """K5 on the B200: the reference's dispatch decisions (decision-log rows:
 target, predicted_peak bits, candidate_peaks bits), suspension and ledger
 state, replayed round by round; plus random multi-pool cases vs the oracle."""
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -50,13 +52,14 @@ def test_dispatch_matches_reference_fixture(gpu_lib, name):
             s.on_request_finished(int(iid), int(uid), float(end))
 
 
-def build_pools(rng, n_pools, per_pool, cap=3000.0, max_batch=8):
+def build_pools(rng, n_pools, per_pool, cap=3000.0, max_batch=8, uniform=False):
     inst, ids = [], []
     for p in range(n_pools):
         for j in range(per_pool):
             iid = 1000 - (p * per_pool + j) * 7  # ids decreasing: tie-break by id, not index
+            k = 50.0 if uniform else 40.0 + 10.0 * (j % 2)
             inst.append(kx.InstanceProfile(id=iid, pool=p, capacity_tokens=cap * (0.8 if j % 3 == 2 else 1.0),
-                                           decode_rate=40.0 + 10.0 * (j % 2), max_batch=max_batch))
+                                           decode_rate=k, max_batch=max_batch))
             ids.append(iid)
     return inst
 
@@ -90,9 +93,29 @@ def test_dispatch_multi_pool_matches_oracle(gpu_lib, monkeypatch, mode, n_pools,
                                             max_batch):
     if per_pool > 32 and mode != "overlap":
         pytest.skip("pools of > 32 instances always dispatch after the full order")
+    run_multi_pool(monkeypatch, mode, n_pools, per_pool, n, rounds, ties, max_batch, uniform=False)
+
+
+# Uniform decode rates: pools of <= 32 instances take the register-resident
+# resolver (kx_dispatch.cu, rr); spans longer than its 16 slots (T up to 8 s
+# at 0.5 s slots), overloads, full batches and tie cuts take the exact path.
+@pytest.mark.parametrize("mode", ["overlap", "serial", "short1"])
+@pytest.mark.parametrize("n_pools,per_pool,n,rounds,ties,max_batch",
+                         MULTI_POOL_CASES + [(2, 32, 12000, 3, 0, 64), (4, 16, 8000, 4, 0, 2)])
+def test_dispatch_register_resolver_matches_oracle(gpu_lib, monkeypatch, mode, n_pools, per_pool, n, rounds, ties,
+                                                   max_batch):
+    cnt = (ctypes.c_uint64 * 2)()
+    gpu_lib.kx_debug_dispatch_counts(cnt, 1)
+    run_multi_pool(monkeypatch, mode, n_pools, per_pool, n, rounds, ties, max_batch, uniform=True)
+    gpu_lib.kx_debug_dispatch_counts(cnt, 1)
+    assert cnt[0] > 0, "the register resolver took no decision"
+    assert cnt[1] > 0, "no head took the exact path (long spans / overloads are expected)"
+
+
+def run_multi_pool(monkeypatch, mode, n_pools, per_pool, n, rounds, ties, max_batch, uniform):
     set_mode(monkeypatch, mode)
-    rng = np.random.default_rng(n_pools * 100 + per_pool + max_batch)
-    inst = build_pools(rng, n_pools, per_pool, max_batch=max_batch)
+    rng = np.random.default_rng(n_pools * 100 + per_pool + max_batch + (7 if uniform else 0))
+    inst = build_pools(rng, n_pools, per_pool, max_batch=max_batch, uniform=uniform)
     s = kx.DeviceScheduler(inst, n_pools=n_pools, queue_capacity=n, max_agents=64)
     q, t = random_queue(rng, n, n_agents=30, n_pools=n_pools)
     # prompts up to 400 against capacities 2400-3000: some heads overload
