@@ -497,6 +497,9 @@ int kx_trace_agents(const kx_trace* t, char* names, int64_t* offsets);
 int kx_trace_columns(const kx_trace* t, int64_t* msg, int32_t* agent, int32_t* upstream, double* exec_start,
                      double* exec_end, int64_t* prompt_tokens, int64_t* output_tokens, double* app_start);
 int kx_trace_msg_id(const kx_trace* t, int64_t msg, char* buf, int64_t cap, int64_t* len);
+/* Byte offset and length, in the parsed bytes, of each of msgs[0..k) (the
+ * msg_id strings of WorkflowGraph diagnostics, workflow.cpp:99-108, in bulk). */
+int kx_trace_msg_spans(const kx_trace* t, int64_t k, const int64_t* msgs, int64_t* off, int32_t* len);
 /* write_trace (trace.cpp:44-48) of the parsed records, formatted on the
  * device (format_seconds' "%.9f" exact); out = NULL returns the size. */
 int kx_trace_format(kx_trace* t, char* out, int64_t cap, int64_t* n_out);

@@ -212,6 +212,7 @@ SIGNATURES = {
     "kx_trace_agents": (C.c_int, [_P, _P, _P]),
     "kx_trace_columns": (C.c_int, [_P] + [_P] * 8),
     "kx_trace_msg_id": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "kx_trace_msg_spans": (C.c_int, [_P, C.c_int64, _P, _P, _P]),
     "kx_trace_format": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
     "kx_workflow_reconstruct": (C.c_int, [_P, C.POINTER(kx_workflow_sizes)]),
     "kx_workflow_fetch": (C.c_int, [_P] + [_P] * 10),

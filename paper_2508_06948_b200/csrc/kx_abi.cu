@@ -2112,6 +2112,16 @@ int kx_debug_dispatch_counts(uint64_t* out2, int32_t reset) {
   return guard([&] { kx::read_dispatch_counts(reinterpret_cast<unsigned long long*>(out2), reset != 0); });
 }
 
+// Diagnostics: phase-3 dispatch start / end per pool (globaltimer, KX_DISPATCH_TIMERS builds).
+int kx_debug_dispatch_pool_times(uint64_t* out128) {
+  return guard([&] { kx::read_dispatch_pool_times(reinterpret_cast<unsigned long long*>(out128)); });
+}
+
+// Diagnostics: globaltimer at the end of the last key generation.
+int kx_debug_keys_done(uint64_t* out1) {
+  return guard([&] { kx::read_keys_done(reinterpret_cast<unsigned long long*>(out1)); });
+}
+
 // Diagnostics: clock stamps of 8 register-resolver steps of pool 0 (KX_DISPATCH_TIMERS=3 builds).
 int kx_debug_dispatch_trace(uint64_t* out128) {
   return guard([&] { kx::read_dispatch_trace(reinterpret_cast<unsigned long long*>(out128)); });

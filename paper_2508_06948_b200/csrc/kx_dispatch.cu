@@ -661,7 +661,8 @@ __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __res
 #endif
 __device__ unsigned long long g_disp_dbg[16];
 __device__ unsigned long long g_disp_st[16];
-__device__ unsigned long long g_disp_cnt[2];  // decisions by the register resolver / heads on the exact path (all pools)
+__device__ unsigned long long g_disp_cnt[2];
+__device__ unsigned long long g_disp_pool_t[2 * 64];  // KX_DISPATCH_TIMERS: phase-3 start / end per pool  // decisions by the register resolver / heads on the exact path (all pools)
 __device__ unsigned long long g_disp_tr[8 * 16];  // KX_DISPATCH_TIMERS=3: clock stamps of 8 rr steps (pool 0)  // KX_DISPATCH_TIMERS=2: per-stage resolver cycles (pool 0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -793,6 +794,10 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     g_disp_dbg[0] = gtimer();
     for (int k = 6; k < 14; ++k) g_disp_dbg[k] = 0;
   }
+  // phase-3 prologue stamps (pool 0): start, rings staged, umax, prefix sorted
+  const bool dbg3 = KX_DISPATCH_TIMERS && pool == 0 && threadIdx.x == 0 && ph.phase == 3;
+  if (dbg3) g_disp_st[12] = gtimer();
+  if (KX_DISPATCH_TIMERS && threadIdx.x == 0 && ph.phase == 3 && pool < 64) g_disp_pool_t[pool] = gtimer();
   // phase 3 learns its heads (and the pool size) only once key generation
   // has finished, below
   int64_t pool_n = ph.phase == 3 ? 0 : pool_offsets[pool + 1] - pool_offsets[pool];
@@ -919,6 +924,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     s_kr[r] = li >= 0 ? in.decode_rate[ib + li] : 0.0;
   }
   __syncthreads();
+  if (dbg3) g_disp_st[13] = gtimer();
   // max stored usage over each instance's ledger window (peak's first term)
   for (int r = threadIdx.x; r < kR; r += kChainThreads) {
     const int li = s_li[r];
@@ -968,6 +974,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   constexpr int kRegSlots = 16;  // the configs' spans are <= 16 slots; longer spans take the exact path
   const bool rr = KX_REG_RESOLVER && NI == 1 && k_uniform && ring >= kRegSlots;
 
+  if (dbg3) g_disp_st[14] = gtimer();
   // ---- phase 3: the prefix collected by key generation, sorted here ----
   if (ph.phase == 3) {
     pool_n = ph.pool_counts[pool];
@@ -981,6 +988,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   }
   __syncthreads();
   if (dbg) g_disp_dbg[1] = gtimer();
+  if (dbg3) g_disp_st[15] = gtimer();
 
   // ---- final state (written by the resolver after the round) ----
   int64_t f_rows = 0, f_adm = 0;
@@ -1840,6 +1848,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     }
   }
   if (dbg) g_disp_dbg[3] = gtimer();
+  if (KX_DISPATCH_TIMERS && threadIdx.x == 0 && ph.phase == 3 && pool < 64) g_disp_pool_t[64 + pool] = gtimer();
 }
 
 // ---- single-instance ledger events (host-driven, tiny launches) ----------
@@ -2210,6 +2219,10 @@ void read_dispatch_counts(unsigned long long* out, bool reset) {
     const unsigned long long z[2] = {0, 0};
     KX_CUDA(cudaMemcpyToSymbol(g_disp_cnt, z, sizeof(z)));
   }
+}
+
+void read_dispatch_pool_times(unsigned long long* out) {
+  KX_CUDA(cudaMemcpyFromSymbol(out, g_disp_pool_t, sizeof(unsigned long long) * 128));
 }
 
 void read_dispatch_trace(unsigned long long* out) {

@@ -90,6 +90,7 @@ void configure_dispatch_kernels();
 void read_dispatch_debug(unsigned long long* out);
 void read_dispatch_stages(unsigned long long* out);
 void read_dispatch_trace(unsigned long long* out);
+void read_dispatch_pool_times(unsigned long long* out);
 void read_dispatch_counts(unsigned long long* out, bool reset);
 bool dispatch_can_overlap(int max_inst_per_pool, int ring);
 void launch_dispatch(const QueueDev& q, const AgentsDev& a, const InstDev& in,

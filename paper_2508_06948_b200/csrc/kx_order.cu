@@ -591,9 +591,17 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
     if (s_pool[i]) atomicAdd(&pool_counts[i], s_pool[i]);
 }
 
+// Diagnostics: globaltimer when the pool offsets (the end of key generation)
+// were written, read by the dispatch probe against the dispatch kernel's start.
+__device__ unsigned long long g_keys_done_ns;
+void read_keys_done(unsigned long long* out) { KX_CUDA(cudaMemcpyFromSymbol(out, g_keys_done_ns, sizeof(*out))); }
+
 __global__ void k_pool_offsets(const uint32_t* __restrict__ counts, int n_pools,
                                int64_t* __restrict__ offsets) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_keys_done_ns = t;
     int64_t acc = 0;
     for (int p = 0; p < n_pools; ++p) {
       offsets[p] = acc;

@@ -100,4 +100,6 @@ void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
 // Diagnostics: per-pass radix tile phase sums (KX_SORT_TIMERS builds).
 void read_sort_debug(unsigned long long* out64, bool reset);
 
+void read_keys_done(unsigned long long* out);
+
 }  // namespace kx

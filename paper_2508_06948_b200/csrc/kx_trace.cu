@@ -783,6 +783,70 @@ struct kx_trace {
   }
 };
 
+// Byte spans (offset, length in the parsed bytes) of msg indices, and the
+// msg_id strings themselves gathered into one packed buffer: a handful of
+// transfers however many diagnostics a trace has.
+__global__ void k_msg_spans(int64_t k, const int64_t* __restrict__ msgs, const uint32_t* __restrict__ msg_first,
+                            const int64_t* __restrict__ rec_line, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ len, int64_t* __restrict__ off_out,
+                            int32_t* __restrict__ len_out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const int64_t L = rec_line[msg_first[msgs[i]]];
+  off_out[i] = off[3 * L];
+  len_out[i] = len[3 * L];
+}
+
+__global__ void k_gather_spans(int64_t k, const char* __restrict__ bytes, const int64_t* __restrict__ off,
+                               const int32_t* __restrict__ len, const int64_t* __restrict__ pos,
+                               char* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.y + threadIdx.y;
+  if (i >= k) return;
+  for (int j = threadIdx.x; j < len[i]; j += blockDim.x) out[pos[i] + j] = bytes[off[i] + j];
+}
+
+static void msg_spans_dev(const kx_trace* t, int64_t k, const int64_t* msgs_host, int64_t* doff, int32_t* dlen) {
+  int64_t* dm = nullptr;
+  KX_CUDA(cudaMalloc(&dm, size_t(k) * 8));
+  KX_CUDA(cudaMemcpyAsync(dm, msgs_host, size_t(k) * 8, cudaMemcpyHostToDevice, t->st));
+  k_msg_spans<<<static_cast<unsigned>((k + 255) / 256), 256, 0, t->st>>>(k, dm, t->msg_first_dev, t->rec_line, t->off,
+                                                                       t->len, doff, dlen);
+  KX_CHECK_LAUNCH();
+  KX_CUDA(cudaStreamSynchronize(t->st));
+  KX_CUDA(cudaFree(dm));
+}
+
+static std::vector<std::string> fetch_msg_names(const kx_trace* t, const std::vector<int64_t>& msgs) {
+  const int64_t k = static_cast<int64_t>(msgs.size());
+  std::vector<std::string> out(msgs.size());
+  if (k == 0) return out;
+  int64_t *doff = nullptr, *dpos = nullptr;
+  int32_t* dlen = nullptr;
+  KX_CUDA(cudaMalloc(&doff, size_t(k) * 8));
+  KX_CUDA(cudaMalloc(&dpos, size_t(k) * 8));
+  KX_CUDA(cudaMalloc(&dlen, size_t(k) * 4));
+  msg_spans_dev(t, k, msgs.data(), doff, dlen);
+  std::vector<int32_t> len(static_cast<size_t>(k));
+  KX_CUDA(cudaMemcpy(len.data(), dlen, size_t(k) * 4, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> pos(static_cast<size_t>(k) + 1, 0);
+  for (int64_t i = 0; i < k; ++i) pos[i + 1] = pos[i] + len[i];
+  char* dbuf = nullptr;
+  KX_CUDA(cudaMalloc(&dbuf, size_t(std::max<int64_t>(pos[k], 1))));
+  KX_CUDA(cudaMemcpyAsync(dpos, pos.data(), size_t(k) * 8, cudaMemcpyHostToDevice, t->st));
+  const dim3 blk(32, 8);
+  k_gather_spans<<<static_cast<unsigned>((k + 7) / 8), blk, 0, t->st>>>(k, t->bytes, doff, dlen, dpos, dbuf);
+  KX_CHECK_LAUNCH();
+  std::string packed(static_cast<size_t>(pos[k]), '\0');
+  if (pos[k]) KX_CUDA(cudaMemcpyAsync(packed.data(), dbuf, size_t(pos[k]), cudaMemcpyDeviceToHost, t->st));
+  KX_CUDA(cudaStreamSynchronize(t->st));
+  for (int64_t i = 0; i < k; ++i) out[i] = packed.substr(static_cast<size_t>(pos[i]), static_cast<size_t>(len[i]));
+  KX_CUDA(cudaFree(doff));
+  KX_CUDA(cudaFree(dpos));
+  KX_CUDA(cudaFree(dlen));
+  KX_CUDA(cudaFree(dbuf));
+  return out;
+}
+
 namespace {
 
 unsigned grid_of(int64_t n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
@@ -1166,18 +1230,12 @@ void reconstruct(kx_trace* t) {
   std::map<int64_t, std::string> mname;
   std::vector<uint32_t> idx(nd);
   std::iota(idx.begin(), idx.end(), 0u);
-  for (uint32_t i = 0; i < nd; ++i) {
-    if (mname.count(dm[i])) continue;
-    uint32_t r = 0;
-    KX_CUDA(cudaMemcpy(&r, t->msg_first_dev + dm[i], 4, cudaMemcpyDeviceToHost));
-    int64_t L = 0, off = 0;
-    int32_t len = 0;
-    KX_CUDA(cudaMemcpy(&L, t->rec_line + r, 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(&off, t->off + 3 * L, 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(&len, t->len + 3 * L, 4, cudaMemcpyDeviceToHost));
-    std::string s(static_cast<size_t>(len), '\0');
-    if (len) KX_CUDA(cudaMemcpy(s.data(), t->bytes + off, len, cudaMemcpyDeviceToHost));
-    mname[dm[i]] = s;
+  {
+    std::vector<int64_t> uniq(dm.begin(), dm.end());
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    const std::vector<std::string> names = fetch_msg_names(t, uniq);
+    for (size_t i = 0; i < uniq.size(); ++i) mname[uniq[i]] = names[i];
   }
   std::sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) {
     const std::string& ma = mname[dm[a]];
@@ -1318,6 +1376,25 @@ int kx_trace_msg_id(const kx_trace* t, int64_t msg, char* buf, int64_t cap, int6
   });
 }
 
+int kx_trace_msg_spans(const kx_trace* t, int64_t k, const int64_t* msgs, int64_t* off_out, int32_t* len_out) {
+  return tguard([&] {
+    if (!t || k < 0 || (k && (!msgs || !off_out || !len_out))) throw std::invalid_argument("kx_trace_msg_spans: bad argument");
+    for (int64_t i = 0; i < k; ++i)
+      if (msgs[i] < 0 || msgs[i] >= t->n_msgs) throw std::invalid_argument("kx_trace_msg_spans: bad msg index");
+    if (k == 0) return;
+    KX_CUDA(cudaSetDevice(t->dev));
+    int64_t* doff = nullptr;
+    int32_t* dlen = nullptr;
+    KX_CUDA(cudaMalloc(&doff, size_t(k) * 8));
+    KX_CUDA(cudaMalloc(&dlen, size_t(k) * 4));
+    msg_spans_dev(t, k, msgs, doff, dlen);
+    KX_CUDA(cudaMemcpy(off_out, doff, size_t(k) * 8, cudaMemcpyDeviceToHost));
+    KX_CUDA(cudaMemcpy(len_out, dlen, size_t(k) * 4, cudaMemcpyDeviceToHost));
+    KX_CUDA(cudaFree(doff));
+    KX_CUDA(cudaFree(dlen));
+  });
+}
+
 int kx_trace_format(kx_trace* t, char* out, int64_t cap, int64_t* n_out) {
   return tguard([&] {
     if (!t) throw std::invalid_argument("null trace");
@@ -1395,3 +1472,5 @@ int kx_workflow_fetch(const kx_trace* t, int32_t* edge_from, int32_t* edge_to, u
 }
 
 }  // extern "C"
+
+

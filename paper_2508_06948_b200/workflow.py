@@ -78,6 +78,15 @@ class Trace:
         check(self._lib.kx_trace_msg_id(self._h, i, buf, n.value, C.byref(n)))
         return buf.raw[:n.value].decode()
 
+    def msg_ids(self, msgs) -> list:
+        """msg_id strings of many msg indices (one device gather)."""
+        msgs = np.ascontiguousarray(msgs, dtype=np.int64)
+        off = np.zeros(len(msgs), np.int64)
+        ln = np.zeros(len(msgs), np.int32)
+        check(self._lib.kx_trace_msg_spans(self._h, len(msgs), msgs.ctypes.data, off.ctypes.data, ln.ctypes.data))
+        d = self._data
+        return [d[o:o + n].decode() for o, n in zip(off.tolist(), ln.tolist())]
+
     def format(self) -> bytes:
         """write_trace (trace.cpp:44-48) of the records, formatted on the device."""
         n = C.c_int64()
@@ -110,8 +119,9 @@ class Trace:
             kind = "single" if p + s == 0 else ("parallel" if p >= s else "sequential")
             down = sorted(t for (f, t) in g._edges if f == self.agents[a])
             g._fanouts[self.agents[a]] = FanoutPattern(self.agents[a], down, kind, p, s, z)
-        g._diagnostics = [f"msg {self.msg_id(int(m))}: conflicting entries '{self.agents[e]}' and "
-                          f"'{self.agents[o]}'" for m, e, o in zip(dm, de, do)]
+        ids = self.msg_ids(dm)
+        g._diagnostics = [f"msg {ids[i]}: conflicting entries '{self.agents[e]}' and '{self.agents[o]}'"
+                          for i, (e, o) in enumerate(zip(de, do))]
         g._instances = int(sz.instances)
         return g
 

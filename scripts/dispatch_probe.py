@@ -51,7 +51,20 @@ def timers():
     if hasattr(s.lib, "kx_debug_dispatch_stages"):
         s.lib.kx_debug_dispatch_stages(buf)
         st = list(buf)
-        if any(st):
+        if st[12]:
+            kd = (C.c_uint64 * 1)()
+            s.lib.kx_debug_keys_done(kd)
+            pt = (C.c_uint64 * 128)()
+            s.lib.kx_debug_dispatch_pool_times(pt)
+            npool = len(w.snap.pool_names) if hasattr(w.snap, "pool_names") else w.snap.n_pools
+            starts = [(pt[i] - kd[0]) / 1e3 for i in range(npool)]
+            ends = [(pt[64 + i] - kd[0]) / 1e3 for i in range(npool)]
+            print("  phase-3 per pool, us after keygen: start " + " ".join(f"{x:.1f}" for x in starts) +
+                  " | end " + " ".join(f"{x:.1f}" for x in ends))
+            print(f"  phase-3 prologue us: start after keygen {(st[12] - kd[0]) / 1e3:.2f}, ring staging "
+                  f"{(st[13] - st[12]) / 1e3:.2f}, umax {(st[14] - st[13]) / 1e3:.2f}, prefix sort "
+                  f"{(st[15] - st[14]) / 1e3:.2f}")
+        if any(st[:12]):
             s.lib.kx_debug_dispatch_timers(buf)
             n = max(1, list(buf)[5])
             print("  resolver stage cycles per record: " + ", ".join(f"{k} {v / n:.0f}" for k, v in zip(STAGES, st)))
