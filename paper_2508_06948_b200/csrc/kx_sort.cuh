@@ -37,8 +37,17 @@ constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
+#ifndef KX_STAGE_EARLY
+#define KX_STAGE_EARLY 1
+#endif
+#ifndef KX_LB_SLEEP
+#define KX_LB_SLEEP 64  // ns of back-off when a predecessor has not published
+#endif
+#ifndef KX_HIST_IN_STAGE
+#define KX_HIST_IN_STAGE 0
+#endif
 #ifndef KX_LOOK_BATCH
-#define KX_LOOK_BATCH 8
+#define KX_LOOK_BATCH 4
 #endif
 constexpr int kLookBatch = KX_LOOK_BATCH;
 // Next-digit counting: digits at or above this shift are counted with
@@ -297,6 +306,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     gexcl = c - gcount;
   }
   __syncthreads();
+  uint32_t gexcl_final = 0;
   if (tid < kRadix) {
     uint32_t add = 0, addc = 0;
     for (int w = 0; w < warp; ++w) {
@@ -304,7 +314,25 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
       addc += s_warp_cnt[w];
     }
     sm.digit_start[tid] += add;
-    gexcl = counts_in ? gexcl + addc : global_excl[tid];
+    gexcl_final = counts_in ? gexcl + addc : global_excl[tid];
+  }
+#if KX_STAGE_EARLY
+  // Stage the tile in digit order before the look-back: the predecessors
+  // get the staging time to publish, so fewer polls find an empty flag.
+  // With KX_HIST_IN_STAGE the next pass's digits are counted here too (keys
+  // still in registers) instead of in the write loop.
+  __syncthreads();
+  const int64_t vbase = base + int64_t(warp) * 32 * kSortItems + lane;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t d = digit_of(key[i], shift);
+    const uint32_t pos = sm.digit_start[d] + sm.warp_hist[warp][d] + rank[i];
+    s_keys[pos] = key[i];
+    s_vals[pos] = val[i];
+    if (KX_HIST_IN_STAGE && next_hist) hist_add(sm.next_hist, digit_of(key[i], next_shift), vbase + i * 32 < n);
+  }
+#endif
+  if (tid < kRadix) {
     // Decoupled look-back for digit `tid`, kLookBatch predecessors per
     // round trip: the walk over tiles that have only published their
     // aggregate costs one L2 latency per batch instead of per tile.
@@ -321,23 +349,29 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
         uint32_t v[kLookBatch];
 #pragma unroll
         for (int j = 0; j < kLookBatch; ++j) v[j] = (p - j >= 0) ? uint32_t(lb[(p - j) * kRadix + tid]) : uint32_t(kFlagIncl);
+        bool empty = false;
 #pragma unroll
         for (int j = 0; j < kLookBatch; ++j) {
-          if (done) break;
+          if (done || empty) break;
           const uint32_t flag = v[j] & ~kCountMask;
-          if (flag == 0) break;  // not published yet: reload from here
+          if (flag == 0) {  // not published yet: reload from here
+            empty = true;
+            break;
+          }
           excl += v[j] & kCountMask;
           --p;
           if (flag == kFlagIncl) done = true;
         }
+        if (KX_LB_SLEEP && empty) __nanosleep(KX_LB_SLEEP);
       }
       lb[int64_t(tile) * kRadix + tid] = kFlagIncl | (excl + total);
     }
-    sm.global_base[tid] = int64_t(gexcl) + excl - int64_t(sm.digit_start[tid]);
+    sm.global_base[tid] = int64_t(gexcl_final) + excl - int64_t(sm.digit_start[tid]);
   }
   __syncthreads();
   if (KX_SORT_TIMERS && tid == 0) tt[3] = sort_gclk();
 
+#if !KX_STAGE_EARLY
   // Stage the tile in digit order.
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -347,10 +381,11 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
     s_vals[pos] = val[i];
   }
   __syncthreads();
+#endif
   if (KX_SORT_TIMERS && tid == 0) tt[4] = sort_gclk();
 
   const int64_t valid = (n - base) < kSortTile ? (n - base) : kSortTile;
-  if (next_hist && next_shift >= kNextAggShift) {
+  if (next_hist && !(KX_STAGE_EARLY && KX_HIST_IN_STAGE) && next_shift >= kNextAggShift) {
     // a high digit (often equal across a warp): aggregated increments need a
     // uniform trip count
 #pragma unroll 4
@@ -364,7 +399,7 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
       }
       hist_add(sm.next_hist, digit_of(k, next_shift), ok);
     }
-  } else if (next_hist) {  // a spread digit: plain shared atomics
+  } else if (next_hist && !(KX_STAGE_EARLY && KX_HIST_IN_STAGE)) {  // a spread digit: plain shared atomics
 #pragma unroll 4
     for (int j = tid; j < valid; j += kSortThreads) {
       const K k = s_keys[j];
