@@ -39,7 +39,21 @@ enum kx_status {
   KX_ERR_LIVELOCK = 6   /* reference would spin forever */
 };
 
-enum kx_mem { KX_MEM_HOST = 0, KX_MEM_DEVICE = 1 };
+enum kx_mem {
+  KX_MEM_HOST = 0,
+  KX_MEM_DEVICE = 1,
+  /* kx_queue_upload only: pinned host memory the device can address
+   * (cudaHostAlloc / cudaMallocHost / cudaHostRegister). The columns every
+   * request's key needs (agent, app_start, queue_enter, pure_exec) are
+   * copied; prompt_tokens, kept_tokens, msg_key and uid stay in host memory
+   * and are read in place by the kernels that need them (dispatched heads,
+   * exact-tuple ties, decision rows) -- a few thousand reads per tick instead
+   * of 32 bytes per request over the host link. The caller keeps those arrays
+   * alive and unchanged until the next upload; enqueue, remove_admitted and
+   * graph capture first copy them to the device. Their values are not range
+   * checked up front (the reference does not check them either). */
+  KX_MEM_HOST_MAPPED = 2
+};
 
 /* SchedulerKind (harness.hpp:16) */
 enum kx_scheduler_kind {

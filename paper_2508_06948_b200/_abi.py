@@ -24,6 +24,7 @@ KX_ERR_LIVELOCK = 6
 
 KX_MEM_HOST = 0
 KX_MEM_DEVICE = 1
+KX_MEM_HOST_MAPPED = 2  # kx_queue_upload: pinned host columns read in place (see kairos_b200.h)
 
 SCHED = {"kairos": 0, "fcfs": 1, "topo_depth": 2, "oracle": 3}
 DISPATCH = {"time_slot": 0, "round_robin": 1, "static_threshold": 2}

@@ -52,7 +52,7 @@ __global__ void k_fill_rem(QueueDev q, int64_t n, const double* __restrict__ tab
   }
 }
 
-__global__ void k_validate_queue(QueueDev q, int64_t n, int n_agents, int need_pure,
+__global__ void k_validate_queue(QueueDev q, int64_t n, int n_agents, int need_pure, int check_tokens,
                                  int* __restrict__ err) {
   int e = 0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -62,7 +62,7 @@ __global__ void k_validate_queue(QueueDev q, int64_t n, int n_agents, int need_p
     const double x = q.app_start[i], y = q.queue_enter[i];
     if (x != x || y != y) e |= 2;
     if (need_pure && !(q.pure_exec[i] >= 0.0)) e |= 8;
-    if (q.prompt[i] < 0 || q.kept[i] < 0) e |= 8;
+    if (check_tokens && (q.prompt[i] < 0 || q.kept[i] < 0)) e |= 8;
   }
   if (e) atomicOr(err, e);
 }
@@ -267,6 +267,8 @@ struct kx_sched {
   std::vector<int32_t> pool_begin_host;
 
   QueueDev q{};
+  QueueDev q_dev{};  // the queue blob's own columns (q differs while mapped)
+  bool q_mapped = false;
   AgentsDev a{};
   InstDev in{};
   int32_t* pool_begin = nullptr;
@@ -430,6 +432,8 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
                     at<double>(b, o_qe),     at<uint64_t>(b, o_msg),   at<uint64_t>(b, o_uid),
                     at<int64_t>(b, o_kept),  at<double>(b, o_pure),    at<double>(b, o_rem),
                     at<uint8_t>(b, o_adm)};
+    s->q_dev = s->q;
+    s->q_mapped = false;
   }
   // agent tables
   {
@@ -1398,28 +1402,68 @@ int kx_set_remaining_table(kx_sched* s, uint64_t uid_base, int64_t n, const doub
 
 // Writes n requests at queue positions [at, at + n) (SoA columns), checks
 // them and refreshes the Oracle key column.
+// Copies the columns a mapped upload left in host memory into the queue
+// blob (before anything that rewrites or appends to the queue, or captures
+// its addresses in a graph).
+static void unmap_queue(kx_sched* s) {
+  if (!s->q_mapped) return;
+  const size_t N = static_cast<size_t>(s->n);
+  if (N) {
+    KX_CUDA(cudaMemcpyAsync(s->q_dev.prompt, s->q.prompt, N * 8, cudaMemcpyDefault, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q_dev.msg, s->q.msg, N * 8, cudaMemcpyDefault, s->stream));
+    KX_CUDA(cudaMemcpyAsync(s->q_dev.uid, s->q.uid, N * 8, cudaMemcpyDefault, s->stream));
+    if (s->q.kept != s->q_dev.kept)
+      KX_CUDA(cudaMemcpyAsync(s->q_dev.kept, s->q.kept, N * 8, cudaMemcpyDefault, s->stream));
+  }
+  s->q = s->q_dev;
+  s->q_mapped = false;
+  s->order_valid = false;  // order/dispatch results stay readable only through the copied columns
+  s->dispatch_valid = false;
+}
+
+static void* device_view(const void* host) {
+  void* d = nullptr;
+  KX_CUDA(cudaHostGetDevicePointer(&d, const_cast<void*>(host), 0));
+  return d;
+}
+
 static void queue_write(kx_sched* s, int64_t at, int64_t n, const kx_queue_view* v, int32_t mem, const char* who) {
   require(s && v, "null argument");
   require(n >= 0 && at >= 0 && at + n <= s->cap, "queue size exceeds queue_capacity");
   KX_CUDA(cudaSetDevice(s->device));
+  const bool mapped = mem == KX_MEM_HOST_MAPPED && at == 0;
+  if (at > 0) unmap_queue(s);
+  else if (s->q_mapped) {
+    s->q = s->q_dev;
+    s->q_mapped = false;
+  }
   const size_t N = static_cast<size_t>(n), A = static_cast<size_t>(at);
   if (n > 0) {
     require(v->agent && v->prompt_tokens && v->app_start && v->queue_enter && v->msg_key && v->uid,
             "queue view is missing a required array");
     if (s->dcfg.oracle_expected_time)
       require(v->pure_exec != nullptr, "oracle_expected_time needs pure_exec");
-    const cudaMemcpyKind k = kind_in(mem);
+    const cudaMemcpyKind k = mem == KX_MEM_HOST_MAPPED ? cudaMemcpyHostToDevice : kind_in(mem);
     KX_CUDA(cudaMemcpyAsync(s->q.agent + A, v->agent, N * 4, k, s->stream));
-    KX_CUDA(cudaMemcpyAsync(s->q.prompt + A, v->prompt_tokens, N * 8, k, s->stream));
     KX_CUDA(cudaMemcpyAsync(s->q.app_start + A, v->app_start, N * 8, k, s->stream));
     KX_CUDA(cudaMemcpyAsync(s->q.queue_enter + A, v->queue_enter, N * 8, k, s->stream));
-    KX_CUDA(cudaMemcpyAsync(s->q.msg + A, v->msg_key, N * 8, k, s->stream));
-    KX_CUDA(cudaMemcpyAsync(s->q.uid + A, v->uid, N * 8, k, s->stream));
-    if (v->kept_tokens)
-      KX_CUDA(cudaMemcpyAsync(s->q.kept + A, v->kept_tokens, N * 8, k, s->stream));
-    else
-      KX_CUDA(cudaMemsetAsync(s->q.kept + A, 0, N * 8, s->stream));
     if (v->pure_exec) KX_CUDA(cudaMemcpyAsync(s->q.pure_exec + A, v->pure_exec, N * 8, k, s->stream));
+    if (mapped) {  // read in place by the kernels that need them
+      s->q.prompt = static_cast<int64_t*>(device_view(v->prompt_tokens));
+      s->q.msg = static_cast<uint64_t*>(device_view(v->msg_key));
+      s->q.uid = static_cast<uint64_t*>(device_view(v->uid));
+      if (v->kept_tokens) s->q.kept = static_cast<int64_t*>(device_view(v->kept_tokens));
+      else KX_CUDA(cudaMemsetAsync(s->q.kept, 0, N * 8, s->stream));
+      s->q_mapped = true;
+    } else {
+      KX_CUDA(cudaMemcpyAsync(s->q.prompt + A, v->prompt_tokens, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.msg + A, v->msg_key, N * 8, k, s->stream));
+      KX_CUDA(cudaMemcpyAsync(s->q.uid + A, v->uid, N * 8, k, s->stream));
+      if (v->kept_tokens)
+        KX_CUDA(cudaMemcpyAsync(s->q.kept + A, v->kept_tokens, N * 8, k, s->stream));
+      else
+        KX_CUDA(cudaMemsetAsync(s->q.kept + A, 0, N * 8, s->stream));
+    }
     KX_CUDA(cudaMemsetAsync(s->err_flag, 0, sizeof(int), s->stream));
     QueueDev part = s->q;
     part.agent += A;
@@ -1434,7 +1478,8 @@ static void queue_write(kx_sched* s, int64_t at, int64_t n, const kx_queue_view*
     part.admitted += A;
     const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, int64_t(s->sms) * 8));
     k_validate_queue<<<grid, 256, 0, s->stream>>>(part, n, std::max(s->n_agents, 0),
-                                                  s->dcfg.oracle_expected_time ? 1 : 0, s->err_flag);
+                                                  s->dcfg.oracle_expected_time ? 1 : 0, mapped ? 0 : 1,
+                                                  s->err_flag);
     KX_CHECK_LAUNCH();
   }
   s->n = at + n;
@@ -1467,6 +1512,12 @@ int kx_queue_remove_admitted(kx_sched* s) {
     require(s, "null handle");
     if (!s->dispatch_valid) throw std::logic_error("no dispatch round to apply");
     KX_CUDA(cudaSetDevice(s->device));
+    if (s->q_mapped) {  // the compaction rewrites every column in the queue blob
+      const bool dv = s->dispatch_valid, ov = s->order_valid;
+      unmap_queue(s);
+      s->dispatch_valid = dv;
+      s->order_valid = ov;
+    }
     const int64_t n = s->n;
     if (n == 0) return;
     const int64_t chunks = (n + kCompactChunk - 1) / kCompactChunk;
@@ -2008,6 +2059,12 @@ int kx_graph_capture_begin(kx_sched* s) {
     require(s, "null handle");
     KX_CUDA(cudaSetDevice(s->device));
     if (s->prof.enabled) throw std::logic_error("disable profiling before capturing a graph");
+    if (s->q_mapped) {  // the graph keeps the queue's addresses
+      const bool dv = s->dispatch_valid, ov = s->order_valid;
+      unmap_queue(s);
+      s->dispatch_valid = dv;
+      s->order_valid = ov;
+    }
     if (s->graph_exec) {
       cudaGraphExecDestroy(s->graph_exec);
       s->graph_exec = nullptr;
@@ -2054,6 +2111,7 @@ int kx_graph_launch(kx_sched* s) {
   return guard([&] {
     require(s, "null handle");
     if (!s->graph_exec) throw std::logic_error("no captured graph");
+    if (s->q_mapped) throw std::logic_error("the queue was uploaded mapped since the capture: capture again");
     // The captured kernels carry the queue size and buffer addresses of the
     // capture: a pop or an enqueue that changed the size needs a new capture.
     if (s->n != s->graph_n || s->queue_blob.base != s->graph_queue_base)

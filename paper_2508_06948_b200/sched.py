@@ -123,10 +123,20 @@ class DeviceScheduler:
         return cols, len(cols[0]), _abi.KX_MEM_HOST
 
     def upload(self, agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens=None,
-               pure_exec=None, device: bool = False):
-        """Replace the queue. Host numpy arrays, or torch CUDA tensors with device=True."""
-        cols, n, mem = self._view(agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens,
-                                  pure_exec, device)
+               pure_exec=None, device: bool = False, mapped: bool = False):
+        """Replace the queue. Host numpy arrays, or torch CUDA tensors with device=True, or
+        pinned host torch tensors with mapped=True (KX_MEM_HOST_MAPPED: prompt, kept, msg and
+        uid are read in place; keep the tensors alive and unchanged until the next upload)."""
+        if mapped:
+            cols = [agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens, pure_exec]
+            for c in cols:
+                if c is not None and not c.is_pinned():
+                    raise ValueError("mapped upload needs pinned host tensors")
+            self._mapped_cols = cols  # the device reads them until the next upload
+            n, mem = int(agent.numel()), _abi.KX_MEM_HOST_MAPPED
+        else:
+            cols, n, mem = self._view(agent, prompt_tokens, app_start, queue_enter, msg_key, uid, kept_tokens,
+                                      pure_exec, device)
         v = _abi.kx_queue_view(*[ptr(c) for c in cols])
         check(self.lib.kx_queue_upload(self.h, n, C.byref(v), mem))
         self.n = n
