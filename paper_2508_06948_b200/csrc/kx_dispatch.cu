@@ -673,6 +673,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef KX_REG_RESOLVER
 #define KX_REG_RESOLVER 1
 #endif
+#ifndef KX_RR_MAX_NI
+#define KX_RR_MAX_NI 1  // instances per lane the register resolver takes (2, pools of 33-64: measured slower, local memory)
+#endif
 #ifndef KX_RR_PUBLISH
 #define KX_RR_PUBLISH 16  // rr: records staged per publication (one fence each)
 #endif
@@ -972,7 +975,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   // table is instance-independent): the resolver keeps each instance's usage
   // of the next kRegSlots slots in registers and needs no helper rows.
   constexpr int kRegSlots = 16;  // the configs' spans are <= 16 slots; longer spans take the exact path
-  const bool rr = KX_REG_RESOLVER && NI == 1 && k_uniform && ring >= kRegSlots;
+  const bool rr = KX_REG_RESOLVER && NI <= KX_RR_MAX_NI && k_uniform && ring >= kRegSlots;
 
   if (dbg3) g_disp_st[14] = gtimer();
   // ---- phase 3: the prefix collected by key generation, sorted here ----
@@ -1323,9 +1326,10 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       const int64_t tr_it = p - pos0 - 100;
       (void)tr_it;
       TRACE(0);
-      if constexpr (NI == 1) {
+      if constexpr (NI <= KX_RR_MAX_NI) {
       if (rr && mode == kModeTabPk && tn <= kRegSlots) {
-        // ---- one head, all instances in registers (lane = instance) ----
+        // ---- one head, all instances in registers (lane = instance; rank
+        // lane + 32 s for the NI sub-rows) ----
         // Prefetch the next head (fields + span table): independent of this
         // decision, so its shared-memory latency hides under the evaluation.
         // (raw loads only: in-order issue stalls at the first consumer, which
@@ -1355,78 +1359,101 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         // [cslot, last], peak = max(stored max, max over the span of used + pk);
         // the flags that do not read the ledger first
         const double P = static_cast<double>(prompt);
-        const bool elig = act_[0] && !susp_[0] && !(run_[0] + wait_[0] >= mb_[0]);
-        const uint32_t ovfm = __ballot_sync(0xffffffffu, elig && (first < base_[0] || last >= base_[0] + ring));
-        const uint32_t ovrm = __ballot_sync(0xffffffffu, __dadd_rn(live_[0], P) > cap_[0]);
-        const uint32_t fullm = __ballot_sync(0xffffffffu, nact_[0] >= kActiveCap);
-        // span totals: violations as a slot mask, the max as a tree
-        uint32_t vm = 0;
-        double t[kRegSlots];
+        bool el_[NI];
+        uint32_t ovfm = 0, ovrm[NI], fullm[NI];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const double x = __dadd_rn(ru[0][j], c_pk[j]);
-          vm |= (j < tn && x > cap_[0]) ? (1u << j) : 0u;
-          t[j] = j < tn ? x : 0.0;
+        for (int s = 0; s < NI; ++s) {
+          el_[s] = act_[s] && !susp_[s] && !(run_[s] + wait_[s] >= mb_[s]);
+          ovfm |= __ballot_sync(0xffffffffu, el_[s] && (first < base_[s] || last >= base_[s] + ring));
+          ovrm[s] = __ballot_sync(0xffffffffu, __dadd_rn(live_[s], P) > cap_[s]);
+          fullm[s] = __ballot_sync(0xffffffffu, nact_[s] >= kActiveCap);
         }
-        if (tn > 8) {
+        // span totals: violations as a slot mask, the max as a tree
+        uint64_t key[NI], peak[NI], lmin = ~0ull;
+        uint32_t vm[NI];
 #pragma unroll
-          for (int j = 8; j < kRegSlots; ++j) {
-            const double x = __dadd_rn(ru[0][j], c_pk[j]);
-            vm |= (j < tn && x > cap_[0]) ? (1u << j) : 0u;
+        for (int s = 0; s < NI; ++s) {
+          uint32_t m = 0;
+          double t[kRegSlots];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double x = __dadd_rn(ru[s][j], c_pk[j]);
+            m |= (j < tn && x > cap_[s]) ? (1u << j) : 0u;
             t[j] = j < tn ? x : 0.0;
           }
+          if (tn > 8) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) t[j] = t[j + 8] > t[j] ? t[j + 8] : t[j];
+            for (int j = 8; j < kRegSlots; ++j) {
+              const double x = __dadd_rn(ru[s][j], c_pk[j]);
+              m |= (j < tn && x > cap_[s]) ? (1u << j) : 0u;
+              t[j] = j < tn ? x : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[j] = t[j + 8] > t[j] ? t[j + 8] : t[j];
+          }
+#pragma unroll
+          for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+            for (int j = 0; j < w; ++j) t[j] = t[j + w] > t[j] ? t[j + w] : t[j];
+          const uint64_t sm = nonneg_bits(t[0]);
+          vm[s] = m;
+          peak[s] = umax_[s] > sm ? umax_[s] : sm;
+          key[s] = (el_[s] && m == 0) ? peak[s] : ~0ull;
+          lmin = key[s] < lmin ? key[s] : lmin;
         }
-#pragma unroll
-        for (int w = 4; w >= 1; w >>= 1)
-#pragma unroll
-          for (int j = 0; j < w; ++j) t[j] = t[j + w] > t[j] ? t[j + w] : t[j];
-        const uint64_t sm = nonneg_bits(t[0]);
-        const uint64_t peak = umax_[0] > sm ? umax_[0] : sm;
-        const uint64_t key = (elig && vm == 0) ? peak : ~0ull;
-        // this head's candidate peak (dispatcher.cpp:143-147), staged below
-        const double cval = !elig ? -1.0
-                            : vm == 0 ? from_ordered_bits(peak)
-                                      : __dsub_rn(-static_cast<double>(cslot + __ffs(vm) - 1), 1.0);
         TRACE(2);
         // select_instance: min (peak, InstanceId rank) over the fitting instances
-        const uint64_t kmin = warp_min_u64(key);
-        const uint32_t wb = __ballot_sync(0xffffffffu, key == kmin);
-        const int bl = wb ? __ffs(wb) - 1 : -1;
-        const bool wovr = bl >= 0 && ((ovrm >> bl) & 1u);
-        const bool wfull = bl >= 0 && ((fullm >> bl) & 1u);
+        const uint64_t kmin = warp_min_u64(lmin);
+        int bl = -1;
+        bool wovr = false, wfull = false;
+#pragma unroll
+        for (int s = NI - 1; s >= 0; --s) {
+          const uint32_t wb = __ballot_sync(0xffffffffu, key[s] == kmin);
+          if (wb) {
+            bl = 32 * s + __ffs(wb) - 1;
+            wovr = (ovrm[s] >> (bl & 31)) & 1u;
+            wfull = (fullm[s] >> (bl & 31)) & 1u;
+          }
+        }
         STAMP(3);
         TRACE(3);
         if (ovfm == 0 && kmin != ~0ull && !wovr && !wfull) {
-          // stage the decision record
+          // stage the decision record (dispatcher.cpp:143-147)
           if ((staged & (kStage / 2 - 1)) == 0) {
             if (staged != rr_pub) rr_publish();
             while (staged - s_flushed > kStage / 2) {
             }
           }
           const int sl = staged & (kStage - 1);
-          st_cand[sl * kR + lane] = cval;
+#pragma unroll
+          for (int s = 0; s < NI; ++s)
+            st_cand[sl * kR + lane + 32 * s] =
+                !el_[s] ? -1.0
+                        : vm[s] == 0 ? from_ordered_bits(peak[s])
+                                     : __dsub_rn(-static_cast<double>(cslot + __ffs(vm[s]) - 1), 1.0);
           if (lane == 0) st_meta[sl] = (static_cast<uint32_t>(p - pos0) << 9) | 256u | static_cast<uint32_t>(bl + 1);
           ++staged;
           ++nrows;
           TRACE(4);
           // Dispatcher::commit + admit (engine.cpp:298-319) in the target's lane
-          const bool me = lane == bl;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ru[0][j] = (me && j < tn) ? __dadd_rn(ru[0][j], c_pk[j]) : ru[0][j];
-          if (tn > 8) {
+          for (int s = 0; s < NI; ++s) {
+            const bool me = (bl >> 5) == s && lane == (bl & 31);
 #pragma unroll
-            for (int j = 8; j < kRegSlots; ++j) ru[0][j] = (me && j < tn) ? __dadd_rn(ru[0][j], c_pk[j]) : ru[0][j];
+            for (int j = 0; j < 8; ++j) ru[s][j] = (me && j < tn) ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
+            if (tn > 8) {
+#pragma unroll
+              for (int j = 8; j < kRegSlots; ++j) ru[s][j] = (me && j < tn) ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
+            }
+            rbook[s] |= me ? (1u << tn) - 1u : 0u;
+            live_[s] = me ? __dadd_rn(live_[s], static_cast<double>(prompt + kept)) : live_[s];
+            run_[s] += me ? 1 : 0;
+            umax_[s] = me ? kmin : umax_[s];
+            hi_[s] = (me && last > hi_[s]) ? last : hi_[s];
+            lm_[s] = me ? commits : lm_[s];
+            nact_[s] += (me && nact_[s] < kActiveCap) ? 1 : 0;
           }
           TRACE(5);
-          rbook[0] |= me ? (1u << tn) - 1u : 0u;
-          live_[0] = me ? __dadd_rn(live_[0], static_cast<double>(prompt + kept)) : live_[0];
-          run_[0] += me ? 1 : 0;
-          umax_[0] = me ? kmin : umax_[0];
-          hi_[0] = (me && last > hi_[0]) ? last : hi_[0];
-          lm_[0] = me ? commits : lm_[0];
-          nact_[0] += (me && nact_[0] < kActiveCap) ? 1 : 0;
           ++commits;
           retries = 0;
           TRACE(6);
