@@ -14,6 +14,8 @@
 // adjacent after the sort and are re-sorted by the exact tuple
 // (ordered-bits of the doubles, msg key, uid, queue index) in K4.
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <vector>
 #include <stdint.h>
 
 #include <algorithm>
@@ -949,6 +951,15 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
   KX_CHECK_LAUNCH();
   if (hooks && hooks->after_keys) hooks->after_keys();  // compact keys + histograms ready
+  if (const char* dump = getenv("KX_DUMP_KEYS")) {  // diagnostics: the compact keys, raw u32
+    std::vector<uint32_t> hk(static_cast<size_t>(n));
+    KX_CUDA(cudaMemcpyAsync(hk.data(), ws.keys[0], size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+    KX_CUDA(cudaStreamSynchronize(st));
+    if (FILE* f = fopen(dump, "wb")) {
+      fwrite(hk.data(), 4, hk.size(), f);
+      fclose(f);
+    }
+  }
 
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   const size_t smem = sort_dyn_smem<uint32_t>();
