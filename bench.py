@@ -89,17 +89,51 @@ def tie_elements(snap) -> int:
 
 
 class Clocks:
-    """nvidia-smi sampling around the timed region (B200_PROFILING.md): started
-    before the warm-up, 50 ms period, and only the samples whose timestamp falls
-    inside the timed region are summarised (the nearest one if the region is
-    shorter than the period)."""
+    """SM clock and throttle reasons sampled during the timed region
+    (B200_PROFILING.md's clocks line): an NVML polling thread (every 2 ms, so
+    even a region of a few milliseconds holds samples) started before the
+    warm-up; only the samples inside the marked region are summarised (the
+    nearest one if the region is shorter than a period). Falls back to
+    `nvidia-smi -lms 50` when NVML is unavailable."""
+
+    REASONS = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80)]
 
     def __init__(self, index: int):
+        import threading
+        self.t0 = self.t1 = None
+        self.rows = []  # (time, sm_mhz, max_mhz, reason bits)
+        self.p = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((time.time(), float(sm), float(mx), int(rs)))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+            self.nvml = True
+        except Exception:
+            self.nvml = False
+            self.th = None
+            self._start_smi(index)
+
+    def _start_smi(self, index):
         self.path = Path("/tmp") / f"kx_clocks_{os.getpid()}.csv"
         q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        self.t0 = self.t1 = None
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
@@ -114,9 +148,7 @@ class Clocks:
         else:
             self.t1 = time.time()
 
-    def stop(self):
-        if self.p is None:
-            return None
+    def _smi_rows(self):
         time.sleep(0.15)  # let the sample after the region land
         self.p.terminate()
         try:
@@ -126,28 +158,41 @@ class Clocks:
         self.f.close()
         import datetime
         rows = []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        bits = dict(self.REASONS)
         for r in self.path.read_text().strip().splitlines():
             c = [x.strip() for x in r.split(",")]
             if len(c) < 10:
                 continue
             try:
                 ts = datetime.datetime.strptime(c[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                sm, mx = float(c[2]), float(c[3])
             except ValueError:
                 continue
-            rows.append((ts, c))
+            rb = sum(bits[n] for n, v in zip(names, c[6:10]) if v == "Active")
+            rows.append((ts, sm, mx, rb))
+        return rows
+
+    def stop(self):
+        if self.nvml:
+            time.sleep(0.01)
+            self._stop.set()
+            self.th.join(timeout=1)
+            rows = list(self.rows)
+        elif self.p is not None:
+            rows = self._smi_rows()
+        else:
+            return None
         if not rows:
             return None
         t0 = self.t0 or rows[0][0]
         t1 = self.t1 or rows[-1][0]
-        inside = [c for ts, c in rows if t0 <= ts <= t1]
+        inside = [r for r in rows if t0 <= r[0] <= t1]
         if not inside:  # region shorter than the period: nearest sample
-            inside = [min(rows, key=lambda r: abs(r[0] - (t0 + t1) / 2))[1]]
-        sm = [float(c[2]) for c in inside if c[2].replace(".", "").isdigit()]
-        mx = [float(c[3]) for c in inside if c[3].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for c in inside for n, v in zip(names, c[6:10]) if v == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(inside)}
+            inside = [min(rows, key=lambda r: abs(r[0] - (t0 + t1) / 2))]
+        reasons = sorted({n for r in inside for n, b in self.REASONS if r[3] & b})
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": reasons, "samples": len(inside), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def config_dict(w, ws):
@@ -477,7 +522,7 @@ class RefPools:
     """The reference's data structures (Dispatcher with pre-loaded ledgers,
     PendingRequest queue, policy table) for `pools` pools of the workload."""
 
-    def __init__(self, L, w, pools):
+    def __init__(self, L, w, pools, max_per_pool=None):
         self.L = L
         snap, insts = w.snap, w.insts
         names = [n.encode() for n in snap.agent_names]
@@ -507,7 +552,9 @@ class RefPools:
             wt = np.zeros(len(ids), np.int32)
             self._keep += [lv, rn, wt]
             L.kxref_pool_set_live(h, lv.ctypes.data, rn.ctypes.data, wt.ctypes.data)
-            m = snap.agent_pool[snap.agent] == p
+            m = np.flatnonzero(snap.agent_pool[snap.agent] == p)
+            if max_per_pool is not None:
+                m = m[:max_per_pool]  # a prefix of the pool's queue (bounded reference sample)
             cols = [np.ascontiguousarray(x[m]) for x in (snap.agent, snap.prompt, snap.app_start,
                                                          snap.queue_enter, snap.msg_counter, snap.uid)]
             L.kxref_pool_set_queue(h, len(cols[0]), *[c.ctypes.data for c in cols], C.cast(self.cnames, C.c_void_p))
@@ -620,22 +667,29 @@ def run_reference(args):
     threads = min(P, ncpu)
     first = ref.tick(threads, w.now)  # warm-up 1, also sizes the sample
     per_round = first
-    k = P
+    m = None
     if first * (args.steps + args.warmup) > REF_BUDGET_S:
-        # bounded sample: fewer pools per step (each pool keeps its full queue)
-        rounds = -(-P // threads)
-        per_pool_round = first / rounds
-        k = max(1, min(P, int(REF_BUDGET_S / (args.steps + args.warmup) / per_pool_round) * threads))
-    if k < P:
-        ref.close()
-        ref = RefPools(L, w, list(range(k)))
-        threads = min(k, ncpu)
+        # bounded sample: every pool keeps its instances and ledgers, each
+        # step ticks a prefix of every pool's queue (the tick's sort is
+        # n log n, so a shorter queue is slightly faster per request)
+        per_pool = ref.n // P
+        m = per_pool
+        for _ in range(4):  # the tick is not linear in the queue length: re-measure and shrink
+            m = max(10_000, int(m * REF_BUDGET_S / ((args.steps + args.warmup) * first)))
+            ref.close()
+            ref = RefPools(L, w, list(range(P)), max_per_pool=m)
+            first = ref.tick(threads, w.now)
+            if first * (args.steps + args.warmup) <= REF_BUDGET_S or m == 10_000:
+                break
     for _ in range(max(0, args.warmup - 1)):
         ref.tick(threads, w.now)
     times = [ref.tick(threads, w.now) for _ in range(args.steps)]
     ms = 1e3 * sum(times) / len(times)
     value = ref.n / (ms / 1e3)
-    sample = (f"{k} of {P} pool(s) per step ({ref.n} requests), {threads} host threads (one pool per "
+    k = P
+    sample = (f"{k} of {P} pool(s) per step ({ref.n} requests"
+              + (f": the first {m} of each pool's queue" if m else "") +
+              f"), {threads} host threads (one pool per "
               f"thread, the reference's one-Simulator-per-thread model, harness.cpp:189-206): reference "
               f"comparator std::sort (harness.cpp:92-100) + reference Dispatcher over the dispatched "
               f"prefix + gc. The prefix walk replaces the reference's O(N) best_index scan per placement "
