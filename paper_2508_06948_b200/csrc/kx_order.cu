@@ -974,10 +974,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
       const uint32_t* vin = p == 0 ? nullptr : ws.vals[cur];
       uint32_t* nh = p + 1 < passes ? ws.hist + (p + 1) * kRadix : nullptr;
       const unsigned g = static_cast<unsigned>(tiles);
-      if (v == 3)
-        k_onesweep_pass<uint32_t, 3><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
-      else if (v == 1)
+      if (v == 1)
         k_onesweep_pass<uint32_t, 1><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
             ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else if (v == 2)
@@ -1065,11 +1062,9 @@ void configure_sort_kernels() {
   preload(k_onesweep_pass<uint32_t, 0>);
   preload(k_onesweep_pass<uint32_t, 1>);
   preload(k_onesweep_pass<uint32_t, 2>);
-  preload(k_onesweep_pass<uint32_t, 3>);
   KX_CUDA(cudaFuncSetAttribute(k_spec_bound, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sizeof(uint32_t) * kSpecMax)));
-  for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>,
-                 k_onesweep_pass<uint32_t, 3>})
+  for (auto f : {k_onesweep_pass<uint32_t, 0>, k_onesweep_pass<uint32_t, 1>, k_onesweep_pass<uint32_t, 2>})
     KX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(sort_dyn_smem<uint32_t>())));
 }

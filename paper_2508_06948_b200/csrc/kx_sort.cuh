@@ -136,7 +136,6 @@ __global__ void k_scan_hist(uint32_t* __restrict__ hist, int passes);
 template <typename K>
 struct SortSmem {
   uint32_t warp_hist[kSortThreads / 32][kRadix];
-  uint32_t peer_mask[kSortThreads / 32][kRadix];  // kRank 3: lanes holding each digit
   uint32_t next_hist[kRadix];                      // next pass's digit counts (this tile)
   uint32_t digit_start[kRadix];
   int64_t global_base[kRadix];
@@ -155,11 +154,10 @@ constexpr size_t sort_dyn_smem() {
 // writes (the next pass's histogram, one read of the keys saved).
 // kRank selects the warp ranking: 0 = MATCH.ANY peers, every peer reads the
 // running count; 1 = eight-ballot peers, same update; 2 = MATCH.ANY peers,
-// the leader reads and broadcasts the count; 3 = peers from a shared-memory
-// atomicOr mask per (warp, digit), the leader reads/bumps the count and
-// clears the mask. MATCH.ANY issues at a small fraction of the shared-memory
-// atomic rate on sm_100 (scripts/micro/pass_probe.cu: a tile's ranking takes
-// ~6 us with MATCH, ~3 us with the mask), so 3 wins on spread digits.
+// the leader reads and broadcasts the count. MATCH.ANY costs ~2 SM-cycles per
+// distinct digit in the warp (scripts/micro/match_probe.cu), the ballots a
+// fixed ~25: MATCH wins on the clustered C4 digits, the ballots on the top
+// digit (few distinct values with the class bits); see kSortRankDefault.
 #ifndef KX_SORT_MINB
 #define KX_SORT_MINB 4  // 32-bit keys: 4 blocks per SM caps registers at 64 (unbounded, ptxas takes 119)
 #endif
@@ -188,8 +186,6 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
   if (KX_SORT_TIMERS && tid == 0) tt[0] = sort_gclk();
   if (tid == 0) sm.tile_id = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
-  if (kRank == 3)
-    for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&sm.peer_mask[0][0])[i] = 0;
   if (next_hist)
     for (int i = tid; i < kRadix; i += kSortThreads) sm.next_hist[i] = 0;
   __syncthreads();
@@ -227,28 +223,8 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t d = digit_of(key[i], shift);
-    uint32_t peers;
-    if (kRank == 3) {
-      uint32_t* pm = sm.peer_mask[warp];
-      atomicOr(&pm[d], 1u << lane);
-      __syncwarp();
-      peers = pm[d];
-      __syncwarp();
-    } else {
-      peers = kRank == 1 ? warp_match8(d) : __match_any_sync(0xffffffffu, d);
-    }
-    if (kRank == 3) {
-      const int leader = __ffs(peers) - 1;
-      uint32_t old = 0;
-      if (lane == leader) {
-        old = wh[d];
-        wh[d] = old + __popc(peers);
-        sm.peer_mask[warp][d] = 0;
-      }
-      old = __shfl_sync(0xffffffffu, old, leader);
-      __syncwarp();
-      rank[i] = old + __popc(peers & lanemask_lt());
-    } else if (kRank == 2) {
+    const uint32_t peers = kRank == 1 ? warp_match8(d) : __match_any_sync(0xffffffffu, d);
+    if (kRank == 2) {
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (lane == leader) {
