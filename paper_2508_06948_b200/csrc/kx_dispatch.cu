@@ -1073,9 +1073,13 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         const double te = __dadd_rn(now, Th);
         const double tee = __dsub_rn(te, kTimeEpsilon);
         double* tab = stab + (hb + hh) * kDtSlots;
-        for (int j = lane; j < tn; j += 32) {
-          const double dt = slot_dt(now, t0e, te, tee, cslot + j, L);
-          tab[j] = hm == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
+        // a pk table is zero-padded to the register resolver's window: its
+        // span evaluation and commit then need no per-slot span test
+        // (usage + 0 is the usage, never above the instance's stored maximum)
+        const int tw = hm == kModeTabPk && tn < kRegSlots ? kRegSlots : tn;
+        for (int j = lane; j < tw; j += 32) {
+          const double dt = j < tn ? slot_dt(now, t0e, te, tee, cslot + j, L) : 0.0;
+          tab[j] = j >= tn ? 0.0 : hm == kModeTabPk ? pk_of(Ph, k0, dt) : dt;
         }
       }
       __threadfence_block();
@@ -1360,33 +1364,33 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         // the flags that do not read the ledger first
         const double P = static_cast<double>(prompt);
         bool el_[NI];
-        uint32_t ovfm = 0, ovrm[NI], fullm[NI];
+        bool ovf_any = false;
+        uint32_t badm[NI];  // overload (engine.cpp:254-258) or a full active table, per lane
 #pragma unroll
         for (int s = 0; s < NI; ++s) {
           el_[s] = act_[s] && !susp_[s] && !(run_[s] + wait_[s] >= mb_[s]);
-          ovfm |= __ballot_sync(0xffffffffu, el_[s] && (first < base_[s] || last >= base_[s] + ring));
-          ovrm[s] = __ballot_sync(0xffffffffu, __dadd_rn(live_[s], P) > cap_[s]);
-          fullm[s] = __ballot_sync(0xffffffffu, nact_[s] >= kActiveCap);
+          ovf_any = ovf_any || __any_sync(0xffffffffu, el_[s] && (first < base_[s] || last >= base_[s] + ring));
+          badm[s] = __ballot_sync(0xffffffffu, __dadd_rn(live_[s], P) > cap_[s] || nact_[s] >= kActiveCap);
         }
         // span totals: violations as a slot mask, the max as a tree
         uint64_t key[NI], peak[NI], lmin = ~0ull;
         uint32_t vm[NI];
 #pragma unroll
         for (int s = 0; s < NI; ++s) {
+          // (the table is zero past the span: those slots add nothing, and
+          // their violation bits are masked off below)
           uint32_t m = 0;
           double t[kRegSlots];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const double x = __dadd_rn(ru[s][j], c_pk[j]);
-            m |= (j < tn && x > cap_[s]) ? (1u << j) : 0u;
-            t[j] = j < tn ? x : 0.0;
+            t[j] = __dadd_rn(ru[s][j], c_pk[j]);
+            m |= t[j] > cap_[s] ? (1u << j) : 0u;
           }
           if (tn > 8) {
 #pragma unroll
             for (int j = 8; j < kRegSlots; ++j) {
-              const double x = __dadd_rn(ru[s][j], c_pk[j]);
-              m |= (j < tn && x > cap_[s]) ? (1u << j) : 0u;
-              t[j] = j < tn ? x : 0.0;
+              t[j] = __dadd_rn(ru[s][j], c_pk[j]);
+              m |= t[j] > cap_[s] ? (1u << j) : 0u;
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) t[j] = t[j + 8] > t[j] ? t[j + 8] : t[j];
@@ -1395,6 +1399,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           for (int w = 4; w >= 1; w >>= 1)
 #pragma unroll
             for (int j = 0; j < w; ++j) t[j] = t[j + w] > t[j] ? t[j + w] : t[j];
+          m &= tn >= 32 ? 0xffffffffu : (1u << tn) - 1u;
           const uint64_t sm = nonneg_bits(t[0]);
           vm[s] = m;
           peak[s] = umax_[s] > sm ? umax_[s] : sm;
@@ -1405,19 +1410,18 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         // select_instance: min (peak, InstanceId rank) over the fitting instances
         const uint64_t kmin = warp_min_u64(lmin);
         int bl = -1;
-        bool wovr = false, wfull = false;
+        bool wbad = false;
 #pragma unroll
         for (int s = NI - 1; s >= 0; --s) {
           const uint32_t wb = __ballot_sync(0xffffffffu, key[s] == kmin);
           if (wb) {
             bl = 32 * s + __ffs(wb) - 1;
-            wovr = (ovrm[s] >> (bl & 31)) & 1u;
-            wfull = (fullm[s] >> (bl & 31)) & 1u;
+            wbad = (badm[s] >> (bl & 31)) & 1u;
           }
         }
         STAMP(3);
         TRACE(3);
-        if (ovfm == 0 && kmin != ~0ull && !wovr && !wfull) {
+        if (!ovf_any && kmin != ~0ull && !wbad) {
           // stage the decision record (dispatcher.cpp:143-147)
           if ((staged & (kStage / 2 - 1)) == 0) {
             if (staged != rr_pub) rr_publish();
@@ -1440,10 +1444,10 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           for (int s = 0; s < NI; ++s) {
             const bool me = (bl >> 5) == s && lane == (bl & 31);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ru[s][j] = (me && j < tn) ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
+            for (int j = 0; j < 8; ++j) ru[s][j] = me ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
             if (tn > 8) {
 #pragma unroll
-              for (int j = 8; j < kRegSlots; ++j) ru[s][j] = (me && j < tn) ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
+              for (int j = 8; j < kRegSlots; ++j) ru[s][j] = me ? __dadd_rn(ru[s][j], c_pk[j]) : ru[s][j];
             }
             rbook[s] |= me ? (1u << tn) - 1u : 0u;
             live_[s] = me ? __dadd_rn(live_[s], static_cast<double>(prompt + kept)) : live_[s];
