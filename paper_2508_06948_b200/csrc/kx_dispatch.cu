@@ -673,6 +673,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef KX_REG_RESOLVER
 #define KX_REG_RESOLVER 1
 #endif
+#ifndef KX_REG_RESOLVER2
+#define KX_REG_RESOLVER2 1
+#endif
 #ifndef KX_RR_MAX_NI
 #define KX_RR_MAX_NI 1  // instances per lane the register resolver takes (2, pools of 33-64: measured slower, local memory)
 #endif
@@ -697,6 +700,7 @@ constexpr int kResolverWarp = kChainThreads / 32 - 1;
 __host__ __device__ constexpr int role_warp(int h) { return h + h / 3; }  // skips wid % 4 == 3
 constexpr int kLoaderWarp = role_warp(kHelpers);
 constexpr int kFlushWarp = role_warp(kHelpers + 1);
+constexpr int kRR2Warp = role_warp(kHelpers - 1);  // a helper slot (helpers idle under the register resolvers)
 constexpr int kStage = 32;                   // staged decision records
 constexpr int kRowRing = 16;                 // helper rows in flight
 static_assert(kFlushWarp < kResolverWarp && kResolverWarp % 4 == 3, "warp roles");
@@ -976,6 +980,9 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   // of the next kRegSlots slots in registers and needs no helper rows.
   constexpr int kRegSlots = 16;  // the configs' spans are <= 16 slots; longer spans take the exact path
   const bool rr = KX_REG_RESOLVER && NI <= KX_RR_MAX_NI && k_uniform && ring >= kRegSlots;
+  // Pools of 33-64 instances: two resolver warps, 32 instances each in
+  // registers, one exchange of their warp minima per placement (rr2).
+  const bool rr2 = KX_REG_RESOLVER2 && NI == 2 && k_uniform && ring >= kRegSlots;
 
   if (dbg3) g_disp_st[14] = gtimer();
   // ---- phase 3: the prefix collected by key generation, sorted here ----
@@ -1102,7 +1109,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
           }
         }
     }
-  } else if (warp < kLoaderWarp && warp % 4 != 3 && !rr) {
+  } else if (warp < kLoaderWarp && warp % 4 != 3 && !rr && !rr2) {
     // ---- helpers: the row of head j, (first violating span slot, span max
     //      of used + pk) per instance, against a snapshot of commit count v ----
     const int h = warp - warp / 4;  // helper index (inverse of role_warp)
@@ -1222,8 +1229,9 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         if (s_staged == f) break;
       }
     }
-  } else if (warp == kResolverWarp) {
+  } else if (warp == kResolverWarp || (rr2 && warp == kRR2Warp)) {
     // ---- resolver ----
+    const int wsel = warp == kResolverWarp ? 0 : 1;  // rr2: the 32 ranks this warp owns
     int64_t p = pos0;
     int64_t nrows = 0;
     int32_t commits = 0, staged = 0;
@@ -1325,7 +1333,206 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
 #else
 #define TRACE(k) do { } while (0)
 #endif
-    while (p < q_end) {
+    // ---- rr2: two resolver warps (pools of 33-64 instances) ----
+    if constexpr (NI == 2) {
+      if (rr2) {
+        __shared__ uint64_t s_xk[2][2];
+        __shared__ int32_t s_xb[2][2];
+        __shared__ uint32_t s_xf[2][2];
+        __shared__ double s_hl[32];
+        __shared__ uint64_t s_hu[32];
+        __shared__ int64_t s_hh[32];
+        __shared__ int32_t s_hr[32], s_hm[32], s_hn[32], s_hs[32];
+        double rw[kRegSlots], cpk[kRegSlots];
+        uint32_t rbw = 0;
+#pragma unroll
+        for (int j = 0; j < kRegSlots; ++j) rw[j] = su[((cslot + j) & rmask) * kRW + lane + 32 * wsel];
+        // this warp's lane state (compile-time selects: no dynamic register indexing)
+        const bool act_w = wsel ? act_[1] : act_[0];
+        const int mb_w = wsel ? mb_[1] : mb_[0], wait_w = wsel ? wait_[1] : wait_[0];
+        const double cap_w = wsel ? cap_[1] : cap_[0];
+        const int64_t base_w = wsel ? base_[1] : base_[0];
+        bool susp_w = wsel ? susp_[1] : susp_[0];
+        int32_t run_w = wsel ? run_[1] : run_[0], lm_w = wsel ? lm_[1] : lm_[0], nact_w = wsel ? nact_[1] : nact_[0];
+        double live_w = wsel ? live_[1] : live_[0];
+        uint64_t umax_w = wsel ? umax_[1] : umax_[0];
+        int64_t hi_w = wsel ? hi_[1] : hi_[0];
+        if (p < q_end) KX_LOAD_PK(cpk, hs);
+        int par = 0;
+        int32_t done_staged = staged;  // records whose halves both warps have written
+        auto publish_done = [&]() {  // (first warp only)
+          smem_order();
+          __syncwarp();
+          if (lane == 0) {
+            s_staged = done_staged;
+            s_cur = p;
+          }
+          rr_pub = done_staged;
+        };
+        while (p < q_end && mode == kModeTabPk && tn <= kRegSlots) {
+          const bool has_next = p + 1 < q_end;
+          if (has_next && p + 1 >= known_loaded) {
+            if (wsel == 0 && done_staged != rr_pub) publish_done();
+            while ((known_loaded = s_loaded) <= p + 1) {
+            }
+            smem_order();
+          }
+          const int n_hs = static_cast<int>((p + 1 - pos0) & (kHR - 1));
+          const int n_mode = h_mode[n_hs];
+          const int64_t n_first = h_first[n_hs];
+          const int64_t n_last = h_last[n_hs];
+          const int64_t n_prompt = h_prompt[n_hs];
+          const int64_t n_kept = h_kept[n_hs];
+          double n_pk[kRegSlots];
+#pragma unroll
+          for (int j = 0; j < kRegSlots; j += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(stab + n_hs * kDtSlots + j);
+            n_pk[j] = v2.x;
+            n_pk[j + 1] = v2.y;
+          }
+          // this warp's 32 entries (as the one-warp register resolver)
+          const double P = static_cast<double>(prompt);
+          const bool el = act_w && !susp_w && !(run_w + wait_w >= mb_w);
+          const bool ovf = __any_sync(0xffffffffu, el && (first < base_w || last >= base_w + ring));
+          const uint32_t badm = __ballot_sync(0xffffffffu, __dadd_rn(live_w, P) > cap_w || nact_w >= kActiveCap);
+          uint32_t m = 0;
+          double t[kRegSlots];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            t[j] = __dadd_rn(rw[j], cpk[j]);
+            m |= t[j] > cap_w ? (1u << j) : 0u;
+          }
+          if (tn > 8) {
+#pragma unroll
+            for (int j = 8; j < kRegSlots; ++j) {
+              t[j] = __dadd_rn(rw[j], cpk[j]);
+              m |= t[j] > cap_w ? (1u << j) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[j] = t[j + 8] > t[j] ? t[j + 8] : t[j];
+          }
+#pragma unroll
+          for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+            for (int j = 0; j < w; ++j) t[j] = t[j + w] > t[j] ? t[j + w] : t[j];
+          m &= tn >= 32 ? 0xffffffffu : (1u << tn) - 1u;
+          const uint64_t smx = nonneg_bits(t[0]);
+          const uint64_t peak = umax_w > smx ? umax_w : smx;
+          const uint64_t key = (el && m == 0) ? peak : ~0ull;
+          const double cval = !el ? -1.0
+                              : m == 0 ? from_ordered_bits(peak)
+                                       : __dsub_rn(-static_cast<double>(cslot + __ffs(m) - 1), 1.0);
+          const uint64_t kw = warp_min_u64(key);
+          const uint32_t wb = __ballot_sync(0xffffffffu, key == kw);
+          const int blw = wb ? __ffs(wb) - 1 : -1;
+          if (lane == 0) {
+            s_xk[par][wsel] = kw;
+            s_xb[par][wsel] = blw;
+            s_xf[par][wsel] = (ovf ? 1u : 0u) | ((blw >= 0 && ((badm >> blw) & 1u)) ? 2u : 0u);
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          const uint64_t k0 = s_xk[par][0], k1 = s_xk[par][1];
+          const int b0 = s_xb[par][0], b1 = s_xb[par][1];
+          const uint32_t f0 = s_xf[par][0], f1 = s_xf[par][1];
+          par ^= 1;
+          // select_instance over both halves: (peak, rank), ranks 0-31 before 32-63
+          const bool win1 = k1 < k0;
+          const uint64_t kmin = win1 ? k1 : k0;
+          const int bl = win1 ? 32 + b1 : b0;
+          // records of earlier placements are complete on both warps here
+          done_staged = staged;
+          if (((f0 | f1) & 1u) || kmin == ~0ull || ((win1 ? f1 : f0) & 2u)) break;  // the exact path takes it
+          if ((staged & (kStage / 2 - 1)) == 0) {  // flush back-pressure, both warps
+            if (wsel == 0 && done_staged != rr_pub) publish_done();
+            while (staged - s_flushed > kStage / 2) {
+            }
+          }
+          if (wsel == 0 && done_staged - rr_pub >= KX_RR_PUBLISH) publish_done();
+          const int sl = staged & (kStage - 1);
+          st_cand[sl * kR + lane + 32 * wsel] = cval;
+          if (wsel == 0 && lane == 0)
+            st_meta[sl] = (static_cast<uint32_t>(p - pos0) << 9) | 256u | static_cast<uint32_t>(bl + 1);
+          ++staged;
+          ++nrows;
+          // Dispatcher::commit + admit (engine.cpp:298-319) in the target's lane
+          const bool me = (bl >> 5) == wsel && lane == (bl & 31);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rw[j] = me ? __dadd_rn(rw[j], cpk[j]) : rw[j];
+          if (tn > 8) {
+#pragma unroll
+            for (int j = 8; j < kRegSlots; ++j) rw[j] = me ? __dadd_rn(rw[j], cpk[j]) : rw[j];
+          }
+          rbw |= me ? (1u << tn) - 1u : 0u;
+          live_w = me ? __dadd_rn(live_w, static_cast<double>(prompt + kept)) : live_w;
+          run_w += me ? 1 : 0;
+          umax_w = me ? kmin : umax_w;
+          hi_w = (me && last > hi_w) ? last : hi_w;
+          lm_w = me ? commits : lm_w;
+          nact_w += (me && nact_w < kActiveCap) ? 1 : 0;
+          ++commits;
+          retries = 0;
+          ++n_rr;
+          ++p;
+          if (has_next) {
+            hs = n_hs;
+            mode = n_mode;
+            first = n_first;
+            last = n_last;
+            prompt = n_prompt;
+            kept = n_kept;
+            fo = static_cast<int32_t>(first - B);
+            tn = static_cast<int>(last - first + 1);
+            pbase = static_cast<int>((B + fo) & rmask);
+#pragma unroll
+            for (int j = 0; j < kRegSlots; ++j) cpk[j] = n_pk[j];
+          }
+        }
+        // hand over: booked slots back to the shared ledger, the second
+        // warp's lane state to the first (which continues on the exact path)
+#pragma unroll
+        for (int j = 0; j < kRegSlots; ++j)
+          if ((rbw >> j) & 1u) {
+            const int p2 = static_cast<int>((cslot + j) & rmask);
+            su[p2 * kRW + lane + 32 * wsel] = rw[j];
+            se[p2 * kRW + lane + 32 * wsel] = 1;
+          }
+        if (wsel == 1) {
+          s_hl[lane] = live_w;
+          s_hu[lane] = umax_w;
+          s_hh[lane] = hi_w;
+          s_hr[lane] = run_w;
+          s_hm[lane] = lm_w;
+          s_hn[lane] = nact_w;
+          s_hs[lane] = susp_w ? 1 : 0;
+        }
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (wsel == 0) {
+          live_[0] = live_w;
+          umax_[0] = umax_w;
+          hi_[0] = hi_w;
+          run_[0] = run_w;
+          lm_[0] = lm_w;
+          nact_[0] = nact_w;
+          susp_[0] = susp_w;
+          live_[1] = s_hl[lane];
+          umax_[1] = s_hu[lane];
+          hi_[1] = s_hh[lane];
+          run_[1] = s_hr[lane];
+          lm_[1] = s_hm[lane];
+          nact_[1] = s_hn[lane];
+          susp_[1] = s_hs[lane] != 0;
+          // every record so far is complete (both halves, ordered by the barrier)
+          smem_order();
+          __syncwarp();
+          if (lane == 0) {
+            s_staged = staged;
+            s_cur = p;
+          }
+          rr_pub = staged;
+        }
+      }
+    }
+    while (wsel == 0 && p < q_end) {
       STAMP(0);  // load_head + loop overhead
       const int64_t tr_it = p - pos0 - 100;
       (void)tr_it;
@@ -1501,7 +1708,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       const double P = static_cast<double>(prompt);
       const double* tab = stab + hs * kDtSlots;
       const bool nonempty = last >= first;
-      if (mode != kModeGeneric && !rr) {
+      if (mode != kModeGeneric && !rr && !rr2) {
         const int slot = static_cast<int>((p - pos0) & (kRowRing - 1));
         while (s_tag[slot] != p) {
         }
@@ -1790,7 +1997,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
       }
     }
     smem_order();
-    if (lane == 0) {
+    if (wsel == 0 && lane == 0) {
       s_stop = 1;
       if (n_rr) atomicAdd(&g_disp_cnt[0], static_cast<unsigned long long>(n_rr));
       if (n_exact) atomicAdd(&g_disp_cnt[1], static_cast<unsigned long long>(n_exact));
@@ -1798,7 +2005,7 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
     f_rows = nrows;
     f_adm = commits;
 #if KX_DISPATCH_TIMERS >= 2
-    if (pool == 0 && lane == 0)
+    if (wsel == 0 && pool == 0 && lane == 0)
       for (int k = 0; k < 12; ++k) g_disp_st[k] = static_cast<unsigned long long>(st_acc[k]);
 #endif
 #undef STAMP
@@ -1807,9 +2014,9 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
 #undef KX_LOAD_PK
 #undef KX_RR_FLUSH
 #if KX_DISPATCH_TIMERS
-    if (pool == 0 && lane == 0)
+    if (wsel == 0 && pool == 0 && lane == 0)
       for (int k = 0; k < 4; ++k) g_disp_dbg[6 + k] = static_cast<unsigned long long>(acc[k]);
-    if (pool == 0 && lane == 0) g_disp_dbg[11] = static_cast<unsigned long long>(acc[4]);
+    if (wsel == 0 && pool == 0 && lane == 0) g_disp_dbg[11] = static_cast<unsigned long long>(acc[4]);
 #endif
   }
   if (dbg) {

@@ -101,7 +101,10 @@ def test_dispatch_multi_pool_matches_oracle(gpu_lib, monkeypatch, mode, n_pools,
 # at 0.5 s slots), overloads, full batches and tie cuts take the exact path.
 @pytest.mark.parametrize("mode", ["overlap", "serial", "short1"])
 @pytest.mark.parametrize("n_pools,per_pool,n,rounds,ties,max_batch",
-                         MULTI_POOL_CASES + [(2, 32, 12000, 3, 0, 64), (4, 16, 8000, 4, 0, 2)])
+                         MULTI_POOL_CASES + [(2, 32, 12000, 3, 0, 64), (4, 16, 8000, 4, 0, 2),
+                                             # two resolver warps (33-64 instances)
+                                             (2, 33, 8000, 3, 0, 8), (1, 64, 20000, 3, 0, 8),
+                                             (1, 64, 30000, 2, 0, 64), (2, 48, 12000, 3, 1, 16)])
 def test_dispatch_register_resolver_matches_oracle(gpu_lib, monkeypatch, mode, n_pools, per_pool, n, rounds, ties,
                                                    max_batch):
     cnt = (ctypes.c_uint64 * 2)()
