@@ -734,23 +734,67 @@ __global__ void k_tie_fix_small(QueueDev q, int policy, const uint32_t* __restri
     const uint32_t w = w0 + threadIdx.x;
     int64_t i = 0, e = 0;
     bool big = false;
+    // the first five keys and four queue indices of the run in one round of
+    // independent loads (a run has at least two; most have two to four)
+    uint32_t kv[5] = {0, 0, 0, 0, 0}, pv[4] = {0, 0, 0, 0};
     if (w < total) {
       i = starts[w];
-      const uint32_t kk = keys[i];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) kv[j] = i + j < n ? keys[i + j] : ~kv[0];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pv[j] = i + j < n ? perm[i + j] : 0u;
+      const uint32_t kk = kv[0];
       e = i + 2;
-      while (e < n && e - i <= kThreadRun && keys[e] == kk) ++e;
-      if (e - i > kThreadRun) {
-        while (e < n && keys[e] == kk) ++e;
-        big = true;
+#pragma unroll
+      for (int j = 2; j < 5; ++j)
+        if (e == i + j && i + j < n && kv[j] == kk) ++e;
+      if (e == i + 5) {  // longer than four: the key scan continues
+        while (e < n && e - i <= kThreadRun && keys[e] == kk) ++e;
+        if (e - i > kThreadRun) {
+          while (e < n && keys[e] == kk) ++e;
+          big = true;
+        }
       }
     }
     list_append(big, static_cast<uint32_t>(i), big_starts, n_big, cap, big_lens,
                 static_cast<uint32_t>(e - i));
     if (w >= total || big) continue;
     const int len = static_cast<int>(e - i);
+    bool moved = false;
+    if (len <= 4) {
+      // the common runs (a workflow's repeated agent: 2-4 calls) in registers:
+      // odd-even transposition with the exact comparator (a total order, the
+      // queue index breaks every tie)
+      TKey r0 = load_tkey(q, policy, pv[0]), r1 = load_tkey(q, policy, pv[1]);
+      TKey r2 = load_tkey(q, policy, len > 2 ? pv[2] : pv[1]), r3 = load_tkey(q, policy, len > 3 ? pv[3] : pv[1]);
+      auto cx = [&](TKey& a, TKey& b, bool on) {
+        if (on && tkey_less(q, b, a)) {
+          const TKey tk = a;
+          a = b;
+          b = tk;
+          moved = true;
+        }
+      };
+#pragma unroll
+      for (int round = 0; round < 4; ++round) {
+        if (round >= len) break;
+        if ((round & 1) == 0) {
+          cx(r0, r1, true);
+          cx(r2, r3, len > 3);
+        } else {
+          cx(r1, r2, len > 2);
+        }
+      }
+      if (moved) {
+        perm[i] = r0.idx;
+        perm[i + 1] = r1.idx;
+        if (len > 2) perm[i + 2] = r2.idx;
+        if (len > 3) perm[i + 3] = r3.idx;
+      }
+      continue;
+    }
     TKey r[kThreadRun];
     for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
-    bool moved = false;
     for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
       const TKey x = r[j];
       int m = j - 1;
