@@ -529,10 +529,10 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     // header block
     Layout H;
     const size_t h_hist = H.take<uint32_t>(4 * 256), h_tiles = H.take<uint32_t>(8),
-                 h_pc = H.take<uint32_t>(P), h_ns = H.take<uint32_t>(1), h_nb = H.take<uint32_t>(1),
+                 h_pc = H.take<uint32_t>(P), h_nb = H.take<uint32_t>(1),
                  h_err = H.take<int>(1);
     const size_t o_hdr = L.take<char>(H.off);
-    const size_t o_ss = L.take<uint32_t>(tie_cap), o_bs = L.take<uint32_t>(tie_cap),
+    const size_t o_bs = L.take<uint32_t>(tie_cap),
                  o_bl = L.take<uint32_t>(tie_cap);
     const size_t o_errf = L.take<int>(1), o_sd = L.take<double>(4), o_si = L.take<int64_t>(4),
                  o_ss2 = L.take<int>(4);
@@ -553,10 +553,8 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->ws.hist = reinterpret_cast<uint32_t*>(hdr + h_hist);
     s->ws.tile_counters = reinterpret_cast<uint32_t*>(hdr + h_tiles);
     s->ws.pool_counts = reinterpret_cast<uint32_t*>(hdr + h_pc);
-    s->ws.n_small = reinterpret_cast<uint32_t*>(hdr + h_ns);
     s->ws.n_big = reinterpret_cast<uint32_t*>(hdr + h_nb);
     s->ws.error_flags = reinterpret_cast<int*>(hdr + h_err);
-    s->ws.small_starts = at<uint32_t>(b, o_ss);
     s->ws.big_starts = at<uint32_t>(b, o_bs);
     s->ws.big_lens = at<uint32_t>(b, o_bl);
     s->ws.tie_cap = static_cast<uint32_t>(tie_cap);

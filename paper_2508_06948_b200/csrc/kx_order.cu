@@ -625,9 +625,7 @@ namespace {
 
 }  // namespace
 
-// Run detection: a coalesced scan of the sorted keys (four per thread) lists
-// the run starts, short runs (<= kThreadRun) for the thread-per-run fixer and
-// longer ones for the CTA fixer; warp-aggregated list appends.
+// Warp-aggregated list append (the long-run list of the CTA fixer).
 __device__ __forceinline__ void list_append(bool want, uint32_t value, uint32_t* list,
                                             uint32_t* count, uint32_t cap, uint32_t* lens = nullptr,
                                             uint32_t len = 0) {
@@ -647,166 +645,162 @@ __device__ __forceinline__ void list_append(bool want, uint32_t value, uint32_t*
   }
 }
 
-// Run detection streams the sorted keys (uint4 loads, two per thread per
-// iteration) and lists every run start; the run length is measured by the
-// fixer, which hands runs longer than kThreadRun to the CTA fixer.
-__global__ void __launch_bounds__(256)
-k_tie_runs(const uint32_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ starts,
-           uint32_t* __restrict__ n_starts, uint32_t cap) {
-  // Block-aggregated appends: one global atomic per block per iteration
-  // (a single list counter hit once per warp serialises at L2).
-  __shared__ uint32_t s_warp[8];
-  __shared__ uint32_t s_base;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nv = (n + 3) >> 2;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  constexpr int U = 2;
-  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x; v0 < nv; v0 += U * stride) {
-    uint32_t k[U][6];  // keys[4v - 1 .. 4v + 4]
+// One CTA per chunk of kTieChunk sorted keys: it finds the runs of equal
+// compact keys that START in its chunk (a run is owned by the chunk of its
+// first element; it may extend past the chunk), compacts their starts into
+// shared memory and fixes them with one thread per run. Runs of up to
+// kThreadRun requests (the common case: a workflow's repeated agent shares
+// app_start) are re-sorted by the exact tuple in registers, msg/uid fetched
+// only when the time fields tie, and written back only when their order
+// changes; longer runs are listed for the CTA fixer (k_tie_fix_big).
+// All key loads are issued before any use; a vector's neighbouring keys come
+// from the adjacent lanes (shuffles), only the warp's edge lanes load them.
+constexpr int kRunVec = 4;
+constexpr int kTieChunk = 256 * kRunVec * 4;
+
+__device__ __forceinline__ void fix_run(const QueueDev& q, int policy, uint32_t* __restrict__ perm,
+                                        int64_t i, int len) {
+  bool moved = false;
+  if (len <= 4) {
+    // the common runs (a workflow's repeated agent: 2-4 calls) in registers:
+    // odd-even transposition with the exact comparator (a total order, the
+    // queue index breaks every tie)
+    uint32_t pv[4];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t v = v0 + u * stride + threadIdx.x;
-      const int64_t b = 4 * v;
-      if (v < nv && b + 3 < n) {
-        const uint4 x = reinterpret_cast<const uint4*>(keys)[v];
-        k[u][1] = x.x; k[u][2] = x.y; k[u][3] = x.z; k[u][4] = x.w;
+    for (int j = 0; j < 4; ++j) pv[j] = j < len ? perm[i + j] : 0u;
+    TKey r0 = load_tkey(q, policy, pv[0]), r1 = load_tkey(q, policy, pv[1]);
+    TKey r2 = load_tkey(q, policy, len > 2 ? pv[2] : pv[1]), r3 = load_tkey(q, policy, len > 3 ? pv[3] : pv[1]);
+    auto cx = [&](TKey& a, TKey& b, bool on) {
+      if (on && tkey_less(q, b, a)) {
+        const TKey tk = a;
+        a = b;
+        b = tk;
+        moved = true;
+      }
+    };
+#pragma unroll
+    for (int round = 0; round < 4; ++round) {
+      if (round >= len) break;
+      if ((round & 1) == 0) {
+        cx(r0, r1, true);
+        cx(r2, r3, len > 3);
       } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) k[u][1 + j] = (v < nv && b + j < n) ? keys[b + j] : 0u;
-      }
-      k[u][0] = (v < nv && b > 0) ? keys[b - 1] : 0u;
-      k[u][5] = (v < nv && b + 4 < n) ? keys[b + 4] : 0u;
-    }
-    uint32_t mask = 0;  // bit u*4+j: element 4v+j of vector u starts a run
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t v = v0 + u * stride + threadIdx.x;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t i = 4 * v + j;
-        const bool start = v < nv && i + 1 < n && (i == 0 || k[u][j] != k[u][j + 1]) && k[u][j + 2] == k[u][j + 1];
-        mask |= start ? (1u << (u * 4 + j)) : 0u;
+        cx(r1, r2, len > 2);
       }
     }
-    // block-wide exclusive prefix of the per-thread counts
-    const uint32_t c = __popc(mask);
-    uint32_t x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+    if (moved) {
+      perm[i] = r0.idx;
+      perm[i + 1] = r1.idx;
+      if (len > 2) perm[i + 2] = r2.idx;
+      if (len > 3) perm[i + 3] = r3.idx;
     }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0;
-      for (int w = 0; w < 8; ++w) {
-        const uint32_t t = s_warp[w];
-        s_warp[w] = tot;
-        tot += t;
-      }
-      s_base = tot ? atomicAdd(n_starts, tot) : 0u;
-    }
-    __syncthreads();
-    uint32_t slot = s_base + s_warp[warp] + x - c;
-    while (mask) {
-      const int bit = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const int u = bit >> 2, j = bit & 3;
-      if (slot < cap) starts[slot] = static_cast<uint32_t>(4 * (v0 + u * stride + threadIdx.x) + j);
-      ++slot;
-    }
-    __syncthreads();
+    return;
   }
+  TKey r[kThreadRun];
+  for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
+  for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
+    const TKey x = r[j];
+    int m = j - 1;
+    while (m >= 0 && tkey_less(q, x, r[m])) {
+      r[m + 1] = r[m];
+      --m;
+      moved = true;
+    }
+    r[m + 1] = x;
+  }
+  if (moved)
+    for (int j = 0; j < len; ++j) perm[i + j] = r[j].idx;
 }
 
-// Runs of 2..kThreadRun: one thread each, insertion sort by the exact
-// tuple (msg/uid fetched only when the time fields tie); only a run whose
-// order changes is written back. Longer runs go to the CTA fixer's list.
-__global__ void k_tie_fix_small(QueueDev q, int policy, const uint32_t* __restrict__ keys,
-                                uint32_t* __restrict__ perm, int64_t n,
-                                const uint32_t* __restrict__ starts, const uint32_t* __restrict__ n_starts,
-                                uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
-                                uint32_t* __restrict__ n_big, uint32_t cap) {
-  const uint32_t total = min(*n_starts, cap);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t w0 = blockIdx.x * blockDim.x; w0 < total; w0 += stride) {
+__global__ void __launch_bounds__(256)
+k_tie_fix(QueueDev q, int policy, const uint32_t* __restrict__ keys, uint32_t* __restrict__ perm,
+          int64_t n, uint32_t* __restrict__ big_starts, uint32_t* __restrict__ big_lens,
+          uint32_t* __restrict__ n_big, uint32_t cap) {
+  __shared__ __align__(16) uint32_t s_keys[kTieChunk];
+  __shared__ uint16_t s_list[kTieChunk / 2];  // chunk-local run starts
+  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cbase = int64_t(blockIdx.x) * kTieChunk;
+  const int64_t nv = (n + 3) >> 2;
+  const int64_t vb = cbase / 4 + threadIdx.x;
+  uint32_t k[kRunVec][6];  // keys[4v - 1 .. 4v + 4]
+#pragma unroll
+  for (int u = 0; u < kRunVec; ++u) {
+    const int64_t v = vb + u * blockDim.x;
+    const int64_t b = 4 * v;
+    if (v < nv && b + 3 < n) {
+      const uint4 x = reinterpret_cast<const uint4*>(keys)[v];
+      k[u][1] = x.x; k[u][2] = x.y; k[u][3] = x.z; k[u][4] = x.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) k[u][1 + j] = (v < nv && b + j < n) ? keys[b + j] : 0u;
+    }
+    k[u][0] = (lane == 0 && v < nv && b > 0) ? keys[b - 1] : 0u;
+    k[u][5] = (lane == 31 && v < nv && b + 4 < n) ? keys[b + 4] : 0u;
+  }
+  uint32_t mask = 0;  // bit u*4+j: element 4v+j of vector u starts a run
+#pragma unroll
+  for (int u = 0; u < kRunVec; ++u) {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, k[u][4], 1);
+    const uint32_t next = __shfl_down_sync(0xffffffffu, k[u][1], 1);
+    if (lane > 0) k[u][0] = prev;
+    if (lane < 31) k[u][5] = next;
+    reinterpret_cast<uint4*>(s_keys)[u * blockDim.x + threadIdx.x] = make_uint4(k[u][1], k[u][2], k[u][3], k[u][4]);
+    const int64_t v = vb + u * blockDim.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t i = 4 * v + j;
+      const bool start = v < nv && i + 1 < n && (i == 0 || k[u][j] != k[u][j + 1]) && k[u][j + 2] == k[u][j + 1];
+      mask |= start ? (1u << (u * 4 + j)) : 0u;
+    }
+  }
+  // block-wide exclusive prefix of the per-thread counts: the chunk's run list
+  const uint32_t c = __popc(mask);
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t t = s_warp[w];
+      s_warp[w] = tot;
+      tot += t;
+    }
+    s_total = tot;
+  }
+  __syncthreads();
+  uint32_t slot = s_warp[warp] + x - c;
+  while (mask) {
+    const int bit = __ffs(mask) - 1;
+    mask &= mask - 1;
+    s_list[slot++] = static_cast<uint16_t>(4 * ((bit >> 2) * blockDim.x + threadIdx.x) + (bit & 3));
+  }
+  __syncthreads();
+  const uint32_t total = s_total;
+  for (uint32_t w0 = 0; w0 < total; w0 += blockDim.x) {  // uniform trip count: list_append is warp-wide
     const uint32_t w = w0 + threadIdx.x;
     int64_t i = 0, e = 0;
     bool big = false;
-    // the first five keys and four queue indices of the run in one round of
-    // independent loads (a run has at least two; most have two to four)
-    uint32_t kv[5] = {0, 0, 0, 0, 0}, pv[4] = {0, 0, 0, 0};
     if (w < total) {
-      i = starts[w];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) kv[j] = i + j < n ? keys[i + j] : ~kv[0];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) pv[j] = i + j < n ? perm[i + j] : 0u;
-      const uint32_t kk = kv[0];
-      e = i + 2;
-#pragma unroll
-      for (int j = 2; j < 5; ++j)
-        if (e == i + j && i + j < n && kv[j] == kk) ++e;
-      if (e == i + 5) {  // longer than four: the key scan continues
-        while (e < n && e - i <= kThreadRun && keys[e] == kk) ++e;
-        if (e - i > kThreadRun) {
-          while (e < n && keys[e] == kk) ++e;
-          big = true;
-        }
+      const int li = s_list[w];
+      i = cbase + li;
+      const uint32_t kk = s_keys[li];
+      e = i + 2;  // a run has at least two
+      while (e < n && e - i <= kThreadRun && (e - cbase < kTieChunk ? s_keys[e - cbase] : keys[e]) == kk) ++e;
+      if (e - i > kThreadRun) {
+        while (e < n && keys[e] == kk) ++e;
+        big = true;
       }
     }
     list_append(big, static_cast<uint32_t>(i), big_starts, n_big, cap, big_lens,
                 static_cast<uint32_t>(e - i));
-    if (w >= total || big) continue;
-    const int len = static_cast<int>(e - i);
-    bool moved = false;
-    if (len <= 4) {
-      // the common runs (a workflow's repeated agent: 2-4 calls) in registers:
-      // odd-even transposition with the exact comparator (a total order, the
-      // queue index breaks every tie)
-      TKey r0 = load_tkey(q, policy, pv[0]), r1 = load_tkey(q, policy, pv[1]);
-      TKey r2 = load_tkey(q, policy, len > 2 ? pv[2] : pv[1]), r3 = load_tkey(q, policy, len > 3 ? pv[3] : pv[1]);
-      auto cx = [&](TKey& a, TKey& b, bool on) {
-        if (on && tkey_less(q, b, a)) {
-          const TKey tk = a;
-          a = b;
-          b = tk;
-          moved = true;
-        }
-      };
-#pragma unroll
-      for (int round = 0; round < 4; ++round) {
-        if (round >= len) break;
-        if ((round & 1) == 0) {
-          cx(r0, r1, true);
-          cx(r2, r3, len > 3);
-        } else {
-          cx(r1, r2, len > 2);
-        }
-      }
-      if (moved) {
-        perm[i] = r0.idx;
-        perm[i + 1] = r1.idx;
-        if (len > 2) perm[i + 2] = r2.idx;
-        if (len > 3) perm[i + 3] = r3.idx;
-      }
-      continue;
-    }
-    TKey r[kThreadRun];
-    for (int j = 0; j < len; ++j) r[j] = load_tkey(q, policy, perm[i + j]);
-    for (int j = 1; j < len; ++j) {  // insertion sort, exact comparator
-      const TKey x = r[j];
-      int m = j - 1;
-      while (m >= 0 && tkey_less(q, x, r[m])) {
-        r[m + 1] = r[m];
-        --m;
-        moved = true;
-      }
-      r[m + 1] = x;
-    }
-    if (moved)
-      for (int j = 0; j < len; ++j) perm[i + j] = r[j].idx;
+    if (w < total && !big) fix_run(q, policy, perm, i, static_cast<int>(e - i));
   }
 }
 
@@ -1037,28 +1031,11 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   res.keys = ws.keys[cur];
   res.perm = ws.vals[cur];
 
-  const int tgrid = static_cast<int>(std::min<int64_t>((n / 4 + 256) / 256, int64_t(sms) * 8));
-  // reads the sorted keys (4 B); tie runs gather their exact tuples
-  P.begin("tie_runs", N * 4.0, st);
-  k_tie_runs<<<tgrid, 256, 0, st>>>(res.keys, n, ws.small_starts, ws.n_small, ws.tie_cap);
-  KX_CHECK_LAUNCH();
-  P.end(st);
-  P.begin("tie_fix", 0.0, st);
-  // one resident wave (grid-stride over the run starts): a partial second
-  // wave would double the latency-bound kernel's span
-  static std::once_flag fix_once[kMaxDevices];
-  static int fix_ctas_dev[kMaxDevices];
-  int dev = 0;
-  KX_CUDA(cudaGetDevice(&dev));
-  once_per_device(fix_once, [dev] {
-    int b = 0;
-    KX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tie_fix_small, 256, 0));
-    fix_ctas_dev[dev] = std::max(b, 1);
-  });
-  const int fix_ctas = fix_ctas_dev[dev];
-  k_tie_fix_small<<<sms * fix_ctas, 256, 0, st>>>(q, op.policy, res.keys, res.perm, n, ws.small_starts,
-                                           ws.n_small, ws.big_starts, ws.big_lens, ws.n_big,
-                                           ws.tie_cap);
+  // finds the runs of equal compact keys (reads the sorted keys, 4 B) and
+  // fixes the short ones; their exact tuples are gathered
+  P.begin("tie_fix", N * 4.0, st);
+  k_tie_fix<<<static_cast<unsigned>((n + kTieChunk - 1) / kTieChunk), 256, 0, st>>>(
+      q, op.policy, res.keys, res.perm, n, ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);
   KX_CHECK_LAUNCH();
   k_tie_fix_big<<<sms, kBigThreads, 0, st>>>(q, op.policy, res.perm, ws.vals[cur ^ 1],
                                              ws.big_starts, ws.big_lens, ws.n_big, ws.tie_cap);
@@ -1099,8 +1076,7 @@ void configure_sort_kernels() {
   preload(k_keygen<true>);
   preload(k_keygen<false>);
   preload(k_pool_offsets);
-  preload(k_tie_runs);
-  preload(k_tie_fix_small);
+  preload(k_tie_fix);
   preload(k_tie_fix_big);
   preload(k_init_ranges);
   preload(k_onesweep_pass<uint32_t, 0>);

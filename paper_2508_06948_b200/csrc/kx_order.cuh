@@ -18,16 +18,14 @@ struct OrderWorkspace {
   PoolRange* ranges;
   int64_t* pool_offsets;  // n_pools + 1
   // small header block, zeroed per order: hist[4*256], tile_counters[8],
-  // pool_counts[n_pools], n_small, n_big, error_flags
+  // pool_counts[n_pools], n_big, error_flags
   void* small_hdr;
   size_t small_hdr_bytes;
   uint32_t* hist;
   uint32_t* tile_counters;
   uint32_t* pool_counts;
-  uint32_t* n_small;
   uint32_t* n_big;
   int* error_flags;
-  uint32_t* small_starts;
   uint32_t* big_starts;
   uint32_t* big_lens;
   uint32_t tie_cap;
