@@ -551,37 +551,96 @@ __device__ __forceinline__ double pk_of(double P, double k, double dt) {
 enum : int32_t { kModeTabPk = 0, kModeTabDt = 1, kModeGeneric = 2 };
 
 // The collected prefix of one pool in order (all threads of the CTA): a
-// bitonic sort of (compact key << 32 | slot) in shared memory, then runs of
+// bitonic sort of (compact key << 32 | slot), then runs of
 // equal compact keys re-sorted by the exact tuple (one thread per run).
 // Returns false when a run is longer than kRunMax (degenerate keys): the
 // caller then dispatches from the full order instead.
 constexpr int kRunMax = 16;
 
+// Diagnostics (see the K5 chain notes below)
+#ifndef KX_DISPATCH_TIMERS
+#define KX_DISPATCH_TIMERS 0
+#endif
+__device__ unsigned long long g_disp_dbg[16];
+__device__ unsigned long long g_disp_st[16];      // KX_DISPATCH_TIMERS=2: per-stage resolver cycles (pool 0); 11-15: phase-3 prologue stamps
+__device__ unsigned long long g_disp_cnt[2];      // decisions by the register resolver / heads on the exact path (all pools)
+__device__ unsigned long long g_disp_pool_t[2 * 64];  // KX_DISPATCH_TIMERS: phase-3 start / end per pool
+__device__ unsigned long long g_disp_tr[8 * 16];  // KX_DISPATCH_TIMERS=3: clock stamps of 8 rr steps (pool 0)
+
+
 __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __restrict__ cand,
                             const uint32_t* __restrict__ ckey, int n, uint32_t* __restrict__ heads,
                             uint64_t* sk, uint32_t* so) {
   __shared__ int s_long;
-  int p2 = 1;
+  // Bitonic network over the next power of two >= n, each thread holding 8
+  // consecutive entries in registers: partner distances 1-4 are in-thread,
+  // 8-128 one shuffle within the warp, only 256-1024 go through shared
+  // memory (6 stages for 2048 entries, against 66 barriers for an all-smem
+  // network).
+  static_assert(kTopKMax == 256 * 8, "8 prefix entries per thread of the 256-thread chain CTA");
+  int p2 = 8;
   while (p2 < n) p2 <<= 1;
-  for (int i = threadIdx.x; i < p2; i += blockDim.x)
-    sk[i] = i < n ? ((static_cast<uint64_t>(__ldcg(ckey + i)) << 32) | static_cast<uint32_t>(i)) : ~0ull;
+  const int base = threadIdx.x * 8;
+  uint64_t v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+    v[r] = base + r < n ? ((static_cast<uint64_t>(__ldcg(ckey + base + r)) << 32) | static_cast<uint32_t>(base + r))
+                        : ~0ull;
   if (threadIdx.x == 0) s_long = 0;
-  __syncthreads();
   for (int kk = 2; kk <= p2; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const uint64_t x = sk[i], y = sk[l];
-          if ((x > y) == ((i & kk) == 0)) {
-            sk[i] = y;
-            sk[l] = x;
-          }
+      if (j >= 256) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) sk[base + r] = v[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = base + r;
+          const uint64_t o = sk[i ^ j];
+          v[r] = (((i & j) == 0) == ((i & kk) == 0)) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
         }
+        __syncthreads();
+      } else if (j >= 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = base + r;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j >> 3);
+          v[r] = (((i & j) == 0) == ((i & kk) == 0)) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+        }
+      } else {
+        // in-thread pairs; j is a compile-time constant in each branch so v
+        // stays in registers
+#define KX_PFX_INREG(J)                                   \
+  _Pragma("unroll") for (int r = 0; r < 8; ++r) {         \
+    if (r & (J)) continue;                                \
+    const bool asc = ((base + r) & kk) == 0;              \
+    const uint64_t a = v[r], b = v[r | (J)];              \
+    if ((a > b) == asc) {                                 \
+      v[r] = b;                                           \
+      v[r | (J)] = a;                                     \
+    }                                                     \
+  }
+        if (j == 4) {
+          KX_PFX_INREG(4)
+        } else if (j == 2) {
+          KX_PFX_INREG(2)
+        } else {
+          KX_PFX_INREG(1)
+        }
+#undef KX_PFX_INREG
       }
-      __syncthreads();
     }
   }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) sk[base + r] = v[r];
+  __syncthreads();
+#if KX_DISPATCH_TIMERS
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_disp_st[11] = t;
+  }
+#endif
   for (int i = threadIdx.x; i < n; i += blockDim.x) so[i] = __ldcg(cand + static_cast<uint32_t>(sk[i]));
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -656,14 +715,6 @@ __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __res
 // Diagnostics (build with -DKX_DISPATCH_TIMERS=1): globaltimer stamps of
 // pool 0's CTA (start, loop start, loop end, end), its placement count and
 // the resolver's cycle split.
-#ifndef KX_DISPATCH_TIMERS
-#define KX_DISPATCH_TIMERS 0
-#endif
-__device__ unsigned long long g_disp_dbg[16];
-__device__ unsigned long long g_disp_st[16];
-__device__ unsigned long long g_disp_cnt[2];
-__device__ unsigned long long g_disp_pool_t[2 * 64];  // KX_DISPATCH_TIMERS: phase-3 start / end per pool  // decisions by the register resolver / heads on the exact path (all pools)
-__device__ unsigned long long g_disp_tr[8 * 16];  // KX_DISPATCH_TIMERS=3: clock stamps of 8 rr steps (pool 0)  // KX_DISPATCH_TIMERS=2: per-stage resolver cycles (pool 0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

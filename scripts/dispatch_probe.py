@@ -63,7 +63,7 @@ def timers():
                   " | end " + " ".join(f"{x:.1f}" for x in ends))
             print(f"  phase-3 prologue us: start after keygen {(st[12] - kd[0]) / 1e3:.2f}, ring staging "
                   f"{(st[13] - st[12]) / 1e3:.2f}, umax {(st[14] - st[13]) / 1e3:.2f}, prefix sort "
-                  f"{(st[15] - st[14]) / 1e3:.2f}")
+                  f"{(st[15] - st[14]) / 1e3:.2f} (network {(st[11] - st[14]) / 1e3:.2f})")
         if any(st[:12]):
             s.lib.kx_debug_dispatch_timers(buf)
             n = max(1, list(buf)[5])
