@@ -847,8 +847,11 @@ void tick_impl(kx_sched* s, double now) {
   // priority stream) sort their prefix and run the round while the main
   // stream sorts the whole queue. A round that outlasts its prefix resumes
   // over the full order (phase 2).
-  KX_CUDA(cudaMemsetAsync(s->q.admitted, 0, static_cast<size_t>(s->n), s->stream));
   OrderHooks hooks;
+  hooks.zero_bytes = s->q.admitted;
+  hooks.n_zero_bytes = s->n;
+  hooks.zero_words = s->topk.plist_count;  // k_sample_keys' per-pool counters
+  hooks.n_zero_words = s->n_pools;
   hooks.before_keygen = [&] {
     launch_spec_bound(s->q, s->a, s->in, s->pool_begin, op, s->n, s->ws, s->topk, s->stream);
   };

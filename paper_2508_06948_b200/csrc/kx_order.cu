@@ -900,7 +900,7 @@ void launch_spec_bound(const QueueDev& q, const AgentsDev& a, const InstDev& in,
   // pools are balanced
   const int64_t per = int64_t(kSpecMax / 2) * op.n_pools;
   const int64_t m = std::max<int64_t>(1, (blocks * kSampleLen + per - 1) / per);
-  KX_CUDA(cudaMemsetAsync(w.plist_count, 0, sizeof(uint32_t) * op.n_pools, st));
+  // w.plist_count was zeroed by the order's init launch (the tick's hooks)
   k_sample_keys<<<static_cast<unsigned>((blocks + m - 1) / m), kSampleLen, 0, st>>>(
       q, a, op, n, stride, m, ws.ranges, w.plist, w.plist_count);
   KX_CHECK_LAUNCH();
@@ -936,6 +936,33 @@ int keygen_grid(int64_t n, int sms) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
 }
 
+// Per-order reset: header counters, window ranges, and the caller's extra
+// buffers (OrderHooks::zero_*), in one launch.
+struct OrderInit {
+  uint32_t* hdr;
+  int hdr_words;
+  PoolRange* ranges;
+  int n_pools;
+  uint32_t* words;
+  int n_words;
+  uint8_t* bytes;
+  int64_t n_bytes;
+};
+
+__global__ void __launch_bounds__(256) k_order_init(OrderInit in) {
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < in.hdr_words; i += blockDim.x) in.hdr[i] = 0;
+    for (int i = threadIdx.x; i < in.n_words; i += blockDim.x) in.words[i] = 0;
+    for (int p = threadIdx.x; p < in.n_pools; p += blockDim.x)
+      in.ranges[p] = PoolRange{~0ull, 0ull, 0.0, 0.0};  // min / max of the sampled window
+  }
+  const int64_t vecs = in.n_bytes / 16;
+  uint4* v = reinterpret_cast<uint4*>(in.bytes);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += int64_t(gridDim.x) * blockDim.x)
+    v[i] = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x == 0 && threadIdx.x < in.n_bytes - vecs * 16) in.bytes[vecs * 16 + threadIdx.x] = 0;
+}
+
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
                             PhaseProfiler* prof, const OrderHooks* hooks) {
@@ -944,10 +971,26 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   const double N = static_cast<double>(n);
   OrderResultDev res{};
   const int passes = op.key_bits / kRadixBits;
-  KX_CUDA(cudaMemsetAsync(ws.small_hdr, 0, ws.small_hdr_bytes, st));
-  // ranges: lo_bits = ~0, hi_bits = 0
-  KX_CUDA(cudaMemsetAsync(ws.ranges, 0, sizeof(PoolRange) * op.n_pools, st));
-  init_ranges(ws.ranges, op.n_pools, st);
+  // one launch resets the per-order state (header counters, window ranges)
+  // and whatever the caller's hooks add (the tick's admitted flags and
+  // sample counters)
+  {
+    OrderInit in{};
+    in.hdr = static_cast<uint32_t*>(ws.small_hdr);
+    in.hdr_words = static_cast<int>(ws.small_hdr_bytes / 4);
+    in.ranges = ws.ranges;
+    in.n_pools = op.n_pools;
+    if (hooks) {
+      in.words = hooks->zero_words;
+      in.n_words = hooks->n_zero_words;
+      in.bytes = hooks->zero_bytes;
+      in.n_bytes = hooks->n_zero_bytes;
+    }
+    const int64_t vecs = in.n_bytes / 16;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, int64_t(sms) * 4)));
+    k_order_init<<<grid, 256, 0, st>>>(in);
+    KX_CHECK_LAUNCH();
+  }
   if (n == 0) {
     k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
     KX_CHECK_LAUNCH();
@@ -1044,18 +1087,7 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   return res;
 }
 
-__global__ void k_init_ranges(PoolRange* r, int n) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) {
-    r[p].lo_bits = ~0ull;
-    r[p].hi_bits = 0ull;
-  }
-}
 
-void init_ranges(PoolRange* r, int n, cudaStream_t st) {
-  k_init_ranges<<<(n + 127) / 128, 128, 0, st>>>(r, n);
-  KX_CHECK_LAUNCH();
-}
 
 // Module lazy loading (CUDA 12 default) loads a kernel at its first launch
 // and may wait for the device to drain while doing so; the overlapped tick
@@ -1078,7 +1110,7 @@ void configure_sort_kernels() {
   preload(k_pool_offsets);
   preload(k_tie_fix);
   preload(k_tie_fix_big);
-  preload(k_init_ranges);
+  preload(k_order_init);
   preload(k_onesweep_pass<uint32_t, 0>);
   preload(k_onesweep_pass<uint32_t, 1>);
   preload(k_onesweep_pass<uint32_t, 2>);

@@ -37,7 +37,6 @@ struct OrderResultDev {
 };
 
 size_t order_lookback_bytes(int64_t cap);
-void init_ranges(PoolRange* r, int n, cudaStream_t st);
 void configure_sort_kernels();
 void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, double* k0,
                   double* k1, double* k2, int sms, cudaStream_t st);
@@ -85,6 +84,11 @@ struct OrderHooks {
   KeygenSpec spec{};                           // speculative prefix collection (bound != nullptr)
   std::function<void()> after_keys;            // compact keys, histograms, pool offsets ready
   std::function<void()> before_key_overwrite;  // after radix pass 0, before pass 1
+  // zeroed by the order's first launch, with its own state
+  uint32_t* zero_words = nullptr;
+  int n_zero_words = 0;
+  uint8_t* zero_bytes = nullptr;  // 16-byte aligned
+  int64_t n_zero_bytes = 0;
 };
 
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
