@@ -919,9 +919,9 @@ size_t spec_list_words(int n_pools) { return size_t(n_pools) * kSpecMax; }
 // digit (few distinct values).
 constexpr int kSortRankDefault[4] = {2, 2, 2, 1};
 
-size_t order_lookback_bytes(int64_t cap) {
+size_t order_lookback_bytes(int64_t cap) {  // two arrays, alternating between passes
   const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
-  return size_t(tiles) * kRadix * sizeof(uint32_t);
+  return 2 * size_t(tiles) * kRadix * sizeof(uint32_t);
 }
 
 void launch_score(const QueueDev& q, const AgentsDev& a, int policy, int64_t n, double* k0,
@@ -947,6 +947,8 @@ struct OrderInit {
   int n_words;
   uint8_t* bytes;
   int64_t n_bytes;
+  uint4* lb;
+  int64_t lb_vecs;
 };
 
 __global__ void __launch_bounds__(256) k_order_init(OrderInit in) {
@@ -960,6 +962,8 @@ __global__ void __launch_bounds__(256) k_order_init(OrderInit in) {
   uint4* v = reinterpret_cast<uint4*>(in.bytes);
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += int64_t(gridDim.x) * blockDim.x)
     v[i] = make_uint4(0, 0, 0, 0);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < in.lb_vecs; i += int64_t(gridDim.x) * blockDim.x)
+    in.lb[i] = make_uint4(0, 0, 0, 0);
   if (blockIdx.x == 0 && threadIdx.x < in.n_bytes - vecs * 16) in.bytes[vecs * 16 + threadIdx.x] = 0;
 }
 
@@ -986,7 +990,10 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
       in.bytes = hooks->zero_bytes;
       in.n_bytes = hooks->n_zero_bytes;
     }
-    const int64_t vecs = in.n_bytes / 16;
+    // the first radix pass's look-back array (later passes clear their successor's)
+    in.lb = reinterpret_cast<uint4*>(ws.lookback);
+    in.lb_vecs = n > 0 ? (n + kSortTile - 1) / kSortTile * kRadix / 4 : 0;
+    const int64_t vecs = std::max<int64_t>(in.n_bytes / 16, in.lb_vecs);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, int64_t(sms) * 4)));
     k_order_init<<<grid, 256, 0, st>>>(in);
     KX_CHECK_LAUNCH();
@@ -1046,7 +1053,8 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   const size_t smem = sort_dyn_smem<uint32_t>();
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
-    KX_CUDA(cudaMemsetAsync(ws.lookback, 0, size_t(tiles) * kRadix * sizeof(uint32_t), st));
+    uint32_t* const lb = ws.lookback + (p & 1) * size_t(tiles) * kRadix;
+    uint32_t* const lb_next = p + 1 < passes ? ws.lookback + ((p + 1) & 1) * size_t(tiles) * kRadix : nullptr;
     // key (4 B) [+ index (4 B) after the first pass] in, key + index out
     P.begin("radix_pass", N * (p == 0 ? 12.0 : 16.0), st);
     {
@@ -1057,13 +1065,13 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
       const unsigned g = static_cast<unsigned>(tiles);
       if (v == 1)
         k_onesweep_pass<uint32_t, 1><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, lb, lb_next, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else if (v == 2)
         k_onesweep_pass<uint32_t, 2><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, lb, lb_next, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
       else
         k_onesweep_pass<uint32_t, 0><<<g, kSortThreads, smem, st>>>(ws.keys[cur], ws.keys[cur ^ 1], vin,
-            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, ws.lookback, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
+            ws.vals[cur ^ 1], n, p * kRadixBits, ws.hist + p * kRadix, lb, lb_next, ws.tile_counters + p, 1, nh, (p + 1) * kRadixBits);
     }
     KX_CHECK_LAUNCH();
     P.end(st);

@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? KX_SORT_MINB : 
 k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                 int64_t n, int shift, const uint32_t* __restrict__ global_excl,
-                uint32_t* __restrict__ lookback, uint32_t* __restrict__ tile_counter, int counts_in,
+                uint32_t* __restrict__ lookback, uint32_t* __restrict__ lookback_next,
+                uint32_t* __restrict__ tile_counter, int counts_in,
                 uint32_t* __restrict__ next_hist, int next_shift
 #ifdef KX_PROBE_NO_LOOKBACK_SWITCH
                 , int probe_no_lookback = 0
@@ -191,6 +192,10 @@ k_onesweep_pass(const K* __restrict__ keys_in, K* __restrict__ keys_out,
   __syncthreads();
   const uint32_t tile = sm.tile_id;
   const int64_t base = int64_t(tile) * kSortTile;
+  // passes alternate between two look-back arrays: this one clears its
+  // tile's words of the other (the previous pass, which used it, is done;
+  // the next pass has the same tiles), so no memset runs between passes
+  if (lookback_next && tid < kRadix) lookback_next[int64_t(tile) * kRadix + tid] = 0u;
 
   K key[kSortItems];
   uint32_t val[kSortItems];

@@ -50,7 +50,7 @@ void sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_
     KX_CUDA(cudaMemsetAsync(lookback, 0, size_t(tiles) * kRadix * 4, st));
     k_onesweep_pass<K><<<static_cast<unsigned>(tiles), kSortThreads, sort_dyn_smem<K>(), st>>>(
         kin, kout, (p == 0 && vals_are_iota) ? nullptr : vin, vout, n, begin_bit + p * kRadixBits,
-        hist + p * kRadix, lookback, counters + p, 0, nullptr, 0);
+        hist + p * kRadix, lookback, nullptr, counters + p, 0, nullptr, 0);
     KX_CHECK_LAUNCH();
     std::swap(kin, kout);
     std::swap(vin, vout);

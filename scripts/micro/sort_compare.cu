@@ -64,7 +64,7 @@ int main(int argc, char** argv) {
     for (int p = 0; p < 4; ++p) {
       cudaMemsetAsync(lb, 0, tiles * kRadix * 4);
       k_onesweep_pass<uint32_t, 2><<<unsigned(tiles), kSortThreads, smem>>>(
-          kin, kout[p & 1], vin, vout[p & 1], n, 8 * p, hist + p * kRadix, lb, tc + p, 0, nullptr, 0);
+          kin, kout[p & 1], vin, vout[p & 1], n, 8 * p, hist + p * kRadix, lb, nullptr, tc + p, 0, nullptr, 0);
       kin = kout[p & 1];
       vin = vout[p & 1];
     }

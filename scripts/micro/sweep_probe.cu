@@ -29,7 +29,7 @@ int main() {
     for (int it = 0; it < 10; ++it) {
       cudaMemset(lb, 0, tiles * kRadix * 4); cudaMemset(tc, 0, 64);
       cudaEventRecord(a);
-      k_onesweep_pass<uint32_t><<<tiles, kSortThreads, smem>>>(k0, k1, nullptr, v1, n, 0, hist, lb, tc, 0, nullptr, 0, mode);
+      k_onesweep_pass<uint32_t><<<tiles, kSortThreads, smem>>>(k0, k1, nullptr, v1, n, 0, hist, lb, nullptr, tc, 0, nullptr, 0, mode);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
     }
