@@ -339,6 +339,8 @@ void alloc_blob(Blob& b, size_t bytes) {
   b.size = std::max<size_t>(bytes, 256);
   KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&b.base), b.size));
   KX_CUDA(cudaMemset(b.base, 0, b.size));
+  // legacy-stream work is not ordered before the handle's non-blocking streams
+  KX_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
 }
 
 void free_blob(Blob& b) {
@@ -514,6 +516,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->in.rr_next = at<int32_t>(b, o_rr);
     std::vector<int64_t> minus1(I, -1);  // hi_slot: nothing booked yet
     KX_CUDA(cudaMemcpy(s->in.hi_slot, minus1.data(), I * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // the DMAs have landed before s->stream uses them
   }
   // order workspace + scratch
   {
@@ -761,7 +764,7 @@ void ensure_waiting(kx_sched* s, int64_t per_inst) {
     const size_t P = static_cast<size_t>(s->n_pools);
     KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->adm), std::max<size_t>(1, P * s->log_cap) * sizeof(kx_admission)));
     KX_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->adm_count), std::max<size_t>(1, P) * 8));
-    KX_CUDA(cudaMemset(s->adm_count, 0, std::max<size_t>(1, P) * 8));
+    KX_CUDA(cudaMemsetAsync(s->adm_count, 0, std::max<size_t>(1, P) * 8, s->stream));
   }
   if (per_inst <= s->wcap) return;
   const size_t I = static_cast<size_t>(s->n_inst);
@@ -927,7 +930,12 @@ struct DevArena {
   template <typename T>
   T* upload(const T* h, size_t n) {
     T* d = alloc<T>(n);
-    if (n) KX_CUDA(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    if (n) {
+      // a pageable cudaMemcpy may return before its DMA lands, and the
+      // kernels run on non-blocking streams: wait for the legacy stream
+      KX_CUDA(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice));
+      KX_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    }
     return d;
   }
   ~DevArena() {
@@ -2273,6 +2281,7 @@ int kx_profiler_create(int32_t n_agents, const kx_convergence_config* exec,
     KX_CUDA(cudaMemcpy(p->d_cfg, cfgs.data(), nd * sizeof(DistCfg), cudaMemcpyHostToDevice));
     KX_CUDA(cudaMemcpy(dd.next_cp, ncp.data(), nd * 8, cudaMemcpyHostToDevice));
     KX_CUDA(cudaMemcpy(dd.last_dist, last.data(), nd * 8, cudaMemcpyHostToDevice));
+    KX_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // the DMA has landed before p->stream uses it
     *out = p.release();
   });
 }

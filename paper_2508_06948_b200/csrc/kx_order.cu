@@ -1035,10 +1035,12 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   }
   KX_CHECK_LAUNCH();
   P.end(st);
+  // compact keys, histograms and pool counts ready (the hook's consumers do
+  // not read the pool offsets, computed next)
+  if (hooks && hooks->after_keys) hooks->after_keys();
   // (pass p scans its raw digit counts itself; pass p counts digit p + 1)
   k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
   KX_CHECK_LAUNCH();
-  if (hooks && hooks->after_keys) hooks->after_keys();  // compact keys + histograms ready
   if (const char* dump = getenv("KX_DUMP_KEYS")) {  // diagnostics: the compact keys, raw u32
     std::vector<uint32_t> hk(static_cast<size_t>(n));
     KX_CUDA(cudaMemcpyAsync(hk.data(), ws.keys[0], size_t(n) * 4, cudaMemcpyDeviceToHost, st));

@@ -82,7 +82,7 @@ struct KeygenSpec {
 struct OrderHooks {
   std::function<void()> before_keygen;         // quantisation window ready, keys not yet built
   KeygenSpec spec{};                           // speculative prefix collection (bound != nullptr)
-  std::function<void()> after_keys;            // compact keys, histograms, pool offsets ready
+  std::function<void()> after_keys;            // compact keys, histograms, pool counts ready (not the offsets)
   std::function<void()> before_key_overwrite;  // after radix pass 0, before pass 1
   // zeroed by the order's first launch, with its own state
   uint32_t* zero_words = nullptr;

@@ -805,6 +805,13 @@ __global__ void k_gather_spans(int64_t k, const char* __restrict__ bytes, const 
   for (int j = threadIdx.x; j < len[i]; j += blockDim.x) out[pos[i] + j] = bytes[off[i] + j];
 }
 
+// Host <-> device copies of the trace, ordered on its (non-blocking) stream:
+// a plain cudaMemcpy runs on the legacy stream, which does not wait for it.
+static void tcopy(const kx_trace* t, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  KX_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, t->st));
+  KX_CUDA(cudaStreamSynchronize(t->st));
+}
+
 static void msg_spans_dev(const kx_trace* t, int64_t k, const int64_t* msgs_host, int64_t* doff, int32_t* dlen) {
   int64_t* dm = nullptr;
   KX_CUDA(cudaMalloc(&dm, size_t(k) * 8));
@@ -827,7 +834,7 @@ static std::vector<std::string> fetch_msg_names(const kx_trace* t, const std::ve
   KX_CUDA(cudaMalloc(&dlen, size_t(k) * 4));
   msg_spans_dev(t, k, msgs.data(), doff, dlen);
   std::vector<int32_t> len(static_cast<size_t>(k));
-  KX_CUDA(cudaMemcpy(len.data(), dlen, size_t(k) * 4, cudaMemcpyDeviceToHost));
+  tcopy(t, len.data(), dlen, size_t(k) * 4, cudaMemcpyDeviceToHost);
   std::vector<int64_t> pos(static_cast<size_t>(k) + 1, 0);
   for (int64_t i = 0; i < k; ++i) pos[i + 1] = pos[i] + len[i];
   char* dbuf = nullptr;
@@ -868,15 +875,15 @@ std::vector<int64_t> host_excl(const int64_t* d, int64_t n, cudaStream_t st, int
 
 std::string line_text(kx_trace* t, int64_t L) {
   int64_t s = 0, e = 0;
-  KX_CUDA(cudaMemcpy(&s, t->starts + L, 8, cudaMemcpyDeviceToHost));
+  tcopy(t, &s, t->starts + L, 8, cudaMemcpyDeviceToHost);
   if (L < t->newlines) {
-    KX_CUDA(cudaMemcpy(&e, t->starts + L + 1, 8, cudaMemcpyDeviceToHost));
+    tcopy(t, &e, t->starts + L + 1, 8, cudaMemcpyDeviceToHost);
     e -= 1;
   } else {
     e = t->n_bytes;
   }
   std::string out(static_cast<size_t>(std::max<int64_t>(e - s, 0)), '\0');
-  if (!out.empty()) KX_CUDA(cudaMemcpy(out.data(), t->bytes + s, out.size(), cudaMemcpyDeviceToHost));
+  if (!out.empty()) tcopy(t, out.data(), t->bytes + s, out.size(), cudaMemcpyDeviceToHost);
   return out;
 }
 
@@ -937,7 +944,7 @@ void parse(kx_trace* t, const char* host_bytes, int64_t n_bytes) {
   KX_CUDA(cudaStreamSynchronize(st));
   if (bad != ~0ull) {  // read_trace's message for the first bad line (trace.cpp:118-123)
     LineOut r{};
-    KX_CUDA(cudaMemcpy(&r, lo + bad, sizeof(r), cudaMemcpyDeviceToHost));
+    tcopy(t, &r, lo + bad, sizeof(r), cudaMemcpyDeviceToHost);
     const std::string line = line_text(t, static_cast<int64_t>(bad));
     const auto f = split(line);
     std::string m;
@@ -1030,7 +1037,7 @@ void parse(kx_trace* t, const char* host_bytes, int64_t n_bytes) {
   const int64_t n_msg = unique_sorted(mkey, n, nullptr, false, &umsg, &fmsg);
   const int64_t n_ag = unique_sorted(akey, na, aval, true, &uag, &fag);
   int col = 0;
-  KX_CUDA(cudaMemcpy(&col, collision, 4, cudaMemcpyDeviceToHost));
+  tcopy(t, &col, collision, 4, cudaMemcpyDeviceToHost);
   if (col) throw KxError(KX_ERR_RUNTIME, "trace: 64-bit string hash collision (distinct ids share a hash)");
   // agent names (std::string order, the std::set/std::map order of the
   // graph); msg ids stay in hash order (only their grouping matters, plus
@@ -1044,8 +1051,8 @@ void parse(kx_trace* t, const char* host_bytes, int64_t n_bytes) {
   std::vector<int64_t> hao(static_cast<size_t>(n_ag));
   std::vector<int32_t> hal(static_cast<size_t>(n_ag));
   if (n_ag) {
-    KX_CUDA(cudaMemcpy(hao.data(), ao, n_ag * 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(hal.data(), al, n_ag * 4, cudaMemcpyDeviceToHost));
+    tcopy(t, hao.data(), ao, n_ag * 8, cudaMemcpyDeviceToHost);
+    tcopy(t, hal.data(), al, n_ag * 4, cudaMemcpyDeviceToHost);
   }
   std::vector<std::string> names(static_cast<size_t>(n_ag));
   for (int64_t u = 0; u < n_ag; ++u) names[u].assign(host_bytes + hao[u], static_cast<size_t>(hal[u]));
@@ -1062,7 +1069,7 @@ void parse(kx_trace* t, const char* host_bytes, int64_t n_bytes) {
   t->umsg = umsg;
   t->msg_first_dev = fmsg;
   int32_t* drank = t->dalloc<int32_t>(n_ag);
-  if (n_ag) KX_CUDA(cudaMemcpy(drank, rank.data(), rank.size() * 4, cudaMemcpyHostToDevice));
+  if (n_ag) tcopy(t, drank, rank.data(), rank.size() * 4, cudaMemcpyHostToDevice);
   t->msg = t->dalloc<int64_t>(n);
   t->agent = t->dalloc<int32_t>(n);
   t->up = t->dalloc<int32_t>(n);
@@ -1198,9 +1205,9 @@ void reconstruct(kx_trace* t) {
   if (nd > dcap) throw KxError(KX_ERR_CAPACITY, "workflow: too many entry diagnostics");
   std::vector<uint32_t> hpos(nh), hkey(nh);
   if (nh) {
-    KX_CUDA(cudaMemcpy(hpos.data(), heads, nh * 4, cudaMemcpyDeviceToHost));
+    tcopy(t, hpos.data(), heads, nh * 4, cudaMemcpyDeviceToHost);
     std::sort(hpos.begin(), hpos.end());
-    for (uint32_t i = 0; i < nh; ++i) KX_CUDA(cudaMemcpy(&hkey[i], ek + hpos[i], 4, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < nh; ++i) tcopy(t, &hkey[i], ek + hpos[i], 4, cudaMemcpyDeviceToHost);
   }
   // edges_ is a std::map keyed by (from name, to name): ranks are name order
   t->e_from.clear();
@@ -1215,17 +1222,17 @@ void reconstruct(kx_trace* t) {
   t->is_entry.resize(static_cast<size_t>(A));
   t->tallies.resize(3 * static_cast<size_t>(A));
   if (A) {
-    KX_CUDA(cudaMemcpy(t->is_entry.data(), is_entry, A, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(t->tallies.data(), tallies, 3 * size_t(A) * 8, cudaMemcpyDeviceToHost));
+    tcopy(t, t->is_entry.data(), is_entry, A, cudaMemcpyDeviceToHost);
+    tcopy(t, t->tallies.data(), tallies, 3 * size_t(A) * 8, cudaMemcpyDeviceToHost);
   }
   // diagnostics in ingest order: msg_id string order, then record order
   std::vector<int64_t> dm(nd);
   std::vector<int32_t> dp(nd), de(nd), dot(nd);
   if (nd) {
-    KX_CUDA(cudaMemcpy(dm.data(), d_msg, nd * 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(dp.data(), d_pos, nd * 4, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(de.data(), d_entry, nd * 4, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(dot.data(), d_other, nd * 4, cudaMemcpyDeviceToHost));
+    tcopy(t, dm.data(), d_msg, nd * 8, cudaMemcpyDeviceToHost);
+    tcopy(t, dp.data(), d_pos, nd * 4, cudaMemcpyDeviceToHost);
+    tcopy(t, de.data(), d_entry, nd * 4, cudaMemcpyDeviceToHost);
+    tcopy(t, dot.data(), d_other, nd * 4, cudaMemcpyDeviceToHost);
   }
   std::map<int64_t, std::string> mname;
   std::vector<uint32_t> idx(nd);
@@ -1337,19 +1344,19 @@ int kx_trace_columns(const kx_trace* t, int64_t* msg, int32_t* agent, int32_t* u
     KX_CUDA(cudaSetDevice(t->dev));
     if (!n) return;
     auto cp = [&](void* dst, const void* src, size_t bytes) {
-      if (dst) KX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+      if (dst) tcopy(t, dst, src, bytes, cudaMemcpyDeviceToHost);
     };
     cp(msg, t->msg, n * 8);
     cp(agent, t->agent, n * 4);
     cp(upstream, t->up, n * 4);
     // per-line columns gathered into record order
     std::vector<int64_t> rl(n);
-    KX_CUDA(cudaMemcpy(rl.data(), t->rec_line, n * 8, cudaMemcpyDeviceToHost));
+    tcopy(t, rl.data(), t->rec_line, n * 8, cudaMemcpyDeviceToHost);
     auto gather = [&](auto* dst, const auto* src) {
       if (!dst) return;
       using T = std::remove_pointer_t<decltype(dst)>;
       std::vector<T> all(static_cast<size_t>(t->n_lines));
-      KX_CUDA(cudaMemcpy(all.data(), src, t->n_lines * sizeof(T), cudaMemcpyDeviceToHost));
+      tcopy(t, all.data(), src, t->n_lines * sizeof(T), cudaMemcpyDeviceToHost);
       for (int64_t r = 0; r < n; ++r) dst[r] = all[rl[r]];
     };
     gather(exec_start, t->es);
@@ -1367,12 +1374,12 @@ int kx_trace_msg_id(const kx_trace* t, int64_t msg, char* buf, int64_t cap, int6
     int64_t L = 0, off = 0;
     int32_t l = 0;
     uint32_t r = 0;
-    KX_CUDA(cudaMemcpy(&r, t->msg_first_dev + msg, 4, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(&L, t->rec_line + r, 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(&off, t->off + 3 * L, 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(&l, t->len + 3 * L, 4, cudaMemcpyDeviceToHost));
+    tcopy(t, &r, t->msg_first_dev + msg, 4, cudaMemcpyDeviceToHost);
+    tcopy(t, &L, t->rec_line + r, 8, cudaMemcpyDeviceToHost);
+    tcopy(t, &off, t->off + 3 * L, 8, cudaMemcpyDeviceToHost);
+    tcopy(t, &l, t->len + 3 * L, 4, cudaMemcpyDeviceToHost);
     if (len) *len = l;
-    if (buf && cap >= l && l) KX_CUDA(cudaMemcpy(buf, t->bytes + off, l, cudaMemcpyDeviceToHost));
+    if (buf && cap >= l && l) tcopy(t, buf, t->bytes + off, l, cudaMemcpyDeviceToHost);
   });
 }
 
@@ -1388,8 +1395,8 @@ int kx_trace_msg_spans(const kx_trace* t, int64_t k, const int64_t* msgs, int64_
     KX_CUDA(cudaMalloc(&doff, size_t(k) * 8));
     KX_CUDA(cudaMalloc(&dlen, size_t(k) * 4));
     msg_spans_dev(t, k, msgs, doff, dlen);
-    KX_CUDA(cudaMemcpy(off_out, doff, size_t(k) * 8, cudaMemcpyDeviceToHost));
-    KX_CUDA(cudaMemcpy(len_out, dlen, size_t(k) * 4, cudaMemcpyDeviceToHost));
+    tcopy(t, off_out, doff, size_t(k) * 8, cudaMemcpyDeviceToHost);
+    tcopy(t, len_out, dlen, size_t(k) * 4, cudaMemcpyDeviceToHost);
     KX_CUDA(cudaFree(doff));
     KX_CUDA(cudaFree(dlen));
   });
