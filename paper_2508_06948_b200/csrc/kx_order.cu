@@ -267,10 +267,11 @@ k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
   }
 }
 
-__global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_pools) return;
-  PoolRange r = ranges[p];
+// The quantisation window of a pool from its sampled extremes (lo_bits /
+// hi_bits, filled by k_pool_sample): lo and scale. Every reader computes it
+// itself (the same correctly-rounded operations, so the same result): no
+// launch of its own between the sample and key generation.
+__device__ __forceinline__ PoolRange finalize_range(PoolRange r, int q_bits) {
   if (r.lo_bits > r.hi_bits) {  // empty pool
     r.lo = 0.0;
     r.scale = 0.0;
@@ -289,7 +290,7 @@ __global__ void k_range_finalize(PoolRange* ranges, int n_pools, int q_bits) {
     // exact tie-fix orders them.
     r.scale = (span > 0.0 && span < 1.0e300 && isfinite(lo)) ? __ddiv_rn(qmax, span) : 0.0;
   }
-  ranges[p] = r;
+  return r;
 }
 
 // Compact key of one request: [pool | class rank | q(primary time)].
@@ -342,7 +343,7 @@ k_sample_keys(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
     const double t = primary_ptr(q, op.policy)[i];
     if (ag >= 0 && ag < op.n_agents && t == t) {
       p = a.pool[ag];
-      key = compact_key(a, op, ranges[p], p, ag, t, q_max(op));
+      key = compact_key(a, op, finalize_range(ranges[p], op.q_bits), p, ag, t, q_max(op));
     }
   }
   const int lane = threadIdx.x & 31;
@@ -475,8 +476,9 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
   for (int i = threadIdx.x; i < kRadix; i += blockDim.x) sh[i] = 0;
   for (int i = threadIdx.x; i < op.n_pools; i += blockDim.x) {
     s_pool[i] = 0;
-    s_lo[i] = ranges[i].lo;
-    s_scale[i] = ranges[i].scale;
+    const PoolRange r = finalize_range(ranges[i], op.q_bits);
+    s_lo[i] = r.lo;
+    s_scale[i] = r.scale;
     s_bnd[i] = (spec.bound && spec.on[i]) ? int64_t(spec.bound[i]) : int64_t(-1);
   }
   if (kSmemTables)
@@ -1017,8 +1019,6 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     KX_CHECK_LAUNCH();
     P.end(st);
   }
-  k_range_finalize<<<(op.n_pools + 127) / 128, 128, 0, st>>>(ws.ranges, op.n_pools, op.q_bits);
-  KX_CHECK_LAUNCH();
   if (hooks && hooks->before_keygen) hooks->before_keygen();
   // reads agent + primary time (12 B), writes the compact key (4 B)
   P.begin("keygen_hist", N * 16.0, st);
@@ -1112,7 +1112,6 @@ static void preload(F f) {
 void configure_sort_kernels() {
   preload(k_scan_hist);
   preload(k_pool_sample);
-  preload(k_range_finalize);
   preload(k_sample_keys);
   preload(k_spec_bound);
   preload(k_keygen<true>);
