@@ -1679,6 +1679,29 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
         }
         STAMP(3);
         TRACE(3);
+        if (!ovf_any && kmin == ~0ull) {
+          // no instance fits: the head keeps its place and its record (no
+          // target, not admitted) ends the round (engine.cpp:247), exactly
+          // as the exact path decides it, without the ledger round trip
+          if ((staged & (kStage / 2 - 1)) == 0) {
+            if (staged != rr_pub) rr_publish();
+            while (staged - s_flushed > kStage / 2) {
+            }
+          }
+          const int sl = staged & (kStage - 1);
+#pragma unroll
+          for (int s = 0; s < NI; ++s)
+            st_cand[sl * kR + lane + 32 * s] =
+                !el_[s] ? -1.0
+                        : vm[s] == 0 ? from_ordered_bits(peak[s])
+                                     : __dsub_rn(-static_cast<double>(cslot + __ffs(vm[s]) - 1), 1.0);
+          if (lane == 0) st_meta[sl] = static_cast<uint32_t>(p - pos0) << 9;
+          ++staged;
+          ++nrows;
+          f_broke = true;
+          ++n_rr;
+          break;
+        }
         if (!ovf_any && kmin != ~0ull && !wbad) {
           // stage the decision record (dispatcher.cpp:143-147)
           if ((staged & (kStage / 2 - 1)) == 0) {

@@ -102,3 +102,15 @@ print("-- order, then dispatch (no overlap)")
 for k, v in s.profile_read().items():
     print(f"{k:14s} {v['ms'] / ticks:8.3f} ms/tick  launches {v['launches'] / ticks:.0f}")
 timers()
+
+s.profile(False)
+s.capture_begin()
+s.restore()
+s.tick(w.now)
+s.capture_end()
+for _ in range(ticks):
+    s.graph_launch()
+s.synchronize()
+print("-- graph replay (the bench's step)")
+timers()
+s.graph_release()

@@ -97,8 +97,14 @@ def test_dispatch_multi_pool_matches_oracle(gpu_lib, monkeypatch, mode, n_pools,
 
 
 # Uniform decode rates: pools of <= 32 instances take the register-resident
-# resolver (kx_dispatch.cu, rr); spans longer than its 16 slots (T up to 8 s
-# at 0.5 s slots), overloads, full batches and tie cuts take the exact path.
+# resolver (kx_dispatch.cu, rr), 33-64 the two-warp one (rr2); both also
+# decide the round's last head (no instance fits). Spans longer than their 16
+# slots (T up to 8 s at 0.5 s slots), overloads and full active tables take
+# the exact path: these cases are known to reach it.
+EXACT_PATH_CASES = {(3, 17, 5000, 5, 0, 8), (2, 32, 12000, 3, 0, 64), (1, 64, 20000, 3, 0, 8),
+                    (2, 48, 12000, 3, 1, 16)}
+
+
 @pytest.mark.parametrize("mode", ["overlap", "serial", "short1"])
 @pytest.mark.parametrize("n_pools,per_pool,n,rounds,ties,max_batch",
                          MULTI_POOL_CASES + [(2, 32, 12000, 3, 0, 64), (4, 16, 8000, 4, 0, 2),
@@ -112,7 +118,8 @@ def test_dispatch_register_resolver_matches_oracle(gpu_lib, monkeypatch, mode, n
     run_multi_pool(monkeypatch, mode, n_pools, per_pool, n, rounds, ties, max_batch, uniform=True)
     gpu_lib.kx_debug_dispatch_counts(cnt, 1)
     assert cnt[0] > 0, "the register resolver took no decision"
-    assert cnt[1] > 0, "no head took the exact path (long spans / overloads are expected)"
+    if (n_pools, per_pool, n, rounds, ties, max_batch) in EXACT_PATH_CASES:
+        assert cnt[1] > 0, "no head took the exact path (long spans / overloads are expected)"
 
 
 def run_multi_pool(monkeypatch, mode, n_pools, per_pool, n, rounds, ties, max_batch, uniform):
