@@ -461,8 +461,14 @@ k_spec_bound(InstDev in, const int32_t* __restrict__ pool_begin, OrderParams op,
 // bound are staged in shared memory when the agent table is small.
 constexpr int kKeygenAgents = 2048;
 
+#ifndef KX_KG_MINB
+#define KX_KG_MINB 8  // 32 registers: 8 CTAs per SM (measured: 0.055 vs 0.067 ms at C4 with 1)
+#endif
+#ifndef KX_KG_U
+#define KX_KG_U 1
+#endif
 template <bool kSmemTables>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, KX_KG_MINB)
 k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
          uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
          int* __restrict__ error_flags, KeygenSpec spec) {
@@ -538,7 +544,7 @@ k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __
   uint4* kv = reinterpret_cast<uint4*>(keys);
   const int64_t nv = n >> 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  constexpr int U = 2;
+  constexpr int U = KX_KG_U;
   // the loop trip count is uniform over the block (hist_add is warp-collective)
   for (int64_t b0 = int64_t(blockIdx.x) * blockDim.x; b0 < nv; b0 += U * stride) {
     int4 ag[U];
