@@ -528,7 +528,8 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
                  o_v0 = L.take<uint32_t>(N), o_v1 = L.take<uint32_t>(N);
     const size_t lb_bytes = order_lookback_bytes(s->cap);
     const size_t o_lb = L.take<char>(lb_bytes);
-    const size_t o_rng = L.take<PoolRange>(P), o_poff = L.take<int64_t>(P + 1);
+    const size_t o_rng = L.take<PoolRange>(P), o_poff = L.take<int64_t>(P + 1),
+                 o_rst = L.take<PoolRange>(P), o_sdone = L.take<uint32_t>(1);
     // header block
     Layout H;
     const size_t h_hist = H.take<uint32_t>(4 * 256), h_tiles = H.take<uint32_t>(8),
@@ -549,6 +550,13 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->ws.vals[1] = at<uint32_t>(b, o_v1);
     s->ws.lookback = at<uint32_t>(b, o_lb);
     s->ws.ranges = at<PoolRange>(b, o_rng);
+    s->ws.range_stage = at<PoolRange>(b, o_rst);
+    s->ws.sample_done = at<uint32_t>(b, o_sdone);  // zeroed with the blob
+    {
+      const std::vector<PoolRange> empty(P, PoolRange{~0ull, 0ull, 0.0, 0.0});
+      KX_CUDA(cudaMemcpy(s->ws.range_stage, empty.data(), P * sizeof(PoolRange), cudaMemcpyHostToDevice));
+      KX_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    }
     s->ws.pool_offsets = at<int64_t>(b, o_poff);
     s->ws.small_hdr = b.base + o_hdr;
     s->ws.small_hdr_bytes = H.off;

@@ -127,94 +127,23 @@ __global__ void k_score(QueueDev q, AgentsDev a, int policy, int64_t n, double* 
   }
 }
 
-// ---- per-pool range of the primary time ------------------------------
-// Also validates agent indices and rejects NaN (error_flags bit 0 / bit 1).
-// Streams the queue with 16-byte loads: four agents (int4) and four times
-// (two double2) per thread per step, two steps in flight.
+// Primary time column of the policy's order key.
 __device__ __forceinline__ const double* primary_ptr(const QueueDev& q, int policy) {
   return policy == KX_SCHED_KAIROS ? q.app_start : policy == KX_SCHED_ORACLE ? q.rem : q.queue_enter;
 }
 
-__global__ void __launch_bounds__(256)
-k_pool_range(QueueDev q, AgentsDev a, OrderParams op, int64_t n, PoolRange* __restrict__ ranges,
-             int* __restrict__ error_flags) {
-  extern __shared__ uint64_t s_rng[];  // [2 * n_pools]: lo, hi
-  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
-    s_rng[2 * p] = ~0ull;
-    s_rng[2 * p + 1] = 0ull;
-  }
-  __syncthreads();
-  int err = 0;
-  // Per-thread running (pool, min, max), flushed to shared memory only when
-  // the pool changes: pools are mostly contiguous in a queue, so the shared
-  // atomics stay rare instead of hitting one address per request.
-  int32_t cur = -1;
-  uint64_t lo = ~0ull, hi = 0ull;
-  auto flush = [&]() {
-    if (cur >= 0) {
-      atomicMin(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur]), (unsigned long long)lo);
-      atomicMax(reinterpret_cast<unsigned long long*>(&s_rng[2 * cur + 1]), (unsigned long long)hi);
-    }
-  };
-  auto take = [&](int32_t ag, double t) {
-    if (ag < 0 || ag >= op.n_agents) {
-      err |= 1;
-      return;
-    }
-    if (t != t) {
-      err |= 2;
-      return;
-    }
-    const int32_t p = a.pool[ag];
-    const uint64_t bb = ordered_bits(t);
-    if (p != cur) {
-      flush();
-      cur = p;
-      lo = ~0ull;
-      hi = 0ull;
-    }
-    lo = bb < lo ? bb : lo;
-    hi = bb > hi ? bb : hi;
-  };
-  const double* tp = primary_ptr(q, op.policy);
-  const int4* av = reinterpret_cast<const int4*>(q.agent);
-  const double2* tv = reinterpret_cast<const double2*>(tp);
-  const int64_t nv = n >> 2;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  constexpr int U = 2;
-  for (int64_t v0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v0 < nv; v0 += U * stride) {
-    int4 ag[U];
-    double2 t0[U], t1[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t v = v0 + u * stride;
-      if (v < nv) {
-        ag[u] = av[v];
-        t0[u] = tv[2 * v];
-        t1[u] = tv[2 * v + 1];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (v0 + u * stride >= nv) continue;
-      take(ag[u].x, t0[u].x);
-      take(ag[u].y, t0[u].y);
-      take(ag[u].z, t1[u].x);
-      take(ag[u].w, t1[u].y);
-    }
-  }
-  if (blockIdx.x == 0)
-    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) take(q.agent[i], tp[i]);
-  flush();
-  if (err) atomicOr(error_flags, err);
-  __syncthreads();
-  for (int p = threadIdx.x; p < op.n_pools; p += blockDim.x) {
-    if (s_rng[2 * p] != ~0ull)
-      atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p].lo_bits), (unsigned long long)s_rng[2 * p]);
-    if (s_rng[2 * p + 1] != 0ull)
-      atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p].hi_bits), (unsigned long long)s_rng[2 * p + 1]);
-  }
-}
+// Per-order reset: header counters, the first radix pass's look-back array
+// and the caller's extra buffers (OrderHooks::zero_*).
+struct OrderInit {
+  uint32_t* hdr;
+  int hdr_words;
+  uint32_t* words;
+  int n_words;
+  uint8_t* bytes;
+  int64_t n_bytes;
+  uint4* lb;
+  int64_t lb_vecs;
+};
 
 // ---- sampled quantisation window ---------------------------------------
 // The compact key only needs the quantisation to be monotone: any window
@@ -231,9 +160,27 @@ __host__ __device__ inline int64_t sample_stride(int64_t n) {
   return n <= target ? kSampleLen : kSampleLen * ((n + target - 1) / target);
 }
 
+// The per-order reset (OrderInit, grid-stride) and the sample, in one launch:
+// the blocks fold their samples' extremes into a persistent staging array;
+// the last block to finish publishes them as the pools' windows and resets
+// the staging array and the block counter for the next order.
+__device__ __forceinline__ void order_reset(const OrderInit& in) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = t; i < in.hdr_words; i += nt) in.hdr[i] = 0;
+  for (int64_t i = t; i < in.n_words; i += nt) in.words[i] = 0;
+  const int64_t vecs = in.n_bytes / 16;
+  uint4* v = reinterpret_cast<uint4*>(in.bytes);
+  for (int64_t i = t; i < vecs; i += nt) v[i] = make_uint4(0, 0, 0, 0);
+  if (t < in.n_bytes - vecs * 16) in.bytes[vecs * 16 + t] = 0;
+  for (int64_t i = t; i < in.lb_vecs; i += nt) in.lb[i] = make_uint4(0, 0, 0, 0);
+}
+
 __global__ void __launch_bounds__(kSampleLen)
 k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
-              PoolRange* __restrict__ ranges) {
+              PoolRange* __restrict__ ranges, PoolRange* __restrict__ stage, uint32_t* __restrict__ done,
+              OrderInit init) {
+  order_reset(init);
   const int64_t i = int64_t(blockIdx.x) * stride + threadIdx.x;
   int32_t p = -1;
   uint64_t lo = ~0ull, hi = 0ull;
@@ -248,23 +195,40 @@ k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
   // one atomic pair per warp when the warp's samples share a pool (pools
   // are mostly contiguous), one per sample otherwise
   const uint32_t valid = __ballot_sync(0xffffffffu, p >= 0);
-  if (!valid) return;
-  const int32_t p0 = __shfl_sync(0xffffffffu, p, __ffs(valid) - 1);
-  if (__all_sync(0xffffffffu, p < 0 || p == p0)) {
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
-      const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
-      lo = l2 < lo ? l2 : lo;
-      hi = h2 > hi ? h2 : hi;
+  if (valid) {
+    const int32_t p0 = __shfl_sync(0xffffffffu, p, __ffs(valid) - 1);
+    if (__all_sync(0xffffffffu, p < 0 || p == p0)) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+        const uint64_t h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&stage[p0].lo_bits), (unsigned long long)lo);
+        atomicMax(reinterpret_cast<unsigned long long*>(&stage[p0].hi_bits), (unsigned long long)hi);
+      }
+    } else if (p >= 0) {
+      atomicMin(reinterpret_cast<unsigned long long*>(&stage[p].lo_bits), (unsigned long long)lo);
+      atomicMax(reinterpret_cast<unsigned long long*>(&stage[p].hi_bits), (unsigned long long)hi);
     }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p0].lo_bits), (unsigned long long)lo);
-      atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p0].hi_bits), (unsigned long long)hi);
-    }
-  } else if (p >= 0) {
-    atomicMin(reinterpret_cast<unsigned long long*>(&ranges[p].lo_bits), (unsigned long long)lo);
-    atomicMax(reinterpret_cast<unsigned long long*>(&ranges[p].hi_bits), (unsigned long long)hi);
   }
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int k = threadIdx.x; k < op.n_pools; k += blockDim.x) {
+    volatile PoolRange* sv = stage + k;
+    ranges[k] = PoolRange{sv->lo_bits, sv->hi_bits, 0.0, 0.0};  // lo / scale: finalize_range
+    sv->lo_bits = ~0ull;
+    sv->hi_bits = 0ull;
+  }
+  if (threadIdx.x == 0) *done = 0u;
 }
 
 // The quantisation window of a pool from its sampled extremes (lo_bits /
@@ -944,36 +908,8 @@ int keygen_grid(int64_t n, int sms) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n / 4 + 511) / 512, int64_t(sms) * 8)));
 }
 
-// Per-order reset: header counters, window ranges, and the caller's extra
-// buffers (OrderHooks::zero_*), in one launch.
-struct OrderInit {
-  uint32_t* hdr;
-  int hdr_words;
-  PoolRange* ranges;
-  int n_pools;
-  uint32_t* words;
-  int n_words;
-  uint8_t* bytes;
-  int64_t n_bytes;
-  uint4* lb;
-  int64_t lb_vecs;
-};
 
-__global__ void __launch_bounds__(256) k_order_init(OrderInit in) {
-  if (blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < in.hdr_words; i += blockDim.x) in.hdr[i] = 0;
-    for (int i = threadIdx.x; i < in.n_words; i += blockDim.x) in.words[i] = 0;
-    for (int p = threadIdx.x; p < in.n_pools; p += blockDim.x)
-      in.ranges[p] = PoolRange{~0ull, 0ull, 0.0, 0.0};  // min / max of the sampled window
-  }
-  const int64_t vecs = in.n_bytes / 16;
-  uint4* v = reinterpret_cast<uint4*>(in.bytes);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < vecs; i += int64_t(gridDim.x) * blockDim.x)
-    v[i] = make_uint4(0, 0, 0, 0);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < in.lb_vecs; i += int64_t(gridDim.x) * blockDim.x)
-    in.lb[i] = make_uint4(0, 0, 0, 0);
-  if (blockIdx.x == 0 && threadIdx.x < in.n_bytes - vecs * 16) in.bytes[vecs * 16 + threadIdx.x] = 0;
-}
+__global__ void __launch_bounds__(256) k_order_init(OrderInit in) { order_reset(in); }
 
 OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderParams& op,
                             int64_t n, OrderWorkspace& ws, int sms, cudaStream_t st,
@@ -983,30 +919,23 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   const double N = static_cast<double>(n);
   OrderResultDev res{};
   const int passes = op.key_bits / kRadixBits;
-  // one launch resets the per-order state (header counters, window ranges)
-  // and whatever the caller's hooks add (the tick's admitted flags and
-  // sample counters)
-  {
-    OrderInit in{};
-    in.hdr = static_cast<uint32_t*>(ws.small_hdr);
-    in.hdr_words = static_cast<int>(ws.small_hdr_bytes / 4);
-    in.ranges = ws.ranges;
-    in.n_pools = op.n_pools;
-    if (hooks) {
-      in.words = hooks->zero_words;
-      in.n_words = hooks->n_zero_words;
-      in.bytes = hooks->zero_bytes;
-      in.n_bytes = hooks->n_zero_bytes;
-    }
-    // the first radix pass's look-back array (later passes clear their successor's)
-    in.lb = reinterpret_cast<uint4*>(ws.lookback);
-    in.lb_vecs = n > 0 ? (n + kSortTile - 1) / kSortTile * kRadix / 4 : 0;
-    const int64_t vecs = std::max<int64_t>(in.n_bytes / 16, in.lb_vecs);
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, int64_t(sms) * 4)));
-    k_order_init<<<grid, 256, 0, st>>>(in);
-    KX_CHECK_LAUNCH();
+  // the per-order reset (header counters, the first radix pass's look-back
+  // array, and whatever the caller's hooks add: the tick's admitted flags
+  // and sample counters) runs inside the sample launch
+  OrderInit in{};
+  in.hdr = static_cast<uint32_t*>(ws.small_hdr);
+  in.hdr_words = static_cast<int>(ws.small_hdr_bytes / 4);
+  if (hooks) {
+    in.words = hooks->zero_words;
+    in.n_words = hooks->n_zero_words;
+    in.bytes = hooks->zero_bytes;
+    in.n_bytes = hooks->n_zero_bytes;
   }
+  in.lb = reinterpret_cast<uint4*>(ws.lookback);
+  in.lb_vecs = n > 0 ? (n + kSortTile - 1) / kSortTile * kRadix / 4 : 0;
   if (n == 0) {
+    k_order_init<<<1, 256, 0, st>>>(in);
+    KX_CHECK_LAUNCH();
     k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
     KX_CHECK_LAUNCH();
     if (hooks && hooks->after_keys) hooks->after_keys();
@@ -1021,7 +950,8 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
     const int64_t stride = sample_stride(n);
     const int64_t blocks = (n + stride - 1) / stride;
     P.begin("pool_sample", double(blocks) * kSampleLen * 12.0, st);
-    k_pool_sample<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges);
+    k_pool_sample<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges,
+                                                                        ws.range_stage, ws.sample_done, in);
     KX_CHECK_LAUNCH();
     P.end(st);
   }

@@ -16,6 +16,8 @@ struct OrderWorkspace {
   uint32_t* vals[2];
   uint32_t* lookback;
   PoolRange* ranges;
+  PoolRange* range_stage;  // [n_pools] sampled extremes in flight; (~0, 0) between orders
+  uint32_t* sample_done;   // blocks of the sample launch done; 0 between orders
   int64_t* pool_offsets;  // n_pools + 1
   // small header block, zeroed per order: hist[4*256], tile_counters[8],
   // pool_counts[n_pools], n_big, error_flags
