@@ -12,7 +12,7 @@ for c in C4 C3 C2 C1; do
 done
 timeout 600 python bench.py --impl reference > gpurun_out/f_ref.json 2> gpurun_out/f_ref.err
 if [[ ${PROF:-1} == 1 ]]; then
-  for c in C4 C1; do
+  for c in C4 C3 C2 C1; do
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_" --csv \
        --log-file gpurun_out/f_launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline \
        > /dev/null 2>&1

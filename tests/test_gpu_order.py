@@ -72,6 +72,30 @@ def test_degenerate_all_equal_keys(gpu_lib, n):
         assert np.array_equal(perm, O.sort(policy, q, t, 1)[0])
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_tie_runs_across_chunk_boundaries(gpu_lib, seed):
+    # runs of 1-20 equal primary times (the thread fixer takes <= 16, the CTA
+    # fixer longer ones), ~31K requests: runs straddle the tie-fix kernel's
+    # 4096-key chunks (a run belongs to the chunk of its first key); few
+    # queue_enter values and msg keys, so the exact tuple reaches msg and uid
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 21, 3000)
+    n = int(lens.sum())
+    app = np.repeat(np.arange(len(lens), dtype=np.float64) * 0.5, lens)
+    qe = rng.integers(0, 4, n).astype(np.float64) + 2000.0
+    msg = rng.integers(0, 3, n).astype(np.uint64)
+    uid = rng.permutation(n).astype(np.uint64)
+    sh = rng.permutation(n)
+    q = O.QueueArrays(np.zeros(n, np.int32), np.ones(n), app[sh], qe[sh], msg[sh], uid[sh])
+    t = O.TableArrays(np.zeros(1, np.int32), [1.0], [2], [1.0])
+    for policy in POLICIES:
+        s = make_sched(1, n)
+        load(s, q, t, policy)
+        s.order()
+        perm, _ = s.fetch_order()
+        assert np.array_equal(perm, O.sort(policy, q, t, 1)[0]), policy
+
+
 def test_negative_zero_equals_zero(gpu_lib):
     n = 64
     app = np.where(np.arange(n) % 2 == 0, -0.0, 0.0)
