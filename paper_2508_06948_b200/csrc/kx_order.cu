@@ -432,7 +432,7 @@ constexpr int kKeygenAgents = 2048;
 #define KX_KG_U 1
 #endif
 template <bool kSmemTables>
-__global__ void __launch_bounds__(256, KX_KG_MINB)
+__global__ void __launch_bounds__(256, kSmemTables ? KX_KG_MINB : 4)
 k_keygen(QueueDev q, AgentsDev a, OrderParams op, int64_t n, const PoolRange* __restrict__ ranges,
          uint32_t* __restrict__ keys, uint32_t* __restrict__ hist, uint32_t* __restrict__ pool_counts,
          int* __restrict__ error_flags, KeygenSpec spec) {

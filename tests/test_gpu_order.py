@@ -55,6 +55,21 @@ def test_order_matches_oracle_random(gpu_lib, policy, n, pools, grain):
     assert np.array_equal(perm, ref_perm)
 
 
+@pytest.mark.parametrize("policy", POLICIES)
+def test_order_many_agents(gpu_lib, policy):
+    # more agents than key generation's shared-memory table (2048): the
+    # global-table variant of k_keygen
+    rng = np.random.default_rng(3000)
+    q, t = random_queue(rng, 50_000, n_agents=3000, n_pools=4, tie_grain=0.25)
+    s = make_sched(4, 50_000)
+    load(s, q, t, policy)
+    s.order()
+    perm, offs = s.fetch_order()
+    ref_perm, ref_offs = O.sort(policy, q, t, 4)
+    assert np.array_equal(offs, ref_offs)
+    assert np.array_equal(perm, ref_perm)
+
+
 @pytest.mark.parametrize("n", [40, 1500, 40_000])
 def test_degenerate_all_equal_keys(gpu_lib, n):
     # every request shares agent, app_start and queue_enter: one tie run of
