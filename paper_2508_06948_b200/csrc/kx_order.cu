@@ -176,12 +176,14 @@ __device__ __forceinline__ void order_reset(const OrderInit& in) {
   for (int64_t i = t; i < in.lb_vecs; i += nt) in.lb[i] = make_uint4(0, 0, 0, 0);
 }
 
-__global__ void __launch_bounds__(kSampleLen)
-k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride,
+constexpr int kSampleWins = 8;  // sample windows per block of the sample launch
+__global__ void __launch_bounds__(kSampleLen * kSampleWins)
+k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride, int64_t windows,
               PoolRange* __restrict__ ranges, PoolRange* __restrict__ stage, uint32_t* __restrict__ done,
               OrderInit init) {
   order_reset(init);
-  const int64_t i = int64_t(blockIdx.x) * stride + threadIdx.x;
+  const int64_t wdw = int64_t(blockIdx.x) * kSampleWins + threadIdx.x / kSampleLen;
+  const int64_t i = wdw < windows ? wdw * stride + threadIdx.x % kSampleLen : n;
   int32_t p = -1;
   uint64_t lo = ~0ull, hi = 0ull;
   if (i < n) {
@@ -192,9 +194,16 @@ k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
       lo = hi = ordered_bits(t);
     }
   }
-  // one atomic pair per warp when the warp's samples share a pool (pools
-  // are mostly contiguous), one per sample otherwise
+  // per warp: one (pool, min, max) when its samples share a pool (pools are
+  // mostly contiguous), per-sample atomics otherwise; then one atomic pair
+  // per distinct pool of the block (few global atomics: the staging array
+  // and the block counter are single addresses)
+  constexpr int kWarps = kSampleLen * kSampleWins / 32;
+  __shared__ int32_t s_wp[kWarps];
+  __shared__ uint64_t s_wlo[kWarps], s_whi[kWarps];
+  const int warp = threadIdx.x >> 5;
   const uint32_t valid = __ballot_sync(0xffffffffu, p >= 0);
+  int32_t wp = -1;
   if (valid) {
     const int32_t p0 = __shfl_sync(0xffffffffu, p, __ffs(valid) - 1);
     if (__all_sync(0xffffffffu, p < 0 || p == p0)) {
@@ -204,13 +213,31 @@ k_pool_sample(QueueDev q, AgentsDev a, OrderParams op, int64_t n, int64_t stride
         lo = l2 < lo ? l2 : lo;
         hi = h2 > hi ? h2 : hi;
       }
-      if ((threadIdx.x & 31) == 0) {
-        atomicMin(reinterpret_cast<unsigned long long*>(&stage[p0].lo_bits), (unsigned long long)lo);
-        atomicMax(reinterpret_cast<unsigned long long*>(&stage[p0].hi_bits), (unsigned long long)hi);
-      }
+      wp = p0;
     } else if (p >= 0) {
       atomicMin(reinterpret_cast<unsigned long long*>(&stage[p].lo_bits), (unsigned long long)lo);
       atomicMax(reinterpret_cast<unsigned long long*>(&stage[p].hi_bits), (unsigned long long)hi);
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_wp[warp] = wp;
+    s_wlo[warp] = lo;
+    s_whi[warp] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kWarps; ++w) {
+      const int32_t pw = s_wp[w];
+      if (pw < 0) continue;
+      uint64_t l = s_wlo[w], h = s_whi[w];
+      for (int w2 = w + 1; w2 < kWarps; ++w2)
+        if (s_wp[w2] == pw) {
+          l = s_wlo[w2] < l ? s_wlo[w2] : l;
+          h = s_whi[w2] > h ? s_whi[w2] : h;
+          s_wp[w2] = -1;
+        }
+      atomicMin(reinterpret_cast<unsigned long long*>(&stage[pw].lo_bits), (unsigned long long)l);
+      atomicMax(reinterpret_cast<unsigned long long*>(&stage[pw].hi_bits), (unsigned long long)h);
     }
   }
   __shared__ bool s_last;
@@ -948,9 +975,10 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   {
     // sampled window: ~256K requests (every request below that)
     const int64_t stride = sample_stride(n);
-    const int64_t blocks = (n + stride - 1) / stride;
+    const int64_t blocks = (n + stride - 1) / stride;  // sample windows
     P.begin("pool_sample", double(blocks) * kSampleLen * 12.0, st);
-    k_pool_sample<<<static_cast<unsigned>(blocks), kSampleLen, 0, st>>>(q, a, op, n, stride, ws.ranges,
+    k_pool_sample<<<static_cast<unsigned>((blocks + kSampleWins - 1) / kSampleWins), kSampleLen * kSampleWins, 0,
+                    st>>>(q, a, op, n, stride, blocks, ws.ranges,
                                                                         ws.range_stage, ws.sample_done, in);
     KX_CHECK_LAUNCH();
     P.end(st);
