@@ -590,22 +590,28 @@ __device__ bool sort_prefix(const QueueDev& q, int policy, const uint32_t* __res
   for (int kk = 2; kk <= p2; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
       if (j >= 256) {
+        // entry i = 8 * tid + r sits at r * 256 + tid (lanes consecutive: no
+        // bank conflicts); its partner i ^ j is entry r of thread tid ^ (j / 8)
 #pragma unroll
-        for (int r = 0; r < 8; ++r) sk[base + r] = v[r];
+        for (int r = 0; r < 8; ++r) sk[r * 256 + threadIdx.x] = v[r];
         __syncthreads();
+        const int pt = threadIdx.x ^ (j >> 3);
+        // j >= 8: the direction is the thread's (base is a multiple of 8)
+        const bool up = ((base & j) == 0) == ((base & kk) == 0);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const int i = base + r;
-          const uint64_t o = sk[i ^ j];
-          v[r] = (((i & j) == 0) == ((i & kk) == 0)) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+          const uint64_t o = sk[r * 256 + pt];
+          const bool lt = o < v[r];
+          v[r] = (lt == up) ? o : v[r];
         }
         __syncthreads();
       } else if (j >= 8) {
+        const bool up = ((base & j) == 0) == ((base & kk) == 0);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          const int i = base + r;
           const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j >> 3);
-          v[r] = (((i & j) == 0) == ((i & kk) == 0)) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+          const bool lt = o < v[r];
+          v[r] = (lt == up) ? o : v[r];
         }
       } else {
         // in-thread pairs; j is a compile-time constant in each branch so v
