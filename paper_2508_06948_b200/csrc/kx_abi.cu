@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -455,7 +456,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     Layout L;
     const size_t o_id = L.take<int32_t>(I), o_pool = L.take<int32_t>(I), o_cap = L.take<double>(I),
                  o_k = L.take<double>(I), o_pf = L.take<double>(I), o_mb = L.take<int32_t>(I),
-                 o_pb = L.take<int32_t>(s->n_pools + 1);
+                 o_pb = L.take<int32_t>(s->n_pools + 1), o_rk = L.take<int32_t>(I);
     alloc_blob(s->inst_const_blob, L.off);
     auto& b = s->inst_const_blob;
     s->in.id = at<int32_t>(b, o_id);
@@ -464,6 +465,7 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     s->in.decode_rate = at<double>(b, o_k);
     s->in.prefill_rate = at<double>(b, o_pf);
     s->in.max_batch = at<int32_t>(b, o_mb);
+    s->in.rank_li = at<int32_t>(b, o_rk);
     s->pool_begin = at<int32_t>(b, o_pb);
     std::vector<int32_t> vid(I), vpool(I), vmb(I);
     std::vector<double> vcap(I), vk(I), vpf(I);
@@ -483,6 +485,17 @@ void create_impl(const kx_sched_config* cfg, kx_sched** out) {
     KX_CUDA(cudaMemcpy(s->in.prefill_rate, vpf.data(), I * 8, cudaMemcpyHostToDevice));
     KX_CUDA(cudaMemcpy(s->pool_begin, pool_begin.data(), (s->n_pools + 1) * 4,
                        cudaMemcpyHostToDevice));
+    // the instances of each pool in InstanceId order (select_instance's tie
+    // rule): local index by rank, ties by position
+    std::vector<int32_t> vrank(I);
+    for (int p = 0; p < s->n_pools; ++p) {
+      const int ib = pool_begin[p], ni = pool_begin[p + 1] - ib;
+      std::vector<int32_t> l(ni);
+      std::iota(l.begin(), l.end(), 0);
+      std::stable_sort(l.begin(), l.end(), [&](int32_t x, int32_t y) { return vid[ib + x] < vid[ib + y]; });
+      for (int r = 0; r < ni; ++r) vrank[ib + r] = l[r];
+    }
+    KX_CUDA(cudaMemcpy(s->in.rank_li, vrank.data(), I * 4, cudaMemcpyHostToDevice));
   }
   // instances: mutable part (one blob so checkpoint/restore is one copy)
   {

@@ -899,28 +899,13 @@ k_dispatch_chain(QueueDev q, AgentsDev ag, InstDev in, const int32_t* __restrict
   double* const st_cand = CL(double, st_cand);
 #undef CL
 
-  // Rank of each instance: position in InstanceId order (H9).
+  // Rank of each instance: position in InstanceId order (H9), tabulated at
+  // creation (kx_sched_create).
   if (warp == 0) {
-    int32_t myid[NI];
 #pragma unroll
     for (int s = 0; s < NI; ++s) {
       const int l = lane + 32 * s;
-      myid[s] = l < ni ? in.id[ib + l] : 0x7fffffff;
-      s_li[l] = -1;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < NI; ++s) {
-      const int l = lane + 32 * s;
-      int rank = 0;
-#pragma unroll
-      for (int s2 = 0; s2 < NI; ++s2)
-        for (int l2 = 0; l2 < 32; ++l2) {
-          const int32_t o = __shfl_sync(0xffffffffu, myid[s2], l2);
-          const int lo = l2 + 32 * s2;
-          rank += (lo < ni) && (o < myid[s] || (o == myid[s] && lo < l));
-        }
-      if (l < ni) s_li[rank] = l;
+      s_li[l] = l < ni ? in.rank_li[ib + l] : -1;
     }
     uint64_t bmin = ~0ull, hmax = 0;
 #pragma unroll

@@ -45,6 +45,7 @@ struct InstDev {
   double* decode_rate;
   double* prefill_rate;
   int32_t* max_batch;
+  int32_t* rank_li;     // [n_inst]: per pool, the local index of the rank-th instance in InstanceId order (H9)
   // mutable (checkpointed) state
   double* live_kv;
   int32_t* running;
