@@ -29,7 +29,7 @@ constexpr int kRadix = 256;
 #define KX_SORT_THREADS 256
 #endif
 #ifndef KX_SORT_ITEMS
-#define KX_SORT_ITEMS 12
+#define KX_SORT_ITEMS 16  // 4096-key tiles (measured at C4: 12 -> 0.484 ms, 13 -> 0.473, 14 -> 0.472, 16 -> 0.468 for the four passes)
 #endif
 constexpr int kSortThreads = KX_SORT_THREADS;
 constexpr int kSortItems = KX_SORT_ITEMS;
