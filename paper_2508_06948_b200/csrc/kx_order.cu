@@ -1005,7 +1005,10 @@ OrderResultDev launch_order(const QueueDev& q, const AgentsDev& a, const OrderPa
   // (pass p scans its raw digit counts itself; pass p counts digit p + 1)
   k_pool_offsets<<<1, 32, 0, st>>>(ws.pool_counts, op.n_pools, ws.pool_offsets);
   KX_CHECK_LAUNCH();
-  if (const char* dump = getenv("KX_DUMP_KEYS")) {  // diagnostics: the compact keys, raw u32
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  KX_CUDA(cudaStreamIsCapturing(st, &cap_status));
+  const char* dump = cap_status == cudaStreamCaptureStatusNone ? getenv("KX_DUMP_KEYS") : nullptr;
+  if (dump) {  // diagnostics: the compact keys, raw u32 (not while a graph is captured)
     std::vector<uint32_t> hk(static_cast<size_t>(n));
     KX_CUDA(cudaMemcpyAsync(hk.data(), ws.keys[0], size_t(n) * 4, cudaMemcpyDeviceToHost, st));
     KX_CUDA(cudaStreamSynchronize(st));
