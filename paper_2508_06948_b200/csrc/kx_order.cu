@@ -913,10 +913,12 @@ size_t spec_list_words(int n_pools) { return size_t(n_pools) * kSpecMax; }
 
 // ---- host orchestration --------------------------------------------------
 // Warp ranking per radix pass (kx_sort.cuh kRank), chosen by measurement
-// on the C4 keys (profiles/r01_sort_rank.md): MATCH.ANY with a leader
-// broadcast for the spread low digits, ballots for the top
-// digit (few distinct values).
-constexpr int kSortRankDefault[4] = {2, 2, 2, 1};
+// on the C4 keys: MATCH.ANY peers for the spread low digits, ballots for the
+// top digit (few distinct values). With 12-key tiles the leader-broadcast
+// form (2) won the low digits (profiles/r01_sort_rank.md); with 16-key tiles
+// every peer reading the running count (0) does: 0001 0.464 ms for the four
+// passes, 2221 0.468, 0201 0.466, 0011 0.478, 0000 0.498.
+constexpr int kSortRankDefault[4] = {0, 0, 0, 1};
 
 size_t order_lookback_bytes(int64_t cap) {  // two arrays, alternating between passes
   const int64_t tiles = (cap + kSortTile - 1) / kSortTile;
